@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""Batched TFHE programmable bootstrapping on B200 -- BASELINE.json config 2.
+
+One step = one PBS pass (mod switch -> 630-step CMUX-ladder blind rotation ->
+sample extraction -> LWE key switch) over a batch of 4096 LWE ciphertexts
+(n = 630, N = 1024, l = 3, Bg = 2^7, KS 2^2 x 8, q = 2^32), messages uniform in
+Z_8, LUT = identity on [0, 4) with the negacyclic sign on [4, 8).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl hwb|reference]
+
+Prints ONE JSON line (rank 0).  `value` = whole-job PBS/s with inputs resident
+in HBM; `e2e` = the same through the public API from pinned host buffers with
+H2D/D2H inside the timed region.  `--impl reference` times the CPU port of the
+reference algorithm (oracle/c, all host threads) on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+
+METRIC = "bootstrappings/sec"
+UNIT = "PBS/s"
+KEY_SEED, ENC_SEED = 1, 2
+L2_FLUSH_BYTES = 512 << 20          # > 126 MB L2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["hwb", "reference"], default="hwb")
+    ap.add_argument("--batch", type=int, default=4096)
+    ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=0, help="PBS per CPU step (0 = auto)")
+    return ap.parse_args()
+
+
+def workload(P, B, rank):
+    from paper_2403_20190_b200 import tfhe
+    keys = tfhe.pbs_keygen(P, KEY_SEED)
+    rng = tfhe.make_rng(ENC_SEED + 1000 * rank)
+    ms = rng.integers(0, P.p, B)
+    lwe = tfhe.enc_lwe_batch(ms * P.delta, keys.lwe_key, rng)
+    tv = tfhe.test_polynomial(np.arange(P.p // 2), P)
+    return keys, ms, lwe, tv
+
+
+def expected(ms, p):
+    half = p // 2
+    return np.where(ms < half, ms, (-(ms - half)) % p)
+
+
+def config(P, B, world, extra=None):
+    c = {"workload": "cfg2 batched PBS (BASELINE.json configs[1])", "batch_per_gpu": B,
+         "global_batch": B * world, "n": P.lwe_n, "N": P.n, "k": 1,
+         "pbs_gadget": f"Bg=2^{P.gadget.base_log} l={P.gadget.levels}",
+         "ks_gadget": f"2^{P.gadget_ks.base_log} l={P.gadget_ks.levels}",
+         "q": "2^32", "p": P.p, "lut": "identity on [0,4), negacyclic sign on [4,8)",
+         "parallelism": f"replicas{world}" if world > 1 else "single",
+         "l2": "flushed (512 MiB write) before every timed step"}
+    if extra:
+        c.update(extra)
+    return c
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_cpu_port(P, keys, lwe, tv, sample, threads):
+    """The oracle port (oracle/c, exact schoolbook restatement of the reference
+    path) on `sample` ciphertexts; returns (PBS/s, outputs)."""
+    from oracle import coracle
+    coracle.build()
+    t0 = time.perf_counter()
+    out = coracle.pbs(lwe[:sample], tv, keys.bsk, keys.ksk, P, nthreads=threads)
+    dt = time.perf_counter() - t0
+    return sample / dt, out
+
+
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "samples": len(rows), "reasons": reasons}
+
+
+def probe_modmul_peak(torch, _lib, tfhe):
+    """Measured P_mm: register-only RNS modmul throughput (one launch filling
+    every SM), best of 3, CUDA events on the launching stream."""
+    import ctypes
+    sink = torch.zeros(4, dtype=torch.int32, device="cuda")
+    L = _lib.load()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    blocks, iters = sms * 8, 2048
+    best = 0.0
+    for _ in range(4):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        n = L.hwb_probe_modmul(ctypes.c_void_p(sink.data_ptr()), blocks, iters, tfhe._stream())
+        e.record()
+        e.synchronize()
+        if n < 0:
+            raise RuntimeError(L.hwb_last_error().decode())
+        best = max(best, n / (s.elapsed_time(e) * 1e-3))
+    return best
+
+
+def bench_hwb(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2403_20190_b200 import _lib, tfhe
+    from paper_2403_20190_b200.params import named_params
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    _lib.set_variant(args.variant)
+
+    P = named_params("CFG2")
+    B = args.batch
+    keys, ms, lwe, tv = workload(P, B, rank)
+    bsk, ksk = keys.device_keys()
+    lwe_d = tfhe.to_device(lwe)
+    tv_d = tfhe.to_device(tv)
+    ext_d = torch.empty((B, P.n + 1), dtype=torch.int32, device="cuda")
+    out_d = torch.empty((B, P.lwe_n + 1), dtype=torch.int32, device="cuda")
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
+
+    def step():
+        tfhe.pbs_batch(P, lwe_d, tv_d, bsk, None, out=ext_d)          # blind rotation + extract
+        tfhe.lwe_keyswitch(P, ext_d, ksk, out=out_d)                  # key switch
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    clocks = Clocks(local)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    for k in range(args.steps):
+        flush.zero_()                                                 # L2 flush, untimed
+        e0, e1, e2 = evs[k]
+        e0.record()
+        tfhe.pbs_batch(P, lwe_d, tv_d, bsk, None, out=ext_d)
+        e1.record()
+        tfhe.lwe_keyswitch(P, ext_d, ksk, out=out_d)
+        e2.record()
+    torch.cuda.synchronize()
+    clock_info = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    br_ms = [evs[k][0].elapsed_time(evs[k][1]) for k in range(args.steps)]
+    ks_ms = [evs[k][1].elapsed_time(evs[k][2]) for k in range(args.steps)]
+    total_ms = sum(br_ms) + sum(ks_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+
+    # correctness of the timed outputs (decryption of every ciphertext)
+    out_h = tfhe.to_host(out_d)
+    dec = tfhe.dec_lwe_batch(out_h, keys.lwe_key)
+    ok = bool(np.array_equal(dec, expected(ms, P.p)))
+
+    # end to end through the public API from pinned host memory
+    lwe_pin = torch.from_numpy(lwe.view(np.int32)).pin_memory()
+    out_pin = torch.empty((B, P.lwe_n + 1), dtype=torch.int32).pin_memory()
+    e2e_ms = []
+    for k in range(args.steps + 1):
+        flush.zero_()
+        s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s_ev.record()
+        dev_in = lwe_pin.to("cuda", non_blocking=True)
+        res = tfhe.pbs_batch(P, dev_in, tv_d, bsk, ksk)
+        out_pin.copy_(res, non_blocking=True)
+        e_ev.record()
+        e_ev.synchronize()
+        if k:                                                         # first = warm-up
+            e2e_ms.append(s_ev.elapsed_time(e_ev))
+    e2e_ok = bool(np.array_equal(out_pin.numpy().view(np.uint32), out_h))
+    e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+
+    # integer roofline of the dominant kernel (blind rotation): W_mm RNS
+    # modmuls per PBS (SURVEY.md §8(d) NTT formulation) over its event time
+    peak = probe_modmul_peak(torch, _lib, tfhe)
+    lv, N, logN = P.gadget.levels, P.n, P.degree_log
+    w_cmux = 2 * lv * (N // 2) * logN + 2 * (N // 2) * logN + 4 * lv * N   # 53,248 at cfg2
+    w_mm = P.lwe_n * w_cmux
+    br_avg_s = statistics.mean(br_ms) * 1e-3
+    achieved = w_mm * B / br_avg_s
+
+    value = B * world * args.steps / (max_ms * 1e-3)
+    result = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (seeded LWE encryptions, BASELINE cfg2 shapes)",
+        "config": config(P, B, world, {"kernel_variant": args.variant}),
+        "e2e": {"value": round(B * world * args.steps / (float(e2e_t.item()) * 1e-3), 2), "unit": UNIT,
+                "h2d_bytes_per_step": int(lwe.nbytes), "d2h_bytes_per_step": int(out_h.nbytes),
+                "api": "tfhe.pbs_batch from pinned host tensors", "matches_device_run": e2e_ok},
+        "roofline": {"bound": "int", "kernel": "blind_rotate_kernel<1024,PBS>",
+                     "achieved": round(achieved / 1e9, 2), "peak": round(peak / 1e9, 2),
+                     "unit": "Gmodmul/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "work_per_pbs": f"W_mm = {w_mm} RNS modmuls (n x 53,248 per CMUX)",
+                     "peak_source": "measured live: probe_modmul_kernel (register-only Shoup, both primes)"},
+        "kernel_ms": {"blind_rotate": round(statistics.mean(br_ms), 3),
+                      "keyswitch": round(statistics.mean(ks_ms), 3)},
+        "gpu_launches": 2 * args.steps,
+        "clocks": clock_info,
+        "check": "all outputs decrypt to the LUT" if ok else "DECRYPTION MISMATCH",
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = cpu_threads()
+        sample = args.cpu_sample or max(16, min(256, 2 * threads))
+        rate, ref_out = run_cpu_port(P, keys, lwe, tv, sample, threads)
+        result["cpu_baseline"] = {
+            "value": round(rate, 3), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{sample} cfg2 PBS of the same batch (oracle/c exact schoolbook, "
+                      f"OpenMP {threads} threads, {cpu_model()})",
+            "bit_exact_vs_gpu": bool(np.array_equal(ref_out, out_h[:sample]))}
+    if world > 1:
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+
+
+def bench_reference(args):
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if rank != 0:
+        return
+    from paper_2403_20190_b200.params import named_params
+    P = named_params("CFG2")
+    threads = cpu_threads()
+    sample = args.cpu_sample or max(16, min(256, 2 * threads))
+    keys, ms, lwe, tv = workload(P, sample, 0)
+    for _ in range(args.warmup):
+        run_cpu_port(P, keys, lwe, tv, min(sample, threads), threads)
+    rates = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r, out = run_cpu_port(P, keys, lwe, tv, sample, threads)
+        rates.append(r)
+    wall = time.perf_counter() - t0
+    from paper_2403_20190_b200 import tfhe
+    ok = bool(np.array_equal(tfhe.dec_lwe_batch(out, keys.lwe_key), expected(ms, P.p)))
+    value = sample * args.steps / wall
+    desc = (f"{sample} cfg2 PBS per step (oracle/c: exact schoolbook port of the reference's "
+            f"blind_rotate/extract path + restated KS, OpenMP {threads} threads, {cpu_model()})")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(wall / args.steps * 1e3, 1), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": config(P, args.batch, world, {"cpu_sample_per_step": sample}),
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": desc},
+        "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "check": "all outputs decrypt to the LUT" if ok else "DECRYPTION MISMATCH",
+    }), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        bench_reference(args)
+    else:
+        bench_hwb(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,132 @@
+/*
+ * hwb.h -- C ABI of libhwb200.so, the B200 (sm_100a) batched TFHE bootstrapping
+ * library.  Flat extern "C" entry points over plain pointers and sizes; no C++
+ * or torch types cross the boundary.
+ *
+ * The reference (`hewisard`, pure Python over numpy uint64) has no FFI; its
+ * drop-in boundary is the Python module API.  Each entry point below names the
+ * reference function whose computation it replaces (hw/ = pkg/src/hewisard/).
+ * The Python mirror of that API lives in paper_2403_20190_b200/ and binds these
+ * symbols with ctypes (see INTEGRATION.md for the binding a maintainer adds).
+ *
+ * Conventions
+ *   - q = 2^32.  Ciphertext words are little-endian uint32, C-contiguous, with
+ *     the reference axis orders: RLWE [a, b] (hw/tfhe.py:124), RGSW rows
+ *     b-gadget then a-gadget (hw/tfhe.py:148-152), LWE [a_0..a_{n-1}, b].
+ *   - All data pointers are DEVICE pointers owned by the caller (e.g. torch
+ *     tensors' data_ptr()); the library never allocates or frees caller memory.
+ *   - `stream` is a cudaStream_t passed as void*; every call is asynchronous on it.
+ *   - Return 0 on success; HWB_EINVAL for shape/parameter errors (the Python
+ *     layer raises TfheError, as the reference does, hw/tfhe.py:25-30);
+ *     HWB_ECUDA for launch/async CUDA errors (RuntimeError).  Nothing throws or
+ *     exits across the ABI.  hwb_last_error() describes the last failure of the
+ *     calling thread.
+ *   - Supported envelope: N in {1024, 2048}; gadget levels <= 3 and
+ *     2*levels * N * beta/2 * 2^31 < 2^55 (exact two-prime RNS NTT); see DESIGN.md.
+ */
+#ifndef HWB_H
+#define HWB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HWB_OK 0
+#define HWB_EINVAL 1
+#define HWB_ECUDA 2
+
+/* Parameter block (hw/params.py:47-82 at q = 2^32, plus the PBS LWE side). */
+typedef struct hwb_params {
+    uint32_t q_bits;      /* must be 32 */
+    uint32_t n;           /* LWE dimension (BSK length) */
+    uint32_t N;           /* ring degree */
+    uint32_t k;           /* GLWE dimension, must be 1 */
+    uint32_t l;           /* external-product gadget levels (GadgetSpec.levels) */
+    uint32_t base_log;    /* external-product gadget log2(beta) */
+    uint32_t ks_l;        /* LWE key-switch gadget levels */
+    uint32_t ks_base_log; /* LWE key-switch gadget log2(beta_ks) */
+} hwb_params;
+
+int hwb_version(void);
+const char *hwb_last_error(void);
+
+/* Select the CMUX-ladder kernel build: 0 = unconstrained registers (default),
+ * 1 = 128-register cap for twice the resident CTAs.  Both are bit-identical;
+ * the switch exists for A/B measurement (bench.py --variant). */
+int hwb_set_variant(int v);
+
+/* Measurement probe (not a reference function): launches a register-only
+ * kernel of `blocks` x 256 threads doing `iters` x 8 independent RNS modular
+ * multiplications each (one Shoup product per prime).  Returns the number of
+ * RNS modmuls enqueued (the caller times the stream), or -HWB_E* on error.
+ * Its rate is P_mm, the integer-pipe roofline denominator. */
+int64_t hwb_probe_modmul(uint32_t *sink, int32_t blocks, int32_t iters, void *stream);
+
+/* Number of uint32 words of one GGSW in the NTT domain used by every kernel:
+ * 2l rows x 2 components x 2 RNS primes x N. */
+size_t hwb_ggsw_ntt_words(const hwb_params *p);
+
+/* Forward transform of `count` GGSWs (coefficient domain, [count][2l][2][N] u32)
+ * into the NTT domain ([count][hwb_ggsw_ntt_words] u32).  Replaces the cached
+ * spectra of RgswCiphertext.spectra()/rgsw_rep (hw/tfhe.py:158-162, 322-324);
+ * used for the bootstrapping key (enc_rgsw_batch of s0, hw/tfhe.py:246-263). */
+int hwb_ggsw_to_ntt(const hwb_params *p, const uint32_t *ggsw, uint32_t *ggsw_ntt,
+                    int64_t count, void *stream);
+
+/* Batched external product (hw/tfhe.py:301-319 ext_product_batch):
+ *   out[b] = sum_r digit_r(in[b]) (*) G[idx[b]][r]
+ * ggsw_ntt: NTT-domain GGSWs; ggsw_idx: [B] int32 or NULL (broadcast GGSW 0);
+ * in/out: [B][2][N].  in and out may alias. */
+int hwb_ext_product(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_t *ggsw_idx,
+                    const uint32_t *in, uint32_t *out, int64_t B, void *stream);
+
+/* Batched CMUX (hw/tfhe.py:334-337 cmux; hw/lut.py:200-206 _cmux_sub):
+ *   out[b] = c0[b] + G[idx[b]] (*) (c1[b] - c0[b])
+ * If c1 == NULL, c1[b] = c0[b] * X^(rot[b]) (the rotated branch of blind_rotate,
+ * hw/tfhe.py:347, and of vp/ivp_batch, hw/lut.py:258, 289); rot may be NULL
+ * only when c1 != NULL.  out may alias c0. */
+int hwb_cmux(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_t *ggsw_idx,
+             const uint32_t *c1, const uint32_t *c0, const int32_t *rot, uint32_t *out,
+             int64_t B, void *stream);
+
+/* Batched CDEMUX (hw/lut.py:113-119): hi = G (*) d, lo = d - hi.
+ * d, lo, hi: [B][2][N]; lo may alias d. */
+int hwb_cdemux(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_t *ggsw_idx,
+               const uint32_t *d, uint32_t *lo, uint32_t *hi, int64_t B, void *stream);
+
+/* Fused blind rotation (hw/tfhe.py:340-349 blind_rotate), one launch for all L
+ * steps: acc[b] <- cmux(G_i, acc[b] * X^(-I[b][i]), acc[b]) for i < L.
+ * ggsw_ntt: L NTT-domain GGSWs shared by the batch (the BSK);
+ * exps: [B][L] int32 I values; acc: [B][2][N] in/out. */
+int hwb_blind_rotate(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_t *exps,
+                     uint32_t *acc, int32_t L, int64_t B, void *stream);
+
+/* Batched sample extraction of coefficient `coeff` (hw/tfhe.py:352-361; the
+ * batched coefficient-0 form is hw/lut.py:263-266): rlwe [B][2][N] ->
+ * lwe [B][N+1] (b last), under the coefficient vector of S1. */
+int hwb_sample_extract(const hwb_params *p, const uint32_t *rlwe, uint32_t *lwe, int64_t B,
+                       int32_t coeff, void *stream);
+
+/* LWE key switch N -> n (NEW; algebra of pack_batch hw/tfhe.py:397-420):
+ * ksk [N][ks_l][n+1], in [B][N+1], out [B][n+1]. */
+int hwb_keyswitch(const hwb_params *p, const uint32_t *ksk, const uint32_t *in, uint32_t *out,
+                  int64_t B, void *stream);
+
+/* Device workspace bytes hwb_pbs needs for a batch of B. */
+size_t hwb_pbs_workspace_bytes(const hwb_params *p, int64_t B);
+
+/* Programmable bootstrapping (NEW composition): mod switch ->
+ * acc = TV * X^(-b~) -> blind rotation with I_i = -a~_i -> extract -> key switch.
+ * tv: [2][N] (tv_per_item = 0) or [B][2][N]; lwe_in/lwe_out: [B][n+1].
+ * If ksk == NULL the key switch is skipped and lwe_out is [B][N+1]. */
+int hwb_pbs(const hwb_params *p, const uint32_t *bsk_ntt, const uint32_t *ksk,
+            const uint32_t *tv, int tv_per_item, const uint32_t *lwe_in, uint32_t *lwe_out,
+            int64_t B, void *workspace, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HWB_H */

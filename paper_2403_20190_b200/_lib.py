@@ -1,0 +1,100 @@
+"""ctypes binding of libhwb200.so (the C ABI declared in include/hwb.h).
+
+There is no CPU fallback: if the library or a GPU is missing, every
+homomorphic entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libhwb200.so")
+
+HWB_OK, HWB_EINVAL, HWB_ECUDA = 0, 1, 2
+
+# every symbol include/hwb.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "hwb_version", "hwb_last_error", "hwb_set_variant", "hwb_probe_modmul", "hwb_ggsw_ntt_words",
+    "hwb_ggsw_to_ntt", "hwb_ext_product", "hwb_cmux", "hwb_cdemux", "hwb_blind_rotate",
+    "hwb_sample_extract", "hwb_keyswitch", "hwb_pbs_workspace_bytes", "hwb_pbs",
+)
+
+
+class TfheError(ValueError):
+    """Parameter, arity, range and geometry errors (reference hw/tfhe.py:25-26)."""
+
+
+class EncodingError(TfheError):
+    """Message coefficient outside Z_p (reference hw/tfhe.py:29-30)."""
+
+
+class HwbParams(ctypes.Structure):
+    _fields_ = [(name, ctypes.c_uint32) for name in
+                ("q_bits", "n", "N", "k", "l", "base_log", "ks_l", "ks_base_log")]
+
+
+_lib = None
+_lock = threading.Lock()
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_pp = ctypes.POINTER(HwbParams)
+
+
+def load() -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        L.hwb_version.restype = ctypes.c_int
+        L.hwb_last_error.restype = ctypes.c_char_p
+        L.hwb_set_variant.argtypes = [ctypes.c_int]
+        L.hwb_probe_modmul.argtypes = [_vp, ctypes.c_int32, ctypes.c_int32, _vp]
+        L.hwb_probe_modmul.restype = ctypes.c_int64
+        L.hwb_ggsw_ntt_words.argtypes = [_pp]
+        L.hwb_ggsw_ntt_words.restype = ctypes.c_size_t
+        L.hwb_ggsw_to_ntt.argtypes = [_pp, _vp, _vp, _i64, _vp]
+        L.hwb_ext_product.argtypes = [_pp, _vp, _vp, _vp, _vp, _i64, _vp]
+        L.hwb_cmux.argtypes = [_pp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp]
+        L.hwb_cdemux.argtypes = [_pp, _vp, _vp, _vp, _vp, _vp, _i64, _vp]
+        L.hwb_blind_rotate.argtypes = [_pp, _vp, _vp, _vp, ctypes.c_int32, _i64, _vp]
+        L.hwb_sample_extract.argtypes = [_pp, _vp, _vp, _i64, ctypes.c_int32, _vp]
+        L.hwb_keyswitch.argtypes = [_pp, _vp, _vp, _vp, _i64, _vp]
+        L.hwb_pbs_workspace_bytes.argtypes = [_pp, _i64]
+        L.hwb_pbs_workspace_bytes.restype = ctypes.c_size_t
+        L.hwb_pbs.argtypes = [_pp, _vp, _vp, _vp, ctypes.c_int, _vp, _vp, _i64, _vp, _vp]
+        for name in EXPORTS:
+            if name not in ("hwb_version", "hwb_last_error", "hwb_ggsw_ntt_words",
+                            "hwb_pbs_workspace_bytes", "hwb_probe_modmul"):
+                getattr(L, name).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc == HWB_OK:
+        return
+    msg = load().hwb_last_error().decode(errors="replace")
+    if rc == HWB_EINVAL:
+        raise TfheError(msg)
+    raise RuntimeError(f"libhwb200: {msg}")
+
+
+def c_params(params) -> HwbParams:
+    """hwb_params from a paper_2403_20190_b200.params.HeParams."""
+    return HwbParams(32, int(params.lwe_n), int(params.n), 1, int(params.gadget.levels),
+                     int(params.gadget.base_log), int(params.gadget_ks.levels),
+                     int(params.gadget_ks.base_log))
+
+
+def set_variant(v: int) -> None:
+    check(load().hwb_set_variant(int(v)))

@@ -1,0 +1,760 @@
+// libhwb200: batched TFHE bootstrapping kernels for B200 (sm_100a) and their C ABI.
+//
+// Kernels:
+//   ggsw_to_ntt_kernel  GGSW -> NTT domain (Montgomery form, N^-1 folded)
+//   cmux_kernel<MODE>   batched external product / CMUX / CDEMUX, one item per CTA
+//   blind_rotate_kernel fused CMUX ladder (hw/tfhe.py:340-349), all L steps in one
+//                       launch with the accumulator resident in shared memory;
+//                       PBS mode adds mod switch, TV rotation and extraction
+//   extract_kernel      coefficient-0 sample extraction (hw/tfhe.py:352-361)
+//   keyswitch_kernel    LWE key switch as a tiled integer contraction mod 2^32
+//
+// CTA shape for the ladder/CMUX kernels: 2 warps = one ciphertext; warp w works
+// modulo prime p_w on both GLWE components, then the warps exchange residues
+// through shared memory and warp w lifts component w by CRT.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/hwb.h"
+#include "hwb_device.cuh"
+
+namespace hwb {
+
+static thread_local std::string g_err;
+// kernel variant: 0 = unconstrained registers (4 CTAs/SM), 1 = 128-register cap
+// (8 CTAs/SM).  Selected with hwb_set_variant() for A/B measurement.
+static int g_variant = 0;
+
+static int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+// ---------------------------------------------------------------------------
+// host-side table construction
+
+static uint32_t powmod(uint64_t b, uint64_t e, uint64_t m) {
+  uint64_t r = 1;
+  b %= m;
+  while (e) {
+    if (e & 1) r = r * b % m;
+    b = b * b % m;
+    e >>= 1;
+  }
+  return (uint32_t)r;
+}
+
+static uint32_t bitrev(uint32_t x, int bits) {
+  uint32_t r = 0;
+  for (int i = 0; i < bits; ++i) r |= ((x >> i) & 1u) << (bits - 1 - i);
+  return r;
+}
+
+static uint2 shoup_pair(uint32_t w, uint32_t p) {
+  return make_uint2(w, (uint32_t)(((uint64_t)w << 32) / p));
+}
+
+struct DevState {
+  bool ready = false;
+  uint2 *lane_fwd[2][2] = {};
+  uint2 *lane_inv[2][2] = {};
+};
+
+static std::mutex g_mu;
+static DevState g_state[64];
+
+static int slots_for(int N) { return (N / 32) * 31 / 32; }
+
+static int init_device(DevState **out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(HWB_ECUDA, std::string("cudaGetDevice: ") + cudaGetErrorString(e));
+  if (dev < 0 || dev >= 64) return fail(HWB_ECUDA, "device index out of range");
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevState &st = g_state[dev];
+  if (st.ready) {
+    *out = &st;
+    return HWB_OK;
+  }
+  const uint32_t primes[2] = {kP0, kP1};
+  static uint2 h_tw[2][2][2][64];
+  uint32_t h_r2ninv[2][2];
+  PrimeConst h_prime[2];
+  for (int pr = 0; pr < 2; ++pr) {
+    uint32_t p = primes[pr];
+    uint32_t inv = 1;   // p^-1 mod 2^32 by Newton
+    for (int i = 0; i < 5; ++i) inv *= 2u - p * inv;
+    h_prime[pr] = PrimeConst{p, 2u * p, inv};
+  }
+  for (int nv = 0; nv < 2; ++nv) {
+    const int N = nv == 0 ? 1024 : 2048;
+    const int logN = nv == 0 ? 10 : 11;
+    const int C = N / 32;
+    const int S = slots_for(N);
+    for (int pr = 0; pr < 2; ++pr) {
+      const uint32_t p = primes[pr];
+      uint32_t psi = 0;
+      for (uint32_t a = 2; a < 1000; ++a) {
+        uint32_t c = powmod(a, (p - 1) / (2 * N), p);
+        if (powmod(c, N, p) == p - 1) {
+          psi = c;
+          break;
+        }
+      }
+      if (!psi) return fail(HWB_ECUDA, "no 2N-th root of unity");
+      const uint32_t psi_inv = powmod(psi, p - 2, p);
+      std::vector<uint32_t> fw(N), iw(N);
+      for (int k = 0; k < N; ++k) {
+        fw[k] = powmod(psi, bitrev(k, logN), p);
+        iw[k] = powmod(psi_inv, bitrev(k, logN), p);
+      }
+      for (int k = 0; k < 64; ++k) {
+        h_tw[nv][0][pr][k] = k < C ? shoup_pair(fw[k], p) : make_uint2(0, 0);
+        h_tw[nv][1][pr][k] = k < C ? shoup_pair(iw[k], p) : make_uint2(0, 0);
+      }
+      // per-lane tables: forward spans t = 16..1, inverse spans t = 1..16; slot
+      // (t, u) of lane l holds psi_rev[N/(2t) + l * C/(2t) + u]
+      std::vector<uint2> lf((size_t)S * 32), li((size_t)S * 32);
+      int slot = 0;
+      for (int t = 16; t >= 1; t >>= 1) {
+        int nb = C / (2 * t);
+        for (int u = 0; u < nb; ++u)
+          for (int l = 0; l < 32; ++l) lf[(size_t)(slot + u) * 32 + l] = shoup_pair(fw[N / (2 * t) + l * nb + u], p);
+        slot += nb;
+      }
+      slot = 0;
+      for (int t = 1; t <= 16; t <<= 1) {
+        int nb = C / (2 * t);
+        for (int u = 0; u < nb; ++u)
+          for (int l = 0; l < 32; ++l) li[(size_t)(slot + u) * 32 + l] = shoup_pair(iw[N / (2 * t) + l * nb + u], p);
+        slot += nb;
+      }
+      size_t bytes = sizeof(uint2) * S * 32;
+      cudaError_t e1 = cudaMalloc(&st.lane_fwd[nv][pr], bytes);
+      cudaError_t e2 = cudaMalloc(&st.lane_inv[nv][pr], bytes);
+      if (e1 != cudaSuccess || e2 != cudaSuccess) return fail(HWB_ECUDA, "cudaMalloc twiddle tables failed");
+      cudaMemcpy(st.lane_fwd[nv][pr], lf.data(), bytes, cudaMemcpyHostToDevice);
+      cudaMemcpy(st.lane_inv[nv][pr], li.data(), bytes, cudaMemcpyHostToDevice);
+      // Montgomery form with N^-1: x -> x * R * N^-1 via mont_mul(x, R^2 N^-1)
+      uint64_t R = ((uint64_t)1 << 32) % p;
+      uint64_t r2 = R * R % p;
+      uint64_t ninv = powmod(N, p - 2, p);
+      h_r2ninv[nv][pr] = (uint32_t)(r2 * ninv % p);
+    }
+  }
+  const uint32_t crt_inv = powmod(kP0, kP1 - 2, kP1);
+  const uint2 crt_pair = shoup_pair(crt_inv, kP1);
+  uint32_t h_crt[4] = {crt_pair.x, crt_pair.y, (uint32_t)((uint64_t)kP0 * kP1), kP1 / 2};
+  cudaError_t ec = cudaMemcpyToSymbol(c_tw, h_tw, sizeof(h_tw));
+  if (ec == cudaSuccess) ec = cudaMemcpyToSymbol(c_prime, h_prime, sizeof(h_prime));
+  if (ec == cudaSuccess) ec = cudaMemcpyToSymbol(c_crt, h_crt, sizeof(h_crt));
+  if (ec == cudaSuccess) ec = cudaMemcpyToSymbol(c_r2ninv, h_r2ninv, sizeof(h_r2ninv));
+  if (ec != cudaSuccess) return fail(HWB_ECUDA, std::string("constant upload: ") + cudaGetErrorString(ec));
+  st.ready = true;
+  *out = &st;
+  return HWB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// kernels
+
+template <int N>
+struct Smem {
+  uint32_t acc[2 * N];   // working ciphertext (a, b)
+  uint32_t v[2 * N];     // decomposition-ready input; then the residue exchange
+  uint32_t scr[2][N];    // per-warp transpose scratch
+};
+
+struct Tw {
+  const uint2 *fwd[2];
+  const uint2 *inv[2];
+};
+
+// One external product for the CTA's item.  Pre: sm.v holds decomp_prep() of
+// the input (both components) and a barrier has passed.  Post (after the
+// internal barriers): x holds, in layout A, the canonical residues mod p_w of
+// component w, and sm.v[w*N + i] holds those mod p_{1-w} of component w.
+template <int N>
+__device__ __forceinline__ void ext_product_core(Smem<N> &sm, const uint32_t *__restrict__ G,
+                                                 const Gadget &g, int w, int lane, const Tw &tw,
+                                                 uint32_t (&x)[N / 32]) {
+  constexpr int C = N / 32;
+  const uint32_t p = c_prime[w].p, two_p = c_prime[w].two_p, pinv = c_prime[w].pinv;
+  const uint32_t off = p - g.half;
+  const int L = (int)g.levels;
+  uint32_t a0[C], a1[C];
+#pragma unroll
+  for (int j = 0; j < C; ++j) a0[j] = a1[j] = 0;
+
+#pragma unroll 1
+  for (int r = 0; r < 2 * L; ++r) {
+    // digit order (hw/tfhe.py:290-298): rows 0..l-1 = digits of b, l..2l-1 of a
+    const int comp = r < L ? 1 : 0;
+    const int t = r < L ? r : r - L;
+    const uint32_t sh = g.base_log * (uint32_t)(L - 1 - t);
+    const uint32_t *vs = sm.v + comp * N;
+#pragma unroll
+    for (int j = 0; j < C; ++j) x[j] = ((vs[lane + 32 * j] >> sh) & g.mask) + off;
+    fwd_ntt<N>(x, sm.scr[w], lane, w, (w ? tw.fwd[1] : tw.fwd[0]));
+    const uint32_t *g0 = G + ((size_t)(r * 2 + 0) * 2 + w) * N;
+    const uint32_t *g1 = G + ((size_t)(r * 2 + 1) * 2 + w) * N;
+#pragma unroll
+    for (int jq = 0; jq < C / 4; ++jq) {
+      const uint4 G0 = __ldg(slice_vec<N>(g0, lane, jq));
+      const uint4 G1 = __ldg(slice_vec<N>(g1, lane, jq));
+      a0[4 * jq + 0] += mont_mul(x[4 * jq + 0], G0.x, p, pinv);
+      a0[4 * jq + 1] += mont_mul(x[4 * jq + 1], G0.y, p, pinv);
+      a0[4 * jq + 2] += mont_mul(x[4 * jq + 2], G0.z, p, pinv);
+      a0[4 * jq + 3] += mont_mul(x[4 * jq + 3], G0.w, p, pinv);
+      a1[4 * jq + 0] += mont_mul(x[4 * jq + 0], G1.x, p, pinv);
+      a1[4 * jq + 1] += mont_mul(x[4 * jq + 1], G1.y, p, pinv);
+      a1[4 * jq + 2] += mont_mul(x[4 * jq + 2], G1.z, p, pinv);
+      a1[4 * jq + 3] += mont_mul(x[4 * jq + 3], G1.w, p, pinv);
+    }
+  }
+  // 2l <= 6 terms in (0, 2p): sums < 12p < 2^32; reduce to [0, 2p)
+#pragma unroll
+  for (int j = 0; j < C; ++j) {
+    uint32_t u = a0[j], v = a1[j];
+    u = umin(u, u - 4 * two_p); v = umin(v, v - 4 * two_p);
+    u = umin(u, u - 2 * two_p); v = umin(v, v - 2 * two_p);
+    u = umin(u, u - two_p);     v = umin(v, v - two_p);
+    a0[j] = u; a1[j] = v;
+  }
+  __syncthreads();   // both warps are done reading sm.v: it becomes the exchange buffer
+#pragma unroll 1
+  for (int it = 0; it < 2; ++it) {
+    const int c = it == 0 ? 1 - w : w;
+#pragma unroll
+    for (int j = 0; j < C; ++j) x[j] = c ? a1[j] : a0[j];
+    inv_ntt<N>(x, sm.scr[w], lane, w, (w ? tw.inv[1] : tw.inv[0]));
+#pragma unroll
+    for (int j = 0; j < C; ++j) x[j] = umin(x[j], x[j] - p);
+    if (it == 0) {
+#pragma unroll
+      for (int j = 0; j < C; ++j) sm.v[c * N + lane + 32 * j] = x[j];
+    }
+  }
+  __syncthreads();   // exchange complete
+}
+
+__device__ __forceinline__ uint32_t lift(int w, uint32_t own, uint32_t other) {
+  return w == 0 ? crt_lift(own, other) : crt_lift(other, own);
+}
+
+// negacyclic rotation read: (x * X^e)[i] with e in [0, 2N)
+template <int N>
+__device__ __forceinline__ uint32_t rot_read(const uint32_t *poly, int i, int e) {
+  const int src = (i - e) & (2 * N - 1);
+  const uint32_t val = poly[src & (N - 1)];
+  return src >= N ? 0u - val : val;
+}
+
+enum { MODE_EXT = 0, MODE_CMUX = 1, MODE_CDEMUX = 2 };
+
+template <int N, int MODE, int MINB>
+__global__ void __launch_bounds__(64, MINB) cmux_kernel(const uint32_t *__restrict__ ggsw, size_t ggsw_words,
+                                                  const int32_t *__restrict__ gidx,
+                                                  const uint32_t *in, const uint32_t *c1,
+                                                  const int32_t *__restrict__ rot, uint32_t *out,
+                                                  uint32_t *out_hi, Gadget g, Tw tw) {
+  extern __shared__ uint4 smem_raw[];
+  Smem<N> &sm = *reinterpret_cast<Smem<N> *>(smem_raw);
+  const int64_t b = blockIdx.x;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const uint32_t *G = ggsw + (size_t)(gidx ? gidx[b] : 0) * ggsw_words;
+  const uint32_t *src = in + b * 2 * N;
+  if (MODE == MODE_EXT) {
+    for (int k = tid; k < 2 * N; k += 64) sm.v[k] = decomp_prep(src[k], g);
+  } else {
+    for (int k = tid; k < 2 * N; k += 64) sm.acc[k] = src[k];
+    __syncthreads();
+    if (MODE == MODE_CMUX) {
+      if (c1) {
+        const uint32_t *s1 = c1 + b * 2 * N;
+        for (int k = tid; k < 2 * N; k += 64) sm.v[k] = decomp_prep(s1[k] - sm.acc[k], g);
+      } else {
+        const int e = ((rot[b] % (2 * N)) + 2 * N) % (2 * N);
+        for (int k = tid; k < 2 * N; k += 64) {
+          const int c = k >= N, i = k & (N - 1);
+          sm.v[k] = decomp_prep(rot_read<N>(sm.acc + c * N, i, e) - sm.acc[k], g);
+        }
+      }
+    } else {
+      for (int k = tid; k < 2 * N; k += 64) sm.v[k] = decomp_prep(sm.acc[k], g);
+    }
+  }
+  __syncthreads();
+  uint32_t x[N / 32];
+  ext_product_core<N>(sm, G, g, w, lane, tw, x);
+  uint32_t *o = out + b * 2 * N + w * N;
+#pragma unroll
+  for (int j = 0; j < N / 32; ++j) {
+    const int i = lane + 32 * j;
+    const uint32_t val = lift(w, x[j], sm.v[w * N + i]);
+    if (MODE == MODE_EXT) {
+      o[i] = val;
+    } else if (MODE == MODE_CMUX) {
+      o[i] = sm.acc[w * N + i] + val;
+    } else {
+      out_hi[b * 2 * N + w * N + i] = val;
+      o[i] = sm.acc[w * N + i] - val;
+    }
+  }
+}
+
+__device__ __forceinline__ int mod_switch(uint32_t x, int log2m) {
+  return (int)((x + (1u << (31 - log2m))) >> (32 - log2m));
+}
+
+// Fused blind rotation.  PBS = false: acc_io [B][2][N] in/out, exps [B][L] are
+// the reference's I values (rotation X^-I).  PBS = true: lwe_in [B][L+1];
+// acc = TV * X^-b~, rotation X^{a~_i} (I_i = -a~_i), output the coefficient-0
+// extraction [B][N+1].
+template <int N, bool PBS, int MINB>
+__global__ void __launch_bounds__(64, MINB) blind_rotate_kernel(
+    const uint32_t *__restrict__ bsk, size_t ggsw_words, const int32_t *__restrict__ exps,
+    const uint32_t *__restrict__ lwe_in, const uint32_t *__restrict__ tv, int tv_per_item,
+    uint32_t *acc_io, uint32_t *lwe_out, int L, Gadget g, Tw tw) {
+  extern __shared__ uint4 smem_raw[];
+  Smem<N> &sm = *reinterpret_cast<Smem<N> *>(smem_raw);
+  constexpr int LOG2M = (N == 1024) ? 11 : 12;
+  const int64_t b = blockIdx.x;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const uint32_t *row = PBS ? lwe_in + b * (int64_t)(L + 1) : nullptr;
+  if (PBS) {
+    const int bt = mod_switch(row[L], LOG2M);
+    const uint32_t *t = tv + (tv_per_item ? b * 2 * N : 0);
+    const int e = (2 * N - bt) & (2 * N - 1);   // X^-b~
+    for (int k = tid; k < 2 * N; k += 64) {
+      const int c = k >= N, i = k & (N - 1);
+      sm.acc[k] = rot_read<N>(t + c * N, i, e);
+    }
+  } else {
+    for (int k = tid; k < 2 * N; k += 64) sm.acc[k] = acc_io[b * 2 * N + k];
+  }
+  __syncthreads();
+  uint32_t x[N / 32];
+#pragma unroll 1
+  for (int s = 0; s < L; ++s) {
+    int e;
+    if (PBS) {
+      e = mod_switch(row[s], LOG2M);   // X^{a~_s}
+    } else {
+      e = (int)((-(int64_t)exps[b * L + s]) % (2 * N));
+      if (e < 0) e += 2 * N;
+    }
+    if (e == 0) continue;   // zero difference -> zero product: exact skip
+    for (int k = tid; k < 2 * N; k += 64) {
+      const int c = k >= N, i = k & (N - 1);
+      sm.v[k] = decomp_prep(rot_read<N>(sm.acc + c * N, i, e) - sm.acc[k], g);
+    }
+    __syncthreads();
+    ext_product_core<N>(sm, bsk + (size_t)s * ggsw_words, g, w, lane, tw, x);
+#pragma unroll
+    for (int j = 0; j < N / 32; ++j) {
+      const int i = lane + 32 * j;
+      sm.acc[w * N + i] += lift(w, x[j], sm.v[w * N + i]);
+    }
+    __syncthreads();
+  }
+  if (PBS) {
+    uint32_t *o = lwe_out + b * (int64_t)(N + 1);
+    for (int k = tid; k < N; k += 64) o[k] = k == 0 ? sm.acc[0] : 0u - sm.acc[N - k];
+    if (tid == 0) o[N] = sm.acc[N];
+  } else {
+    for (int k = tid; k < 2 * N; k += 64) acc_io[b * 2 * N + k] = sm.acc[k];
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(64) ggsw_to_ntt_kernel(const uint32_t *__restrict__ in, uint32_t *out,
+                                                         Tw tw) {
+  __shared__ uint32_t scr[2][N];
+  constexpr int C = N / 32;
+  constexpr int NV = NVar<N>::v;
+  const int64_t poly = blockIdx.x;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t p = c_prime[w].p, pinv = c_prime[w].pinv;
+  uint32_t x[C];
+#pragma unroll
+  for (int j = 0; j < C; ++j) {
+    int32_t s = (int32_t)in[poly * N + lane + 32 * j];   // centred coefficient
+    int32_t r = s % (int32_t)p;
+    x[j] = (uint32_t)(r < 0 ? r + (int32_t)p : r);
+  }
+  fwd_ntt<N>(x, scr[w], lane, w, (w ? tw.fwd[1] : tw.fwd[0]));
+  const uint32_t k = c_r2ninv[NV][w];
+  uint4 *o = reinterpret_cast<uint4 *>(out + (poly * 2 + w) * N);
+#pragma unroll
+  for (int jq = 0; jq < C / 4; ++jq) {
+    uint32_t y[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t v = mont_mul(x[4 * jq + q], k, p, pinv);   // (0, 2p)
+      y[q] = umin(v, v - p);
+    }
+    o[jq * 32 + lane] = make_uint4(y[0], y[1], y[2], y[3]);
+  }
+}
+
+// hw/tfhe.py:352-361: LWE of coefficient i: a'[j] = a[i-j] (j <= i),
+// -a[N+i-j] (j > i); b' = b[i].
+template <int N>
+__global__ void extract_kernel(const uint32_t *__restrict__ rlwe, uint32_t *lwe, int64_t B, int coeff) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= B * (N + 1)) return;
+  const int64_t b = idx / (N + 1);
+  const int k = (int)(idx % (N + 1));
+  const uint32_t *a = rlwe + b * 2 * N;
+  lwe[idx] = k == N ? a[N + coeff] : (k <= coeff ? a[coeff - k] : 0u - a[N + coeff - k]);
+}
+
+// LWE key switch: out[b][c] = (c < n ? 0 : in[b][N]) - sum_{j,t} d[b][j][t] * ksk[j][t][c]
+// CTA tile: 64 items x 64 output columns, K chunked by KS_TJ input coefficients.
+constexpr int KS_TB = 64, KS_TC = 64, KS_TJ = 4, KS_MAXL = 16;
+
+__global__ void __launch_bounds__(256) keyswitch_kernel(const uint32_t *__restrict__ ksk,
+                                                        const uint32_t *__restrict__ in, uint32_t *out,
+                                                        int64_t B, int N, int n, Gadget gk) {
+  __shared__ int32_t dig[KS_TJ * KS_MAXL][KS_TB];
+  __shared__ uint32_t kt[KS_TJ * KS_MAXL][KS_TC];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int64_t b0 = (int64_t)blockIdx.x * KS_TB;
+  const int c0 = blockIdx.y * KS_TC;
+  const int L = (int)gk.levels;
+  const int rows = KS_TJ * L;
+  const int ncol = n + 1;
+  uint32_t acc[4][4] = {};
+  for (int jc = 0; jc < N; jc += KS_TJ) {
+    {   // digits of a'_j for 64 items x KS_TJ coefficients: one per thread
+      const int item = tid & 63, jj = tid >> 6;
+      const int64_t bi = b0 + item;
+      uint32_t a = (bi < B && jc + jj < N) ? in[bi * (N + 1) + jc + jj] : 0u;
+      const uint32_t v = decomp_prep(a, gk);
+      for (int t = 0; t < L; ++t) {
+        const uint32_t sh = gk.base_log * (uint32_t)(L - 1 - t);
+        dig[jj * L + t][item] = (int32_t)((v >> sh) & gk.mask) - (int32_t)gk.half;
+      }
+    }
+    for (int e = tid; e < rows * KS_TC; e += 256) {
+      const int r = e / KS_TC, cc = e % KS_TC;
+      const int col = c0 + cc;
+      kt[r][cc] = col < ncol ? ksk[((size_t)jc * L + r) * ncol + col] : 0u;
+    }
+    __syncthreads();
+    for (int r = 0; r < rows; ++r) {
+      const int4 dv = *reinterpret_cast<const int4 *>(&dig[r][ty * 4]);
+      const uint4 kv = *reinterpret_cast<const uint4 *>(&kt[r][tx * 4]);
+      const uint32_t d[4] = {(uint32_t)dv.x, (uint32_t)dv.y, (uint32_t)dv.z, (uint32_t)dv.w};
+      const uint32_t k[4] = {kv.x, kv.y, kv.z, kv.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[i][q] += d[i] * k[q];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t bi = b0 + ty * 4 + i;
+    if (bi >= B) continue;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int col = c0 + tx * 4 + q;
+      if (col >= ncol) continue;
+      out[bi * ncol + col] = (col < n ? 0u : in[bi * (N + 1) + N]) - acc[i][q];
+    }
+  }
+}
+
+// Register-only throughput probe of the shipped modular multiplication: each
+// thread runs 8 independent chains; one "RNS modmul" = one Shoup product mod p0
+// and one mod p1 (the two-prime counterpart of a 64-bit-prime modmul).  Gives
+// P_mm, the denominator of the integer roofline.
+__global__ void __launch_bounds__(256) probe_modmul_kernel(uint32_t *sink, int iters) {
+  const uint32_t p0 = kP0, p1 = kP1;
+  const uint32_t w0 = 123456789u % kP0, w1 = 987654321u % kP1;
+  const uint32_t q0 = (uint32_t)(((uint64_t)w0 << 32) / kP0), q1 = (uint32_t)(((uint64_t)w1 << 32) / kP1);
+  uint32_t a[8], b[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = b[k] = threadIdx.x * 8 + k + blockIdx.x;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      a[k] = shoup_mul(a[k], w0, q0, p0);
+      b[k] = shoup_mul(b[k], w1, q1, p1);
+    }
+  }
+  uint32_t s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s ^= a[k] ^ b[k];
+  if (s == 0x12345678u) sink[0] = s;
+}
+
+// ---------------------------------------------------------------------------
+// host helpers
+
+static Gadget make_gadget(uint32_t levels, uint32_t base_log) {
+  Gadget g;
+  const uint32_t total = levels * base_log;
+  g.round_add = total < 32 ? (1u << (31 - total)) : 0u;
+  g.shift = 32 - total;
+  uint32_t h = 0;
+  for (uint32_t k = 0; k < levels; ++k) h += (1u << (base_log - 1)) << (base_log * k);
+  g.hsum = h;
+  g.mask = base_log >= 32 ? 0xFFFFFFFFu : ((1u << base_log) - 1u);
+  g.half = 1u << (base_log - 1);
+  g.base_log = base_log;
+  g.levels = levels;
+  return g;
+}
+
+static int check_glwe(const hwb_params *p) {
+  if (!p) return fail(HWB_EINVAL, "null params");
+  if (p->q_bits != 32) return fail(HWB_EINVAL, "q_bits must be 32");
+  if (p->k != 1) return fail(HWB_EINVAL, "only GLWE dimension k = 1 is supported");
+  if (p->N != 1024 && p->N != 2048) return fail(HWB_EINVAL, "ring degree N must be 1024 or 2048");
+  if (p->l < 1 || p->l > 3) return fail(HWB_EINVAL, "gadget levels must be in [1, 3]");
+  if (p->base_log < 1 || p->l * p->base_log > 32) return fail(HWB_EINVAL, "gadget spans more than 32 bits");
+  // exactness of the two-prime RNS: max |sum| = 2l * N * beta/2 * 2^31 < P/2
+  const double bound = 2.0 * p->l * p->N * std::ldexp(1.0, (int)p->base_log - 1) * std::ldexp(1.0, 31);
+  const double halfP = 0.5 * (double)kP0 * (double)kP1;
+  if (!(bound < halfP)) return fail(HWB_EINVAL, "gadget/ring too wide for the exact 2-prime NTT (2l N beta/2 2^31 >= P/2)");
+  return HWB_OK;
+}
+
+static int check_ks(const hwb_params *p) {
+  if (p->ks_l < 1 || p->ks_l > (uint32_t)KS_MAXL) return fail(HWB_EINVAL, "key-switch levels must be in [1, 16]");
+  if (p->ks_base_log < 1 || p->ks_l * p->ks_base_log > 32) return fail(HWB_EINVAL, "key-switch gadget spans more than 32 bits");
+  if (p->n < 1) return fail(HWB_EINVAL, "LWE dimension n must be positive");
+  return HWB_OK;
+}
+
+static int post_launch(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(HWB_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return HWB_OK;
+}
+
+static Tw make_tw(DevState *st, int N) {
+  const int nv = N == 1024 ? 0 : 1;
+  Tw tw;
+  for (int pr = 0; pr < 2; ++pr) {
+    tw.fwd[pr] = st->lane_fwd[nv][pr];
+    tw.inv[pr] = st->lane_inv[nv][pr];
+  }
+  return tw;
+}
+
+template <typename K>
+static int set_smem(K kernel, size_t bytes) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return fail(HWB_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+  return HWB_OK;
+}
+
+template <int N, int MODE>
+static int launch_cmux(const hwb_params *p, DevState *st, const uint32_t *ggsw, const int32_t *gidx,
+                       const uint32_t *in, const uint32_t *c1, const int32_t *rot, uint32_t *out,
+                       uint32_t *out_hi, int64_t B, cudaStream_t s) {
+  const size_t smem = sizeof(Smem<N>);
+  const size_t words = hwb_ggsw_ntt_words(p);
+  const Gadget g = make_gadget(p->l, p->base_log);
+  int rc;
+  if (g_variant == 1) {
+    if ((rc = set_smem(cmux_kernel<N, MODE, 8>, smem))) return rc;
+    cmux_kernel<N, MODE, 8><<<(unsigned)B, 64, smem, s>>>(ggsw, words, gidx, in, c1, rot, out, out_hi, g, make_tw(st, N));
+  } else {
+    if ((rc = set_smem(cmux_kernel<N, MODE, 1>, smem))) return rc;
+    cmux_kernel<N, MODE, 1><<<(unsigned)B, 64, smem, s>>>(ggsw, words, gidx, in, c1, rot, out, out_hi, g, make_tw(st, N));
+  }
+  return post_launch("cmux_kernel");
+}
+
+template <int N, bool PBS>
+static int launch_br(const hwb_params *p, DevState *st, const uint32_t *bsk, const int32_t *exps,
+                     const uint32_t *lwe_in, const uint32_t *tv, int tv_per_item, uint32_t *acc,
+                     uint32_t *lwe_out, int L, int64_t B, cudaStream_t s) {
+  const size_t smem = sizeof(Smem<N>);
+  const Gadget g = make_gadget(p->l, p->base_log);
+  const size_t words = hwb_ggsw_ntt_words(p);
+  int rc;
+  if (g_variant == 1) {
+    if ((rc = set_smem(blind_rotate_kernel<N, PBS, 8>, smem))) return rc;
+    blind_rotate_kernel<N, PBS, 8><<<(unsigned)B, 64, smem, s>>>(bsk, words, exps, lwe_in, tv, tv_per_item, acc,
+                                                                 lwe_out, L, g, make_tw(st, N));
+  } else {
+    if ((rc = set_smem(blind_rotate_kernel<N, PBS, 1>, smem))) return rc;
+    blind_rotate_kernel<N, PBS, 1><<<(unsigned)B, 64, smem, s>>>(bsk, words, exps, lwe_in, tv, tv_per_item, acc,
+                                                                 lwe_out, L, g, make_tw(st, N));
+  }
+  return post_launch("blind_rotate_kernel");
+}
+
+static int keyswitch_launch(const hwb_params *p, const uint32_t *ksk, const uint32_t *in, uint32_t *out,
+                            int64_t B, cudaStream_t s) {
+  dim3 grid((unsigned)((B + KS_TB - 1) / KS_TB), (unsigned)((p->n + 1 + KS_TC - 1) / KS_TC));
+  keyswitch_kernel<<<grid, 256, 0, s>>>(ksk, in, out, B, (int)p->N, (int)p->n,
+                                        make_gadget(p->ks_l, p->ks_base_log));
+  return post_launch("keyswitch_kernel");
+}
+
+}  // namespace hwb
+
+using namespace hwb;
+
+extern "C" {
+
+int hwb_version(void) { return 1; }
+
+int64_t hwb_probe_modmul(uint32_t *sink, int32_t blocks, int32_t iters, void *stream) {
+  if (blocks < 1 || iters < 1) return -fail(HWB_EINVAL, "probe needs positive blocks and iters");
+  probe_modmul_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(sink, iters);
+  if (post_launch("probe_modmul_kernel")) return -HWB_ECUDA;
+  return (int64_t)blocks * 256 * 8 * iters;
+}
+
+int hwb_set_variant(int v) {
+  if (v < 0 || v > 1) return fail(HWB_EINVAL, "unknown kernel variant");
+  g_variant = v;
+  return HWB_OK;
+}
+
+const char *hwb_last_error(void) { return g_err.c_str(); }
+
+size_t hwb_ggsw_ntt_words(const hwb_params *p) {
+  if (!p) return 0;
+  return (size_t)2 * p->l * 2 * 2 * p->N;
+}
+
+int hwb_ggsw_to_ntt(const hwb_params *p, const uint32_t *ggsw, uint32_t *ggsw_ntt, int64_t count,
+                    void *stream) {
+  int rc = check_glwe(p);
+  if (rc) return rc;
+  if (count < 0) return fail(HWB_EINVAL, "negative count");
+  if (count == 0) return HWB_OK;
+  DevState *st;
+  if ((rc = init_device(&st))) return rc;
+  const int64_t polys = count * 2 * p->l * 2;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p->N == 1024)
+    ggsw_to_ntt_kernel<1024><<<(unsigned)polys, 64, 0, s>>>(ggsw, ggsw_ntt, make_tw(st, 1024));
+  else
+    ggsw_to_ntt_kernel<2048><<<(unsigned)polys, 64, 0, s>>>(ggsw, ggsw_ntt, make_tw(st, 2048));
+  return post_launch("ggsw_to_ntt_kernel");
+}
+
+static int cmux_dispatch(int mode, const hwb_params *p, const uint32_t *ggsw, const int32_t *gidx,
+                         const uint32_t *in, const uint32_t *c1, const int32_t *rot, uint32_t *out,
+                         uint32_t *out_hi, int64_t B, void *stream) {
+  int rc = check_glwe(p);
+  if (rc) return rc;
+  if (B < 0) return fail(HWB_EINVAL, "negative batch");
+  if (B == 0) return HWB_OK;
+  if (B > 0x7FFFFFFF) return fail(HWB_EINVAL, "batch too large");
+  DevState *st;
+  if ((rc = init_device(&st))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p->N == 1024) {
+    if (mode == MODE_EXT) return launch_cmux<1024, MODE_EXT>(p, st, ggsw, gidx, in, c1, rot, out, out_hi, B, s);
+    if (mode == MODE_CMUX) return launch_cmux<1024, MODE_CMUX>(p, st, ggsw, gidx, in, c1, rot, out, out_hi, B, s);
+    return launch_cmux<1024, MODE_CDEMUX>(p, st, ggsw, gidx, in, c1, rot, out, out_hi, B, s);
+  }
+  if (mode == MODE_EXT) return launch_cmux<2048, MODE_EXT>(p, st, ggsw, gidx, in, c1, rot, out, out_hi, B, s);
+  if (mode == MODE_CMUX) return launch_cmux<2048, MODE_CMUX>(p, st, ggsw, gidx, in, c1, rot, out, out_hi, B, s);
+  return launch_cmux<2048, MODE_CDEMUX>(p, st, ggsw, gidx, in, c1, rot, out, out_hi, B, s);
+}
+
+int hwb_ext_product(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_t *ggsw_idx,
+                    const uint32_t *in, uint32_t *out, int64_t B, void *stream) {
+  return cmux_dispatch(MODE_EXT, p, ggsw_ntt, ggsw_idx, in, nullptr, nullptr, out, nullptr, B, stream);
+}
+
+int hwb_cmux(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_t *ggsw_idx, const uint32_t *c1,
+             const uint32_t *c0, const int32_t *rot, uint32_t *out, int64_t B, void *stream) {
+  if (!c1 && !rot) return fail(HWB_EINVAL, "cmux needs c1 or a rotation vector");
+  return cmux_dispatch(MODE_CMUX, p, ggsw_ntt, ggsw_idx, c0, c1, rot, out, nullptr, B, stream);
+}
+
+int hwb_cdemux(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_t *ggsw_idx, const uint32_t *d,
+               uint32_t *lo, uint32_t *hi, int64_t B, void *stream) {
+  return cmux_dispatch(MODE_CDEMUX, p, ggsw_ntt, ggsw_idx, d, nullptr, nullptr, lo, hi, B, stream);
+}
+
+int hwb_blind_rotate(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_t *exps, uint32_t *acc,
+                     int32_t L, int64_t B, void *stream) {
+  int rc = check_glwe(p);
+  if (rc) return rc;
+  if (B < 0 || L < 0) return fail(HWB_EINVAL, "negative batch or length");
+  if (B == 0) return HWB_OK;
+  DevState *st;
+  if ((rc = init_device(&st))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p->N == 1024) return launch_br<1024, false>(p, st, ggsw_ntt, exps, nullptr, nullptr, 0, acc, nullptr, L, B, s);
+  return launch_br<2048, false>(p, st, ggsw_ntt, exps, nullptr, nullptr, 0, acc, nullptr, L, B, s);
+}
+
+int hwb_sample_extract(const hwb_params *p, const uint32_t *rlwe, uint32_t *lwe, int64_t B, int32_t coeff,
+                       void *stream) {
+  int rc = check_glwe(p);
+  if (rc) return rc;
+  if (coeff < 0 || coeff >= (int32_t)p->N) return fail(HWB_EINVAL, "coefficient index out of range");
+  if (B < 0) return fail(HWB_EINVAL, "negative batch");
+  if (B == 0) return HWB_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t total = B * (p->N + 1);
+  const unsigned blocks = (unsigned)((total + 255) / 256);
+  if (p->N == 1024)
+    extract_kernel<1024><<<blocks, 256, 0, s>>>(rlwe, lwe, B, coeff);
+  else
+    extract_kernel<2048><<<blocks, 256, 0, s>>>(rlwe, lwe, B, coeff);
+  return post_launch("extract_kernel");
+}
+
+int hwb_keyswitch(const hwb_params *p, const uint32_t *ksk, const uint32_t *in, uint32_t *out, int64_t B,
+                  void *stream) {
+  if (!p) return fail(HWB_EINVAL, "null params");
+  int rc = check_ks(p);
+  if (rc) return rc;
+  if (p->N < 1) return fail(HWB_EINVAL, "N must be positive");
+  if (B < 0) return fail(HWB_EINVAL, "negative batch");
+  if (B == 0) return HWB_OK;
+  return keyswitch_launch(p, ksk, in, out, B, (cudaStream_t)stream);
+}
+
+size_t hwb_pbs_workspace_bytes(const hwb_params *p, int64_t B) {
+  if (!p || B <= 0) return 0;
+  return sizeof(uint32_t) * (size_t)B * (p->N + 1);
+}
+
+int hwb_pbs(const hwb_params *p, const uint32_t *bsk_ntt, const uint32_t *ksk, const uint32_t *tv,
+            int tv_per_item, const uint32_t *lwe_in, uint32_t *lwe_out, int64_t B, void *workspace,
+            void *stream) {
+  int rc = check_glwe(p);
+  if (rc) return rc;
+  if (ksk && (rc = check_ks(p))) return rc;
+  if (p->n < 1) return fail(HWB_EINVAL, "LWE dimension n must be positive");
+  if (B < 0) return fail(HWB_EINVAL, "negative batch");
+  if (B == 0) return HWB_OK;
+  if (B > 0x7FFFFFFF) return fail(HWB_EINVAL, "batch too large");
+  if (ksk && !workspace) return fail(HWB_EINVAL, "hwb_pbs with key switch needs a workspace");
+  DevState *st;
+  if ((rc = init_device(&st))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  uint32_t *ext = ksk ? (uint32_t *)workspace : lwe_out;
+  if (p->N == 1024)
+    rc = launch_br<1024, true>(p, st, bsk_ntt, nullptr, lwe_in, tv, tv_per_item, nullptr, ext, (int)p->n, B, s);
+  else
+    rc = launch_br<2048, true>(p, st, bsk_ntt, nullptr, lwe_in, tv, tv_per_item, nullptr, ext, (int)p->n, B, s);
+  if (rc || !ksk) return rc;
+  return keyswitch_launch(p, ksk, ext, lwe_out, B, s);
+}
+
+}  // extern "C"

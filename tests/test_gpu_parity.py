@@ -1,0 +1,219 @@
+"""GPU parity: libhwb200 kernels (through the C ABI) vs the reference-generated
+fixtures and the CPU oracle.  Bit-exact everywhere (integer arithmetic mod 2^32)."""
+
+import dataclasses
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import assert_u32_equal, golden
+from oracle import tfhe32 as o
+from paper_2403_20190_b200 import _lib, tfhe
+from paper_2403_20190_b200.params import HeParams, GadgetSpec, named_params
+
+pytestmark = pytest.mark.gpu
+
+
+def rand_u32(rng, shape):
+    return rng.integers(0, 1 << 32, shape, dtype=np.uint64).astype(np.uint32)
+
+
+def emb_params(N_log, lv, w, n=0):
+    return HeParams("t", N_log, 0.0, GadgetSpec(lv, w), GadgetSpec(8, 2), p=8, lwe_n=n)
+
+
+@pytest.fixture(params=[0, 1], ids=["regs255", "regs128"])
+def variant(request):
+    _lib.set_variant(request.param)
+    yield request.param
+    _lib.set_variant(0)
+
+
+# ---------------------------------------------------------------- external product
+
+@pytest.mark.parametrize("tag,N_log,lv,w", [("cfg2", 10, 3, 7), ("cfg1", 10, 2, 8), ("cfg4", 11, 2, 10)])
+def test_ext_product_golden(tag, N_log, lv, w, variant):
+    g = golden("ext_product.npz")
+    P = emb_params(N_log, lv, w)
+    G, cts = g[f"{tag}_G"], g[f"{tag}_cts"]
+    assert_u32_equal(tfhe.ext_product_batch(P, G, cts), g[f"{tag}_out"])
+    assert_u32_equal(tfhe.ext_product_batch(P, G[:1], cts), g[f"{tag}_out_bcast"])
+
+
+def test_ext_product_outside_envelope_raises():
+    g = golden("ext_product.npz")
+    P = emb_params(10, 2, 16)
+    with pytest.raises(tfhe.TfheError):
+        tfhe.ext_product_batch(P, g["ins_G"], g["ins_cts"])
+
+
+def test_ext_product_random_batch_and_index(coracle):
+    rng = np.random.default_rng(11)
+    P = emb_params(10, 3, 7)
+    G = rand_u32(rng, (7, 6, 2, 1024))
+    cts = rand_u32(rng, (64, 2, 1024))
+    idx = rng.integers(0, 7, 64)
+    ref = coracle.ext_product_batch(G[idx], cts, 3, 7)
+    ntt = tfhe.rgsw_to_ntt(P, G)
+    assert_u32_equal(tfhe.ext_product_batch(P, ntt, cts, idx=idx), ref)
+    # device-resident in, in-place out (aliasing allowed by the ABI)
+    d = tfhe.to_device(cts)
+    out = tfhe.ext_product_batch(P, ntt, d, idx=idx)
+    assert isinstance(out, torch.Tensor)
+    assert_u32_equal(tfhe.to_host(out), ref)
+
+
+def test_ext_product_extreme_inputs(coracle):
+    """Maximal-magnitude digits and GGSW words stress the CRT range bound."""
+    P = emb_params(10, 3, 7)
+    G = np.full((1, 6, 2, 1024), 0x80000000, np.uint32)      # -2^31 everywhere
+    cts = np.full((3, 2, 1024), 0, np.uint32)
+    cts[0] = 0xFFFFFFFF
+    cts[1] = 0x7FFFFFFF
+    cts[2, :, ::2] = 0x80000000
+    assert_u32_equal(tfhe.ext_product_batch(P, G, cts), coracle.ext_product_batch(G, cts, 3, 7))
+    P4 = emb_params(11, 2, 10)
+    G4 = np.full((1, 4, 2, 2048), 0x80000000, np.uint32)
+    c4 = np.full((2, 2, 2048), 0x7FFFFFFF, np.uint32)
+    assert_u32_equal(tfhe.ext_product_batch(P4, G4, c4), coracle.ext_product_batch(G4, c4, 2, 10))
+
+
+def test_cmux_cdemux(coracle):
+    rng = np.random.default_rng(12)
+    P = emb_params(10, 3, 7)
+    G = rand_u32(rng, (5, 6, 2, 1024))
+    c0 = rand_u32(rng, (5, 2, 1024))
+    c1 = rand_u32(rng, (5, 2, 1024))
+    ext = coracle.ext_product_batch(G, c1 - c0, 3, 7)
+    assert_u32_equal(tfhe.cmux_batch(P, G, c1, c0), c0 + ext)
+    rot = np.array([0, 1, -7, 2047, 3000])
+    c1r = np.stack([o.monomial_mul(c0[i], int(rot[i])) for i in range(5)])
+    ext = coracle.ext_product_batch(G, c1r - c0, 3, 7)
+    assert_u32_equal(tfhe.cmux_batch(P, G, None, c0, rot=rot), c0 + ext)
+    hi = coracle.ext_product_batch(G, c0, 3, 7)
+    lo_g, hi_g = tfhe.cdemux_batch(P, G, c0)
+    assert_u32_equal(hi_g, hi)
+    assert_u32_equal(lo_g, c0 - hi)
+
+
+# ---------------------------------------------------------------- blind rotation
+
+@pytest.mark.parametrize("tag,N_log,lv,w", [("cfg2", 10, 3, 7), ("cfg4", 11, 2, 10)])
+def test_blind_rotate_golden(tag, N_log, lv, w, variant):
+    g = golden("blind_rotate.npz")
+    P = emb_params(N_log, lv, w)
+    out = tfhe.blind_rotate_batch(P, g[f"{tag}_c"][None], g[f"{tag}_C"], g[f"{tag}_I"][None])[0]
+    assert_u32_equal(out, g[f"{tag}_out"])
+    ext = tfhe.sample_extract_batch(P, out[None])[0]
+    assert_u32_equal(ext[:-1], g[f"{tag}_ext_a"])
+    assert int(ext[-1]) == int(g[f"{tag}_ext_b"][0])
+
+
+def test_blind_rotate_reference_api():
+    g = golden("blind_rotate.npz")
+    P = emb_params(10, 3, 7)
+    c = tfhe.RlweCiphertext(P, g["cfg2_c"])
+    C = [tfhe.RgswCiphertext(P, x) for x in g["cfg2_C"]]
+    assert_u32_equal(tfhe.blind_rotate(c, C, list(g["cfg2_I"])).data, g["cfg2_out"])
+    with pytest.raises(tfhe.TfheError):
+        tfhe.blind_rotate(c, C, [1])
+
+
+def test_blind_rotate_batch_vs_oracle(coracle):
+    rng = np.random.default_rng(13)
+    P = emb_params(10, 3, 7)
+    L, B = 9, 33
+    C = rand_u32(rng, (L, 6, 2, 1024))
+    acc = rand_u32(rng, (B, 2, 1024))
+    exps = rng.integers(-4096, 4096, (B, L)).astype(np.int32)
+    exps[0] = 0                                       # all-skip item
+    exps[1, ::2] = 2048                               # exponent == 2N -> skip
+    ref = coracle.blind_rotate_batch(acc, C, exps, 3, 7)
+    assert_u32_equal(tfhe.blind_rotate_batch(P, acc, C, exps), ref)
+
+
+@pytest.mark.parametrize("coeff", [0, 1, 17, 1023])
+def test_sample_extract_all_positions(coeff):
+    rng = np.random.default_rng(14)
+    P = emb_params(10, 3, 7)
+    c = rand_u32(rng, (2, 1024))
+    a, b = o.extract_lwe(c, coeff)
+    out = tfhe.extract_lwe(tfhe.RlweCiphertext(P, c), coeff)
+    assert_u32_equal(out, np.concatenate([a, [b]]))
+
+
+# ---------------------------------------------------------------- key switch and PBS
+
+def test_keyswitch_vs_oracle(coracle):
+    P = dataclasses.replace(named_params("CFG2"), lwe_n=100)
+    K = tfhe.pbs_keygen(P, 21)
+    _, kd = K.device_keys()
+    rng = np.random.default_rng(15)
+    for B in (1, 63, 130):
+        lwe = rand_u32(rng, (B, P.n + 1))
+        gk = P.gadget_ks
+        assert_u32_equal(tfhe.lwe_keyswitch(P, lwe, kd), coracle.keyswitch(lwe, K.ksk, gk.levels, gk.base_log))
+
+
+@pytest.mark.parametrize("name", ["CFG1", "CFG2", "CFG4"])
+def test_pbs_golden(name, variant):
+    P = named_params(name)
+    g = golden(f"pbs_{name.lower()}.npz")
+    K = tfhe.pbs_keygen(P, int(g["key_seed"]))
+    bsk, ksk = K.device_keys()
+    ext = tfhe.pbs_batch(P, g["lwe_in"], g["tv"], bsk, None)
+    assert_u32_equal(ext, g["extracted"])
+    out = tfhe.pbs_batch(P, g["lwe_in"], g["tv"], bsk, ksk)
+    assert_u32_equal(out, g["lwe_out"])
+
+
+def test_pbs_batch_vs_c_oracle_and_decrypt(coracle):
+    P = named_params("CFG2")
+    K = tfhe.pbs_keygen(P, 31)
+    bsk, ksk = K.device_keys()
+    rng = tfhe.make_rng(32)
+    B = 48
+    ms = rng.integers(0, P.p, B)
+    lwe = tfhe.enc_lwe_batch(ms * P.delta, K.lwe_key, rng)
+    lwe[0, :-1] = 0                                        # every rotation skipped
+    tv = tfhe.test_polynomial(np.arange(4), P)
+    out = tfhe.pbs_batch(P, lwe, tv, bsk, ksk)
+    assert_u32_equal(out, coracle.pbs(lwe, tv, K.bsk, K.ksk, P))
+    # per-item test polynomials (sign LUT for odd items)
+    tvs = np.stack([tv if i % 2 == 0 else tfhe.test_polynomial(np.ones(4, int), P) for i in range(B)])
+    out2 = tfhe.pbs_batch(P, lwe, tvs, bsk, ksk)
+    assert_u32_equal(out2, coracle.pbs(lwe, tvs, K.bsk, K.ksk, P))
+
+
+def test_pbs_full_batch_decrypts():
+    """BASELINE cfg2 size (4096): size-independent property -- every output
+    decrypts to the negacyclic LUT of its input (identity on [0, 4))."""
+    P = named_params("CFG2")
+    K = tfhe.pbs_keygen(P, 41)
+    bsk, ksk = K.device_keys()
+    rng = tfhe.make_rng(42)
+    ms = rng.integers(0, P.p, 4096)
+    lwe = tfhe.enc_lwe_batch(ms * P.delta, K.lwe_key, rng)
+    out = tfhe.pbs_batch(P, tfhe.to_device(lwe), tfhe.test_polynomial(np.arange(4), P), bsk, ksk)
+    dec = tfhe.dec_lwe_batch(tfhe.to_host(out), K.lwe_key)
+    expect = np.where(ms < 4, ms, (-(ms - 4)) % 8)
+    assert np.array_equal(dec, expect)
+    # chaining: a second PBS of the outputs is the LUT applied twice
+    out2 = tfhe.pbs_batch(P, out, tfhe.test_polynomial(np.arange(4), P), bsk, ksk)
+    dec2 = tfhe.dec_lwe_batch(tfhe.to_host(out2), K.lwe_key)
+    assert np.array_equal(dec2, np.where(expect < 4, expect, (-(expect - 4)) % 8))
+
+
+def test_pbs_empty_and_errors():
+    P = named_params("CFG2")
+    K = tfhe.pbs_keygen(dataclasses.replace(P, lwe_n=4), 1)
+    P4 = dataclasses.replace(P, lwe_n=4)
+    bsk, ksk = K.device_keys()
+    tv = tfhe.test_polynomial(np.arange(4), P4)
+    out = tfhe.pbs_batch(P4, np.zeros((0, 5), np.uint32), tv, bsk, ksk)
+    assert out.shape == (0, 5)
+    with pytest.raises(tfhe.TfheError):
+        tfhe.pbs_batch(P4, np.zeros((2, 7), np.uint32), tv, bsk, ksk)
+    with pytest.raises(tfhe.TfheError):
+        tfhe.pbs_batch(P, np.zeros((2, 631), np.uint32), tfhe.test_polynomial(np.arange(4), P), bsk, ksk)
