@@ -6,12 +6,13 @@
 //   blind_rotate_kernel fused CMUX ladder (hw/tfhe.py:340-349), all L steps in one
 //                       launch with the accumulator resident in shared memory;
 //                       PBS mode adds mod switch, TV rotation and extraction
-//   extract_kernel      coefficient-0 sample extraction (hw/tfhe.py:352-361)
+//   extract_kernel      sample extraction (hw/tfhe.py:352-361)
 //   keyswitch_kernel    LWE key switch as a tiled integer contraction mod 2^32
 //
-// CTA shape for the ladder/CMUX kernels: 2 warps = one ciphertext; warp w works
-// modulo prime p_w on both GLWE components, then the warps exchange residues
-// through shared memory and warp w lifts component w by CRT.
+// CTA shape for the ladder/CMUX kernels: 2 groups of TPP threads = one
+// ciphertext; group g works modulo prime p_g on both GLWE components, then the
+// groups exchange residues through shared memory and group g lifts component g
+// by CRT.  TPP = 32 (N = 1024) or 64 (N = 2048): 32 coefficients per thread.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -27,14 +28,28 @@
 namespace hwb {
 
 static thread_local std::string g_err;
-// kernel variant: 0 = unconstrained registers (4 CTAs/SM), 1 = 128-register cap
-// (8 CTAs/SM).  Selected with hwb_set_variant() for A/B measurement.
+// kernel variant: selects the register/occupancy build of the ladder kernels
+// (0 = default, 1 = alternative); both bit-identical, for A/B measurement.
 static int g_variant = 0;
 
 static int fail(int code, const std::string &msg) {
   g_err = msg;
   return code;
 }
+
+// Per-ring-degree launch shape.  32 threads per (polynomial, prime) at N = 1024
+// and 64 at N = 2048 (32 coefficients per thread either way).  Measured on
+// B200 (profiles/r01_*): 64 threads at N = 1024 (16 coefficients, a middle
+// layout, 2 transposes per NTT) was 8-20% slower than 32 threads.
+// Kernel variants (hwb_set_variant): V0 = prime taken at run time (one code
+// copy shared by both groups), V1 = code specialised per prime (uniform
+// twiddles as constant-bank operands, twice the code).
+template <int N> struct Cfg {
+  static constexpr int TPP = (N == 1024) ? 32 : 64;
+  static constexpr int THREADS = 2 * TPP;
+  __host__ __device__ static constexpr bool spec(int v) { return v == 1; }
+  __host__ __device__ static constexpr int minb(int) { return 1; }
+};
 
 // ---------------------------------------------------------------------------
 // host-side table construction
@@ -62,14 +77,46 @@ static uint2 shoup_pair(uint32_t w, uint32_t p) {
 
 struct DevState {
   bool ready = false;
-  uint2 *lane_fwd[2][2] = {};
+  uint2 *lane_fwd[2][2] = {};   // [n_variant][prime] -> [slot][TPP]
   uint2 *lane_inv[2][2] = {};
 };
 
 static std::mutex g_mu;
 static DevState g_state[64];
 
-static int slots_for(int N) { return (N / 32) * 31 / 32; }
+// Per-thread twiddle table in the slot order fwd_ntt/inv_ntt consume
+// (hwb_device.cuh): twiddle index of stage s, block b is m + b, m = N/2^(s+1).
+template <int N>
+static std::vector<uint2> thread_table(const std::vector<uint32_t> &w, uint32_t p, bool fwd) {
+  using G = Geo<N, Cfg<N>::TPP>;
+  constexpr int TPP = Cfg<N>::TPP;
+  std::vector<uint2> tab((size_t)G::SLOTS * TPP);
+  int slot = 0;
+  auto m_stage = [&](int s) {   // middle layout: block = t_hi 2^(T-s-1) + u
+    const int nb = 1 << (G::T - s - 1);
+    for (int u = 0; u < nb; ++u)
+      for (int t = 0; t < TPP; ++t)
+        tab[(size_t)(slot + u) * TPP + t] = shoup_pair(w[(N >> (s + 1)) + (t >> G::LO) * nb + u], p);
+    slot += nb;
+  };
+  auto b_stage = [&](int s) {   // bit-reversed layout: block = t C/2^(s+1) + u
+    const int nb = G::C >> (s + 1);
+    for (int u = 0; u < nb; ++u)
+      for (int t = 0; t < TPP; ++t)
+        tab[(size_t)(slot + u) * TPP + t] = shoup_pair(w[(N >> (s + 1)) + t * nb + u], p);
+    slot += nb;
+  };
+  if (fwd) {
+    if (G::HAS_M)
+      for (int s = G::T - 1; s >= G::LOGC; --s) m_stage(s);
+    for (int s = G::B_TOP - 1; s >= 0; --s) b_stage(s);
+  } else {
+    for (int s = 0; s < G::B_TOP; ++s) b_stage(s);
+    if (G::HAS_M)
+      for (int s = G::LOGC; s < G::T; ++s) m_stage(s);
+  }
+  return tab;
+}
 
 static int init_device(DevState **out) {
   int dev = 0;
@@ -95,8 +142,6 @@ static int init_device(DevState **out) {
   for (int nv = 0; nv < 2; ++nv) {
     const int N = nv == 0 ? 1024 : 2048;
     const int logN = nv == 0 ? 10 : 11;
-    const int C = N / 32;
-    const int S = slots_for(N);
     for (int pr = 0; pr < 2; ++pr) {
       const uint32_t p = primes[pr];
       uint32_t psi = 0;
@@ -115,32 +160,18 @@ static int init_device(DevState **out) {
         iw[k] = powmod(psi_inv, bitrev(k, logN), p);
       }
       for (int k = 0; k < 64; ++k) {
-        h_tw[nv][0][pr][k] = k < C ? shoup_pair(fw[k], p) : make_uint2(0, 0);
-        h_tw[nv][1][pr][k] = k < C ? shoup_pair(iw[k], p) : make_uint2(0, 0);
+        h_tw[nv][0][pr][k] = shoup_pair(fw[k], p);
+        h_tw[nv][1][pr][k] = shoup_pair(iw[k], p);
       }
-      // per-lane tables: forward spans t = 16..1, inverse spans t = 1..16; slot
-      // (t, u) of lane l holds psi_rev[N/(2t) + l * C/(2t) + u]
-      std::vector<uint2> lf((size_t)S * 32), li((size_t)S * 32);
-      int slot = 0;
-      for (int t = 16; t >= 1; t >>= 1) {
-        int nb = C / (2 * t);
-        for (int u = 0; u < nb; ++u)
-          for (int l = 0; l < 32; ++l) lf[(size_t)(slot + u) * 32 + l] = shoup_pair(fw[N / (2 * t) + l * nb + u], p);
-        slot += nb;
-      }
-      slot = 0;
-      for (int t = 1; t <= 16; t <<= 1) {
-        int nb = C / (2 * t);
-        for (int u = 0; u < nb; ++u)
-          for (int l = 0; l < 32; ++l) li[(size_t)(slot + u) * 32 + l] = shoup_pair(iw[N / (2 * t) + l * nb + u], p);
-        slot += nb;
-      }
-      size_t bytes = sizeof(uint2) * S * 32;
+      std::vector<uint2> lf = nv == 0 ? thread_table<1024>(fw, p, true) : thread_table<2048>(fw, p, true);
+      std::vector<uint2> li = nv == 0 ? thread_table<1024>(iw, p, false) : thread_table<2048>(iw, p, false);
+      const size_t bytes = sizeof(uint2) * lf.size();
       cudaError_t e1 = cudaMalloc(&st.lane_fwd[nv][pr], bytes);
       cudaError_t e2 = cudaMalloc(&st.lane_inv[nv][pr], bytes);
       if (e1 != cudaSuccess || e2 != cudaSuccess) return fail(HWB_ECUDA, "cudaMalloc twiddle tables failed");
-      cudaMemcpy(st.lane_fwd[nv][pr], lf.data(), bytes, cudaMemcpyHostToDevice);
-      cudaMemcpy(st.lane_inv[nv][pr], li.data(), bytes, cudaMemcpyHostToDevice);
+      e1 = cudaMemcpy(st.lane_fwd[nv][pr], lf.data(), bytes, cudaMemcpyHostToDevice);
+      e2 = cudaMemcpy(st.lane_inv[nv][pr], li.data(), bytes, cudaMemcpyHostToDevice);
+      if (e1 != cudaSuccess || e2 != cudaSuccess) return fail(HWB_ECUDA, "twiddle upload failed");
       // Montgomery form with N^-1: x -> x * R * N^-1 via mont_mul(x, R^2 N^-1)
       uint64_t R = ((uint64_t)1 << 32) % p;
       uint64_t r2 = R * R % p;
@@ -168,7 +199,7 @@ template <int N>
 struct Smem {
   uint32_t acc[2 * N];   // working ciphertext (a, b)
   uint32_t v[2 * N];     // decomposition-ready input; then the residue exchange
-  uint32_t scr[2][N];    // per-warp transpose scratch
+  uint32_t scr[2][N];    // per-group transpose scratch
 };
 
 struct Tw {
@@ -176,18 +207,34 @@ struct Tw {
   const uint2 *inv[2];
 };
 
+// Thread coordinates inside a ciphertext CTA.
+template <int N>
+struct Who {
+  static constexpr int TPP = Cfg<N>::TPP;
+  int tid, grp, t;
+  LayBase lay;
+  __device__ __forceinline__ Who() : tid(threadIdx.x), grp(threadIdx.x / TPP), t(threadIdx.x % TPP) {
+    lay = make_lay<N, TPP>(t);
+  }
+};
+
 // One external product for the CTA's item.  Pre: sm.v holds decomp_prep() of
 // the input (both components) and a barrier has passed.  Post (after the
-// internal barriers): x holds, in layout A, the canonical residues mod p_w of
-// component w, and sm.v[w*N + i] holds those mod p_{1-w} of component w.
-template <int N>
-__device__ __forceinline__ void ext_product_core(Smem<N> &sm, const uint32_t *__restrict__ G,
-                                                 const Gadget &g, int w, int lane, const Tw &tw,
-                                                 uint32_t (&x)[N / 32]) {
-  constexpr int C = N / 32;
-  const uint32_t p = c_prime[w].p, two_p = c_prime[w].two_p, pinv = c_prime[w].pinv;
+// internal barriers): x holds, in layout A, the canonical residues mod p_grp of
+// component grp, and sm.v[grp*N + i] holds those mod p_{1-grp} of component grp.
+template <int N, int PRIME>
+__device__ __forceinline__ void ext_product_core_p(Smem<N> &sm, const uint32_t *__restrict__ G, const Gadget &g,
+                                                   const Who<N> &me, const Tw &tw, uint32_t (&x)[N / Cfg<N>::TPP]) {
+  constexpr int TPP = Cfg<N>::TPP;
+  constexpr int C = N / TPP;
+  const int w = PRIME >= 0 ? PRIME : me.grp;
+  const int t = me.t;
+  const uint32_t p = PRIME >= 0 ? (PRIME ? kP1 : kP0) : c_prime[w].p, two_p = 2 * p;
+  const uint32_t pinv = c_prime[w].pinv;
   const uint32_t off = p - g.half;
   const int L = (int)g.levels;
+  const uint2 *twf = w ? tw.fwd[1] : tw.fwd[0];
+  const uint2 *twi = w ? tw.inv[1] : tw.inv[0];
   uint32_t a0[C], a1[C];
 #pragma unroll
   for (int j = 0; j < C; ++j) a0[j] = a1[j] = 0;
@@ -196,18 +243,18 @@ __device__ __forceinline__ void ext_product_core(Smem<N> &sm, const uint32_t *__
   for (int r = 0; r < 2 * L; ++r) {
     // digit order (hw/tfhe.py:290-298): rows 0..l-1 = digits of b, l..2l-1 of a
     const int comp = r < L ? 1 : 0;
-    const int t = r < L ? r : r - L;
-    const uint32_t sh = g.base_log * (uint32_t)(L - 1 - t);
-    const uint32_t *vs = sm.v + comp * N;
+    const int tt = r < L ? r : r - L;
+    const uint32_t sh = g.base_log * (uint32_t)(L - 1 - tt);
+    const uint32_t *vs = sm.v + comp * N + t;
 #pragma unroll
-    for (int j = 0; j < C; ++j) x[j] = ((vs[lane + 32 * j] >> sh) & g.mask) + off;
-    fwd_ntt<N>(x, sm.scr[w], lane, w, (w ? tw.fwd[1] : tw.fwd[0]));
+    for (int j = 0; j < C; ++j) x[j] = ((vs[TPP * j] >> sh) & g.mask) + off;
+    fwd_ntt<N, TPP, PRIME>(x, sm.scr[w], me.lay, t, w, twf);
     const uint32_t *g0 = G + ((size_t)(r * 2 + 0) * 2 + w) * N;
     const uint32_t *g1 = G + ((size_t)(r * 2 + 1) * 2 + w) * N;
 #pragma unroll
     for (int jq = 0; jq < C / 4; ++jq) {
-      const uint4 G0 = __ldg(slice_vec<N>(g0, lane, jq));
-      const uint4 G1 = __ldg(slice_vec<N>(g1, lane, jq));
+      const uint4 G0 = __ldg(slice_vec<TPP>(g0, t, jq));
+      const uint4 G1 = __ldg(slice_vec<TPP>(g1, t, jq));
       a0[4 * jq + 0] += mont_mul(x[4 * jq + 0], G0.x, p, pinv);
       a0[4 * jq + 1] += mont_mul(x[4 * jq + 1], G0.y, p, pinv);
       a0[4 * jq + 2] += mont_mul(x[4 * jq + 2], G0.z, p, pinv);
@@ -227,21 +274,34 @@ __device__ __forceinline__ void ext_product_core(Smem<N> &sm, const uint32_t *__
     u = umin(u, u - two_p);     v = umin(v, v - two_p);
     a0[j] = u; a1[j] = v;
   }
-  __syncthreads();   // both warps are done reading sm.v: it becomes the exchange buffer
+  __syncthreads();   // both groups are done reading sm.v: it becomes the exchange buffer
 #pragma unroll 1
   for (int it = 0; it < 2; ++it) {
     const int c = it == 0 ? 1 - w : w;
 #pragma unroll
     for (int j = 0; j < C; ++j) x[j] = c ? a1[j] : a0[j];
-    inv_ntt<N>(x, sm.scr[w], lane, w, (w ? tw.inv[1] : tw.inv[0]));
+    inv_ntt<N, TPP, PRIME>(x, sm.scr[w], me.lay, t, w, twi);
 #pragma unroll
     for (int j = 0; j < C; ++j) x[j] = umin(x[j], x[j] - p);
     if (it == 0) {
 #pragma unroll
-      for (int j = 0; j < C; ++j) sm.v[c * N + lane + 32 * j] = x[j];
+      for (int j = 0; j < C; ++j) sm.v[c * N + t + TPP * j] = x[j];
     }
   }
   __syncthreads();   // exchange complete
+}
+
+// SPEC: each group runs its own instantiation (the prime, hence every uniform
+// twiddle and modulus, is a compile-time constant); otherwise one shared copy.
+template <int N, bool SPEC>
+__device__ __forceinline__ void ext_product_core(Smem<N> &sm, const uint32_t *__restrict__ G, const Gadget &g,
+                                                 const Who<N> &me, const Tw &tw, uint32_t (&x)[N / Cfg<N>::TPP]) {
+  if (!SPEC)
+    ext_product_core_p<N, -1>(sm, G, g, me, tw, x);
+  else if (me.grp == 0)
+    ext_product_core_p<N, 0>(sm, G, g, me, tw, x);
+  else
+    ext_product_core_p<N, 1>(sm, G, g, me, tw, x);
 }
 
 __device__ __forceinline__ uint32_t lift(int w, uint32_t own, uint32_t other) {
@@ -258,45 +318,47 @@ __device__ __forceinline__ uint32_t rot_read(const uint32_t *poly, int i, int e)
 
 enum { MODE_EXT = 0, MODE_CMUX = 1, MODE_CDEMUX = 2 };
 
-template <int N, int MODE, int MINB>
-__global__ void __launch_bounds__(64, MINB) cmux_kernel(const uint32_t *__restrict__ ggsw, size_t ggsw_words,
-                                                  const int32_t *__restrict__ gidx,
-                                                  const uint32_t *in, const uint32_t *c1,
-                                                  const int32_t *__restrict__ rot, uint32_t *out,
-                                                  uint32_t *out_hi, Gadget g, Tw tw) {
+template <int N, int MODE, int V>
+__global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::minb(V))
+    cmux_kernel(const uint32_t *__restrict__ ggsw, size_t ggsw_words, const int32_t *__restrict__ gidx,
+                const uint32_t *in, const uint32_t *c1, const int32_t *__restrict__ rot, uint32_t *out,
+                uint32_t *out_hi, Gadget g, Tw tw) {
+  constexpr int TPP = Cfg<N>::TPP, NT = Cfg<N>::THREADS;
   extern __shared__ uint4 smem_raw[];
   Smem<N> &sm = *reinterpret_cast<Smem<N> *>(smem_raw);
   const int64_t b = blockIdx.x;
-  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const Who<N> me;
+  const int tid = me.tid;
   const uint32_t *G = ggsw + (size_t)(gidx ? gidx[b] : 0) * ggsw_words;
   const uint32_t *src = in + b * 2 * N;
   if (MODE == MODE_EXT) {
-    for (int k = tid; k < 2 * N; k += 64) sm.v[k] = decomp_prep(src[k], g);
+    for (int k = tid; k < 2 * N; k += NT) sm.v[k] = decomp_prep(src[k], g);
   } else {
-    for (int k = tid; k < 2 * N; k += 64) sm.acc[k] = src[k];
+    for (int k = tid; k < 2 * N; k += NT) sm.acc[k] = src[k];
     __syncthreads();
     if (MODE == MODE_CMUX) {
       if (c1) {
         const uint32_t *s1 = c1 + b * 2 * N;
-        for (int k = tid; k < 2 * N; k += 64) sm.v[k] = decomp_prep(s1[k] - sm.acc[k], g);
+        for (int k = tid; k < 2 * N; k += NT) sm.v[k] = decomp_prep(s1[k] - sm.acc[k], g);
       } else {
         const int e = ((rot[b] % (2 * N)) + 2 * N) % (2 * N);
-        for (int k = tid; k < 2 * N; k += 64) {
+        for (int k = tid; k < 2 * N; k += NT) {
           const int c = k >= N, i = k & (N - 1);
           sm.v[k] = decomp_prep(rot_read<N>(sm.acc + c * N, i, e) - sm.acc[k], g);
         }
       }
     } else {
-      for (int k = tid; k < 2 * N; k += 64) sm.v[k] = decomp_prep(sm.acc[k], g);
+      for (int k = tid; k < 2 * N; k += NT) sm.v[k] = decomp_prep(sm.acc[k], g);
     }
   }
   __syncthreads();
-  uint32_t x[N / 32];
-  ext_product_core<N>(sm, G, g, w, lane, tw, x);
+  uint32_t x[N / TPP];
+  ext_product_core<N, Cfg<N>::spec(V)>(sm, G, g, me, tw, x);
+  const int w = me.grp;
   uint32_t *o = out + b * 2 * N + w * N;
 #pragma unroll
-  for (int j = 0; j < N / 32; ++j) {
-    const int i = lane + 32 * j;
+  for (int j = 0; j < N / TPP; ++j) {
+    const int i = me.t + TPP * j;
     const uint32_t val = lift(w, x[j], sm.v[w * N + i]);
     if (MODE == MODE_EXT) {
       o[i] = val;
@@ -317,30 +379,32 @@ __device__ __forceinline__ int mod_switch(uint32_t x, int log2m) {
 // the reference's I values (rotation X^-I).  PBS = true: lwe_in [B][L+1];
 // acc = TV * X^-b~, rotation X^{a~_i} (I_i = -a~_i), output the coefficient-0
 // extraction [B][N+1].
-template <int N, bool PBS, int MINB>
-__global__ void __launch_bounds__(64, MINB) blind_rotate_kernel(
-    const uint32_t *__restrict__ bsk, size_t ggsw_words, const int32_t *__restrict__ exps,
-    const uint32_t *__restrict__ lwe_in, const uint32_t *__restrict__ tv, int tv_per_item,
-    uint32_t *acc_io, uint32_t *lwe_out, int L, Gadget g, Tw tw) {
+template <int N, bool PBS, int V>
+__global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::minb(V))
+    blind_rotate_kernel(const uint32_t *__restrict__ bsk, size_t ggsw_words, const int32_t *__restrict__ exps,
+                        const uint32_t *__restrict__ lwe_in, const uint32_t *__restrict__ tv, int tv_per_item,
+                        uint32_t *acc_io, uint32_t *lwe_out, int L, Gadget g, Tw tw) {
+  constexpr int TPP = Cfg<N>::TPP, NT = Cfg<N>::THREADS;
   extern __shared__ uint4 smem_raw[];
   Smem<N> &sm = *reinterpret_cast<Smem<N> *>(smem_raw);
   constexpr int LOG2M = (N == 1024) ? 11 : 12;
   const int64_t b = blockIdx.x;
-  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const Who<N> me;
+  const int tid = me.tid, w = me.grp;
   const uint32_t *row = PBS ? lwe_in + b * (int64_t)(L + 1) : nullptr;
   if (PBS) {
     const int bt = mod_switch(row[L], LOG2M);
-    const uint32_t *t = tv + (tv_per_item ? b * 2 * N : 0);
+    const uint32_t *tp = tv + (tv_per_item ? b * 2 * N : 0);
     const int e = (2 * N - bt) & (2 * N - 1);   // X^-b~
-    for (int k = tid; k < 2 * N; k += 64) {
+    for (int k = tid; k < 2 * N; k += NT) {
       const int c = k >= N, i = k & (N - 1);
-      sm.acc[k] = rot_read<N>(t + c * N, i, e);
+      sm.acc[k] = rot_read<N>(tp + c * N, i, e);
     }
   } else {
-    for (int k = tid; k < 2 * N; k += 64) sm.acc[k] = acc_io[b * 2 * N + k];
+    for (int k = tid; k < 2 * N; k += NT) sm.acc[k] = acc_io[b * 2 * N + k];
   }
   __syncthreads();
-  uint32_t x[N / 32];
+  uint32_t x[N / TPP];
 #pragma unroll 1
   for (int s = 0; s < L; ++s) {
     int e;
@@ -351,45 +415,47 @@ __global__ void __launch_bounds__(64, MINB) blind_rotate_kernel(
       if (e < 0) e += 2 * N;
     }
     if (e == 0) continue;   // zero difference -> zero product: exact skip
-    for (int k = tid; k < 2 * N; k += 64) {
+    for (int k = tid; k < 2 * N; k += NT) {
       const int c = k >= N, i = k & (N - 1);
       sm.v[k] = decomp_prep(rot_read<N>(sm.acc + c * N, i, e) - sm.acc[k], g);
     }
     __syncthreads();
-    ext_product_core<N>(sm, bsk + (size_t)s * ggsw_words, g, w, lane, tw, x);
+    ext_product_core<N, Cfg<N>::spec(V)>(sm, bsk + (size_t)s * ggsw_words, g, me, tw, x);
 #pragma unroll
-    for (int j = 0; j < N / 32; ++j) {
-      const int i = lane + 32 * j;
+    for (int j = 0; j < N / TPP; ++j) {
+      const int i = me.t + TPP * j;
       sm.acc[w * N + i] += lift(w, x[j], sm.v[w * N + i]);
     }
     __syncthreads();
   }
   if (PBS) {
     uint32_t *o = lwe_out + b * (int64_t)(N + 1);
-    for (int k = tid; k < N; k += 64) o[k] = k == 0 ? sm.acc[0] : 0u - sm.acc[N - k];
+    for (int k = tid; k < N; k += NT) o[k] = k == 0 ? sm.acc[0] : 0u - sm.acc[N - k];
     if (tid == 0) o[N] = sm.acc[N];
   } else {
-    for (int k = tid; k < 2 * N; k += 64) acc_io[b * 2 * N + k] = sm.acc[k];
+    for (int k = tid; k < 2 * N; k += NT) acc_io[b * 2 * N + k] = sm.acc[k];
   }
 }
 
 template <int N>
-__global__ void __launch_bounds__(64) ggsw_to_ntt_kernel(const uint32_t *__restrict__ in, uint32_t *out,
-                                                         Tw tw) {
-  __shared__ uint32_t scr[2][N];
-  constexpr int C = N / 32;
+__global__ void __launch_bounds__(Cfg<N>::THREADS) ggsw_to_ntt_kernel(const uint32_t *__restrict__ in,
+                                                                      uint32_t *out, Tw tw) {
+  constexpr int TPP = Cfg<N>::TPP;
+  constexpr int C = N / TPP;
   constexpr int NV = NVar<N>::v;
+  __shared__ uint32_t scr[2][N];
   const int64_t poly = blockIdx.x;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Who<N> me;
+  const int w = me.grp, t = me.t;
   const uint32_t p = c_prime[w].p, pinv = c_prime[w].pinv;
   uint32_t x[C];
 #pragma unroll
   for (int j = 0; j < C; ++j) {
-    int32_t s = (int32_t)in[poly * N + lane + 32 * j];   // centred coefficient
+    int32_t s = (int32_t)in[poly * N + t + TPP * j];   // centred coefficient
     int32_t r = s % (int32_t)p;
     x[j] = (uint32_t)(r < 0 ? r + (int32_t)p : r);
   }
-  fwd_ntt<N>(x, scr[w], lane, w, (w ? tw.fwd[1] : tw.fwd[0]));
+  fwd_ntt<N, TPP, -1>(x, scr[w], me.lay, t, w, w ? tw.fwd[1] : tw.fwd[0]);
   const uint32_t k = c_r2ninv[NV][w];
   uint4 *o = reinterpret_cast<uint4 *>(out + (poly * 2 + w) * N);
 #pragma unroll
@@ -400,7 +466,7 @@ __global__ void __launch_bounds__(64) ggsw_to_ntt_kernel(const uint32_t *__restr
       uint32_t v = mont_mul(x[4 * jq + q], k, p, pinv);   // (0, 2p)
       y[q] = umin(v, v - p);
     }
-    o[jq * 32 + lane] = make_uint4(y[0], y[1], y[2], y[3]);
+    o[jq * TPP + t] = make_uint4(y[0], y[1], y[2], y[3]);
   }
 }
 
@@ -415,7 +481,6 @@ __global__ void extract_kernel(const uint32_t *__restrict__ rlwe, uint32_t *lwe,
   const uint32_t *a = rlwe + b * 2 * N;
   lwe[idx] = k == N ? a[N + coeff] : (k <= coeff ? a[coeff - k] : 0u - a[N + coeff - k]);
 }
-
 // LWE key switch: out[b][c] = (c < n ? 0 : in[b][N]) - sum_{j,t} d[b][j][t] * ksk[j][t][c]
 // CTA tile: 64 items x 64 output columns, K chunked by KS_TJ input coefficients.
 constexpr int KS_TB = 64, KS_TC = 64, KS_TJ = 4, KS_MAXL = 16;
@@ -497,7 +562,6 @@ __global__ void __launch_bounds__(256) probe_modmul_kernel(uint32_t *sink, int i
   for (int k = 0; k < 8; ++k) s ^= a[k] ^ b[k];
   if (s == 0x12345678u) sink[0] = s;
 }
-
 // ---------------------------------------------------------------------------
 // host helpers
 
@@ -560,6 +624,7 @@ static int set_smem(K kernel, size_t bytes) {
   return HWB_OK;
 }
 
+
 template <int N, int MODE>
 static int launch_cmux(const hwb_params *p, DevState *st, const uint32_t *ggsw, const int32_t *gidx,
                        const uint32_t *in, const uint32_t *c1, const int32_t *rot, uint32_t *out,
@@ -569,11 +634,13 @@ static int launch_cmux(const hwb_params *p, DevState *st, const uint32_t *ggsw, 
   const Gadget g = make_gadget(p->l, p->base_log);
   int rc;
   if (g_variant == 1) {
-    if ((rc = set_smem(cmux_kernel<N, MODE, 8>, smem))) return rc;
-    cmux_kernel<N, MODE, 8><<<(unsigned)B, 64, smem, s>>>(ggsw, words, gidx, in, c1, rot, out, out_hi, g, make_tw(st, N));
-  } else {
     if ((rc = set_smem(cmux_kernel<N, MODE, 1>, smem))) return rc;
-    cmux_kernel<N, MODE, 1><<<(unsigned)B, 64, smem, s>>>(ggsw, words, gidx, in, c1, rot, out, out_hi, g, make_tw(st, N));
+    cmux_kernel<N, MODE, 1><<<(unsigned)B, Cfg<N>::THREADS, smem, s>>>(ggsw, words, gidx, in, c1, rot, out,
+                                                                              out_hi, g, make_tw(st, N));
+  } else {
+    if ((rc = set_smem(cmux_kernel<N, MODE, 0>, smem))) return rc;
+    cmux_kernel<N, MODE, 0><<<(unsigned)B, Cfg<N>::THREADS, smem, s>>>(ggsw, words, gidx, in, c1, rot, out,
+                                                                              out_hi, g, make_tw(st, N));
   }
   return post_launch("cmux_kernel");
 }
@@ -587,13 +654,13 @@ static int launch_br(const hwb_params *p, DevState *st, const uint32_t *bsk, con
   const size_t words = hwb_ggsw_ntt_words(p);
   int rc;
   if (g_variant == 1) {
-    if ((rc = set_smem(blind_rotate_kernel<N, PBS, 8>, smem))) return rc;
-    blind_rotate_kernel<N, PBS, 8><<<(unsigned)B, 64, smem, s>>>(bsk, words, exps, lwe_in, tv, tv_per_item, acc,
-                                                                 lwe_out, L, g, make_tw(st, N));
-  } else {
     if ((rc = set_smem(blind_rotate_kernel<N, PBS, 1>, smem))) return rc;
-    blind_rotate_kernel<N, PBS, 1><<<(unsigned)B, 64, smem, s>>>(bsk, words, exps, lwe_in, tv, tv_per_item, acc,
-                                                                 lwe_out, L, g, make_tw(st, N));
+    blind_rotate_kernel<N, PBS, 1><<<(unsigned)B, Cfg<N>::THREADS, smem, s>>>(
+        bsk, words, exps, lwe_in, tv, tv_per_item, acc, lwe_out, L, g, make_tw(st, N));
+  } else {
+    if ((rc = set_smem(blind_rotate_kernel<N, PBS, 0>, smem))) return rc;
+    blind_rotate_kernel<N, PBS, 0><<<(unsigned)B, Cfg<N>::THREADS, smem, s>>>(
+        bsk, words, exps, lwe_in, tv, tv_per_item, acc, lwe_out, L, g, make_tw(st, N));
   }
   return post_launch("blind_rotate_kernel");
 }
@@ -607,7 +674,6 @@ static int keyswitch_launch(const hwb_params *p, const uint32_t *ksk, const uint
 }
 
 }  // namespace hwb
-
 using namespace hwb;
 
 extern "C" {
@@ -645,9 +711,9 @@ int hwb_ggsw_to_ntt(const hwb_params *p, const uint32_t *ggsw, uint32_t *ggsw_nt
   const int64_t polys = count * 2 * p->l * 2;
   cudaStream_t s = (cudaStream_t)stream;
   if (p->N == 1024)
-    ggsw_to_ntt_kernel<1024><<<(unsigned)polys, 64, 0, s>>>(ggsw, ggsw_ntt, make_tw(st, 1024));
+    ggsw_to_ntt_kernel<1024><<<(unsigned)polys, Cfg<1024>::THREADS, 0, s>>>(ggsw, ggsw_ntt, make_tw(st, 1024));
   else
-    ggsw_to_ntt_kernel<2048><<<(unsigned)polys, 64, 0, s>>>(ggsw, ggsw_ntt, make_tw(st, 2048));
+    ggsw_to_ntt_kernel<2048><<<(unsigned)polys, Cfg<2048>::THREADS, 0, s>>>(ggsw, ggsw_ntt, make_tw(st, 2048));
   return post_launch("ggsw_to_ntt_kernel");
 }
 

@@ -1,0 +1,48 @@
+#!/usr/bin/env python
+"""Summarise an ncu --set full report: duration, issue, pipes, stalls, memory.
+Usage: python profiles/ncu_summary.py report.ncu-rep [...]"""
+import csv
+import subprocess
+import sys
+
+KEYS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("sm__inst_executed.sum", "warp instructions"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
+    ("launch__registers_per_thread", "registers/thread"),
+    ("launch__occupancy_limit_registers", "CTA limit (regs)"),
+    ("launch__occupancy_limit_shared_mem", "CTA limit (smem)"),
+    ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "pipe alu %"),
+    ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "pipe fma %"),
+    ("sm__inst_executed_pipe_fmaheavy.avg.pct_of_peak_sustained_active", "pipe fmaheavy %"),
+    ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "pipe lsu %"),
+    ("sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active", "pipe uniform %"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem wavefronts"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
+    ("dram__bytes_read.sum", "dram read"),
+    ("dram__bytes_write.sum", "dram write"),
+    ("lts__t_bytes.sum", "L2 bytes"),
+    ("l1tex__t_sector_hit_rate.pct", "L1 hit %"),
+]
+
+
+def raw(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    return {h: (v, u) for h, u, v in zip(hdr, units, vals)}
+
+
+for path in sys.argv[1:]:
+    d = raw(path)
+    print(f"== {path}  kernel: {d.get('Kernel Name', ('?',))[0][:80]}")
+    for k, name in KEYS:
+        if k in d:
+            print(f"  {name:28s} {d[k][0]:>20s} {d[k][1]}")
+    stalls = [(float(v[0]), k) for k, v in d.items()
+              if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio")
+              and v[0] not in ("", "n/a")]
+    print("  stalls per issued instruction:")
+    for v, k in sorted(stalls, reverse=True)[:9]:
+        print(f"    {v:7.3f} {k[len('smsp__average_warps_issue_stalled_'):-len('_per_issue_active.ratio')]}")
