@@ -83,6 +83,25 @@ __device__ __forceinline__ void ct_bfly(uint32_t &X, uint32_t &Y, uint32_t w, ui
   Y = x - t + two_p;
 }
 
+// Lazier CT butterfly for the forward transform.  Outputs are < x_bound + 2p
+// (Shoup's t < 2p for any 32-bit input), so from inputs < 2p the bound grows
+// by 2p per stage and reaches 12p after 5 stages; RED stages (execution index
+// 5 and 10) first bring x from < 12p down to < 2p.  All values stay < 12p <
+// 2^32 (p < 2^32/12), replacing 10-11 reductions per transform with 1-2.
+template <bool RED>
+__device__ __forceinline__ void ct_bfly_lazy(uint32_t &X, uint32_t &Y, uint32_t w, uint32_t wq,
+                                             uint32_t p, uint32_t two_p) {
+  uint32_t x = X;
+  if (RED) {
+    x = umin(x, x - 4 * two_p);
+    x = umin(x, x - 2 * two_p);
+    x = umin(x, x - two_p);
+  }
+  uint32_t t = shoup_mul(Y, w, wq, p);
+  X = x + t;
+  Y = x - t + two_p;
+}
+
 // Harvey lazy Gentleman-Sande butterfly: X, Y in [0, 2p) -> [0, 2p).
 __device__ __forceinline__ void gs_bfly(uint32_t &X, uint32_t &Y, uint32_t w, uint32_t wq,
                                         uint32_t p, uint32_t two_p) {
@@ -188,7 +207,7 @@ __device__ __forceinline__ uint2 ld_tw(const uint2 *ptr) {
 // PRIME >= 0 specialises the code for one prime (uniform twiddles become
 // direct constant-bank operands); PRIME < 0 takes the prime at run time, so
 // both groups of a CTA share one copy of the code (smaller I-cache footprint).
-template <int N, int TPP, int PRIME, bool FWD, int JB, bool UNIFORM, int MBASE, int SLOT>
+template <int N, int TPP, int PRIME, bool FWD, int JB, bool UNIFORM, int MBASE, int SLOT, bool RED = true>
 __device__ __forceinline__ void ntt_stage(uint32_t (&x)[N / TPP], int t, int prime, const uint2 *__restrict__ tw) {
   constexpr int C = N / TPP;
   constexpr int NBT = C >> (JB + 1);
@@ -204,7 +223,7 @@ __device__ __forceinline__ void ntt_stage(uint32_t (&x)[N / TPP], int t, int pri
     for (int lo = 0; lo < HALF; ++lo) {
       const int j = (u << (JB + 1)) | lo;
       if (FWD)
-        ct_bfly(x[j], x[j + HALF], w.x, w.y, p, two_p);
+        ct_bfly_lazy<RED>(x[j], x[j + HALF], w.x, w.y, p, two_p);
       else
         gs_bfly(x[j], x[j + HALF], w.x, w.y, p, two_p);
     }
@@ -212,7 +231,8 @@ __device__ __forceinline__ void ntt_stage(uint32_t (&x)[N / TPP], int t, int pri
 }
 
 // Forward negacyclic NTT (merged psi twist, CT, natural -> bit-reversed).
-// In: layout A, values in [0, 4p).  Out: layout B, values in [0, 4p).
+// In: layout A, values < 2p.  Out: layout B, values < 12p (lazy reduction:
+// x is reduced only on execution stages 5 and 10 -- see ct_bfly_lazy).
 // Per-thread twiddle slots: M stages s = T-1..LOGC, then B stages s = B_TOP-1..0.
 template <int N, int TPP, int PRIME>
 __device__ __forceinline__ void fwd_ntt(uint32_t (&x)[N / TPP], uint32_t *scr, const LayBase &L, int t, int prime,
@@ -221,14 +241,16 @@ __device__ __forceinline__ void fwd_ntt(uint32_t (&x)[N / TPP], uint32_t *scr, c
   const int group = PRIME >= 0 ? PRIME : prime;
   static_for<0, G::LOGN - G::T>([&](auto K) {          // A stages s = LOGN-1 .. T
     constexpr int s = G::LOGN - 1 - decltype(K)::value;
-    ntt_stage<N, TPP, PRIME, true, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x, t, prime, tw);
+    constexpr bool red = (G::LOGN - 1 - s) % 5 == 0 && s != G::LOGN - 1;
+    ntt_stage<N, TPP, PRIME, true, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0, red>(x, t, prime, tw);
   });
   if constexpr (G::HAS_M) {
     relayout<N, TPP, LAY_A, LAY_M>(x, scr, L, group);
     static_for<0, G::T - G::LOGC>([&](auto K) {        // M stages s = T-1 .. LOGC
       constexpr int s = G::T - 1 - decltype(K)::value;
       constexpr int slot = (1 << decltype(K)::value) - 1;
-      ntt_stage<N, TPP, PRIME, true, s - G::LO, false, 0, slot>(x, t, prime, tw);
+      constexpr bool red = (G::LOGN - 1 - s) % 5 == 0 && s != G::LOGN - 1;
+      ntt_stage<N, TPP, PRIME, true, s - G::LO, false, 0, slot, red>(x, t, prime, tw);
     });
     relayout<N, TPP, LAY_M, LAY_B>(x, scr, L, group);
   } else {
@@ -237,7 +259,8 @@ __device__ __forceinline__ void fwd_ntt(uint32_t (&x)[N / TPP], uint32_t *scr, c
   static_for<0, G::B_TOP>([&](auto K) {                  // B stages s = B_TOP-1 .. 0
     constexpr int s = G::B_TOP - 1 - decltype(K)::value;
     constexpr int slot = G::M_SLOTS + (G::C >> G::B_TOP) * ((1 << decltype(K)::value) - 1);
-    ntt_stage<N, TPP, PRIME, true, s, false, 0, slot>(x, t, prime, tw);
+    constexpr bool red = (G::LOGN - 1 - s) % 5 == 0 && s != G::LOGN - 1;
+    ntt_stage<N, TPP, PRIME, true, s, false, 0, slot, red>(x, t, prime, tw);
   });
 }
 

@@ -42,13 +42,17 @@ static int fail(int code, const std::string &msg) {
 // B200 (profiles/r01_*): 64 threads at N = 1024 (16 coefficients, a middle
 // layout, 2 transposes per NTT) was 8-20% slower than 32 threads.
 // Kernel variants (hwb_set_variant): V0 = prime taken at run time (one code
-// copy shared by both groups), V1 = code specialised per prime (uniform
-// twiddles as constant-bank operands, twice the code).
+// copy shared by both groups), V1 = V0 with a register cap for HWB_V1_MINB
+// resident CTAs/SM.  (A per-prime specialised build -- uniform twiddles as
+// constant-bank operands, twice the code -- measured 2x slower: I-cache.)
+#ifndef HWB_V1_MINB
+#define HWB_V1_MINB 6
+#endif
 template <int N> struct Cfg {
   static constexpr int TPP = (N == 1024) ? 32 : 64;
   static constexpr int THREADS = 2 * TPP;
-  __host__ __device__ static constexpr bool spec(int v) { return v == 1; }
-  __host__ __device__ static constexpr int minb(int) { return 1; }
+  __host__ __device__ static constexpr bool spec(int v) { return v == 2; }
+  __host__ __device__ static constexpr int minb(int v) { return v == 1 ? HWB_V1_MINB : 1; }
 };
 
 // ---------------------------------------------------------------------------
