@@ -97,6 +97,46 @@ int hwb_cmux(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_t *ggsw_
 int hwb_cdemux(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_t *ggsw_idx,
                const uint32_t *d, uint32_t *lo, uint32_t *hi, int64_t B, void *stream);
 
+/* One level of the inverse-vertical-packing CDEMUX tree (hw/lut.py:294-313):
+ * for item b < B and poly i < m, with C = G[idx[b]] (the item's tree bit):
+ *   hi = C (*) cur[b][i];  next[b][i] = cur[b][i] - hi;  next[b][m+i] = hi.
+ * cur: [B][m][2][N], next: [B][2m][2][N]. */
+int hwb_ivp_level(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_t *ggsw_idx,
+                  const uint32_t *cur, uint32_t *next, int32_t m, int64_t B, void *stream);
+
+/* One level of the vertical-packing CMUX tree (hw/lut.py:233-247, 130-136):
+ *   next[b][i] = cmux(G[idx[b]], cur[b][m+i], cur[b][i]) for i < m.
+ * cur: [B][2m][2][N], next: [B][m][2][N]. */
+int hwb_vp_level(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_t *ggsw_idx,
+                 const uint32_t *cur, uint32_t *next, int32_t m, int64_t B, void *stream);
+
+/* Per-item negacyclic monomial product out[b] = in[b] * X^(exps[b]) (exponents
+ * mod 2N; hw/lut.py:317-325 monomial_gather, hw/ring.py:106-113).  in, out:
+ * [B][2][N], must not alias. */
+int hwb_monomial_gather(const hwb_params *p, const uint32_t *in, uint32_t *out, const int32_t *exps,
+                        int64_t B, void *stream);
+
+/* Forward transform of npolys coefficient-domain polynomials [npolys][N] into
+ * the NTT layout of one GGSW row ([npolys][2 primes][N]); used for the secret
+ * key of hwb_key_mul. */
+int hwb_poly_to_ntt(const hwb_params *p, const uint32_t *in, uint32_t *out, int64_t npolys, void *stream);
+
+/* Client-side key product (hw/tfhe.py:69-78 SecretKey._key_mul, the core of
+ * enc_rgsw_batch hw/tfhe.py:246-263): out[i] = in[i] (*) s + add[i] mod 2^32,
+ * s given as hwb_poly_to_ntt(s); add may be NULL.  Exact for binary keys. */
+int hwb_key_mul(const hwb_params *p, const uint32_t *key_ntt, const uint32_t *in, const uint32_t *add,
+                uint32_t *out, int64_t npolys, void *stream);
+
+/* Add the RGSW gadget term m * q/beta^(t+1) (hw/tfhe.py:259-262) to B RGSW
+ * ciphertexts [B][2l][2][N] for selector bits[B] in {0, 1}. */
+int hwb_rgsw_add_gadget(const hwb_params *p, uint32_t *rgsw, const int32_t *bits, int64_t B, void *stream);
+
+/* dst[k] += (negate ? -1 : 1) * src[k mod src_words] mod 2^32 for k < words: exact
+ * ciphertext addition for model accumulation and federated merge
+ * (hw/hewnn.py:213, 264-271). */
+int hwb_accumulate(uint32_t *dst, const uint32_t *src, int64_t words, int64_t src_words, int negate,
+                   void *stream);
+
 /* Fused blind rotation (hw/tfhe.py:340-349 blind_rotate), one launch for all L
  * steps: acc[b] <- cmux(G_i, acc[b] * X^(-I[b][i]), acc[b]) for i < L.
  * ggsw_ntt: L NTT-domain GGSWs shared by the batch (the BSK);

@@ -20,6 +20,8 @@ EXPORTS = (
     "hwb_version", "hwb_last_error", "hwb_set_variant", "hwb_probe_modmul", "hwb_ggsw_ntt_words",
     "hwb_ggsw_to_ntt", "hwb_ext_product", "hwb_cmux", "hwb_cdemux", "hwb_blind_rotate",
     "hwb_sample_extract", "hwb_keyswitch", "hwb_pbs_workspace_bytes", "hwb_pbs",
+    "hwb_ivp_level", "hwb_vp_level", "hwb_monomial_gather", "hwb_accumulate",
+    "hwb_poly_to_ntt", "hwb_key_mul", "hwb_rgsw_add_gadget",
 )
 
 
@@ -72,6 +74,13 @@ def load() -> ctypes.CDLL:
         L.hwb_pbs_workspace_bytes.argtypes = [_pp, _i64]
         L.hwb_pbs_workspace_bytes.restype = ctypes.c_size_t
         L.hwb_pbs.argtypes = [_pp, _vp, _vp, _vp, ctypes.c_int, _vp, _vp, _i64, _vp, _vp]
+        L.hwb_ivp_level.argtypes = [_pp, _vp, _vp, _vp, _vp, ctypes.c_int32, _i64, _vp]
+        L.hwb_vp_level.argtypes = [_pp, _vp, _vp, _vp, _vp, ctypes.c_int32, _i64, _vp]
+        L.hwb_monomial_gather.argtypes = [_pp, _vp, _vp, _vp, _i64, _vp]
+        L.hwb_accumulate.argtypes = [_vp, _vp, _i64, _i64, ctypes.c_int, _vp]
+        L.hwb_poly_to_ntt.argtypes = [_pp, _vp, _vp, _i64, _vp]
+        L.hwb_key_mul.argtypes = [_pp, _vp, _vp, _vp, _vp, _i64, _vp]
+        L.hwb_rgsw_add_gadget.argtypes = [_pp, _vp, _vp, _i64, _vp]
         for name in EXPORTS:
             if name not in ("hwb_version", "hwb_last_error", "hwb_ggsw_ntt_words",
                             "hwb_pbs_workspace_bytes", "hwb_probe_modmul"):

@@ -320,29 +320,39 @@ __device__ __forceinline__ uint32_t rot_read(const uint32_t *poly, int i, int e)
   return src >= N ? 0u - val : val;
 }
 
-enum { MODE_EXT = 0, MODE_CMUX = 1, MODE_CDEMUX = 2 };
+// MODE_IVP_LEVEL / MODE_VP_LEVEL process one level of the inverse / forward
+// vertical-packing tree (hw/lut.py:294-313 / 233-247) for B items of m (resp.
+// 2m) polynomials each; block = item*m + sub, the GGSW is per item.
+enum { MODE_EXT = 0, MODE_CMUX = 1, MODE_CDEMUX = 2, MODE_IVP_LEVEL = 3, MODE_VP_LEVEL = 4 };
 
 template <int N, int MODE, int V>
 __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::minb(V))
     cmux_kernel(const uint32_t *__restrict__ ggsw, size_t ggsw_words, const int32_t *__restrict__ gidx,
                 const uint32_t *in, const uint32_t *c1, const int32_t *__restrict__ rot, uint32_t *out,
-                uint32_t *out_hi, Gadget g, Tw tw) {
+                uint32_t *out_hi, int m, Gadget g, Tw tw) {
   constexpr int TPP = Cfg<N>::TPP, NT = Cfg<N>::THREADS;
+  constexpr bool LEVEL = MODE == MODE_IVP_LEVEL || MODE == MODE_VP_LEVEL;
+  constexpr bool DEMUX = MODE == MODE_CDEMUX || MODE == MODE_IVP_LEVEL;
+  constexpr bool MUX = MODE == MODE_CMUX || MODE == MODE_VP_LEVEL;
   extern __shared__ uint4 smem_raw[];
   Smem<N> &sm = *reinterpret_cast<Smem<N> *>(smem_raw);
   const int64_t b = blockIdx.x;
+  const int64_t item = LEVEL ? b / m : b, sub = LEVEL ? b % m : 0;
   const Who<N> me;
   const int tid = me.tid;
-  const uint32_t *G = ggsw + (size_t)(gidx ? gidx[b] : 0) * ggsw_words;
-  const uint32_t *src = in + b * 2 * N;
+  const uint32_t *G = ggsw + (size_t)(gidx ? gidx[item] : 0) * ggsw_words;
+  // operand / result addresses (see the mode comment above)
+  const uint32_t *src = in + (MODE == MODE_VP_LEVEL ? (item * 2 * m + sub) : b) * 2 * N;
+  const uint32_t *s1 = MODE == MODE_VP_LEVEL ? in + (item * 2 * m + m + sub) * 2 * N : (c1 ? c1 + b * 2 * N : nullptr);
+  uint32_t *o_lo = out + (MODE == MODE_IVP_LEVEL ? (item * 2 * m + sub) : b) * 2 * N;
+  uint32_t *o_hi = MODE == MODE_IVP_LEVEL ? out + (item * 2 * m + m + sub) * 2 * N : (out_hi ? out_hi + b * 2 * N : nullptr);
   if (MODE == MODE_EXT) {
     for (int k = tid; k < 2 * N; k += NT) sm.v[k] = decomp_prep(src[k], g);
   } else {
     for (int k = tid; k < 2 * N; k += NT) sm.acc[k] = src[k];
     __syncthreads();
-    if (MODE == MODE_CMUX) {
-      if (c1) {
-        const uint32_t *s1 = c1 + b * 2 * N;
+    if (MUX) {
+      if (s1) {
         for (int k = tid; k < 2 * N; k += NT) sm.v[k] = decomp_prep(s1[k] - sm.acc[k], g);
       } else {
         const int e = ((rot[b] % (2 * N)) + 2 * N) % (2 * N);
@@ -359,20 +369,42 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::minb(V))
   uint32_t x[N / TPP];
   ext_product_core<N, Cfg<N>::spec(V)>(sm, G, g, me, tw, x);
   const int w = me.grp;
-  uint32_t *o = out + b * 2 * N + w * N;
 #pragma unroll
   for (int j = 0; j < N / TPP; ++j) {
-    const int i = me.t + TPP * j;
-    const uint32_t val = lift(w, x[j], sm.v[w * N + i]);
+    const int i = w * N + me.t + TPP * j;
+    const uint32_t val = lift(w, x[j], sm.v[i]);
     if (MODE == MODE_EXT) {
-      o[i] = val;
-    } else if (MODE == MODE_CMUX) {
-      o[i] = sm.acc[w * N + i] + val;
+      o_lo[i] = val;
+    } else if (MUX) {
+      o_lo[i] = sm.acc[i] + val;
     } else {
-      out_hi[b * 2 * N + w * N + i] = val;
-      o[i] = sm.acc[w * N + i] - val;
+      o_hi[i] = val;
+      o_lo[i] = sm.acc[i] - val;
     }
   }
+}
+
+// x_b * X^(e_b) per item (hw/lut.py:317-325), e_b taken mod 2N; in may not alias out.
+template <int N>
+__global__ void monomial_gather_kernel(const uint32_t *__restrict__ in, uint32_t *__restrict__ out,
+                                       const int32_t *__restrict__ exps, int64_t B) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= B * 2 * N) return;
+  const int64_t b = idx / (2 * N);
+  const int k = (int)(idx % (2 * N));
+  const int e = ((exps[b] % (2 * N)) + 2 * N) % (2 * N);
+  const int c = k >= N, i = k & (N - 1);
+  out[idx] = rot_read<N>(in + b * 2 * N + c * N, i, e);
+}
+
+// dst[k] += sign * src[k] mod 2^32 (exact ring addition for model accumulation,
+// hw/hewnn.py:213, 264-271); src is indexed k mod src_words (broadcast rows).
+__global__ void accumulate_kernel(uint32_t *__restrict__ dst, const uint32_t *__restrict__ src, int64_t words,
+                                  int64_t src_words, int negate) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= words) return;
+  const uint32_t v = src[k % src_words];
+  dst[k] += negate ? 0u - v : v;
 }
 
 __device__ __forceinline__ int mod_switch(uint32_t x, int log2m) {
@@ -472,6 +504,65 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS) ggsw_to_ntt_kernel(const uint
     }
     o[jq * TPP + t] = make_uint4(y[0], y[1], y[2], y[3]);
   }
+}
+
+// Client-side key product (hw/tfhe.py:69-78 SecretKey._key_mul; used by
+// enc_rgsw_batch, hw/tfhe.py:246-263): out[b] = in[b] (*) s + add[b] mod 2^32
+// for a small key s given in the NTT domain (key_ntt: [2 primes][N], as
+// ggsw_to_ntt lays out one polynomial).  Exact while N * 2^31 * max|s| < P/2.
+template <int N>
+__global__ void __launch_bounds__(Cfg<N>::THREADS) key_mul_kernel(const uint32_t *__restrict__ in,
+                                                                  const uint32_t *__restrict__ key_ntt,
+                                                                  const uint32_t *__restrict__ add, uint32_t *out,
+                                                                  Tw tw) {
+  constexpr int TPP = Cfg<N>::TPP, NT = Cfg<N>::THREADS;
+  constexpr int C = N / TPP;
+  __shared__ uint32_t scr[2][N];
+  __shared__ uint32_t ex[2][N];
+  const int64_t poly = blockIdx.x;
+  const Who<N> me;
+  const int w = me.grp, t = me.t;
+  const uint32_t p = c_prime[w].p, pinv = c_prime[w].pinv;
+  uint32_t x[C];
+#pragma unroll
+  for (int j = 0; j < C; ++j) {
+    int32_t s = (int32_t)in[poly * N + t + TPP * j];   // centred coefficient
+    int32_t r = s % (int32_t)p;
+    x[j] = (uint32_t)(r < 0 ? r + (int32_t)p : r);
+  }
+  fwd_ntt<N, TPP, -1>(x, scr[w], me.lay, t, w, w ? tw.fwd[1] : tw.fwd[0]);
+  const uint32_t *ks = key_ntt + (size_t)w * N;
+#pragma unroll
+  for (int jq = 0; jq < C / 4; ++jq) {
+    const uint4 K = __ldg(slice_vec<TPP>(ks, t, jq));
+    x[4 * jq + 0] = mont_mul(x[4 * jq + 0], K.x, p, pinv);
+    x[4 * jq + 1] = mont_mul(x[4 * jq + 1], K.y, p, pinv);
+    x[4 * jq + 2] = mont_mul(x[4 * jq + 2], K.z, p, pinv);
+    x[4 * jq + 3] = mont_mul(x[4 * jq + 3], K.w, p, pinv);
+  }
+  inv_ntt<N, TPP, -1>(x, scr[w], me.lay, t, w, w ? tw.inv[1] : tw.inv[0]);
+#pragma unroll
+  for (int j = 0; j < C; ++j) ex[w][t + TPP * j] = umin(x[j], x[j] - p);
+  __syncthreads();
+  for (int i = me.tid; i < N; i += NT) {
+    uint32_t v = crt_lift(ex[0][i], ex[1][i]);
+    if (add) v += add[poly * N + i];
+    out[poly * N + i] = v;
+  }
+}
+
+// RGSW gadget term (hw/tfhe.py:259-262): rows t get m * q/beta^(t+1) on the b
+// constant coefficient, rows l+t on the a constant coefficient.
+__global__ void rgsw_gadget_kernel(uint32_t *rgsw, const int32_t *__restrict__ bits, int64_t B, int N, int levels,
+                                   int base_log) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= B * levels) return;
+  const int64_t b = idx / levels;
+  const int t = (int)(idx % levels);
+  const uint32_t gt = bits[b] ? (1u << (32 - (t + 1) * base_log)) : 0u;
+  uint32_t *g = rgsw + b * (int64_t)(2 * levels) * 2 * N;
+  g[((int64_t)t * 2 + 1) * N] += gt;              // row t, component b, coefficient 0
+  g[((int64_t)(levels + t) * 2 + 0) * N] += gt;   // row l+t, component a, coefficient 0
 }
 
 // hw/tfhe.py:352-361: LWE of coefficient i: a'[j] = a[i-j] (j <= i),
@@ -629,22 +720,23 @@ static int set_smem(K kernel, size_t bytes) {
 }
 
 
+// blocks = items (MODE < MODE_IVP_LEVEL) or items * m (tree levels)
 template <int N, int MODE>
 static int launch_cmux(const hwb_params *p, DevState *st, const uint32_t *ggsw, const int32_t *gidx,
                        const uint32_t *in, const uint32_t *c1, const int32_t *rot, uint32_t *out,
-                       uint32_t *out_hi, int64_t B, cudaStream_t s) {
+                       uint32_t *out_hi, int64_t blocks, int m, cudaStream_t s) {
   const size_t smem = sizeof(Smem<N>);
   const size_t words = hwb_ggsw_ntt_words(p);
   const Gadget g = make_gadget(p->l, p->base_log);
   int rc;
   if (g_variant == 1) {
     if ((rc = set_smem(cmux_kernel<N, MODE, 1>, smem))) return rc;
-    cmux_kernel<N, MODE, 1><<<(unsigned)B, Cfg<N>::THREADS, smem, s>>>(ggsw, words, gidx, in, c1, rot, out,
-                                                                              out_hi, g, make_tw(st, N));
+    cmux_kernel<N, MODE, 1><<<(unsigned)blocks, Cfg<N>::THREADS, smem, s>>>(ggsw, words, gidx, in, c1, rot, out,
+                                                                            out_hi, m, g, make_tw(st, N));
   } else {
     if ((rc = set_smem(cmux_kernel<N, MODE, 0>, smem))) return rc;
-    cmux_kernel<N, MODE, 0><<<(unsigned)B, Cfg<N>::THREADS, smem, s>>>(ggsw, words, gidx, in, c1, rot, out,
-                                                                              out_hi, g, make_tw(st, N));
+    cmux_kernel<N, MODE, 0><<<(unsigned)blocks, Cfg<N>::THREADS, smem, s>>>(ggsw, words, gidx, in, c1, rot, out,
+                                                                            out_hi, m, g, make_tw(st, N));
   }
   return post_launch("cmux_kernel");
 }
@@ -721,25 +813,115 @@ int hwb_ggsw_to_ntt(const hwb_params *p, const uint32_t *ggsw, uint32_t *ggsw_nt
   return post_launch("ggsw_to_ntt_kernel");
 }
 
+extern "C++" {
+template <int N>
+static int launch_mode(int mode, const hwb_params *p, DevState *st, const uint32_t *ggsw, const int32_t *gidx,
+                       const uint32_t *in, const uint32_t *c1, const int32_t *rot, uint32_t *out,
+                       uint32_t *out_hi, int64_t blocks, int m, cudaStream_t s) {
+  switch (mode) {
+    case MODE_EXT: return launch_cmux<N, MODE_EXT>(p, st, ggsw, gidx, in, c1, rot, out, out_hi, blocks, m, s);
+    case MODE_CMUX: return launch_cmux<N, MODE_CMUX>(p, st, ggsw, gidx, in, c1, rot, out, out_hi, blocks, m, s);
+    case MODE_CDEMUX: return launch_cmux<N, MODE_CDEMUX>(p, st, ggsw, gidx, in, c1, rot, out, out_hi, blocks, m, s);
+    case MODE_IVP_LEVEL:
+      return launch_cmux<N, MODE_IVP_LEVEL>(p, st, ggsw, gidx, in, c1, rot, out, out_hi, blocks, m, s);
+    default: return launch_cmux<N, MODE_VP_LEVEL>(p, st, ggsw, gidx, in, c1, rot, out, out_hi, blocks, m, s);
+  }
+}
+}  // extern "C++"
+
 static int cmux_dispatch(int mode, const hwb_params *p, const uint32_t *ggsw, const int32_t *gidx,
                          const uint32_t *in, const uint32_t *c1, const int32_t *rot, uint32_t *out,
-                         uint32_t *out_hi, int64_t B, void *stream) {
+                         uint32_t *out_hi, int64_t B, void *stream, int m = 1) {
+  int rc = check_glwe(p);
+  if (rc) return rc;
+  if (B < 0) return fail(HWB_EINVAL, "negative batch");
+  if (m < 1) return fail(HWB_EINVAL, "tree level needs m >= 1 polynomials per item");
+  if (B == 0) return HWB_OK;
+  const int64_t blocks = B * m;
+  if (blocks > 0x7FFFFFFF) return fail(HWB_EINVAL, "batch too large");
+  DevState *st;
+  if ((rc = init_device(&st))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p->N == 1024) return launch_mode<1024>(mode, p, st, ggsw, gidx, in, c1, rot, out, out_hi, blocks, m, s);
+  return launch_mode<2048>(mode, p, st, ggsw, gidx, in, c1, rot, out, out_hi, blocks, m, s);
+}
+
+int hwb_ivp_level(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_t *ggsw_idx, const uint32_t *cur,
+                  uint32_t *next, int32_t m, int64_t B, void *stream) {
+  return cmux_dispatch(MODE_IVP_LEVEL, p, ggsw_ntt, ggsw_idx, cur, nullptr, nullptr, next, nullptr, B, stream, m);
+}
+
+int hwb_vp_level(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_t *ggsw_idx, const uint32_t *cur,
+                 uint32_t *next, int32_t m, int64_t B, void *stream) {
+  return cmux_dispatch(MODE_VP_LEVEL, p, ggsw_ntt, ggsw_idx, cur, nullptr, nullptr, next, nullptr, B, stream, m);
+}
+
+int hwb_monomial_gather(const hwb_params *p, const uint32_t *in, uint32_t *out, const int32_t *exps, int64_t B,
+                        void *stream) {
   int rc = check_glwe(p);
   if (rc) return rc;
   if (B < 0) return fail(HWB_EINVAL, "negative batch");
   if (B == 0) return HWB_OK;
-  if (B > 0x7FFFFFFF) return fail(HWB_EINVAL, "batch too large");
+  if (in == out) return fail(HWB_EINVAL, "monomial_gather cannot run in place");
+  const int64_t total = B * 2 * p->N;
+  const unsigned blocks = (unsigned)((total + 255) / 256);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p->N == 1024)
+    monomial_gather_kernel<1024><<<blocks, 256, 0, s>>>(in, out, exps, B);
+  else
+    monomial_gather_kernel<2048><<<blocks, 256, 0, s>>>(in, out, exps, B);
+  return post_launch("monomial_gather_kernel");
+}
+
+int hwb_poly_to_ntt(const hwb_params *p, const uint32_t *in, uint32_t *out, int64_t npolys, void *stream) {
+  int rc = check_glwe(p);
+  if (rc) return rc;
+  if (npolys < 0) return fail(HWB_EINVAL, "negative count");
+  if (npolys == 0) return HWB_OK;
   DevState *st;
   if ((rc = init_device(&st))) return rc;
   cudaStream_t s = (cudaStream_t)stream;
-  if (p->N == 1024) {
-    if (mode == MODE_EXT) return launch_cmux<1024, MODE_EXT>(p, st, ggsw, gidx, in, c1, rot, out, out_hi, B, s);
-    if (mode == MODE_CMUX) return launch_cmux<1024, MODE_CMUX>(p, st, ggsw, gidx, in, c1, rot, out, out_hi, B, s);
-    return launch_cmux<1024, MODE_CDEMUX>(p, st, ggsw, gidx, in, c1, rot, out, out_hi, B, s);
-  }
-  if (mode == MODE_EXT) return launch_cmux<2048, MODE_EXT>(p, st, ggsw, gidx, in, c1, rot, out, out_hi, B, s);
-  if (mode == MODE_CMUX) return launch_cmux<2048, MODE_CMUX>(p, st, ggsw, gidx, in, c1, rot, out, out_hi, B, s);
-  return launch_cmux<2048, MODE_CDEMUX>(p, st, ggsw, gidx, in, c1, rot, out, out_hi, B, s);
+  if (p->N == 1024)
+    ggsw_to_ntt_kernel<1024><<<(unsigned)npolys, Cfg<1024>::THREADS, 0, s>>>(in, out, make_tw(st, 1024));
+  else
+    ggsw_to_ntt_kernel<2048><<<(unsigned)npolys, Cfg<2048>::THREADS, 0, s>>>(in, out, make_tw(st, 2048));
+  return post_launch("poly_to_ntt");
+}
+
+int hwb_key_mul(const hwb_params *p, const uint32_t *key_ntt, const uint32_t *in, const uint32_t *add, uint32_t *out,
+                int64_t npolys, void *stream) {
+  int rc = check_glwe(p);
+  if (rc) return rc;
+  if (npolys < 0) return fail(HWB_EINVAL, "negative count");
+  if (npolys == 0) return HWB_OK;
+  DevState *st;
+  if ((rc = init_device(&st))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p->N == 1024)
+    key_mul_kernel<1024><<<(unsigned)npolys, Cfg<1024>::THREADS, 0, s>>>(in, key_ntt, add, out, make_tw(st, 1024));
+  else
+    key_mul_kernel<2048><<<(unsigned)npolys, Cfg<2048>::THREADS, 0, s>>>(in, key_ntt, add, out, make_tw(st, 2048));
+  return post_launch("key_mul_kernel");
+}
+
+int hwb_rgsw_add_gadget(const hwb_params *p, uint32_t *rgsw, const int32_t *bits, int64_t B, void *stream) {
+  int rc = check_glwe(p);
+  if (rc) return rc;
+  if (B < 0) return fail(HWB_EINVAL, "negative batch");
+  if (B == 0) return HWB_OK;
+  const int64_t total = B * p->l;
+  rgsw_gadget_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(rgsw, bits, B, (int)p->N,
+                                                                                         (int)p->l, (int)p->base_log);
+  return post_launch("rgsw_gadget_kernel");
+}
+
+int hwb_accumulate(uint32_t *dst, const uint32_t *src, int64_t words, int64_t src_words, int negate, void *stream) {
+  if (words < 0 || src_words < 1 || (words > 0 && (words % src_words) != 0))
+    return fail(HWB_EINVAL, "accumulate: words must be a multiple of src_words");
+  if (words == 0) return HWB_OK;
+  accumulate_kernel<<<(unsigned)((words + 255) / 256), 256, 0, (cudaStream_t)stream>>>(dst, src, words, src_words,
+                                                                                         negate);
+  return post_launch("accumulate_kernel");
 }
 
 int hwb_ext_product(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_t *ggsw_idx,

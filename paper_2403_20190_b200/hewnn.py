@@ -1,0 +1,305 @@
+"""WiSARD training and inference over TFHE-encrypted data, on B200.
+
+Mirror of the reference's `hewisard.hewnn` (`pkg/src/hewisard/hewnn.py`):
+training deposits, per sample and RAM, an encrypted +1 at the (label,
+address) entry of the RAM's row by inverse vertical packing of the payload
+(0, q/p) (`hewnn.py:189-229`); a small IVP over the label bits accumulates
+encrypted class counts (`hewnn.py:180-186`).  Rows are added by exact ring
+addition, so sample order and batching cannot change the ciphertexts.
+
+Differences in mechanics (not results): samples are processed in batches of
+`batch` images whose RGSW bits share one device GGSW table, so every kernel
+launch covers batch*k0 items; the model lives in device memory.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Iterable, Sequence
+
+import numpy as np
+import torch
+
+from . import lut, tfhe
+from ._lib import TfheError
+from .params import HeParams
+from .tfhe import RgswCiphertext, RlweCiphertext
+from .wnn import ClassCounts, WisardGeometry, permutation
+
+
+@dataclass
+class EncryptedSample:
+    """One preprocessed sample encrypted bit by bit as RGSW (hw/hewnn.py:33-43).
+
+    `rgsw` holds all s data bits then the label bits (LSB-first) as one
+    (s + label_bits, 2l, 2, N) uint32 array (numpy or a device tensor)."""
+
+    params: HeParams
+    rgsw: object
+    s: int
+    label_bits: int = 0
+
+    @property
+    def data_bits(self) -> list[RgswCiphertext]:
+        host = self.rgsw if isinstance(self.rgsw, np.ndarray) else tfhe.to_host(self.rgsw)
+        return [RgswCiphertext(self.params, host[i]) for i in range(self.s)]
+
+    @property
+    def labels(self) -> list[RgswCiphertext] | None:
+        if not self.label_bits:
+            return None
+        host = self.rgsw if isinstance(self.rgsw, np.ndarray) else tfhe.to_host(self.rgsw)
+        return [RgswCiphertext(self.params, host[self.s + i]) for i in range(self.label_bits)]
+
+
+@dataclass
+class HomWisardModel:
+    """Encrypted integer WiSARD: k0 x k1 RLWE rows plus encrypted class counts
+    (hw/hewnn.py:46-64), resident on the device."""
+
+    geometry: WisardGeometry
+    params: HeParams
+    rams: torch.Tensor            # int32 (k0, k1, 2, N)
+    counts_ct: torch.Tensor       # int32 (2, N)
+
+    @classmethod
+    def zeros(cls, geometry: WisardGeometry, params: HeParams) -> "HomWisardModel":
+        k1 = model_row_polys(geometry, params)
+        dev = tfhe._device()
+        return cls(geometry, params,
+                   torch.zeros((geometry.k0, k1, 2, params.n), dtype=torch.int32, device=dev),
+                   torch.zeros((2, params.n), dtype=torch.int32, device=dev))
+
+    def copy(self) -> "HomWisardModel":
+        return HomWisardModel(self.geometry, self.params, self.rams.clone(), self.counts_ct.clone())
+
+
+def model_row_polys(geometry: WisardGeometry, params: HeParams) -> int:
+    """RLWE ciphertexts per RAM row: max(1, 2^(label_bits + a) / N) (hw/hewnn.py:95-97)."""
+    return max(1, (1 << geometry.selector_bits) // params.n)
+
+
+def _check_geometry(geometry: WisardGeometry, params: HeParams):
+    if geometry.p != params.p:
+        raise TfheError(f"geometry counter modulus {geometry.p} != params p {params.p}")
+
+
+# ---------------------------------------------------------------------------
+# encryption (client side)
+
+
+class DeviceKey:
+    """A secret key's NTT image on the device, for GPU-side key products."""
+
+    def __init__(self, key: tfhe.SecretKey):
+        params = key.params
+        self.params = params
+        s = tfhe.to_device(key.s)
+        cp = _lib_params(params)
+        self.ntt = torch.empty((2, params.n), dtype=torch.int32, device=s.device)
+        tfhe._lib.check(tfhe._lib.load().hwb_poly_to_ntt(cp, tfhe._ptr(s), tfhe._ptr(self.ntt), 1,
+                                                         tfhe._stream()))
+
+
+def _lib_params(params):
+    import ctypes
+    return ctypes.byref(tfhe._lib.c_params(params))
+
+
+_device_keys: dict[int, DeviceKey] = {}
+
+
+def _device_key(key: tfhe.SecretKey) -> DeviceKey:
+    dk = _device_keys.get(id(key))
+    if dk is None or dk.params != key.params:
+        dk = DeviceKey(key)
+        _device_keys[id(key)] = dk
+    return dk
+
+
+def enc_rgsw_batch_device(ms, key: tfhe.SecretKey, rng) -> torch.Tensor:
+    """enc_rgsw_batch (hw/tfhe.py:246-263) with the key product on the GPU.
+
+    Same RNG stream as the host version (a then e, drawn on the host); returns
+    the device tensor (B, 2l, 2, N), bit-identical to tfhe.enc_rgsw_batch."""
+    ms = np.asarray(ms, dtype=np.int64)
+    params = key.params
+    g = params.gadget
+    rows = 2 * g.levels
+    B = len(ms)
+    if np.any((ms != 0) & (ms != 1)):
+        raise tfhe.EncodingError("RGSW messages are bits")
+    a = tfhe.uniform_u32(rng, (B, rows, params.n))
+    e = tfhe.gaussian_u32(rng, params.sigma, (B, rows, params.n))
+    dev = tfhe._device()
+    out = torch.empty((B, rows, 2, params.n), dtype=torch.int32, device=dev)
+    if B == 0:
+        return out
+    a_d = tfhe.to_device(a)
+    e_d = tfhe.to_device(e)
+    b_d = torch.empty_like(a_d)
+    dk = _device_key(key)
+    cp = _lib_params(params)
+    L = tfhe._lib.load()
+    tfhe._lib.check(L.hwb_key_mul(cp, tfhe._ptr(dk.ntt), tfhe._ptr(a_d), tfhe._ptr(e_d), tfhe._ptr(b_d),
+                                  B * rows, tfhe._stream()))
+    out[:, :, 0] = a_d
+    out[:, :, 1] = b_d
+    bits = torch.as_tensor(ms, dtype=torch.int32).to(dev)
+    tfhe._lib.check(L.hwb_rgsw_add_gadget(cp, tfhe._ptr(out), tfhe._ptr(bits), B, tfhe._stream()))
+    return out
+
+
+def encrypt_sample(bits: Sequence[int], label: int | None, key: tfhe.SecretKey, rng, *,
+                   label_bits: int = 0, device: bool = True) -> EncryptedSample:
+    """Encrypt preprocessed input bits and the label (hw/hewnn.py:109-119).
+
+    RNG stream as the reference: the data batch, then the label batch."""
+    enc = enc_rgsw_batch_device if device else _enc_rgsw_host
+    data = enc(np.asarray(bits, dtype=np.int64), key, rng)
+    lb = 0
+    if label is not None:
+        if label >= (1 << label_bits):
+            raise TfheError(f"label {label} does not fit in {label_bits} bits")
+        lab = enc(np.array([(label >> i) & 1 for i in range(label_bits)], dtype=np.int64), key, rng)
+        data = torch.cat([data, lab]) if device else np.concatenate([data, lab])
+        lb = label_bits
+    return EncryptedSample(key.params, data, len(bits), lb)
+
+
+def _enc_rgsw_host(ms, key, rng) -> np.ndarray:
+    if len(ms) == 0:
+        g = key.params.gadget
+        return np.zeros((0, 2 * g.levels, 2, key.params.n), dtype=np.uint32)
+    return np.stack([c.data for c in tfhe.enc_rgsw_batch(ms, key, rng)])
+
+
+# ---------------------------------------------------------------------------
+# selector construction (hw/hewnn.py:134-173)
+
+
+def _selector_template(geometry: WisardGeometry, params: HeParams, *, clear_label: int | None = None):
+    """(k0, k) codes relative to a sample's first RGSW row.
+
+    Positions follow the canonical tree-MSB / rotate-LSB order
+    (hw/hewnn.py:134-150); address bit w of RAM j is permuted input bit
+    perm[j*a + w] (hw/wnn.py:189-196), zero padding past s is a clear 0
+    (hw/hewnn.py:164-166); label bit i is row s + i, or the clear bits of
+    `clear_label` (inference, hw/hewnn.py:303-304)."""
+    k = geometry.selector_bits
+    z = lut.tree_depth(k, params)
+    a, s = geometry.a, geometry.s
+    perm = permutation(geometry.r, geometry.s)
+    weights = [k - 1 - i for i in range(z)] + lut.rotate_weights(k, params)
+    out = np.empty((geometry.k0, k), dtype=np.int64)
+    for j in range(geometry.k0):
+        for pos, w in enumerate(weights):
+            if w < a:
+                idx = j * a + w
+                out[j, pos] = perm[idx] if idx < s else lut.CLEAR0
+            elif clear_label is None:
+                out[j, pos] = s + (w - a)
+            else:
+                out[j, pos] = lut.CLEAR1 if (clear_label >> (w - a)) & 1 else lut.CLEAR0
+    return out
+
+
+def _shift(codes: np.ndarray, base: int) -> np.ndarray:
+    return np.where(codes >= 0, codes + base, codes)
+
+
+def _payload(params: HeParams) -> np.ndarray:
+    return tfhe.trivial_rlwe(1, params).data
+
+
+# ---------------------------------------------------------------------------
+# training
+
+
+def _stack_table(params: HeParams, samples: list[EncryptedSample]):
+    rg = [s.rgsw if isinstance(s.rgsw, torch.Tensor) else tfhe.to_device(s.rgsw) for s in samples]
+    big = rg[0] if len(rg) == 1 else torch.cat(rg)
+    return tfhe.rgsw_to_ntt(params, big)
+
+
+def he_count_labels_batch(params: HeParams, counts_ct: torch.Tensor, table, label_rows: np.ndarray):
+    """hw/hewnn.py:180-186 for several samples: counts += IVP(label bits, (0, q/p))."""
+    rows = lut.ivp_codes(params, label_rows, table, _payload(params))     # (I, 1, 2, N)
+    for i in range(rows.shape[0]):
+        lut.accumulate_(counts_ct, rows[i, 0])
+    return counts_ct
+
+
+def he_train(samples: Iterable[EncryptedSample], geometry: WisardGeometry, params: HeParams,
+             model: HomWisardModel | None = None, threads: int = 1, batch: int = 16) -> HomWisardModel:
+    """Homomorphic integer WiSARD training (hw/hewnn.py:189-229); pass an
+    existing model to continue training.  `threads` is accepted for API
+    compatibility (the GPU batches `batch` samples per launch instead)."""
+    _check_geometry(geometry, params)
+    if model is None:
+        model = HomWisardModel.zeros(geometry, params)
+    if model.geometry != geometry or model.params != params:
+        raise TfheError("model geometry/params mismatch")
+    tmpl = _selector_template(geometry, params)
+    chunk: list[EncryptedSample] = []
+
+    def flush():
+        if not chunk:
+            return
+        table = _stack_table(params, chunk)
+        stride = geometry.s + geometry.label_bits
+        codes = np.concatenate([_shift(tmpl, i * stride) for i in range(len(chunk))])
+        rows = lut.ivp_codes(params, codes, table, _payload(params))      # (I*k0, k1, 2, N)
+        per = model.rams.numel()
+        flat = rows.reshape(len(chunk), per)
+        for i in range(len(chunk)):
+            lut.accumulate_(model.rams, flat[i])
+        label_rows = np.array([[i * stride + geometry.s + b for b in range(geometry.label_bits)]
+                               for i in range(len(chunk))], dtype=np.int64)
+        he_count_labels_batch(params, model.counts_ct, table, label_rows)
+        chunk.clear()
+
+    for sample in samples:
+        if sample.s != geometry.s:
+            raise TfheError(f"sample has {sample.s} bits, geometry wants {geometry.s}")
+        if sample.label_bits != geometry.label_bits:
+            raise TfheError("training samples need encrypted label bits")
+        chunk.append(sample)
+        if len(chunk) == batch:
+            flush()
+    flush()
+    return model
+
+
+def he_merge(m1: HomWisardModel, m2: HomWisardModel) -> HomWisardModel:
+    """Federated merge: entry-wise RLWE addition (hw/hewnn.py:264-271)."""
+    if m1.geometry != m2.geometry:
+        raise TfheError("cannot merge models with different geometry or seed")
+    if m1.params != m2.params:
+        raise TfheError("cannot merge models with different parameters")
+    out = m1.copy()
+    lut.accumulate_(out.rams, m2.rams)
+    lut.accumulate_(out.counts_ct, m2.counts_ct)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# client side: decryption of a trained model (oracle bridge, hw/hewnn.py:352-365)
+
+
+def decrypt_counts(counts_ct, params: HeParams, l: int, key: tfhe.SecretKey) -> ClassCounts:
+    data = counts_ct if isinstance(counts_ct, np.ndarray) else tfhe.to_host(counts_ct)
+    vals = tfhe.dec_rlwe(RlweCiphertext(params, data), key)
+    return ClassCounts(vals[:l].astype(np.int64))
+
+
+def decrypt_model(model: HomWisardModel, key: tfhe.SecretKey):
+    """Decrypt the RLWE matrix into integer counters (l, k0, 2^a) and class counts."""
+    g, params = model.geometry, model.params
+    rams = tfhe.to_host(model.rams)                               # (k0, k1, 2, N)
+    phase = (rams[:, :, 1] - tfhe._key_mul_host(rams[:, :, 0], key.s)).astype(np.uint32)
+    vals = tfhe.decode_phase(phase, params).reshape(g.k0, -1)[:, : 1 << g.selector_bits]
+    counters = np.zeros((g.l, g.k0, 1 << g.a), dtype=np.int64)
+    for c in range(g.l):
+        counters[c] = vals[:, c << g.a: (c << g.a) + (1 << g.a)]
+    return counters, decrypt_counts(model.counts_ct, params, g.l, key)

@@ -1,0 +1,314 @@
+"""Encrypted lookup tables on B200: vertical packing and its inverse.
+
+Mirror of the reference's `hewisard.lut` (`pkg/src/hewisard/lut.py`).  The
+selector order is the reference's: a k-bit selector feeds the CMUX/CDEMUX tree
+with the most-significant index bits first (positions 0..z-1, z = max(0, k -
+log2 N)) and the blind rotation with the least-significant bits (position z+i
+carries weight 2^i); table entry m lives at polynomial m // N, coefficient
+m % N (`lut.py:1-11`).
+
+Every homomorphic step runs in libhwb200: the rotation CMUXes (`hwb_cmux` with a
+per-item rotation and GGSW), the tree levels (`hwb_ivp_level` / `hwb_vp_level`),
+clear rotations (`hwb_monomial_gather`) and extraction.  Encrypted selector bits
+are addressed as rows of one device GGSW table (`tfhe.GgswNtt`); the batched
+entry points take an int32 code matrix: code >= 0 is a table row, -1 a clear 0,
+-2 a clear 1.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib, tfhe
+from ._lib import TfheError
+from .params import HeParams
+from .tfhe import GgswNtt, RgswCiphertext, RlweCiphertext
+
+CLEAR0, CLEAR1 = -1, -2
+
+
+@dataclass
+class SelectorBit:
+    """Either a public bit or an RGSW encryption of one (hw/lut.py:25-44)."""
+
+    ct: RgswCiphertext | None = None
+    bit: int | None = None
+
+    @classmethod
+    def clear(cls, bit: int) -> "SelectorBit":
+        if bit not in (0, 1):
+            raise ValueError("selector bits are binary")
+        return cls(bit=bit)
+
+    @classmethod
+    def enc(cls, ct: RgswCiphertext) -> "SelectorBit":
+        return cls(ct=ct)
+
+    @property
+    def is_clear(self) -> bool:
+        return self.ct is None
+
+
+def tree_depth(k: int, params: HeParams) -> int:
+    """hw/lut.py:66-67."""
+    return max(0, k - params.degree_log)
+
+
+def rotate_weights(k: int, params: HeParams) -> list[int]:
+    """Index weights of the rotation positions, LSB-first (hw/lut.py:70-72)."""
+    return list(range(min(k, params.degree_log)))
+
+
+def selector_index(bits: list[int], k: int, params: HeParams) -> int:
+    """Table index encoded by a full selector vector (hw/lut.py:75-83)."""
+    z = tree_depth(k, params)
+    m = 0
+    for i in range(z):
+        m += bits[i] << (k - 1 - i)
+    for i, w in enumerate(rotate_weights(k, params)):
+        m += bits[z + i] << w
+    return m
+
+
+# ---------------------------------------------------------------------------
+# device primitives
+
+
+def _cp(params):
+    return ctypes.byref(_lib.c_params(params))
+
+
+def _i32(x, device) -> torch.Tensor:
+    t = x if isinstance(x, torch.Tensor) else torch.as_tensor(np.asarray(x, dtype=np.int64))
+    return t.to(device=device, dtype=torch.int32).contiguous()
+
+
+def monomial_gather(params: HeParams, x, es):
+    """Per-item x_i * X^(es_i) (hw/lut.py:317-325) on the GPU."""
+    t = tfhe.to_device(x)
+    B = t.shape[0]
+    e = _i32(np.asarray(es, dtype=np.int64) % (2 * params.n) if not isinstance(es, torch.Tensor) else es, t.device)
+    out = torch.empty_like(t)
+    _lib.check(_lib.load().hwb_monomial_gather(_cp(params), tfhe._ptr(t), tfhe._ptr(out), tfhe._ptr(e), B,
+                                               tfhe._stream()))
+    return tfhe._wrap(x, out)
+
+
+def accumulate_(dst: torch.Tensor, src: torch.Tensor, negate: bool = False) -> torch.Tensor:
+    """dst += src (mod 2^32, in place); src may be a shorter block repeated over dst."""
+    if dst.numel() % max(1, src.numel()):
+        raise TfheError("accumulate: shapes do not tile")
+    _lib.check(_lib.load().hwb_accumulate(tfhe._ptr(dst), tfhe._ptr(src), dst.numel(), src.numel(),
+                                          1 if negate else 0, tfhe._stream()))
+    return dst
+
+
+def _cmux_rot(params, table: GgswNtt, acc: torch.Tensor, idx: torch.Tensor, rot: int) -> torch.Tensor:
+    """acc[b] <- acc[b] + C_idx[b] (*) (acc[b] X^rot - acc[b]) for all rows of acc."""
+    out = torch.empty_like(acc)
+    rt = torch.full((acc.shape[0],), rot % (2 * params.n), dtype=torch.int32, device=acc.device)
+    _lib.check(_lib.load().hwb_cmux(_cp(params), tfhe._ptr(table.data), tfhe._ptr(idx), None, tfhe._ptr(acc),
+                                    tfhe._ptr(rt), tfhe._ptr(out), acc.shape[0], tfhe._stream()))
+    return out
+
+
+def _level(params, table: GgswNtt, cur: torch.Tensor, idx: torch.Tensor, inverse: bool) -> torch.Tensor:
+    B, mm = cur.shape[0], cur.shape[1]
+    if inverse:
+        nxt = torch.empty((B, 2 * mm) + tuple(cur.shape[2:]), dtype=torch.int32, device=cur.device)
+        fn, m = _lib.load().hwb_ivp_level, mm
+    else:
+        nxt = torch.empty((B, mm // 2) + tuple(cur.shape[2:]), dtype=torch.int32, device=cur.device)
+        fn, m = _lib.load().hwb_vp_level, mm // 2
+    _lib.check(fn(_cp(params), tfhe._ptr(table.data), tfhe._ptr(idx), tfhe._ptr(cur), tfhe._ptr(nxt), m, B,
+                  tfhe._stream()))
+    return nxt
+
+
+# ---------------------------------------------------------------------------
+# batched engines over code matrices
+
+
+def ivp_codes(params: HeParams, codes, table: GgswNtt | None, payload) -> torch.Tensor:
+    """Inverse vertical packing (hw/lut.py:269-314) for B items sharing one payload.
+
+    codes: (B, k) int (row of `table`, CLEAR0 or CLEAR1).  Returns the device
+    tensor (B, max(1, 2^z), 2, N) of single-valued LUT rows."""
+    codes = np.asarray(codes, dtype=np.int64)
+    B, k = codes.shape
+    z = tree_depth(k, params)
+    n = params.n
+    pay = tfhe.to_device(payload)
+    dev = pay.device
+    acc = pay.reshape(1, 2, n).expand(B, 2, n).contiguous()
+    clear_e = np.zeros(B, dtype=np.int64)
+    for i, w in enumerate(rotate_weights(k, params)):
+        col = codes[:, z + i]
+        enc = col >= 0
+        clear_e += (col == CLEAR1).astype(np.int64) << w
+        if not enc.any():
+            continue
+        if enc.all():
+            acc = _cmux_rot(params, table, acc, _i32(col, dev), 1 << w)
+        else:
+            sel = torch.as_tensor(np.nonzero(enc)[0], device=dev)
+            acc[sel] = _cmux_rot(params, table, acc[sel].contiguous(), _i32(col[enc], dev), 1 << w)
+    if clear_e.any():
+        acc = monomial_gather(params, acc, clear_e)
+    cur = acc.unsqueeze(1)
+    for pos in range(z - 1, -1, -1):
+        col = codes[:, pos]
+        enc = col >= 0
+        if enc.all():
+            cur = _level(params, table, cur.contiguous(), _i32(col, dev), inverse=True)
+            continue
+        mm = cur.shape[1]
+        new = torch.zeros((B, 2 * mm, 2, n), dtype=torch.int32, device=dev)
+        c0 = torch.as_tensor(np.nonzero(col == CLEAR0)[0], device=dev)
+        c1 = torch.as_tensor(np.nonzero(col == CLEAR1)[0], device=dev)
+        if c0.numel():
+            new[c0, :mm] = cur[c0]
+        if c1.numel():
+            new[c1, mm:] = cur[c1]
+        if enc.any():
+            sel = torch.as_tensor(np.nonzero(enc)[0], device=dev)
+            new[sel] = _level(params, table, cur[sel].contiguous(), _i32(col[enc], dev), inverse=True)
+        cur = new
+    return cur
+
+
+def vp_codes(params: HeParams, codes, table: GgswNtt | None, lut_table: torch.Tensor, lut_idx):
+    """Vertical packing (hw/lut.py:209-266) for B items.
+
+    lut_table: device (T, 2^z, 2, N) tables; lut_idx: (B,) which table each item
+    reads.  Returns the extracted LWE pieces as a device tensor (B, N+1) (b last)."""
+    codes = np.asarray(codes, dtype=np.int64)
+    lut_idx = np.asarray(lut_idx, dtype=np.int64)
+    B, k = codes.shape
+    z = tree_depth(k, params)
+    n = params.n
+    dev = lut_table.device
+    # clear-prefix tree levels are pure index arithmetic (hw/lut.py:221-231)
+    start = np.zeros(B, dtype=np.int64)
+    length = np.full(B, max(1, 1 << z), dtype=np.int64)
+    lvl = 0
+    while lvl < z and (codes[:, lvl] < 0).all():
+        length //= 2
+        start += np.where(codes[:, lvl] == CLEAR1, length, 0)
+        lvl += 1
+    L = int(length[0]) if B else 1
+    rows = (lut_idx[:, None] * lut_table.shape[1] + start[:, None] + np.arange(L)[None, :]).reshape(-1)
+    cur = lut_table.reshape(-1, 2, n)[torch.as_tensor(rows, device=dev)].reshape(B, L, 2, n)
+    for pos in range(lvl, z):
+        col = codes[:, pos]
+        enc = col >= 0
+        half = cur.shape[1] // 2
+        if enc.all():
+            cur = _level(params, table, cur.contiguous(), _i32(col, dev), inverse=False)
+            continue
+        new = torch.empty((B, half, 2, n), dtype=torch.int32, device=dev)
+        c0 = torch.as_tensor(np.nonzero(col == CLEAR0)[0], device=dev)
+        c1 = torch.as_tensor(np.nonzero(col == CLEAR1)[0], device=dev)
+        if c0.numel():
+            new[c0] = cur[c0, :half]
+        if c1.numel():
+            new[c1] = cur[c1, half:]
+        if enc.any():
+            sel = torch.as_tensor(np.nonzero(enc)[0], device=dev)
+            new[sel] = _level(params, table, cur[sel].contiguous(), _i32(col[enc], dev), inverse=False)
+        cur = new
+    acc = cur[:, 0].contiguous()
+    clear_e = np.zeros(B, dtype=np.int64)
+    for i, w in enumerate(rotate_weights(k, params)):
+        col = codes[:, z + i]
+        enc = col >= 0
+        clear_e += (col == CLEAR1).astype(np.int64) << w
+        if not enc.any():
+            continue
+        if enc.all():
+            acc = _cmux_rot(params, table, acc, _i32(col, dev), -(1 << w))
+        else:
+            sel = torch.as_tensor(np.nonzero(enc)[0], device=dev)
+            acc[sel] = _cmux_rot(params, table, acc[sel].contiguous(), _i32(col[enc], dev), -(1 << w))
+    if clear_e.any():
+        acc = monomial_gather(params, acc, -clear_e)
+    return tfhe.sample_extract_batch(params, acc)
+
+
+# ---------------------------------------------------------------------------
+# reference-shaped API over SelectorBit lists
+
+
+def _codes_of(selectors: list[list[SelectorBit]], params: HeParams):
+    """Code matrix + one device GGSW table for the distinct encrypted bits."""
+    rows: dict[int, int] = {}
+    cts: list[RgswCiphertext] = []
+    codes = np.empty((len(selectors), len(selectors[0]) if selectors else 0), dtype=np.int64)
+    for i, sel in enumerate(selectors):
+        if len(sel) != codes.shape[1]:
+            raise TfheError("selector vectors must share one arity")
+        for j, s in enumerate(sel):
+            if s.is_clear:
+                codes[i, j] = CLEAR1 if s.bit else CLEAR0
+            else:
+                key = id(s.ct)
+                if key not in rows:
+                    rows[key] = len(cts)
+                    cts.append(s.ct)
+                codes[i, j] = rows[key]
+    table = None
+    if cts:
+        table = tfhe.rgsw_to_ntt(params, np.stack([np.asarray(c.data) for c in cts]))
+    return codes, table
+
+
+def ivp_batch(selectors: list[list[SelectorBit]], payload, params: HeParams):
+    """hw/lut.py:269-314: returns (B, max(1, 2^z), 2, N) uint32 rows (numpy)."""
+    codes, table = _codes_of(selectors, params)
+    return tfhe.to_host(ivp_codes(params, codes, table, np.asarray(payload)))
+
+
+def vp_batch(selectors: list[list[SelectorBit]], luts: list, params: HeParams):
+    """hw/lut.py:209-266: returns (lwe_a (B, N), lwe_b (B,)) uint32 (numpy)."""
+    codes, table = _codes_of(selectors, params)
+    lut_table = tfhe.to_device(np.stack([np.asarray(x) for x in luts]))
+    out = tfhe.to_host(vp_codes(params, codes, table, lut_table, np.arange(len(luts))))
+    return out[:, :-1], out[:, -1].copy()
+
+
+def encode_lut(values, params: HeParams) -> list[RlweCiphertext]:
+    """Pack 2^k public values mod p into trivial ciphertexts (hw/lut.py:86-97)."""
+    values = np.asarray(values, dtype=np.int64)
+    size = len(values)
+    if size < 1 or size & (size - 1):
+        raise TfheError("LUT size must be a power of two")
+    n = params.n
+    if size >= n:
+        return [tfhe.trivial_rlwe(values[i: i + n], params) for i in range(0, size, n)]
+    return [tfhe.trivial_rlwe(values, params)]
+
+
+def vertical_packing(bits: list[SelectorBit], lut: list[RlweCiphertext]):
+    """hw/lut.py:122-149 for one selector vector: LWE (N+1,) of lut[m]."""
+    params = lut[0].params
+    k = len(bits)
+    if max(1, (1 << k) // params.n) != len(lut):
+        raise TfheError(f"selector arity {k} does not match a LUT of {len(lut)} polynomials")
+    a, b = vp_batch([bits], [np.stack([np.asarray(c.data) for c in lut])], params)
+    return np.concatenate([a[0], [b[0]]]).astype(np.uint32)
+
+
+def inverse_vertical_packing(bits: list[SelectorBit], payload: RlweCiphertext) -> list[RlweCiphertext]:
+    """hw/lut.py:152-189: deposit the payload at the selected entry."""
+    rows = ivp_batch([bits], payload.data, payload.params)[0]
+    return [RlweCiphertext(payload.params, r) for r in rows]
+
+
+def cdemux(C: RgswCiphertext, d: RlweCiphertext) -> tuple[RlweCiphertext, RlweCiphertext]:
+    """hw/lut.py:113-119."""
+    lo, hi = tfhe.cdemux_batch(d.params, C.spectra(), np.asarray(d.data)[None])
+    return RlweCiphertext(d.params, lo[0]), RlweCiphertext(d.params, hi[0])

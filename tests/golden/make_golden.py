@@ -154,6 +154,34 @@ def gen_pbs(name, count, key_seed=1, enc_seed=2):
         sha_ksk=sha(keys["ksk"]))
 
 
+sys.path.insert(0, HERE)
+from cases import TRAIN_CASES, train_inputs  # noqa: E402
+
+
+def gen_train(name):
+    """Encrypted WiSARD training by the REFERENCE's he_train (hw/hewnn.py:189)
+    on embedded q = 2^32 RGSW inputs."""
+    from hewisard import hewnn as rh
+    from hewisard import wnn as rw
+    P, s1, bits, labels, stacks = train_inputs(name)
+    (s, l, a, r) = TRAIN_CASES[name][2]
+    g = P.gadget
+    RP = ref_params(P.degree_log, g.levels, g.base_log, p=P.p)
+    geom = rw.WisardGeometry(s=s, l=l, a=a, r=r, p=P.p)
+    samples = [rh.EncryptedSample(RP, [rt.RgswCiphertext(RP, emb(x)) for x in st[:s]],
+                                  [rt.RgswCiphertext(RP, emb(x)) for x in st[s:]]) for st in stacks]
+    model = rh.he_train(samples, geom, RP)
+    rams, counts = unemb(model.rams), unemb(model.counts_ct)
+    # sanity: the reference's own decryption equals its plaintext trainer
+    key = rt.SecretKey(RP, s1.astype(np.uint64))
+    plain, cc = rh.decrypt_model(model, key)
+    ref_int, ref_counts = rw.train_integer(bits, labels, geom)
+    assert np.array_equal(plain.counters, ref_int.counters) and np.array_equal(cc.counts, ref_counts.counts)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), rams_head=rams[:, :2], counts_ct=counts,
+                        sha_rams=sha(rams), sha_stacks=sha(*stacks), counters=ref_int.counters,
+                        class_counts=ref_counts.counts, bits=bits, labels=labels)
+
+
 def main():
     rng = np.random.default_rng(20240329)
     t = time.time()
@@ -166,6 +194,10 @@ def main():
         t = time.time()
         gen_pbs(name, count)
         print(f"pbs {name}: {time.time() - t:.1f}s", flush=True)
+    for name in TRAIN_CASES:
+        t = time.time()
+        gen_train(name)
+        print(f"{name}: {time.time() - t:.1f}s", flush=True)
 
 
 if __name__ == "__main__":

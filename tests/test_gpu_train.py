@@ -1,0 +1,133 @@
+"""GPU parity for encrypted WiSARD training/LUT evaluation: the device
+IVP/VP engine and he_train vs the reference-generated fixtures and the oracle."""
+
+import hashlib
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN, assert_u32_equal, golden
+from oracle import tfhe32 as o
+from oracle import wnn32
+from paper_2403_20190_b200 import hewnn, lut, tfhe, wnn
+from paper_2403_20190_b200.params import named_params
+
+sys.path.insert(0, GOLDEN)
+from cases import TRAIN_CASES, train_inputs  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def samples_of(name, device=True):
+    P, s1, bits, labels, stacks = train_inputs(name)
+    s, l, a, r = TRAIN_CASES[name][2]
+    lb = max(1, (l - 1).bit_length())
+    smp = [hewnn.EncryptedSample(P, tfhe.to_device(st) if device else st, s, lb) for st in stacks]
+    return P, s1, bits, labels, smp, wnn.WisardGeometry(s, l, a, r, P.p)
+
+
+@pytest.mark.parametrize("name", sorted(TRAIN_CASES))
+@pytest.mark.parametrize("batch", [1, 16])
+def test_he_train_matches_reference(name, batch):
+    g = golden(f"{name}.npz")
+    P, s1, bits, labels, smp, geom = samples_of(name)
+    model = hewnn.he_train(smp, geom, P, batch=batch)
+    rams = tfhe.to_host(model.rams)
+    assert sha(rams) == str(g["sha_rams"])
+    assert_u32_equal(rams[:, :2], g["rams_head"])
+    assert_u32_equal(tfhe.to_host(model.counts_ct), g["counts_ct"])
+    counters, cc = hewnn.decrypt_model(model, tfhe.SecretKey(P, s1))
+    assert np.array_equal(counters, g["counters"])
+    assert np.array_equal(cc.counts, g["class_counts"])
+
+
+def test_continuous_training_and_merge():
+    name = "train_cfg1"
+    P, s1, bits, labels, smp, geom = samples_of(name)
+    full = hewnn.he_train(smp, geom, P)
+    part = hewnn.he_train(smp[:1], geom, P)
+    cont = hewnn.he_train(smp[1:], geom, P, model=part.copy())               # hw/hewnn.py:189-202
+    assert torch.equal(cont.rams, full.rams) and torch.equal(cont.counts_ct, full.counts_ct)
+    other = hewnn.he_train(smp[1:], geom, P)
+    merged = hewnn.he_merge(part, other)                                    # hw/hewnn.py:264-271
+    assert torch.equal(merged.rams, full.rams) and torch.equal(merged.counts_ct, full.counts_ct)
+
+
+def test_device_rgsw_encryption_matches_host():
+    P = named_params("CFG2", 256)
+    key = tfhe.SecretKey(P, tfhe.make_rng(3).integers(0, 2, P.n).astype(np.uint32))
+    ms = tfhe.make_rng(4).integers(0, 2, 37)
+    host = np.stack([c.data for c in tfhe.enc_rgsw_batch(ms, key, tfhe.make_rng(5))])
+    dev = hewnn.enc_rgsw_batch_device(ms, key, tfhe.make_rng(5))
+    assert_u32_equal(tfhe.to_host(dev), host)
+    P4 = named_params("CFG4")
+    key4 = tfhe.SecretKey(P4, tfhe.make_rng(3).integers(0, 2, P4.n).astype(np.uint32))
+    host4 = np.stack([c.data for c in tfhe.enc_rgsw_batch(ms[:5], key4, tfhe.make_rng(6))])
+    assert_u32_equal(tfhe.to_host(hewnn.enc_rgsw_batch_device(ms[:5], key4, tfhe.make_rng(6))), host4)
+
+
+def _random_codes(rng, B, k, R, clear_frac=0.25):
+    codes = rng.integers(0, R, (B, k))
+    mask = rng.random((B, k)) < clear_frac
+    codes[mask] = rng.choice([lut.CLEAR0, lut.CLEAR1], size=mask.sum())
+    return codes
+
+
+@pytest.mark.parametrize("k", [4, 12, 13])
+def test_ivp_vp_codes_vs_oracle(k):
+    """Random selector matrices mixing encrypted and clear bits, tree (k > 10)
+    and rotation-only (k <= 10) shapes."""
+    P = named_params("CFG2", 256)
+    rng = np.random.default_rng(k)
+    R = 6
+    table = rng.integers(0, 1 << 32, (R, 6, 2, P.n), dtype=np.uint64).astype(np.uint32)
+    payload = rng.integers(0, 1 << 32, (2, P.n), dtype=np.uint64).astype(np.uint32)
+    codes = _random_codes(rng, 5, k, R)
+    ntt = tfhe.rgsw_to_ntt(P, table)
+    got = tfhe.to_host(lut.ivp_codes(P, codes, ntt, payload))
+    want = wnn32.ivp_batch(codes, table, payload, 3, 7, P.degree_log)
+    assert_u32_equal(got, want)
+    z = lut.tree_depth(k, P)
+    luts = rng.integers(0, 1 << 32, (3, max(1, 1 << z), 2, P.n), dtype=np.uint64).astype(np.uint32)
+    lut_idx = rng.integers(0, 3, 5)
+    vcodes = _random_codes(rng, 5, k, R)
+    vcodes[:, 0] = lut.CLEAR1                       # exercise the clear-prefix slicing
+    got = tfhe.to_host(lut.vp_codes(P, vcodes, ntt, tfhe.to_device(luts), lut_idx))
+    want = wnn32.vp_batch(vcodes, table, luts[lut_idx], 3, 7, P.degree_log)
+    assert_u32_equal(got, want)
+
+
+def test_lut_roundtrip_decrypts():
+    """VP(IVP(payload)) exposes the payload at the selected entry (pkg/tests/test_lut.py:170-181)."""
+    P = named_params("CFG2", 256)
+    key = tfhe.SecretKey(P, tfhe.make_rng(8).integers(0, 2, P.n).astype(np.uint32))
+    rng = tfhe.make_rng(9)
+    k = 12
+    for m in (0, 1, 1023, 1024, 4095):
+        bits = [(m >> (k - 1 - i)) & 1 for i in range(2)] + [(m >> w) & 1 for w in range(10)]
+        sel = [lut.SelectorBit.enc(c) for c in tfhe.enc_rgsw_batch(bits, key, rng)]
+        assert lut.selector_index(bits, k, P) == m
+        rows = lut.ivp_batch([sel], tfhe.trivial_rlwe(5, P).data, P)[0]        # (4, 2, N)
+        dec = np.concatenate([tfhe.dec_rlwe(tfhe.RlweCiphertext(P, r), key) for r in rows])
+        expect = np.zeros(4 * P.n, dtype=np.int64)
+        expect[m] = 5
+        assert np.array_equal(dec, expect)
+        out = lut.vertical_packing(sel, [tfhe.RlweCiphertext(P, r) for r in rows])
+        assert tfhe.dec_lwe_batch(out[None], key)[0] == 5
+
+
+def test_monomial_gather_vs_oracle():
+    P = named_params("CFG2")
+    rng = np.random.default_rng(3)
+    x = rng.integers(0, 1 << 32, (6, 2, P.n), dtype=np.uint64).astype(np.uint32)
+    es = np.array([0, 1, -1, 2047, 3000, -5000])
+    assert_u32_equal(lut.monomial_gather(P, x, es), o.monomial_gather(x, es))
