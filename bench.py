@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="PBS per CPU step (0 = auto)")
+    ap.add_argument("--train-cfg", type=int, default=3, choices=[1, 3, 4, 5])
+    ap.add_argument("--train-images", type=int, default=32, help="0 disables the training measurement")
+    ap.add_argument("--train-batch", type=int, default=16)
     return ap.parse_args()
 
 
@@ -172,6 +175,83 @@ def probe_modmul_peak(torch, _lib, tfhe):
     return best
 
 
+def bench_train(args, world, rank, torch, dist):
+    """Encrypted WiSARD training throughput (the metric's second half):
+    hewnn.he_train over `--train-images` client-encrypted images of BASELINE
+    config `--train-cfg` (default 3), inputs device-resident (value) and from
+    pinned host memory with H2D/D2H inside the timed region (e2e)."""
+    from paper_2403_20190_b200 import data, hewnn, tfhe, wnn
+    from paper_2403_20190_b200.params import named_params
+    cfg, images, batch = args.train_cfg, args.train_images, args.train_batch
+    (s, l, a, r, p), pname = data.CONFIG_GEOMETRY[cfg]
+    P = named_params(pname, p)
+    geom = wnn.WisardGeometry(s, l, a, r, p)
+    ds = data.config_dataset(cfg, n=images, seed=rank)
+    key = tfhe.SecretKey(P, tfhe.make_rng(KEY_SEED).integers(0, 2, P.n).astype(np.uint32))
+    rng = tfhe.make_rng(ENC_SEED + 1000 * rank)
+    t0 = time.perf_counter()
+    samples = [hewnn.encrypt_sample(ds.bits[i], int(ds.labels[i]), key, rng, label_bits=geom.label_bits)
+               for i in range(images)]
+    torch.cuda.synchronize()
+    enc_s = time.perf_counter() - t0
+    hewnn.he_train(samples[:batch], geom, P, batch=batch)                    # warm-up
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    model = hewnn.he_train(samples, geom, P, batch=batch)
+    e1.record()
+    e1.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    counters, cc = hewnn.decrypt_model(model, key)
+    ref, rc = wnn.train_integer(ds.bits, ds.labels, geom)
+    ok = bool(np.array_equal(counters, ref) and np.array_equal(cc.counts, rc.counts))
+    # end to end from pinned host ciphertexts, model read back
+    host = [hewnn.EncryptedSample(P, smp.rgsw.cpu().pin_memory(), smp.s, smp.label_bits) for smp in samples]
+    h2d = sum(int(h.rgsw.numel()) * 4 for h in host)
+    rams_pin = torch.empty(model.rams.shape, dtype=torch.int32).pin_memory()
+    del samples
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    m2 = hewnn.he_train(host, geom, P, batch=batch)
+    rams_pin.copy_(m2.rams, non_blocking=True)
+    f1.record()
+    f1.synchronize()
+    te = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    k1 = hewnn.model_row_polys(geom, P)
+    lb = geom.label_bits
+    ext_per_img = geom.k0 * (min(lb + geom.a, P.degree_log) + (1 << max(0, lb + geom.a - P.degree_log)) - 1) + lb
+    out = {"metric": "encrypted train images/sec", "unit": "images/s",
+           "value": round(images * world / (float(t.item()) * 1e-3), 2),
+           "config": {"workload": f"BASELINE cfg{cfg} encrypted WiSARD training (he_train)",
+                      "params": pname, "p": p, "geometry": {"s": s, "l": l, "a": a, "r": r, "k0": geom.k0,
+                                                            "k1": k1}, "images_per_gpu": images,
+                      "batch_images": batch, "ext_products_per_image": ext_per_img,
+                      "data": "synthetic (data.config_dataset)"},
+           "e2e": {"value": round(images * world / (float(te.item()) * 1e-3), 2), "unit": "images/s",
+                   "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(model.rams.numel()) * 4,
+                   "api": "hewnn.he_train from pinned host RGSW stacks, model read back"},
+           "client_encrypt_s_per_image": round(enc_s / images, 4),
+           "check": "decrypted counters == train_integer" if ok else "COUNTER MISMATCH"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import coracle, wnn32
+        coracle.build()
+        n_cpu = min(2, images)
+        stacks = [np.asarray(tfhe.to_host(h.rgsw)) for h in host[:n_cpu]]
+        c0 = time.perf_counter()
+        wnn32.he_train(stacks, s, l, a, r, P)
+        dt = time.perf_counter() - c0
+        out["cpu_baseline"] = {"value": round(n_cpu / dt, 4), "unit": "images/s", "cores": cpu_threads(),
+                               "kind": "port", "sample": f"{n_cpu} cfg{cfg} images, oracle/wnn32.he_train "
+                                                         f"(C oracle exact ext products, OpenMP)"}
+    return out
+
+
 def bench_hwb(args):
     import torch
     import torch.distributed as dist
@@ -295,6 +375,8 @@ def bench_hwb(args):
             "sample": f"{sample} cfg2 PBS of the same batch (oracle/c exact schoolbook, "
                       f"OpenMP {threads} threads, {cpu_model()})",
             "bit_exact_vs_gpu": bool(np.array_equal(ref_out, out_h[:sample]))}
+    if args.train_images > 0:
+        result["train"] = bench_train(args, world, rank, torch, dist)
     if world > 1:
         dist.destroy_process_group()
     if rank == 0:

@@ -217,7 +217,7 @@ def _payload(params: HeParams) -> np.ndarray:
 
 
 def _stack_table(params: HeParams, samples: list[EncryptedSample]):
-    rg = [s.rgsw if isinstance(s.rgsw, torch.Tensor) else tfhe.to_device(s.rgsw) for s in samples]
+    rg = [tfhe.to_device(s.rgsw) for s in samples]      # H2D (non-blocking) for host tensors
     big = rg[0] if len(rg) == 1 else torch.cat(rg)
     return tfhe.rgsw_to_ntt(params, big)
 

@@ -4,8 +4,9 @@ Mirrors the parts of the reference's `hewisard.wnn` (`pkg/src/hewisard/wnn.py`)
 that encrypted training/inference and the client need: geometry
 (`wnn.py:26-60`), the recorded-PRNG permutation (`wnn.py:189-196`), addresses
 (`wnn.py:209-219`), thermometer encoding (`wnn.py:158-182`) and the activation /
-balancing / argmax tail (`wnn.py:86-109, 241-293`).  Plaintext training
-(`train_integer`) is not part of the accelerated path; it lives in the oracle.
+balancing / argmax tail (`wnn.py:86-109, 241-293`), and the plaintext integer
+trainer/evaluator (`wnn.py:222-238, 296-309`) that a decrypted model is checked
+against.  The plaintext WiSARD is not part of the accelerated path.
 """
 
 from __future__ import annotations
@@ -151,6 +152,37 @@ def addresses(bits: np.ndarray, geometry: WisardGeometry) -> np.ndarray:
     return px @ (1 << np.arange(geometry.a, dtype=np.int64))
 
 
+def train_integer(bits: np.ndarray, labels: np.ndarray, geometry: WisardGeometry):
+    """Plaintext integer WiSARD (hw/wnn.py:222-238): counters (l, k0, 2^a) mod p
+    and class counts -- what a correctly trained encrypted model decrypts to."""
+    labels = np.asarray(labels, dtype=np.int64)
+    counters = np.zeros((geometry.l, geometry.k0, 1 << geometry.a), dtype=np.int64)
+    counts = ClassCounts(np.zeros(geometry.l, dtype=np.int64))
+    if labels.size == 0:
+        return counters, counts
+    if labels.max() >= geometry.l:
+        raise WnnError(f"label {labels.max()} out of range for {geometry.l} classes")
+    addr = addresses(bits, geometry)
+    rams = np.broadcast_to(np.arange(geometry.k0), addr.shape)
+    lab = np.broadcast_to(labels[:, np.newaxis], addr.shape)
+    np.add.at(counters, (lab, rams, addr), 1)
+    counters &= geometry.p - 1
+    counts.counts += np.bincount(labels, minlength=geometry.l)
+    return counters, counts
+
+
+def evaluate_dataset(counters: np.ndarray, geometry: WisardGeometry, bits: np.ndarray, spec: ActivationSpec,
+                     counts: ClassCounts | None = None) -> np.ndarray:
+    """Predicted classes for many samples (hw/wnn.py:296-309)."""
+    x = counters.astype(np.float64)
+    if counts is not None:
+        x = x * rescale_factors(counts, geometry.l)[:, None, None]
+    act_t = np.ascontiguousarray(spec.apply(x).transpose(1, 2, 0))          # (k0, 2^a, l)
+    addr = addresses(bits, geometry)
+    gathered = act_t[np.arange(geometry.k0)[None, :], addr, :]
+    return np.argmax(gathered.sum(axis=1), axis=1)
+
+
 def rescale_factors(counts: ClassCounts, l: int) -> np.ndarray:
     """hw/wnn.py:241-247."""
     c = counts.counts.astype(np.float64)
@@ -174,4 +206,5 @@ def predict_from_lookups(raw: np.ndarray, spec: ActivationSpec, counts: ClassCou
 
 __all__ = ["WnnError", "WisardGeometry", "ClassCounts", "ActivationSpec", "thermometer_thresholds",
            "thermometer_encode", "encode_bits", "quantize_tabular", "permutation", "addresses",
-           "rescale_factors", "scores_from_lookups", "predict_from_lookups"]
+           "rescale_factors", "scores_from_lookups", "predict_from_lookups", "train_integer",
+           "evaluate_dataset"]
