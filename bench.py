@@ -47,8 +47,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="PBS per CPU step (0 = auto)")
     ap.add_argument("--train-cfg", type=int, default=3, choices=[1, 3, 4, 5])
-    ap.add_argument("--train-images", type=int, default=32, help="0 disables the training measurement")
-    ap.add_argument("--train-batch", type=int, default=16)
+    ap.add_argument("--train-images", type=int, default=64, help="0 disables the training measurement")
+    ap.add_argument("--train-batch", type=int, default=32)
     return ap.parse_args()
 
 
@@ -207,6 +207,8 @@ def bench_train(args, world, rank, torch, dist):
     counters, cc = hewnn.decrypt_model(model, key)
     ref, rc = wnn.train_integer(ds.bits, ds.labels, geom)
     ok = bool(np.array_equal(counters, ref) and np.array_equal(cc.counts, rc.counts))
+    noise, margin = hewnn.model_noise(model, key)
+    frac_ok = float(np.mean(counters == ref))
     # end to end from pinned host ciphertexts, model read back
     host = [hewnn.EncryptedSample(P, smp.rgsw.cpu().pin_memory(), smp.s, smp.label_bits) for smp in samples]
     h2d = sum(int(h.rgsw.numel()) * 4 for h in host)
@@ -237,6 +239,8 @@ def bench_train(args, world, rank, torch, dist):
                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(model.rams.numel()) * 4,
                    "api": "hewnn.he_train from pinned host RGSW stacks, model read back"},
            "client_encrypt_s_per_image": round(enc_s / images, 4),
+           "noise": {"max_log2": round(float(np.log2(max(noise, 1))), 2),
+                     "margin_log2": round(float(np.log2(margin)), 2), "counters_correct": round(frac_ok, 6)},
            "check": "decrypted counters == train_integer" if ok else "COUNTER MISMATCH"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import coracle, wnn32

@@ -293,6 +293,17 @@ def decrypt_counts(counts_ct, params: HeParams, l: int, key: tfhe.SecretKey) -> 
     return ClassCounts(vals[:l].astype(np.int64))
 
 
+def model_noise(model: HomWisardModel, key: tfhe.SecretKey) -> tuple[int, int]:
+    """Max |phase - nearest codeword| over every model coefficient and the
+    decryption margin q/(2p) (hw/tfhe.py:446-473 measure_noise)."""
+    params = model.params
+    rams = tfhe.to_host(model.rams)
+    phase = (rams[:, :, 1] - tfhe._key_mul_host(rams[:, :, 0], key.s)).astype(np.int64)
+    delta = params.delta
+    err = (phase + delta // 2) % delta - delta // 2
+    return int(np.abs(err).max()), delta // 2
+
+
 def decrypt_model(model: HomWisardModel, key: tfhe.SecretKey):
     """Decrypt the RLWE matrix into integer counters (l, k0, 2^a) and class counts."""
     g, params = model.geometry, model.params
