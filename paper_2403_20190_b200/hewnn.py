@@ -271,6 +271,18 @@ def he_train(samples: Iterable[EncryptedSample], geometry: WisardGeometry, param
     return model
 
 
+def he_train_sharded(samples: Sequence[EncryptedSample], geometry: WisardGeometry, params: HeParams,
+                     rank: int, world: int, group=None, batch: int = 16) -> HomWisardModel:
+    """Multi-GPU training: rank trains the stripe samples[rank::world] (the
+    reference's thread stripes, hw/hewnn.py:216-229) and the partial models are
+    summed mod 2^32 across ranks -- bit-identical to he_train on all samples."""
+    from . import distributed
+    model = he_train(distributed.stripe(list(samples), rank, world), geometry, params, batch=batch)
+    if world > 1:
+        distributed.merge_models_(model.rams, model.counts_ct, group)
+    return model
+
+
 def he_merge(m1: HomWisardModel, m2: HomWisardModel) -> HomWisardModel:
     """Federated merge: entry-wise RLWE addition (hw/hewnn.py:264-271)."""
     if m1.geometry != m2.geometry:
