@@ -131,6 +131,18 @@ int hwb_key_mul(const hwb_params *p, const uint32_t *key_ntt, const uint32_t *in
  * ciphertexts [B][2l][2][N] for selector bits[B] in {0, 1}. */
 int hwb_rgsw_add_gadget(const hwb_params *p, uint32_t *rgsw, const int32_t *bits, int64_t B, void *stream);
 
+/* Packing key switch (hw/tfhe.py:390-439 pack_batch): B outputs, each packing
+ * up to N extracted LWEs into one RLWE whose coefficient i carries LWE i:
+ *   out[b] = (-sum_{j,t} D_{j,t} (*) K[j,t,0],  b_polys[b] - sum_{j,t} D_{j,t} (*) K[j,t,1]),
+ *   D_{j,t}(X) = sum_i digit_t(a^(i)_j) X^i  (gadget `levels` x `base_log`).
+ * ksk_ntt: hwb_poly_to_ntt of the packing key [N][levels][2][N] (N*levels*2 polys);
+ * apolys: [B][N][N] with apolys[b][j][i] = a^(i)_j (zero for i >= number of LWEs);
+ * b_polys: [B][N]; out: [B][2][N]; workspace: hwb_pack_ks_workspace_bytes. */
+size_t hwb_pack_ks_workspace_bytes(const hwb_params *p, int64_t B);
+int hwb_pack_ks(const hwb_params *p, int32_t levels, int32_t base_log, const uint32_t *ksk_ntt,
+                const uint32_t *apolys, const uint32_t *b_polys, uint32_t *out, int64_t B, void *workspace,
+                void *stream);
+
 /* dst[k] += (negate ? -1 : 1) * src[k mod src_words] mod 2^32 for k < words: exact
  * ciphertext addition for model accumulation and federated merge
  * (hw/hewnn.py:213, 264-271). */

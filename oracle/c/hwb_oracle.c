@@ -175,6 +175,44 @@ void orc_keyswitch(int N, int n, int lks, int wks, const uint32_t *ksk, const ui
         keyswitch_one(N, n, lks, wks, ksk, in + b * (N + 1), out + b * (n + 1));
 }
 
+/* Packing key switch, hw/tfhe.py:390-420 (exact branch): for output b,
+ * acc[c] = sum_{j<N} sum_{t<l} D_{j,t} (*) ksk[j][t][c] with D_{j,t}(X) =
+ * sum_{i<k} digit_t(a^(i)_j) X^i; out = (-acc[0], b_poly - acc[1]).
+ * ksk (N, l, 2, N); a_stacks (B, k, N); b_polys (B, N); out (B, 2, N). */
+void orc_pack_ks(int N, int levels, int w, const uint32_t *ksk, const uint32_t *a_stacks,
+                 const uint32_t *b_polys, uint32_t *out, int64_t B, int k, int nthreads)
+{
+    set_threads(nthreads);
+#pragma omp parallel
+    {
+        uint32_t *acc = (uint32_t *)malloc(sizeof(uint32_t) * 2 * N);
+        int32_t d[32];
+#pragma omp for schedule(dynamic)
+        for (int64_t b = 0; b < B; ++b) {
+            memset(acc, 0, sizeof(uint32_t) * 2 * N);
+            for (int j = 0; j < N; ++j)
+                for (int i = 0; i < k; ++i) {
+                    decompose(a_stacks[((size_t)b * k + i) * N + j], levels, w, d);
+                    for (int t = 0; t < levels; ++t) {
+                        uint32_t dt = (uint32_t)d[t];
+                        if (!dt) continue;
+                        for (int c = 0; c < 2; ++c) {   /* acc[c] += dt X^i (*) K */
+                            const uint32_t *K = ksk + (((size_t)j * levels + t) * 2 + c) * N;
+                            uint32_t *o = acc + c * N;
+                            for (int m = 0; m < N - i; ++m) o[i + m] += dt * K[m];
+                            for (int m = N - i; m < N; ++m) o[i + m - N] -= dt * K[m];
+                        }
+                    }
+                }
+            for (int m = 0; m < N; ++m) {
+                out[(size_t)b * 2 * N + m] = 0u - acc[m];
+                out[(size_t)b * 2 * N + N + m] = b_polys[(size_t)b * N + m] - acc[N + m];
+            }
+        }
+        free(acc);
+    }
+}
+
 /* NEW: mod switch round(x 2N / q) mod 2N (rounding idiom hw/ring.py:139-140). */
 static int32_t mod_switch(uint32_t x, int N)
 {

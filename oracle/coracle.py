@@ -39,6 +39,7 @@ def lib():
         L.orc_keyswitch.argtypes = [i, i, i, i, _u32p, _u32p, _u32p, i64, i]
         L.orc_pbs.argtypes = [i, i, i, i, i, i, _u32p, _u32p, _u32p, i, _u32p, _u32p, i64, i, i]
         L.orc_max_threads.restype = i
+        L.orc_pack_ks.argtypes = [i, i, i, _u32p, _u32p, _u32p, _u32p, i64, i, i]
         _lib = L
     return _lib
 
@@ -82,6 +83,15 @@ def keyswitch(lwe, ksk, levels, base_log, nthreads=0):
     n = ksk.shape[-1] - 1
     out = np.empty((B, n + 1), dtype=np.uint32)
     lib().orc_keyswitch(N, n, levels, base_log, _p(ksk), _p(lwe), _p(out), B, nthreads)
+    return out
+
+
+def pack_batch(a_stacks, b_polys, ksk, levels, base_log, nthreads=0):
+    """hw/tfhe.py:390-420 exact: a_stacks (B, k, N), b_polys (B, N), ksk (N, l, 2, N)."""
+    a_stacks, b_polys, ksk = _u32(a_stacks), _u32(b_polys), _u32(ksk)
+    B, k, N = a_stacks.shape
+    out = np.empty((B, 2, N), dtype=np.uint32)
+    lib().orc_pack_ks(N, levels, base_log, _p(ksk), _p(a_stacks), _p(b_polys), _p(out), B, k, nthreads)
     return out
 
 

@@ -350,6 +350,27 @@ def pbs_keygen(params, rng_seed) -> dict:
     return dict(s0=s0, s1=s1, bsk=bsk, ksk=ksk)
 
 
+def keygen_packing(params, rng_seed) -> tuple[np.ndarray, np.ndarray]:
+    """hw/tfhe.py:95-114 at q = 2^32: S1 and the packing key-switch key
+    (N, l, 2, N), in the reference's chunked RNG order."""
+    rng = make_rng(rng_seed)
+    n = params.n
+    s = rng.integers(0, 2, n).astype(U32)
+    g = params.gadget_pks
+    ksk = np.empty((n, g.levels, 2, n), dtype=U32)
+    step = max(1, 2 ** 20 // (g.levels * n))
+    for j0 in range(0, n, step):
+        j1 = min(n, j0 + step)
+        a = uniform_u32(rng, (j1 - j0, g.levels, n))
+        e = gaussian_u32(rng, params.sigma, (j1 - j0, g.levels, n))
+        b = (key_mul(a, s) + e).astype(U32)
+        for t in range(g.levels):
+            b[:, t, 0] += s[j0:j1] * U32(1 << (Q_BITS - (t + 1) * g.base_log))
+        ksk[j0:j1, :, 0, :] = a
+        ksk[j0:j1, :, 1, :] = b
+    return s, ksk
+
+
 def mod_switch(x, n_ring: int) -> np.ndarray:
     """NEW: round(x * 2N / q) mod 2N with the rounding idiom of hw/ring.py:139-140."""
     logm = (2 * n_ring).bit_length() - 1

@@ -21,7 +21,7 @@ EXPORTS = (
     "hwb_ggsw_to_ntt", "hwb_ext_product", "hwb_cmux", "hwb_cdemux", "hwb_blind_rotate",
     "hwb_sample_extract", "hwb_keyswitch", "hwb_pbs_workspace_bytes", "hwb_pbs",
     "hwb_ivp_level", "hwb_vp_level", "hwb_monomial_gather", "hwb_accumulate",
-    "hwb_poly_to_ntt", "hwb_key_mul", "hwb_rgsw_add_gadget",
+    "hwb_poly_to_ntt", "hwb_key_mul", "hwb_rgsw_add_gadget", "hwb_pack_ks_workspace_bytes", "hwb_pack_ks",
 )
 
 
@@ -81,9 +81,12 @@ def load() -> ctypes.CDLL:
         L.hwb_poly_to_ntt.argtypes = [_pp, _vp, _vp, _i64, _vp]
         L.hwb_key_mul.argtypes = [_pp, _vp, _vp, _vp, _vp, _i64, _vp]
         L.hwb_rgsw_add_gadget.argtypes = [_pp, _vp, _vp, _i64, _vp]
+        L.hwb_pack_ks_workspace_bytes.argtypes = [_pp, _i64]
+        L.hwb_pack_ks_workspace_bytes.restype = ctypes.c_size_t
+        L.hwb_pack_ks.argtypes = [_pp, ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp, _vp, _i64, _vp, _vp]
         for name in EXPORTS:
             if name not in ("hwb_version", "hwb_last_error", "hwb_ggsw_ntt_words",
-                            "hwb_pbs_workspace_bytes", "hwb_probe_modmul"):
+                            "hwb_pbs_workspace_bytes", "hwb_probe_modmul", "hwb_pack_ks_workspace_bytes"):
                 getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib

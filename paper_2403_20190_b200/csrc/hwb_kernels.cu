@@ -551,6 +551,117 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS) key_mul_kernel(const uint32_t
   }
 }
 
+// Packing key switch (hw/tfhe.py:390-439 pack_batch), phase 1: for output b
+// and a chunk of key rows j, accumulate in the NTT domain
+//   sum_{j in chunk} sum_t D_{j,t} * KSK[j,t][c],  D_{j,t}(X) = sum_i digit_t(a^(i)_j) X^i,
+// where apolys[b][j][i] = a^(i)_j (the transposed a-stack, zero past k).
+// Partial sums (both components, this CTA's prime) go to part[b][chunk][c][prime][N].
+template <int N>
+__global__ void __launch_bounds__(Cfg<N>::THREADS) pack_ks_partial_kernel(
+    const uint32_t *__restrict__ apolys, const uint32_t *__restrict__ ksk_ntt, uint32_t *part, int rows_j,
+    Gadget gk, Tw tw) {
+  constexpr int TPP = Cfg<N>::TPP;
+  constexpr int C = N / TPP;
+  __shared__ uint32_t scr[2][N];
+  const int64_t b = blockIdx.y;
+  const int chunk = blockIdx.x, nchunks = gridDim.x;
+  const Who<N> me;
+  const int w = me.grp, t = me.t;
+  const uint32_t p = c_prime[w].p, two_p = 2 * p, pinv = c_prime[w].pinv;
+  const uint32_t off = p - gk.half;
+  const int L = (int)gk.levels;
+  const uint2 *twf = w ? tw.fwd[1] : tw.fwd[0];
+  uint32_t a0[C], a1[C], v[C], x[C];
+#pragma unroll
+  for (int j = 0; j < C; ++j) a0[j] = a1[j] = 0;
+  const int j0 = chunk * rows_j, j1 = min(N, j0 + rows_j);
+#pragma unroll 1
+  for (int jr = j0; jr < j1; ++jr) {
+    const uint32_t *src = apolys + ((int64_t)b * N + jr) * N + t;
+#pragma unroll
+    for (int jj = 0; jj < C; ++jj) v[jj] = decomp_prep(src[TPP * jj], gk);
+#pragma unroll 1
+    for (int tt = 0; tt < L; ++tt) {
+      const uint32_t sh = gk.base_log * (uint32_t)(L - 1 - tt);
+#pragma unroll
+      for (int jj = 0; jj < C; ++jj) x[jj] = ((v[jj] >> sh) & gk.mask) + off;
+      fwd_ntt<N, TPP, -1>(x, scr[w], me.lay, t, w, twf);
+      const uint32_t *k0 = ksk_ntt + (((size_t)(jr * L + tt) * 2 + 0) * 2 + w) * N;
+      const uint32_t *k1 = ksk_ntt + (((size_t)(jr * L + tt) * 2 + 1) * 2 + w) * N;
+#pragma unroll
+      for (int jq = 0; jq < C / 4; ++jq) {
+        const uint4 K0 = __ldg(slice_vec<TPP>(k0, t, jq));
+        const uint4 K1 = __ldg(slice_vec<TPP>(k1, t, jq));
+        const uint32_t k0v[4] = {K0.x, K0.y, K0.z, K0.w}, k1v[4] = {K1.x, K1.y, K1.z, K1.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t u0 = a0[4 * jq + q] + mont_mul(x[4 * jq + q], k0v[q], p, pinv);
+          uint32_t u1 = a1[4 * jq + q] + mont_mul(x[4 * jq + q], k1v[q], p, pinv);
+          a0[4 * jq + q] = umin(u0, u0 - two_p);
+          a1[4 * jq + q] = umin(u1, u1 - two_p);
+        }
+      }
+    }
+  }
+  uint4 *o0 = reinterpret_cast<uint4 *>(part + ((((int64_t)b * nchunks + chunk) * 2 + 0) * 2 + w) * N);
+  uint4 *o1 = reinterpret_cast<uint4 *>(part + ((((int64_t)b * nchunks + chunk) * 2 + 1) * 2 + w) * N);
+#pragma unroll
+  for (int jq = 0; jq < C / 4; ++jq) {
+    o0[jq * TPP + t] = make_uint4(a0[4 * jq], a0[4 * jq + 1], a0[4 * jq + 2], a0[4 * jq + 3]);
+    o1[jq * TPP + t] = make_uint4(a1[4 * jq], a1[4 * jq + 1], a1[4 * jq + 2], a1[4 * jq + 3]);
+  }
+}
+
+// Packing key switch phase 2: each chunk's partial sum is bounded (rows_j *
+// levels * N * beta/2 * 2^31 < P/2), so it is inverse-transformed and CRT-lifted
+// on its own; the lifted chunks are added mod 2^32 and
+// out[b] = (-acc_a, b_poly - acc_b) (hw/tfhe.py:418-419).
+template <int N>
+__global__ void __launch_bounds__(Cfg<N>::THREADS) pack_ks_finish_kernel(const uint32_t *__restrict__ part,
+                                                                         int nchunks,
+                                                                         const uint32_t *__restrict__ b_polys,
+                                                                         uint32_t *out, Tw tw) {
+  constexpr int TPP = Cfg<N>::TPP, NT = Cfg<N>::THREADS;
+  constexpr int C = N / TPP;
+  constexpr int PER = 2 * N / NT;   // output words per thread
+  __shared__ uint32_t scr[2][N];
+  __shared__ uint32_t ex[2][2][N];   // [comp][prime][i]
+  const int64_t b = blockIdx.x;
+  const Who<N> me;
+  const int w = me.grp, t = me.t;
+  const uint32_t p = c_prime[w].p;
+  uint32_t x[C], acc[PER];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) acc[k] = 0;
+#pragma unroll 1
+  for (int ch = 0; ch < nchunks; ++ch) {
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      const uint32_t *src = part + ((((int64_t)b * nchunks + ch) * 2 + c) * 2 + w) * N;
+#pragma unroll
+      for (int jq = 0; jq < C / 4; ++jq) {
+        const uint4 P4 = __ldg(slice_vec<TPP>(src, t, jq));
+        x[4 * jq] = P4.x; x[4 * jq + 1] = P4.y; x[4 * jq + 2] = P4.z; x[4 * jq + 3] = P4.w;
+      }
+      inv_ntt<N, TPP, -1>(x, scr[w], me.lay, t, w, w ? tw.inv[1] : tw.inv[0]);
+#pragma unroll
+      for (int j = 0; j < C; ++j) ex[c][w][t + TPP * j] = umin(x[j], x[j] - p);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int kk = me.tid + NT * k, c = kk >= N, i = kk & (N - 1);
+      acc[k] += crt_lift(ex[c][0][i], ex[c][1][i]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int kk = me.tid + NT * k, c = kk >= N, i = kk & (N - 1);
+    out[b * 2 * N + kk] = c ? b_polys[b * N + i] - acc[k] : 0u - acc[k];
+  }
+}
+
 // RGSW gadget term (hw/tfhe.py:259-262): rows t get m * q/beta^(t+1) on the b
 // constant coefficient, rows l+t on the a constant coefficient.
 __global__ void rgsw_gadget_kernel(uint32_t *rgsw, const int32_t *__restrict__ bits, int64_t B, int N, int levels,
@@ -902,6 +1013,51 @@ int hwb_key_mul(const hwb_params *p, const uint32_t *key_ntt, const uint32_t *in
   else
     key_mul_kernel<2048><<<(unsigned)npolys, Cfg<2048>::THREADS, 0, s>>>(in, key_ntt, add, out, make_tw(st, 2048));
   return post_launch("key_mul_kernel");
+}
+
+static const int kPackRowsJ = 32;   // key rows j per partial-sum CTA
+
+size_t hwb_pack_ks_workspace_bytes(const hwb_params *p, int64_t B) {
+  if (!p || B <= 0) return 0;
+  const int64_t chunks = (p->N + kPackRowsJ - 1) / kPackRowsJ;
+  return sizeof(uint32_t) * (size_t)B * chunks * 2 * 2 * p->N;
+}
+
+int hwb_pack_ks(const hwb_params *p, int32_t levels, int32_t base_log, const uint32_t *ksk_ntt,
+                const uint32_t *apolys, const uint32_t *b_polys, uint32_t *out, int64_t B, void *workspace,
+                void *stream) {
+  int rc = check_glwe(p);
+  if (rc) return rc;
+  if (levels < 1 || base_log < 1 || levels * base_log > 32)
+    return fail(HWB_EINVAL, "packing gadget spans more than 32 bits");
+  // exactness of one chunk: rows_j key rows x levels digits x N LWEs x beta/2 x 2^31 < P/2
+  const double bound = (double)kPackRowsJ * levels * p->N * std::ldexp(1.0, base_log - 1) * std::ldexp(1.0, 31);
+  if (!(bound < 0.5 * (double)kP0 * (double)kP1))
+    return fail(HWB_EINVAL, "packing gadget too wide for the exact 2-prime NTT");
+  if (B < 0) return fail(HWB_EINVAL, "negative batch");
+  if (B == 0) return HWB_OK;
+  if (!workspace) return fail(HWB_EINVAL, "hwb_pack_ks needs a workspace");
+  DevState *st;
+  if ((rc = init_device(&st))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int chunks = (int)((p->N + kPackRowsJ - 1) / kPackRowsJ);
+  const Gadget gk = make_gadget(levels, base_log);
+  uint32_t *part = (uint32_t *)workspace;
+  dim3 grid(chunks, (unsigned)B);
+  if (p->N == 1024) {
+    pack_ks_partial_kernel<1024><<<grid, Cfg<1024>::THREADS, 0, s>>>(apolys, ksk_ntt, part, kPackRowsJ, gk,
+                                                                     make_tw(st, 1024));
+    if ((rc = post_launch("pack_ks_partial_kernel"))) return rc;
+    pack_ks_finish_kernel<1024><<<(unsigned)B, Cfg<1024>::THREADS, 0, s>>>(part, chunks, b_polys, out,
+                                                                           make_tw(st, 1024));
+  } else {
+    pack_ks_partial_kernel<2048><<<grid, Cfg<2048>::THREADS, 0, s>>>(apolys, ksk_ntt, part, kPackRowsJ, gk,
+                                                                     make_tw(st, 2048));
+    if ((rc = post_launch("pack_ks_partial_kernel"))) return rc;
+    pack_ks_finish_kernel<2048><<<(unsigned)B, Cfg<2048>::THREADS, 0, s>>>(part, chunks, b_polys, out,
+                                                                           make_tw(st, 2048));
+  }
+  return post_launch("pack_ks_finish_kernel");
 }
 
 int hwb_rgsw_add_gadget(const hwb_params *p, uint32_t *rgsw, const int32_t *bits, int64_t B, void *stream) {

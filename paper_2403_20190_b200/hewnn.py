@@ -296,6 +296,94 @@ def he_merge(m1: HomWisardModel, m2: HomWisardModel) -> HomWisardModel:
 
 
 # ---------------------------------------------------------------------------
+# homomorphic inference (PD-act, hw/hewnn.py:278-320)
+
+
+@dataclass
+class ScorePack:
+    """PD-act output: packed raw scores plus encrypted class counts (hw/hewnn.py:67-78).
+    Coefficient i*k0 + j (chunked over RLWEs of N coefficients) holds the
+    class-i, RAM-j counter lookup."""
+
+    geometry: WisardGeometry
+    params: HeParams
+    packed: np.ndarray            # (ceil(l*k0/N), 2, N)
+    counts_ct: np.ndarray         # (2, N)
+
+
+@dataclass
+class FinalizeResult:
+    prediction: int
+    scores: np.ndarray
+    raw: np.ndarray
+    counts: ClassCounts
+    noise_max: int
+    noise_margin: int
+
+    @property
+    def noise_ok(self) -> bool:
+        return self.noise_max < self.noise_margin
+
+
+def he_infer_pd_batch(model: HomWisardModel, samples: Sequence[EncryptedSample],
+                      ksk: tfhe.PackingKeySwitchKey) -> list[ScorePack]:
+    """he_infer_pd (hw/hewnn.py:278-320) for several samples in one pass: every
+    (sample, class, RAM) triple is one vertical-packing item (clear label bits,
+    encrypted address bits), then each sample's l*k0 extracted LWEs are packed."""
+    geometry, params = model.geometry, model.params
+    for smp in samples:
+        if smp.s != geometry.s:
+            raise TfheError(f"sample has {smp.s} bits, geometry wants {geometry.s}")
+        if smp.params != params:
+            raise TfheError("sample parameter set differs from the model's")
+    n = params.n
+    l, k0 = geometry.l, geometry.k0
+    total = l * k0
+    tmpl = np.concatenate([_selector_template(geometry, params, clear_label=i) for i in range(l)])
+    strides = np.cumsum([0] + [int(np.asarray(smp.rgsw.shape[0])) for smp in samples])
+    codes = np.concatenate([_shift(tmpl, int(strides[i])) for i in range(len(samples))])
+    lut_idx = np.tile(np.tile(np.arange(k0), l), len(samples))
+    table = _stack_table(params, list(samples))
+    lwe = lut.vp_codes(params, codes, table, model.rams, lut_idx)          # (S*l*k0, N+1)
+    n_ct = -(-total // n)
+    S = len(samples)
+    a_st = torch.zeros((S * n_ct, n, n), dtype=torch.int32, device=lwe.device)
+    b_p = torch.zeros((S * n_ct, n), dtype=torch.int32, device=lwe.device)
+    for si in range(S):
+        for t in range(n_ct):
+            lo, hi = si * total + t * n, si * total + min(total, (t + 1) * n)
+            a_st[si * n_ct + t, : hi - lo] = lwe[lo:hi, :n]
+            b_p[si * n_ct + t, : hi - lo] = lwe[lo:hi, n]
+    packed = tfhe.to_host(tfhe.pack_batch(a_st, b_p, ksk)).reshape(S, n_ct, 2, n)
+    cc = tfhe.to_host(model.counts_ct)
+    return [ScorePack(geometry, params, packed[si], cc.copy()) for si in range(S)]
+
+
+def he_infer_pd(model: HomWisardModel, sample: EncryptedSample, ksk: tfhe.PackingKeySwitchKey) -> ScorePack:
+    """Score every (class, RAM) pair and pack the results (hw/hewnn.py:278-320)."""
+    return he_infer_pd_batch(model, [sample], ksk)[0]
+
+
+def client_finalize(pack: ScorePack, key: tfhe.SecretKey, activation, *, balance: bool = False) -> FinalizeResult:
+    """Decrypt, rescale, activate and argmax (hw/hewnn.py:329-345), on the client."""
+    from . import wnn
+    geometry, params = pack.geometry, pack.params
+    raw_flat, noise_max = [], 0
+    delta = params.delta
+    for t in range(pack.packed.shape[0]):
+        ct = RlweCiphertext(params, pack.packed[t])
+        phase = tfhe.phase_rlwe(ct, key).astype(np.int64)
+        raw_flat.append(tfhe.decode_phase(phase, params))
+        err = (phase + delta // 2) % delta - delta // 2
+        noise_max = max(noise_max, int(np.abs(err).max()))
+    raw = np.concatenate(raw_flat)[: geometry.l * geometry.k0].reshape(geometry.l, geometry.k0)
+    counts = decrypt_counts(pack.counts_ct, params, geometry.l, key)
+    pred = wnn.predict_from_lookups(raw, activation, counts if balance else None)
+    scores = wnn.scores_from_lookups(raw, activation, counts if balance else None)
+    return FinalizeResult(pred, scores, raw, counts, noise_max, delta // 2)
+
+
+# ---------------------------------------------------------------------------
 # client side: decryption of a trained model (oracle bridge, hw/hewnn.py:352-365)
 
 

@@ -257,6 +257,85 @@ def pbs_keygen(params: HeParams, rng_seed) -> PbsKeys:
     return PbsKeys(params, LweSecretKey(params, s0), key1, bsk, ksk)
 
 
+@dataclass
+class PackingKeySwitchKey:
+    """RLWE encryptions of s_j * q/beta^(t+1) for every key coefficient j
+    (hw/tfhe.py:81-92), (N, l_pks, 2, N); spectra() uploads the NTT image."""
+
+    params: HeParams
+    data: np.ndarray
+    _ntt: torch.Tensor | None = field(default=None, repr=False)
+
+    def spectra(self) -> torch.Tensor:
+        if self._ntt is None:
+            t = to_device(self.data)
+            npolys = t.numel() // self.params.n
+            out = torch.empty((npolys, 2, self.params.n), dtype=torch.int32, device=t.device)
+            cp = _lib.c_params(self.params)
+            _lib.check(_lib.load().hwb_poly_to_ntt(ctypes.byref(cp), _ptr(t), _ptr(out), npolys, _stream()))
+            self._ntt = out
+        return self._ntt
+
+
+def keygen(params: HeParams, rng_seed) -> tuple[SecretKey, PackingKeySwitchKey]:
+    """hw/tfhe.py:95-114 at q = 2^32: binary RLWE key S1 and the packing
+    key-switch key, drawn in the reference's chunked order (step = 2^20 //
+    (l N) key rows per chunk: a, then e, per chunk)."""
+    rng = make_rng(rng_seed)
+    n = params.n
+    s = rng.integers(0, 2, n).astype(U32)
+    key = SecretKey(params, s)
+    g = params.gadget_pks
+    ksk = np.empty((n, g.levels, 2, n), dtype=U32)
+    step = max(1, 2 ** 20 // (g.levels * n))
+    for j0 in range(0, n, step):
+        j1 = min(n, j0 + step)
+        a = uniform_u32(rng, (j1 - j0, g.levels, n))
+        e = gaussian_u32(rng, params.sigma, (j1 - j0, g.levels, n))
+        b = (key._key_mul(a) + e).astype(U32)
+        for t in range(g.levels):
+            b[:, t, 0] += s[j0:j1] * U32(g.power(t))
+        ksk[j0:j1, :, 0, :] = a
+        ksk[j0:j1, :, 1, :] = b
+    return key, PackingKeySwitchKey(params, ksk)
+
+
+def pack_batch(a_stacks, b_polys, ksk: PackingKeySwitchKey):
+    """Batched packing key switch (hw/tfhe.py:390-439): a_stacks (B, k, N) LWE
+    a-vectors (k <= N, row i = input i), b_polys (B, N) with coefficient i = b
+    of input i -> (B, 2, N) RLWEs whose coefficient i decrypts to input i."""
+    params = ksk.params
+    n = params.n
+    a = to_device(a_stacks)
+    bp = to_device(b_polys)
+    if a.dim() != 3 or a.shape[2] != n or a.shape[1] > n:
+        raise TfheError(f"cannot pack {a.shape[1] if a.dim() == 3 else '?'} > N = {n} ciphertexts")
+    B, k = a.shape[0], a.shape[1]
+    apolys = torch.zeros((B, n, n), dtype=torch.int32, device=a.device)   # apolys[b][j][i] = a^(i)_j
+    apolys[:, :, :k] = a.transpose(1, 2)
+    out = torch.empty((B, 2, n), dtype=torch.int32, device=a.device)
+    cp = _lib.c_params(params)
+    L = _lib.load()
+    ws = torch.empty(max(1, (L.hwb_pack_ks_workspace_bytes(ctypes.byref(cp), B) + 3) // 4),
+                     dtype=torch.int32, device=a.device)
+    g = params.gadget_pks
+    _lib.check(L.hwb_pack_ks(ctypes.byref(cp), g.levels, g.base_log, _ptr(ksk.spectra()), _ptr(apolys),
+                             _ptr(bp), _ptr(out), B, _ptr(ws), _stream()))
+    return _wrap(a_stacks, out)
+
+
+def packing_key_switch(cs, ksk: PackingKeySwitchKey) -> RlweCiphertext:
+    """hw/tfhe.py:373-387: pack <= N extracted LWEs ((N+1,) rows, b last)."""
+    rows = np.stack([np.asarray(c, dtype=U32) for c in cs])
+    n = ksk.params.n
+    if len(rows) > n:
+        raise TfheError(f"cannot pack {len(rows)} > N = {n} ciphertexts")
+    b = np.zeros(n, dtype=U32)
+    b[: len(rows)] = rows[:, n]
+    out = pack_batch(rows[None, :, :n], b[None], ksk)[0]
+    return RlweCiphertext(ksk.params, out)
+
+
 def _encode(m, params: HeParams) -> np.ndarray:
     """hw/tfhe.py:181-190."""
     n = params.n

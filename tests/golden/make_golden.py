@@ -182,6 +182,45 @@ def gen_train(name):
                         class_counts=ref_counts.counts, bits=bits, labels=labels)
 
 
+def gen_infer():
+    """Reference pack_batch (hw/tfhe.py:390) and he_infer_pd (hw/hewnn.py:278)
+    on the train_tree model, embedded at q = 2^32.  The packing key comes from
+    the q = 2^32 restatement of keygen (its first draw is the training key s1)."""
+    from hewisard import hewnn as rh
+    from hewisard import wnn as rw
+    from hewisard.params import GadgetSpec as RG
+    name = "train_tree"
+    P, s1, bits, labels, stacks = train_inputs(name)
+    (s, l, a, r) = TRAIN_CASES[name][2]
+    kseed = TRAIN_CASES[name][4]
+    s_pk, ksk = o.keygen_packing(P, kseed)
+    assert np.array_equal(s_pk, s1)
+    g, gp = P.gadget, P.gadget_pks
+    RP = RParams(name="emb", degree_log=P.degree_log, sigma_rel=0.0, gadget=RG(g.levels, g.base_log),
+                 gadget_ks=RG(gp.levels, gp.base_log), p=P.p, insecure=True, exact_mul=True)
+    rksk = rt.PackingKeySwitchKey(RP, emb(ksk))
+    # pack_batch on random LWEs
+    prng = np.random.default_rng(99)
+    k = 7
+    a_st = rand_u32(prng, (2, k, P.n))
+    b_p = np.zeros((2, P.n), dtype=np.uint32)
+    b_p[:, :k] = rand_u32(prng, (2, k))
+    packed = unemb(rt.pack_batch(emb(a_st), emb(b_p), rksk))
+    # he_infer_pd on the trained model and a fresh (unlabelled) test sample
+    geom = rw.WisardGeometry(s=s, l=l, a=a, r=r, p=P.p)
+    samples = [rh.EncryptedSample(RP, [rt.RgswCiphertext(RP, emb(x)) for x in st[:s]],
+                                  [rt.RgswCiphertext(RP, emb(x)) for x in st[s:]]) for st in stacks]
+    model = rh.he_train(samples, geom, RP)
+    test_bits = prng.integers(0, 2, s)
+    test_rgsw = o.enc_rgsw_batch(test_bits, s1, P.sigma, g.levels, g.base_log, o.make_rng(13))
+    tsample = rh.EncryptedSample(RP, [rt.RgswCiphertext(RP, emb(x)) for x in test_rgsw], None)
+    pack = rh.he_infer_pd(model, tsample, rksk)
+    fin = rh.client_finalize(pack, rt.SecretKey(RP, s1.astype(np.uint64)), rw.ActivationSpec("bin", 0))
+    np.savez_compressed(os.path.join(HERE, "infer_tree.npz"), sha_ksk=sha(ksk), pack_a=a_st, pack_b=b_p,
+                        pack_out=packed, test_bits=test_bits, sha_test_rgsw=sha(test_rgsw),
+                        infer_packed=unemb(pack.packed), raw=fin.raw, prediction=fin.prediction)
+
+
 def main():
     rng = np.random.default_rng(20240329)
     t = time.time()
@@ -198,6 +237,9 @@ def main():
         t = time.time()
         gen_train(name)
         print(f"{name}: {time.time() - t:.1f}s", flush=True)
+    t = time.time()
+    gen_infer()
+    print(f"infer: {time.time() - t:.1f}s", flush=True)
 
 
 if __name__ == "__main__":

@@ -131,3 +131,26 @@ def test_monomial_gather_vs_oracle():
     x = rng.integers(0, 1 << 32, (6, 2, P.n), dtype=np.uint64).astype(np.uint32)
     es = np.array([0, 1, -1, 2047, 3000, -5000])
     assert_u32_equal(lut.monomial_gather(P, x, es), o.monomial_gather(x, es))
+
+
+def test_pack_batch_and_he_infer_pd_match_reference():
+    g = golden("infer_tree.npz")
+    name = "train_tree"
+    P, s1, bits, labels, smp, geom = samples_of(name)
+    key, pksk = tfhe.keygen(P, TRAIN_CASES[name][4])
+    assert np.array_equal(key.s, s1)
+    assert_u32_equal(tfhe.pack_batch(g["pack_a"], g["pack_b"], pksk), g["pack_out"])     # hw/tfhe.py:390
+    model = hewnn.he_train(smp, geom, P)
+    test_rgsw = o.enc_rgsw_batch(g["test_bits"], s1, P.sigma, P.gadget.levels, P.gadget.base_log, o.make_rng(13))
+    assert sha(test_rgsw) == str(g["sha_test_rgsw"])
+    tsample = hewnn.EncryptedSample(P, tfhe.to_device(test_rgsw), geom.s, 0)
+    pack = hewnn.he_infer_pd(model, tsample, pksk)                                         # hw/hewnn.py:278
+    assert_u32_equal(pack.packed, g["infer_packed"])
+    fin = hewnn.client_finalize(pack, key, wnn.ActivationSpec("bin", 0))
+    assert np.array_equal(fin.raw, g["raw"]) and fin.prediction == int(g["prediction"])
+    assert fin.noise_ok
+    # batched inference over several samples equals per-sample calls
+    packs = hewnn.he_infer_pd_batch(model, [tsample, smp[0], tsample], pksk)
+    assert_u32_equal(packs[0].packed, g["infer_packed"])
+    assert_u32_equal(packs[2].packed, g["infer_packed"])
+    assert_u32_equal(packs[1].packed, hewnn.he_infer_pd(model, smp[0], pksk).packed)

@@ -80,3 +80,18 @@ def test_host_rgsw_encryption_matches_oracle():
     for i in range(count):
         smp = hewnn.encrypt_sample(bits[i], int(labels[i]), key, rng, label_bits=1, device=False)
         assert_u32_equal(smp.rgsw, stacks[i])
+
+
+def test_packing_keygen_and_pack_batch_match_reference(coracle):
+    from oracle import tfhe32 as o
+    from paper_2403_20190_b200 import tfhe
+    g = golden("infer_tree.npz")
+    P = named_params("CFG2", 256)
+    kseed = TRAIN_CASES["train_tree"][4]
+    s, ksk = o.keygen_packing(P, kseed)
+    assert sha(ksk) == str(g["sha_ksk"])
+    key, pk = tfhe.keygen(P, kseed)                    # product restatement of hw/tfhe.py:95-114
+    assert_u32_equal(key.s, s)
+    assert_u32_equal(pk.data, ksk)
+    gp = P.gadget_pks
+    assert_u32_equal(coracle.pack_batch(g["pack_a"], g["pack_b"], ksk, gp.levels, gp.base_log), g["pack_out"])
