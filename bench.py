@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--train-cfg", type=int, default=3, choices=[1, 3, 4, 5])
     ap.add_argument("--train-images", type=int, default=64, help="0 disables the training measurement")
     ap.add_argument("--train-batch", type=int, default=32)
+    ap.add_argument("--infer-images", type=int, default=8, help="0 disables the inference measurement")
     return ap.parse_args()
 
 
@@ -242,6 +243,30 @@ def bench_train(args, world, rank, torch, dist):
            "noise": {"max_log2": round(float(np.log2(max(noise, 1))), 2),
                      "margin_log2": round(float(np.log2(margin)), 2), "counters_correct": round(frac_ok, 6)},
            "check": "decrypted counters == train_integer" if ok else "COUNTER MISMATCH"}
+    if args.infer_images > 0:
+        # PD-act inference (hw/hewnn.py:278-345) with the trained model
+        tds = data.config_dataset(cfg, split="test", n=args.infer_images, seed=rank)
+        _, pksk = tfhe.keygen(P, KEY_SEED)                       # same S1 as `key` (first draw)
+        trng = tfhe.make_rng(ENC_SEED + 7 + 1000 * rank)
+        tsamples = [hewnn.encrypt_sample(tds.bits[i], None, key, trng) for i in range(args.infer_images)]
+        pksk.spectra()
+        hewnn.he_infer_pd_batch(model, tsamples[:1], pksk)                 # warm-up
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        packs = hewnn.he_infer_pd_batch(model, tsamples, pksk)
+        g1.record()
+        g1.synchronize()
+        act = wnn.ActivationSpec("bin", 0)
+        preds = [hewnn.client_finalize(pk, key, act).prediction for pk in packs]
+        plain = wnn.evaluate_dataset(ref, geom, tds.bits, act)
+        vp_items = geom.l * geom.k0
+        out["infer"] = {"metric": "encrypted inference images/sec", "unit": "images/s",
+                        "value": round(args.infer_images / (g0.elapsed_time(g1) * 1e-3), 2),
+                        "images": args.infer_images, "vp_items_per_image": vp_items,
+                        "packed_rlwe_per_image": -(-vp_items // P.n),
+                        "check": "predictions == plaintext evaluate" if list(plain) == preds
+                        else "PREDICTION MISMATCH"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import coracle, wnn32
         coracle.build()
