@@ -190,18 +190,17 @@ def _selector_template(geometry: WisardGeometry, params: HeParams, *, clear_labe
     z = lut.tree_depth(k, params)
     a, s = geometry.a, geometry.s
     perm = permutation(geometry.r, geometry.s)
-    weights = [k - 1 - i for i in range(z)] + lut.rotate_weights(k, params)
-    out = np.empty((geometry.k0, k), dtype=np.int64)
-    for j in range(geometry.k0):
-        for pos, w in enumerate(weights):
-            if w < a:
-                idx = j * a + w
-                out[j, pos] = perm[idx] if idx < s else lut.CLEAR0
-            elif clear_label is None:
-                out[j, pos] = s + (w - a)
-            else:
-                out[j, pos] = lut.CLEAR1 if (clear_label >> (w - a)) & 1 else lut.CLEAR0
-    return out
+    weights = np.array([k - 1 - i for i in range(z)] + lut.rotate_weights(k, params), dtype=np.int64)
+    j = np.arange(geometry.k0, dtype=np.int64)[:, None]
+    idx = j * a + weights[None, :]                                  # address-bit input index
+    addr = np.where(idx < s, perm[np.minimum(idx, s - 1)], lut.CLEAR0)
+    lw = weights - a                                                # label-bit number (w >= a)
+    if clear_label is None:
+        lab = np.broadcast_to(s + lw, addr.shape)
+    else:
+        bit = (clear_label >> np.maximum(lw, 0)) & 1
+        lab = np.broadcast_to(np.where(bit == 1, lut.CLEAR1, lut.CLEAR0), addr.shape)
+    return np.where(weights[None, :] < a, addr, lab).astype(np.int64)
 
 
 def _shift(codes: np.ndarray, base: int) -> np.ndarray:

@@ -12,6 +12,7 @@ against.  The plaintext WiSARD is not part of the accelerated path.
 from __future__ import annotations
 
 from dataclasses import dataclass
+from functools import lru_cache
 
 import numpy as np
 
@@ -129,14 +130,22 @@ def quantize_tabular(raw: np.ndarray, lo: np.ndarray, hi: np.ndarray) -> np.ndar
     return np.clip((raw - lo) / span * 255, 0, 255).astype(np.int64)
 
 
-def permutation(r: int, s: int) -> np.ndarray:
-    """Deterministic Fisher-Yates shuffle of [0, s) from the recorded PRNG (hw/wnn.py:189-196)."""
+@lru_cache(maxsize=64)
+def _permutation_cached(r: int, s: int) -> np.ndarray:
     rng = make_rng(r)
     perm = np.arange(s)
     for i in range(s - 1, 0, -1):
         j = int(rng.integers(0, i + 1))
         perm[i], perm[j] = perm[j], perm[i]
+    perm.setflags(write=False)
     return perm
+
+
+def permutation(r: int, s: int) -> np.ndarray:
+    """Deterministic Fisher-Yates shuffle of [0, s) from the recorded PRNG
+    (hw/wnn.py:189-196); memoised per (r, s) -- the Python-level shuffle of a
+    2352-bit input costs milliseconds and every selector build needs it."""
+    return _permutation_cached(int(r), int(s)).copy()
 
 
 def addresses(bits: np.ndarray, geometry: WisardGeometry) -> np.ndarray:
