@@ -143,6 +143,11 @@ int hwb_pack_ks(const hwb_params *p, int32_t levels, int32_t base_log, const uin
                 const uint32_t *apolys, const uint32_t *b_polys, uint32_t *out, int64_t B, void *workspace,
                 void *stream);
 
+/* dst[k] += sum_{i < count} src[i*words + k] mod 2^32: the IVP rows of `count`
+ * samples added into an encrypted model in one pass (hw/hewnn.py:213).
+ * 16-byte aligned pointers. */
+int hwb_accumulate_rows(uint32_t *dst, const uint32_t *src, int64_t words, int32_t count, void *stream);
+
 /* dst[k] += (negate ? -1 : 1) * src[k mod src_words] mod 2^32 for k < words: exact
  * ciphertext addition for model accumulation and federated merge
  * (hw/hewnn.py:213, 264-271). */
@@ -150,11 +155,13 @@ int hwb_accumulate(uint32_t *dst, const uint32_t *src, int64_t words, int64_t sr
                    void *stream);
 
 /* Fused blind rotation (hw/tfhe.py:340-349 blind_rotate), one launch for all L
- * steps: acc[b] <- cmux(G_i, acc[b] * X^(-I[b][i]), acc[b]) for i < L.
- * ggsw_ntt: L NTT-domain GGSWs shared by the batch (the BSK);
+ * steps: acc[b] <- cmux(G, acc[b] * X^(-I[b][i]), acc[b]) for i < L, with
+ * G = ggsw_ntt[i] (ggsw_idx == NULL: L GGSWs shared by the batch, the BSK) or
+ * G = ggsw_ntt[ggsw_idx[b][i]] (per-item selector ladders of vertical packing,
+ * hw/lut.py:249-260, 280-291; an index < 0 skips the step).
  * exps: [B][L] int32 I values; acc: [B][2][N] in/out. */
-int hwb_blind_rotate(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_t *exps,
-                     uint32_t *acc, int32_t L, int64_t B, void *stream);
+int hwb_blind_rotate(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_t *ggsw_idx,
+                     const int32_t *exps, uint32_t *acc, int32_t L, int64_t B, void *stream);
 
 /* Batched sample extraction of coefficient `coeff` (hw/tfhe.py:352-361; the
  * batched coefficient-0 form is hw/lut.py:263-266): rlwe [B][2][N] ->

@@ -22,6 +22,7 @@ EXPORTS = (
     "hwb_sample_extract", "hwb_keyswitch", "hwb_pbs_workspace_bytes", "hwb_pbs",
     "hwb_ivp_level", "hwb_vp_level", "hwb_monomial_gather", "hwb_accumulate",
     "hwb_poly_to_ntt", "hwb_key_mul", "hwb_rgsw_add_gadget", "hwb_pack_ks_workspace_bytes", "hwb_pack_ks",
+    "hwb_accumulate_rows",
 )
 
 
@@ -68,7 +69,7 @@ def load() -> ctypes.CDLL:
         L.hwb_ext_product.argtypes = [_pp, _vp, _vp, _vp, _vp, _i64, _vp]
         L.hwb_cmux.argtypes = [_pp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp]
         L.hwb_cdemux.argtypes = [_pp, _vp, _vp, _vp, _vp, _vp, _i64, _vp]
-        L.hwb_blind_rotate.argtypes = [_pp, _vp, _vp, _vp, ctypes.c_int32, _i64, _vp]
+        L.hwb_blind_rotate.argtypes = [_pp, _vp, _vp, _vp, _vp, ctypes.c_int32, _i64, _vp]
         L.hwb_sample_extract.argtypes = [_pp, _vp, _vp, _i64, ctypes.c_int32, _vp]
         L.hwb_keyswitch.argtypes = [_pp, _vp, _vp, _vp, _i64, _vp]
         L.hwb_pbs_workspace_bytes.argtypes = [_pp, _i64]
@@ -78,6 +79,7 @@ def load() -> ctypes.CDLL:
         L.hwb_vp_level.argtypes = [_pp, _vp, _vp, _vp, _vp, ctypes.c_int32, _i64, _vp]
         L.hwb_monomial_gather.argtypes = [_pp, _vp, _vp, _vp, _i64, _vp]
         L.hwb_accumulate.argtypes = [_vp, _vp, _i64, _i64, ctypes.c_int, _vp]
+        L.hwb_accumulate_rows.argtypes = [_vp, _vp, _i64, ctypes.c_int32, _vp]
         L.hwb_poly_to_ntt.argtypes = [_pp, _vp, _vp, _i64, _vp]
         L.hwb_key_mul.argtypes = [_pp, _vp, _vp, _vp, _vp, _i64, _vp]
         L.hwb_rgsw_add_gadget.argtypes = [_pp, _vp, _vp, _i64, _vp]

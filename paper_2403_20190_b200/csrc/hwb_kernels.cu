@@ -384,6 +384,28 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::minb(V))
   }
 }
 
+// dst[k] += sum_{i < count} src[i * words + k] mod 2^32: the rows of `count`
+// samples added into the model in one pass (hw/hewnn.py:213).
+__global__ void accumulate_rows_kernel(uint32_t *__restrict__ dst, const uint32_t *__restrict__ src, int64_t words,
+                                       int count) {
+  const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (k >= words) return;
+  if (k + 4 <= words && (words & 3) == 0) {
+    uint4 acc = *reinterpret_cast<const uint4 *>(dst + k);
+    for (int i = 0; i < count; ++i) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4 *>(src + (int64_t)i * words + k));
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    *reinterpret_cast<uint4 *>(dst + k) = acc;
+  } else {
+    for (int64_t kk = k; kk < k + 4 && kk < words; ++kk) {
+      uint32_t a = dst[kk];
+      for (int i = 0; i < count; ++i) a += src[(int64_t)i * words + kk];
+      dst[kk] = a;
+    }
+  }
+}
+
 // x_b * X^(e_b) per item (hw/lut.py:317-325), e_b taken mod 2N; in may not alias out.
 template <int N>
 __global__ void monomial_gather_kernel(const uint32_t *__restrict__ in, uint32_t *__restrict__ out,
@@ -412,14 +434,17 @@ __device__ __forceinline__ int mod_switch(uint32_t x, int log2m) {
 }
 
 // Fused blind rotation.  PBS = false: acc_io [B][2][N] in/out, exps [B][L] are
-// the reference's I values (rotation X^-I).  PBS = true: lwe_in [B][L+1];
-// acc = TV * X^-b~, rotation X^{a~_i} (I_i = -a~_i), output the coefficient-0
-// extraction [B][N+1].
+// the reference's I values (rotation X^-I); step s uses GGSW s of `bsk`, or,
+// with gidx [B][L], GGSW gidx[b][s] (< 0: the step is skipped) -- the per-item
+// CMUX ladders of vertical packing (hw/lut.py:249-260, 280-291).  PBS = true:
+// lwe_in [B][L+1]; acc = TV * X^-b~, rotation X^{a~_i} (I_i = -a~_i), output the
+// coefficient-0 extraction [B][N+1].
 template <int N, bool PBS, int V>
 __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::minb(V))
-    blind_rotate_kernel(const uint32_t *__restrict__ bsk, size_t ggsw_words, const int32_t *__restrict__ exps,
-                        const uint32_t *__restrict__ lwe_in, const uint32_t *__restrict__ tv, int tv_per_item,
-                        uint32_t *acc_io, uint32_t *lwe_out, int L, Gadget g, Tw tw) {
+    blind_rotate_kernel(const uint32_t *__restrict__ bsk, size_t ggsw_words, const int32_t *__restrict__ gidx,
+                        const int32_t *__restrict__ exps, const uint32_t *__restrict__ lwe_in,
+                        const uint32_t *__restrict__ tv, int tv_per_item, uint32_t *acc_io, uint32_t *lwe_out, int L,
+                        Gadget g, Tw tw) {
   constexpr int TPP = Cfg<N>::TPP, NT = Cfg<N>::THREADS;
   extern __shared__ uint4 smem_raw[];
   Smem<N> &sm = *reinterpret_cast<Smem<N> *>(smem_raw);
@@ -451,12 +476,17 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::minb(V))
       if (e < 0) e += 2 * N;
     }
     if (e == 0) continue;   // zero difference -> zero product: exact skip
+    int gi = s;
+    if (!PBS && gidx) {
+      gi = gidx[b * L + s];
+      if (gi < 0) continue;   // clear selector bit: handled by the caller
+    }
     for (int k = tid; k < 2 * N; k += NT) {
       const int c = k >= N, i = k & (N - 1);
       sm.v[k] = decomp_prep(rot_read<N>(sm.acc + c * N, i, e) - sm.acc[k], g);
     }
     __syncthreads();
-    ext_product_core<N, Cfg<N>::spec(V)>(sm, bsk + (size_t)s * ggsw_words, g, me, tw, x);
+    ext_product_core<N, Cfg<N>::spec(V)>(sm, bsk + (size_t)gi * ggsw_words, g, me, tw, x);
 #pragma unroll
     for (int j = 0; j < N / TPP; ++j) {
       const int i = me.t + TPP * j;
@@ -853,9 +883,9 @@ static int launch_cmux(const hwb_params *p, DevState *st, const uint32_t *ggsw, 
 }
 
 template <int N, bool PBS>
-static int launch_br(const hwb_params *p, DevState *st, const uint32_t *bsk, const int32_t *exps,
-                     const uint32_t *lwe_in, const uint32_t *tv, int tv_per_item, uint32_t *acc,
-                     uint32_t *lwe_out, int L, int64_t B, cudaStream_t s) {
+static int launch_br(const hwb_params *p, DevState *st, const uint32_t *bsk, const int32_t *gidx,
+                     const int32_t *exps, const uint32_t *lwe_in, const uint32_t *tv, int tv_per_item,
+                     uint32_t *acc, uint32_t *lwe_out, int L, int64_t B, cudaStream_t s) {
   const size_t smem = sizeof(Smem<N>);
   const Gadget g = make_gadget(p->l, p->base_log);
   const size_t words = hwb_ggsw_ntt_words(p);
@@ -863,11 +893,11 @@ static int launch_br(const hwb_params *p, DevState *st, const uint32_t *bsk, con
   if (g_variant == 1) {
     if ((rc = set_smem(blind_rotate_kernel<N, PBS, 1>, smem))) return rc;
     blind_rotate_kernel<N, PBS, 1><<<(unsigned)B, Cfg<N>::THREADS, smem, s>>>(
-        bsk, words, exps, lwe_in, tv, tv_per_item, acc, lwe_out, L, g, make_tw(st, N));
+        bsk, words, gidx, exps, lwe_in, tv, tv_per_item, acc, lwe_out, L, g, make_tw(st, N));
   } else {
     if ((rc = set_smem(blind_rotate_kernel<N, PBS, 0>, smem))) return rc;
     blind_rotate_kernel<N, PBS, 0><<<(unsigned)B, Cfg<N>::THREADS, smem, s>>>(
-        bsk, words, exps, lwe_in, tv, tv_per_item, acc, lwe_out, L, g, make_tw(st, N));
+        bsk, words, gidx, exps, lwe_in, tv, tv_per_item, acc, lwe_out, L, g, make_tw(st, N));
   }
   return post_launch("blind_rotate_kernel");
 }
@@ -1071,6 +1101,15 @@ int hwb_rgsw_add_gadget(const hwb_params *p, uint32_t *rgsw, const int32_t *bits
   return post_launch("rgsw_gadget_kernel");
 }
 
+int hwb_accumulate_rows(uint32_t *dst, const uint32_t *src, int64_t words, int32_t count, void *stream) {
+  if (words < 0 || count < 0) return fail(HWB_EINVAL, "accumulate_rows: negative size");
+  if (words == 0 || count == 0) return HWB_OK;
+  if (((uintptr_t)dst | (uintptr_t)src) & 15) return fail(HWB_EINVAL, "accumulate_rows: pointers must be 16-byte aligned");
+  const int64_t threads = (words + 3) / 4;
+  accumulate_rows_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(dst, src, words, count);
+  return post_launch("accumulate_rows_kernel");
+}
+
 int hwb_accumulate(uint32_t *dst, const uint32_t *src, int64_t words, int64_t src_words, int negate, void *stream) {
   if (words < 0 || src_words < 1 || (words > 0 && (words % src_words) != 0))
     return fail(HWB_EINVAL, "accumulate: words must be a multiple of src_words");
@@ -1096,8 +1135,8 @@ int hwb_cdemux(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_t *ggs
   return cmux_dispatch(MODE_CDEMUX, p, ggsw_ntt, ggsw_idx, d, nullptr, nullptr, lo, hi, B, stream);
 }
 
-int hwb_blind_rotate(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_t *exps, uint32_t *acc,
-                     int32_t L, int64_t B, void *stream) {
+int hwb_blind_rotate(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_t *ggsw_idx, const int32_t *exps,
+                     uint32_t *acc, int32_t L, int64_t B, void *stream) {
   int rc = check_glwe(p);
   if (rc) return rc;
   if (B < 0 || L < 0) return fail(HWB_EINVAL, "negative batch or length");
@@ -1105,8 +1144,9 @@ int hwb_blind_rotate(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_
   DevState *st;
   if ((rc = init_device(&st))) return rc;
   cudaStream_t s = (cudaStream_t)stream;
-  if (p->N == 1024) return launch_br<1024, false>(p, st, ggsw_ntt, exps, nullptr, nullptr, 0, acc, nullptr, L, B, s);
-  return launch_br<2048, false>(p, st, ggsw_ntt, exps, nullptr, nullptr, 0, acc, nullptr, L, B, s);
+  if (p->N == 1024)
+    return launch_br<1024, false>(p, st, ggsw_ntt, ggsw_idx, exps, nullptr, nullptr, 0, acc, nullptr, L, B, s);
+  return launch_br<2048, false>(p, st, ggsw_ntt, ggsw_idx, exps, nullptr, nullptr, 0, acc, nullptr, L, B, s);
 }
 
 int hwb_sample_extract(const hwb_params *p, const uint32_t *rlwe, uint32_t *lwe, int64_t B, int32_t coeff,
@@ -1158,9 +1198,9 @@ int hwb_pbs(const hwb_params *p, const uint32_t *bsk_ntt, const uint32_t *ksk, c
   cudaStream_t s = (cudaStream_t)stream;
   uint32_t *ext = ksk ? (uint32_t *)workspace : lwe_out;
   if (p->N == 1024)
-    rc = launch_br<1024, true>(p, st, bsk_ntt, nullptr, lwe_in, tv, tv_per_item, nullptr, ext, (int)p->n, B, s);
+    rc = launch_br<1024, true>(p, st, bsk_ntt, nullptr, nullptr, lwe_in, tv, tv_per_item, nullptr, ext, (int)p->n, B, s);
   else
-    rc = launch_br<2048, true>(p, st, bsk_ntt, nullptr, lwe_in, tv, tv_per_item, nullptr, ext, (int)p->n, B, s);
+    rc = launch_br<2048, true>(p, st, bsk_ntt, nullptr, nullptr, lwe_in, tv, tv_per_item, nullptr, ext, (int)p->n, B, s);
   if (rc || !ksk) return rc;
   return keyswitch_launch(p, ksk, ext, lwe_out, B, s);
 }

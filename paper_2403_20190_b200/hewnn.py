@@ -216,16 +216,27 @@ def _payload(params: HeParams) -> np.ndarray:
 
 
 def _stack_table(params: HeParams, samples: list[EncryptedSample]):
-    rg = [tfhe.to_device(s.rgsw) for s in samples]      # H2D (non-blocking) for host tensors
-    big = rg[0] if len(rg) == 1 else torch.cat(rg)
-    return tfhe.rgsw_to_ntt(params, big)
+    """One device NTT-domain GGSW table holding every sample's RGSW rows, each
+    sample transformed straight into its slice (no stacking copy)."""
+    import ctypes
+    cp = _lib_params(params)
+    L = tfhe._lib.load()
+    words = L.hwb_ggsw_ntt_words(cp)
+    rows = [int(s.rgsw.shape[0]) for s in samples]
+    table = torch.empty((sum(rows), words), dtype=torch.int32, device=tfhe._device())
+    off = 0
+    for smp, r in zip(samples, rows):
+        src = tfhe.to_device(smp.rgsw)                  # H2D (non-blocking) for pinned host tensors
+        dst = ctypes.c_void_p(table.data_ptr() + off * words * 4)
+        tfhe._lib.check(L.hwb_ggsw_to_ntt(cp, tfhe._ptr(src), dst, r, tfhe._stream()))
+        off += r
+    return tfhe.GgswNtt(params, table)
 
 
 def he_count_labels_batch(params: HeParams, counts_ct: torch.Tensor, table, label_rows: np.ndarray):
     """hw/hewnn.py:180-186 for several samples: counts += IVP(label bits, (0, q/p))."""
     rows = lut.ivp_codes(params, label_rows, table, _payload(params))     # (I, 1, 2, N)
-    for i in range(rows.shape[0]):
-        lut.accumulate_(counts_ct, rows[i, 0])
+    lut.accumulate_rows_(counts_ct, rows)
     return counts_ct
 
 
@@ -249,10 +260,7 @@ def he_train(samples: Iterable[EncryptedSample], geometry: WisardGeometry, param
         stride = geometry.s + geometry.label_bits
         codes = np.concatenate([_shift(tmpl, i * stride) for i in range(len(chunk))])
         rows = lut.ivp_codes(params, codes, table, _payload(params))      # (I*k0, k1, 2, N)
-        per = model.rams.numel()
-        flat = rows.reshape(len(chunk), per)
-        for i in range(len(chunk)):
-            lut.accumulate_(model.rams, flat[i])
+        lut.accumulate_rows_(model.rams, rows)                             # hw/hewnn.py:213
         label_rows = np.array([[i * stride + geometry.s + b for b in range(geometry.label_bits)]
                                for i in range(len(chunk))], dtype=np.int64)
         he_count_labels_batch(params, model.counts_ct, table, label_rows)

@@ -107,12 +107,31 @@ def accumulate_(dst: torch.Tensor, src: torch.Tensor, negate: bool = False) -> t
     return dst
 
 
-def _cmux_rot(params, table: GgswNtt, acc: torch.Tensor, idx: torch.Tensor, rot: int) -> torch.Tensor:
-    """acc[b] <- acc[b] + C_idx[b] (*) (acc[b] X^rot - acc[b]) for all rows of acc."""
-    out = torch.empty_like(acc)
-    rt = torch.full((acc.shape[0],), rot % (2 * params.n), dtype=torch.int32, device=acc.device)
-    _lib.check(_lib.load().hwb_cmux(_cp(params), tfhe._ptr(table.data), tfhe._ptr(idx), None, tfhe._ptr(acc),
-                                    tfhe._ptr(rt), tfhe._ptr(out), acc.shape[0], tfhe._stream()))
+def accumulate_rows_(dst: torch.Tensor, rows: torch.Tensor) -> torch.Tensor:
+    """dst += sum_i rows[i] (mod 2^32, in place, one pass over rows)."""
+    words = dst.numel()
+    if rows.numel() % words:
+        raise TfheError("accumulate_rows: rows do not tile dst")
+    _lib.check(_lib.load().hwb_accumulate_rows(tfhe._ptr(dst), tfhe._ptr(rows), words, rows.numel() // words,
+                                               tfhe._stream()))
+    return dst
+
+
+def _rotation_ladder(params, table: GgswNtt, acc: torch.Tensor, cols: np.ndarray, sign: int) -> torch.Tensor:
+    """All encrypted rotation positions of a selector batch in ONE launch
+    (hwb_blind_rotate with per-item GGSW rows): for position i (weight 2^i),
+    acc <- cmux(C, acc * X^(sign 2^i), acc) where the bit is encrypted; clear
+    positions (code < 0) are skipped here and applied by the caller's gather,
+    exactly the reference's order (hw/lut.py:249-261, 280-292)."""
+    B, L = cols.shape
+    if L == 0 or not (cols >= 0).any():
+        return acc
+    dev = acc.device
+    idx = _i32(np.where(cols >= 0, cols, -1), dev)
+    exps = _i32(np.broadcast_to(-sign * (1 << np.arange(L, dtype=np.int64)), (B, L)) % (2 * params.n), dev)
+    out = acc.contiguous().clone()
+    _lib.check(_lib.load().hwb_blind_rotate(_cp(params), tfhe._ptr(table.data), tfhe._ptr(idx), tfhe._ptr(exps),
+                                            tfhe._ptr(out), L, B, tfhe._stream()))
     return out
 
 
@@ -145,18 +164,10 @@ def ivp_codes(params: HeParams, codes, table: GgswNtt | None, payload) -> torch.
     pay = tfhe.to_device(payload)
     dev = pay.device
     acc = pay.reshape(1, 2, n).expand(B, 2, n).contiguous()
-    clear_e = np.zeros(B, dtype=np.int64)
-    for i, w in enumerate(rotate_weights(k, params)):
-        col = codes[:, z + i]
-        enc = col >= 0
-        clear_e += (col == CLEAR1).astype(np.int64) << w
-        if not enc.any():
-            continue
-        if enc.all():
-            acc = _cmux_rot(params, table, acc, _i32(col, dev), 1 << w)
-        else:
-            sel = torch.as_tensor(np.nonzero(enc)[0], device=dev)
-            acc[sel] = _cmux_rot(params, table, acc[sel].contiguous(), _i32(col[enc], dev), 1 << w)
+    nrot = len(rotate_weights(k, params))
+    rcols = codes[:, z: z + nrot]
+    clear_e = ((rcols == CLEAR1).astype(np.int64) << np.arange(nrot, dtype=np.int64)).sum(axis=1)
+    acc = _rotation_ladder(params, table, acc, rcols, +1)                  # X^{+2^w} (hw/lut.py:289)
     if clear_e.any():
         acc = monomial_gather(params, acc, clear_e)
     cur = acc.unsqueeze(1)
@@ -222,18 +233,10 @@ def vp_codes(params: HeParams, codes, table: GgswNtt | None, lut_table: torch.Te
             new[sel] = _level(params, table, cur[sel].contiguous(), _i32(col[enc], dev), inverse=False)
         cur = new
     acc = cur[:, 0].contiguous()
-    clear_e = np.zeros(B, dtype=np.int64)
-    for i, w in enumerate(rotate_weights(k, params)):
-        col = codes[:, z + i]
-        enc = col >= 0
-        clear_e += (col == CLEAR1).astype(np.int64) << w
-        if not enc.any():
-            continue
-        if enc.all():
-            acc = _cmux_rot(params, table, acc, _i32(col, dev), -(1 << w))
-        else:
-            sel = torch.as_tensor(np.nonzero(enc)[0], device=dev)
-            acc[sel] = _cmux_rot(params, table, acc[sel].contiguous(), _i32(col[enc], dev), -(1 << w))
+    nrot = len(rotate_weights(k, params))
+    rcols = codes[:, z: z + nrot]
+    clear_e = ((rcols == CLEAR1).astype(np.int64) << np.arange(nrot, dtype=np.int64)).sum(axis=1)
+    acc = _rotation_ladder(params, table, acc, rcols, -1)                  # X^{-2^w} (hw/lut.py:258)
     if clear_e.any():
         acc = monomial_gather(params, acc, -clear_e)
     return tfhe.sample_extract_batch(params, acc)

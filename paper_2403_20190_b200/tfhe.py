@@ -599,7 +599,7 @@ def blind_rotate_batch(params: HeParams, acc, ggsw, exps):
         raise TfheError("selector/exponent length mismatch")
     e = e.to(t.device).contiguous()
     cp = _lib.c_params(params)
-    _lib.check(_lib.load().hwb_blind_rotate(ctypes.byref(cp), _ptr(ntt.data), _ptr(e), _ptr(t),
+    _lib.check(_lib.load().hwb_blind_rotate(ctypes.byref(cp), _ptr(ntt.data), None, _ptr(e), _ptr(t),
                                             ntt.count, B, _stream()))
     return _wrap(acc, t)
 
