@@ -154,3 +154,26 @@ def test_pack_batch_and_he_infer_pd_match_reference():
     assert_u32_equal(packs[0].packed, g["infer_packed"])
     assert_u32_equal(packs[2].packed, g["infer_packed"])
     assert_u32_equal(packs[1].packed, hewnn.he_infer_pd(model, smp[0], pksk).packed)
+
+
+@pytest.mark.parametrize("cfg", [1, 3, 4, 5])
+def test_full_geometry_training_vs_oracle(cfg):
+    """BASELINE configs' real geometries (cfg4: N = 2048, a = 16, 9 tree levels,
+    512 polynomials per RAM row) on one encrypted image: GPU he_train is
+    bit-exact with the oracle's restatement of hw/hewnn.py:189-229, and (where
+    the noise budget allows) decrypts to train_integer."""
+    from paper_2403_20190_b200 import data
+    (s, l, a, r, p), pname = data.CONFIG_GEOMETRY[cfg]
+    P = named_params(pname, p)
+    geom = wnn.WisardGeometry(s, l, a, r, p)
+    ds = data.config_dataset(cfg, n=1, seed=5)
+    key = tfhe.SecretKey(P, tfhe.make_rng(6).integers(0, 2, P.n).astype(np.uint32))
+    smp = hewnn.encrypt_sample(ds.bits[0], int(ds.labels[0]), key, tfhe.make_rng(7), label_bits=geom.label_bits)
+    model = hewnn.he_train([smp], geom, P)
+    rams, counts = wnn32.he_train([tfhe.to_host(smp.rgsw)], s, l, a, r, P)
+    assert_u32_equal(tfhe.to_host(model.rams), rams)
+    assert_u32_equal(tfhe.to_host(model.counts_ct), counts)
+    if cfg != 4:
+        counters, cc = hewnn.decrypt_model(model, key)
+        ref, rc = wnn.train_integer(ds.bits, ds.labels, geom)
+        assert np.array_equal(counters, ref) and np.array_equal(cc.counts, rc.counts)
