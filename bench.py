@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--train-images", type=int, default=64, help="0 disables the training measurement")
     ap.add_argument("--train-batch", type=int, default=32)
     ap.add_argument("--infer-images", type=int, default=8, help="0 disables the inference measurement")
+    ap.add_argument("--sweep", default="1,16,148,592,1184,4096,16384,65536",
+                    help="comma-separated PBS batch sizes for the cfg2 sweep ('' disables)")
     return ap.parse_args()
 
 
@@ -404,6 +406,28 @@ def bench_hwb(args):
             "sample": f"{sample} cfg2 PBS of the same batch (oracle/c exact schoolbook, "
                       f"OpenMP {threads} threads, {cpu_model()})",
             "bit_exact_vs_gpu": bool(np.array_equal(ref_out, out_h[:sample]))}
+    if args.sweep:
+        # BASELINE cfg2 batch sweep 1..65536: PBS/s and per-batch latency, device-resident
+        sweep = {}
+        rng_s = tfhe.make_rng(ENC_SEED + 99)
+        for Bs in [int(x) for x in args.sweep.split(",")]:
+            ms_s = rng_s.integers(0, P.p, Bs)
+            lw = tfhe.to_device(tfhe.enc_lwe_batch(ms_s * P.delta, keys.lwe_key, rng_s))
+            tfhe.pbs_batch(P, lw, tv_d, bsk, ksk)                      # warm-up
+            reps = 3 if Bs <= 4096 else 1
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            s0.record()
+            for _ in range(reps):
+                res = tfhe.pbs_batch(P, lw, tv_d, bsk, ksk)
+            s1.record()
+            s1.synchronize()
+            t_ms = s0.elapsed_time(s1) / reps
+            ok_s = bool(np.array_equal(tfhe.dec_lwe_batch(tfhe.to_host(res), keys.lwe_key), expected(ms_s, P.p)))
+            sweep[str(Bs)] = {"pbs_per_s": round(Bs / (t_ms * 1e-3), 1), "latency_ms": round(t_ms, 3),
+                              "decrypt_ok": ok_s}
+            del lw, res
+        result["sweep"] = sweep
     if args.train_images > 0:
         result["train"] = bench_train(args, world, rank, torch, dist)
     if world > 1:
