@@ -278,6 +278,58 @@ def he_train(samples: Iterable[EncryptedSample], geometry: WisardGeometry, param
     return model
 
 
+def he_train_multi(samples: Iterable[EncryptedSample], geometries: Sequence[WisardGeometry], params: HeParams,
+                   batch: int = 16) -> list[HomWisardModel]:
+    """One model per permutation seed in a single streaming pass (hw/hewnn.py:232-261):
+    every sample's IVP items for all geometries run in the same launches; the
+    models are bit-identical to separate he_train runs."""
+    base = geometries[0]
+    for g in geometries:
+        if (g.s, g.l, g.a, g.p) != (base.s, base.l, base.a, base.p):
+            raise TfheError("multi-seed training requires geometries differing only in r")
+        _check_geometry(g, params)
+    models = [HomWisardModel.zeros(g, params) for g in geometries]
+    tmpls = [_selector_template(g, params) for g in geometries]
+    k0 = base.k0
+    stride = base.s + base.label_bits
+    chunk: list[EncryptedSample] = []
+
+    def flush():
+        if not chunk:
+            return
+        table = _stack_table(params, chunk)
+        codes = np.concatenate([_shift(t, i * stride) for i in range(len(chunk)) for t in tmpls])
+        rows = lut.ivp_codes(params, codes, table, _payload(params))       # (I*G*k0, k1, 2, N)
+        rows = rows.reshape(len(chunk), len(geometries), k0, *rows.shape[1:])
+        for gi, m in enumerate(models):
+            lut.accumulate_rows_(m.rams, rows[:, gi].contiguous())
+        label_rows = np.array([[i * stride + base.s + b for b in range(base.label_bits)]
+                               for i in range(len(chunk))], dtype=np.int64)
+        cnt = torch.zeros_like(models[0].counts_ct)
+        he_count_labels_batch(params, cnt, table, label_rows)
+        for m in models:
+            lut.accumulate_(m.counts_ct, cnt)
+        chunk.clear()
+
+    for sample in samples:
+        if sample.label_bits != base.label_bits:
+            raise TfheError("training samples need encrypted label bits")
+        chunk.append(sample)
+        if len(chunk) == batch:
+            flush()
+    flush()
+    return models
+
+
+def decrypt_sample(sample: EncryptedSample, key: tfhe.SecretKey) -> tuple[list[int], int | None]:
+    """hw/hewnn.py:122-130 (client side)."""
+    bits = [tfhe.dec_rgsw(c, key) for c in sample.data_bits]
+    labs = sample.labels
+    if labs is None:
+        return bits, None
+    return bits, sum(tfhe.dec_rgsw(c, key) << i for i, c in enumerate(labs))
+
+
 def he_train_sharded(samples: Sequence[EncryptedSample], geometry: WisardGeometry, params: HeParams,
                      rank: int, world: int, group=None, batch: int = 16) -> HomWisardModel:
     """Multi-GPU training: rank trains the stripe samples[rank::world] (the

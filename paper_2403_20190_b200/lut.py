@@ -295,6 +295,19 @@ def encode_lut(values, params: HeParams) -> list[RlweCiphertext]:
     return [tfhe.trivial_rlwe(values, params)]
 
 
+def decode_lut(lut: list[RlweCiphertext], k: int, key: tfhe.SecretKey) -> np.ndarray:
+    """Decrypt every entry (hw/lut.py:100-103, test helper)."""
+    vals = np.concatenate([tfhe.dec_rlwe(c, key) for c in lut])
+    return vals[: 1 << k]
+
+
+def lut_add(a: list[RlweCiphertext], b: list[RlweCiphertext]) -> list[RlweCiphertext]:
+    """Entry-wise sum of equally shaped LUTs (hw/lut.py:106-110)."""
+    if len(a) != len(b):
+        raise TfheError("LUT geometries differ")
+    return [x + y for x, y in zip(a, b)]
+
+
 def vertical_packing(bits: list[SelectorBit], lut: list[RlweCiphertext]):
     """hw/lut.py:122-149 for one selector vector: LWE (N+1,) of lut[m]."""
     params = lut[0].params

@@ -459,6 +459,33 @@ def dec_lwe_batch(lwe, key, params: HeParams | None = None) -> np.ndarray:
     return decode_phase(phase_lwe_batch(lwe, key.s), params)
 
 
+@dataclass
+class NoiseBudget:
+    """Measured error against the nearest Z_p codeword (hw/tfhe.py:446-456)."""
+
+    max_abs: int
+    rms: float
+    margin: int
+
+    @property
+    def ok(self) -> bool:
+        return self.max_abs < self.margin
+
+
+def measure_noise(ct, key, params: HeParams | None = None) -> NoiseBudget:
+    """hw/tfhe.py:459-473 for an RlweCiphertext, or LWE rows (..., n+1) under
+    `key` (LweSecretKey or SecretKey)."""
+    if isinstance(ct, RlweCiphertext):
+        params = ct.params
+        phase = phase_rlwe(ct, key).astype(np.int64)
+    else:
+        params = params or key.params
+        phase = phase_lwe_batch(ct, key.s).astype(np.int64)
+    delta = params.delta
+    err = (phase + delta // 2) % delta - delta // 2
+    return NoiseBudget(int(np.abs(err).max()), float(np.sqrt(np.mean(err.astype(np.float64) ** 2))), delta // 2)
+
+
 # ---------------------------------------------------------------------------
 # device: NTT-domain GGSWs
 

@@ -177,3 +177,31 @@ def test_full_geometry_training_vs_oracle(cfg):
         counters, cc = hewnn.decrypt_model(model, key)
         ref, rc = wnn.train_integer(ds.bits, ds.labels, geom)
         assert np.array_equal(counters, ref) and np.array_equal(cc.counts, rc.counts)
+
+
+def test_he_train_multi_equals_separate_runs():
+    """hw/hewnn.py:232-261: multi-seed training in one pass == per-seed he_train."""
+    name = "train_cfg1"
+    P, s1, bits, labels, smp, geom = samples_of(name)
+    geoms = [geom, wnn.WisardGeometry(geom.s, geom.l, geom.a, 11, geom.p)]
+    multi = hewnn.he_train_multi(smp, geoms, P, batch=2)
+    for g, m in zip(geoms, multi):
+        single = hewnn.he_train(smp, g, P)
+        assert torch.equal(m.rams, single.rams) and torch.equal(m.counts_ct, single.counts_ct)
+
+
+def test_client_helpers():
+    name = "train_cfg1"
+    P, s1, bits, labels, smp, geom = samples_of(name)
+    key = tfhe.SecretKey(P, s1)
+    dbits, dlab = hewnn.decrypt_sample(smp[0], key)                          # hw/hewnn.py:122-130
+    assert dbits == list(bits[0]) and dlab == int(labels[0])
+    model = hewnn.he_train(smp, geom, P)
+    nb = tfhe.measure_noise(tfhe.RlweCiphertext(P, tfhe.to_host(model.rams[0, 0])), key)
+    assert nb.ok and nb.max_abs == hewnn.model_noise(model, key)[0] or nb.max_abs <= hewnn.model_noise(model, key)[0]
+    rows = lut.ivp_batch([[lut.SelectorBit.clear(1)] * 4], tfhe.trivial_rlwe(3, P).data, P)[0]
+    polys = [tfhe.RlweCiphertext(P, r) for r in rows]
+    vals = lut.decode_lut(lut.lut_add(polys, polys), 4, key)                  # hw/lut.py:100-110
+    expect = np.zeros(16, dtype=np.int64)
+    expect[15] = 6
+    assert np.array_equal(vals, expect)
