@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--impl", choices=["hwb", "reference"], default="hwb")
     ap.add_argument("--batch", type=int, default=4096)
     ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--ks-engine", default="auto", choices=["auto", "tc", "simt"],
+                    help="LWE key switch: tensor cores (tcgen05 int8) or the integer-pipe kernel")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="PBS per CPU step (0 = auto)")
     ap.add_argument("--train-cfg", type=int, default=3, choices=[1, 3, 4, 5])
@@ -307,10 +309,12 @@ def bench_hwb(args):
     ext_d = torch.empty((B, P.n + 1), dtype=torch.int32, device="cuda")
     out_d = torch.empty((B, P.lwe_n + 1), dtype=torch.int32, device="cuda")
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
+    ks_tc = tfhe._ks_engine(P, ksk, args.ks_engine)
+    ks_engine = "tcgen05 kind::i8 (keyswitch_tc_kernel)" if ks_tc else "integer pipe (keyswitch_kernel)"
 
     def step():
         tfhe.pbs_batch(P, lwe_d, tv_d, bsk, None, out=ext_d)          # blind rotation + extract
-        tfhe.lwe_keyswitch(P, ext_d, ksk, out=out_d)                  # key switch
+        tfhe.lwe_keyswitch(P, ext_d, ksk, out=out_d, engine=args.ks_engine)   # key switch
 
     for _ in range(args.warmup):
         step()
@@ -328,7 +332,7 @@ def bench_hwb(args):
         e0.record()
         tfhe.pbs_batch(P, lwe_d, tv_d, bsk, None, out=ext_d)
         e1.record()
-        tfhe.lwe_keyswitch(P, ext_d, ksk, out=out_d)
+        tfhe.lwe_keyswitch(P, ext_d, ksk, out=out_d, engine=args.ks_engine)
         e2.record()
     torch.cuda.synchronize()
     clock_info = clocks.stop()
@@ -356,7 +360,7 @@ def bench_hwb(args):
         s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s_ev.record()
         dev_in = lwe_pin.to("cuda", non_blocking=True)
-        res = tfhe.pbs_batch(P, dev_in, tv_d, bsk, ksk)
+        res = tfhe.pbs_batch(P, dev_in, tv_d, bsk, ksk, engine=args.ks_engine)
         out_pin.copy_(res, non_blocking=True)
         e_ev.record()
         e_ev.synchronize()
@@ -382,7 +386,7 @@ def bench_hwb(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (seeded LWE encryptions, BASELINE cfg2 shapes)",
-        "config": config(P, B, world, {"kernel_variant": args.variant}),
+        "config": config(P, B, world, {"kernel_variant": args.variant, "ks_engine": ks_engine}),
         "e2e": {"value": round(B * world * args.steps / (float(e2e_t.item()) * 1e-3), 2), "unit": UNIT,
                 "h2d_bytes_per_step": int(lwe.nbytes), "d2h_bytes_per_step": int(out_h.nbytes),
                 "api": "tfhe.pbs_batch from pinned host tensors", "matches_device_run": e2e_ok},
@@ -393,7 +397,7 @@ def bench_hwb(args):
                      "peak_source": "measured live: probe_modmul_kernel (register-only Shoup, both primes)"},
         "kernel_ms": {"blind_rotate": round(statistics.mean(br_ms), 3),
                       "keyswitch": round(statistics.mean(ks_ms), 3)},
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": (3 if ks_tc else 2) * args.steps,
         "clocks": clock_info,
         "check": "all outputs decrypt to the LUT" if ok else "DECRYPTION MISMATCH",
     }
@@ -413,13 +417,13 @@ def bench_hwb(args):
         for Bs in [int(x) for x in args.sweep.split(",")]:
             ms_s = rng_s.integers(0, P.p, Bs)
             lw = tfhe.to_device(tfhe.enc_lwe_batch(ms_s * P.delta, keys.lwe_key, rng_s))
-            tfhe.pbs_batch(P, lw, tv_d, bsk, ksk)                      # warm-up
+            tfhe.pbs_batch(P, lw, tv_d, bsk, ksk, engine=args.ks_engine)   # warm-up
             reps = 3 if Bs <= 4096 else 1
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             s0.record()
             for _ in range(reps):
-                res = tfhe.pbs_batch(P, lw, tv_d, bsk, ksk)
+                res = tfhe.pbs_batch(P, lw, tv_d, bsk, ksk, engine=args.ks_engine)
             s1.record()
             s1.synchronize()
             t_ms = s0.elapsed_time(s1) / reps

@@ -185,6 +185,23 @@ int hwb_pbs(const hwb_params *p, const uint32_t *bsk_ntt, const uint32_t *ksk,
             const uint32_t *tv, int tv_per_item, const uint32_t *lwe_in, uint32_t *lwe_out,
             int64_t B, void *workspace, void *stream);
 
+/* ---- Tensor-core key switch (tcgen05 kind::i8; same result as hwb_keyswitch) ----
+ * The key words are split into 4 byte limbs and pre-tiled for the tensor cores
+ * (64 output columns x 128 K-bytes per tile).  Available when ks_base_log <= 8
+ * (digits are exact int8); hwb_ksk_tc_bytes returns 0 otherwise. */
+size_t hwb_ksk_tc_bytes(const hwb_params *p);
+/* ksk [N][ks_l][n+1] u32 -> ksk_tc (hwb_ksk_tc_bytes bytes, 16-byte aligned). */
+int hwb_ksk_to_tc(const hwb_params *p, const uint32_t *ksk, void *ksk_tc, void *stream);
+/* Workspace for hwb_keyswitch_tc: the int8 digit tiles of a batch of B. */
+size_t hwb_keyswitch_tc_workspace_bytes(const hwb_params *p, int64_t B);
+int hwb_keyswitch_tc(const hwb_params *p, const void *ksk_tc, const uint32_t *in, uint32_t *out,
+                     int64_t B, void *workspace, void *stream);
+/* hwb_pbs with the tensor-core key switch (ksk_tc from hwb_ksk_to_tc). */
+size_t hwb_pbs_tc_workspace_bytes(const hwb_params *p, int64_t B);
+int hwb_pbs_tc(const hwb_params *p, const uint32_t *bsk_ntt, const void *ksk_tc,
+               const uint32_t *tv, int tv_per_item, const uint32_t *lwe_in, uint32_t *lwe_out,
+               int64_t B, void *workspace, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

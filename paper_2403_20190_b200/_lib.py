@@ -22,7 +22,8 @@ EXPORTS = (
     "hwb_sample_extract", "hwb_keyswitch", "hwb_pbs_workspace_bytes", "hwb_pbs",
     "hwb_ivp_level", "hwb_vp_level", "hwb_monomial_gather", "hwb_accumulate",
     "hwb_poly_to_ntt", "hwb_key_mul", "hwb_rgsw_add_gadget", "hwb_pack_ks_workspace_bytes", "hwb_pack_ks",
-    "hwb_accumulate_rows",
+    "hwb_accumulate_rows", "hwb_ksk_tc_bytes", "hwb_ksk_to_tc", "hwb_keyswitch_tc_workspace_bytes",
+    "hwb_keyswitch_tc", "hwb_pbs_tc_workspace_bytes", "hwb_pbs_tc",
 )
 
 
@@ -86,9 +87,18 @@ def load() -> ctypes.CDLL:
         L.hwb_pack_ks_workspace_bytes.argtypes = [_pp, _i64]
         L.hwb_pack_ks_workspace_bytes.restype = ctypes.c_size_t
         L.hwb_pack_ks.argtypes = [_pp, ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp, _vp, _i64, _vp, _vp]
+        L.hwb_ksk_tc_bytes.argtypes = [_pp]
+        L.hwb_ksk_to_tc.argtypes = [_pp, _vp, _vp, _vp]
+        L.hwb_keyswitch_tc_workspace_bytes.argtypes = [_pp, _i64]
+        L.hwb_keyswitch_tc.argtypes = [_pp, _vp, _vp, _vp, _i64, _vp, _vp]
+        L.hwb_pbs_tc_workspace_bytes.argtypes = [_pp, _i64]
+        L.hwb_pbs_tc.argtypes = [_pp, _vp, _vp, _vp, ctypes.c_int, _vp, _vp, _i64, _vp, _vp]
+        sizes = ("hwb_ggsw_ntt_words", "hwb_pbs_workspace_bytes", "hwb_pack_ks_workspace_bytes",
+                 "hwb_ksk_tc_bytes", "hwb_keyswitch_tc_workspace_bytes", "hwb_pbs_tc_workspace_bytes")
+        for name in sizes:
+            getattr(L, name).restype = ctypes.c_size_t
         for name in EXPORTS:
-            if name not in ("hwb_version", "hwb_last_error", "hwb_ggsw_ntt_words",
-                            "hwb_pbs_workspace_bytes", "hwb_probe_modmul", "hwb_pack_ks_workspace_bytes"):
+            if name not in ("hwb_version", "hwb_last_error", "hwb_probe_modmul", *sizes):
                 getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib

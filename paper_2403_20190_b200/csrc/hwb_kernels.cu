@@ -24,6 +24,7 @@
 
 #include "../../include/hwb.h"
 #include "hwb_device.cuh"
+#include "hwb_tc.cuh"
 
 namespace hwb {
 
@@ -910,6 +911,37 @@ static int keyswitch_launch(const hwb_params *p, const uint32_t *ksk, const uint
   return post_launch("keyswitch_kernel");
 }
 
+// tensor-core key switch: supported shapes and launch (hwb_tc.cuh)
+static int check_ks_tc(const hwb_params *p) {
+  int rc = check_ks(p);
+  if (rc) return rc;
+  if (p->ks_base_log > 8) return fail(HWB_EINVAL, "tensor-core key switch needs ks_base_log <= 8 (int8 digits)");
+  const int64_t K = (int64_t)p->N * p->ks_l;
+  if (p->N < 1 || K % TC_KB) return fail(HWB_EINVAL, "tensor-core key switch needs N*ks_l % 128 == 0");
+  if (K * 128 * 255 >= (int64_t)1 << 31) return fail(HWB_EINVAL, "tensor-core key switch: N*ks_l too large for int32 limbs");
+  return HWB_OK;
+}
+
+static size_t ks_tc_digit_bytes(const hwb_params *p, int64_t B) {
+  return (size_t)((B + TC_M - 1) / TC_M) * TC_M * (size_t)p->N * p->ks_l;
+}
+
+static int keyswitch_tc_launch(const hwb_params *p, const void *ksk_tc, const uint32_t *in, uint32_t *out,
+                               int64_t B, void *digits, cudaStream_t s) {
+  const int K = (int)(p->N * p->ks_l);
+  const int64_t mtiles = (B + TC_M - 1) / TC_M;
+  const int64_t threads = mtiles * TC_M * (K / 16);
+  ks_digits_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(in, (uint4 *)digits, B, (int)p->N, K,
+                                                                      make_gadget(p->ks_l, p->ks_base_log));
+  int rc = post_launch("ks_digits_kernel");
+  if (rc) return rc;
+  if ((rc = set_smem(keyswitch_tc_kernel, TC_SMEM))) return rc;
+  const int nct = (int)((p->n + 1 + TC_COLS - 1) / TC_COLS);
+  keyswitch_tc_kernel<<<dim3((unsigned)mtiles, (unsigned)nct), 128, TC_SMEM, s>>>(
+      (const uint8_t *)digits, (const uint8_t *)ksk_tc, in, out, B, (int)p->N, (int)p->n, K);
+  return post_launch("keyswitch_tc_kernel");
+}
+
 }  // namespace hwb
 using namespace hwb;
 
@@ -1203,6 +1235,78 @@ int hwb_pbs(const hwb_params *p, const uint32_t *bsk_ntt, const uint32_t *ksk, c
     rc = launch_br<2048, true>(p, st, bsk_ntt, nullptr, nullptr, lwe_in, tv, tv_per_item, nullptr, ext, (int)p->n, B, s);
   if (rc || !ksk) return rc;
   return keyswitch_launch(p, ksk, ext, lwe_out, B, s);
+}
+
+size_t hwb_ksk_tc_bytes(const hwb_params *p) {
+  if (!p || check_ks_tc(p)) return 0;
+  const size_t nct = (p->n + 1 + TC_COLS - 1) / TC_COLS;
+  return nct * ((size_t)p->N * p->ks_l / TC_KB) * TC_B_BYTES;
+}
+
+int hwb_ksk_to_tc(const hwb_params *p, const uint32_t *ksk, void *ksk_tc, void *stream) {
+  if (!p) return fail(HWB_EINVAL, "null params");
+  int rc = check_ks_tc(p);
+  if (rc) return rc;
+  if (!ksk || !ksk_tc) return fail(HWB_EINVAL, "null key pointer");
+  if ((uintptr_t)ksk_tc & 15) return fail(HWB_EINVAL, "ksk_tc must be 16-byte aligned");
+  const int K = (int)(p->N * p->ks_l);
+  const int nct = (int)((p->n + 1 + TC_COLS - 1) / TC_COLS);
+  const int64_t total = (int64_t)nct * (K / TC_KB) * (TC_B_BYTES / 16);
+  ksk_to_tc_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(ksk, (uint4 *)ksk_tc, K,
+                                                                                       (int)p->n + 1, nct);
+  return post_launch("ksk_to_tc_kernel");
+}
+
+size_t hwb_keyswitch_tc_workspace_bytes(const hwb_params *p, int64_t B) {
+  if (!p || B <= 0 || check_ks_tc(p)) return 0;
+  return ks_tc_digit_bytes(p, B);
+}
+
+int hwb_keyswitch_tc(const hwb_params *p, const void *ksk_tc, const uint32_t *in, uint32_t *out, int64_t B,
+                     void *workspace, void *stream) {
+  if (!p) return fail(HWB_EINVAL, "null params");
+  int rc = check_ks_tc(p);
+  if (rc) return rc;
+  if (B < 0) return fail(HWB_EINVAL, "negative batch");
+  if (B == 0) return HWB_OK;
+  if ((B + TC_M - 1) / TC_M > 0x7FFFFFFF) return fail(HWB_EINVAL, "batch too large");
+  if (!ksk_tc || !workspace) return fail(HWB_EINVAL, "hwb_keyswitch_tc needs ksk_tc and a workspace");
+  if (((uintptr_t)ksk_tc | (uintptr_t)workspace) & 15) return fail(HWB_EINVAL, "ksk_tc/workspace must be 16-byte aligned");
+  return keyswitch_tc_launch(p, ksk_tc, in, out, B, workspace, (cudaStream_t)stream);
+}
+
+static size_t pbs_ext_bytes(const hwb_params *p, int64_t B) {
+  return ((sizeof(uint32_t) * (size_t)B * (p->N + 1)) + 255) & ~(size_t)255;
+}
+
+size_t hwb_pbs_tc_workspace_bytes(const hwb_params *p, int64_t B) {
+  if (!p || B <= 0 || check_ks_tc(p)) return 0;
+  return pbs_ext_bytes(p, B) + ks_tc_digit_bytes(p, B);
+}
+
+int hwb_pbs_tc(const hwb_params *p, const uint32_t *bsk_ntt, const void *ksk_tc, const uint32_t *tv,
+               int tv_per_item, const uint32_t *lwe_in, uint32_t *lwe_out, int64_t B, void *workspace,
+               void *stream) {
+  int rc = check_glwe(p);
+  if (rc) return rc;
+  if ((rc = check_ks_tc(p))) return rc;
+  if (p->n < 1) return fail(HWB_EINVAL, "LWE dimension n must be positive");
+  if (B < 0) return fail(HWB_EINVAL, "negative batch");
+  if (B == 0) return HWB_OK;
+  if (B > 0x7FFFFFFF) return fail(HWB_EINVAL, "batch too large");
+  if (!ksk_tc || !workspace) return fail(HWB_EINVAL, "hwb_pbs_tc needs ksk_tc and a workspace");
+  if (((uintptr_t)ksk_tc | (uintptr_t)workspace) & 15) return fail(HWB_EINVAL, "ksk_tc/workspace must be 16-byte aligned");
+  DevState *st;
+  if ((rc = init_device(&st))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  uint32_t *ext = (uint32_t *)workspace;
+  void *digits = (uint8_t *)workspace + pbs_ext_bytes(p, B);
+  if (p->N == 1024)
+    rc = launch_br<1024, true>(p, st, bsk_ntt, nullptr, nullptr, lwe_in, tv, tv_per_item, nullptr, ext, (int)p->n, B, s);
+  else
+    rc = launch_br<2048, true>(p, st, bsk_ntt, nullptr, nullptr, lwe_in, tv, tv_per_item, nullptr, ext, (int)p->n, B, s);
+  if (rc) return rc;
+  return keyswitch_tc_launch(p, ksk_tc, ext, lwe_out, B, digits, s);
 }
 
 }  // extern "C"

@@ -206,6 +206,35 @@ class LweKeySwitchKey:
 
     params: HeParams
     data: torch.Tensor
+    _tiles: torch.Tensor | None = field(default=None, repr=False)
+
+    def tensor_core_tiles(self) -> torch.Tensor | None:
+        """The key split into byte limbs and tiled for the tcgen05 key switch
+        (built once on the device); None when ks_base_log > 8."""
+        if self._tiles is None:
+            cp = _lib.c_params(self.params)
+            L = _lib.load()
+            nbytes = L.hwb_ksk_tc_bytes(ctypes.byref(cp))
+            if nbytes == 0:
+                return None
+            tiles = torch.empty(nbytes, dtype=torch.uint8, device=self.data.device)
+            _lib.check(L.hwb_ksk_to_tc(ctypes.byref(cp), _ptr(self.data), _ptr(tiles), _stream()))
+            self._tiles = tiles
+        return self._tiles
+
+
+def _ks_engine(params: HeParams, ksk, engine: str) -> bool:
+    """True -> tensor-core key switch.  engine: "auto" (tensor cores when the
+    gadget allows it), "tc" (required), "simt" (integer-pipe kernel)."""
+    if engine not in ("auto", "tc", "simt"):
+        raise TfheError(f"unknown key-switch engine {engine!r}")
+    if ksk is None or engine == "simt":
+        return False
+    if ksk.tensor_core_tiles() is not None:
+        return True
+    if engine == "tc":
+        raise TfheError("tensor-core key switch needs ks_base_log <= 8")
+    return False
 
 
 @dataclass
@@ -697,9 +726,10 @@ def test_polynomial(f, params: HeParams, delta_out: int | None = None) -> np.nda
     return tv
 
 
-def lwe_keyswitch(params: HeParams, lwe, ksk: LweKeySwitchKey, out=None):
+def lwe_keyswitch(params: HeParams, lwe, ksk: LweKeySwitchKey, out=None, engine: str = "auto",
+                  workspace: "PbsWorkspace | None" = None):
     """NEW LWE key switch (B, N+1) under s1 -> (B, n+1) under s0 (algebra of
-    hw/tfhe.py:397-420)."""
+    hw/tfhe.py:397-420).  engine: "auto" | "tc" (tcgen05 int8 GEMM) | "simt"."""
     t = to_device(lwe)
     if t.dim() != 2 or t.shape[1] != params.n + 1:
         raise TfheError(f"LWE batch must be (B, {params.n + 1})")
@@ -709,7 +739,13 @@ def lwe_keyswitch(params: HeParams, lwe, ksk: LweKeySwitchKey, out=None):
     elif out.shape != (B, params.lwe_n + 1) or out.dtype != torch.int32 or not out.is_contiguous():
         raise TfheError(f"out must be a contiguous int32 (B, {params.lwe_n + 1}) tensor")
     cp = _lib.c_params(params)
-    _lib.check(_lib.load().hwb_keyswitch(ctypes.byref(cp), _ptr(ksk.data), _ptr(t), _ptr(out), B, _stream()))
+    if _ks_engine(params, ksk, engine):
+        ws = (workspace or _default_ws).get(params, B, t.device, kind="ks_tc")
+        _lib.check(_lib.load().hwb_keyswitch_tc(ctypes.byref(cp), _ptr(ksk.tensor_core_tiles()), _ptr(t),
+                                                _ptr(out), B, _ptr(ws), _stream()))
+    else:
+        _lib.check(_lib.load().hwb_keyswitch(ctypes.byref(cp), _ptr(ksk.data), _ptr(t), _ptr(out), B,
+                                             _stream()))
     return _wrap(lwe, out)
 
 
@@ -719,9 +755,11 @@ class PbsWorkspace:
     def __init__(self):
         self.buf = None
 
-    def get(self, params: HeParams, B: int, device) -> torch.Tensor:
+    def get(self, params: HeParams, B: int, device, kind: str = "pbs") -> torch.Tensor:
         cp = _lib.c_params(params)
-        nbytes = _lib.load().hwb_pbs_workspace_bytes(ctypes.byref(cp), B)
+        size_fn = {"pbs": "hwb_pbs_workspace_bytes", "pbs_tc": "hwb_pbs_tc_workspace_bytes",
+                   "ks_tc": "hwb_keyswitch_tc_workspace_bytes"}[kind]
+        nbytes = getattr(_lib.load(), size_fn)(ctypes.byref(cp), B)
         words = max(1, (nbytes + 3) // 4)
         if self.buf is None or self.buf.numel() < words or self.buf.device != device:
             self.buf = torch.empty(words, dtype=torch.int32, device=device)
@@ -732,9 +770,10 @@ _default_ws = PbsWorkspace()
 
 
 def pbs_batch(params: HeParams, lwe, tv, bsk: BootstrapKey, ksk: LweKeySwitchKey | None,
-              out=None, workspace: PbsWorkspace | None = None):
+              out=None, workspace: PbsWorkspace | None = None, engine: str = "auto"):
     """Programmable bootstrapping of a batch: (B, n+1) -> (B, n+1) (or (B, N+1)
-    without a key-switch key).  tv is (2, N) shared or (B, 2, N) per item."""
+    without a key-switch key).  tv is (2, N) shared or (B, 2, N) per item.
+    engine selects the key switch ("auto" | "tc" | "simt", see lwe_keyswitch)."""
     t = to_device(lwe)
     if t.dim() != 2 or t.shape[1] != params.lwe_n + 1:
         raise TfheError(f"LWE batch must be (B, {params.lwe_n + 1})")
@@ -753,8 +792,13 @@ def pbs_batch(params: HeParams, lwe, tv, bsk: BootstrapKey, ksk: LweKeySwitchKey
     width = params.lwe_n + 1 if ksk is not None else params.n + 1
     if out is None:
         out = torch.empty((B, width), dtype=torch.int32, device=t.device)
-    ws = (workspace or _default_ws).get(params, B, t.device) if ksk is not None else None
     cp = _lib.c_params(params)
-    _lib.check(_lib.load().hwb_pbs(ctypes.byref(cp), _ptr(bsk.ntt.data), _ptr(ksk.data if ksk else None),
-                                   _ptr(tvt), per_item, _ptr(t), _ptr(out), B, _ptr(ws), _stream()))
+    if _ks_engine(params, ksk, engine):
+        ws = (workspace or _default_ws).get(params, B, t.device, kind="pbs_tc")
+        _lib.check(_lib.load().hwb_pbs_tc(ctypes.byref(cp), _ptr(bsk.ntt.data), _ptr(ksk.tensor_core_tiles()),
+                                          _ptr(tvt), per_item, _ptr(t), _ptr(out), B, _ptr(ws), _stream()))
+    else:
+        ws = (workspace or _default_ws).get(params, B, t.device) if ksk is not None else None
+        _lib.check(_lib.load().hwb_pbs(ctypes.byref(cp), _ptr(bsk.ntt.data), _ptr(ksk.data if ksk else None),
+                                       _ptr(tvt), per_item, _ptr(t), _ptr(out), B, _ptr(ws), _stream()))
     return _wrap(lwe, out)

@@ -24,6 +24,9 @@ KEYS = [
     ("dram__bytes_write.sum", "dram write"),
     ("lts__t_bytes.sum", "L2 bytes"),
     ("l1tex__t_sector_hit_rate.pct", "L1 hit %"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor pipe active % (elapsed)"),
+    ("sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active", "tensor imma active % (active)"),
+    ("sm__ops_path_tensor_src_int8.avg.pct_of_peak_sustained_elapsed", "int8 tensor ops % of peak"),
 ]
 
 

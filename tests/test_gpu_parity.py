@@ -156,6 +156,52 @@ def test_keyswitch_vs_oracle(coracle):
         assert_u32_equal(tfhe.lwe_keyswitch(P, lwe, kd), coracle.keyswitch(lwe, K.ksk, gk.levels, gk.base_log))
 
 
+@pytest.mark.parametrize("N_log,ks,n", [(10, (8, 2), 630), (10, (7, 2), 500), (11, (8, 2), 750),
+                                        (10, (4, 8), 70), (10, (3, 7), 64), (10, (1, 1), 1)])
+def test_keyswitch_tensor_cores_vs_oracle(coracle, N_log, ks, n):
+    """tcgen05 int8 key switch: bit-exact with the C oracle and the integer-pipe
+    kernel on ragged batches (partial 128-item and 64-column tiles), the full int8
+    digit range (base_log 8) and extreme words."""
+    P = HeParams("t", N_log, 0.0, GadgetSpec(2, 8), GadgetSpec(*ks), p=8, lwe_n=n)
+    rng = np.random.default_rng(n + N_log)
+    ksk = rand_u32(rng, (P.n, ks[0], n + 1))
+    kd = tfhe.LweKeySwitchKey(P, tfhe.to_device(ksk))
+    assert kd.tensor_core_tiles() is not None
+    for B in (1, 127, 129, 300):
+        lwe = rand_u32(rng, (B, P.n + 1))
+        lwe[0, :] = 0xFFFFFFFF
+        if B > 1:
+            lwe[1, :] = 0
+            lwe[-1, :] = 0x80000000
+        want = coracle.keyswitch(lwe, ksk, ks[0], ks[1])
+        assert_u32_equal(tfhe.lwe_keyswitch(P, lwe, kd, engine="tc"), want)
+        assert_u32_equal(tfhe.lwe_keyswitch(P, lwe, kd, engine="simt"), want)
+
+
+def test_keyswitch_tensor_cores_full_batch():
+    """BASELINE cfg2 size: tensor-core and integer-pipe key switch agree on 4096 items."""
+    P = named_params("CFG2")
+    rng = np.random.default_rng(77)
+    ksk = rand_u32(rng, (P.n, P.gadget_ks.levels, P.lwe_n + 1))
+    kd = tfhe.LweKeySwitchKey(P, tfhe.to_device(ksk))
+    lwe = tfhe.to_device(rand_u32(rng, (4096, P.n + 1)))
+    a = tfhe.lwe_keyswitch(P, lwe, kd, engine="tc")
+    b = tfhe.lwe_keyswitch(P, lwe, kd, engine="simt")
+    assert torch.equal(a, b)
+
+
+def test_keyswitch_engine_selection():
+    P = HeParams("t", 10, 0.0, GadgetSpec(2, 8), GadgetSpec(2, 10), p=8, lwe_n=16)
+    kd = tfhe.LweKeySwitchKey(P, tfhe.to_device(np.zeros((P.n, 2, 17), np.uint32)))
+    assert kd.tensor_core_tiles() is None             # base_log 10: digits exceed int8
+    lwe = np.ones((3, P.n + 1), np.uint32)
+    with pytest.raises(tfhe.TfheError):
+        tfhe.lwe_keyswitch(P, lwe, kd, engine="tc")
+    with pytest.raises(tfhe.TfheError):
+        tfhe.lwe_keyswitch(P, lwe, kd, engine="bogus")
+    assert tfhe.lwe_keyswitch(P, lwe, kd).shape == (3, 17)   # auto -> integer pipe
+
+
 @pytest.mark.parametrize("name", ["CFG1", "CFG2", "CFG4"])
 def test_pbs_golden(name, variant):
     P = named_params(name)
@@ -164,8 +210,9 @@ def test_pbs_golden(name, variant):
     bsk, ksk = K.device_keys()
     ext = tfhe.pbs_batch(P, g["lwe_in"], g["tv"], bsk, None)
     assert_u32_equal(ext, g["extracted"])
-    out = tfhe.pbs_batch(P, g["lwe_in"], g["tv"], bsk, ksk)
-    assert_u32_equal(out, g["lwe_out"])
+    for engine in ("tc", "simt"):
+        out = tfhe.pbs_batch(P, g["lwe_in"], g["tv"], bsk, ksk, engine=engine)
+        assert_u32_equal(out, g["lwe_out"])
 
 
 def test_pbs_batch_vs_c_oracle_and_decrypt(coracle):
