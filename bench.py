@@ -180,6 +180,26 @@ def probe_modmul_peak(torch, _lib, tfhe):
     return best
 
 
+def probe_i8mma_peak(torch, _lib, tfhe):
+    """Measured P_i8: tcgen05.mma kind::i8 MAC rate of the key switch's MMA shape
+    (M128 N256 K32 from shared memory, one CTA per SM), best of 4."""
+    import ctypes
+    sink = torch.zeros(4, dtype=torch.int32, device="cuda")
+    L = _lib.load()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    best = 0.0
+    for _ in range(4):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        n = L.hwb_probe_i8mma(ctypes.c_void_p(sink.data_ptr()), sms, 4096, tfhe._stream())
+        e.record()
+        e.synchronize()
+        if n < 0:
+            raise RuntimeError(L.hwb_last_error().decode())
+        best = max(best, n / (s.elapsed_time(e) * 1e-3))
+    return best
+
+
 def bench_train(args, world, rank, torch, dist):
     """Encrypted WiSARD training throughput (the metric's second half):
     hewnn.he_train over `--train-images` client-encrypted images of BASELINE
@@ -379,6 +399,15 @@ def bench_hwb(args):
     w_mm = P.lwe_n * w_cmux
     br_avg_s = statistics.mean(br_ms) * 1e-3
     achieved = w_mm * B / br_avg_s
+    # key switch: W_ks int32 MACs; on tensor cores 4 byte limbs
+    w_ks = P.n * P.gadget_ks.levels * (P.lwe_n + 1)
+    ks_avg_s = statistics.mean(ks_ms) * 1e-3
+    if ks_tc:
+        p_ks, ks_unit, w_ks_eff = probe_i8mma_peak(torch, _lib, tfhe), "int8 MAC/s", 4 * w_ks
+    else:
+        p_ks, ks_unit, w_ks_eff = None, "int32 MAC/s", w_ks
+    # PBS-level roofline: 1 / (W_mm/P_mm + W_ks/P_ks)
+    pbs_roof = 1.0 / (w_mm / peak + (w_ks_eff / p_ks if p_ks else 0.0))
 
     value = B * world * args.steps / (max_ms * 1e-3)
     result = {
@@ -394,7 +423,17 @@ def bench_hwb(args):
                      "achieved": round(achieved / 1e9, 2), "peak": round(peak / 1e9, 2),
                      "unit": "Gmodmul/s", "frac": round(achieved / peak, 4), "traffic": None,
                      "work_per_pbs": f"W_mm = {w_mm} RNS modmuls (n x 53,248 per CMUX)",
-                     "peak_source": "measured live: probe_modmul_kernel (register-only Shoup, both primes)"},
+                     "peak_source": "measured live: probe_modmul_kernel (register-only Shoup, both primes)",
+                     "pbs": {"roofline_pbs_per_s": round(pbs_roof, 1),
+                             "frac": round(B / (max_ms / args.steps * 1e-3) / pbs_roof, 4),
+                             "formula": "1 / (W_mm/P_mm + 4 W_ks/P_i8)" if ks_tc else "W_mm/P_mm only"},
+                     "keyswitch": {"bound": "tensor" if ks_tc else "int", "kernel": ks_engine,
+                                   "achieved": round(w_ks_eff * B / ks_avg_s / 1e12, 3),
+                                   "peak": round(p_ks / 1e12, 3) if p_ks else None, "unit": "T" + ks_unit,
+                                   "frac": round(w_ks_eff * B / ks_avg_s / p_ks, 4) if p_ks else None,
+                                   "work_per_pbs": f"{w_ks_eff} MACs",
+                                   "peak_source": "measured live: probe_i8mma_kernel (M128 N256 K32 from smem)"
+                                   if ks_tc else None}},
         "kernel_ms": {"blind_rotate": round(statistics.mean(br_ms), 3),
                       "keyswitch": round(statistics.mean(ks_ms), 3)},
         "gpu_launches": (3 if ks_tc else 2) * args.steps,

@@ -65,6 +65,12 @@ int hwb_set_variant(int v);
  * Its rate is P_mm, the integer-pipe roofline denominator. */
 int64_t hwb_probe_modmul(uint32_t *sink, int32_t blocks, int32_t iters, void *stream);
 
+/* Tensor-core throughput probe (NEW): `blocks` CTAs (one per SM) each issue
+ * iters x 4 tcgen05.mma kind::i8 M128 N256 K32 from shared memory into TMEM,
+ * the key switch's MMA shape.  Returns the int8 MACs enqueued (the caller times
+ * the stream), or -HWB_E* on error.  Its rate is P_i8. */
+int64_t hwb_probe_i8mma(uint32_t *sink, int32_t blocks, int32_t iters, void *stream);
+
 /* Number of uint32 words of one GGSW in the NTT domain used by every kernel:
  * 2l rows x 2 components x 2 RNS primes x N. */
 size_t hwb_ggsw_ntt_words(const hwb_params *p);

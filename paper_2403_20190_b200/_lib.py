@@ -23,7 +23,7 @@ EXPORTS = (
     "hwb_ivp_level", "hwb_vp_level", "hwb_monomial_gather", "hwb_accumulate",
     "hwb_poly_to_ntt", "hwb_key_mul", "hwb_rgsw_add_gadget", "hwb_pack_ks_workspace_bytes", "hwb_pack_ks",
     "hwb_accumulate_rows", "hwb_ksk_tc_bytes", "hwb_ksk_to_tc", "hwb_keyswitch_tc_workspace_bytes",
-    "hwb_keyswitch_tc", "hwb_pbs_tc_workspace_bytes", "hwb_pbs_tc",
+    "hwb_keyswitch_tc", "hwb_pbs_tc_workspace_bytes", "hwb_pbs_tc", "hwb_probe_i8mma",
 )
 
 
@@ -64,6 +64,8 @@ def load() -> ctypes.CDLL:
         L.hwb_set_variant.argtypes = [ctypes.c_int]
         L.hwb_probe_modmul.argtypes = [_vp, ctypes.c_int32, ctypes.c_int32, _vp]
         L.hwb_probe_modmul.restype = ctypes.c_int64
+        L.hwb_probe_i8mma.argtypes = [_vp, ctypes.c_int32, ctypes.c_int32, _vp]
+        L.hwb_probe_i8mma.restype = ctypes.c_int64
         L.hwb_ggsw_ntt_words.argtypes = [_pp]
         L.hwb_ggsw_ntt_words.restype = ctypes.c_size_t
         L.hwb_ggsw_to_ntt.argtypes = [_pp, _vp, _vp, _i64, _vp]
@@ -98,7 +100,7 @@ def load() -> ctypes.CDLL:
         for name in sizes:
             getattr(L, name).restype = ctypes.c_size_t
         for name in EXPORTS:
-            if name not in ("hwb_version", "hwb_last_error", "hwb_probe_modmul", *sizes):
+            if name not in ("hwb_version", "hwb_last_error", "hwb_probe_modmul", "hwb_probe_i8mma", *sizes):
                 getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib

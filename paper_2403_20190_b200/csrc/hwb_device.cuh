@@ -74,6 +74,13 @@ __device__ __forceinline__ uint32_t mont_mul(uint32_t a, uint32_t b, uint32_t p,
   return hi - __umulhi(m, p) + p;
 }
 
+// Montgomery reduction of a 64-bit sum T < 2^63.01 (signed variant, pinv = p^-1
+// mod 2^32): T * 2^-32 mod p in (0, 7p).
+__device__ __forceinline__ uint32_t redc64(uint64_t T, uint32_t p, uint32_t pinv) {
+  const uint32_t m = (uint32_t)T * pinv;
+  return (uint32_t)(T >> 32) - __umulhi(m, p) + p;
+}
+
 // Harvey lazy Cooley-Tukey butterfly: X, Y in [0, 4p) -> [0, 4p).
 __device__ __forceinline__ void ct_bfly(uint32_t &X, uint32_t &Y, uint32_t w, uint32_t wq,
                                         uint32_t p, uint32_t two_p) {

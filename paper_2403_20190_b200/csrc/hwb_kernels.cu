@@ -49,6 +49,9 @@ static int fail(int code, const std::string &msg) {
 #ifndef HWB_V1_MINB
 #define HWB_V1_MINB 6
 #endif
+#ifndef HWB_ACC64
+#define HWB_ACC64 0
+#endif
 template <int N> struct Cfg {
   static constexpr int TPP = (N == 1024) ? 32 : 64;
   static constexpr int THREADS = 2 * TPP;
@@ -240,7 +243,14 @@ __device__ __forceinline__ void ext_product_core_p(Smem<N> &sm, const uint32_t *
   const int L = (int)g.levels;
   const uint2 *twf = w ? tw.fwd[1] : tw.fwd[0];
   const uint2 *twi = w ? tw.inv[1] : tw.inv[0];
+#if HWB_ACC64
+  // 64-bit accumulation of the 2l products (IMAD.WIDE with accumulate), one
+  // Montgomery reduction per output: x < 2^32, G < p < 2^28.42, 2l <= 6 terms
+  // -> sum < 2^63.01; REDC gives hi - umulhi(m, p) + p < 7p.
+  uint64_t a0[C], a1[C];
+#else
   uint32_t a0[C], a1[C];
+#endif
 #pragma unroll
   for (int j = 0; j < C; ++j) a0[j] = a1[j] = 0;
 
@@ -260,6 +270,16 @@ __device__ __forceinline__ void ext_product_core_p(Smem<N> &sm, const uint32_t *
     for (int jq = 0; jq < C / 4; ++jq) {
       const uint4 G0 = __ldg(slice_vec<TPP>(g0, t, jq));
       const uint4 G1 = __ldg(slice_vec<TPP>(g1, t, jq));
+#if HWB_ACC64
+      a0[4 * jq + 0] += (uint64_t)x[4 * jq + 0] * G0.x;
+      a0[4 * jq + 1] += (uint64_t)x[4 * jq + 1] * G0.y;
+      a0[4 * jq + 2] += (uint64_t)x[4 * jq + 2] * G0.z;
+      a0[4 * jq + 3] += (uint64_t)x[4 * jq + 3] * G0.w;
+      a1[4 * jq + 0] += (uint64_t)x[4 * jq + 0] * G1.x;
+      a1[4 * jq + 1] += (uint64_t)x[4 * jq + 1] * G1.y;
+      a1[4 * jq + 2] += (uint64_t)x[4 * jq + 2] * G1.z;
+      a1[4 * jq + 3] += (uint64_t)x[4 * jq + 3] * G1.w;
+#else
       a0[4 * jq + 0] += mont_mul(x[4 * jq + 0], G0.x, p, pinv);
       a0[4 * jq + 1] += mont_mul(x[4 * jq + 1], G0.y, p, pinv);
       a0[4 * jq + 2] += mont_mul(x[4 * jq + 2], G0.z, p, pinv);
@@ -268,23 +288,34 @@ __device__ __forceinline__ void ext_product_core_p(Smem<N> &sm, const uint32_t *
       a1[4 * jq + 1] += mont_mul(x[4 * jq + 1], G1.y, p, pinv);
       a1[4 * jq + 2] += mont_mul(x[4 * jq + 2], G1.z, p, pinv);
       a1[4 * jq + 3] += mont_mul(x[4 * jq + 3], G1.w, p, pinv);
+#endif
     }
   }
-  // 2l <= 6 terms in (0, 2p): sums < 12p < 2^32; reduce to [0, 2p)
+#if HWB_ACC64
+  uint32_t b0[C], b1[C];
 #pragma unroll
   for (int j = 0; j < C; ++j) {
-    uint32_t u = a0[j], v = a1[j];
+    b0[j] = redc64(a0[j], p, pinv);
+    b1[j] = redc64(a1[j], p, pinv);
+  }
+#else
+  uint32_t (&b0)[C] = a0, (&b1)[C] = a1;
+#endif
+  // sums < 16p: reduce to [0, 2p)
+#pragma unroll
+  for (int j = 0; j < C; ++j) {
+    uint32_t u = b0[j], v = b1[j];
     u = umin(u, u - 4 * two_p); v = umin(v, v - 4 * two_p);
     u = umin(u, u - 2 * two_p); v = umin(v, v - 2 * two_p);
     u = umin(u, u - two_p);     v = umin(v, v - two_p);
-    a0[j] = u; a1[j] = v;
+    b0[j] = u; b1[j] = v;
   }
   __syncthreads();   // both groups are done reading sm.v: it becomes the exchange buffer
 #pragma unroll 1
   for (int it = 0; it < 2; ++it) {
     const int c = it == 0 ? 1 - w : w;
 #pragma unroll
-    for (int j = 0; j < C; ++j) x[j] = c ? a1[j] : a0[j];
+    for (int j = 0; j < C; ++j) x[j] = c ? b1[j] : b0[j];
     inv_ntt<N, TPP, PRIME>(x, sm.scr[w], me.lay, t, w, twi);
 #pragma unroll
     for (int j = 0; j < C; ++j) x[j] = umin(x[j], x[j] - p);
@@ -954,6 +985,14 @@ int64_t hwb_probe_modmul(uint32_t *sink, int32_t blocks, int32_t iters, void *st
   probe_modmul_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(sink, iters);
   if (post_launch("probe_modmul_kernel")) return -HWB_ECUDA;
   return (int64_t)blocks * 256 * 8 * iters;
+}
+
+int64_t hwb_probe_i8mma(uint32_t *sink, int32_t blocks, int32_t iters, void *stream) {
+  if (blocks < 1 || iters < 1) return -fail(HWB_EINVAL, "probe needs positive blocks and iters");
+  if (set_smem(probe_i8mma_kernel, TC_SMEM)) return -HWB_ECUDA;
+  probe_i8mma_kernel<<<blocks, 128, TC_SMEM, (cudaStream_t)stream>>>(sink, iters);
+  if (post_launch("probe_i8mma_kernel")) return -HWB_ECUDA;
+  return (int64_t)blocks * iters * (TC_KB / 32) * TC_M * TC_N * 32;
 }
 
 int hwb_set_variant(int v) {

@@ -262,4 +262,60 @@ __global__ void __launch_bounds__(128, 1)
   }
 }
 
+// Throughput probe of the shipped MMA shape (kind::i8, M128 N256 K32, operands in
+// shared memory, accumulator in TMEM): one CTA per SM, `iters` x 4 back-to-back MMAs
+// into one accumulator, the same issue pattern as keyswitch_tc_kernel's K loop.
+// Its rate is P_i8 (int8 MACs/s), the tensor-core roofline denominator.
+__global__ void __launch_bounds__(128, 1) probe_i8mma_kernel(uint32_t *sink, int iters) {
+  extern __shared__ __align__(1024) uint8_t tc_smem[];
+  uint8_t *base = (uint8_t *)(((uintptr_t)tc_smem + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t done;
+  __shared__ uint32_t tmem_slot;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < TC_STAGE_BYTES / 16; i += blockDim.x)
+    reinterpret_cast<uint4 *>(base)[i] = make_uint4(i, i * 3u, i * 5u, i * 7u);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (threadIdx.x == 0) {
+    mbar_init(&done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
+                 "r"((uint32_t)TC_N));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_slot;
+  if (threadIdx.x == 0) {
+    const uint32_t sa = smem_u32(base), sb = sa + TC_A_BYTES;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int k = 0; k < TC_KB / 32; ++k) {
+        const uint64_t da = umma_desc(sa + k * 2 * (TC_M / 8) * 128, (TC_M / 8) * 128, 128);
+        const uint64_t db = umma_desc(sb + k * 2 * (TC_N / 8) * 128, (TC_N / 8) * 128, 128);
+        umma_i8(tmem, da, db, (it | k) != 0);
+      }
+    }
+    umma_commit(&done);
+  }
+  __syncwarp();
+  mbar_wait(&done, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  uint32_t v[16];
+  tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16), v);
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s ^= v[i];
+  if (s == 0x12345678u) sink[0] = s;
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)TC_N));
+  }
+}
+
 }  // namespace hwb

@@ -12,8 +12,10 @@ constexpr int ITERS = 4096;
 template <int OP>
 __global__ void bench(uint32_t *sink, uint32_t a, uint32_t b) {
   uint32_t x[CH], y[CH];
+  double xd[CH], yd[CH];
+  const double ad = 1.0000001 + a * 1e-12, wp = (double)a / 357900289.0;
 #pragma unroll
-  for (int k = 0; k < CH; ++k) { x[k] = threadIdx.x + k; y[k] = blockIdx.x * 7 + k; }
+  for (int k = 0; k < CH; ++k) { x[k] = threadIdx.x + k; y[k] = blockIdx.x * 7 + k; xd[k] = x[k]; yd[k] = y[k]; }
   for (int it = 0; it < ITERS; ++it) {
 #pragma unroll
     for (int k = 0; k < CH; ++k) {
@@ -24,11 +26,21 @@ __global__ void bench(uint32_t *sink, uint32_t a, uint32_t b) {
       if (OP == 4) { uint32_t q = __umulhi(x[k], a); x[k] = x[k] * b - q * 7u; }   // Shoup-like
       if (OP == 5) x[k] = (x[k] ^ y[k]) & a;                    // LOP3
       if (OP == 6) { x[k] = x[k] * a + y[k]; y[k] = y[k] + x[k] + b; }  // IMAD + IADD3 mix
+      if (OP == 7) xd[k] = fma(xd[k], ad, yd[k]);                // DFMA
+      if (OP == 8) { x[k] = x[k] * a + y[k]; xd[k] = fma(xd[k], ad, yd[k]); }   // IMAD || DFMA
+      if (OP == 9) {   // hybrid modmul: quotient on the FP64 pipe, remainder with 2 IMADs
+        const double qd = fma(xd[k], wp, 6755399441055744.0);   // 1.5 * 2^52: round to integer
+        const uint32_t q = (uint32_t)__double2loint(qd);
+        uint32_t r = x[k] * a - q * 357900289u;
+        r = min(r, r + 357900289u);
+        x[k] = r;
+        xd[k] = __hiloint2double(0x43300000, r) - 4503599627370496.0;
+      }
     }
   }
   uint32_t s = 0;
 #pragma unroll
-  for (int k = 0; k < CH; ++k) s ^= x[k] ^ y[k];
+  for (int k = 0; k < CH; ++k) s ^= x[k] ^ y[k] ^ (uint32_t)__double2loint(xd[k]);
   if (s == 0x9e3779b9u) sink[0] = s;
 }
 
@@ -70,5 +82,8 @@ int main() {
   run<4>("Shoup (HI + 2 IMAD)", 3, sms);
   run<5>("LOP3", 1, sms);
   run<6>("IMAD + IADD3", 2, sms);
+  run<7>("DFMA", 1, sms);
+  run<8>("IMAD || DFMA (independent)", 2, sms);
+  run<9>("hybrid modmul (DFMA q, 2 IMAD)", 1, sms);
   return 0;
 }
