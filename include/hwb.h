@@ -58,6 +58,13 @@ const char *hwb_last_error(void);
  * the switch exists for A/B measurement (bench.py --variant). */
 int hwb_set_variant(int v);
 
+/* Batches of at most max_batch ciphertexts (N = 1024, no per-item GGSW index)
+ * run the latency-mode ladder: one ciphertext per CTA of 4l warps, one warp per
+ * (digit, prime) transform.  Bit-identical to the throughput kernel.  -1 selects
+ * the automatic threshold (3 x SM count, the default); < -1 only queries.
+ * Returns the previous setting. */
+int64_t hwb_set_latency_batch(int64_t max_batch);
+
 /* Measurement probe (not a reference function): launches a register-only
  * kernel of `blocks` x 256 threads doing `iters` x 8 independent RNS modular
  * multiplications each (one Shoup product per prime).  Returns the number of

@@ -24,6 +24,7 @@ EXPORTS = (
     "hwb_poly_to_ntt", "hwb_key_mul", "hwb_rgsw_add_gadget", "hwb_pack_ks_workspace_bytes", "hwb_pack_ks",
     "hwb_accumulate_rows", "hwb_ksk_tc_bytes", "hwb_ksk_to_tc", "hwb_keyswitch_tc_workspace_bytes",
     "hwb_keyswitch_tc", "hwb_pbs_tc_workspace_bytes", "hwb_pbs_tc", "hwb_probe_i8mma",
+    "hwb_set_latency_batch",
 )
 
 
@@ -66,6 +67,8 @@ def load() -> ctypes.CDLL:
         L.hwb_probe_modmul.restype = ctypes.c_int64
         L.hwb_probe_i8mma.argtypes = [_vp, ctypes.c_int32, ctypes.c_int32, _vp]
         L.hwb_probe_i8mma.restype = ctypes.c_int64
+        L.hwb_set_latency_batch.argtypes = [_i64]
+        L.hwb_set_latency_batch.restype = ctypes.c_int64
         L.hwb_ggsw_ntt_words.argtypes = [_pp]
         L.hwb_ggsw_ntt_words.restype = ctypes.c_size_t
         L.hwb_ggsw_to_ntt.argtypes = [_pp, _vp, _vp, _i64, _vp]
@@ -100,7 +103,8 @@ def load() -> ctypes.CDLL:
         for name in sizes:
             getattr(L, name).restype = ctypes.c_size_t
         for name in EXPORTS:
-            if name not in ("hwb_version", "hwb_last_error", "hwb_probe_modmul", "hwb_probe_i8mma", *sizes):
+            if name not in ("hwb_version", "hwb_last_error", "hwb_probe_modmul", "hwb_probe_i8mma",
+                            "hwb_set_latency_batch", *sizes):
                 getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -124,3 +128,9 @@ def c_params(params) -> HwbParams:
 
 def set_variant(v: int) -> None:
     check(load().hwb_set_variant(int(v)))
+
+
+def set_latency_batch(max_batch: int) -> int:
+    """Batches of at most max_batch ciphertexts use the latency-mode ladder
+    (N = 1024); returns the previous threshold."""
+    return int(load().hwb_set_latency_batch(int(max_batch)))

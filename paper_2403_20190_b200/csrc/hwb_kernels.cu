@@ -32,6 +32,9 @@ static thread_local std::string g_err;
 // kernel variant: selects the register/occupancy build of the ladder kernels
 // (0 = default, 1 = alternative); both bit-identical, for A/B measurement.
 static int g_variant = 0;
+// batches up to this size run the latency-mode ladder (blind_rotate_lat_kernel);
+// -1 = automatic (3 x the SM count: up to three waves of 2 CTAs per SM).
+static int64_t g_lat_max_batch = -1;
 
 static int fail(int code, const std::string &msg) {
   g_err = msg;
@@ -85,6 +88,7 @@ static uint2 shoup_pair(uint32_t w, uint32_t p) {
 
 struct DevState {
   bool ready = false;
+  int sms = 148;
   uint2 *lane_fwd[2][2] = {};   // [n_variant][prime] -> [slot][TPP]
   uint2 *lane_inv[2][2] = {};
 };
@@ -138,6 +142,7 @@ static int init_device(DevState **out) {
     return HWB_OK;
   }
   const uint32_t primes[2] = {kP0, kP1};
+  cudaDeviceGetAttribute(&st.sms, cudaDevAttrMultiProcessorCount, dev);
   static uint2 h_tw[2][2][2][64];
   uint32_t h_r2ninv[2][2];
   PrimeConst h_prime[2];
@@ -535,6 +540,142 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::minb(V))
   }
 }
 
+// Latency-mode ladder (small batches): one ciphertext per CTA of 4*LV warps, one
+// warp per (digit row r, prime w).  Same arithmetic and bit-exact results as
+// blind_rotate_kernel; each CMUX step runs as
+//   (a) all threads: v = decomp_prep(acc * X^e - acc)
+//   (b) warp (r, w): forward NTT of digit r mod p_w, Montgomery products with the
+//       GGSW row r, red.shared.add into the spectra accumulators macc[c][w]
+//       (<= 2l terms in (0, 2p): sums < 12p < 2^32)
+//   (c) warps (c, w), c, w in {0,1}: reduce, inverse NTT, canonical residues
+//   (d) all threads: acc += CRT(macc[c][0], macc[c][1]); macc = 0
+// so the 12 forward transforms of a step run concurrently on 12 warps instead of
+// 6 + 6 sequentially on 2 -- a single PBS finishes ~3x sooner.
+template <int N, int LV>
+struct SmemLat {
+  uint32_t acc[2 * N];
+  uint32_t v[2 * N];
+  uint32_t macc[2][2][N];          // [component][prime], NTT domain
+  uint32_t scr[4 * LV][N];         // per-warp transpose scratch
+};
+
+// MINB = resident CTAs per SM the build targets: 1 (168 registers, lowest
+// single-ciphertext latency) or 2 (80 registers, higher per-SM throughput).
+template <int N, int LV, bool PBS, int MINB>
+__global__ void __launch_bounds__(128 * LV, MINB)
+    blind_rotate_lat_kernel(const uint32_t *__restrict__ bsk, size_t ggsw_words,
+                            const int32_t *__restrict__ exps, const uint32_t *__restrict__ lwe_in,
+                            const uint32_t *__restrict__ tv, int tv_per_item, uint32_t *acc_io, uint32_t *lwe_out,
+                            int L, Gadget g, Tw tw) {
+  static_assert(N == 1024, "latency mode: one warp per transform (TPP = 32)");
+  constexpr int TPP = 32, C = N / TPP, NT = 128 * LV;
+  constexpr int LOG2M = 11;
+  extern __shared__ uint4 smem_raw[];
+  SmemLat<N, LV> &sm = *reinterpret_cast<SmemLat<N, LV> *>(smem_raw);
+  const int64_t b = blockIdx.x;
+  const int tid = threadIdx.x, wi = tid >> 5, t = tid & 31;
+  const int w = wi & 1, r = wi >> 1;                 // forward phase: digit row r, prime w
+  const LayBase lay = make_lay<N, TPP>(t);
+  const uint32_t p = c_prime[w].p, pinv = c_prime[w].pinv;
+  const uint32_t off = p - g.half;
+  const uint32_t *row = PBS ? lwe_in + b * (int64_t)(L + 1) : nullptr;
+  if (PBS) {
+    const int bt = mod_switch(row[L], LOG2M);
+    const uint32_t *tp = tv + (tv_per_item ? b * 2 * N : 0);
+    const int e = (2 * N - bt) & (2 * N - 1);   // X^-b~
+    for (int k = tid; k < 2 * N; k += NT) {
+      const int c = k >= N, i = k & (N - 1);
+      sm.acc[k] = rot_read<N>(tp + c * N, i, e);
+    }
+  } else {
+    for (int k = tid; k < 2 * N; k += NT) sm.acc[k] = acc_io[b * 2 * N + k];
+  }
+  for (int k = tid; k < 4 * N; k += NT) (&sm.macc[0][0][0])[k] = 0u;
+  __syncthreads();
+  uint32_t x[C];
+#pragma unroll 1
+  for (int s = 0; s < L; ++s) {
+    int e;
+    if (PBS) {
+      e = mod_switch(row[s], LOG2M);
+    } else {
+      e = (int)((-(int64_t)exps[b * L + s]) % (2 * N));
+      if (e < 0) e += 2 * N;
+    }
+    if (e == 0) continue;
+    // (a)
+    for (int k = tid; k < 2 * N; k += NT) {
+      const int c = k >= N, i = k & (N - 1);
+      sm.v[k] = decomp_prep(rot_read<N>(sm.acc + c * N, i, e) - sm.acc[k], g);
+    }
+    __syncthreads();
+    const uint32_t *G = bsk + (size_t)s * ggsw_words;
+    if (r < 2 * LV && r < 2 * (int)g.levels) {
+      // (b) digit order (hw/tfhe.py:290-298): rows 0..l-1 = digits of b, l..2l-1 of a
+      const int comp = r < (int)g.levels ? 1 : 0;
+      const int tt = r < (int)g.levels ? r : r - (int)g.levels;
+      const uint32_t sh = g.base_log * (uint32_t)((int)g.levels - 1 - tt);
+      const uint32_t *vs = sm.v + comp * N + t;
+#pragma unroll
+      for (int j = 0; j < C; ++j) x[j] = ((vs[TPP * j] >> sh) & g.mask) + off;
+      fwd_ntt<N, TPP, -1>(x, sm.scr[wi], lay, t, w, w ? tw.fwd[1] : tw.fwd[0]);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const uint32_t *gs = G + ((size_t)(r * 2 + c) * 2 + w) * N;
+        uint32_t *dst = sm.macc[c][w];
+#pragma unroll
+        for (int jq = 0; jq < C / 4; ++jq) {
+          const uint4 Gv = __ldg(slice_vec<TPP>(gs, t, jq));
+          uint32_t *d = dst + (jq * TPP + t) * 4;
+          atomicAdd(d + 0, mont_mul(x[4 * jq + 0], Gv.x, p, pinv));
+          atomicAdd(d + 1, mont_mul(x[4 * jq + 1], Gv.y, p, pinv));
+          atomicAdd(d + 2, mont_mul(x[4 * jq + 2], Gv.z, p, pinv));
+          atomicAdd(d + 3, mont_mul(x[4 * jq + 3], Gv.w, p, pinv));
+        }
+      }
+    }
+    __syncthreads();
+    if (wi < 4) {
+      // (c) component c = wi >> 1, prime w
+      const int c = wi >> 1;
+      uint32_t *src = sm.macc[c][w];
+      const uint32_t two_p = 2 * p;
+#pragma unroll
+      for (int jq = 0; jq < C / 4; ++jq) {
+        const uint4 a = *reinterpret_cast<const uint4 *>(src + (jq * TPP + t) * 4);
+        x[4 * jq + 0] = a.x; x[4 * jq + 1] = a.y; x[4 * jq + 2] = a.z; x[4 * jq + 3] = a.w;
+      }
+#pragma unroll
+      for (int j = 0; j < C; ++j) {
+        uint32_t u = x[j];
+        u = umin(u, u - 4 * two_p);
+        u = umin(u, u - 2 * two_p);
+        u = umin(u, u - two_p);
+        x[j] = u;
+      }
+      inv_ntt<N, TPP, -1>(x, sm.scr[wi], lay, t, w, w ? tw.inv[1] : tw.inv[0]);
+#pragma unroll
+      for (int j = 0; j < C; ++j) src[t + TPP * j] = umin(x[j], x[j] - p);
+    }
+    __syncthreads();
+    // (d)
+    for (int k = tid; k < 2 * N; k += NT) {
+      const int c = k >= N, i = k & (N - 1);
+      sm.acc[k] += crt_lift(sm.macc[c][0][i], sm.macc[c][1][i]);
+      sm.macc[c][0][i] = 0u;
+      sm.macc[c][1][i] = 0u;
+    }
+    __syncthreads();
+  }
+  if (PBS) {
+    uint32_t *o = lwe_out + b * (int64_t)(N + 1);
+    for (int k = tid; k < N; k += NT) o[k] = k == 0 ? sm.acc[0] : 0u - sm.acc[N - k];
+    if (tid == 0) o[N] = sm.acc[N];
+  } else {
+    for (int k = tid; k < 2 * N; k += NT) acc_io[b * 2 * N + k] = sm.acc[k];
+  }
+}
+
 template <int N>
 __global__ void __launch_bounds__(Cfg<N>::THREADS) ggsw_to_ntt_kernel(const uint32_t *__restrict__ in,
                                                                       uint32_t *out, Tw tw) {
@@ -914,6 +1055,29 @@ static int launch_cmux(const hwb_params *p, DevState *st, const uint32_t *ggsw, 
   return post_launch("cmux_kernel");
 }
 
+template <int LV, bool PBS, int MINB>
+static int launch_br_lat(const hwb_params *p, DevState *st, const uint32_t *bsk, const int32_t *exps,
+                         const uint32_t *lwe_in, const uint32_t *tv, int tv_per_item, uint32_t *acc,
+                         uint32_t *lwe_out, int L, int64_t B, cudaStream_t s) {
+  constexpr int N = 1024;
+  const size_t smem = sizeof(SmemLat<N, LV>);
+  int rc;
+  if ((rc = set_smem(blind_rotate_lat_kernel<N, LV, PBS, MINB>, smem))) return rc;
+  blind_rotate_lat_kernel<N, LV, PBS, MINB><<<(unsigned)B, 128 * LV, smem, s>>>(
+      bsk, hwb_ggsw_ntt_words(p), exps, lwe_in, tv, tv_per_item, acc, lwe_out, L,
+      make_gadget(p->l, p->base_log), make_tw(st, N));
+  return post_launch("blind_rotate_lat_kernel");
+}
+
+template <int LV, bool PBS>
+static int launch_br_lat_b(const hwb_params *p, DevState *st, const uint32_t *bsk, const int32_t *exps,
+                           const uint32_t *lwe_in, const uint32_t *tv, int tv_per_item, uint32_t *acc,
+                           uint32_t *lwe_out, int L, int64_t B, cudaStream_t s) {
+  if (B <= st->sms)   // one wave of 1-CTA/SM ciphertexts: the lowest-latency build
+    return launch_br_lat<LV, PBS, 1>(p, st, bsk, exps, lwe_in, tv, tv_per_item, acc, lwe_out, L, B, s);
+  return launch_br_lat<LV, PBS, 2>(p, st, bsk, exps, lwe_in, tv, tv_per_item, acc, lwe_out, L, B, s);
+}
+
 template <int N, bool PBS>
 static int launch_br(const hwb_params *p, DevState *st, const uint32_t *bsk, const int32_t *gidx,
                      const int32_t *exps, const uint32_t *lwe_in, const uint32_t *tv, int tv_per_item,
@@ -922,6 +1086,12 @@ static int launch_br(const hwb_params *p, DevState *st, const uint32_t *bsk, con
   const Gadget g = make_gadget(p->l, p->base_log);
   const size_t words = hwb_ggsw_ntt_words(p);
   int rc;
+  const int64_t lat_max = g_lat_max_batch >= 0 ? g_lat_max_batch : 3 * (int64_t)st->sms;
+  if (N == 1024 && !gidx && B <= lat_max) {   // latency mode (small batches)
+    if (p->l == 1) return launch_br_lat_b<1, PBS>(p, st, bsk, exps, lwe_in, tv, tv_per_item, acc, lwe_out, L, B, s);
+    if (p->l == 2) return launch_br_lat_b<2, PBS>(p, st, bsk, exps, lwe_in, tv, tv_per_item, acc, lwe_out, L, B, s);
+    return launch_br_lat_b<3, PBS>(p, st, bsk, exps, lwe_in, tv, tv_per_item, acc, lwe_out, L, B, s);
+  }
   if (g_variant == 1) {
     if ((rc = set_smem(blind_rotate_kernel<N, PBS, 1>, smem))) return rc;
     blind_rotate_kernel<N, PBS, 1><<<(unsigned)B, Cfg<N>::THREADS, smem, s>>>(
@@ -993,6 +1163,12 @@ int64_t hwb_probe_i8mma(uint32_t *sink, int32_t blocks, int32_t iters, void *str
   probe_i8mma_kernel<<<blocks, 128, TC_SMEM, (cudaStream_t)stream>>>(sink, iters);
   if (post_launch("probe_i8mma_kernel")) return -HWB_ECUDA;
   return (int64_t)blocks * iters * (TC_KB / 32) * TC_M * TC_N * 32;
+}
+
+int64_t hwb_set_latency_batch(int64_t max_batch) {
+  const int64_t prev = g_lat_max_batch;
+  if (max_batch >= -1) g_lat_max_batch = max_batch;
+  return prev;
 }
 
 int hwb_set_variant(int v) {

@@ -30,6 +30,15 @@ def variant(request):
     _lib.set_variant(0)
 
 
+@pytest.fixture(params=["throughput", "latency"])
+def ladder(request):
+    """Run the test with the throughput ladder or with every batch on the
+    latency-mode ladder (one warp per digit transform)."""
+    prev = _lib.set_latency_batch(1 << 40 if request.param == "latency" else 0)
+    yield request.param
+    _lib.set_latency_batch(prev)
+
+
 # ---------------------------------------------------------------- external product
 
 @pytest.mark.parametrize("tag,N_log,lv,w", [("cfg2", 10, 3, 7), ("cfg1", 10, 2, 8), ("cfg4", 11, 2, 10)])
@@ -100,7 +109,7 @@ def test_cmux_cdemux(coracle):
 # ---------------------------------------------------------------- blind rotation
 
 @pytest.mark.parametrize("tag,N_log,lv,w", [("cfg2", 10, 3, 7), ("cfg4", 11, 2, 10)])
-def test_blind_rotate_golden(tag, N_log, lv, w, variant):
+def test_blind_rotate_golden(tag, N_log, lv, w, variant, ladder):
     g = golden("blind_rotate.npz")
     P = emb_params(N_log, lv, w)
     out = tfhe.blind_rotate_batch(P, g[f"{tag}_c"][None], g[f"{tag}_C"], g[f"{tag}_I"][None])[0]
@@ -120,7 +129,7 @@ def test_blind_rotate_reference_api():
         tfhe.blind_rotate(c, C, [1])
 
 
-def test_blind_rotate_batch_vs_oracle(coracle):
+def test_blind_rotate_batch_vs_oracle(coracle, ladder):
     rng = np.random.default_rng(13)
     P = emb_params(10, 3, 7)
     L, B = 9, 33
@@ -144,6 +153,26 @@ def test_sample_extract_all_positions(coeff):
 
 
 # ---------------------------------------------------------------- key switch and PBS
+
+@pytest.mark.parametrize("lv,w", [(1, 12), (2, 8), (3, 7)])
+def test_latency_ladder_gadgets(coracle, lv, w):
+    """Latency-mode ladder (4l warps per ciphertext) for every gadget depth."""
+    rng = np.random.default_rng(lv)
+    P = emb_params(10, lv, w)
+    L = 5
+    C = rand_u32(rng, (L, 2 * lv, 2, 1024))
+    for B in (5, 300):            # 1-CTA/SM build (B <= #SMs) and the 2-CTA/SM build
+        acc = rand_u32(rng, (B, 2, 1024))
+        exps = rng.integers(-4096, 4096, (B, L)).astype(np.int32)
+        exps[0, 1] = 0
+        ref = coracle.blind_rotate_batch(acc, C, exps, lv, w)
+        prev = _lib.set_latency_batch(1 << 40)
+        try:
+            out = tfhe.blind_rotate_batch(P, acc, C, exps)
+        finally:
+            _lib.set_latency_batch(prev)
+        assert_u32_equal(out, ref)
+
 
 def test_keyswitch_vs_oracle(coracle):
     P = dataclasses.replace(named_params("CFG2"), lwe_n=100)
@@ -203,7 +232,7 @@ def test_keyswitch_engine_selection():
 
 
 @pytest.mark.parametrize("name", ["CFG1", "CFG2", "CFG4"])
-def test_pbs_golden(name, variant):
+def test_pbs_golden(name, variant, ladder):
     P = named_params(name)
     g = golden(f"pbs_{name.lower()}.npz")
     K = tfhe.pbs_keygen(P, int(g["key_seed"]))
@@ -215,7 +244,7 @@ def test_pbs_golden(name, variant):
         assert_u32_equal(out, g["lwe_out"])
 
 
-def test_pbs_batch_vs_c_oracle_and_decrypt(coracle):
+def test_pbs_batch_vs_c_oracle_and_decrypt(coracle, ladder):
     P = named_params("CFG2")
     K = tfhe.pbs_keygen(P, 31)
     bsk, ksk = K.device_keys()
