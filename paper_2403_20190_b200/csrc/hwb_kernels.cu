@@ -626,11 +626,11 @@ __global__ void __launch_bounds__(128 * LV, MINB)
 #pragma unroll
         for (int jq = 0; jq < C / 4; ++jq) {
           const uint4 Gv = __ldg(slice_vec<TPP>(gs, t, jq));
-          uint32_t *d = dst + (jq * TPP + t) * 4;
-          atomicAdd(d + 0, mont_mul(x[4 * jq + 0], Gv.x, p, pinv));
-          atomicAdd(d + 1, mont_mul(x[4 * jq + 1], Gv.y, p, pinv));
-          atomicAdd(d + 2, mont_mul(x[4 * jq + 2], Gv.z, p, pinv));
-          atomicAdd(d + 3, mont_mul(x[4 * jq + 3], Gv.w, p, pinv));
+          uint32_t *d = dst + jq * 4 * TPP + t;      // element k of lane t at k*32 + t: conflict-free
+          atomicAdd(d + 0 * TPP, mont_mul(x[4 * jq + 0], Gv.x, p, pinv));
+          atomicAdd(d + 1 * TPP, mont_mul(x[4 * jq + 1], Gv.y, p, pinv));
+          atomicAdd(d + 2 * TPP, mont_mul(x[4 * jq + 2], Gv.z, p, pinv));
+          atomicAdd(d + 3 * TPP, mont_mul(x[4 * jq + 3], Gv.w, p, pinv));
         }
       }
     }
@@ -641,10 +641,7 @@ __global__ void __launch_bounds__(128 * LV, MINB)
       uint32_t *src = sm.macc[c][w];
       const uint32_t two_p = 2 * p;
 #pragma unroll
-      for (int jq = 0; jq < C / 4; ++jq) {
-        const uint4 a = *reinterpret_cast<const uint4 *>(src + (jq * TPP + t) * 4);
-        x[4 * jq + 0] = a.x; x[4 * jq + 1] = a.y; x[4 * jq + 2] = a.z; x[4 * jq + 3] = a.w;
-      }
+      for (int j = 0; j < C; ++j) x[j] = src[j * TPP + t];
 #pragma unroll
       for (int j = 0; j < C; ++j) {
         uint32_t u = x[j];
