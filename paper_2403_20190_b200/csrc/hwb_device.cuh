@@ -74,6 +74,10 @@ __device__ __forceinline__ uint32_t mont_mul(uint32_t a, uint32_t b, uint32_t p,
   return hi - __umulhi(m, p) + p;
 }
 
+__device__ __forceinline__ void prefetch_l2(const void *ptr) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+}
+
 // Montgomery reduction of a 64-bit sum T < 2^63.01 (signed variant, pinv = p^-1
 // mod 2^32): T * 2^-32 mod p in (0, 7p).
 __device__ __forceinline__ uint32_t redc64(uint64_t T, uint32_t p, uint32_t pinv) {

@@ -235,9 +235,10 @@ struct Who {
 // the input (both components) and a barrier has passed.  Post (after the
 // internal barriers): x holds, in layout A, the canonical residues mod p_grp of
 // component grp, and sm.v[grp*N + i] holds those mod p_{1-grp} of component grp.
-template <int N, int PRIME>
+template <int N, int PRIME, bool PF>
 __device__ __forceinline__ void ext_product_core_p(Smem<N> &sm, const uint32_t *__restrict__ G, const Gadget &g,
-                                                   const Who<N> &me, const Tw &tw, uint32_t (&x)[N / Cfg<N>::TPP]) {
+                                                   const Who<N> &me, const Tw &tw, uint32_t (&x)[N / Cfg<N>::TPP],
+                                                   const uint32_t *Gnext) {
   constexpr int TPP = Cfg<N>::TPP;
   constexpr int C = N / TPP;
   const int w = PRIME >= 0 ? PRIME : me.grp;
@@ -266,6 +267,17 @@ __device__ __forceinline__ void ext_product_core_p(Smem<N> &sm, const uint32_t *
     const int tt = r < L ? r : r - L;
     const uint32_t sh = g.base_log * (uint32_t)(L - 1 - tt);
     const uint32_t *vs = sm.v + comp * N + t;
+    {   // prefetch the GGSW rows the next digit (or the next step's first digit)
+        // multiplies by while this digit's transform runs: per-item GGSWs come
+        // from HBM, not L2 (rotation ladders of vertical packing, IVP levels)
+      const uint32_t *gn = r + 1 < 2 * L ? G + (size_t)(r + 1) * 4 * N : Gnext;
+      if (PF && gn) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int q = t; q < N / 32; q += TPP) prefetch_l2(gn + ((size_t)c * 2 + w) * N + q * 32);
+      }
+    }
 #pragma unroll
     for (int j = 0; j < C; ++j) x[j] = ((vs[TPP * j] >> sh) & g.mask) + off;
     fwd_ntt<N, TPP, PRIME>(x, sm.scr[w], me.lay, t, w, twf);
@@ -334,15 +346,16 @@ __device__ __forceinline__ void ext_product_core_p(Smem<N> &sm, const uint32_t *
 
 // SPEC: each group runs its own instantiation (the prime, hence every uniform
 // twiddle and modulus, is a compile-time constant); otherwise one shared copy.
-template <int N, bool SPEC>
+template <int N, bool SPEC, bool PF = true>
 __device__ __forceinline__ void ext_product_core(Smem<N> &sm, const uint32_t *__restrict__ G, const Gadget &g,
-                                                 const Who<N> &me, const Tw &tw, uint32_t (&x)[N / Cfg<N>::TPP]) {
+                                                 const Who<N> &me, const Tw &tw, uint32_t (&x)[N / Cfg<N>::TPP],
+                                                 const uint32_t *Gnext = nullptr) {
   if (!SPEC)
-    ext_product_core_p<N, -1>(sm, G, g, me, tw, x);
+    ext_product_core_p<N, -1, PF>(sm, G, g, me, tw, x, Gnext);
   else if (me.grp == 0)
-    ext_product_core_p<N, 0>(sm, G, g, me, tw, x);
+    ext_product_core_p<N, 0, PF>(sm, G, g, me, tw, x, Gnext);
   else
-    ext_product_core_p<N, 1>(sm, G, g, me, tw, x);
+    ext_product_core_p<N, 1, PF>(sm, G, g, me, tw, x, Gnext);
 }
 
 __device__ __forceinline__ uint32_t lift(int w, uint32_t own, uint32_t other) {
@@ -523,7 +536,13 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::minb(V))
       sm.v[k] = decomp_prep(rot_read<N>(sm.acc + c * N, i, e) - sm.acc[k], g);
     }
     __syncthreads();
-    ext_product_core<N, Cfg<N>::spec(V)>(sm, bsk + (size_t)gi * ggsw_words, g, me, tw, x);
+    const uint32_t *gnext = nullptr;
+    if (s + 1 < L) {
+      const int gn = (!PBS && gidx) ? gidx[b * L + s + 1] : s + 1;
+      if (gn >= 0) gnext = bsk + (size_t)gn * ggsw_words;
+    }
+    // prefetching pays for per-item GGSWs (HBM); the PBS key is L2-resident
+    ext_product_core<N, Cfg<N>::spec(V), !PBS>(sm, bsk + (size_t)gi * ggsw_words, g, me, tw, x, gnext);
 #pragma unroll
     for (int j = 0; j < N / TPP; ++j) {
       const int i = me.t + TPP * j;
@@ -616,6 +635,8 @@ __global__ void __launch_bounds__(128 * LV, MINB)
       const int tt = r < (int)g.levels ? r : r - (int)g.levels;
       const uint32_t sh = g.base_log * (uint32_t)((int)g.levels - 1 - tt);
       const uint32_t *vs = sm.v + comp * N + t;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) prefetch_l2(G + ((size_t)(r * 2 + c) * 2 + w) * N + t * 32);
 #pragma unroll
       for (int j = 0; j < C; ++j) x[j] = ((vs[TPP * j] >> sh) & g.mask) + off;
       fwd_ntt<N, TPP, -1>(x, sm.scr[wi], lay, t, w, w ? tw.fwd[1] : tw.fwd[0]);
