@@ -280,9 +280,10 @@ __device__ __forceinline__ void fwd_ntt(uint32_t (&x)[N / TPP], uint32_t *scr, c
 // Per-thread twiddle slots: B stages s = 0..B_TOP-1, then M stages s = LOGC..T-1.
 template <int N, int TPP, int PRIME>
 __device__ __forceinline__ void inv_ntt(uint32_t (&x)[N / TPP], uint32_t *scr, const LayBase &L, int t, int prime,
-                                        const uint2 *__restrict__ tw) {
+                                        const uint2 *__restrict__ tw, int bar_group = -1) {
   using G = Geo<N, TPP>;
-  const int group = PRIME >= 0 ? PRIME : prime;
+  // named-barrier group of the TPP threads (TPP > 32): the prime unless overridden
+  const int group = bar_group >= 0 ? bar_group : (PRIME >= 0 ? PRIME : prime);
   static_for<0, G::B_TOP>([&](auto K) {                  // B stages s = 0 .. B_TOP-1
     constexpr int s = decltype(K)::value;
     constexpr int slot = G::C - 2 * (G::C >> (s + 1));   // C/2 + C/4 + ... (s terms)

@@ -91,6 +91,7 @@ struct DevState {
   int sms = 148;
   uint2 *lane_fwd[2][2] = {};   // [n_variant][prime] -> [slot][TPP]
   uint2 *lane_inv[2][2] = {};
+  uint2 *lane_inv64[2] = {};    // N = 1024 inverse transform on 64 threads (latency ladder)
 };
 
 static std::mutex g_mu;
@@ -98,10 +99,9 @@ static DevState g_state[64];
 
 // Per-thread twiddle table in the slot order fwd_ntt/inv_ntt consume
 // (hwb_device.cuh): twiddle index of stage s, block b is m + b, m = N/2^(s+1).
-template <int N>
+template <int N, int TPP = Cfg<N>::TPP>
 static std::vector<uint2> thread_table(const std::vector<uint32_t> &w, uint32_t p, bool fwd) {
-  using G = Geo<N, Cfg<N>::TPP>;
-  constexpr int TPP = Cfg<N>::TPP;
+  using G = Geo<N, TPP>;
   std::vector<uint2> tab((size_t)G::SLOTS * TPP);
   int slot = 0;
   auto m_stage = [&](int s) {   // middle layout: block = t_hi 2^(T-s-1) + u
@@ -185,6 +185,13 @@ static int init_device(DevState **out) {
       e1 = cudaMemcpy(st.lane_fwd[nv][pr], lf.data(), bytes, cudaMemcpyHostToDevice);
       e2 = cudaMemcpy(st.lane_inv[nv][pr], li.data(), bytes, cudaMemcpyHostToDevice);
       if (e1 != cudaSuccess || e2 != cudaSuccess) return fail(HWB_ECUDA, "twiddle upload failed");
+      if (nv == 0) {
+        std::vector<uint2> l64 = thread_table<1024, 64>(iw, p, false);
+        const size_t b64 = sizeof(uint2) * l64.size();
+        e1 = cudaMalloc(&st.lane_inv64[pr], b64);
+        if (e1 == cudaSuccess) e1 = cudaMemcpy(st.lane_inv64[pr], l64.data(), b64, cudaMemcpyHostToDevice);
+        if (e1 != cudaSuccess) return fail(HWB_ECUDA, "twiddle upload failed");
+      }
       // Montgomery form with N^-1: x -> x * R * N^-1 via mont_mul(x, R^2 N^-1)
       uint64_t R = ((uint64_t)1 << 32) % p;
       uint64_t r2 = R * R % p;
@@ -218,6 +225,7 @@ struct Smem {
 struct Tw {
   const uint2 *fwd[2];
   const uint2 *inv[2];
+  const uint2 *inv64[2];   // N = 1024, 64 threads per transform
 };
 
 // Thread coordinates inside a ciphertext CTA.
@@ -656,7 +664,34 @@ __global__ void __launch_bounds__(128 * LV, MINB)
       }
     }
     __syncthreads();
-    if (wi < 4) {
+    if (LV >= 2 && MINB == 1) {
+      // (c) 8 warps: warp pair q = (component q >> 1, prime q & 1) shares one
+      // inverse transform on 64 threads (named barrier 1 + q).  (The 2-CTA/SM
+      // build keeps 4 warps: there the other CTA fills the idle slots.)
+      if (wi < 8) {
+        constexpr int T2 = 64, C2 = N / T2;
+        const int q = wi >> 1, c = q >> 1, w2 = q & 1, t2 = ((wi & 1) << 5) | t;
+        const uint32_t p2 = c_prime[w2].p, two_p2 = 2 * p2;
+        uint32_t *src = sm.macc[c][w2];
+        uint32_t y[C2];
+#pragma unroll
+        for (int j = 0; j < C2; ++j) {
+          // layout-B index i = C2*t2 + j of the 64-thread transform; the spectra were
+          // accumulated in the 32-thread order: (t32, j32) = (i / 32, i % 32) at
+          // (j32 / 4) * 128 + (j32 % 4) * 32 + t32
+          const int i = C2 * t2 + j, j32 = i & 31, t32 = i >> 5;
+          uint32_t u = src[(j32 >> 2) * 128 + (j32 & 3) * 32 + t32];
+          u = umin(u, u - 4 * two_p2);
+          u = umin(u, u - 2 * two_p2);
+          u = umin(u, u - two_p2);
+          y[j] = u;
+        }
+        const LayBase lay2 = make_lay<N, T2>(t2);
+        inv_ntt<N, T2, -1>(y, sm.scr[2 * q], lay2, t2, w2, tw.inv64[w2], q);
+#pragma unroll
+        for (int j = 0; j < C2; ++j) src[t2 + T2 * j] = umin(y[j], y[j] - p2);
+      }
+    } else if (wi < 4) {
       // (c) component c = wi >> 1, prime w
       const int c = wi >> 1;
       uint32_t *src = sm.macc[c][w];
@@ -1040,6 +1075,7 @@ static Tw make_tw(DevState *st, int N) {
   for (int pr = 0; pr < 2; ++pr) {
     tw.fwd[pr] = st->lane_fwd[nv][pr];
     tw.inv[pr] = st->lane_inv[nv][pr];
+    tw.inv64[pr] = st->lane_inv64[pr];
   }
   return tw;
 }
