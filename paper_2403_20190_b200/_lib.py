@@ -11,7 +11,9 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhwb200.so")
+# HWB_LIB_PATH: load another build of the library (A/B measurement of kernel
+# variants, tools/ab_variants.sh); the default is the in-tree build.
+LIB_PATH = os.environ.get("HWB_LIB_PATH") or os.path.join(HERE, "libhwb200.so")
 
 HWB_OK, HWB_EINVAL, HWB_ECUDA = 0, 1, 2
 

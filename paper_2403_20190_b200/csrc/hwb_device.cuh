@@ -37,6 +37,19 @@ __constant__ uint2 c_tw[2][2][2][64];
 __constant__ PrimeConst c_prime[2];
 __constant__ uint32_t c_crt[4];        // {p0^-1 mod p1, its Shoup quotient, P mod 2^32, p1/2}
 __constant__ uint32_t c_r2ninv[2][2];  // [n_variant][prime]: R^2 N^-1 mod p
+// Always 0 (written by the host).  Two-operand adds written as x + y + c_zero
+// compile to one IADD3 with a constant-bank operand on the ALU pipe; plain
+// x + y is often emitted as IMAD.IADD, which occupies the FMA-heavy pipe the
+// modular products are bound by.
+__constant__ uint32_t c_zero;
+#ifndef HWB_CZERO
+#define HWB_CZERO 1
+#endif
+#if HWB_CZERO
+#define HWB_Z + c_zero
+#else
+#define HWB_Z
+#endif
 
 template <int C> struct Log2 { static constexpr int v = (C <= 1) ? 0 : 1 + Log2<C / 2>::v; };
 template <int N> struct NVar { static constexpr int v = (N == 1024) ? 0 : 1; };
@@ -78,6 +91,16 @@ __device__ __forceinline__ void prefetch_l2(const void *ptr) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
 }
 
+// Montgomery product without the +p offset: a*b*2^-32 mod p in (-p, p) as a
+// wrapped 32-bit value; accumulate with acc + mont_mul_nop(...) (one IADD3)
+// and add the sum of the offsets once.
+__device__ __forceinline__ uint32_t mont_hi(uint32_t a, uint32_t b, uint32_t pinv, uint32_t p, uint32_t acc) {
+  uint64_t t = (uint64_t)a * b;
+  uint32_t lo = (uint32_t)t, hi = (uint32_t)(t >> 32);
+  uint32_t m = lo * pinv;
+  return acc + hi - __umulhi(m, p);
+}
+
 // Montgomery reduction of a 64-bit sum T < 2^63.01 (signed variant, pinv = p^-1
 // mod 2^32): T * 2^-32 mod p in (0, 7p).
 __device__ __forceinline__ uint32_t redc64(uint64_t T, uint32_t p, uint32_t pinv) {
@@ -90,7 +113,7 @@ __device__ __forceinline__ void ct_bfly(uint32_t &X, uint32_t &Y, uint32_t w, ui
                                         uint32_t p, uint32_t two_p) {
   uint32_t x = umin(X, X - two_p);
   uint32_t t = shoup_mul(Y, w, wq, p);
-  X = x + t;
+  X = x + t HWB_Z;
   Y = x - t + two_p;
 }
 
@@ -109,7 +132,7 @@ __device__ __forceinline__ void ct_bfly_lazy(uint32_t &X, uint32_t &Y, uint32_t 
     x = umin(x, x - two_p);
   }
   uint32_t t = shoup_mul(Y, w, wq, p);
-  X = x + t;
+  X = x + t HWB_Z;
   Y = x - t + two_p;
 }
 
@@ -117,7 +140,7 @@ __device__ __forceinline__ void ct_bfly_lazy(uint32_t &X, uint32_t &Y, uint32_t 
 __device__ __forceinline__ void gs_bfly(uint32_t &X, uint32_t &Y, uint32_t w, uint32_t wq,
                                         uint32_t p, uint32_t two_p) {
   uint32_t x = X, y = Y;
-  uint32_t s = x + y;
+  uint32_t s = x + y HWB_Z;
   X = umin(s, s - two_p);
   Y = shoup_mul(x - y + two_p, w, wq, p);
 }

@@ -55,6 +55,9 @@ static int fail(int code, const std::string &msg) {
 #ifndef HWB_ACC64
 #define HWB_ACC64 0
 #endif
+#ifndef HWB_MONTHI
+#define HWB_MONTHI 0
+#endif
 template <int N> struct Cfg {
   static constexpr int TPP = (N == 1024) ? 32 : 64;
   static constexpr int THREADS = 2 * TPP;
@@ -202,7 +205,9 @@ static int init_device(DevState **out) {
   const uint32_t crt_inv = powmod(kP0, kP1 - 2, kP1);
   const uint2 crt_pair = shoup_pair(crt_inv, kP1);
   uint32_t h_crt[4] = {crt_pair.x, crt_pair.y, (uint32_t)((uint64_t)kP0 * kP1), kP1 / 2};
+  const uint32_t zero = 0;
   cudaError_t ec = cudaMemcpyToSymbol(c_tw, h_tw, sizeof(h_tw));
+  if (ec == cudaSuccess) ec = cudaMemcpyToSymbol(c_zero, &zero, sizeof(zero));
   if (ec == cudaSuccess) ec = cudaMemcpyToSymbol(c_prime, h_prime, sizeof(h_prime));
   if (ec == cudaSuccess) ec = cudaMemcpyToSymbol(c_crt, h_crt, sizeof(h_crt));
   if (ec == cudaSuccess) ec = cudaMemcpyToSymbol(c_r2ninv, h_r2ninv, sizeof(h_r2ninv));
@@ -265,8 +270,16 @@ __device__ __forceinline__ void ext_product_core_p(Smem<N> &sm, const uint32_t *
 #else
   uint32_t a0[C], a1[C];
 #endif
+#if HWB_ACC64 || !HWB_MONTHI
 #pragma unroll
   for (int j = 0; j < C; ++j) a0[j] = a1[j] = 0;
+#else
+  // each Montgomery term is added as hi - umulhi(m, p) in (-p, p); the 2l
+  // offsets of +p are folded into the initial value (sum in (0, 12p) as before)
+  const uint32_t acc0 = 2u * (uint32_t)L * p + c_zero;
+#pragma unroll
+  for (int j = 0; j < C; ++j) a0[j] = a1[j] = acc0;
+#endif
 
 #pragma unroll 1
   for (int r = 0; r < 2 * L; ++r) {
@@ -304,7 +317,7 @@ __device__ __forceinline__ void ext_product_core_p(Smem<N> &sm, const uint32_t *
       a1[4 * jq + 1] += (uint64_t)x[4 * jq + 1] * G1.y;
       a1[4 * jq + 2] += (uint64_t)x[4 * jq + 2] * G1.z;
       a1[4 * jq + 3] += (uint64_t)x[4 * jq + 3] * G1.w;
-#else
+#elif !HWB_MONTHI
       a0[4 * jq + 0] += mont_mul(x[4 * jq + 0], G0.x, p, pinv);
       a0[4 * jq + 1] += mont_mul(x[4 * jq + 1], G0.y, p, pinv);
       a0[4 * jq + 2] += mont_mul(x[4 * jq + 2], G0.z, p, pinv);
@@ -313,6 +326,15 @@ __device__ __forceinline__ void ext_product_core_p(Smem<N> &sm, const uint32_t *
       a1[4 * jq + 1] += mont_mul(x[4 * jq + 1], G1.y, p, pinv);
       a1[4 * jq + 2] += mont_mul(x[4 * jq + 2], G1.z, p, pinv);
       a1[4 * jq + 3] += mont_mul(x[4 * jq + 3], G1.w, p, pinv);
+#else
+      a0[4 * jq + 0] = mont_hi(x[4 * jq + 0], G0.x, pinv, p, a0[4 * jq + 0]);
+      a0[4 * jq + 1] = mont_hi(x[4 * jq + 1], G0.y, pinv, p, a0[4 * jq + 1]);
+      a0[4 * jq + 2] = mont_hi(x[4 * jq + 2], G0.z, pinv, p, a0[4 * jq + 2]);
+      a0[4 * jq + 3] = mont_hi(x[4 * jq + 3], G0.w, pinv, p, a0[4 * jq + 3]);
+      a1[4 * jq + 0] = mont_hi(x[4 * jq + 0], G1.x, pinv, p, a1[4 * jq + 0]);
+      a1[4 * jq + 1] = mont_hi(x[4 * jq + 1], G1.y, pinv, p, a1[4 * jq + 1]);
+      a1[4 * jq + 2] = mont_hi(x[4 * jq + 2], G1.z, pinv, p, a1[4 * jq + 2]);
+      a1[4 * jq + 3] = mont_hi(x[4 * jq + 3], G1.w, pinv, p, a1[4 * jq + 3]);
 #endif
     }
   }
