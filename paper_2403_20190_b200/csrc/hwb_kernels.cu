@@ -58,6 +58,16 @@ static int fail(int code, const std::string &msg) {
 #ifndef HWB_MONTHI
 #define HWB_MONTHI 0
 #endif
+// the MAC accumulation as a 3-operand add too (measured slower in the 2-warp
+// ladder: 119 vs 106 ms -- the compiler then schedules the digit loop worse)
+#ifndef HWB_MACZ_ON
+#define HWB_MACZ_ON 0
+#endif
+#if HWB_MACZ_ON
+#define HWB_MACZ HWB_Z
+#else
+#define HWB_MACZ
+#endif
 template <int N> struct Cfg {
   static constexpr int TPP = (N == 1024) ? 32 : 64;
   static constexpr int THREADS = 2 * TPP;
@@ -318,14 +328,14 @@ __device__ __forceinline__ void ext_product_core_p(Smem<N> &sm, const uint32_t *
       a1[4 * jq + 2] += (uint64_t)x[4 * jq + 2] * G1.z;
       a1[4 * jq + 3] += (uint64_t)x[4 * jq + 3] * G1.w;
 #elif !HWB_MONTHI
-      a0[4 * jq + 0] += mont_mul(x[4 * jq + 0], G0.x, p, pinv);
-      a0[4 * jq + 1] += mont_mul(x[4 * jq + 1], G0.y, p, pinv);
-      a0[4 * jq + 2] += mont_mul(x[4 * jq + 2], G0.z, p, pinv);
-      a0[4 * jq + 3] += mont_mul(x[4 * jq + 3], G0.w, p, pinv);
-      a1[4 * jq + 0] += mont_mul(x[4 * jq + 0], G1.x, p, pinv);
-      a1[4 * jq + 1] += mont_mul(x[4 * jq + 1], G1.y, p, pinv);
-      a1[4 * jq + 2] += mont_mul(x[4 * jq + 2], G1.z, p, pinv);
-      a1[4 * jq + 3] += mont_mul(x[4 * jq + 3], G1.w, p, pinv);
+      a0[4 * jq + 0] = a0[4 * jq + 0] + mont_mul(x[4 * jq + 0], G0.x, p, pinv) HWB_MACZ;
+      a0[4 * jq + 1] = a0[4 * jq + 1] + mont_mul(x[4 * jq + 1], G0.y, p, pinv) HWB_MACZ;
+      a0[4 * jq + 2] = a0[4 * jq + 2] + mont_mul(x[4 * jq + 2], G0.z, p, pinv) HWB_MACZ;
+      a0[4 * jq + 3] = a0[4 * jq + 3] + mont_mul(x[4 * jq + 3], G0.w, p, pinv) HWB_MACZ;
+      a1[4 * jq + 0] = a1[4 * jq + 0] + mont_mul(x[4 * jq + 0], G1.x, p, pinv) HWB_MACZ;
+      a1[4 * jq + 1] = a1[4 * jq + 1] + mont_mul(x[4 * jq + 1], G1.y, p, pinv) HWB_MACZ;
+      a1[4 * jq + 2] = a1[4 * jq + 2] + mont_mul(x[4 * jq + 2], G1.z, p, pinv) HWB_MACZ;
+      a1[4 * jq + 3] = a1[4 * jq + 3] + mont_mul(x[4 * jq + 3], G1.w, p, pinv) HWB_MACZ;
 #else
       a0[4 * jq + 0] = mont_hi(x[4 * jq + 0], G0.x, pinv, p, a0[4 * jq + 0]);
       a0[4 * jq + 1] = mont_hi(x[4 * jq + 1], G0.y, pinv, p, a0[4 * jq + 1]);
@@ -668,7 +678,7 @@ __global__ void __launch_bounds__(128 * LV, MINB)
 #pragma unroll
       for (int c = 0; c < 2; ++c) prefetch_l2(G + ((size_t)(r * 2 + c) * 2 + w) * N + t * 32);
 #pragma unroll
-      for (int j = 0; j < C; ++j) x[j] = ((vs[TPP * j] >> sh) & g.mask) + off;
+      for (int j = 0; j < C; ++j) x[j] = ((vs[TPP * j] >> sh) & g.mask) + off HWB_Z;
       fwd_ntt<N, TPP, -1>(x, sm.scr[wi], lay, t, w, w ? tw.fwd[1] : tw.fwd[0]);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -736,7 +746,7 @@ __global__ void __launch_bounds__(128 * LV, MINB)
     // (d)
     for (int k = tid; k < 2 * N; k += NT) {
       const int c = k >= N, i = k & (N - 1);
-      sm.acc[k] += crt_lift(sm.macc[c][0][i], sm.macc[c][1][i]);
+      sm.acc[k] = sm.acc[k] + crt_lift(sm.macc[c][0][i], sm.macc[c][1][i]) HWB_Z;
       sm.macc[c][0][i] = 0u;
       sm.macc[c][1][i] = 0u;
     }
