@@ -215,7 +215,39 @@ def _payload(params: HeParams) -> np.ndarray:
 # training
 
 
-def _stack_table(params: HeParams, samples: list[EncryptedSample]):
+class _Staged:
+    """A chunk's host RGSW stacks copied to the device on a side stream, so the
+    H2D of chunk k+1 overlaps the ladders of chunk k (pinned host tensors)."""
+
+    _copy_stream = None
+
+    def __init__(self, samples: list[EncryptedSample]):
+        self.samples = samples
+        self.dev: list | None = None
+        self.event = None
+        if not any(isinstance(s.rgsw, np.ndarray) or (isinstance(s.rgsw, torch.Tensor) and not s.rgsw.is_cuda)
+                   for s in samples):
+            return                                          # already device-resident
+        if _Staged._copy_stream is None:
+            _Staged._copy_stream = torch.cuda.Stream(device=tfhe._device())
+        cs = _Staged._copy_stream
+        cs.wait_stream(torch.cuda.current_stream())         # buffers freed on the main stream
+        with torch.cuda.stream(cs):
+            self.dev = [tfhe.to_device(s.rgsw) for s in samples]
+            self.event = torch.cuda.Event()
+            self.event.record(cs)
+
+    def tensors(self) -> list:
+        if self.dev is None:
+            return [tfhe.to_device(s.rgsw) for s in self.samples]
+        main = torch.cuda.current_stream()
+        main.wait_event(self.event)
+        for t in self.dev:
+            t.record_stream(main)                           # allocator: used on the main stream
+        return self.dev
+
+
+def _stack_table(params: HeParams, samples: list[EncryptedSample], staged: _Staged | None = None):
     """One device NTT-domain GGSW table holding every sample's RGSW rows, each
     sample transformed straight into its slice (no stacking copy)."""
     import ctypes
@@ -224,9 +256,9 @@ def _stack_table(params: HeParams, samples: list[EncryptedSample]):
     words = L.hwb_ggsw_ntt_words(cp)
     rows = [int(s.rgsw.shape[0]) for s in samples]
     table = torch.empty((sum(rows), words), dtype=torch.int32, device=tfhe._device())
+    srcs = (staged or _Staged(samples)).tensors()
     off = 0
-    for smp, r in zip(samples, rows):
-        src = tfhe.to_device(smp.rgsw)                  # H2D (non-blocking) for pinned host tensors
+    for src, r in zip(srcs, rows):
         dst = ctypes.c_void_p(table.data_ptr() + off * words * 4)
         tfhe._lib.check(L.hwb_ggsw_to_ntt(cp, tfhe._ptr(src), dst, r, tfhe._stream()))
         off += r
@@ -251,12 +283,9 @@ def he_train(samples: Iterable[EncryptedSample], geometry: WisardGeometry, param
     if model.geometry != geometry or model.params != params:
         raise TfheError("model geometry/params mismatch")
     tmpl = _selector_template(geometry, params)
-    chunk: list[EncryptedSample] = []
 
-    def flush():
-        if not chunk:
-            return
-        table = _stack_table(params, chunk)
+    def run(chunk: list[EncryptedSample], staged: _Staged):
+        table = _stack_table(params, chunk, staged)
         stride = geometry.s + geometry.label_bits
         codes = np.concatenate([_shift(tmpl, i * stride) for i in range(len(chunk))])
         rows = lut.ivp_codes(params, codes, table, _payload(params))      # (I*k0, k1, 2, N)
@@ -264,18 +293,41 @@ def he_train(samples: Iterable[EncryptedSample], geometry: WisardGeometry, param
         label_rows = np.array([[i * stride + geometry.s + b for b in range(geometry.label_bits)]
                                for i in range(len(chunk))], dtype=np.int64)
         he_count_labels_batch(params, model.counts_ct, table, label_rows)
-        chunk.clear()
 
-    for sample in samples:
+    def check(sample):
         if sample.s != geometry.s:
             raise TfheError(f"sample has {sample.s} bits, geometry wants {geometry.s}")
         if sample.label_bits != geometry.label_bits:
             raise TfheError("training samples need encrypted label bits")
+
+    # one chunk in flight: chunk k+1's H2D is enqueued on the copy stream before
+    # chunk k's ladders, so host->device traffic overlaps the GPU work
+    for chunk, staged in _chunks_staged(samples, batch, check):
+        run(chunk, staged)
+    return model
+
+
+def _chunks_staged(samples: Iterable[EncryptedSample], batch: int, check=None):
+    """Yield (chunk, staged) with the next chunk's H2D already enqueued."""
+    pending = None
+    chunk: list[EncryptedSample] = []
+    for sample in samples:
+        if check:
+            check(sample)
         chunk.append(sample)
         if len(chunk) == batch:
-            flush()
-    flush()
-    return model
+            nxt = (chunk, _Staged(chunk))
+            chunk = []
+            if pending is not None:
+                yield pending
+            pending = nxt
+    if chunk:
+        nxt = (chunk, _Staged(chunk))
+        if pending is not None:
+            yield pending
+        pending = nxt
+    if pending is not None:
+        yield pending
 
 
 def he_train_multi(samples: Iterable[EncryptedSample], geometries: Sequence[WisardGeometry], params: HeParams,
