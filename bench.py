@@ -180,6 +180,21 @@ def probe_modmul_peak(torch, _lib, tfhe):
     return best
 
 
+def ncu_traffic(B, alg_bytes=None):
+    """DRAM bytes per blind-rotation launch from the committed ncu --set full
+    capture (profiles/ncu_traffic.json) when it was taken at this batch size."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            rec = json.load(f)["blind_rotate_kernel<1024,PBS>"]
+    except (OSError, KeyError, ValueError):
+        return None
+    if rec.get("batch") != B:
+        return None
+    return {"bytes": int(rec["dram_bytes_read"] + rec["dram_bytes_write"]), "unit": "B/launch",
+            "algorithmic_bytes": alg_bytes, "source": rec.get("source")}
+
+
 def probe_i8mma_peak(torch, _lib, tfhe):
     """Measured P_i8: tcgen05.mma kind::i8 MAC rate of the key switch's MMA shape
     (M128 N256 K32 from shared memory, one CTA per SM), best of 4."""
@@ -421,7 +436,8 @@ def bench_hwb(args):
                 "api": "tfhe.pbs_batch from pinned host tensors", "matches_device_run": e2e_ok},
         "roofline": {"bound": "int", "kernel": "blind_rotate_kernel<1024,PBS>",
                      "achieved": round(achieved / 1e9, 2), "peak": round(peak / 1e9, 2),
-                     "unit": "Gmodmul/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "unit": "Gmodmul/s", "frac": round(achieved / peak, 4), "traffic": ncu_traffic(
+                         B, 4 * (P.lwe_n * 2 * lv * 2 * 2 * N + B * (P.lwe_n + 1) + B * (N + 1) + 2 * N)),
                      "work_per_pbs": f"W_mm = {w_mm} RNS modmuls (n x 53,248 per CMUX)",
                      "peak_source": "measured live: probe_modmul_kernel (register-only Shoup, both primes)",
                      "pbs": {"roofline_pbs_per_s": round(pbs_roof, 1),
