@@ -136,6 +136,17 @@ __device__ __forceinline__ void ct_bfly_lazy(uint32_t &X, uint32_t &Y, uint32_t 
   Y = x - t + two_p;
 }
 
+// First forward stage on gadget digits: inputs are d + p - beta/2 with digit
+// index d in [0, beta), so the twiddle product w0 * (d - beta/2) mod p comes from
+// a beta-entry table (tab[d], canonical) instead of a Shoup product.  Outputs
+// X < 3p, Y < 4p: within the lazy bound ct_bfly_lazy assumes after one stage.
+__device__ __forceinline__ void digit_stage0(uint32_t &X, uint32_t &Y, uint32_t da, uint32_t db,
+                                             const uint32_t *tab, uint32_t off, uint32_t two_p) {
+  const uint32_t x = da + off, t = tab[db];
+  X = x + t HWB_Z;
+  Y = x - t + two_p;
+}
+
 // Harvey lazy Gentleman-Sande butterfly: X, Y in [0, 2p) -> [0, 2p).
 __device__ __forceinline__ void gs_bfly(uint32_t &X, uint32_t &Y, uint32_t w, uint32_t wq,
                                         uint32_t p, uint32_t two_p) {
@@ -268,12 +279,14 @@ __device__ __forceinline__ void ntt_stage(uint32_t (&x)[N / TPP], int t, int pri
 // In: layout A, values < 2p.  Out: layout B, values < 12p (lazy reduction:
 // x is reduced only on execution stages 5 and 10 -- see ct_bfly_lazy).
 // Per-thread twiddle slots: M stages s = T-1..LOGC, then B stages s = B_TOP-1..0.
-template <int N, int TPP, int PRIME>
+// SKIP0: the caller already applied the first stage (s = LOGN-1, uniform
+// twiddle c_tw[..][1]) -- see digit_stage0.
+template <int N, int TPP, int PRIME, bool SKIP0 = false>
 __device__ __forceinline__ void fwd_ntt(uint32_t (&x)[N / TPP], uint32_t *scr, const LayBase &L, int t, int prime,
                                         const uint2 *__restrict__ tw) {
   using G = Geo<N, TPP>;
   const int group = PRIME >= 0 ? PRIME : prime;
-  static_for<0, G::LOGN - G::T>([&](auto K) {          // A stages s = LOGN-1 .. T
+  static_for<SKIP0 ? 1 : 0, G::LOGN - G::T>([&](auto K) {   // A stages s = LOGN-1 .. T
     constexpr int s = G::LOGN - 1 - decltype(K)::value;
     constexpr bool red = (G::LOGN - 1 - s) % 5 == 0 && s != G::LOGN - 1;
     ntt_stage<N, TPP, PRIME, true, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0, red>(x, t, prime, tw);

@@ -58,6 +58,14 @@ static int fail(int code, const std::string &msg) {
 #ifndef HWB_MONTHI
 #define HWB_MONTHI 0
 #endif
+// first forward stage of the digit transforms from a beta-entry shared-memory
+// table instead of Shoup products.  Measured slower (throughput ladder 109.6 vs
+// 106.1 ms, latency ladder 113.8 vs 109.7 ms at B = 4096: the random-index table
+// reads bank-conflict), so off by default.
+#ifndef HWB_T0
+#define HWB_T0 0
+#endif
+constexpr int kT0Max = 1024;
 // the MAC accumulation as a 3-operand add too (measured slower in the 2-warp
 // ladder: 119 vs 106 ms -- the compiler then schedules the digit loop worse)
 #ifndef HWB_MACZ_ON
@@ -235,7 +243,24 @@ struct Smem {
   uint32_t acc[2 * N];   // working ciphertext (a, b)
   uint32_t v[2 * N];     // decomposition-ready input; then the residue exchange
   uint32_t scr[2][N];    // per-group transpose scratch
+#if HWB_T0
+  uint32_t t0[2][kT0Max];   // first-stage digit products w0 * (d - beta/2) mod p_w
+#endif
 };
+
+// Fill the first-stage digit tables (beta <= kT0Max entries per prime); every
+// ladder kernel calls this before its first barrier.
+__device__ __forceinline__ void init_t0(uint32_t (*t0)[kT0Max], const Gadget &g, int nv, int tid, int nt) {
+  const int beta = (int)g.mask + 1;
+  if (beta > kT0Max) return;
+  for (int k = tid; k < 2 * beta; k += nt) {
+    const int w = k >= beta, d = k - w * beta;
+    const uint32_t p = c_prime[w].p;
+    const uint2 w0 = c_tw[nv][0][w][1];
+    const uint32_t r = shoup_mul((uint32_t)d + p - g.half, w0.x, w0.y, p);
+    t0[w][d] = umin(r, r - p);
+  }
+}
 
 struct Tw {
   const uint2 *fwd[2];
@@ -309,9 +334,28 @@ __device__ __forceinline__ void ext_product_core_p(Smem<N> &sm, const uint32_t *
           for (int q = t; q < N / 32; q += TPP) prefetch_l2(gn + ((size_t)c * 2 + w) * N + q * 32);
       }
     }
+#if HWB_T0
+    if (g.mask < (uint32_t)kT0Max) {
+      const uint32_t *tab = sm.t0[w];
+#pragma unroll
+      for (int j = 0; j < C / 2; ++j)
+        digit_stage0(x[j], x[j + C / 2], (vs[TPP * j] >> sh) & g.mask, (vs[TPP * (j + C / 2)] >> sh) & g.mask,
+                     tab, off, 2 * p);
+    } else {
+      const uint2 w0 = c_tw[NVar<N>::v][0][w][1];
+#pragma unroll
+      for (int j = 0; j < C / 2; ++j) {
+        x[j] = ((vs[TPP * j] >> sh) & g.mask) + off;
+        x[j + C / 2] = ((vs[TPP * (j + C / 2)] >> sh) & g.mask) + off;
+        ct_bfly_lazy<false>(x[j], x[j + C / 2], w0.x, w0.y, p, 2 * p);
+      }
+    }
+    fwd_ntt<N, TPP, PRIME, true>(x, sm.scr[w], me.lay, t, w, twf);
+#else
 #pragma unroll
     for (int j = 0; j < C; ++j) x[j] = ((vs[TPP * j] >> sh) & g.mask) + off;
     fwd_ntt<N, TPP, PRIME>(x, sm.scr[w], me.lay, t, w, twf);
+#endif
     const uint32_t *g0 = G + ((size_t)(r * 2 + 0) * 2 + w) * N;
     const uint32_t *g1 = G + ((size_t)(r * 2 + 1) * 2 + w) * N;
 #pragma unroll
@@ -436,6 +480,9 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::minb(V))
   const uint32_t *s1 = MODE == MODE_VP_LEVEL ? in + (item * 2 * m + m + sub) * 2 * N : (c1 ? c1 + b * 2 * N : nullptr);
   uint32_t *o_lo = out + (MODE == MODE_IVP_LEVEL ? (item * 2 * m + sub) : b) * 2 * N;
   uint32_t *o_hi = MODE == MODE_IVP_LEVEL ? out + (item * 2 * m + m + sub) * 2 * N : (out_hi ? out_hi + b * 2 * N : nullptr);
+#if HWB_T0
+  init_t0(sm.t0, g, NVar<N>::v, tid, NT);
+#endif
   if (MODE == MODE_EXT) {
     for (int k = tid; k < 2 * N; k += NT) sm.v[k] = decomp_prep(src[k], g);
   } else {
@@ -543,6 +590,9 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::minb(V))
   const Who<N> me;
   const int tid = me.tid, w = me.grp;
   const uint32_t *row = PBS ? lwe_in + b * (int64_t)(L + 1) : nullptr;
+#if HWB_T0
+  init_t0(sm.t0, g, NVar<N>::v, tid, NT);
+#endif
   if (PBS) {
     const int bt = mod_switch(row[L], LOG2M);
     const uint32_t *tp = tv + (tv_per_item ? b * 2 * N : 0);
@@ -616,6 +666,9 @@ struct SmemLat {
   uint32_t v[2 * N];
   uint32_t macc[2][2][N];          // [component][prime], NTT domain
   uint32_t scr[4 * LV][N];         // per-warp transpose scratch
+#if HWB_T0
+  uint32_t t0[2][kT0Max];
+#endif
 };
 
 // MINB = resident CTAs per SM the build targets: 1 (168 registers, lowest
@@ -650,6 +703,9 @@ __global__ void __launch_bounds__(128 * LV, MINB)
     for (int k = tid; k < 2 * N; k += NT) sm.acc[k] = acc_io[b * 2 * N + k];
   }
   for (int k = tid; k < 4 * N; k += NT) (&sm.macc[0][0][0])[k] = 0u;
+#if HWB_T0
+  init_t0(sm.t0, g, 0, tid, NT);
+#endif
   __syncthreads();
   uint32_t x[C];
 #pragma unroll 1
@@ -677,9 +733,28 @@ __global__ void __launch_bounds__(128 * LV, MINB)
       const uint32_t *vs = sm.v + comp * N + t;
 #pragma unroll
       for (int c = 0; c < 2; ++c) prefetch_l2(G + ((size_t)(r * 2 + c) * 2 + w) * N + t * 32);
+#if HWB_T0
+      if (g.mask < (uint32_t)kT0Max) {
+        const uint32_t *tab = sm.t0[w];
+#pragma unroll
+        for (int j = 0; j < C / 2; ++j)
+          digit_stage0(x[j], x[j + C / 2], (vs[TPP * j] >> sh) & g.mask, (vs[TPP * (j + C / 2)] >> sh) & g.mask,
+                       tab, off, 2 * p);
+      } else {
+        const uint2 w0 = c_tw[0][0][w][1];
+#pragma unroll
+        for (int j = 0; j < C / 2; ++j) {
+          x[j] = ((vs[TPP * j] >> sh) & g.mask) + off HWB_Z;
+          x[j + C / 2] = ((vs[TPP * (j + C / 2)] >> sh) & g.mask) + off HWB_Z;
+          ct_bfly_lazy<false>(x[j], x[j + C / 2], w0.x, w0.y, p, 2 * p);
+        }
+      }
+      fwd_ntt<N, TPP, -1, true>(x, sm.scr[wi], lay, t, w, w ? tw.fwd[1] : tw.fwd[0]);
+#else
 #pragma unroll
       for (int j = 0; j < C; ++j) x[j] = ((vs[TPP * j] >> sh) & g.mask) + off HWB_Z;
       fwd_ntt<N, TPP, -1>(x, sm.scr[wi], lay, t, w, w ? tw.fwd[1] : tw.fwd[0]);
+#endif
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const uint32_t *gs = G + ((size_t)(r * 2 + c) * 2 + w) * N;
