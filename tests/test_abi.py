@@ -77,3 +77,33 @@ def test_variant_switch_validation():
     with pytest.raises(_lib.TfheError):
         _lib.set_variant(7)
     _lib.set_variant(0)
+
+
+def test_tensor_core_keyswitch_sizes_and_validation():
+    """hwb_ksk_tc_bytes / workspace sizes and argument checks (host-only)."""
+    L = _lib.load()
+    P = named_params("CFG2")                       # n = 630, N = 1024, KS 2^2 x 8
+    cp = _lib.c_params(P)
+    n_col_tiles, k_blocks = (P.lwe_n + 1 + 63) // 64, 1024 * 8 // 128
+    assert L.hwb_ksk_tc_bytes(ctypes.byref(cp)) == n_col_tiles * k_blocks * 32768
+    assert L.hwb_keyswitch_tc_workspace_bytes(ctypes.byref(cp), 129) == 256 * 1024 * 8
+    ext = (4 * 129 * 1025 + 255) // 256 * 256
+    assert L.hwb_pbs_tc_workspace_bytes(ctypes.byref(cp), 129) == ext + 256 * 1024 * 8
+    null = ctypes.c_void_p(0)
+    assert L.hwb_keyswitch_tc(ctypes.byref(cp), null, null, null, 0, null, null) == 0     # B = 0
+    assert L.hwb_keyswitch_tc(ctypes.byref(cp), null, null, null, 1, null, null) == _lib.HWB_EINVAL
+    assert "workspace" in L.hwb_last_error().decode()
+    cp.ks_base_log, cp.ks_l = 10, 2                # digits beyond int8
+    assert L.hwb_ksk_tc_bytes(ctypes.byref(cp)) == 0
+    assert L.hwb_ksk_to_tc(ctypes.byref(cp), null, null, null) == _lib.HWB_EINVAL
+    assert "int8" in L.hwb_last_error().decode()
+
+
+def test_latency_threshold_roundtrip():
+    prev = _lib.set_latency_batch(5)
+    try:
+        assert _lib.set_latency_batch(-2) == 5          # < -1 only queries
+        assert _lib.set_latency_batch(-1) == 5          # -1 = automatic
+        assert _lib.set_latency_batch(-2) == -1
+    finally:
+        _lib.set_latency_batch(prev)
