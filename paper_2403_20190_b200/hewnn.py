@@ -207,12 +207,28 @@ def _shift(codes: np.ndarray, base: int) -> np.ndarray:
     return np.where(codes >= 0, codes + base, codes)
 
 
-def _payload(params: HeParams) -> np.ndarray:
-    return tfhe.trivial_rlwe(1, params).data
+_PAYLOADS: dict = {}
+
+
+def _payload(params: HeParams) -> torch.Tensor:
+    """Trivial RLWE (0, q/p) payload of the IVP, cached on the device."""
+    key = (params, torch.cuda.current_device())
+    if key not in _PAYLOADS:
+        _PAYLOADS[key] = tfhe.to_device(tfhe.trivial_rlwe(1, params).data)
+    return _PAYLOADS[key]
 
 
 # ---------------------------------------------------------------------------
 # training
+
+
+_TRACE = None          # list of (label, cuda.Event) when tracing the pipeline (tools/)
+
+
+def _ev(stream=None):
+    e = torch.cuda.Event(enable_timing=True)
+    e.record(stream)
+    return e
 
 
 class _Staged:
@@ -233,9 +249,13 @@ class _Staged:
         cs = _Staged._copy_stream
         cs.wait_stream(torch.cuda.current_stream())         # buffers freed on the main stream
         with torch.cuda.stream(cs):
+            if _TRACE is not None:
+                _TRACE.append(("copy_start", _ev(cs)))
             self.dev = [tfhe.to_device(s.rgsw) for s in samples]
-            self.event = torch.cuda.Event()
+            self.event = torch.cuda.Event(enable_timing=_TRACE is not None)
             self.event.record(cs)
+            if _TRACE is not None:
+                _TRACE.append(("copy_end", self.event))
 
     def tensors(self) -> list:
         if self.dev is None:
@@ -265,9 +285,10 @@ def _stack_table(params: HeParams, samples: list[EncryptedSample], staged: _Stag
     return tfhe.GgswNtt(params, table)
 
 
-def he_count_labels_batch(params: HeParams, counts_ct: torch.Tensor, table, label_rows: np.ndarray):
+def he_count_labels_batch(params: HeParams, counts_ct: torch.Tensor, table, label_rows: np.ndarray,
+                          dev_rows: torch.Tensor | None = None):
     """hw/hewnn.py:180-186 for several samples: counts += IVP(label bits, (0, q/p))."""
-    rows = lut.ivp_codes(params, label_rows, table, _payload(params))     # (I, 1, 2, N)
+    rows = lut.ivp_codes(params, label_rows, table, _payload(params), dev_rows)     # (I, 1, 2, N)
     lut.accumulate_rows_(counts_ct, rows)
     return counts_ct
 
@@ -283,16 +304,24 @@ def he_train(samples: Iterable[EncryptedSample], geometry: WisardGeometry, param
     if model.geometry != geometry or model.params != params:
         raise TfheError("model geometry/params mismatch")
     tmpl = _selector_template(geometry, params)
+    # a chunk's selector codes and label rows depend only on the sample's slot in
+    # the chunk: build them once for a full chunk and upload them now, before
+    # the staged RGSW transfers start (no host->device copy inside the pipeline)
+    stride = geometry.s + geometry.label_bits
+    k0 = geometry.k0
+    all_codes = np.concatenate([_shift(tmpl, i * stride) for i in range(batch)])
+    all_labels = np.array([[i * stride + geometry.s + b for b in range(geometry.label_bits)]
+                           for i in range(batch)], dtype=np.int64).reshape(batch, geometry.label_bits)
+    d_codes, d_labels = lut._upload_i32([all_codes, all_labels], tfhe._device())
+    _payload(params)
 
     def run(chunk: list[EncryptedSample], staged: _Staged):
         table = _stack_table(params, chunk, staged)
-        stride = geometry.s + geometry.label_bits
-        codes = np.concatenate([_shift(tmpl, i * stride) for i in range(len(chunk))])
-        rows = lut.ivp_codes(params, codes, table, _payload(params))      # (I*k0, k1, 2, N)
+        I = len(chunk)
+        rows = lut.ivp_codes(params, all_codes[: I * k0], table, _payload(params),
+                             d_codes[: I * k0])                              # (I*k0, k1, 2, N)
         lut.accumulate_rows_(model.rams, rows)                             # hw/hewnn.py:213
-        label_rows = np.array([[i * stride + geometry.s + b for b in range(geometry.label_bits)]
-                               for i in range(len(chunk))], dtype=np.int64)
-        he_count_labels_batch(params, model.counts_ct, table, label_rows)
+        he_count_labels_batch(params, model.counts_ct, table, all_labels[:I], d_labels[:I])
 
     def check(sample):
         if sample.s != geometry.s:
@@ -303,7 +332,11 @@ def he_train(samples: Iterable[EncryptedSample], geometry: WisardGeometry, param
     # one chunk in flight: chunk k+1's H2D is enqueued on the copy stream before
     # chunk k's ladders, so host->device traffic overlaps the GPU work
     for chunk, staged in _chunks_staged(samples, batch, check):
+        if _TRACE is not None:
+            _TRACE.append(("run_start", _ev()))
         run(chunk, staged)
+        if _TRACE is not None:
+            _TRACE.append(("run_end", _ev()))
     return model
 
 

@@ -117,7 +117,23 @@ def accumulate_rows_(dst: torch.Tensor, rows: torch.Tensor) -> torch.Tensor:
     return dst
 
 
-def _rotation_ladder(params, table: GgswNtt, acc: torch.Tensor, cols: np.ndarray, sign: int) -> torch.Tensor:
+def _upload_i32(arrays, device) -> list[torch.Tensor]:
+    """Several small host index arrays -> device int32 views through ONE pinned,
+    non-blocking copy.  A pageable copy would block the host until the stream
+    drains and queue behind in-flight bulk transfers (he_train stages the next
+    chunk's RGSW stacks on a copy stream)."""
+    flat = [np.ascontiguousarray(np.asarray(a, dtype=np.int64).astype(np.int32)).ravel() for a in arrays]
+    host = torch.from_numpy(np.concatenate(flat) if flat else np.zeros(0, np.int32)).pin_memory()
+    dev = host.to(device, non_blocking=True)
+    out, off = [], 0
+    for a, f in zip(arrays, flat):
+        out.append(dev[off: off + f.size].view(np.shape(a)))
+        off += f.size
+    return out
+
+
+def _rotation_ladder(params, table: GgswNtt, acc: torch.Tensor, cols: np.ndarray, sign: int,
+                     dev_args: tuple | None = None) -> torch.Tensor:
     """All encrypted rotation positions of a selector batch in ONE launch
     (hwb_blind_rotate with per-item GGSW rows): for position i (weight 2^i),
     acc <- cmux(C, acc * X^(sign 2^i), acc) where the bit is encrypted; clear
@@ -127,12 +143,19 @@ def _rotation_ladder(params, table: GgswNtt, acc: torch.Tensor, cols: np.ndarray
     if L == 0 or not (cols >= 0).any():
         return acc
     dev = acc.device
-    idx = _i32(np.where(cols >= 0, cols, -1), dev)
-    exps = _i32(np.broadcast_to(-sign * (1 << np.arange(L, dtype=np.int64)), (B, L)) % (2 * params.n), dev)
+    if dev_args is not None:
+        idx, exps = dev_args
+    else:
+        idx = _i32(np.where(cols >= 0, cols, -1), dev)
+        exps = _i32(_rotation_exps(params, B, L, sign), dev)
     out = acc.contiguous().clone()
     _lib.check(_lib.load().hwb_blind_rotate(_cp(params), tfhe._ptr(table.data), tfhe._ptr(idx), tfhe._ptr(exps),
                                             tfhe._ptr(out), L, B, tfhe._stream()))
     return out
+
+
+def _rotation_exps(params, B: int, L: int, sign: int) -> np.ndarray:
+    return np.broadcast_to(-sign * (1 << np.arange(L, dtype=np.int64)), (B, L)) % (2 * params.n)
 
 
 def _level(params, table: GgswNtt, cur: torch.Tensor, idx: torch.Tensor, inverse: bool) -> torch.Tensor:
@@ -152,11 +175,14 @@ def _level(params, table: GgswNtt, cur: torch.Tensor, idx: torch.Tensor, inverse
 # batched engines over code matrices
 
 
-def ivp_codes(params: HeParams, codes, table: GgswNtt | None, payload) -> torch.Tensor:
+def ivp_codes(params: HeParams, codes, table: GgswNtt | None, payload,
+              dev_codes: torch.Tensor | None = None) -> torch.Tensor:
     """Inverse vertical packing (hw/lut.py:269-314) for B items sharing one payload.
 
     codes: (B, k) int (row of `table`, CLEAR0 or CLEAR1).  Returns the device
-    tensor (B, max(1, 2^z), 2, N) of single-valued LUT rows."""
+    tensor (B, max(1, 2^z), 2, N) of single-valued LUT rows.  dev_codes: the
+    same codes already on the device (int32), so the pass issues no host->device
+    copy at all (he_train uploads one chunk's codes once and reuses them)."""
     codes = np.asarray(codes, dtype=np.int64)
     B, k = codes.shape
     z = tree_depth(k, params)
@@ -167,7 +193,17 @@ def ivp_codes(params: HeParams, codes, table: GgswNtt | None, payload) -> torch.
     nrot = len(rotate_weights(k, params))
     rcols = codes[:, z: z + nrot]
     clear_e = ((rcols == CLEAR1).astype(np.int64) << np.arange(nrot, dtype=np.int64)).sum(axis=1)
-    acc = _rotation_ladder(params, table, acc, rcols, +1)                  # X^{+2^w} (hw/lut.py:289)
+    # every index array of the pass in one pinned upload: rotation GGSW rows and
+    # exponents, then the tree levels' columns
+    if dev_codes is not None:
+        d_idx = dev_codes[:, z: z + nrot].contiguous()                       # CLEAR codes are < 0: skipped
+        d_exps = torch.remainder(-(2 ** torch.arange(nrot, device=dev, dtype=torch.int64)), 2 * n)
+        d_exps = d_exps.to(torch.int32).expand(B, nrot).contiguous()
+        d_cols = [dev_codes[:, pos].contiguous() for pos in range(z)]
+    else:
+        d_idx, d_exps, d_cols = _upload_i32([np.where(rcols >= 0, rcols, -1), _rotation_exps(params, B, nrot, +1),
+                                             codes[:, :z].T], dev)
+    acc = _rotation_ladder(params, table, acc, rcols, +1, (d_idx, d_exps))    # X^{+2^w} (hw/lut.py:289)
     if clear_e.any():
         acc = monomial_gather(params, acc, clear_e)
     cur = acc.unsqueeze(1)
@@ -175,7 +211,7 @@ def ivp_codes(params: HeParams, codes, table: GgswNtt | None, payload) -> torch.
         col = codes[:, pos]
         enc = col >= 0
         if enc.all():
-            cur = _level(params, table, cur.contiguous(), _i32(col, dev), inverse=True)
+            cur = _level(params, table, cur.contiguous(), d_cols[pos], inverse=True)
             continue
         mm = cur.shape[1]
         new = torch.zeros((B, 2 * mm, 2, n), dtype=torch.int32, device=dev)
