@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="PBS per CPU step (0 = auto)")
     ap.add_argument("--train-cfg", type=int, default=3, choices=[1, 3, 4, 5])
-    ap.add_argument("--train-images", type=int, default=64, help="0 disables the training measurement")
+    ap.add_argument("--train-images", type=int, default=128, help="0 disables the training measurement")
     ap.add_argument("--train-batch", type=int, default=32)
     ap.add_argument("--infer-images", type=int, default=32, help="0 disables the inference measurement")
     ap.add_argument("--sweep", default="1,16,148,592,1184,4096,16384,65536",
