@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--train-images", type=int, default=128, help="0 disables the training measurement")
     ap.add_argument("--train-batch", type=int, default=32)
     ap.add_argument("--infer-images", type=int, default=32, help="0 disables the inference measurement")
+    ap.add_argument("--no-other-configs", dest="other_configs", action="store_false",
+                    help="skip the cfg1/cfg4 PBS measurements")
     ap.add_argument("--sweep", default="1,16,148,592,1184,4096,16384,65536",
                     help="comma-separated PBS batch sizes for the cfg2 sweep ('' disables)")
     return ap.parse_args()
@@ -487,6 +489,35 @@ def bench_hwb(args):
                               "decrypt_ok": ok_s}
             del lw, res
         result["sweep"] = sweep
+    if args.other_configs:
+        # the other BASELINE PBS parameter sets (cfg1: n=500, l=2, 2^8; cfg4: N=2048,
+        # n=750, l=2, 2^10), same batch, device-resident, decryption checked
+        other = {}
+        for name in ("CFG1", "CFG4"):
+            Po = named_params(name)
+            ko, mo, lo, tvo = workload(Po, B, rank)
+            bo, kso = ko.device_keys()
+            lwo, tvd = tfhe.to_device(lo), tfhe.to_device(tvo)
+            res = tfhe.pbs_batch(Po, lwo, tvd, bo, kso)                        # warm-up
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            s0.record()
+            for _ in range(2):
+                res = tfhe.pbs_batch(Po, lwo, tvd, bo, kso)
+            s1.record()
+            s1.synchronize()
+            t_ms = s0.elapsed_time(s1) / 2
+            lvo, No = Po.gadget.levels, Po.n
+            w_o = Po.lwe_n * (2 * lvo * (No // 2) * Po.degree_log + 2 * (No // 2) * Po.degree_log + 4 * lvo * No)
+            entry = {"pbs_per_s": round(B / (t_ms * 1e-3), 1), "ms_per_batch": round(t_ms, 3),
+                     "roofline_frac": round(w_o * B / (t_ms * 1e-3) / peak, 4),
+                     "params": f"n={Po.lwe_n} N={No} Bg=2^{Po.gadget.base_log} l={lvo}"}
+            if Po.p * 2 <= No:   # PBS decryption is meaningful (>= 2 phase units per message)
+                entry["decrypt_ok"] = bool(np.array_equal(tfhe.dec_lwe_batch(tfhe.to_host(res), ko.lwe_key),
+                                                          expected(mo, Po.p)))
+            other[name.lower()] = entry
+            del bo, kso, lwo, res
+        result["other_configs"] = other
     if args.train_images > 0:
         result["train"] = bench_train(args, world, rank, torch, dist)
     if world > 1:
