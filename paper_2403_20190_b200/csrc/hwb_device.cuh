@@ -91,23 +91,6 @@ __device__ __forceinline__ void prefetch_l2(const void *ptr) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
 }
 
-// Montgomery product without the +p offset: a*b*2^-32 mod p in (-p, p) as a
-// wrapped 32-bit value; accumulate with acc + mont_mul_nop(...) (one IADD3)
-// and add the sum of the offsets once.
-__device__ __forceinline__ uint32_t mont_hi(uint32_t a, uint32_t b, uint32_t pinv, uint32_t p, uint32_t acc) {
-  uint64_t t = (uint64_t)a * b;
-  uint32_t lo = (uint32_t)t, hi = (uint32_t)(t >> 32);
-  uint32_t m = lo * pinv;
-  return acc + hi - __umulhi(m, p);
-}
-
-// Montgomery reduction of a 64-bit sum T < 2^63.01 (signed variant, pinv = p^-1
-// mod 2^32): T * 2^-32 mod p in (0, 7p).
-__device__ __forceinline__ uint32_t redc64(uint64_t T, uint32_t p, uint32_t pinv) {
-  const uint32_t m = (uint32_t)T * pinv;
-  return (uint32_t)(T >> 32) - __umulhi(m, p) + p;
-}
-
 // Harvey lazy Cooley-Tukey butterfly: X, Y in [0, 4p) -> [0, 4p).
 __device__ __forceinline__ void ct_bfly(uint32_t &X, uint32_t &Y, uint32_t w, uint32_t wq,
                                         uint32_t p, uint32_t two_p) {
@@ -132,17 +115,6 @@ __device__ __forceinline__ void ct_bfly_lazy(uint32_t &X, uint32_t &Y, uint32_t 
     x = umin(x, x - two_p);
   }
   uint32_t t = shoup_mul(Y, w, wq, p);
-  X = x + t HWB_Z;
-  Y = x - t + two_p;
-}
-
-// First forward stage on gadget digits: inputs are d + p - beta/2 with digit
-// index d in [0, beta), so the twiddle product w0 * (d - beta/2) mod p comes from
-// a beta-entry table (tab[d], canonical) instead of a Shoup product.  Outputs
-// X < 3p, Y < 4p: within the lazy bound ct_bfly_lazy assumes after one stage.
-__device__ __forceinline__ void digit_stage0(uint32_t &X, uint32_t &Y, uint32_t da, uint32_t db,
-                                             const uint32_t *tab, uint32_t off, uint32_t two_p) {
-  const uint32_t x = da + off, t = tab[db];
   X = x + t HWB_Z;
   Y = x - t + two_p;
 }
@@ -279,14 +251,12 @@ __device__ __forceinline__ void ntt_stage(uint32_t (&x)[N / TPP], int t, int pri
 // In: layout A, values < 2p.  Out: layout B, values < 12p (lazy reduction:
 // x is reduced only on execution stages 5 and 10 -- see ct_bfly_lazy).
 // Per-thread twiddle slots: M stages s = T-1..LOGC, then B stages s = B_TOP-1..0.
-// SKIP0: the caller already applied the first stage (s = LOGN-1, uniform
-// twiddle c_tw[..][1]) -- see digit_stage0.
-template <int N, int TPP, int PRIME, bool SKIP0 = false>
+template <int N, int TPP, int PRIME>
 __device__ __forceinline__ void fwd_ntt(uint32_t (&x)[N / TPP], uint32_t *scr, const LayBase &L, int t, int prime,
                                         const uint2 *__restrict__ tw) {
   using G = Geo<N, TPP>;
   const int group = PRIME >= 0 ? PRIME : prime;
-  static_for<SKIP0 ? 1 : 0, G::LOGN - G::T>([&](auto K) {   // A stages s = LOGN-1 .. T
+  static_for<0, G::LOGN - G::T>([&](auto K) {          // A stages s = LOGN-1 .. T
     constexpr int s = G::LOGN - 1 - decltype(K)::value;
     constexpr bool red = (G::LOGN - 1 - s) % 5 == 0 && s != G::LOGN - 1;
     ntt_stage<N, TPP, PRIME, true, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0, red>(x, t, prime, tw);

@@ -52,30 +52,6 @@ static int fail(int code, const std::string &msg) {
 #ifndef HWB_V1_MINB
 #define HWB_V1_MINB 6
 #endif
-#ifndef HWB_ACC64
-#define HWB_ACC64 0
-#endif
-#ifndef HWB_MONTHI
-#define HWB_MONTHI 0
-#endif
-// first forward stage of the digit transforms from a beta-entry shared-memory
-// table instead of Shoup products.  Measured slower (throughput ladder 109.6 vs
-// 106.1 ms, latency ladder 113.8 vs 109.7 ms at B = 4096: the random-index table
-// reads bank-conflict), so off by default.
-#ifndef HWB_T0
-#define HWB_T0 0
-#endif
-constexpr int kT0Max = 1024;
-// the MAC accumulation as a 3-operand add too (measured slower in the 2-warp
-// ladder: 119 vs 106 ms -- the compiler then schedules the digit loop worse)
-#ifndef HWB_MACZ_ON
-#define HWB_MACZ_ON 0
-#endif
-#if HWB_MACZ_ON
-#define HWB_MACZ HWB_Z
-#else
-#define HWB_MACZ
-#endif
 template <int N> struct Cfg {
   static constexpr int TPP = (N == 1024) ? 32 : 64;
   static constexpr int THREADS = 2 * TPP;
@@ -243,24 +219,7 @@ struct Smem {
   uint32_t acc[2 * N];   // working ciphertext (a, b)
   uint32_t v[2 * N];     // decomposition-ready input; then the residue exchange
   uint32_t scr[2][N];    // per-group transpose scratch
-#if HWB_T0
-  uint32_t t0[2][kT0Max];   // first-stage digit products w0 * (d - beta/2) mod p_w
-#endif
 };
-
-// Fill the first-stage digit tables (beta <= kT0Max entries per prime); every
-// ladder kernel calls this before its first barrier.
-__device__ __forceinline__ void init_t0(uint32_t (*t0)[kT0Max], const Gadget &g, int nv, int tid, int nt) {
-  const int beta = (int)g.mask + 1;
-  if (beta > kT0Max) return;
-  for (int k = tid; k < 2 * beta; k += nt) {
-    const int w = k >= beta, d = k - w * beta;
-    const uint32_t p = c_prime[w].p;
-    const uint2 w0 = c_tw[nv][0][w][1];
-    const uint32_t r = shoup_mul((uint32_t)d + p - g.half, w0.x, w0.y, p);
-    t0[w][d] = umin(r, r - p);
-  }
-}
 
 struct Tw {
   const uint2 *fwd[2];
@@ -297,24 +256,9 @@ __device__ __forceinline__ void ext_product_core_p(Smem<N> &sm, const uint32_t *
   const int L = (int)g.levels;
   const uint2 *twf = w ? tw.fwd[1] : tw.fwd[0];
   const uint2 *twi = w ? tw.inv[1] : tw.inv[0];
-#if HWB_ACC64
-  // 64-bit accumulation of the 2l products (IMAD.WIDE with accumulate), one
-  // Montgomery reduction per output: x < 2^32, G < p < 2^28.42, 2l <= 6 terms
-  // -> sum < 2^63.01; REDC gives hi - umulhi(m, p) + p < 7p.
-  uint64_t a0[C], a1[C];
-#else
   uint32_t a0[C], a1[C];
-#endif
-#if HWB_ACC64 || !HWB_MONTHI
 #pragma unroll
   for (int j = 0; j < C; ++j) a0[j] = a1[j] = 0;
-#else
-  // each Montgomery term is added as hi - umulhi(m, p) in (-p, p); the 2l
-  // offsets of +p are folded into the initial value (sum in (0, 12p) as before)
-  const uint32_t acc0 = 2u * (uint32_t)L * p + c_zero;
-#pragma unroll
-  for (int j = 0; j < C; ++j) a0[j] = a1[j] = acc0;
-#endif
 
 #pragma unroll 1
   for (int r = 0; r < 2 * L; ++r) {
@@ -334,89 +278,40 @@ __device__ __forceinline__ void ext_product_core_p(Smem<N> &sm, const uint32_t *
           for (int q = t; q < N / 32; q += TPP) prefetch_l2(gn + ((size_t)c * 2 + w) * N + q * 32);
       }
     }
-#if HWB_T0
-    if (g.mask < (uint32_t)kT0Max) {
-      const uint32_t *tab = sm.t0[w];
-#pragma unroll
-      for (int j = 0; j < C / 2; ++j)
-        digit_stage0(x[j], x[j + C / 2], (vs[TPP * j] >> sh) & g.mask, (vs[TPP * (j + C / 2)] >> sh) & g.mask,
-                     tab, off, 2 * p);
-    } else {
-      const uint2 w0 = c_tw[NVar<N>::v][0][w][1];
-#pragma unroll
-      for (int j = 0; j < C / 2; ++j) {
-        x[j] = ((vs[TPP * j] >> sh) & g.mask) + off;
-        x[j + C / 2] = ((vs[TPP * (j + C / 2)] >> sh) & g.mask) + off;
-        ct_bfly_lazy<false>(x[j], x[j + C / 2], w0.x, w0.y, p, 2 * p);
-      }
-    }
-    fwd_ntt<N, TPP, PRIME, true>(x, sm.scr[w], me.lay, t, w, twf);
-#else
 #pragma unroll
     for (int j = 0; j < C; ++j) x[j] = ((vs[TPP * j] >> sh) & g.mask) + off;
     fwd_ntt<N, TPP, PRIME>(x, sm.scr[w], me.lay, t, w, twf);
-#endif
     const uint32_t *g0 = G + ((size_t)(r * 2 + 0) * 2 + w) * N;
     const uint32_t *g1 = G + ((size_t)(r * 2 + 1) * 2 + w) * N;
 #pragma unroll
     for (int jq = 0; jq < C / 4; ++jq) {
       const uint4 G0 = __ldg(slice_vec<TPP>(g0, t, jq));
       const uint4 G1 = __ldg(slice_vec<TPP>(g1, t, jq));
-#if HWB_ACC64
-      a0[4 * jq + 0] += (uint64_t)x[4 * jq + 0] * G0.x;
-      a0[4 * jq + 1] += (uint64_t)x[4 * jq + 1] * G0.y;
-      a0[4 * jq + 2] += (uint64_t)x[4 * jq + 2] * G0.z;
-      a0[4 * jq + 3] += (uint64_t)x[4 * jq + 3] * G0.w;
-      a1[4 * jq + 0] += (uint64_t)x[4 * jq + 0] * G1.x;
-      a1[4 * jq + 1] += (uint64_t)x[4 * jq + 1] * G1.y;
-      a1[4 * jq + 2] += (uint64_t)x[4 * jq + 2] * G1.z;
-      a1[4 * jq + 3] += (uint64_t)x[4 * jq + 3] * G1.w;
-#elif !HWB_MONTHI
-      a0[4 * jq + 0] = a0[4 * jq + 0] + mont_mul(x[4 * jq + 0], G0.x, p, pinv) HWB_MACZ;
-      a0[4 * jq + 1] = a0[4 * jq + 1] + mont_mul(x[4 * jq + 1], G0.y, p, pinv) HWB_MACZ;
-      a0[4 * jq + 2] = a0[4 * jq + 2] + mont_mul(x[4 * jq + 2], G0.z, p, pinv) HWB_MACZ;
-      a0[4 * jq + 3] = a0[4 * jq + 3] + mont_mul(x[4 * jq + 3], G0.w, p, pinv) HWB_MACZ;
-      a1[4 * jq + 0] = a1[4 * jq + 0] + mont_mul(x[4 * jq + 0], G1.x, p, pinv) HWB_MACZ;
-      a1[4 * jq + 1] = a1[4 * jq + 1] + mont_mul(x[4 * jq + 1], G1.y, p, pinv) HWB_MACZ;
-      a1[4 * jq + 2] = a1[4 * jq + 2] + mont_mul(x[4 * jq + 2], G1.z, p, pinv) HWB_MACZ;
-      a1[4 * jq + 3] = a1[4 * jq + 3] + mont_mul(x[4 * jq + 3], G1.w, p, pinv) HWB_MACZ;
-#else
-      a0[4 * jq + 0] = mont_hi(x[4 * jq + 0], G0.x, pinv, p, a0[4 * jq + 0]);
-      a0[4 * jq + 1] = mont_hi(x[4 * jq + 1], G0.y, pinv, p, a0[4 * jq + 1]);
-      a0[4 * jq + 2] = mont_hi(x[4 * jq + 2], G0.z, pinv, p, a0[4 * jq + 2]);
-      a0[4 * jq + 3] = mont_hi(x[4 * jq + 3], G0.w, pinv, p, a0[4 * jq + 3]);
-      a1[4 * jq + 0] = mont_hi(x[4 * jq + 0], G1.x, pinv, p, a1[4 * jq + 0]);
-      a1[4 * jq + 1] = mont_hi(x[4 * jq + 1], G1.y, pinv, p, a1[4 * jq + 1]);
-      a1[4 * jq + 2] = mont_hi(x[4 * jq + 2], G1.z, pinv, p, a1[4 * jq + 2]);
-      a1[4 * jq + 3] = mont_hi(x[4 * jq + 3], G1.w, pinv, p, a1[4 * jq + 3]);
-#endif
+      a0[4 * jq + 0] += mont_mul(x[4 * jq + 0], G0.x, p, pinv);
+      a0[4 * jq + 1] += mont_mul(x[4 * jq + 1], G0.y, p, pinv);
+      a0[4 * jq + 2] += mont_mul(x[4 * jq + 2], G0.z, p, pinv);
+      a0[4 * jq + 3] += mont_mul(x[4 * jq + 3], G0.w, p, pinv);
+      a1[4 * jq + 0] += mont_mul(x[4 * jq + 0], G1.x, p, pinv);
+      a1[4 * jq + 1] += mont_mul(x[4 * jq + 1], G1.y, p, pinv);
+      a1[4 * jq + 2] += mont_mul(x[4 * jq + 2], G1.z, p, pinv);
+      a1[4 * jq + 3] += mont_mul(x[4 * jq + 3], G1.w, p, pinv);
     }
   }
-#if HWB_ACC64
-  uint32_t b0[C], b1[C];
+  // 2l <= 6 terms in (0, 2p): sums < 12p < 2^32; reduce to [0, 2p)
 #pragma unroll
   for (int j = 0; j < C; ++j) {
-    b0[j] = redc64(a0[j], p, pinv);
-    b1[j] = redc64(a1[j], p, pinv);
-  }
-#else
-  uint32_t (&b0)[C] = a0, (&b1)[C] = a1;
-#endif
-  // sums < 16p: reduce to [0, 2p)
-#pragma unroll
-  for (int j = 0; j < C; ++j) {
-    uint32_t u = b0[j], v = b1[j];
+    uint32_t u = a0[j], v = a1[j];
     u = umin(u, u - 4 * two_p); v = umin(v, v - 4 * two_p);
     u = umin(u, u - 2 * two_p); v = umin(v, v - 2 * two_p);
     u = umin(u, u - two_p);     v = umin(v, v - two_p);
-    b0[j] = u; b1[j] = v;
+    a0[j] = u; a1[j] = v;
   }
   __syncthreads();   // both groups are done reading sm.v: it becomes the exchange buffer
 #pragma unroll 1
   for (int it = 0; it < 2; ++it) {
     const int c = it == 0 ? 1 - w : w;
 #pragma unroll
-    for (int j = 0; j < C; ++j) x[j] = c ? b1[j] : b0[j];
+    for (int j = 0; j < C; ++j) x[j] = c ? a1[j] : a0[j];
     inv_ntt<N, TPP, PRIME>(x, sm.scr[w], me.lay, t, w, twi);
 #pragma unroll
     for (int j = 0; j < C; ++j) x[j] = umin(x[j], x[j] - p);
@@ -466,7 +361,6 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::minb(V))
                 uint32_t *out_hi, int m, Gadget g, Tw tw) {
   constexpr int TPP = Cfg<N>::TPP, NT = Cfg<N>::THREADS;
   constexpr bool LEVEL = MODE == MODE_IVP_LEVEL || MODE == MODE_VP_LEVEL;
-  constexpr bool DEMUX = MODE == MODE_CDEMUX || MODE == MODE_IVP_LEVEL;
   constexpr bool MUX = MODE == MODE_CMUX || MODE == MODE_VP_LEVEL;
   extern __shared__ uint4 smem_raw[];
   Smem<N> &sm = *reinterpret_cast<Smem<N> *>(smem_raw);
@@ -480,9 +374,6 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::minb(V))
   const uint32_t *s1 = MODE == MODE_VP_LEVEL ? in + (item * 2 * m + m + sub) * 2 * N : (c1 ? c1 + b * 2 * N : nullptr);
   uint32_t *o_lo = out + (MODE == MODE_IVP_LEVEL ? (item * 2 * m + sub) : b) * 2 * N;
   uint32_t *o_hi = MODE == MODE_IVP_LEVEL ? out + (item * 2 * m + m + sub) * 2 * N : (out_hi ? out_hi + b * 2 * N : nullptr);
-#if HWB_T0
-  init_t0(sm.t0, g, NVar<N>::v, tid, NT);
-#endif
   if (MODE == MODE_EXT) {
     for (int k = tid; k < 2 * N; k += NT) sm.v[k] = decomp_prep(src[k], g);
   } else {
@@ -590,9 +481,6 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::minb(V))
   const Who<N> me;
   const int tid = me.tid, w = me.grp;
   const uint32_t *row = PBS ? lwe_in + b * (int64_t)(L + 1) : nullptr;
-#if HWB_T0
-  init_t0(sm.t0, g, NVar<N>::v, tid, NT);
-#endif
   if (PBS) {
     const int bt = mod_switch(row[L], LOG2M);
     const uint32_t *tp = tv + (tv_per_item ? b * 2 * N : 0);
@@ -666,9 +554,6 @@ struct SmemLat {
   uint32_t v[2 * N];
   uint32_t macc[2][2][N];          // [component][prime], NTT domain
   uint32_t scr[4 * LV][N];         // per-warp transpose scratch
-#if HWB_T0
-  uint32_t t0[2][kT0Max];
-#endif
 };
 
 // MINB = resident CTAs per SM the build targets: 1 (168 registers, lowest
@@ -703,9 +588,6 @@ __global__ void __launch_bounds__(128 * LV, MINB)
     for (int k = tid; k < 2 * N; k += NT) sm.acc[k] = acc_io[b * 2 * N + k];
   }
   for (int k = tid; k < 4 * N; k += NT) (&sm.macc[0][0][0])[k] = 0u;
-#if HWB_T0
-  init_t0(sm.t0, g, 0, tid, NT);
-#endif
   __syncthreads();
   uint32_t x[C];
 #pragma unroll 1
@@ -733,28 +615,9 @@ __global__ void __launch_bounds__(128 * LV, MINB)
       const uint32_t *vs = sm.v + comp * N + t;
 #pragma unroll
       for (int c = 0; c < 2; ++c) prefetch_l2(G + ((size_t)(r * 2 + c) * 2 + w) * N + t * 32);
-#if HWB_T0
-      if (g.mask < (uint32_t)kT0Max) {
-        const uint32_t *tab = sm.t0[w];
-#pragma unroll
-        for (int j = 0; j < C / 2; ++j)
-          digit_stage0(x[j], x[j + C / 2], (vs[TPP * j] >> sh) & g.mask, (vs[TPP * (j + C / 2)] >> sh) & g.mask,
-                       tab, off, 2 * p);
-      } else {
-        const uint2 w0 = c_tw[0][0][w][1];
-#pragma unroll
-        for (int j = 0; j < C / 2; ++j) {
-          x[j] = ((vs[TPP * j] >> sh) & g.mask) + off HWB_Z;
-          x[j + C / 2] = ((vs[TPP * (j + C / 2)] >> sh) & g.mask) + off HWB_Z;
-          ct_bfly_lazy<false>(x[j], x[j + C / 2], w0.x, w0.y, p, 2 * p);
-        }
-      }
-      fwd_ntt<N, TPP, -1, true>(x, sm.scr[wi], lay, t, w, w ? tw.fwd[1] : tw.fwd[0]);
-#else
 #pragma unroll
       for (int j = 0; j < C; ++j) x[j] = ((vs[TPP * j] >> sh) & g.mask) + off HWB_Z;
       fwd_ntt<N, TPP, -1>(x, sm.scr[wi], lay, t, w, w ? tw.fwd[1] : tw.fwd[0]);
-#endif
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const uint32_t *gs = G + ((size_t)(r * 2 + c) * 2 + w) * N;
