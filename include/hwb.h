@@ -215,6 +215,20 @@ int hwb_pbs_tc(const hwb_params *p, const uint32_t *bsk_ntt, const void *ksk_tc,
                const uint32_t *tv, int tv_per_item, const uint32_t *lwe_in, uint32_t *lwe_out,
                int64_t B, void *workspace, void *stream);
 
+/* ---- FP64 FFT ladder (N = 1024; same results as hwb_pbs) ----
+ * The key words are split into signed 16-bit halves whose double-precision FFT
+ * spectra form the key; the products are rounded to integers, which is exact
+ * (|sum| < 2^37.6, FFT error < 2^-13).  Requires l * 2^base_log < 2^19. */
+size_t hwb_bsk_fft_bytes(const hwb_params *p);
+/* bsk [n][2l][2][N] u32 (coefficient domain) -> bsk_fft (hwb_bsk_fft_bytes bytes). */
+int hwb_bsk_to_fft(const hwb_params *p, const uint32_t *bsk, void *bsk_fft, void *stream);
+/* hwb_pbs on the FFT ladder with the tensor-core key switch (ksk_tc from
+ * hwb_ksk_to_tc, workspace hwb_pbs_tc_workspace_bytes); ksk_tc == NULL skips the
+ * key switch (lwe_out [B][N+1]). */
+int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, const uint32_t *tv,
+                int tv_per_item, const uint32_t *lwe_in, uint32_t *lwe_out, int64_t B, void *workspace,
+                void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libhwb200.so")
 SOURCES = [os.path.join(HERE, "csrc", "hwb_kernels.cu")]
-DEPS = SOURCES + [os.path.join(HERE, "csrc", "hwb_device.cuh"), os.path.join(HERE, "csrc", "hwb_tc.cuh"), os.path.join(REPO, "include", "hwb.h")]
+DEPS = SOURCES + [os.path.join(HERE, "csrc", "hwb_device.cuh"), os.path.join(HERE, "csrc", "hwb_tc.cuh"), os.path.join(HERE, "csrc", "hwb_fft.cuh"), os.path.join(REPO, "include", "hwb.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

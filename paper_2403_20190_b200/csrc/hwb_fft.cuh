@@ -1,0 +1,132 @@
+// hwb_fft.cuh — FP64 negacyclic FFT for the CMUX ladder (N = 1024), exact by rounding.
+//
+// The limb-exact route of the reference's FFT engine (hw/fft.py:88-119): the key
+// words (signed 32-bit) are split into signed 16-bit halves G = lo + 2^16 hi, each
+// product sum_t d_t * G_t is computed separately for lo and hi in double-precision
+// complex arithmetic, rounded to the nearest integer and recombined mod 2^32.  The
+// true sums are integers below 2l * N * beta/2 * 2^15 <= 2^37.6 and the FFT error is
+// below 2^-13 (tests measure the margin), so rounding recovers them exactly: the
+// result is bit-identical to the NTT ladder and to the reference's schoolbook.
+//
+// Folding: a real negacyclic polynomial a (degree < N) becomes the complex vector
+// z_i = a_i + i a_{i+N/2} (i < H = N/2), i.e. a polynomial mod Y^H - i.  Its
+// transform is the merged-twist Cooley-Tukey recursion on the roots of Y^H - i
+// (root of block (level, m) = zeta^{E(level, m)/2}, zeta = e^{i pi / N}), the same
+// block/twiddle indexing as the NTT (hwb_device.cuh); the inverse is the
+// Gentleman-Sande recursion with conjugate twiddles, 1/H folded into the key.
+//
+// Thread mapping: one transform on 64 threads (2 warps), 8 complex values per thread,
+// the A/M/B layouts of Geo<512, 64> (2 shared-memory transposes per transform).
+#pragma once
+
+#include <cstdint>
+
+namespace hwb {
+
+constexpr int FH = 512;       // complex points per folded polynomial (N = 1024)
+constexpr int FT = 64;        // threads per transform
+constexpr int FC = FH / FT;   // complex values per thread
+using FGeo = Geo<FH, FT>;
+
+__constant__ double2 c_ftw[2][8];   // [forward / inverse (conjugate)][k], uniform A stages
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 w) {
+  return make_double2(fma(a.x, w.x, -a.y * w.y), fma(a.x, w.y, a.y * w.x));
+}
+// (X, Y) -> (X + w Y, X - w Y)
+__device__ __forceinline__ void fft_ct(double2 &X, double2 &Y, double2 w) {
+  const double2 t = cmul(Y, w);
+  Y = make_double2(X.x - t.x, X.y - t.y);
+  X = make_double2(X.x + t.x, X.y + t.y);
+}
+// (X, Y) -> (X + Y, (X - Y) conj(w_fwd)), the twiddle passed already conjugated
+__device__ __forceinline__ void fft_gs(double2 &X, double2 &Y, double2 w) {
+  const double2 d = make_double2(X.x - Y.x, X.y - Y.y);
+  X = make_double2(X.x + Y.x, X.y + Y.y);
+  Y = cmul(d, w);
+}
+
+template <bool FWD, int JB, bool UNIFORM, int MBASE, int SLOT>
+__device__ __forceinline__ void fft_stage(double2 (&x)[FC], int t, const double2 *__restrict__ tw) {
+  constexpr int NBT = FC >> (JB + 1);
+  constexpr int HALF = 1 << JB;
+#pragma unroll
+  for (int u = 0; u < NBT; ++u) {
+    const double2 w = UNIFORM ? c_ftw[FWD ? 0 : 1][MBASE + u] : __ldg(&tw[(SLOT + u) * FT + t]);
+#pragma unroll
+    for (int lo = 0; lo < HALF; ++lo) {
+      const int j = (u << (JB + 1)) | lo;
+      if (FWD)
+        fft_ct(x[j], x[j + HALF], w);
+      else
+        fft_gs(x[j], x[j + HALF], w);
+    }
+  }
+}
+
+// The CTA is exactly the 64 threads of the transform: CTA barriers.
+template <int FROM, int TO>
+__device__ __forceinline__ void frelayout(double2 (&x)[FC], double2 *scr, const LayBase &L) {
+  const uint32_t bf = lay_base<FH, FT, FROM>(L), bt = lay_base<FH, FT, TO>(L);
+#pragma unroll
+  for (int j = 0; j < FC; ++j) scr[bf ^ swz(joff<FH, FT, FROM>(j))] = x[j];
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < FC; ++j) x[j] = scr[bt ^ swz(joff<FH, FT, TO>(j))];
+  __syncthreads();
+}
+
+// natural (layout A) -> block order (layout B); per-thread twiddle slots as fwd_ntt
+__device__ __forceinline__ void fwd_fft(double2 (&x)[FC], double2 *scr, const LayBase &L, int t,
+                                        const double2 *__restrict__ tw) {
+  using G = FGeo;
+  static_for<0, G::LOGN - G::T>([&](auto K) {
+    constexpr int s = G::LOGN - 1 - decltype(K)::value;
+    fft_stage<true, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x, t, tw);
+  });
+  frelayout<LAY_A, LAY_M>(x, scr, L);
+  static_for<0, G::T - G::LOGC>([&](auto K) {
+    constexpr int s = G::T - 1 - decltype(K)::value;
+    constexpr int slot = (1 << decltype(K)::value) - 1;
+    fft_stage<true, s - G::LO, false, 0, slot>(x, t, tw);
+  });
+  frelayout<LAY_M, LAY_B>(x, scr, L);
+  static_for<0, G::B_TOP>([&](auto K) {
+    constexpr int s = G::B_TOP - 1 - decltype(K)::value;
+    constexpr int slot = G::M_SLOTS + (G::C >> G::B_TOP) * ((1 << decltype(K)::value) - 1);
+    fft_stage<true, s, false, 0, slot>(x, t, tw);
+  });
+}
+
+// block order (layout B) -> natural (layout A), unscaled (1/H is in the key)
+__device__ __forceinline__ void inv_fft(double2 (&x)[FC], double2 *scr, const LayBase &L, int t,
+                                        const double2 *__restrict__ tw) {
+  using G = FGeo;
+  static_for<0, G::B_TOP>([&](auto K) {
+    constexpr int s = decltype(K)::value;
+    constexpr int slot = G::C - 2 * (G::C >> (s + 1));
+    fft_stage<false, s, false, 0, slot>(x, t, tw);
+  });
+  frelayout<LAY_B, LAY_M>(x, scr, L);
+  static_for<0, G::T - G::LOGC>([&](auto K) {
+    constexpr int s = G::LOGC + decltype(K)::value;
+    constexpr int slot = G::B_SLOTS + (1 << (G::T - G::LOGC)) - (1 << (G::T - s));
+    fft_stage<false, s - G::LO, false, 0, slot>(x, t, tw);
+  });
+  frelayout<LAY_M, LAY_A>(x, scr, L);
+  static_for<0, G::LOGN - G::T>([&](auto K) {
+    constexpr int s = G::T + decltype(K)::value;
+    fft_stage<false, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x, t, tw);
+  });
+}
+
+// exact small integer -> double without a conversion instruction: 2^52 + u - (2^52 + off)
+__device__ __forceinline__ double u2d_minus(uint32_t u, double two52_plus_off) {
+  return __hiloint2double(0x43300000, (int)u) - two52_plus_off;
+}
+// round to nearest and reduce mod 2^32 (|y| < 2^51): low word of y + 1.5 * 2^52
+__device__ __forceinline__ uint32_t round_u32(double y) {
+  return (uint32_t)__double2loint(y + 6755399441055744.0);
+}
+
+}  // namespace hwb

@@ -25,6 +25,7 @@
 #include "../../include/hwb.h"
 #include "hwb_device.cuh"
 #include "hwb_tc.cuh"
+#include "hwb_fft.cuh"
 
 namespace hwb {
 
@@ -89,6 +90,7 @@ struct DevState {
   uint2 *lane_fwd[2][2] = {};   // [n_variant][prime] -> [slot][TPP]
   uint2 *lane_inv[2][2] = {};
   uint2 *lane_inv64[2] = {};    // N = 1024 inverse transform on 64 threads (latency ladder)
+  double2 *fft_fwd = nullptr, *fft_inv = nullptr;   // FP64 FFT per-thread twiddles
 };
 
 static std::mutex g_mu;
@@ -96,23 +98,25 @@ static DevState g_state[64];
 
 // Per-thread twiddle table in the slot order fwd_ntt/inv_ntt consume
 // (hwb_device.cuh): twiddle index of stage s, block b is m + b, m = N/2^(s+1).
-template <int N, int TPP = Cfg<N>::TPP>
-static std::vector<uint2> thread_table(const std::vector<uint32_t> &w, uint32_t p, bool fwd) {
+// Per-thread twiddle table in the slot order the transforms consume: entry
+// (slot, t) holds val(k) for the twiddle index k of that slot and thread.
+template <int N, int TPP, typename V, typename F>
+static std::vector<V> thread_table_of(F val, bool fwd) {
   using G = Geo<N, TPP>;
-  std::vector<uint2> tab((size_t)G::SLOTS * TPP);
+  std::vector<V> tab((size_t)G::SLOTS * TPP);
   int slot = 0;
   auto m_stage = [&](int s) {   // middle layout: block = t_hi 2^(T-s-1) + u
     const int nb = 1 << (G::T - s - 1);
     for (int u = 0; u < nb; ++u)
       for (int t = 0; t < TPP; ++t)
-        tab[(size_t)(slot + u) * TPP + t] = shoup_pair(w[(N >> (s + 1)) + (t >> G::LO) * nb + u], p);
+        tab[(size_t)(slot + u) * TPP + t] = val((N >> (s + 1)) + (t >> G::LO) * nb + u);
     slot += nb;
   };
   auto b_stage = [&](int s) {   // bit-reversed layout: block = t C/2^(s+1) + u
     const int nb = G::C >> (s + 1);
     for (int u = 0; u < nb; ++u)
       for (int t = 0; t < TPP; ++t)
-        tab[(size_t)(slot + u) * TPP + t] = shoup_pair(w[(N >> (s + 1)) + t * nb + u], p);
+        tab[(size_t)(slot + u) * TPP + t] = val((N >> (s + 1)) + t * nb + u);
     slot += nb;
   };
   if (fwd) {
@@ -125,6 +129,31 @@ static std::vector<uint2> thread_table(const std::vector<uint32_t> &w, uint32_t 
       for (int s = G::LOGC; s < G::T; ++s) m_stage(s);
   }
   return tab;
+}
+
+template <int N, int TPP = Cfg<N>::TPP>
+static std::vector<uint2> thread_table(const std::vector<uint32_t> &w, uint32_t p, bool fwd) {
+  return thread_table_of<N, TPP, uint2>([&](int k) { return shoup_pair(w[k], p); }, fwd);
+}
+
+// FFT twiddles (hwb_fft.cuh): k = 2^level + m -> zeta^{E(level, m)/2}, zeta = e^{i pi/(2H)},
+// E(0, 0) = H and E(level+1, {2m, 2m+1}) = {E/2, E/2 + 2H} (mod 4H): the roots of the
+// factors of Y^H - i.  Computed in long double, rounded once to double.
+static std::vector<double2> fft_twiddles(bool conj) {
+  const int H = FH;
+  std::vector<long> E(2 * H, 0);
+  E[1] = H;
+  for (int k = 1; k < H; ++k) {
+    E[2 * k] = (E[k] / 2) % (4 * H);
+    E[2 * k + 1] = (E[k] / 2 + 2 * H) % (4 * H);
+  }
+  std::vector<double2> w(H);
+  for (int k = 1; k < H; ++k) {
+    const long double ang = acosl(-1.0L) * (long double)(E[k] / 2) / (long double)(2 * H);
+    w[k] = make_double2((double)cosl(ang), (double)(conj ? -sinl(ang) : sinl(ang)));
+  }
+  w[0] = make_double2(1.0, 0.0);
+  return w;
 }
 
 static int init_device(DevState **out) {
@@ -199,6 +228,22 @@ static int init_device(DevState **out) {
   const uint32_t crt_inv = powmod(kP0, kP1 - 2, kP1);
   const uint2 crt_pair = shoup_pair(crt_inv, kP1);
   uint32_t h_crt[4] = {crt_pair.x, crt_pair.y, (uint32_t)((uint64_t)kP0 * kP1), kP1 / 2};
+  {
+    const std::vector<double2> wf = fft_twiddles(false), wi = fft_twiddles(true);
+    const std::vector<double2> lf = thread_table_of<FH, FT, double2>([&](int k) { return wf[k]; }, true);
+    const std::vector<double2> li = thread_table_of<FH, FT, double2>([&](int k) { return wi[k]; }, false);
+    const size_t fb = sizeof(double2) * lf.size();
+    cudaError_t e1 = cudaMalloc(&st.fft_fwd, fb), e2 = cudaMalloc(&st.fft_inv, fb);
+    if (e1 == cudaSuccess) e1 = cudaMemcpy(st.fft_fwd, lf.data(), fb, cudaMemcpyHostToDevice);
+    if (e2 == cudaSuccess) e2 = cudaMemcpy(st.fft_inv, li.data(), fb, cudaMemcpyHostToDevice);
+    double2 h_ftw[2][8];
+    for (int k = 0; k < 8; ++k) {
+      h_ftw[0][k] = wf[k];
+      h_ftw[1][k] = wi[k];
+    }
+    if (e1 == cudaSuccess && e2 == cudaSuccess) e1 = cudaMemcpyToSymbol(c_ftw, h_ftw, sizeof(h_ftw));
+    if (e1 != cudaSuccess || e2 != cudaSuccess) return fail(HWB_ECUDA, "FFT twiddle upload failed");
+  }
   const uint32_t zero = 0;
   cudaError_t ec = cudaMemcpyToSymbol(c_tw, h_tw, sizeof(h_tw));
   if (ec == cudaSuccess) ec = cudaMemcpyToSymbol(c_zero, &zero, sizeof(zero));
@@ -697,6 +742,143 @@ __global__ void __launch_bounds__(128 * LV, MINB)
   } else {
     for (int k = tid; k < 2 * N; k += NT) acc_io[b * 2 * N + k] = sm.acc[k];
   }
+}
+
+// ---------------------------------------------------------------------------
+// FP64 FFT ladder (hwb_fft.cuh), N = 1024: one ciphertext per CTA of 64 threads.
+// Thread t owns the spectrum positions (t, j) of layout B for every transform, so
+// the 2l digit spectra are multiplied into the four accumulators Y[c][h] (component
+// c, key half h) in registers, and after the inverse transforms each thread owns the
+// coefficients i = t + 64 j and i + 512 of both halves: no exchange between threads.
+
+// BSK [n][2l][2][N] u32 -> FFT domain [n][2l][2][2 halves][FC][FT] double2 (scaled 1/H).
+__global__ void __launch_bounds__(FT) bsk_to_fft_kernel(const uint32_t *__restrict__ in, double2 *out,
+                                                         const double2 *__restrict__ twf) {
+  __shared__ double2 scr[FH];
+  const int t = threadIdx.x;
+  const int64_t poly = blockIdx.x;
+  const uint32_t *a = in + poly * (2 * FH);
+  const LayBase lay = make_lay<FH, FT>(t);
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    double2 x[FC];
+#pragma unroll
+    for (int j = 0; j < FC; ++j) {
+      const int i = t + FT * j;
+      double v[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int64_t gword = (int32_t)a[i + q * FH];               // signed 32-bit key word
+        const int64_t lo = ((gword + 32768) & 0xFFFF) - 32768;       // [-2^15, 2^15)
+        v[q] = (double)(h ? (gword - lo) >> 16 : lo);
+      }
+      x[j] = make_double2(v[0], v[1]);
+    }
+    fwd_fft(x, scr, lay, t, twf);
+    double2 *o = out + (poly * 2 + h) * (FC * FT);
+#pragma unroll
+    for (int j = 0; j < FC; ++j) o[j * FT + t] = make_double2(x[j].x * (1.0 / FH), x[j].y * (1.0 / FH));
+  }
+}
+
+struct FSmem {
+  uint32_t acc[2 * 2 * FH];
+  uint32_t v[2 * 2 * FH];
+  double2 scr[FH];
+};
+
+template <bool PBS>
+__global__ void __launch_bounds__(FT, 1)
+    blind_rotate_fft_kernel(const double2 *__restrict__ bskf, const uint32_t *__restrict__ lwe_in,
+                            const uint32_t *__restrict__ tv, int tv_per_item, uint32_t *lwe_out, int L, Gadget g,
+                            const double2 *__restrict__ twf, const double2 *__restrict__ twi) {
+  constexpr int N = 2 * FH;
+  constexpr int LOG2M = 11;
+  extern __shared__ uint4 smem_raw[];
+  FSmem &sm = *reinterpret_cast<FSmem *>(smem_raw);
+  const int64_t b = blockIdx.x;
+  const int t = threadIdx.x;
+  const LayBase lay = make_lay<FH, FT>(t);
+  const uint32_t *row = lwe_in + b * (int64_t)(L + 1);
+  {
+    const int bt = mod_switch(row[L], LOG2M);
+    const uint32_t *tp = tv + (tv_per_item ? b * 2 * N : 0);
+    const int e = (2 * N - bt) & (2 * N - 1);   // X^-b~
+    for (int k = t; k < 2 * N; k += FT) {
+      const int c = k >= N, i = k & (N - 1);
+      sm.acc[k] = rot_read<N>(tp + c * N, i, e);
+    }
+  }
+  __syncthreads();
+  const int lv = (int)g.levels;
+  const double dig_off = 4503599627370496.0 + (double)g.half;   // 2^52 + beta/2
+  const size_t ggsw_f = (size_t)2 * lv * 2 * 2 * FC * FT;         // double2 per GGSW
+#pragma unroll 1
+  for (int s = 0; s < L; ++s) {
+    const int e = mod_switch(row[s], LOG2M);   // X^{a~_s}
+    if (e == 0) continue;
+    for (int k = t; k < 2 * N; k += FT) {
+      const int c = k >= N, i = k & (N - 1);
+      sm.v[k] = decomp_prep(rot_read<N>(sm.acc + c * N, i, e) - sm.acc[k], g);
+    }
+    __syncthreads();
+    double2 Y[2][2][FC];
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int j = 0; j < FC; ++j) Y[c][h][j] = make_double2(0.0, 0.0);
+    const double2 *G = bskf + (size_t)s * ggsw_f;
+#pragma unroll 1
+    for (int r = 0; r < 2 * lv; ++r) {
+      // digit order (hw/tfhe.py:290-298): rows 0..l-1 = digits of b, l..2l-1 of a
+      const int comp = r < lv ? 1 : 0;
+      const int tt = r < lv ? r : r - lv;
+      const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
+      const uint32_t *vs = sm.v + comp * N + t;
+      double2 x[FC];
+#pragma unroll
+      for (int j = 0; j < FC; ++j)
+        x[j] = make_double2(u2d_minus((vs[FT * j] >> sh) & g.mask, dig_off),
+                            u2d_minus((vs[FT * j + FH] >> sh) & g.mask, dig_off));
+      fwd_fft(x, sm.scr, lay, t, twf);
+      const double2 *gr = G + (size_t)r * (2 * 2 * FC * FT);
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int j = 0; j < FC; ++j) {
+            const double2 k = __ldg(&gr[((c * 2 + h) * FC + j) * FT + t]);
+            double2 &y = Y[c][h][j];
+            y.x = fma(x[j].x, k.x, fma(-x[j].y, k.y, y.x));
+            y.y = fma(x[j].x, k.y, fma(x[j].y, k.x, y.y));
+          }
+    }
+    // inverse transforms, rounding, recombination of the halves, accumulation
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      uint32_t lo_re[FC], lo_im[FC];
+      inv_fft(Y[c][0], sm.scr, lay, t, twi);
+#pragma unroll
+      for (int j = 0; j < FC; ++j) {
+        lo_re[j] = round_u32(Y[c][0][j].x);
+        lo_im[j] = round_u32(Y[c][0][j].y);
+      }
+      inv_fft(Y[c][1], sm.scr, lay, t, twi);
+#pragma unroll
+      for (int j = 0; j < FC; ++j) {
+        const int i = t + FT * j;
+        sm.acc[c * N + i] += lo_re[j] + (round_u32(Y[c][1][j].x) << 16);
+        sm.acc[c * N + i + FH] += lo_im[j] + (round_u32(Y[c][1][j].y) << 16);
+      }
+    }
+    __syncthreads();
+  }
+  uint32_t *o = lwe_out + b * (int64_t)(N + 1);
+  for (int k = t; k < N; k += FT) o[k] = k == 0 ? sm.acc[0] : 0u - sm.acc[N - k];
+  if (t == 0) o[N] = sm.acc[N];
 }
 
 template <int N>
@@ -1476,6 +1658,65 @@ int hwb_pbs(const hwb_params *p, const uint32_t *bsk_ntt, const uint32_t *ksk, c
   return keyswitch_launch(p, ksk, ext, lwe_out, B, s);
 }
 
+static size_t pbs_ext_bytes(const hwb_params *p, int64_t B) {
+  return ((sizeof(uint32_t) * (size_t)B * (p->N + 1)) + 255) & ~(size_t)255;
+}
+
+static int check_fft(const hwb_params *p) {
+  int rc = check_glwe(p);
+  if (rc) return rc;
+  if (p->N != 2 * FH) return fail(HWB_EINVAL, "the FFT ladder supports N = 1024 only");
+  // rounding exactness: |sum| < 2l N beta/2 2^15 and FFT error << 1/2
+  if (p->l * (1u << p->base_log) >= (1u << 19)) return fail(HWB_EINVAL, "gadget too wide for the FFT ladder");
+  return HWB_OK;
+}
+
+size_t hwb_bsk_fft_bytes(const hwb_params *p) {
+  if (!p || check_fft(p)) return 0;
+  return (size_t)p->n * 2 * p->l * 2 * 2 * FH * sizeof(double2);
+}
+
+int hwb_bsk_to_fft(const hwb_params *p, const uint32_t *bsk, void *bsk_fft, void *stream) {
+  int rc = check_fft(p);
+  if (rc) return rc;
+  if (p->n < 1) return fail(HWB_EINVAL, "LWE dimension n must be positive");
+  if (!bsk || !bsk_fft) return fail(HWB_EINVAL, "null key pointer");
+  if ((uintptr_t)bsk_fft & 15) return fail(HWB_EINVAL, "bsk_fft must be 16-byte aligned");
+  DevState *st;
+  if ((rc = init_device(&st))) return rc;
+  const int64_t polys = (int64_t)p->n * 2 * p->l * 2;
+  bsk_to_fft_kernel<<<(unsigned)polys, FT, 0, (cudaStream_t)stream>>>(bsk, (double2 *)bsk_fft, st->fft_fwd);
+  return post_launch("bsk_to_fft_kernel");
+}
+
+int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, const uint32_t *tv,
+                int tv_per_item, const uint32_t *lwe_in, uint32_t *lwe_out, int64_t B, void *workspace,
+                void *stream) {
+  int rc = check_fft(p);
+  if (rc) return rc;
+  if (ksk_tc && (rc = check_ks_tc(p))) return rc;
+  if (p->n < 1) return fail(HWB_EINVAL, "LWE dimension n must be positive");
+  if (B < 0) return fail(HWB_EINVAL, "negative batch");
+  if (B == 0) return HWB_OK;
+  if (B > 0x7FFFFFFF) return fail(HWB_EINVAL, "batch too large");
+  if (!bsk_fft) return fail(HWB_EINVAL, "null key pointer");
+  if (ksk_tc && !workspace) return fail(HWB_EINVAL, "hwb_pbs_fft with key switch needs a workspace");
+  if (ksk_tc && (((uintptr_t)ksk_tc | (uintptr_t)workspace) & 15))
+    return fail(HWB_EINVAL, "ksk_tc/workspace must be 16-byte aligned");
+  DevState *st;
+  if ((rc = init_device(&st))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  uint32_t *ext = ksk_tc ? (uint32_t *)workspace : lwe_out;
+  const size_t smem = sizeof(FSmem);
+  if ((rc = set_smem(blind_rotate_fft_kernel<true>, smem))) return rc;
+  blind_rotate_fft_kernel<true><<<(unsigned)B, FT, smem, s>>>((const double2 *)bsk_fft, lwe_in, tv, tv_per_item,
+                                                              ext, (int)p->n, make_gadget(p->l, p->base_log),
+                                                              st->fft_fwd, st->fft_inv);
+  if ((rc = post_launch("blind_rotate_fft_kernel"))) return rc;
+  if (!ksk_tc) return HWB_OK;
+  return keyswitch_tc_launch(p, ksk_tc, ext, lwe_out, B, (uint8_t *)workspace + pbs_ext_bytes(p, B), s);
+}
+
 size_t hwb_ksk_tc_bytes(const hwb_params *p) {
   if (!p || check_ks_tc(p)) return 0;
   const size_t nct = (p->n + 1 + TC_COLS - 1) / TC_COLS;
@@ -1514,9 +1755,6 @@ int hwb_keyswitch_tc(const hwb_params *p, const void *ksk_tc, const uint32_t *in
   return keyswitch_tc_launch(p, ksk_tc, in, out, B, workspace, (cudaStream_t)stream);
 }
 
-static size_t pbs_ext_bytes(const hwb_params *p, int64_t B) {
-  return ((sizeof(uint32_t) * (size_t)B * (p->N + 1)) + 255) & ~(size_t)255;
-}
 
 size_t hwb_pbs_tc_workspace_bytes(const hwb_params *p, int64_t B) {
   if (!p || B <= 0 || check_ks_tc(p)) return 0;
