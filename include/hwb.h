@@ -222,9 +222,13 @@ int hwb_pbs_tc(const hwb_params *p, const uint32_t *bsk_ntt, const void *ksk_tc,
 size_t hwb_bsk_fft_bytes(const hwb_params *p);
 /* bsk [n][2l][2][N] u32 (coefficient domain) -> bsk_fft (hwb_bsk_fft_bytes bytes). */
 int hwb_bsk_to_fft(const hwb_params *p, const uint32_t *bsk, void *bsk_fft, void *stream);
+/* Workspace of hwb_pbs_fft: the accumulators between ladder segments, plus the
+ * key switch's buffers when with_keyswitch. */
+size_t hwb_pbs_fft_workspace_bytes(const hwb_params *p, int64_t B, int with_keyswitch);
+/* Ladder steps per launch (default 64): each launch's key slice stays L2-resident. */
+int hwb_set_fft_segment(int steps);
 /* hwb_pbs on the FFT ladder with the tensor-core key switch (ksk_tc from
- * hwb_ksk_to_tc, workspace hwb_pbs_tc_workspace_bytes); ksk_tc == NULL skips the
- * key switch (lwe_out [B][N+1]). */
+ * hwb_ksk_to_tc); ksk_tc == NULL skips the key switch (lwe_out [B][N+1]). */
 int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, const uint32_t *tv,
                 int tv_per_item, const uint32_t *lwe_in, uint32_t *lwe_out, int64_t B, void *workspace,
                 void *stream);

@@ -64,33 +64,57 @@ __device__ __forceinline__ void fft_stage(double2 (&x)[FC], int t, const double2
   }
 }
 
-// The CTA is exactly the 64 threads of the transform: CTA barriers.
-template <int FROM, int TO>
-__device__ __forceinline__ void frelayout(double2 (&x)[FC], double2 *scr, const LayBase &L) {
-  const uint32_t bf = lay_base<FH, FT, FROM>(L), bt = lay_base<FH, FT, TO>(L);
-#pragma unroll
-  for (int j = 0; j < FC; ++j) scr[bf ^ swz(joff<FH, FT, FROM>(j))] = x[j];
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < FC; ++j) x[j] = scr[bt ^ swz(joff<FH, FT, TO>(j))];
-  __syncthreads();
+// Bank swizzle for 16-byte elements: a quarter-warp's 8 accesses must hit distinct
+// element slots mod 8.  e ^ ((e >> 3) & 7) achieves it in all three layouts (A and M
+// already differ in e & 7 across a quarter-warp; B = 8t + j needs the row bits t
+// folded in), and being GF(2)-linear it splits into thread and register parts.
+__host__ __device__ constexpr uint32_t fswz(uint32_t e) { return e ^ ((e >> 3) & 7u); }
+
+struct FLay {
+  uint32_t a, m, b;
+};
+__device__ __forceinline__ FLay make_flay(int t) {
+  return FLay{fswz(toff<FH, FT, LAY_A>(t)), fswz(toff<FH, FT, LAY_M>(t)), fswz(toff<FH, FT, LAY_B>(t))};
+}
+template <int LAY>
+__device__ __forceinline__ uint32_t flay_base(const FLay &L) {
+  return LAY == LAY_A ? L.a : (LAY == LAY_M ? L.m : L.b);
 }
 
+// The CTA is exactly the 64 threads of the transform: CTA barriers.  `after_first`
+// runs once all threads have passed the first barrier (everyone finished the
+// previous consumer of any shared buffer -- the key-slice prefetch hook).
+template <int FROM, int TO, typename F>
+__device__ __forceinline__ void frelayout(double2 (&x)[FC], double2 *scr, const FLay &L, F &&after_first) {
+  const uint32_t bf = flay_base<FROM>(L), bt = flay_base<TO>(L);
+#pragma unroll
+  for (int j = 0; j < FC; ++j) scr[bf ^ fswz(joff<FH, FT, FROM>(j))] = x[j];
+  __syncthreads();
+  after_first();
+#pragma unroll
+  for (int j = 0; j < FC; ++j) x[j] = scr[bt ^ fswz(joff<FH, FT, TO>(j))];
+  __syncthreads();
+}
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
 // natural (layout A) -> block order (layout B); per-thread twiddle slots as fwd_ntt
-__device__ __forceinline__ void fwd_fft(double2 (&x)[FC], double2 *scr, const LayBase &L, int t,
-                                        const double2 *__restrict__ tw) {
+template <typename F = NoHook>
+__device__ __forceinline__ void fwd_fft(double2 (&x)[FC], double2 *scr, const FLay &L, int t,
+                                        const double2 *__restrict__ tw, F &&hook = F()) {
   using G = FGeo;
   static_for<0, G::LOGN - G::T>([&](auto K) {
     constexpr int s = G::LOGN - 1 - decltype(K)::value;
     fft_stage<true, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x, t, tw);
   });
-  frelayout<LAY_A, LAY_M>(x, scr, L);
+  frelayout<LAY_A, LAY_M>(x, scr, L, hook);
   static_for<0, G::T - G::LOGC>([&](auto K) {
     constexpr int s = G::T - 1 - decltype(K)::value;
     constexpr int slot = (1 << decltype(K)::value) - 1;
     fft_stage<true, s - G::LO, false, 0, slot>(x, t, tw);
   });
-  frelayout<LAY_M, LAY_B>(x, scr, L);
+  frelayout<LAY_M, LAY_B>(x, scr, L, NoHook());
   static_for<0, G::B_TOP>([&](auto K) {
     constexpr int s = G::B_TOP - 1 - decltype(K)::value;
     constexpr int slot = G::M_SLOTS + (G::C >> G::B_TOP) * ((1 << decltype(K)::value) - 1);
@@ -99,7 +123,7 @@ __device__ __forceinline__ void fwd_fft(double2 (&x)[FC], double2 *scr, const La
 }
 
 // block order (layout B) -> natural (layout A), unscaled (1/H is in the key)
-__device__ __forceinline__ void inv_fft(double2 (&x)[FC], double2 *scr, const LayBase &L, int t,
+__device__ __forceinline__ void inv_fft(double2 (&x)[FC], double2 *scr, const FLay &L, int t,
                                         const double2 *__restrict__ tw) {
   using G = FGeo;
   static_for<0, G::B_TOP>([&](auto K) {
@@ -107,13 +131,13 @@ __device__ __forceinline__ void inv_fft(double2 (&x)[FC], double2 *scr, const La
     constexpr int slot = G::C - 2 * (G::C >> (s + 1));
     fft_stage<false, s, false, 0, slot>(x, t, tw);
   });
-  frelayout<LAY_B, LAY_M>(x, scr, L);
+  frelayout<LAY_B, LAY_M>(x, scr, L, NoHook());
   static_for<0, G::T - G::LOGC>([&](auto K) {
     constexpr int s = G::LOGC + decltype(K)::value;
     constexpr int slot = G::B_SLOTS + (1 << (G::T - G::LOGC)) - (1 << (G::T - s));
     fft_stage<false, s - G::LO, false, 0, slot>(x, t, tw);
   });
-  frelayout<LAY_M, LAY_A>(x, scr, L);
+  frelayout<LAY_M, LAY_A>(x, scr, L, NoHook());
   static_for<0, G::LOGN - G::T>([&](auto K) {
     constexpr int s = G::T + decltype(K)::value;
     fft_stage<false, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x, t, tw);

@@ -758,7 +758,7 @@ __global__ void __launch_bounds__(FT) bsk_to_fft_kernel(const uint32_t *__restri
   const int t = threadIdx.x;
   const int64_t poly = blockIdx.x;
   const uint32_t *a = in + poly * (2 * FH);
-  const LayBase lay = make_lay<FH, FT>(t);
+  const FLay lay = make_flay(t);
 #pragma unroll 1
   for (int h = 0; h < 2; ++h) {
     double2 x[FC];
@@ -781,26 +781,35 @@ __global__ void __launch_bounds__(FT) bsk_to_fft_kernel(const uint32_t *__restri
   }
 }
 
+#ifndef HWB_FFT_PF
+#define HWB_FFT_PF 1
+#endif
 struct FSmem {
   uint32_t acc[2 * 2 * FH];
   uint32_t v[2 * 2 * FH];
   double2 scr[FH];
 };
 
+// Steps [s0, s1) of the ladder.  first: the accumulator starts as TV * X^-b~,
+// else it is read from acc_io; last: coefficient-0 extraction to lwe_out, else the
+// accumulator is written to acc_io.  Running the ladder in segments keeps the
+// segment's slice of the FFT key (192 KB per step) L2-resident for the whole batch:
+// the full key (n x 192 KB = 121 MB at cfg2) does not fit next to everything else.
 template <bool PBS>
 __global__ void __launch_bounds__(FT, 1)
     blind_rotate_fft_kernel(const double2 *__restrict__ bskf, const uint32_t *__restrict__ lwe_in,
                             const uint32_t *__restrict__ tv, int tv_per_item, uint32_t *lwe_out, int L, Gadget g,
-                            const double2 *__restrict__ twf, const double2 *__restrict__ twi) {
+                            const double2 *__restrict__ twf, const double2 *__restrict__ twi, uint32_t *acc_io,
+                            int s0, int s1) {
   constexpr int N = 2 * FH;
   constexpr int LOG2M = 11;
   extern __shared__ uint4 smem_raw[];
   FSmem &sm = *reinterpret_cast<FSmem *>(smem_raw);
   const int64_t b = blockIdx.x;
   const int t = threadIdx.x;
-  const LayBase lay = make_lay<FH, FT>(t);
+  const FLay lay = make_flay(t);
   const uint32_t *row = lwe_in + b * (int64_t)(L + 1);
-  {
+  if (s0 == 0) {
     const int bt = mod_switch(row[L], LOG2M);
     const uint32_t *tp = tv + (tv_per_item ? b * 2 * N : 0);
     const int e = (2 * N - bt) & (2 * N - 1);   // X^-b~
@@ -808,13 +817,15 @@ __global__ void __launch_bounds__(FT, 1)
       const int c = k >= N, i = k & (N - 1);
       sm.acc[k] = rot_read<N>(tp + c * N, i, e);
     }
+  } else {
+    for (int k = t; k < 2 * N; k += FT) sm.acc[k] = acc_io[b * 2 * N + k];
   }
   __syncthreads();
   const int lv = (int)g.levels;
   const double dig_off = 4503599627370496.0 + (double)g.half;   // 2^52 + beta/2
   const size_t ggsw_f = (size_t)2 * lv * 2 * 2 * FC * FT;         // double2 per GGSW
 #pragma unroll 1
-  for (int s = 0; s < L; ++s) {
+  for (int s = s0; s < s1; ++s) {
     const int e = mod_switch(row[s], LOG2M);   // X^{a~_s}
     if (e == 0) continue;
     for (int k = t; k < 2 * N; k += FT) {
@@ -837,13 +848,18 @@ __global__ void __launch_bounds__(FT, 1)
       const int tt = r < lv ? r : r - lv;
       const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
       const uint32_t *vs = sm.v + comp * N + t;
+      const double2 *gr = G + (size_t)r * (2 * 2 * FC * FT);
+#if HWB_FFT_PF
+      // bring this digit's key slice (32 KB per CTA) towards L1 while the transform runs
+#pragma unroll
+      for (int q = 0; q < 2 * 2 * FC; ++q) prefetch_l1(&gr[q * FT + t]);
+#endif
       double2 x[FC];
 #pragma unroll
       for (int j = 0; j < FC; ++j)
         x[j] = make_double2(u2d_minus((vs[FT * j] >> sh) & g.mask, dig_off),
                             u2d_minus((vs[FT * j + FH] >> sh) & g.mask, dig_off));
       fwd_fft(x, sm.scr, lay, t, twf);
-      const double2 *gr = G + (size_t)r * (2 * 2 * FC * FT);
 #pragma unroll
       for (int c = 0; c < 2; ++c)
 #pragma unroll
@@ -875,6 +891,10 @@ __global__ void __launch_bounds__(FT, 1)
       }
     }
     __syncthreads();
+  }
+  if (s1 < L) {
+    for (int k = t; k < 2 * N; k += FT) acc_io[b * 2 * N + k] = sm.acc[k];
+    return;
   }
   uint32_t *o = lwe_out + b * (int64_t)(N + 1);
   for (int k = t; k < N; k += FT) o[k] = k == 0 ? sm.acc[0] : 0u - sm.acc[N - k];
@@ -1662,6 +1682,10 @@ static size_t pbs_ext_bytes(const hwb_params *p, int64_t B) {
   return ((sizeof(uint32_t) * (size_t)B * (p->N + 1)) + 255) & ~(size_t)255;
 }
 
+static size_t fft_acc_bytes(int64_t B) { return ((size_t)B * 2 * 2 * FH * 4 + 255) & ~(size_t)255; }
+// ladder steps per launch of the FFT ladder (L2 residency of the key slice)
+static int g_fft_segment = 64;
+
 static int check_fft(const hwb_params *p) {
   int rc = check_glwe(p);
   if (rc) return rc;
@@ -1700,21 +1724,44 @@ int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, co
   if (B == 0) return HWB_OK;
   if (B > 0x7FFFFFFF) return fail(HWB_EINVAL, "batch too large");
   if (!bsk_fft) return fail(HWB_EINVAL, "null key pointer");
-  if (ksk_tc && !workspace) return fail(HWB_EINVAL, "hwb_pbs_fft with key switch needs a workspace");
   if (ksk_tc && (((uintptr_t)ksk_tc | (uintptr_t)workspace) & 15))
     return fail(HWB_EINVAL, "ksk_tc/workspace must be 16-byte aligned");
+  if (!workspace) return fail(HWB_EINVAL, "hwb_pbs_fft needs a workspace (hwb_pbs_fft_workspace_bytes)");
   DevState *st;
   if ((rc = init_device(&st))) return rc;
   cudaStream_t s = (cudaStream_t)stream;
-  uint32_t *ext = ksk_tc ? (uint32_t *)workspace : lwe_out;
+  uint8_t *ws = (uint8_t *)workspace;
+  uint32_t *acc = (uint32_t *)ws;                               // [B][2][N] between segments
+  uint32_t *ext = ksk_tc ? (uint32_t *)(ws + fft_acc_bytes(B)) : lwe_out;
   const size_t smem = sizeof(FSmem);
   if ((rc = set_smem(blind_rotate_fft_kernel<true>, smem))) return rc;
-  blind_rotate_fft_kernel<true><<<(unsigned)B, FT, smem, s>>>((const double2 *)bsk_fft, lwe_in, tv, tv_per_item,
-                                                              ext, (int)p->n, make_gadget(p->l, p->base_log),
-                                                              st->fft_fwd, st->fft_inv);
-  if ((rc = post_launch("blind_rotate_fft_kernel"))) return rc;
+  const Gadget g = make_gadget(p->l, p->base_log);
+  const int L = (int)p->n;
+  for (int s0 = 0; s0 < L; s0 += g_fft_segment) {
+    const int s1 = s0 + g_fft_segment < L ? s0 + g_fft_segment : L;
+    blind_rotate_fft_kernel<true><<<(unsigned)B, FT, smem, s>>>((const double2 *)bsk_fft, lwe_in, tv, tv_per_item,
+                                                                ext, L, g, st->fft_fwd, st->fft_inv, acc, s0, s1);
+    if ((rc = post_launch("blind_rotate_fft_kernel"))) return rc;
+  }
   if (!ksk_tc) return HWB_OK;
-  return keyswitch_tc_launch(p, ksk_tc, ext, lwe_out, B, (uint8_t *)workspace + pbs_ext_bytes(p, B), s);
+  return keyswitch_tc_launch(p, ksk_tc, ext, lwe_out, B,
+                             ws + fft_acc_bytes(B) + pbs_ext_bytes(p, B), s);
+}
+
+size_t hwb_pbs_fft_workspace_bytes(const hwb_params *p, int64_t B, int with_keyswitch) {
+  if (!p || B <= 0 || check_fft(p)) return 0;
+  size_t bytes = fft_acc_bytes(B);
+  if (with_keyswitch) {
+    if (check_ks_tc(p)) return 0;
+    bytes += pbs_ext_bytes(p, B) + ks_tc_digit_bytes(p, B);
+  }
+  return bytes;
+}
+
+int hwb_set_fft_segment(int steps) {
+  if (steps < 1) return fail(HWB_EINVAL, "segment must be >= 1 step");
+  g_fft_segment = steps;
+  return HWB_OK;
 }
 
 size_t hwb_ksk_tc_bytes(const hwb_params *p) {

@@ -28,10 +28,13 @@ def main(B=4096):
         tv = tfhe.to_device(tfhe.test_polynomial(np.arange(P.p // 2), P))
         ref = tfhe.pbs_batch(P, lwe, tv, bsk, None)
         out = torch.empty_like(ref)
+        ws = torch.empty(L.hwb_pbs_fft_workspace_bytes(ctypes.byref(cp), B, 0), dtype=torch.uint8, device="cuda")
+        seg = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+        _lib.check(L.hwb_set_fft_segment(seg))
 
         def fft():
             _lib.check(L.hwb_pbs_fft(ctypes.byref(cp), tfhe._ptr(fk), None, tfhe._ptr(tv), 0, tfhe._ptr(lwe),
-                                     tfhe._ptr(out), B, None, tfhe._stream()))
+                                     tfhe._ptr(out), B, tfhe._ptr(ws), tfhe._stream()))
         fft()
         torch.cuda.synchronize()
         same = torch.equal(out, ref)
@@ -51,4 +54,4 @@ def main(B=4096):
 
 
 if __name__ == "__main__":
-    main(*[int(x) for x in sys.argv[1:]])
+    main(*[int(x) for x in sys.argv[1:2]])
