@@ -781,13 +781,11 @@ __global__ void __launch_bounds__(FT) bsk_to_fft_kernel(const uint32_t *__restri
   }
 }
 
-#ifndef HWB_FFT_PF
-#define HWB_FFT_PF 1
-#endif
 struct FSmem {
   uint32_t acc[2 * 2 * FH];
-  uint32_t v[2 * 2 * FH];
   double2 scr[FH];
+  double2 key[2 * 2 * FC * FT];   // the current digit's key slice [c][h][j][t] (32 KB, TMA)
+  uint64_t key_full;              // mbarrier: slice landed
 };
 
 // Steps [s0, s1) of the ladder.  first: the accumulator starts as TV * X^-b~,
@@ -820,19 +818,20 @@ __global__ void __launch_bounds__(FT, 1)
   } else {
     for (int k = t; k < 2 * N; k += FT) sm.acc[k] = acc_io[b * 2 * N + k];
   }
+  if (t == 0) {
+    mbar_init(&sm.key_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
+  uint32_t key_phase = 0;
   const int lv = (int)g.levels;
   const double dig_off = 4503599627370496.0 + (double)g.half;   // 2^52 + beta/2
   const size_t ggsw_f = (size_t)2 * lv * 2 * 2 * FC * FT;         // double2 per GGSW
+  constexpr uint32_t kSliceBytes = 2 * 2 * FC * FT * sizeof(double2);
 #pragma unroll 1
   for (int s = s0; s < s1; ++s) {
     const int e = mod_switch(row[s], LOG2M);   // X^{a~_s}
     if (e == 0) continue;
-    for (int k = t; k < 2 * N; k += FT) {
-      const int c = k >= N, i = k & (N - 1);
-      sm.v[k] = decomp_prep(rot_read<N>(sm.acc + c * N, i, e) - sm.acc[k], g);
-    }
-    __syncthreads();
     double2 Y[2][2][FC];
 #pragma unroll
     for (int c = 0; c < 2; ++c)
@@ -847,26 +846,37 @@ __global__ void __launch_bounds__(FT, 1)
       const int comp = r < lv ? 1 : 0;
       const int tt = r < lv ? r : r - lv;
       const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
-      const uint32_t *vs = sm.v + comp * N + t;
+      const uint32_t *ac = sm.acc + comp * N;
       const double2 *gr = G + (size_t)r * (2 * 2 * FC * FT);
-#if HWB_FFT_PF
-      // bring this digit's key slice (32 KB per CTA) towards L1 while the transform runs
-#pragma unroll
-      for (int q = 0; q < 2 * 2 * FC; ++q) prefetch_l1(&gr[q * FT + t]);
-#endif
+      // digits of (acc X^e - acc) at this thread's positions i and i + H, straight
+      // from the accumulator (every thread reads only; it changes after the step)
       double2 x[FC];
 #pragma unroll
-      for (int j = 0; j < FC; ++j)
-        x[j] = make_double2(u2d_minus((vs[FT * j] >> sh) & g.mask, dig_off),
-                            u2d_minus((vs[FT * j + FH] >> sh) & g.mask, dig_off));
-      fwd_fft(x, sm.scr, lay, t, twf);
+      for (int j = 0; j < FC; ++j) {
+        const int i = t + FT * j;
+        const uint32_t p0 = decomp_prep(rot_read<N>(ac, i, e) - ac[i], g);
+        const uint32_t p1 = decomp_prep(rot_read<N>(ac, i + FH, e) - ac[i + FH], g);
+        x[j] = make_double2(u2d_minus((p0 >> sh) & g.mask, dig_off), u2d_minus((p1 >> sh) & g.mask, dig_off));
+      }
+      // the digit's key slice (32 KB, contiguous) lands in shared memory by TMA while
+      // the transform runs; it is issued after the transform's first barrier, when
+      // every thread has finished reading the previous slice
+      fwd_fft(x, sm.scr, lay, t, twf, [&] {
+        if (t == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_expect_tx(&sm.key_full, kSliceBytes);
+          bulk_g2s(sm.key, gr, kSliceBytes, &sm.key_full);
+        }
+      });
+      mbar_wait(&sm.key_full, key_phase);
+      key_phase ^= 1u;
 #pragma unroll
       for (int c = 0; c < 2; ++c)
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
           for (int j = 0; j < FC; ++j) {
-            const double2 k = __ldg(&gr[((c * 2 + h) * FC + j) * FT + t]);
+            const double2 k = sm.key[((c * 2 + h) * FC + j) * FT + t];
             double2 &y = Y[c][h][j];
             y.x = fma(x[j].x, k.x, fma(-x[j].y, k.y, y.x));
             y.y = fma(x[j].x, k.y, fma(x[j].y, k.x, y.y));
