@@ -194,10 +194,25 @@ class RgswCiphertext:
 
 @dataclass
 class BootstrapKey:
-    """RGSW_{S1}(s0_i) for i < n, resident on the device in the NTT domain."""
+    """RGSW_{S1}(s0_i) for i < n, resident on the device in the NTT domain and,
+    where the FP64 FFT ladder applies (N = 1024), as the FFT spectra of its signed
+    16-bit key halves (hwb_bsk_to_fft)."""
 
     params: HeParams
     ntt: GgswNtt
+    fft: torch.Tensor | None = field(default=None, repr=False)
+
+    @staticmethod
+    def from_coefficients(params: HeParams, bsk) -> "BootstrapKey":
+        coeff = to_device(bsk)
+        key = BootstrapKey(params, rgsw_to_ntt(params, coeff))
+        cp = _lib.c_params(params)
+        L = _lib.load()
+        nbytes = L.hwb_bsk_fft_bytes(ctypes.byref(cp))
+        if nbytes:
+            key.fft = torch.empty(nbytes, dtype=torch.uint8, device=coeff.device)
+            _lib.check(L.hwb_bsk_to_fft(ctypes.byref(cp), _ptr(coeff), _ptr(key.fft), _stream()))
+        return key
 
 
 @dataclass
@@ -246,8 +261,8 @@ class PbsKeys:
     ksk: np.ndarray                # (N, ks_l, n+1)
 
     def device_keys(self) -> tuple[BootstrapKey, LweKeySwitchKey]:
-        """Upload once: the BSK is transformed to the NTT domain on the GPU."""
-        return (BootstrapKey(self.params, rgsw_to_ntt(self.params, self.bsk)),
+        """Upload once: the BSK is transformed to the NTT (and FFT) domain on the GPU."""
+        return (BootstrapKey.from_coefficients(self.params, self.bsk),
                 LweKeySwitchKey(self.params, to_device(self.ksk)))
 
 
@@ -757,9 +772,13 @@ class PbsWorkspace:
 
     def get(self, params: HeParams, B: int, device, kind: str = "pbs") -> torch.Tensor:
         cp = _lib.c_params(params)
-        size_fn = {"pbs": "hwb_pbs_workspace_bytes", "pbs_tc": "hwb_pbs_tc_workspace_bytes",
-                   "ks_tc": "hwb_keyswitch_tc_workspace_bytes"}[kind]
-        nbytes = getattr(_lib.load(), size_fn)(ctypes.byref(cp), B)
+        L = _lib.load()
+        if kind.startswith("pbs_fft"):
+            nbytes = L.hwb_pbs_fft_workspace_bytes(ctypes.byref(cp), B, int(kind == "pbs_fft_ks"))
+        else:
+            size_fn = {"pbs": "hwb_pbs_workspace_bytes", "pbs_tc": "hwb_pbs_tc_workspace_bytes",
+                       "ks_tc": "hwb_keyswitch_tc_workspace_bytes"}[kind]
+            nbytes = getattr(L, size_fn)(ctypes.byref(cp), B)
         words = max(1, (nbytes + 3) // 4)
         if self.buf is None or self.buf.numel() < words or self.buf.device != device:
             self.buf = torch.empty(words, dtype=torch.int32, device=device)
@@ -769,11 +788,27 @@ class PbsWorkspace:
 _default_ws = PbsWorkspace()
 
 
+def _use_fft_ladder(bsk: BootstrapKey, B: int, ladder: str) -> bool:
+    """"auto": the FP64 FFT ladder when its key exists and the batch fills more
+    than one CTA per SM (single ciphertexts run faster on the NTT latency ladder);
+    "fft" / "ntt" force one (all ladders are bit-identical)."""
+    if ladder not in ("auto", "fft", "ntt"):
+        raise TfheError(f"unknown ladder {ladder!r}")
+    if ladder == "ntt":
+        return False
+    if bsk.fft is None:
+        if ladder == "fft":
+            raise TfheError("no FFT bootstrapping key for these parameters (N = 1024 only)")
+        return False
+    return ladder == "fft" or B > torch.cuda.get_device_properties(bsk.fft.device).multi_processor_count
+
+
 def pbs_batch(params: HeParams, lwe, tv, bsk: BootstrapKey, ksk: LweKeySwitchKey | None,
-              out=None, workspace: PbsWorkspace | None = None, engine: str = "auto"):
+              out=None, workspace: PbsWorkspace | None = None, engine: str = "auto", ladder: str = "auto"):
     """Programmable bootstrapping of a batch: (B, n+1) -> (B, n+1) (or (B, N+1)
     without a key-switch key).  tv is (2, N) shared or (B, 2, N) per item.
-    engine selects the key switch ("auto" | "tc" | "simt", see lwe_keyswitch)."""
+    engine selects the key switch ("auto" | "tc" | "simt", see lwe_keyswitch),
+    ladder the blind rotation ("auto" | "fft" | "ntt", see _use_fft_ladder)."""
     t = to_device(lwe)
     if t.dim() != 2 or t.shape[1] != params.lwe_n + 1:
         raise TfheError(f"LWE batch must be (B, {params.lwe_n + 1})")
@@ -793,7 +828,18 @@ def pbs_batch(params: HeParams, lwe, tv, bsk: BootstrapKey, ksk: LweKeySwitchKey
     if out is None:
         out = torch.empty((B, width), dtype=torch.int32, device=t.device)
     cp = _lib.c_params(params)
-    if _ks_engine(params, ksk, engine):
+    if _use_fft_ladder(bsk, B, ladder):
+        ks_tc = _ks_engine(params, ksk, engine)
+        if ksk is not None and not ks_tc:
+            # the FFT ladder pairs with the tensor-core key switch; the integer-pipe
+            # one runs as a separate pass
+            ext = pbs_batch(params, t, tvt, bsk, None, workspace=workspace, ladder="fft")
+            return _wrap(lwe, lwe_keyswitch(params, ext, ksk, out=out, engine=engine, workspace=workspace))
+        ws = (workspace or _default_ws).get(params, B, t.device, kind="pbs_fft_ks" if ks_tc else "pbs_fft")
+        _lib.check(_lib.load().hwb_pbs_fft(ctypes.byref(cp), _ptr(bsk.fft),
+                                           _ptr(ksk.tensor_core_tiles() if ks_tc else None), _ptr(tvt), per_item,
+                                           _ptr(t), _ptr(out), B, _ptr(ws), _stream()))
+    elif _ks_engine(params, ksk, engine):
         ws = (workspace or _default_ws).get(params, B, t.device, kind="pbs_tc")
         _lib.check(_lib.load().hwb_pbs_tc(ctypes.byref(cp), _ptr(bsk.ntt.data), _ptr(ksk.tensor_core_tiles()),
                                           _ptr(tvt), per_item, _ptr(t), _ptr(out), B, _ptr(ws), _stream()))

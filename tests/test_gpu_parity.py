@@ -242,6 +242,11 @@ def test_pbs_golden(name, variant, ladder):
     for engine in ("tc", "simt"):
         out = tfhe.pbs_batch(P, g["lwe_in"], g["tv"], bsk, ksk, engine=engine)
         assert_u32_equal(out, g["lwe_out"])
+    if bsk.fft is not None:                       # FP64 FFT ladder (N = 1024)
+        assert_u32_equal(tfhe.pbs_batch(P, g["lwe_in"], g["tv"], bsk, None, ladder="fft"), g["extracted"])
+        for engine in ("tc", "simt"):
+            out = tfhe.pbs_batch(P, g["lwe_in"], g["tv"], bsk, ksk, engine=engine, ladder="fft")
+            assert_u32_equal(out, g["lwe_out"])
 
 
 def test_pbs_batch_vs_c_oracle_and_decrypt(coracle, ladder):
@@ -260,6 +265,45 @@ def test_pbs_batch_vs_c_oracle_and_decrypt(coracle, ladder):
     tvs = np.stack([tv if i % 2 == 0 else tfhe.test_polynomial(np.ones(4, int), P) for i in range(B)])
     out2 = tfhe.pbs_batch(P, lwe, tvs, bsk, ksk)
     assert_u32_equal(out2, coracle.pbs(lwe, tvs, K.bsk, K.ksk, P))
+
+
+@pytest.mark.parametrize("name", ["CFG1", "CFG2"])
+def test_pbs_fft_ladder_vs_c_oracle(coracle, name):
+    """FP64 FFT ladder: bit-exact with the C oracle (schoolbook) on random inputs,
+    per-item test polynomials, several segment lengths and a ragged batch."""
+    P = dataclasses.replace(named_params(name), lwe_n=40)
+    K = tfhe.pbs_keygen(P, 61)
+    bsk, ksk = K.device_keys()
+    assert bsk.fft is not None
+    rng = np.random.default_rng(62)
+    lwe = rand_u32(rng, (37, P.lwe_n + 1))
+    tvs = rand_u32(rng, (37, 2, P.n))
+    want = coracle.pbs(lwe, tvs, K.bsk, K.ksk, P)
+    L = _lib.load()
+    try:
+        for seg in (1, 7, 64):
+            _lib.check(L.hwb_set_fft_segment(seg))
+            assert_u32_equal(tfhe.pbs_batch(P, lwe, tvs, bsk, ksk, ladder="fft"), want)
+    finally:
+        _lib.check(L.hwb_set_fft_segment(64))
+
+
+def test_pbs_fft_ladder_extreme_key():
+    """Largest-magnitude key halves (word 0x7FFF8000: lo = -2^15, hi = +2^15) and
+    all-ones / alternating inputs: the rounding margin's worst case, checked
+    against the NTT ladder (itself pinned to the oracle)."""
+    P = dataclasses.replace(named_params("CFG2"), lwe_n=24)
+    K = tfhe.pbs_keygen(P, 71)
+    for word in (0x7FFF8000, 0x80000000, 0x7FFFFFFF):
+        K.bsk[:] = word
+        bsk, _ = K.device_keys()
+        lwe = np.full((8, P.lwe_n + 1), 0xFFFFFFFF, np.uint32)
+        lwe[1::2, ::2] = 0x55555555
+        lwe[2] = np.arange(P.lwe_n + 1, dtype=np.uint32) * 0x9E3779B9
+        tv = np.full((2, P.n), 0x7FFFFFFF, np.uint32)
+        a = tfhe.pbs_batch(P, lwe, tv, bsk, None, ladder="fft")
+        b = tfhe.pbs_batch(P, lwe, tv, bsk, None, ladder="ntt")
+        assert_u32_equal(a, b)
 
 
 def test_pbs_full_batch_decrypts():
