@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--impl", choices=["hwb", "reference"], default="hwb")
     ap.add_argument("--batch", type=int, default=4096)
     ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--ladder", default="auto", choices=["auto", "fft", "ntt"],
+                    help="blind rotation: FP64 FFT ladder or two-prime NTT ladder (bit-identical)")
     ap.add_argument("--ks-engine", default="auto", choices=["auto", "tc", "simt"],
                     help="LWE key switch: tensor cores (tcgen05 int8) or the integer-pipe kernel")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -182,19 +184,39 @@ def probe_modmul_peak(torch, _lib, tfhe):
     return best
 
 
-def ncu_traffic(B, alg_bytes=None):
+def ncu_traffic(B, alg_bytes=None, ladder="ntt"):
     """DRAM bytes per blind-rotation launch from the committed ncu --set full
     capture (profiles/ncu_traffic.json) when it was taken at this batch size."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            rec = json.load(f)["blind_rotate_kernel<1024,PBS>"]
+            rec = json.load(f)["blind_rotate_fft_kernel" if ladder == "fft" else "blind_rotate_kernel<1024,PBS>"]
     except (OSError, KeyError, ValueError):
         return None
     if rec.get("batch") != B:
         return None
     return {"bytes": int(rec["dram_bytes_read"] + rec["dram_bytes_write"]), "unit": "B/launch",
             "algorithmic_bytes": alg_bytes, "source": rec.get("source")}
+
+
+def probe_fp64_peak(torch, _lib, tfhe):
+    """Measured P_fp64: register-only DFMA throughput (one launch filling every SM),
+    best of 4, CUDA events on the launching stream."""
+    import ctypes
+    sink = torch.zeros(4, dtype=torch.int32, device="cuda")
+    L = _lib.load()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    best = 0.0
+    for _ in range(4):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        n = L.hwb_probe_fp64(ctypes.c_void_p(sink.data_ptr()), sms * 8, 1024, tfhe._stream())
+        e.record()
+        e.synchronize()
+        if n < 0:
+            raise RuntimeError(L.hwb_last_error().decode())
+        best = max(best, n / (s.elapsed_time(e) * 1e-3))
+    return best
 
 
 def probe_i8mma_peak(torch, _lib, tfhe):
@@ -350,7 +372,7 @@ def bench_hwb(args):
     ks_engine = "tcgen05 kind::i8 (keyswitch_tc_kernel)" if ks_tc else "integer pipe (keyswitch_kernel)"
 
     def step():
-        tfhe.pbs_batch(P, lwe_d, tv_d, bsk, None, out=ext_d)          # blind rotation + extract
+        tfhe.pbs_batch(P, lwe_d, tv_d, bsk, None, out=ext_d, ladder=args.ladder)   # blind rotation + extract
         tfhe.lwe_keyswitch(P, ext_d, ksk, out=out_d, engine=args.ks_engine)   # key switch
 
     for _ in range(args.warmup):
@@ -367,7 +389,7 @@ def bench_hwb(args):
         flush.zero_()                                                 # L2 flush, untimed
         e0, e1, e2 = evs[k]
         e0.record()
-        tfhe.pbs_batch(P, lwe_d, tv_d, bsk, None, out=ext_d)
+        tfhe.pbs_batch(P, lwe_d, tv_d, bsk, None, out=ext_d, ladder=args.ladder)
         e1.record()
         tfhe.lwe_keyswitch(P, ext_d, ksk, out=out_d, engine=args.ks_engine)
         e2.record()
@@ -397,7 +419,7 @@ def bench_hwb(args):
         s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s_ev.record()
         dev_in = lwe_pin.to("cuda", non_blocking=True)
-        res = tfhe.pbs_batch(P, dev_in, tv_d, bsk, ksk, engine=args.ks_engine)
+        res = tfhe.pbs_batch(P, dev_in, tv_d, bsk, ksk, engine=args.ks_engine, ladder=args.ladder)
         out_pin.copy_(res, non_blocking=True)
         e_ev.record()
         e_ev.synchronize()
@@ -408,14 +430,32 @@ def bench_hwb(args):
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
 
-    # integer roofline of the dominant kernel (blind rotation): W_mm RNS
-    # modmuls per PBS (SURVEY.md §8(d) NTT formulation) over its event time
-    peak = probe_modmul_peak(torch, _lib, tfhe)
+    # roofline of the dominant kernel (blind rotation) over its event time.
+    # NTT ladder: W_mm RNS modmuls per PBS (SURVEY.md §8(d) NTT formulation) vs the
+    # measured P_mm.  FFT ladder: W_fp64 FP64 instructions per PBS vs the measured
+    # DFMA rate P_fp64 (both counts in DESIGN.md §4-5).
+    use_fft = tfhe._use_fft_ladder(bsk, B, args.ladder)
     lv, N, logN = P.gadget.levels, P.n, P.degree_log
     w_cmux = 2 * lv * (N // 2) * logN + 2 * (N // 2) * logN + 4 * lv * N   # 53,248 at cfg2
     w_mm = P.lwe_n * w_cmux
+    H, logH = N // 2, logN - 1
+    w_fstep = (2 * lv + 4) * (H // 2) * logH * 8 + 2 * lv * 4 * H * 4 + 2 * lv * N + 4 * N   # 243,712 at cfg2
+    w_fp64 = P.lwe_n * w_fstep
     br_avg_s = statistics.mean(br_ms) * 1e-3
-    achieved = w_mm * B / br_avg_s
+    if use_fft:
+        peak = probe_fp64_peak(torch, _lib, tfhe)
+        achieved = w_fp64 * B / br_avg_s
+        w_main, unit_main = w_fp64, "G FP64-instr/s"
+        roof_kernel = "blind_rotate_fft_kernel (FP64 FFT ladder)"
+        work_txt = f"W_fp64 = {w_fp64} FP64 instructions (n x {w_fstep} per CMUX)"
+        peak_src = "measured live: probe_fp64_kernel (8 independent DFMA chains per thread)"
+    else:
+        peak = probe_modmul_peak(torch, _lib, tfhe)
+        achieved = w_mm * B / br_avg_s
+        w_main, unit_main = w_mm, "Gmodmul/s"
+        roof_kernel = "blind_rotate_kernel<1024,PBS> (two-prime NTT ladder)"
+        work_txt = f"W_mm = {w_mm} RNS modmuls (n x 53,248 per CMUX)"
+        peak_src = "measured live: probe_modmul_kernel (register-only Shoup, both primes)"
     # key switch: W_ks int32 MACs; on tensor cores 4 byte limbs
     w_ks = P.n * P.gadget_ks.levels * (P.lwe_n + 1)
     ks_avg_s = statistics.mean(ks_ms) * 1e-3
@@ -424,7 +464,7 @@ def bench_hwb(args):
     else:
         p_ks, ks_unit, w_ks_eff = None, "int32 MAC/s", w_ks
     # PBS-level roofline: 1 / (W_mm/P_mm + W_ks/P_ks)
-    pbs_roof = 1.0 / (w_mm / peak + (w_ks_eff / p_ks if p_ks else 0.0))
+    pbs_roof = 1.0 / (w_main / peak + (w_ks_eff / p_ks if p_ks else 0.0))
 
     value = B * world * args.steps / (max_ms * 1e-3)
     result = {
@@ -432,19 +472,21 @@ def bench_hwb(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (seeded LWE encryptions, BASELINE cfg2 shapes)",
-        "config": config(P, B, world, {"kernel_variant": args.variant, "ks_engine": ks_engine}),
+        "config": config(P, B, world, {"kernel_variant": args.variant, "ks_engine": ks_engine,
+                                       "ladder": "fp64 FFT" if use_fft else "two-prime NTT"}),
         "e2e": {"value": round(B * world * args.steps / (float(e2e_t.item()) * 1e-3), 2), "unit": UNIT,
                 "h2d_bytes_per_step": int(lwe.nbytes), "d2h_bytes_per_step": int(out_h.nbytes),
                 "api": "tfhe.pbs_batch from pinned host tensors", "matches_device_run": e2e_ok},
-        "roofline": {"bound": "int", "kernel": "blind_rotate_kernel<1024,PBS>",
+        "roofline": {"bound": "fp64" if use_fft else "int", "kernel": roof_kernel,
                      "achieved": round(achieved / 1e9, 2), "peak": round(peak / 1e9, 2),
-                     "unit": "Gmodmul/s", "frac": round(achieved / peak, 4), "traffic": ncu_traffic(
-                         B, 4 * (P.lwe_n * 2 * lv * 2 * 2 * N + B * (P.lwe_n + 1) + B * (N + 1) + 2 * N)),
-                     "work_per_pbs": f"W_mm = {w_mm} RNS modmuls (n x 53,248 per CMUX)",
-                     "peak_source": "measured live: probe_modmul_kernel (register-only Shoup, both primes)",
+                     "unit": unit_main, "frac": round(achieved / peak, 4),
+                     "traffic": ncu_traffic(B, 4 * (P.lwe_n * 2 * lv * 2 * 2 * N + B * (P.lwe_n + 1)
+                                                    + B * (N + 1) + 2 * N), "fft" if use_fft else "ntt"),
+                     "work_per_pbs": work_txt, "peak_source": peak_src,
                      "pbs": {"roofline_pbs_per_s": round(pbs_roof, 1),
                              "frac": round(B / (max_ms / args.steps * 1e-3) / pbs_roof, 4),
-                             "formula": "1 / (W_mm/P_mm + 4 W_ks/P_i8)" if ks_tc else "W_mm/P_mm only"},
+                             "formula": ("1 / (W/P + 4 W_ks/P_i8)" if ks_tc else "W/P only")
+                             + (" with W = W_fp64, P = P_fp64" if use_fft else " with W = W_mm, P = P_mm")},
                      "keyswitch": {"bound": "tensor" if ks_tc else "int", "kernel": ks_engine,
                                    "achieved": round(w_ks_eff * B / ks_avg_s / 1e12, 3),
                                    "peak": round(p_ks / 1e12, 3) if p_ks else None, "unit": "T" + ks_unit,
@@ -454,7 +496,7 @@ def bench_hwb(args):
                                    if ks_tc else None}},
         "kernel_ms": {"blind_rotate": round(statistics.mean(br_ms), 3),
                       "keyswitch": round(statistics.mean(ks_ms), 3)},
-        "gpu_launches": (3 if ks_tc else 2) * args.steps,
+        "gpu_launches": ((-(-P.lwe_n // 64) if use_fft else 1) + (2 if ks_tc else 1)) * args.steps,
         "clocks": clock_info,
         "check": "all outputs decrypt to the LUT" if ok else "DECRYPTION MISMATCH",
     }
@@ -474,13 +516,13 @@ def bench_hwb(args):
         for Bs in [int(x) for x in args.sweep.split(",")]:
             ms_s = rng_s.integers(0, P.p, Bs)
             lw = tfhe.to_device(tfhe.enc_lwe_batch(ms_s * P.delta, keys.lwe_key, rng_s))
-            tfhe.pbs_batch(P, lw, tv_d, bsk, ksk, engine=args.ks_engine)   # warm-up
+            tfhe.pbs_batch(P, lw, tv_d, bsk, ksk, engine=args.ks_engine, ladder=args.ladder)   # warm-up
             reps = 3 if Bs <= 4096 else 1
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             s0.record()
             for _ in range(reps):
-                res = tfhe.pbs_batch(P, lw, tv_d, bsk, ksk, engine=args.ks_engine)
+                res = tfhe.pbs_batch(P, lw, tv_d, bsk, ksk, engine=args.ks_engine, ladder=args.ladder)
             s1.record()
             s1.synchronize()
             t_ms = s0.elapsed_time(s1) / reps
@@ -493,24 +535,31 @@ def bench_hwb(args):
         # the other BASELINE PBS parameter sets (cfg1: n=500, l=2, 2^8; cfg4: N=2048,
         # n=750, l=2, 2^10), same batch, device-resident, decryption checked
         other = {}
+        peaks = {"fft": probe_fp64_peak(torch, _lib, tfhe), "ntt": probe_modmul_peak(torch, _lib, tfhe)}
         for name in ("CFG1", "CFG4"):
             Po = named_params(name)
             ko, mo, lo, tvo = workload(Po, B, rank)
             bo, kso = ko.device_keys()
             lwo, tvd = tfhe.to_device(lo), tfhe.to_device(tvo)
-            res = tfhe.pbs_batch(Po, lwo, tvd, bo, kso)                        # warm-up
+            res = tfhe.pbs_batch(Po, lwo, tvd, bo, kso, ladder=args.ladder)   # warm-up
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             s0.record()
             for _ in range(2):
-                res = tfhe.pbs_batch(Po, lwo, tvd, bo, kso)
+                res = tfhe.pbs_batch(Po, lwo, tvd, bo, kso, ladder=args.ladder)
             s1.record()
             s1.synchronize()
             t_ms = s0.elapsed_time(s1) / 2
-            lvo, No = Po.gadget.levels, Po.n
-            w_o = Po.lwe_n * (2 * lvo * (No // 2) * Po.degree_log + 2 * (No // 2) * Po.degree_log + 4 * lvo * No)
+            lvo, No, lgo = Po.gadget.levels, Po.n, Po.degree_log
+            fft_o = tfhe._use_fft_ladder(bo, B, args.ladder)
+            if fft_o:
+                w_o = Po.lwe_n * ((2 * lvo + 4) * (No // 4) * (lgo - 1) * 8 + 2 * lvo * 4 * (No // 2) * 4
+                                  + 2 * lvo * No + 4 * No)
+            else:
+                w_o = Po.lwe_n * (2 * lvo * (No // 2) * lgo + 2 * (No // 2) * lgo + 4 * lvo * No)
             entry = {"pbs_per_s": round(B / (t_ms * 1e-3), 1), "ms_per_batch": round(t_ms, 3),
-                     "roofline_frac": round(w_o * B / (t_ms * 1e-3) / peak, 4),
+                     "ladder": "fp64 FFT" if fft_o else "two-prime NTT",
+                     "roofline_frac": round(w_o * B / (t_ms * 1e-3) / peaks["fft" if fft_o else "ntt"], 4),
                      "params": f"n={Po.lwe_n} N={No} Bg=2^{Po.gadget.base_log} l={lvo}"}
             if Po.p * 2 <= No:   # PBS decryption is meaningful (>= 2 phase units per message)
                 entry["decrypt_ok"] = bool(np.array_equal(tfhe.dec_lwe_batch(tfhe.to_host(res), ko.lwe_key),

@@ -72,6 +72,11 @@ int64_t hwb_set_latency_batch(int64_t max_batch);
  * Its rate is P_mm, the integer-pipe roofline denominator. */
 int64_t hwb_probe_modmul(uint32_t *sink, int32_t blocks, int32_t iters, void *stream);
 
+/* FP64 pipe probe (NEW): `blocks` x 256 threads, `iters` x 8 independent DFMA
+ * chains each.  Returns the FP64 instructions enqueued; its rate is P_fp64, the
+ * FFT ladder's roofline denominator. */
+int64_t hwb_probe_fp64(uint32_t *sink, int32_t blocks, int32_t iters, void *stream);
+
 /* Tensor-core throughput probe (NEW): `blocks` CTAs (one per SM) each issue
  * iters x 4 tcgen05.mma kind::i8 M128 N256 K32 from shared memory into TMEM,
  * the key switch's MMA shape.  Returns the int8 MACs enqueued (the caller times

@@ -27,7 +27,7 @@ EXPORTS = (
     "hwb_accumulate_rows", "hwb_ksk_tc_bytes", "hwb_ksk_to_tc", "hwb_keyswitch_tc_workspace_bytes",
     "hwb_keyswitch_tc", "hwb_pbs_tc_workspace_bytes", "hwb_pbs_tc", "hwb_probe_i8mma",
     "hwb_set_latency_batch", "hwb_bsk_fft_bytes", "hwb_bsk_to_fft", "hwb_pbs_fft",
-    "hwb_pbs_fft_workspace_bytes", "hwb_set_fft_segment",
+    "hwb_pbs_fft_workspace_bytes", "hwb_set_fft_segment", "hwb_probe_fp64",
 )
 
 
@@ -69,6 +69,8 @@ def load() -> ctypes.CDLL:
         L.hwb_probe_modmul.argtypes = [_vp, ctypes.c_int32, ctypes.c_int32, _vp]
         L.hwb_probe_modmul.restype = ctypes.c_int64
         L.hwb_probe_i8mma.argtypes = [_vp, ctypes.c_int32, ctypes.c_int32, _vp]
+        L.hwb_probe_fp64.argtypes = [_vp, ctypes.c_int32, ctypes.c_int32, _vp]
+        L.hwb_probe_fp64.restype = ctypes.c_int64
         L.hwb_probe_i8mma.restype = ctypes.c_int64
         L.hwb_bsk_fft_bytes.argtypes = [_pp]
         L.hwb_bsk_to_fft.argtypes = [_pp, _vp, _vp, _vp]
@@ -112,7 +114,7 @@ def load() -> ctypes.CDLL:
         for name in sizes:
             getattr(L, name).restype = ctypes.c_size_t
         for name in EXPORTS:
-            if name not in ("hwb_version", "hwb_last_error", "hwb_probe_modmul", "hwb_probe_i8mma",
+            if name not in ("hwb_version", "hwb_last_error", "hwb_probe_modmul", "hwb_probe_i8mma", "hwb_probe_fp64",
                             "hwb_set_latency_batch", *sizes):
                 getattr(L, name).restype = ctypes.c_int
         _lib = L

@@ -1206,6 +1206,22 @@ __global__ void __launch_bounds__(256) probe_modmul_kernel(uint32_t *sink, int i
   for (int k = 0; k < 8; ++k) s ^= a[k] ^ b[k];
   if (s == 0x12345678u) sink[0] = s;
 }
+// FP64 pipe probe: 8 independent DFMA chains per thread (the FFT ladder's
+// denominator P_fp64, in FP64 instructions per second).
+__global__ void __launch_bounds__(256) probe_fp64_kernel(uint32_t *sink, int iters) {
+  double a[8];
+  const double m = 1.0000000001, c = 1e-9 * (threadIdx.x + 1);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = threadIdx.x * 8 + k + blockIdx.x;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = fma(a[k], m, c);
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 0.123) sink[0] = 1u;
+}
 // ---------------------------------------------------------------------------
 // host helpers
 
@@ -1390,6 +1406,13 @@ int64_t hwb_probe_modmul(uint32_t *sink, int32_t blocks, int32_t iters, void *st
   if (blocks < 1 || iters < 1) return -fail(HWB_EINVAL, "probe needs positive blocks and iters");
   probe_modmul_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(sink, iters);
   if (post_launch("probe_modmul_kernel")) return -HWB_ECUDA;
+  return (int64_t)blocks * 256 * 8 * iters;
+}
+
+int64_t hwb_probe_fp64(uint32_t *sink, int32_t blocks, int32_t iters, void *stream) {
+  if (blocks < 1 || iters < 1) return -fail(HWB_EINVAL, "probe needs positive blocks and iters");
+  probe_fp64_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(sink, iters);
+  if (post_launch("probe_fp64_kernel")) return -HWB_ECUDA;
   return (int64_t)blocks * 256 * 8 * iters;
 }
 
