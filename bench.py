@@ -480,8 +480,10 @@ def bench_hwb(args):
         "roofline": {"bound": "fp64" if use_fft else "int", "kernel": roof_kernel,
                      "achieved": round(achieved / 1e9, 2), "peak": round(peak / 1e9, 2),
                      "unit": unit_main, "frac": round(achieved / peak, 4),
-                     "traffic": ncu_traffic(B, 4 * (P.lwe_n * 2 * lv * 2 * 2 * N + B * (P.lwe_n + 1)
-                                                    + B * (N + 1) + 2 * N), "fft" if use_fft else "ntt"),
+                     "traffic": ncu_traffic(B, (P.lwe_n * 2 * lv * 2 * 2 * (N // 2) * 16 if use_fft
+                                                else 4 * P.lwe_n * 2 * lv * 2 * 2 * N)
+                                               + 4 * (B * (P.lwe_n + 1) + B * (N + 1) + 2 * N),
+                                            "fft" if use_fft else "ntt"),
                      "work_per_pbs": work_txt, "peak_source": peak_src,
                      "pbs": {"roofline_pbs_per_s": round(pbs_roof, 1),
                              "frac": round(B / (max_ms / args.steps * 1e-3) / pbs_roof, 4),
