@@ -227,6 +227,18 @@ int hwb_pbs_tc(const hwb_params *p, const uint32_t *bsk_ntt, const void *ksk_tc,
 size_t hwb_bsk_fft_bytes(const hwb_params *p);
 /* bsk [n][2l][2][N] u32 (coefficient domain) -> bsk_fft (hwb_bsk_fft_bytes bytes). */
 int hwb_bsk_to_fft(const hwb_params *p, const uint32_t *bsk, void *bsk_fft, void *stream);
+/* FFT-domain GGSWs for the vertical-packing ladders (training / inference):
+ * bytes per GGSW, and the transform of `count` GGSWs [count][2l][2][N] u32. */
+size_t hwb_ggsw_fft_bytes(const hwb_params *p);
+int hwb_ggsw_to_fft(const hwb_params *p, const uint32_t *ggsw, void *ggsw_fft, int64_t count, void *stream);
+/* hwb_blind_rotate / hwb_ivp_level / hwb_vp_level on the FFT path (same results;
+ * ggsw_fft from hwb_ggsw_to_fft, indices as in the NTT versions). */
+int hwb_blind_rotate_fft(const hwb_params *p, const void *ggsw_fft, const int32_t *ggsw_idx, const int32_t *exps,
+                         uint32_t *acc, int32_t L, int64_t B, void *stream);
+int hwb_ivp_level_fft(const hwb_params *p, const void *ggsw_fft, const int32_t *ggsw_idx, const uint32_t *cur,
+                      uint32_t *next, int32_t m, int64_t B, void *stream);
+int hwb_vp_level_fft(const hwb_params *p, const void *ggsw_fft, const int32_t *ggsw_idx, const uint32_t *cur,
+                     uint32_t *next, int32_t m, int64_t B, void *stream);
 /* Workspace of hwb_pbs_fft: the accumulators between ladder segments, plus the
  * key switch's buffers when with_keyswitch. */
 size_t hwb_pbs_fft_workspace_bytes(const hwb_params *p, int64_t B, int with_keyswitch);

@@ -28,6 +28,7 @@ EXPORTS = (
     "hwb_keyswitch_tc", "hwb_pbs_tc_workspace_bytes", "hwb_pbs_tc", "hwb_probe_i8mma",
     "hwb_set_latency_batch", "hwb_bsk_fft_bytes", "hwb_bsk_to_fft", "hwb_pbs_fft",
     "hwb_pbs_fft_workspace_bytes", "hwb_set_fft_segment", "hwb_probe_fp64",
+    "hwb_ggsw_fft_bytes", "hwb_ggsw_to_fft", "hwb_blind_rotate_fft", "hwb_ivp_level_fft", "hwb_vp_level_fft",
 )
 
 
@@ -77,6 +78,11 @@ def load() -> ctypes.CDLL:
         L.hwb_pbs_fft.argtypes = [_pp, _vp, _vp, _vp, ctypes.c_int, _vp, _vp, _i64, _vp, _vp]
         L.hwb_pbs_fft_workspace_bytes.argtypes = [_pp, _i64, ctypes.c_int]
         L.hwb_set_fft_segment.argtypes = [ctypes.c_int]
+        L.hwb_ggsw_fft_bytes.argtypes = [_pp]
+        L.hwb_ggsw_to_fft.argtypes = [_pp, _vp, _vp, _i64, _vp]
+        L.hwb_blind_rotate_fft.argtypes = [_pp, _vp, _vp, _vp, _vp, ctypes.c_int32, _i64, _vp]
+        L.hwb_ivp_level_fft.argtypes = [_pp, _vp, _vp, _vp, _vp, ctypes.c_int32, _i64, _vp]
+        L.hwb_vp_level_fft.argtypes = [_pp, _vp, _vp, _vp, _vp, ctypes.c_int32, _i64, _vp]
         L.hwb_set_latency_batch.argtypes = [_i64]
         L.hwb_set_latency_batch.restype = ctypes.c_int64
         L.hwb_ggsw_ntt_words.argtypes = [_pp]
@@ -110,7 +116,7 @@ def load() -> ctypes.CDLL:
         L.hwb_pbs_tc.argtypes = [_pp, _vp, _vp, _vp, ctypes.c_int, _vp, _vp, _i64, _vp, _vp]
         sizes = ("hwb_ggsw_ntt_words", "hwb_pbs_workspace_bytes", "hwb_pack_ks_workspace_bytes",
                  "hwb_ksk_tc_bytes", "hwb_keyswitch_tc_workspace_bytes", "hwb_pbs_tc_workspace_bytes",
-                 "hwb_bsk_fft_bytes", "hwb_pbs_fft_workspace_bytes")
+                 "hwb_bsk_fft_bytes", "hwb_pbs_fft_workspace_bytes", "hwb_ggsw_fft_bytes")
         for name in sizes:
             getattr(L, name).restype = ctypes.c_size_t
         for name in EXPORTS:

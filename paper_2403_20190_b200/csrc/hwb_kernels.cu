@@ -788,14 +788,101 @@ struct FSmem {
   uint64_t key_full;              // mbarrier: slice landed
 };
 
-// Steps [s0, s1) of the ladder.  first: the accumulator starts as TV * X^-b~,
-// else it is read from acc_io; last: coefficient-0 extraction to lwe_out, else the
-// accumulator is written to acc_io.  Running the ladder in segments keeps the
-// segment's slice of the FFT key (192 KB per step) L2-resident for the whole batch:
-// the full key (n x 192 KB = 121 MB at cfg2) does not fit next to everything else.
+// One exact external product on the FFT path for the CTA's item.  prep(c, i) gives
+// the decomposition-ready value (decomp_prep) of component c, coefficient i; G is the
+// item's GGSW in the FFT domain [2l rows][2 comps][2 halves][FC][FT]; sink(c, i, v)
+// receives coefficient i of component c of the product for this thread's positions
+// i = t + 64 j and i + 512 (every thread owns the same positions in all transforms,
+// so no exchange is needed).  Each digit's 32 KB key slice is staged in shared
+// memory by a TMA bulk copy issued after the digit transform's first barrier.
+template <typename Prep, typename Sink>
+__device__ __forceinline__ void fft_ext_product(FSmem &sm, const double2 *__restrict__ G, const Gadget &g, int t,
+                                                const FLay &lay, const double2 *__restrict__ twf,
+                                                const double2 *__restrict__ twi, uint32_t &key_phase, Prep &&prep,
+                                                Sink &&sink) {
+  constexpr uint32_t kSliceBytes = 2 * 2 * FC * FT * sizeof(double2);
+  const int lv = (int)g.levels;
+  const double dig_off = 4503599627370496.0 + (double)g.half;   // 2^52 + beta/2
+  double2 Y[2][2][FC];
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int j = 0; j < FC; ++j) Y[c][h][j] = make_double2(0.0, 0.0);
+#pragma unroll 1
+  for (int r = 0; r < 2 * lv; ++r) {
+    // digit order (hw/tfhe.py:290-298): rows 0..l-1 = digits of b, l..2l-1 of a
+    const int comp = r < lv ? 1 : 0;
+    const int tt = r < lv ? r : r - lv;
+    const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
+    const double2 *gr = G + (size_t)r * (2 * 2 * FC * FT);
+    double2 x[FC];
+#pragma unroll
+    for (int j = 0; j < FC; ++j) {
+      const int i = t + FT * j;
+      const uint32_t p0 = prep(comp, i), p1 = prep(comp, i + FH);
+      x[j] = make_double2(u2d_minus((p0 >> sh) & g.mask, dig_off), u2d_minus((p1 >> sh) & g.mask, dig_off));
+    }
+    fwd_fft(x, sm.scr, lay, t, twf, [&] {
+      if (t == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&sm.key_full, kSliceBytes);
+        bulk_g2s(sm.key, gr, kSliceBytes, &sm.key_full);
+      }
+    });
+    mbar_wait(&sm.key_full, key_phase);
+    key_phase ^= 1u;
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int j = 0; j < FC; ++j) {
+          const double2 k = sm.key[((c * 2 + h) * FC + j) * FT + t];
+          double2 &y = Y[c][h][j];
+          y.x = fma(x[j].x, k.x, fma(-x[j].y, k.y, y.x));
+          y.y = fma(x[j].x, k.y, fma(x[j].y, k.x, y.y));
+        }
+  }
+  // inverse transforms, rounding, recombination of the halves
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    uint32_t lo_re[FC], lo_im[FC];
+    inv_fft(Y[c][0], sm.scr, lay, t, twi);
+#pragma unroll
+    for (int j = 0; j < FC; ++j) {
+      lo_re[j] = round_u32(Y[c][0][j].x);
+      lo_im[j] = round_u32(Y[c][0][j].y);
+    }
+    inv_fft(Y[c][1], sm.scr, lay, t, twi);
+#pragma unroll
+    for (int j = 0; j < FC; ++j) {
+      const int i = t + FT * j;
+      sink(c, i, lo_re[j] + (round_u32(Y[c][1][j].x) << 16));
+      sink(c, i + FH, lo_im[j] + (round_u32(Y[c][1][j].y) << 16));
+    }
+  }
+}
+
+__device__ __forceinline__ void fft_smem_init(FSmem &sm, int t) {
+  if (t == 0) {
+    mbar_init(&sm.key_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+}
+
+// The CMUX ladder on the FFT path.  PBS: lwe_in [B][L+1], the accumulator starts as
+// TV * X^-b~ (at s0 == 0), rotation X^{a~_s} with GGSW s, coefficient-0 extraction
+// at s1 == L; steps [s0, s1) per launch, the accumulator resting in acc_io between
+// launches -- running the ladder in segments keeps the segment's slice of the FFT key
+// (192 KB per step, 121 MB in all at cfg2) L2-resident for the whole batch.
+// !PBS: acc_io [B][2][N] in/out, exps [B][L] (rotation X^-I), GGSW gidx[b][s] (< 0:
+// skip) or s -- the per-item rotation ladders of vertical packing.
 template <bool PBS>
 __global__ void __launch_bounds__(FT, 1)
-    blind_rotate_fft_kernel(const double2 *__restrict__ bskf, const uint32_t *__restrict__ lwe_in,
+    blind_rotate_fft_kernel(const double2 *__restrict__ ggsw, const int32_t *__restrict__ gidx,
+                            const int32_t *__restrict__ exps, const uint32_t *__restrict__ lwe_in,
                             const uint32_t *__restrict__ tv, int tv_per_item, uint32_t *lwe_out, int L, Gadget g,
                             const double2 *__restrict__ twf, const double2 *__restrict__ twi, uint32_t *acc_io,
                             int s0, int s1) {
@@ -806,8 +893,8 @@ __global__ void __launch_bounds__(FT, 1)
   const int64_t b = blockIdx.x;
   const int t = threadIdx.x;
   const FLay lay = make_flay(t);
-  const uint32_t *row = lwe_in + b * (int64_t)(L + 1);
-  if (s0 == 0) {
+  const uint32_t *row = PBS ? lwe_in + b * (int64_t)(L + 1) : nullptr;
+  if (PBS && s0 == 0) {
     const int bt = mod_switch(row[L], LOG2M);
     const uint32_t *tp = tv + (tv_per_item ? b * 2 * N : 0);
     const int e = (2 * N - bt) & (2 * N - 1);   // X^-b~
@@ -818,97 +905,79 @@ __global__ void __launch_bounds__(FT, 1)
   } else {
     for (int k = t; k < 2 * N; k += FT) sm.acc[k] = acc_io[b * 2 * N + k];
   }
-  if (t == 0) {
-    mbar_init(&sm.key_full, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
+  fft_smem_init(sm, t);
   __syncthreads();
   uint32_t key_phase = 0;
-  const int lv = (int)g.levels;
-  const double dig_off = 4503599627370496.0 + (double)g.half;   // 2^52 + beta/2
-  const size_t ggsw_f = (size_t)2 * lv * 2 * 2 * FC * FT;         // double2 per GGSW
-  constexpr uint32_t kSliceBytes = 2 * 2 * FC * FT * sizeof(double2);
+  const size_t ggsw_f = (size_t)2 * g.levels * 2 * 2 * FC * FT;   // double2 per GGSW
 #pragma unroll 1
   for (int s = s0; s < s1; ++s) {
-    const int e = mod_switch(row[s], LOG2M);   // X^{a~_s}
-    if (e == 0) continue;
-    double2 Y[2][2][FC];
-#pragma unroll
-    for (int c = 0; c < 2; ++c)
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int j = 0; j < FC; ++j) Y[c][h][j] = make_double2(0.0, 0.0);
-    const double2 *G = bskf + (size_t)s * ggsw_f;
-#pragma unroll 1
-    for (int r = 0; r < 2 * lv; ++r) {
-      // digit order (hw/tfhe.py:290-298): rows 0..l-1 = digits of b, l..2l-1 of a
-      const int comp = r < lv ? 1 : 0;
-      const int tt = r < lv ? r : r - lv;
-      const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
-      const uint32_t *ac = sm.acc + comp * N;
-      const double2 *gr = G + (size_t)r * (2 * 2 * FC * FT);
-      // digits of (acc X^e - acc) at this thread's positions i and i + H, straight
-      // from the accumulator (every thread reads only; it changes after the step)
-      double2 x[FC];
-#pragma unroll
-      for (int j = 0; j < FC; ++j) {
-        const int i = t + FT * j;
-        const uint32_t p0 = decomp_prep(rot_read<N>(ac, i, e) - ac[i], g);
-        const uint32_t p1 = decomp_prep(rot_read<N>(ac, i + FH, e) - ac[i + FH], g);
-        x[j] = make_double2(u2d_minus((p0 >> sh) & g.mask, dig_off), u2d_minus((p1 >> sh) & g.mask, dig_off));
-      }
-      // the digit's key slice (32 KB, contiguous) lands in shared memory by TMA while
-      // the transform runs; it is issued after the transform's first barrier, when
-      // every thread has finished reading the previous slice
-      fwd_fft(x, sm.scr, lay, t, twf, [&] {
-        if (t == 0) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_expect_tx(&sm.key_full, kSliceBytes);
-          bulk_g2s(sm.key, gr, kSliceBytes, &sm.key_full);
-        }
-      });
-      mbar_wait(&sm.key_full, key_phase);
-      key_phase ^= 1u;
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int j = 0; j < FC; ++j) {
-            const double2 k = sm.key[((c * 2 + h) * FC + j) * FT + t];
-            double2 &y = Y[c][h][j];
-            y.x = fma(x[j].x, k.x, fma(-x[j].y, k.y, y.x));
-            y.y = fma(x[j].x, k.y, fma(x[j].y, k.x, y.y));
-          }
+    int e, gi = s;
+    if (PBS) {
+      e = mod_switch(row[s], LOG2M);   // X^{a~_s}
+    } else {
+      e = (int)((-(int64_t)exps[b * L + s]) % (2 * N));
+      if (e < 0) e += 2 * N;
+      if (gidx) gi = gidx[b * L + s];
     }
-    // inverse transforms, rounding, recombination of the halves, accumulation
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      uint32_t lo_re[FC], lo_im[FC];
-      inv_fft(Y[c][0], sm.scr, lay, t, twi);
-#pragma unroll
-      for (int j = 0; j < FC; ++j) {
-        lo_re[j] = round_u32(Y[c][0][j].x);
-        lo_im[j] = round_u32(Y[c][0][j].y);
-      }
-      inv_fft(Y[c][1], sm.scr, lay, t, twi);
-#pragma unroll
-      for (int j = 0; j < FC; ++j) {
-        const int i = t + FT * j;
-        sm.acc[c * N + i] += lo_re[j] + (round_u32(Y[c][1][j].x) << 16);
-        sm.acc[c * N + i + FH] += lo_im[j] + (round_u32(Y[c][1][j].y) << 16);
-      }
-    }
+    if (e == 0 || gi < 0) continue;
+    fft_ext_product(
+        sm, ggsw + (size_t)gi * ggsw_f, g, t, lay, twf, twi, key_phase,
+        [&](int c, int i) {   // digits of (acc X^e - acc), straight from the accumulator
+          const uint32_t *ac = sm.acc + c * N;
+          return decomp_prep(rot_read<N>(ac, i, e) - ac[i], g);
+        },
+        [&](int c, int i, uint32_t v) { sm.acc[c * N + i] += v; });
     __syncthreads();
   }
-  if (s1 < L) {
+  if (!PBS || s1 < L) {
     for (int k = t; k < 2 * N; k += FT) acc_io[b * 2 * N + k] = sm.acc[k];
     return;
   }
   uint32_t *o = lwe_out + b * (int64_t)(N + 1);
   for (int k = t; k < N; k += FT) o[k] = k == 0 ? sm.acc[0] : 0u - sm.acc[N - k];
   if (t == 0) o[N] = sm.acc[N];
+}
+
+// One tree level of vertical packing on the FFT path (cmux_kernel's MODE_IVP_LEVEL /
+// MODE_VP_LEVEL): block = item * m + sub, GGSW gidx[item].
+template <int MODE>
+__global__ void __launch_bounds__(FT, 1)
+    level_fft_kernel(const double2 *__restrict__ ggsw, const int32_t *__restrict__ gidx,
+                     const uint32_t *__restrict__ in, uint32_t *out, int m, Gadget g,
+                     const double2 *__restrict__ twf, const double2 *__restrict__ twi) {
+  constexpr int N = 2 * FH;
+  extern __shared__ uint4 smem_raw[];
+  FSmem &sm = *reinterpret_cast<FSmem *>(smem_raw);
+  const int64_t b = blockIdx.x, item = b / m, sub = b % m;
+  const int t = threadIdx.x;
+  const FLay lay = make_flay(t);
+  const size_t ggsw_f = (size_t)2 * g.levels * 2 * 2 * FC * FT;
+  const double2 *G = ggsw + (size_t)gidx[item] * ggsw_f;
+  uint32_t key_phase = 0;
+  if (MODE == MODE_IVP_LEVEL) {
+    // CDEMUX (hw/lut.py:113-119, 294-313): hi = C (*) d, lo = d - hi
+    const uint32_t *d = in + (item * m + sub) * 2 * N;
+    uint32_t *o_lo = out + (item * 2 * m + sub) * 2 * N, *o_hi = out + (item * 2 * m + m + sub) * 2 * N;
+    for (int k = t; k < 2 * N; k += FT) sm.acc[k] = d[k];
+    fft_smem_init(sm, t);
+    __syncthreads();
+    fft_ext_product(
+        sm, G, g, t, lay, twf, twi, key_phase, [&](int c, int i) { return decomp_prep(sm.acc[c * N + i], g); },
+        [&](int c, int i, uint32_t v) {
+          o_hi[c * N + i] = v;
+          o_lo[c * N + i] = sm.acc[c * N + i] - v;
+        });
+  } else {
+    // CMUX (hw/lut.py:130-136, 233-247): next = c0 + C (*) (c1 - c0)
+    const uint32_t *c0 = in + (item * 2 * m + sub) * 2 * N, *c1 = in + (item * 2 * m + m + sub) * 2 * N;
+    uint32_t *o = out + (item * m + sub) * 2 * N;
+    for (int k = t; k < 2 * N; k += FT) sm.acc[k] = c1[k] - c0[k];
+    fft_smem_init(sm, t);
+    __syncthreads();
+    fft_ext_product(
+        sm, G, g, t, lay, twf, twi, key_phase, [&](int c, int i) { return decomp_prep(sm.acc[c * N + i], g); },
+        [&](int c, int i, uint32_t v) { o[c * N + i] = c0[c * N + i] + v; });
+  }
 }
 
 template <int N>
@@ -1772,13 +1841,82 @@ int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, co
   const int L = (int)p->n;
   for (int s0 = 0; s0 < L; s0 += g_fft_segment) {
     const int s1 = s0 + g_fft_segment < L ? s0 + g_fft_segment : L;
-    blind_rotate_fft_kernel<true><<<(unsigned)B, FT, smem, s>>>((const double2 *)bsk_fft, lwe_in, tv, tv_per_item,
-                                                                ext, L, g, st->fft_fwd, st->fft_inv, acc, s0, s1);
+    blind_rotate_fft_kernel<true><<<(unsigned)B, FT, smem, s>>>((const double2 *)bsk_fft, nullptr, nullptr, lwe_in, tv,
+                                                                tv_per_item, ext, L, g, st->fft_fwd, st->fft_inv,
+                                                                acc, s0, s1);
     if ((rc = post_launch("blind_rotate_fft_kernel"))) return rc;
   }
   if (!ksk_tc) return HWB_OK;
   return keyswitch_tc_launch(p, ksk_tc, ext, lwe_out, B,
                              ws + fft_acc_bytes(B) + pbs_ext_bytes(p, B), s);
+}
+
+size_t hwb_ggsw_fft_bytes(const hwb_params *p) {
+  if (!p || check_fft(p)) return 0;
+  return (size_t)2 * p->l * 2 * 2 * FH * sizeof(double2);
+}
+
+int hwb_ggsw_to_fft(const hwb_params *p, const uint32_t *ggsw, void *ggsw_fft, int64_t count, void *stream) {
+  int rc = check_fft(p);
+  if (rc) return rc;
+  if (count < 0) return fail(HWB_EINVAL, "negative count");
+  if (count == 0) return HWB_OK;
+  if (!ggsw || !ggsw_fft) return fail(HWB_EINVAL, "null pointer");
+  if ((uintptr_t)ggsw_fft & 15) return fail(HWB_EINVAL, "ggsw_fft must be 16-byte aligned");
+  const int64_t polys = count * 2 * p->l * 2;
+  if (polys > 0x7FFFFFFF) return fail(HWB_EINVAL, "too many GGSWs");
+  DevState *st;
+  if ((rc = init_device(&st))) return rc;
+  bsk_to_fft_kernel<<<(unsigned)polys, FT, 0, (cudaStream_t)stream>>>(ggsw, (double2 *)ggsw_fft, st->fft_fwd);
+  return post_launch("bsk_to_fft_kernel");
+}
+
+int hwb_blind_rotate_fft(const hwb_params *p, const void *ggsw_fft, const int32_t *ggsw_idx, const int32_t *exps,
+                         uint32_t *acc, int32_t L, int64_t B, void *stream) {
+  int rc = check_fft(p);
+  if (rc) return rc;
+  if (L < 0 || B < 0) return fail(HWB_EINVAL, "negative size");
+  if (L == 0 || B == 0) return HWB_OK;
+  if (B > 0x7FFFFFFF) return fail(HWB_EINVAL, "batch too large");
+  if (!ggsw_fft || !exps || !acc) return fail(HWB_EINVAL, "null pointer");
+  DevState *st;
+  if ((rc = init_device(&st))) return rc;
+  const size_t smem = sizeof(FSmem);
+  if ((rc = set_smem(blind_rotate_fft_kernel<false>, smem))) return rc;
+  blind_rotate_fft_kernel<false><<<(unsigned)B, FT, smem, (cudaStream_t)stream>>>(
+      (const double2 *)ggsw_fft, ggsw_idx, exps, nullptr, nullptr, 0, nullptr, L, make_gadget(p->l, p->base_log),
+      st->fft_fwd, st->fft_inv, acc, 0, L);
+  return post_launch("blind_rotate_fft_kernel");
+}
+
+extern "C++" {
+template <int MODE>
+static int level_fft(const hwb_params *p, const void *ggsw_fft, const int32_t *ggsw_idx, const uint32_t *cur,
+                     uint32_t *next, int32_t m, int64_t B, void *stream) {
+  int rc = check_fft(p);
+  if (rc) return rc;
+  if (m < 1 || B < 0) return fail(HWB_EINVAL, "bad level shape");
+  if (B == 0) return HWB_OK;
+  if (B * m > 0x7FFFFFFF) return fail(HWB_EINVAL, "batch too large");
+  if (!ggsw_fft || !ggsw_idx || !cur || !next) return fail(HWB_EINVAL, "null pointer");
+  DevState *st;
+  if ((rc = init_device(&st))) return rc;
+  const size_t smem = sizeof(FSmem);
+  if ((rc = set_smem(level_fft_kernel<MODE>, smem))) return rc;
+  level_fft_kernel<MODE><<<(unsigned)(B * m), FT, smem, (cudaStream_t)stream>>>(
+      (const double2 *)ggsw_fft, ggsw_idx, cur, next, m, make_gadget(p->l, p->base_log), st->fft_fwd, st->fft_inv);
+  return post_launch("level_fft_kernel");
+}
+}  // extern "C++"
+
+int hwb_ivp_level_fft(const hwb_params *p, const void *ggsw_fft, const int32_t *ggsw_idx, const uint32_t *cur,
+                      uint32_t *next, int32_t m, int64_t B, void *stream) {
+  return level_fft<MODE_IVP_LEVEL>(p, ggsw_fft, ggsw_idx, cur, next, m, B, stream);
+}
+
+int hwb_vp_level_fft(const hwb_params *p, const void *ggsw_fft, const int32_t *ggsw_idx, const uint32_t *cur,
+                     uint32_t *next, int32_t m, int64_t B, void *stream) {
+  return level_fft<MODE_VP_LEVEL>(p, ggsw_fft, ggsw_idx, cur, next, m, B, stream);
 }
 
 size_t hwb_pbs_fft_workspace_bytes(const hwb_params *p, int64_t B, int with_keyswitch) {

@@ -267,22 +267,41 @@ class _Staged:
         return self.dev
 
 
-def _stack_table(params: HeParams, samples: list[EncryptedSample], staged: _Staged | None = None):
-    """One device NTT-domain GGSW table holding every sample's RGSW rows, each
-    sample transformed straight into its slice (no stacking copy)."""
+def _use_fft(params: HeParams, ladder: str) -> bool:
+    """Vertical-packing ladders on the FP64 FFT path ("auto": wherever it applies,
+    N = 1024) or the two-prime NTT path; both are bit-identical."""
+    if ladder not in ("auto", "fft", "ntt"):
+        raise TfheError(f"unknown ladder {ladder!r}")
+    ok = tfhe.ggsw_fft_bytes(params) > 0
+    if ladder == "fft" and not ok:
+        raise TfheError("the FFT ladder needs N = 1024")
+    return ok and ladder != "ntt"
+
+
+def _stack_table(params: HeParams, samples: list[EncryptedSample], staged: _Staged | None = None,
+                 ladder: str = "auto"):
+    """One device GGSW table (NTT or FFT domain) holding every sample's RGSW rows,
+    each sample transformed straight into its slice (no stacking copy)."""
     import ctypes
     cp = _lib_params(params)
     L = tfhe._lib.load()
-    words = L.hwb_ggsw_ntt_words(cp)
     rows = [int(s.rgsw.shape[0]) for s in samples]
-    table = torch.empty((sum(rows), words), dtype=torch.int32, device=tfhe._device())
+    fft = _use_fft(params, ladder)
+    if fft:
+        nbytes = L.hwb_ggsw_fft_bytes(cp)
+        table = torch.empty(sum(rows) * nbytes, dtype=torch.uint8, device=tfhe._device())
+        conv = L.hwb_ggsw_to_fft
+    else:
+        nbytes = L.hwb_ggsw_ntt_words(cp) * 4
+        table = torch.empty((sum(rows), nbytes // 4), dtype=torch.int32, device=tfhe._device())
+        conv = L.hwb_ggsw_to_ntt
     srcs = (staged or _Staged(samples)).tensors()
     off = 0
     for src, r in zip(srcs, rows):
-        dst = ctypes.c_void_p(table.data_ptr() + off * words * 4)
-        tfhe._lib.check(L.hwb_ggsw_to_ntt(cp, tfhe._ptr(src), dst, r, tfhe._stream()))
+        dst = ctypes.c_void_p(table.data_ptr() + off * nbytes)
+        tfhe._lib.check(conv(cp, tfhe._ptr(src), dst, r, tfhe._stream()))
         off += r
-    return tfhe.GgswNtt(params, table)
+    return tfhe.GgswFft(params, table, sum(rows)) if fft else tfhe.GgswNtt(params, table)
 
 
 def he_count_labels_batch(params: HeParams, counts_ct: torch.Tensor, table, label_rows: np.ndarray,
@@ -294,7 +313,8 @@ def he_count_labels_batch(params: HeParams, counts_ct: torch.Tensor, table, labe
 
 
 def he_train(samples: Iterable[EncryptedSample], geometry: WisardGeometry, params: HeParams,
-             model: HomWisardModel | None = None, threads: int = 1, batch: int = 16) -> HomWisardModel:
+             model: HomWisardModel | None = None, threads: int = 1, batch: int = 16,
+             ladder: str = "auto") -> HomWisardModel:
     """Homomorphic integer WiSARD training (hw/hewnn.py:189-229); pass an
     existing model to continue training.  `threads` is accepted for API
     compatibility (the GPU batches `batch` samples per launch instead)."""
@@ -316,7 +336,7 @@ def he_train(samples: Iterable[EncryptedSample], geometry: WisardGeometry, param
     _payload(params)
 
     def run(chunk: list[EncryptedSample], staged: _Staged):
-        table = _stack_table(params, chunk, staged)
+        table = _stack_table(params, chunk, staged, ladder)
         I = len(chunk)
         rows = lut.ivp_codes(params, all_codes[: I * k0], table, _payload(params),
                              d_codes[: I * k0])                              # (I*k0, k1, 2, N)

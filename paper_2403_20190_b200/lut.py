@@ -26,7 +26,7 @@ import torch
 from . import _lib, tfhe
 from ._lib import TfheError
 from .params import HeParams
-from .tfhe import GgswNtt, RgswCiphertext, RlweCiphertext
+from .tfhe import GgswFft, GgswNtt, RgswCiphertext, RlweCiphertext
 
 CLEAR0, CLEAR1 = -1, -2
 
@@ -132,7 +132,7 @@ def _upload_i32(arrays, device) -> list[torch.Tensor]:
     return out
 
 
-def _rotation_ladder(params, table: GgswNtt, acc: torch.Tensor, cols: np.ndarray, sign: int,
+def _rotation_ladder(params, table: GgswNtt | GgswFft, acc: torch.Tensor, cols: np.ndarray, sign: int,
                      dev_args: tuple | None = None) -> torch.Tensor:
     """All encrypted rotation positions of a selector batch in ONE launch
     (hwb_blind_rotate with per-item GGSW rows): for position i (weight 2^i),
@@ -149,8 +149,9 @@ def _rotation_ladder(params, table: GgswNtt, acc: torch.Tensor, cols: np.ndarray
         idx = _i32(np.where(cols >= 0, cols, -1), dev)
         exps = _i32(_rotation_exps(params, B, L, sign), dev)
     out = acc.contiguous().clone()
-    _lib.check(_lib.load().hwb_blind_rotate(_cp(params), tfhe._ptr(table.data), tfhe._ptr(idx), tfhe._ptr(exps),
-                                            tfhe._ptr(out), L, B, tfhe._stream()))
+    fn = _lib.load().hwb_blind_rotate_fft if isinstance(table, GgswFft) else _lib.load().hwb_blind_rotate
+    _lib.check(fn(_cp(params), tfhe._ptr(table.data), tfhe._ptr(idx), tfhe._ptr(exps), tfhe._ptr(out), L, B,
+                  tfhe._stream()))
     return out
 
 
@@ -158,14 +159,15 @@ def _rotation_exps(params, B: int, L: int, sign: int) -> np.ndarray:
     return np.broadcast_to(-sign * (1 << np.arange(L, dtype=np.int64)), (B, L)) % (2 * params.n)
 
 
-def _level(params, table: GgswNtt, cur: torch.Tensor, idx: torch.Tensor, inverse: bool) -> torch.Tensor:
+def _level(params, table: GgswNtt | GgswFft, cur: torch.Tensor, idx: torch.Tensor, inverse: bool) -> torch.Tensor:
     B, mm = cur.shape[0], cur.shape[1]
+    fft = isinstance(table, GgswFft)
     if inverse:
         nxt = torch.empty((B, 2 * mm) + tuple(cur.shape[2:]), dtype=torch.int32, device=cur.device)
-        fn, m = _lib.load().hwb_ivp_level, mm
+        fn, m = (_lib.load().hwb_ivp_level_fft if fft else _lib.load().hwb_ivp_level), mm
     else:
         nxt = torch.empty((B, mm // 2) + tuple(cur.shape[2:]), dtype=torch.int32, device=cur.device)
-        fn, m = _lib.load().hwb_vp_level, mm // 2
+        fn, m = (_lib.load().hwb_vp_level_fft if fft else _lib.load().hwb_vp_level), mm // 2
     _lib.check(fn(_cp(params), tfhe._ptr(table.data), tfhe._ptr(idx), tfhe._ptr(cur), tfhe._ptr(nxt), m, B,
                   tfhe._stream()))
     return nxt

@@ -40,6 +40,7 @@ __all__ = [
     "phase_lwe_batch", "rgsw_rep", "rgsw_to_ntt", "ext_product_batch", "external_product",
     "cmux", "cmux_batch", "cdemux_batch", "blind_rotate", "blind_rotate_batch", "extract_lwe",
     "sample_extract_batch", "mod_switch", "test_polynomial", "lwe_keyswitch", "pbs_batch",
+    "GgswFft", "rgsw_to_fft", "ggsw_fft_bytes",
 ]
 
 
@@ -176,6 +177,37 @@ class GgswNtt:
     @property
     def count(self) -> int:
         return int(self.data.shape[0])
+
+
+@dataclass
+class GgswFft:
+    """Device-resident FFT-domain GGSWs (hwb_ggsw_to_fft): `count` GGSWs of
+    hwb_ggsw_fft_bytes each -- the spectra of the signed 16-bit halves of every key
+    polynomial, consumed by the FP64 FFT ladders (N = 1024)."""
+
+    params: HeParams
+    data: torch.Tensor       # uint8, count * ggsw_bytes
+    count: int
+
+
+def ggsw_fft_bytes(params: HeParams) -> int:
+    """Bytes of one FFT-domain GGSW, 0 where the FFT ladders do not apply."""
+    cp = _lib.c_params(params)
+    return int(_lib.load().hwb_ggsw_fft_bytes(ctypes.byref(cp)))
+
+
+def rgsw_to_fft(params: HeParams, ggsw) -> GgswFft:
+    """Transform (count, 2l, 2, N) GGSWs into the FFT domain on the GPU."""
+    t = to_device(ggsw if not (isinstance(ggsw, np.ndarray) and ggsw.ndim == 3) else ggsw[np.newaxis])
+    if t.dim() != 4 or t.shape[1:] != (2 * params.gadget.levels, 2, params.n):
+        raise TfheError(f"GGSW batch must be (count, {2 * params.gadget.levels}, 2, {params.n})")
+    nb = ggsw_fft_bytes(params)
+    if nb == 0:
+        raise TfheError("FFT-domain GGSWs need N = 1024")
+    out = torch.empty(t.shape[0] * nb, dtype=torch.uint8, device=t.device)
+    cp = _lib.c_params(params)
+    _lib.check(_lib.load().hwb_ggsw_to_fft(ctypes.byref(cp), _ptr(t), _ptr(out), t.shape[0], _stream()))
+    return GgswFft(params, out, int(t.shape[0]))
 
 
 @dataclass

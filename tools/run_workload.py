@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--cfg", type=int, default=3)
     ap.add_argument("--images", type=int, default=32)
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--ladder", default="auto", choices=["auto", "fft", "ntt"])
     a = ap.parse_args()
     if a.what == "pbs":
         P = named_params("CFG2")
@@ -50,7 +51,7 @@ def main():
         smp = [hewnn.encrypt_sample(ds.bits[i], None if lab is None else int(lab[i]), key, rng,
                                     label_bits=geom.label_bits) for i in range(a.images)]
         if a.what == "train":
-            run = lambda: hewnn.he_train(smp, geom, P, batch=a.images)  # noqa: E731
+            run = lambda: hewnn.he_train(smp, geom, P, batch=a.images, ladder=a.ladder)  # noqa: E731
         else:
             model = hewnn.HomWisardModel.zeros(geom, P)
             run = lambda: hewnn.he_infer_pd_batch(model, smp, pksk)  # noqa: E731
