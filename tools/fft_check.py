@@ -26,7 +26,7 @@ def main(B=4096):
         ms = rng.integers(0, P.p, B)
         lwe = tfhe.to_device(tfhe.enc_lwe_batch(ms * P.delta, keys.lwe_key, rng))
         tv = tfhe.to_device(tfhe.test_polynomial(np.arange(P.p // 2), P))
-        ref = tfhe.pbs_batch(P, lwe, tv, bsk, None)
+        ref = tfhe.pbs_batch(P, lwe, tv, bsk, None, ladder="ntt")
         out = torch.empty_like(ref)
         ws = torch.empty(L.hwb_pbs_fft_workspace_bytes(ctypes.byref(cp), B, 0), dtype=torch.uint8, device="cuda")
         seg = int(sys.argv[2]) if len(sys.argv) > 2 else 64
@@ -40,7 +40,7 @@ def main(B=4096):
         same = torch.equal(out, ref)
         nd = int((out != ref).sum())
         times = {}
-        for label, fn in (("ntt", lambda: tfhe.pbs_batch(P, lwe, tv, bsk, None, out=ref)), ("fft", fft)):
+        for label, fn in (("ntt", lambda: tfhe.pbs_batch(P, lwe, tv, bsk, None, out=ref, ladder="ntt")), ("fft", fft)):
             fn()
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
