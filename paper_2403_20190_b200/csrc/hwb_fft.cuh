@@ -144,6 +144,49 @@ __device__ __forceinline__ void inv_fft(double2 (&x)[FC], double2 *scr, const FL
   });
 }
 
+// K independent inverse transforms in lockstep (the four accumulators of a CMUX
+// step): one pair of barriers per transpose for all K, K times the ILP per stage.
+// scr holds K * FH elements.
+template <int K, int FROM, int TO>
+__device__ __forceinline__ void frelayout_k(double2 (*x)[FC], double2 *scr, const FLay &L) {
+  const uint32_t bf = flay_base<FROM>(L), bt = flay_base<TO>(L);
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int j = 0; j < FC; ++j) scr[k * FH + (bf ^ fswz(joff<FH, FT, FROM>(j)))] = x[k][j];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int j = 0; j < FC; ++j) x[k][j] = scr[k * FH + (bt ^ fswz(joff<FH, FT, TO>(j)))];
+  __syncthreads();
+}
+
+template <int K>
+__device__ __forceinline__ void inv_fft_k(double2 (*x)[FC], double2 *scr, const FLay &L, int t,
+                                          const double2 *__restrict__ tw) {
+  using G = FGeo;
+  static_for<0, G::B_TOP>([&](auto Q) {
+    constexpr int s = decltype(Q)::value;
+    constexpr int slot = G::C - 2 * (G::C >> (s + 1));
+#pragma unroll
+    for (int k = 0; k < K; ++k) fft_stage<false, s, false, 0, slot>(x[k], t, tw);
+  });
+  frelayout_k<K, LAY_B, LAY_M>(x, scr, L);
+  static_for<0, G::T - G::LOGC>([&](auto Q) {
+    constexpr int s = G::LOGC + decltype(Q)::value;
+    constexpr int slot = G::B_SLOTS + (1 << (G::T - G::LOGC)) - (1 << (G::T - s));
+#pragma unroll
+    for (int k = 0; k < K; ++k) fft_stage<false, s - G::LO, false, 0, slot>(x[k], t, tw);
+  });
+  frelayout_k<K, LAY_M, LAY_A>(x, scr, L);
+  static_for<0, G::LOGN - G::T>([&](auto Q) {
+    constexpr int s = G::T + decltype(Q)::value;
+#pragma unroll
+    for (int k = 0; k < K; ++k) fft_stage<false, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x[k], t, tw);
+  });
+}
+
 // exact small integer -> double without a conversion instruction: 2^52 + u - (2^52 + off)
 __device__ __forceinline__ double u2d_minus(uint32_t u, double two52_plus_off) {
   return __hiloint2double(0x43300000, (int)u) - two52_plus_off;

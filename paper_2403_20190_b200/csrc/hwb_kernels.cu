@@ -845,24 +845,18 @@ __device__ __forceinline__ void fft_ext_product(FSmem &sm, const double2 *__rest
           y.y = fma(x[j].x, k.y, fma(x[j].y, k.x, y.y));
         }
   }
-  // inverse transforms, rounding, recombination of the halves
+  // the four inverse transforms in lockstep, their transposes in the (now idle) key
+  // buffer; then rounding and recombination of the halves
+  __syncthreads();   // every thread has finished reading the last key slice
+  inv_fft_k<4>(&Y[0][0], sm.key, lay, t, twi);
 #pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    uint32_t lo_re[FC], lo_im[FC];
-    inv_fft(Y[c][0], sm.scr, lay, t, twi);
-#pragma unroll
-    for (int j = 0; j < FC; ++j) {
-      lo_re[j] = round_u32(Y[c][0][j].x);
-      lo_im[j] = round_u32(Y[c][0][j].y);
-    }
-    inv_fft(Y[c][1], sm.scr, lay, t, twi);
+  for (int c = 0; c < 2; ++c)
 #pragma unroll
     for (int j = 0; j < FC; ++j) {
       const int i = t + FT * j;
-      sink(c, i, lo_re[j] + (round_u32(Y[c][1][j].x) << 16));
-      sink(c, i + FH, lo_im[j] + (round_u32(Y[c][1][j].y) << 16));
+      sink(c, i, round_u32(Y[c][0][j].x) + (round_u32(Y[c][1][j].x) << 16));
+      sink(c, i + FH, round_u32(Y[c][0][j].y) + (round_u32(Y[c][1][j].y) << 16));
     }
-  }
 }
 
 __device__ __forceinline__ void fft_smem_init(FSmem &sm, int t) {
