@@ -490,7 +490,7 @@ class FinalizeResult:
 
 
 def he_infer_pd_batch(model: HomWisardModel, samples: Sequence[EncryptedSample],
-                      ksk: tfhe.PackingKeySwitchKey) -> list[ScorePack]:
+                      ksk: tfhe.PackingKeySwitchKey, ladder: str = "auto") -> list[ScorePack]:
     """he_infer_pd (hw/hewnn.py:278-320) for several samples in one pass: every
     (sample, class, RAM) triple is one vertical-packing item (clear label bits,
     encrypted address bits), then each sample's l*k0 extracted LWEs are packed."""
@@ -507,7 +507,7 @@ def he_infer_pd_batch(model: HomWisardModel, samples: Sequence[EncryptedSample],
     strides = np.cumsum([0] + [int(np.asarray(smp.rgsw.shape[0])) for smp in samples])
     codes = np.concatenate([_shift(tmpl, int(strides[i])) for i in range(len(samples))])
     lut_idx = np.tile(np.tile(np.arange(k0), l), len(samples))
-    table = _stack_table(params, list(samples))
+    table = _stack_table(params, list(samples), ladder=ladder)
     lwe = lut.vp_codes(params, codes, table, model.rams, lut_idx)          # (S*l*k0, N+1)
     n_ct = -(-total // n)
     S = len(samples)

@@ -37,10 +37,11 @@ def samples_of(name, device=True):
 
 @pytest.mark.parametrize("name", sorted(TRAIN_CASES))
 @pytest.mark.parametrize("batch", [1, 16])
-def test_he_train_matches_reference(name, batch):
+@pytest.mark.parametrize("ladder", ["fft", "ntt"])
+def test_he_train_matches_reference(name, batch, ladder):
     g = golden(f"{name}.npz")
     P, s1, bits, labels, smp, geom = samples_of(name)
-    model = hewnn.he_train(smp, geom, P, batch=batch)
+    model = hewnn.he_train(smp, geom, P, batch=batch, ladder=ladder)
     rams = tfhe.to_host(model.rams)
     assert sha(rams) == str(g["sha_rams"])
     assert_u32_equal(rams[:, :2], g["rams_head"])
@@ -92,18 +93,17 @@ def test_ivp_vp_codes_vs_oracle(k):
     table = rng.integers(0, 1 << 32, (R, 6, 2, P.n), dtype=np.uint64).astype(np.uint32)
     payload = rng.integers(0, 1 << 32, (2, P.n), dtype=np.uint64).astype(np.uint32)
     codes = _random_codes(rng, 5, k, R)
-    ntt = tfhe.rgsw_to_ntt(P, table)
-    got = tfhe.to_host(lut.ivp_codes(P, codes, ntt, payload))
     want = wnn32.ivp_batch(codes, table, payload, 3, 7, P.degree_log)
-    assert_u32_equal(got, want)
     z = lut.tree_depth(k, P)
     luts = rng.integers(0, 1 << 32, (3, max(1, 1 << z), 2, P.n), dtype=np.uint64).astype(np.uint32)
     lut_idx = rng.integers(0, 3, 5)
     vcodes = _random_codes(rng, 5, k, R)
     vcodes[:, 0] = lut.CLEAR1                       # exercise the clear-prefix slicing
-    got = tfhe.to_host(lut.vp_codes(P, vcodes, ntt, tfhe.to_device(luts), lut_idx))
-    want = wnn32.vp_batch(vcodes, table, luts[lut_idx], 3, 7, P.degree_log)
-    assert_u32_equal(got, want)
+    vwant = wnn32.vp_batch(vcodes, table, luts[lut_idx], 3, 7, P.degree_log)
+    for tab in (tfhe.rgsw_to_ntt(P, table), tfhe.rgsw_to_fft(P, table)):     # both ladders
+        assert_u32_equal(tfhe.to_host(lut.ivp_codes(P, codes, tab, payload)), want)
+        got = tfhe.to_host(lut.vp_codes(P, vcodes, tab, tfhe.to_device(luts), lut_idx))
+        assert_u32_equal(got, vwant)
 
 
 def test_lut_roundtrip_decrypts():
@@ -146,6 +146,7 @@ def test_pack_batch_and_he_infer_pd_match_reference():
     tsample = hewnn.EncryptedSample(P, tfhe.to_device(test_rgsw), geom.s, 0)
     pack = hewnn.he_infer_pd(model, tsample, pksk)                                         # hw/hewnn.py:278
     assert_u32_equal(pack.packed, g["infer_packed"])
+    assert_u32_equal(hewnn.he_infer_pd_batch(model, [tsample], pksk, ladder="ntt")[0].packed, g["infer_packed"])
     fin = hewnn.client_finalize(pack, key, wnn.ActivationSpec("bin", 0))
     assert np.array_equal(fin.raw, g["raw"]) and fin.prediction == int(g["prediction"])
     assert fin.noise_ok
