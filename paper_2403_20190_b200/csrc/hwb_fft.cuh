@@ -162,6 +162,32 @@ __device__ __forceinline__ void frelayout_k(double2 (*x)[FC], double2 *scr, cons
   __syncthreads();
 }
 
+// K independent forward transforms in lockstep (the two key halves of a GGSW row)
+template <int K>
+__device__ __forceinline__ void fwd_fft_k(double2 (*x)[FC], double2 *scr, const FLay &L, int t,
+                                          const double2 *__restrict__ tw) {
+  using G = FGeo;
+  static_for<0, G::LOGN - G::T>([&](auto Q) {
+    constexpr int s = G::LOGN - 1 - decltype(Q)::value;
+#pragma unroll
+    for (int k = 0; k < K; ++k) fft_stage<true, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x[k], t, tw);
+  });
+  frelayout_k<K, LAY_A, LAY_M>(x, scr, L);
+  static_for<0, G::T - G::LOGC>([&](auto Q) {
+    constexpr int s = G::T - 1 - decltype(Q)::value;
+    constexpr int slot = (1 << decltype(Q)::value) - 1;
+#pragma unroll
+    for (int k = 0; k < K; ++k) fft_stage<true, s - G::LO, false, 0, slot>(x[k], t, tw);
+  });
+  frelayout_k<K, LAY_M, LAY_B>(x, scr, L);
+  static_for<0, G::B_TOP>([&](auto Q) {
+    constexpr int s = G::B_TOP - 1 - decltype(Q)::value;
+    constexpr int slot = G::M_SLOTS + (G::C >> G::B_TOP) * ((1 << decltype(Q)::value) - 1);
+#pragma unroll
+    for (int k = 0; k < K; ++k) fft_stage<true, s, false, 0, slot>(x[k], t, tw);
+  });
+}
+
 template <int K>
 __device__ __forceinline__ void inv_fft_k(double2 (*x)[FC], double2 *scr, const FLay &L, int t,
                                           const double2 *__restrict__ tw) {

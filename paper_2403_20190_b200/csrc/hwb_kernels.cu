@@ -754,30 +754,32 @@ __global__ void __launch_bounds__(128 * LV, MINB)
 // BSK [n][2l][2][N] u32 -> FFT domain [n][2l][2][2 halves][FC][FT] double2 (scaled 1/H).
 __global__ void __launch_bounds__(FT) bsk_to_fft_kernel(const uint32_t *__restrict__ in, double2 *out,
                                                          const double2 *__restrict__ twf) {
-  __shared__ double2 scr[FH];
+  __shared__ double2 scr[2 * FH];
   const int t = threadIdx.x;
   const int64_t poly = blockIdx.x;
   const uint32_t *a = in + poly * (2 * FH);
   const FLay lay = make_flay(t);
-#pragma unroll 1
-  for (int h = 0; h < 2; ++h) {
-    double2 x[FC];
+  double2 x[2][FC];   // [half][j]: both halves transformed in lockstep
 #pragma unroll
-    for (int j = 0; j < FC; ++j) {
-      const int i = t + FT * j;
-      double v[2];
+  for (int j = 0; j < FC; ++j) {
+    const int i = t + FT * j;
+    double lo[2], hi[2];
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int64_t gword = (int32_t)a[i + q * FH];               // signed 32-bit key word
-        const int64_t lo = ((gword + 32768) & 0xFFFF) - 32768;       // [-2^15, 2^15)
-        v[q] = (double)(h ? (gword - lo) >> 16 : lo);
-      }
-      x[j] = make_double2(v[0], v[1]);
+    for (int q = 0; q < 2; ++q) {
+      const int64_t gword = (int32_t)a[i + q * FH];               // signed 32-bit key word
+      const int64_t l16 = ((gword + 32768) & 0xFFFF) - 32768;      // [-2^15, 2^15)
+      lo[q] = (double)l16;
+      hi[q] = (double)((gword - l16) >> 16);
     }
-    fwd_fft(x, scr, lay, t, twf);
+    x[0][j] = make_double2(lo[0], lo[1]);
+    x[1][j] = make_double2(hi[0], hi[1]);
+  }
+  fwd_fft_k<2>(x, scr, lay, t, twf);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
     double2 *o = out + (poly * 2 + h) * (FC * FT);
 #pragma unroll
-    for (int j = 0; j < FC; ++j) o[j * FT + t] = make_double2(x[j].x * (1.0 / FH), x[j].y * (1.0 / FH));
+    for (int j = 0; j < FC; ++j) o[j * FT + t] = make_double2(x[h][j].x * (1.0 / FH), x[h][j].y * (1.0 / FH));
   }
 }
 
