@@ -244,6 +244,9 @@ int hwb_vp_level_fft(const hwb_params *p, const void *ggsw_fft, const int32_t *g
 size_t hwb_pbs_fft_workspace_bytes(const hwb_params *p, int64_t B, int with_keyswitch);
 /* Ladder steps per launch (default 64): each launch's key slice stays L2-resident. */
 int hwb_set_fft_segment(int steps);
+/* Ciphertexts per CTA of the FFT PBS ladder (1, 2 or 4): they share every staged key
+ * slice (one shared-memory write, several reads). */
+int hwb_set_fft_group(int ciphertexts_per_cta);
 /* hwb_pbs on the FFT ladder with the tensor-core key switch (ksk_tc from
  * hwb_ksk_to_tc); ksk_tc == NULL skips the key switch (lwe_out [B][N+1]). */
 int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, const uint32_t *tv,

@@ -81,19 +81,29 @@ __device__ __forceinline__ uint32_t flay_base(const FLay &L) {
   return LAY == LAY_A ? L.a : (LAY == LAY_M ? L.m : L.b);
 }
 
+// Barrier of the 64 threads of one transform: the whole CTA (bar == 0) or a named
+// barrier when a CTA holds several transform groups.
+__device__ __forceinline__ void fsync(int bar) {
+  if (bar == 0)
+    __syncthreads();
+  else
+    asm volatile("bar.sync %0, 64;" ::"r"(bar) : "memory");
+}
+
 // The CTA is exactly the 64 threads of the transform: CTA barriers.  `after_first`
 // runs once all threads have passed the first barrier (everyone finished the
 // previous consumer of any shared buffer -- the key-slice prefetch hook).
 template <int FROM, int TO, typename F>
-__device__ __forceinline__ void frelayout(double2 (&x)[FC], double2 *scr, const FLay &L, F &&after_first) {
+__device__ __forceinline__ void frelayout(double2 (&x)[FC], double2 *scr, const FLay &L, F &&after_first,
+                                          int bar = 0) {
   const uint32_t bf = flay_base<FROM>(L), bt = flay_base<TO>(L);
 #pragma unroll
   for (int j = 0; j < FC; ++j) scr[bf ^ fswz(joff<FH, FT, FROM>(j))] = x[j];
-  __syncthreads();
+  fsync(bar);
   after_first();
 #pragma unroll
   for (int j = 0; j < FC; ++j) x[j] = scr[bt ^ fswz(joff<FH, FT, TO>(j))];
-  __syncthreads();
+  fsync(bar);
 }
 struct NoHook {
   __device__ __forceinline__ void operator()() const {}
@@ -102,19 +112,19 @@ struct NoHook {
 // natural (layout A) -> block order (layout B); per-thread twiddle slots as fwd_ntt
 template <typename F = NoHook>
 __device__ __forceinline__ void fwd_fft(double2 (&x)[FC], double2 *scr, const FLay &L, int t,
-                                        const double2 *__restrict__ tw, F &&hook = F()) {
+                                        const double2 *__restrict__ tw, F &&hook = F(), int bar = 0) {
   using G = FGeo;
   static_for<0, G::LOGN - G::T>([&](auto K) {
     constexpr int s = G::LOGN - 1 - decltype(K)::value;
     fft_stage<true, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x, t, tw);
   });
-  frelayout<LAY_A, LAY_M>(x, scr, L, hook);
+  frelayout<LAY_A, LAY_M>(x, scr, L, hook, bar);
   static_for<0, G::T - G::LOGC>([&](auto K) {
     constexpr int s = G::T - 1 - decltype(K)::value;
     constexpr int slot = (1 << decltype(K)::value) - 1;
     fft_stage<true, s - G::LO, false, 0, slot>(x, t, tw);
   });
-  frelayout<LAY_M, LAY_B>(x, scr, L, NoHook());
+  frelayout<LAY_M, LAY_B>(x, scr, L, NoHook(), bar);
   static_for<0, G::B_TOP>([&](auto K) {
     constexpr int s = G::B_TOP - 1 - decltype(K)::value;
     constexpr int slot = G::M_SLOTS + (G::C >> G::B_TOP) * ((1 << decltype(K)::value) - 1);
@@ -124,20 +134,20 @@ __device__ __forceinline__ void fwd_fft(double2 (&x)[FC], double2 *scr, const FL
 
 // block order (layout B) -> natural (layout A), unscaled (1/H is in the key)
 __device__ __forceinline__ void inv_fft(double2 (&x)[FC], double2 *scr, const FLay &L, int t,
-                                        const double2 *__restrict__ tw) {
+                                        const double2 *__restrict__ tw, int bar = 0) {
   using G = FGeo;
   static_for<0, G::B_TOP>([&](auto K) {
     constexpr int s = decltype(K)::value;
     constexpr int slot = G::C - 2 * (G::C >> (s + 1));
     fft_stage<false, s, false, 0, slot>(x, t, tw);
   });
-  frelayout<LAY_B, LAY_M>(x, scr, L, NoHook());
+  frelayout<LAY_B, LAY_M>(x, scr, L, NoHook(), bar);
   static_for<0, G::T - G::LOGC>([&](auto K) {
     constexpr int s = G::LOGC + decltype(K)::value;
     constexpr int slot = G::B_SLOTS + (1 << (G::T - G::LOGC)) - (1 << (G::T - s));
     fft_stage<false, s - G::LO, false, 0, slot>(x, t, tw);
   });
-  frelayout<LAY_M, LAY_A>(x, scr, L, NoHook());
+  frelayout<LAY_M, LAY_A>(x, scr, L, NoHook(), bar);
   static_for<0, G::LOGN - G::T>([&](auto K) {
     constexpr int s = G::T + decltype(K)::value;
     fft_stage<false, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x, t, tw);

@@ -783,12 +783,16 @@ __global__ void __launch_bounds__(FT) bsk_to_fft_kernel(const uint32_t *__restri
   }
 }
 
-struct FSmem {
-  uint32_t acc[2 * 2 * FH];
-  double2 scr[FH];
+// CPB ciphertexts per CTA (64 threads each) share one staged key slice per digit:
+// the slice is written into shared memory once and read CPB times.
+template <int CPB>
+struct FSmemT {
+  uint32_t acc[CPB][2 * 2 * FH];
+  double2 scr[CPB][FH];
   double2 key[2 * 2 * FC * FT];   // the current digit's key slice [c][h][j][t] (32 KB, TMA)
   uint64_t key_full;              // mbarrier: slice landed
 };
+using FSmem = FSmemT<1>;
 
 // One exact external product on the FFT path for the CTA's item.  prep(c, i) gives
 // the decomposition-ready value (decomp_prep) of component c, coefficient i; G is the
@@ -797,11 +801,13 @@ struct FSmem {
 // i = t + 64 j and i + 512 (every thread owns the same positions in all transforms,
 // so no exchange is needed).  Each digit's 32 KB key slice is staged in shared
 // memory by a TMA bulk copy issued after the digit transform's first barrier.
-template <typename Prep, typename Sink>
-__device__ __forceinline__ void fft_ext_product(FSmem &sm, const double2 *__restrict__ G, const Gadget &g, int t,
-                                                const FLay &lay, const double2 *__restrict__ twf,
+template <int CPB = 1, typename Prep, typename Sink>
+__device__ __forceinline__ void fft_ext_product(FSmemT<CPB> &sm, const double2 *__restrict__ G, const Gadget &g,
+                                                int t, const FLay &lay, const double2 *__restrict__ twf,
                                                 const double2 *__restrict__ twi, uint32_t &key_phase, Prep &&prep,
-                                                Sink &&sink) {
+                                                Sink &&sink, int grp = 0) {
+  double2 *scr = sm.scr[grp];
+  const int bar = CPB == 1 ? 0 : 1 + grp;
   constexpr uint32_t kSliceBytes = 2 * 2 * FC * FT * sizeof(double2);
   const int lv = (int)g.levels;
   const double dig_off = 4503599627370496.0 + (double)g.half;   // 2^52 + beta/2
@@ -826,13 +832,22 @@ __device__ __forceinline__ void fft_ext_product(FSmem &sm, const double2 *__rest
       const uint32_t p0 = prep(comp, i), p1 = prep(comp, i + FH);
       x[j] = make_double2(u2d_minus((p0 >> sh) & g.mask, dig_off), u2d_minus((p1 >> sh) & g.mask, dig_off));
     }
-    fwd_fft(x, sm.scr, lay, t, twf, [&] {
-      if (t == 0) {
+    auto stage_key = [&] {
+      if (threadIdx.x == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&sm.key_full, kSliceBytes);
         bulk_g2s(sm.key, gr, kSliceBytes, &sm.key_full);
       }
-    });
+    };
+    if (CPB == 1) {
+      // issued after the transform's first barrier: every thread is past the MAC
+      // that read the previous slice
+      fwd_fft(x, scr, lay, t, twf, stage_key);
+    } else {
+      __syncthreads();   // all groups are past the previous slice's MAC
+      stage_key();
+      fwd_fft(x, scr, lay, t, twf, NoHook(), bar);
+    }
     mbar_wait(&sm.key_full, key_phase);
     key_phase ^= 1u;
 #pragma unroll
@@ -847,10 +862,16 @@ __device__ __forceinline__ void fft_ext_product(FSmem &sm, const double2 *__rest
           y.y = fma(x[j].x, k.y, fma(x[j].y, k.x, y.y));
         }
   }
-  // the four inverse transforms in lockstep, their transposes in the (now idle) key
-  // buffer; then rounding and recombination of the halves
-  __syncthreads();   // every thread has finished reading the last key slice
-  inv_fft_k<4>(&Y[0][0], sm.key, lay, t, twi);
+  if (CPB == 1) {
+    // the four inverse transforms in lockstep, their transposes in the (now idle)
+    // key buffer
+    __syncthreads();   // every thread has finished reading the last key slice
+    inv_fft_k<4>(&Y[0][0], sm.key, lay, t, twi);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) inv_fft((&Y[0][0])[q], scr, lay, t, twi, bar);
+  }
+  // rounding and recombination of the halves
 #pragma unroll
   for (int c = 0; c < 2; ++c)
 #pragma unroll
@@ -875,19 +896,24 @@ __device__ __forceinline__ void fft_smem_init(FSmem &sm, int t) {
 // (192 KB per step, 121 MB in all at cfg2) L2-resident for the whole batch.
 // !PBS: acc_io [B][2][N] in/out, exps [B][L] (rotation X^-I), GGSW gidx[b][s] (< 0:
 // skip) or s -- the per-item rotation ladders of vertical packing.
-template <bool PBS>
-__global__ void __launch_bounds__(FT, 1)
+template <bool PBS, int CPB = 1>
+__global__ void __launch_bounds__(FT * CPB, 1)
     blind_rotate_fft_kernel(const double2 *__restrict__ ggsw, const int32_t *__restrict__ gidx,
                             const int32_t *__restrict__ exps, const uint32_t *__restrict__ lwe_in,
                             const uint32_t *__restrict__ tv, int tv_per_item, uint32_t *lwe_out, int L, Gadget g,
                             const double2 *__restrict__ twf, const double2 *__restrict__ twi, uint32_t *acc_io,
-                            int s0, int s1) {
+                            int s0, int s1, int64_t B) {
   constexpr int N = 2 * FH;
   constexpr int LOG2M = 11;
   extern __shared__ uint4 smem_raw[];
-  FSmem &sm = *reinterpret_cast<FSmem *>(smem_raw);
-  const int64_t b = blockIdx.x;
-  const int t = threadIdx.x;
+  FSmemT<CPB> &sm = *reinterpret_cast<FSmemT<CPB> *>(smem_raw);
+  const int grp = threadIdx.x / FT, t = threadIdx.x % FT;
+  // groups past the end of the batch run a clamped copy of the last ciphertext (they
+  // must take part in every CTA barrier) and write nothing
+  const int64_t bb = (int64_t)blockIdx.x * CPB + grp;
+  const bool valid = bb < B;
+  const int64_t b = valid ? bb : B - 1;
+  uint32_t *acc = sm.acc[grp];
   const FLay lay = make_flay(t);
   const uint32_t *row = PBS ? lwe_in + b * (int64_t)(L + 1) : nullptr;
   if (PBS && s0 == 0) {
@@ -896,12 +922,15 @@ __global__ void __launch_bounds__(FT, 1)
     const int e = (2 * N - bt) & (2 * N - 1);   // X^-b~
     for (int k = t; k < 2 * N; k += FT) {
       const int c = k >= N, i = k & (N - 1);
-      sm.acc[k] = rot_read<N>(tp + c * N, i, e);
+      acc[k] = rot_read<N>(tp + c * N, i, e);
     }
   } else {
-    for (int k = t; k < 2 * N; k += FT) sm.acc[k] = acc_io[b * 2 * N + k];
+    for (int k = t; k < 2 * N; k += FT) acc[k] = acc_io[b * 2 * N + k];
   }
-  fft_smem_init(sm, t);
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.key_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
   uint32_t key_phase = 0;
   const size_t ggsw_f = (size_t)2 * g.levels * 2 * 2 * FC * FT;   // double2 per GGSW
@@ -915,23 +944,33 @@ __global__ void __launch_bounds__(FT, 1)
       if (e < 0) e += 2 * N;
       if (gidx) gi = gidx[b * L + s];
     }
-    if (e == 0 || gi < 0) continue;
-    fft_ext_product(
-        sm, ggsw + (size_t)gi * ggsw_f, g, t, lay, twf, twi, key_phase,
+    if (CPB == 1 && (e == 0 || gi < 0)) continue;
+    const bool skip = e == 0 || gi < 0;
+    // (CPB > 1: every group runs the step -- the key slices and barriers are shared --
+    // and a group whose step is an exact no-op discards the product)
+    fft_ext_product<CPB>(
+        sm, ggsw + (size_t)(gi < 0 ? 0 : gi) * ggsw_f, g, t, lay, twf, twi, key_phase,
         [&](int c, int i) {   // digits of (acc X^e - acc), straight from the accumulator
-          const uint32_t *ac = sm.acc + c * N;
+          const uint32_t *ac = acc + c * N;
           return decomp_prep(rot_read<N>(ac, i, e) - ac[i], g);
         },
-        [&](int c, int i, uint32_t v) { sm.acc[c * N + i] += v; });
-    __syncthreads();
+        [&](int c, int i, uint32_t v) {
+          if (!skip) acc[c * N + i] += v;
+        },
+        grp);
+    if (CPB == 1)
+      __syncthreads();
+    else
+      fsync(1 + grp);
   }
+  if (!valid) return;
   if (!PBS || s1 < L) {
-    for (int k = t; k < 2 * N; k += FT) acc_io[b * 2 * N + k] = sm.acc[k];
+    for (int k = t; k < 2 * N; k += FT) acc_io[b * 2 * N + k] = acc[k];
     return;
   }
   uint32_t *o = lwe_out + b * (int64_t)(N + 1);
-  for (int k = t; k < N; k += FT) o[k] = k == 0 ? sm.acc[0] : 0u - sm.acc[N - k];
-  if (t == 0) o[N] = sm.acc[N];
+  for (int k = t; k < N; k += FT) o[k] = k == 0 ? acc[0] : 0u - acc[N - k];
+  if (t == 0) o[N] = acc[N];
 }
 
 // One tree level of vertical packing on the FFT path (cmux_kernel's MODE_IVP_LEVEL /
@@ -954,24 +993,24 @@ __global__ void __launch_bounds__(FT, 1)
     // CDEMUX (hw/lut.py:113-119, 294-313): hi = C (*) d, lo = d - hi
     const uint32_t *d = in + (item * m + sub) * 2 * N;
     uint32_t *o_lo = out + (item * 2 * m + sub) * 2 * N, *o_hi = out + (item * 2 * m + m + sub) * 2 * N;
-    for (int k = t; k < 2 * N; k += FT) sm.acc[k] = d[k];
+    for (int k = t; k < 2 * N; k += FT) sm.acc[0][k] = d[k];
     fft_smem_init(sm, t);
     __syncthreads();
     fft_ext_product(
-        sm, G, g, t, lay, twf, twi, key_phase, [&](int c, int i) { return decomp_prep(sm.acc[c * N + i], g); },
+        sm, G, g, t, lay, twf, twi, key_phase, [&](int c, int i) { return decomp_prep(sm.acc[0][c * N + i], g); },
         [&](int c, int i, uint32_t v) {
           o_hi[c * N + i] = v;
-          o_lo[c * N + i] = sm.acc[c * N + i] - v;
+          o_lo[c * N + i] = sm.acc[0][c * N + i] - v;
         });
   } else {
     // CMUX (hw/lut.py:130-136, 233-247): next = c0 + C (*) (c1 - c0)
     const uint32_t *c0 = in + (item * 2 * m + sub) * 2 * N, *c1 = in + (item * 2 * m + m + sub) * 2 * N;
     uint32_t *o = out + (item * m + sub) * 2 * N;
-    for (int k = t; k < 2 * N; k += FT) sm.acc[k] = c1[k] - c0[k];
+    for (int k = t; k < 2 * N; k += FT) sm.acc[0][k] = c1[k] - c0[k];
     fft_smem_init(sm, t);
     __syncthreads();
     fft_ext_product(
-        sm, G, g, t, lay, twf, twi, key_phase, [&](int c, int i) { return decomp_prep(sm.acc[c * N + i], g); },
+        sm, G, g, t, lay, twf, twi, key_phase, [&](int c, int i) { return decomp_prep(sm.acc[0][c * N + i], g); },
         [&](int c, int i, uint32_t v) { o[c * N + i] = c0[c * N + i] + v; });
   }
 }
@@ -1783,6 +1822,23 @@ static size_t pbs_ext_bytes(const hwb_params *p, int64_t B) {
 static size_t fft_acc_bytes(int64_t B) { return ((size_t)B * 2 * 2 * FH * 4 + 255) & ~(size_t)255; }
 // ladder steps per launch of the FFT ladder (L2 residency of the key slice)
 static int g_fft_segment = 64;
+// ciphertexts per CTA of the FFT PBS ladder (sharing each staged key slice)
+static int g_fft_cpb = 1;
+
+extern "C++" {
+template <int CPB>
+static int launch_pbs_fft(const void *bsk_fft, const uint32_t *lwe_in, const uint32_t *tv, int tv_per_item,
+                          uint32_t *ext, int L, const Gadget &g, DevState *st, uint32_t *acc, int s0, int s1,
+                          int64_t B, cudaStream_t s) {
+  const size_t smem = sizeof(FSmemT<CPB>);
+  int rc;
+  if ((rc = set_smem(blind_rotate_fft_kernel<true, CPB>, smem))) return rc;
+  blind_rotate_fft_kernel<true, CPB><<<(unsigned)((B + CPB - 1) / CPB), FT * CPB, smem, s>>>(
+      (const double2 *)bsk_fft, nullptr, nullptr, lwe_in, tv, tv_per_item, ext, L, g, st->fft_fwd, st->fft_inv, acc,
+      s0, s1, B);
+  return post_launch("blind_rotate_fft_kernel");
+}
+}  // extern "C++"
 
 static int check_fft(const hwb_params *p) {
   int rc = check_glwe(p);
@@ -1831,16 +1887,17 @@ int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, co
   uint8_t *ws = (uint8_t *)workspace;
   uint32_t *acc = (uint32_t *)ws;                               // [B][2][N] between segments
   uint32_t *ext = ksk_tc ? (uint32_t *)(ws + fft_acc_bytes(B)) : lwe_out;
-  const size_t smem = sizeof(FSmem);
-  if ((rc = set_smem(blind_rotate_fft_kernel<true>, smem))) return rc;
   const Gadget g = make_gadget(p->l, p->base_log);
   const int L = (int)p->n;
   for (int s0 = 0; s0 < L; s0 += g_fft_segment) {
     const int s1 = s0 + g_fft_segment < L ? s0 + g_fft_segment : L;
-    blind_rotate_fft_kernel<true><<<(unsigned)B, FT, smem, s>>>((const double2 *)bsk_fft, nullptr, nullptr, lwe_in, tv,
-                                                                tv_per_item, ext, L, g, st->fft_fwd, st->fft_inv,
-                                                                acc, s0, s1);
-    if ((rc = post_launch("blind_rotate_fft_kernel"))) return rc;
+    if (g_fft_cpb == 4)
+      rc = launch_pbs_fft<4>(bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st, acc, s0, s1, B, s);
+    else if (g_fft_cpb == 2)
+      rc = launch_pbs_fft<2>(bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st, acc, s0, s1, B, s);
+    else
+      rc = launch_pbs_fft<1>(bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st, acc, s0, s1, B, s);
+    if (rc) return rc;
   }
   if (!ksk_tc) return HWB_OK;
   return keyswitch_tc_launch(p, ksk_tc, ext, lwe_out, B,
@@ -1881,7 +1938,7 @@ int hwb_blind_rotate_fft(const hwb_params *p, const void *ggsw_fft, const int32_
   if ((rc = set_smem(blind_rotate_fft_kernel<false>, smem))) return rc;
   blind_rotate_fft_kernel<false><<<(unsigned)B, FT, smem, (cudaStream_t)stream>>>(
       (const double2 *)ggsw_fft, ggsw_idx, exps, nullptr, nullptr, 0, nullptr, L, make_gadget(p->l, p->base_log),
-      st->fft_fwd, st->fft_inv, acc, 0, L);
+      st->fft_fwd, st->fft_inv, acc, 0, L, B);
   return post_launch("blind_rotate_fft_kernel");
 }
 
@@ -1923,6 +1980,13 @@ size_t hwb_pbs_fft_workspace_bytes(const hwb_params *p, int64_t B, int with_keys
     bytes += pbs_ext_bytes(p, B) + ks_tc_digit_bytes(p, B);
   }
   return bytes;
+}
+
+int hwb_set_fft_group(int ciphertexts_per_cta) {
+  if (ciphertexts_per_cta != 1 && ciphertexts_per_cta != 2 && ciphertexts_per_cta != 4)
+    return fail(HWB_EINVAL, "ciphertexts per CTA must be 1, 2 or 4");
+  g_fft_cpb = ciphertexts_per_cta;
+  return HWB_OK;
 }
 
 int hwb_set_fft_segment(int steps) {

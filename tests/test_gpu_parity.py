@@ -281,11 +281,13 @@ def test_pbs_fft_ladder_vs_c_oracle(coracle, name):
     want = coracle.pbs(lwe, tvs, K.bsk, K.ksk, P)
     L = _lib.load()
     try:
-        for seg in (1, 7, 64):
+        for seg, group in ((1, 1), (7, 2), (64, 4), (64, 1)):
             _lib.check(L.hwb_set_fft_segment(seg))
+            _lib.check(L.hwb_set_fft_group(group))     # ragged: 37 items in CTAs of 1, 2 or 4
             assert_u32_equal(tfhe.pbs_batch(P, lwe, tvs, bsk, ksk, ladder="fft"), want)
     finally:
         _lib.check(L.hwb_set_fft_segment(64))
+        _lib.check(L.hwb_set_fft_group(1))
 
 
 def test_pbs_fft_ladder_extreme_key():

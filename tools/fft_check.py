@@ -31,6 +31,7 @@ def main(B=4096):
         ws = torch.empty(L.hwb_pbs_fft_workspace_bytes(ctypes.byref(cp), B, 0), dtype=torch.uint8, device="cuda")
         seg = int(sys.argv[2]) if len(sys.argv) > 2 else 64
         _lib.check(L.hwb_set_fft_segment(seg))
+        _lib.check(L.hwb_set_fft_group(int(sys.argv[3]) if len(sys.argv) > 3 else 1))
 
         def fft():
             _lib.check(L.hwb_pbs_fft(ctypes.byref(cp), tfhe._ptr(fk), None, tfhe._ptr(tv), 0, tfhe._ptr(lwe),
