@@ -151,6 +151,9 @@ static std::vector<double2> fft_twiddles(bool conj) {
   for (int k = 1; k < H; ++k) {
     const long double ang = acosl(-1.0L) * (long double)(E[k] / 2) / (long double)(2 * H);
     w[k] = make_double2((double)cosl(ang), (double)(conj ? -sinl(ang) : sinl(ang)));
+#if HWB_FFT_TAN
+    if (!conj) w[k] = make_double2((double)cosl(ang), (double)tanl(ang));   // tangent form (fft_ct)
+#endif
   }
   w[0] = make_double2(1.0, 0.0);
   return w;
@@ -785,10 +788,17 @@ __global__ void __launch_bounds__(FT) bsk_to_fft_kernel(const uint32_t *__restri
 
 // CPB ciphertexts per CTA (64 threads each) share one staged key slice per digit:
 // the slice is written into shared memory once and read CPB times.
+#ifndef HWB_FFT_DIG
+#define HWB_FFT_DIG 1
+#endif
+constexpr int FDR = 6;   // digit rows 2l staged per product (FFT path: l <= 3, base_log <= 8)
 template <int CPB>
 struct FSmemT {
   uint32_t acc[CPB][2 * 2 * FH];
   double2 scr[CPB][FH];
+#if HWB_FFT_DIG
+  uint4 dig[CPB][FDR * FT];       // the product's digits, biased bytes [row][thread][16 positions]
+#endif
   double2 key[2 * 2 * FC * FT];   // the current digit's key slice [c][h][j][t] (32 KB, TMA)
   uint64_t key_full;              // mbarrier: slice landed
 };
@@ -811,6 +821,35 @@ __device__ __forceinline__ void fft_ext_product(FSmemT<CPB> &sm, const double2 *
   constexpr uint32_t kSliceBytes = 2 * 2 * FC * FT * sizeof(double2);
   const int lv = (int)g.levels;
   const double dig_off = 4503599627370496.0 + (double)g.half;   // 2^52 + beta/2
+#if HWB_FFT_DIG
+  // The whole decomposition once per product: each prep word (rotation, difference,
+  // rounding) is formed once and its l digits, biased into [0, beta), are stored as
+  // bytes -- row r, thread t: 16 bytes, byte 2j + q for position t + 64 j + 512 q.
+  // Each thread reads back only its own slots, so no barrier is needed.
+  uint4 *dig = sm.dig[grp];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    uint32_t pw[2 * FC];
+#pragma unroll
+    for (int j = 0; j < FC; ++j) {
+      pw[2 * j] = prep(c, t + FT * j);
+      pw[2 * j + 1] = prep(c, t + FT * j + FH);
+    }
+    const uint32_t bmask = g.mask * 0x01010101u;
+#pragma unroll 1
+    for (int tt = 0; tt < lv; ++tt) {
+      const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
+      uint32_t wd[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const uint32_t lo = __byte_perm(pw[4 * m] >> sh, pw[4 * m + 1] >> sh, 0x0040);
+        const uint32_t hi = __byte_perm(pw[4 * m + 2] >> sh, pw[4 * m + 3] >> sh, 0x0040);
+        wd[m] = __byte_perm(lo, hi, 0x5410) & bmask;
+      }
+      dig[((c == 1 ? 0 : lv) + tt) * FT + t] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+    }
+  }
+#endif
   double2 Y[2][2][FC];
 #pragma unroll
   for (int c = 0; c < 2; ++c)
@@ -821,17 +860,28 @@ __device__ __forceinline__ void fft_ext_product(FSmemT<CPB> &sm, const double2 *
 #pragma unroll 1
   for (int r = 0; r < 2 * lv; ++r) {
     // digit order (hw/tfhe.py:290-298): rows 0..l-1 = digits of b, l..2l-1 of a
+    const double2 *gr = G + (size_t)r * (2 * 2 * FC * FT);
+    double2 x[FC];
+#if HWB_FFT_DIG
+    const uint4 dv = dig[r * FT + t];
+    const uint32_t dw[4] = {dv.x, dv.y, dv.z, dv.w};
+#pragma unroll
+    for (int j = 0; j < FC; ++j) {
+      const uint32_t w = dw[j >> 1], k = 2 * (j & 1);
+      x[j] = make_double2(u2d_minus(__byte_perm(w, 0, 0x4440 + k), dig_off),
+                          u2d_minus(__byte_perm(w, 0, 0x4441 + k), dig_off));
+    }
+#else
     const int comp = r < lv ? 1 : 0;
     const int tt = r < lv ? r : r - lv;
     const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
-    const double2 *gr = G + (size_t)r * (2 * 2 * FC * FT);
-    double2 x[FC];
 #pragma unroll
     for (int j = 0; j < FC; ++j) {
       const int i = t + FT * j;
       const uint32_t p0 = prep(comp, i), p1 = prep(comp, i + FH);
       x[j] = make_double2(u2d_minus((p0 >> sh) & g.mask, dig_off), u2d_minus((p1 >> sh) & g.mask, dig_off));
     }
+#endif
     auto stage_key = [&] {
       if (threadIdx.x == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1846,6 +1896,10 @@ static int check_fft(const hwb_params *p) {
   if (p->N != 2 * FH) return fail(HWB_EINVAL, "the FFT ladder supports N = 1024 only");
   // rounding exactness: |sum| < 2l N beta/2 2^15 and FFT error << 1/2
   if (p->l * (1u << p->base_log) >= (1u << 19)) return fail(HWB_EINVAL, "gadget too wide for the FFT ladder");
+#if HWB_FFT_DIG
+  // digits staged as bytes, 2l <= FDR rows (every BASELINE gadget at N = 1024)
+  if (p->base_log > 8 || 2 * p->l > (uint32_t)FDR) return fail(HWB_EINVAL, "the FFT ladder needs base_log <= 8, l <= 3");
+#endif
   return HWB_OK;
 }
 
