@@ -231,27 +231,66 @@ def _ev(stream=None):
     return e
 
 
+class _StageRing:
+    """Two device staging slots for the RGSW stacks of consecutive chunks, allocated
+    once per training call (two large blocks instead of one allocation per sample):
+    chunk k's host->device copy lands in slot k % 2 on the copy stream, and waits
+    for the GPU to have consumed chunk k-2 from that slot (its table conversion)."""
+
+    def __init__(self, words: int):
+        dev = tfhe._device()
+        self.slots = [torch.empty(words, dtype=torch.int32, device=dev) for _ in range(2)]
+        self.free = [None, None]        # main-stream event: the slot's last reader is done
+        self.k = 0
+
+    def take(self) -> int:
+        slot = self.k % 2
+        self.k += 1
+        return slot
+
+
 class _Staged:
     """A chunk's host RGSW stacks copied to the device on a side stream, so the
     H2D of chunk k+1 overlaps the ladders of chunk k (pinned host tensors)."""
 
     _copy_stream = None
 
-    def __init__(self, samples: list[EncryptedSample]):
+    def __init__(self, samples: list[EncryptedSample], ring: _StageRing | None = None):
         self.samples = samples
         self.dev: list | None = None
         self.event = None
+        self.ring, self.slot = ring, None
         if not any(isinstance(s.rgsw, np.ndarray) or (isinstance(s.rgsw, torch.Tensor) and not s.rgsw.is_cuda)
                    for s in samples):
             return                                          # already device-resident
         if _Staged._copy_stream is None:
             _Staged._copy_stream = torch.cuda.Stream(device=tfhe._device())
         cs = _Staged._copy_stream
-        cs.wait_stream(torch.cuda.current_stream())         # buffers freed on the main stream
+        need = sum(int(np.prod(s.rgsw.shape)) for s in samples)
+        if ring is not None and need <= ring.slots[0].numel():
+            self.slot = ring.take()
+            if ring.free[self.slot] is not None:
+                cs.wait_event(ring.free[self.slot])         # chunk k-2 has left the slot
+        else:
+            self.ring = None
+            cs.wait_stream(torch.cuda.current_stream())     # buffers freed on the main stream
         with torch.cuda.stream(cs):
             if _TRACE is not None:
                 _TRACE.append(("copy_start", _ev(cs)))
-            self.dev = [tfhe.to_device(s.rgsw) for s in samples]
+            if self.ring is None:
+                self.dev = [tfhe.to_device(s.rgsw) for s in samples]
+            else:
+                buf, off, self.dev = ring.slots[self.slot], 0, []
+                for smp in samples:
+                    src = smp.rgsw
+                    if isinstance(src, np.ndarray):
+                        src = torch.from_numpy(np.ascontiguousarray(src, dtype=np.uint32).view(np.int32))
+                    src = src.view(torch.int32) if src.dtype == torch.uint32 else src
+                    n = src.numel()
+                    dst = buf[off: off + n].view(src.shape)
+                    dst.copy_(src, non_blocking=True)
+                    self.dev.append(dst)
+                    off += n
             self.event = torch.cuda.Event(enable_timing=_TRACE is not None)
             self.event.record(cs)
             if _TRACE is not None:
@@ -262,9 +301,17 @@ class _Staged:
             return [tfhe.to_device(s.rgsw) for s in self.samples]
         main = torch.cuda.current_stream()
         main.wait_event(self.event)
-        for t in self.dev:
-            t.record_stream(main)                           # allocator: used on the main stream
+        if self.ring is None:
+            for t in self.dev:
+                t.record_stream(main)                       # allocator: used on the main stream
         return self.dev
+
+    def release(self):
+        """The main stream has enqueued the last reader of this chunk's slot."""
+        if self.ring is not None:
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream())
+            self.ring.free[self.slot] = ev
 
 
 def _use_fft(params: HeParams, ladder: str) -> bool:
@@ -278,29 +325,44 @@ def _use_fft(params: HeParams, ladder: str) -> bool:
     return ok and ladder != "ntt"
 
 
+def _table_bytes(params: HeParams, rows: int, ladder: str = "auto") -> int:
+    """Device bytes of a GGSW table of `rows` RGSW ciphertexts (FFT or NTT domain)."""
+    cp = _lib_params(params)
+    L = tfhe._lib.load()
+    per = L.hwb_ggsw_fft_bytes(cp) if _use_fft(params, ladder) else L.hwb_ggsw_ntt_words(cp) * 4
+    return rows * int(per)
+
+
 def _stack_table(params: HeParams, samples: list[EncryptedSample], staged: _Staged | None = None,
-                 ladder: str = "auto"):
+                 ladder: str = "auto", arena: torch.Tensor | None = None):
     """One device GGSW table (NTT or FFT domain) holding every sample's RGSW rows,
-    each sample transformed straight into its slice (no stacking copy)."""
+    each sample transformed straight into its slice (no stacking copy).  `arena`
+    (uint8, reused across a training call's chunks) holds the table when given."""
     import ctypes
     cp = _lib_params(params)
     L = tfhe._lib.load()
     rows = [int(s.rgsw.shape[0]) for s in samples]
     fft = _use_fft(params, ladder)
+    nbytes = L.hwb_ggsw_fft_bytes(cp) if fft else L.hwb_ggsw_ntt_words(cp) * 4
+    total = sum(rows) * nbytes
+    if arena is not None and arena.numel() >= total:
+        raw = arena[:total]
+    else:
+        raw = torch.empty(total, dtype=torch.uint8, device=tfhe._device())
     if fft:
-        nbytes = L.hwb_ggsw_fft_bytes(cp)
-        table = torch.empty(sum(rows) * nbytes, dtype=torch.uint8, device=tfhe._device())
+        table = raw
         conv = L.hwb_ggsw_to_fft
     else:
-        nbytes = L.hwb_ggsw_ntt_words(cp) * 4
-        table = torch.empty((sum(rows), nbytes // 4), dtype=torch.int32, device=tfhe._device())
+        table = raw.view(torch.int32).view(sum(rows), nbytes // 4)
         conv = L.hwb_ggsw_to_ntt
-    srcs = (staged or _Staged(samples)).tensors()
+    st = staged or _Staged(samples)
+    srcs = st.tensors()
     off = 0
     for src, r in zip(srcs, rows):
         dst = ctypes.c_void_p(table.data_ptr() + off * nbytes)
         tfhe._lib.check(conv(cp, tfhe._ptr(src), dst, r, tfhe._stream()))
         off += r
+    st.release()
     return tfhe.GgswFft(params, table, sum(rows)) if fft else tfhe.GgswNtt(params, table)
 
 
@@ -334,9 +396,17 @@ def he_train(samples: Iterable[EncryptedSample], geometry: WisardGeometry, param
                            for i in range(batch)], dtype=np.int64).reshape(batch, geometry.label_bits)
     d_codes, d_labels = lut._upload_i32([all_codes, all_labels], tfhe._device())
     _payload(params)
+    # one table buffer for every chunk (the ladders of chunk k precede chunk k+1's
+    # conversion on the same stream) and, for host samples, two staging slots
+    # (sized by the first chunk, the largest)
+    arena = ring = None
 
     def run(chunk: list[EncryptedSample], staged: _Staged):
-        table = _stack_table(params, chunk, staged, ladder)
+        nonlocal arena
+        if arena is None:
+            nbytes = _table_bytes(params, sum(int(x.rgsw.shape[0]) for x in chunk), ladder)
+            arena = torch.empty(nbytes, dtype=torch.uint8, device=tfhe._device())
+        table = _stack_table(params, chunk, staged, ladder, arena)
         I = len(chunk)
         rows = lut.ivp_codes(params, all_codes[: I * k0], table, _payload(params),
                              d_codes[: I * k0])                              # (I*k0, k1, 2, N)
@@ -351,7 +421,13 @@ def he_train(samples: Iterable[EncryptedSample], geometry: WisardGeometry, param
 
     # one chunk in flight: chunk k+1's H2D is enqueued on the copy stream before
     # chunk k's ladders, so host->device traffic overlaps the GPU work
-    for chunk, staged in _chunks_staged(samples, batch, check):
+    def stage(chunk):
+        nonlocal ring
+        if ring is None and any(not (isinstance(x.rgsw, torch.Tensor) and x.rgsw.is_cuda) for x in chunk):
+            ring = _StageRing(sum(int(np.prod(x.rgsw.shape)) for x in chunk))
+        return _Staged(chunk, ring)
+
+    for chunk, staged in _chunks_staged(samples, batch, check, stage):
         if _TRACE is not None:
             _TRACE.append(("run_start", _ev()))
         run(chunk, staged)
@@ -360,8 +436,9 @@ def he_train(samples: Iterable[EncryptedSample], geometry: WisardGeometry, param
     return model
 
 
-def _chunks_staged(samples: Iterable[EncryptedSample], batch: int, check=None):
+def _chunks_staged(samples: Iterable[EncryptedSample], batch: int, check=None, stage=None):
     """Yield (chunk, staged) with the next chunk's H2D already enqueued."""
+    stage = stage or _Staged
     pending = None
     chunk: list[EncryptedSample] = []
     for sample in samples:
@@ -369,13 +446,13 @@ def _chunks_staged(samples: Iterable[EncryptedSample], batch: int, check=None):
             check(sample)
         chunk.append(sample)
         if len(chunk) == batch:
-            nxt = (chunk, _Staged(chunk))
+            nxt = (chunk, stage(chunk))
             chunk = []
             if pending is not None:
                 yield pending
             pending = nxt
     if chunk:
-        nxt = (chunk, _Staged(chunk))
+        nxt = (chunk, stage(chunk))
         if pending is not None:
             yield pending
         pending = nxt

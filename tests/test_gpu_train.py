@@ -51,6 +51,22 @@ def test_he_train_matches_reference(name, batch, ladder):
     assert np.array_equal(cc.counts, g["class_counts"])
 
 
+@pytest.mark.parametrize("host", ["numpy", "pinned"])
+def test_he_train_from_host_stacks_staged(host):
+    """Host RGSW stacks go through the two-slot staging ring (chunks of 1 sample,
+    so every slot is reused several times): bit-identical to device-resident input."""
+    name = sorted(TRAIN_CASES)[0]
+    g = golden(f"{name}.npz")
+    P, s1, bits, labels, smp, geom = samples_of(name, device=False)
+    if host == "pinned":
+        smp = [hewnn.EncryptedSample(P, torch.from_numpy(x.rgsw.view(np.int32)).pin_memory(), x.s, x.label_bits)
+               for x in smp]
+    for batch in (1, 2):
+        model = hewnn.he_train(smp, geom, P, batch=batch)
+        assert sha(tfhe.to_host(model.rams)) == str(g["sha_rams"])
+        assert_u32_equal(tfhe.to_host(model.counts_ct), g["counts_ct"])
+
+
 def test_continuous_training_and_merge():
     name = "train_cfg1"
     P, s1, bits, labels, smp, geom = samples_of(name)
