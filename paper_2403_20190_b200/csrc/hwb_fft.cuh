@@ -28,7 +28,10 @@ constexpr int FT = 64;        // threads per transform
 constexpr int FC = FH / FT;   // complex values per thread
 using FGeo = Geo<FH, FT>;
 
-__constant__ double2 c_ftw[2][8];   // [forward / inverse (conjugate)][k], uniform A stages
+// uniform A-stage twiddles [row][forward / inverse (conjugate)][k]: row 0 = the
+// N = 1024 transform, rows 1 + g = half g of the N = 2048 transform (FFT2 below)
+__constant__ double2 c_ftw[3][2][8];
+__constant__ double2 c_fw0[2];   // FFT2 level-0 twiddle: [0] forward (cos, tan), [1] inverse (conjugate)
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 w) {
   return make_double2(fma(a.x, w.x, -a.y * w.y), fma(a.x, w.y, a.y * w.x));
@@ -60,12 +63,12 @@ __device__ __forceinline__ void fft_gs(double2 &X, double2 &Y, double2 w) {
 }
 
 template <bool FWD, int JB, bool UNIFORM, int MBASE, int SLOT>
-__device__ __forceinline__ void fft_stage(double2 (&x)[FC], int t, const double2 *__restrict__ tw) {
+__device__ __forceinline__ void fft_stage(double2 (&x)[FC], int t, const double2 *__restrict__ tw, int cg = 0) {
   constexpr int NBT = FC >> (JB + 1);
   constexpr int HALF = 1 << JB;
 #pragma unroll
   for (int u = 0; u < NBT; ++u) {
-    const double2 w = UNIFORM ? c_ftw[FWD ? 0 : 1][MBASE + u] : __ldg(&tw[(SLOT + u) * FT + t]);
+    const double2 w = UNIFORM ? c_ftw[cg][FWD ? 0 : 1][MBASE + u] : __ldg(&tw[(SLOT + u) * FT + t]);
 #pragma unroll
     for (int lo = 0; lo < HALF; ++lo) {
       const int j = (u << (JB + 1)) | lo;
@@ -125,45 +128,45 @@ struct NoHook {
 // natural (layout A) -> block order (layout B); per-thread twiddle slots as fwd_ntt
 template <typename F = NoHook>
 __device__ __forceinline__ void fwd_fft(double2 (&x)[FC], double2 *scr, const FLay &L, int t,
-                                        const double2 *__restrict__ tw, F &&hook = F(), int bar = 0) {
+                                        const double2 *__restrict__ tw, F &&hook = F(), int bar = 0, int cg = 0) {
   using G = FGeo;
   static_for<0, G::LOGN - G::T>([&](auto K) {
     constexpr int s = G::LOGN - 1 - decltype(K)::value;
-    fft_stage<true, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x, t, tw);
+    fft_stage<true, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x, t, tw, cg);
   });
   frelayout<LAY_A, LAY_M>(x, scr, L, hook, bar);
   static_for<0, G::T - G::LOGC>([&](auto K) {
     constexpr int s = G::T - 1 - decltype(K)::value;
     constexpr int slot = (1 << decltype(K)::value) - 1;
-    fft_stage<true, s - G::LO, false, 0, slot>(x, t, tw);
+    fft_stage<true, s - G::LO, false, 0, slot>(x, t, tw, cg);
   });
   frelayout<LAY_M, LAY_B>(x, scr, L, NoHook(), bar);
   static_for<0, G::B_TOP>([&](auto K) {
     constexpr int s = G::B_TOP - 1 - decltype(K)::value;
     constexpr int slot = G::M_SLOTS + (G::C >> G::B_TOP) * ((1 << decltype(K)::value) - 1);
-    fft_stage<true, s, false, 0, slot>(x, t, tw);
+    fft_stage<true, s, false, 0, slot>(x, t, tw, cg);
   });
 }
 
 // block order (layout B) -> natural (layout A), unscaled (1/H is in the key)
 __device__ __forceinline__ void inv_fft(double2 (&x)[FC], double2 *scr, const FLay &L, int t,
-                                        const double2 *__restrict__ tw, int bar = 0) {
+                                        const double2 *__restrict__ tw, int bar = 0, int cg = 0) {
   using G = FGeo;
   static_for<0, G::B_TOP>([&](auto K) {
     constexpr int s = decltype(K)::value;
     constexpr int slot = G::C - 2 * (G::C >> (s + 1));
-    fft_stage<false, s, false, 0, slot>(x, t, tw);
+    fft_stage<false, s, false, 0, slot>(x, t, tw, cg);
   });
   frelayout<LAY_B, LAY_M>(x, scr, L, NoHook(), bar);
   static_for<0, G::T - G::LOGC>([&](auto K) {
     constexpr int s = G::LOGC + decltype(K)::value;
     constexpr int slot = G::B_SLOTS + (1 << (G::T - G::LOGC)) - (1 << (G::T - s));
-    fft_stage<false, s - G::LO, false, 0, slot>(x, t, tw);
+    fft_stage<false, s - G::LO, false, 0, slot>(x, t, tw, cg);
   });
   frelayout<LAY_M, LAY_A>(x, scr, L, NoHook(), bar);
   static_for<0, G::LOGN - G::T>([&](auto K) {
     constexpr int s = G::T + decltype(K)::value;
-    fft_stage<false, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x, t, tw);
+    fft_stage<false, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x, t, tw, cg);
   });
 }
 
@@ -188,51 +191,51 @@ __device__ __forceinline__ void frelayout_k(double2 (*x)[FC], double2 *scr, cons
 // K independent forward transforms in lockstep (the two key halves of a GGSW row)
 template <int K>
 __device__ __forceinline__ void fwd_fft_k(double2 (*x)[FC], double2 *scr, const FLay &L, int t,
-                                          const double2 *__restrict__ tw) {
+                                          const double2 *__restrict__ tw, int cg = 0) {
   using G = FGeo;
   static_for<0, G::LOGN - G::T>([&](auto Q) {
     constexpr int s = G::LOGN - 1 - decltype(Q)::value;
 #pragma unroll
-    for (int k = 0; k < K; ++k) fft_stage<true, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x[k], t, tw);
+    for (int k = 0; k < K; ++k) fft_stage<true, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x[k], t, tw, cg);
   });
   frelayout_k<K, LAY_A, LAY_M>(x, scr, L);
   static_for<0, G::T - G::LOGC>([&](auto Q) {
     constexpr int s = G::T - 1 - decltype(Q)::value;
     constexpr int slot = (1 << decltype(Q)::value) - 1;
 #pragma unroll
-    for (int k = 0; k < K; ++k) fft_stage<true, s - G::LO, false, 0, slot>(x[k], t, tw);
+    for (int k = 0; k < K; ++k) fft_stage<true, s - G::LO, false, 0, slot>(x[k], t, tw, cg);
   });
   frelayout_k<K, LAY_M, LAY_B>(x, scr, L);
   static_for<0, G::B_TOP>([&](auto Q) {
     constexpr int s = G::B_TOP - 1 - decltype(Q)::value;
     constexpr int slot = G::M_SLOTS + (G::C >> G::B_TOP) * ((1 << decltype(Q)::value) - 1);
 #pragma unroll
-    for (int k = 0; k < K; ++k) fft_stage<true, s, false, 0, slot>(x[k], t, tw);
+    for (int k = 0; k < K; ++k) fft_stage<true, s, false, 0, slot>(x[k], t, tw, cg);
   });
 }
 
 template <int K>
 __device__ __forceinline__ void inv_fft_k(double2 (*x)[FC], double2 *scr, const FLay &L, int t,
-                                          const double2 *__restrict__ tw) {
+                                          const double2 *__restrict__ tw, int cg = 0) {
   using G = FGeo;
   static_for<0, G::B_TOP>([&](auto Q) {
     constexpr int s = decltype(Q)::value;
     constexpr int slot = G::C - 2 * (G::C >> (s + 1));
 #pragma unroll
-    for (int k = 0; k < K; ++k) fft_stage<false, s, false, 0, slot>(x[k], t, tw);
+    for (int k = 0; k < K; ++k) fft_stage<false, s, false, 0, slot>(x[k], t, tw, cg);
   });
   frelayout_k<K, LAY_B, LAY_M>(x, scr, L);
   static_for<0, G::T - G::LOGC>([&](auto Q) {
     constexpr int s = G::LOGC + decltype(Q)::value;
     constexpr int slot = G::B_SLOTS + (1 << (G::T - G::LOGC)) - (1 << (G::T - s));
 #pragma unroll
-    for (int k = 0; k < K; ++k) fft_stage<false, s - G::LO, false, 0, slot>(x[k], t, tw);
+    for (int k = 0; k < K; ++k) fft_stage<false, s - G::LO, false, 0, slot>(x[k], t, tw, cg);
   });
   frelayout_k<K, LAY_M, LAY_A>(x, scr, L);
   static_for<0, G::LOGN - G::T>([&](auto Q) {
     constexpr int s = G::T + decltype(Q)::value;
 #pragma unroll
-    for (int k = 0; k < K; ++k) fft_stage<false, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x[k], t, tw);
+    for (int k = 0; k < K; ++k) fft_stage<false, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x[k], t, tw, cg);
   });
 }
 

@@ -91,6 +91,7 @@ struct DevState {
   uint2 *lane_inv[2][2] = {};
   uint2 *lane_inv64[2] = {};    // N = 1024 inverse transform on 64 threads (latency ladder)
   double2 *fft_fwd = nullptr, *fft_inv = nullptr;   // FP64 FFT per-thread twiddles
+  double2 *fft2_fwd[2] = {}, *fft2_inv[2] = {};     // N = 2048: the sub-transform of half g
 };
 
 static std::mutex g_mu;
@@ -139,8 +140,7 @@ static std::vector<uint2> thread_table(const std::vector<uint32_t> &w, uint32_t 
 // FFT twiddles (hwb_fft.cuh): k = 2^level + m -> zeta^{E(level, m)/2}, zeta = e^{i pi/(2H)},
 // E(0, 0) = H and E(level+1, {2m, 2m+1}) = {E/2, E/2 + 2H} (mod 4H): the roots of the
 // factors of Y^H - i.  Computed in long double, rounded once to double.
-static std::vector<double2> fft_twiddles(bool conj) {
-  const int H = FH;
+static std::vector<double2> fft_twiddles(bool conj, int H = FH) {
   std::vector<long> E(2 * H, 0);
   E[1] = H;
   for (int k = 1; k < H; ++k) {
@@ -239,11 +239,35 @@ static int init_device(DevState **out) {
     cudaError_t e1 = cudaMalloc(&st.fft_fwd, fb), e2 = cudaMalloc(&st.fft_inv, fb);
     if (e1 == cudaSuccess) e1 = cudaMemcpy(st.fft_fwd, lf.data(), fb, cudaMemcpyHostToDevice);
     if (e2 == cudaSuccess) e2 = cudaMemcpy(st.fft_inv, li.data(), fb, cudaMemcpyHostToDevice);
-    double2 h_ftw[2][8];
+    double2 h_ftw[3][2][8];
     for (int k = 0; k < 8; ++k) {
-      h_ftw[0][k] = wf[k];
-      h_ftw[1][k] = wi[k];
+      h_ftw[0][0][k] = wf[k];
+      h_ftw[0][1][k] = wi[k];
     }
+    // N = 2048 (FFT2): the 1024-point folded transform's first stage (level 0,
+    // twiddle k = 1) is done by hand; half g is a 512-point transform whose local
+    // twiddle k' = 2^l' + m' is the full one at level l' + 1, block g 2^l' + m'
+    const std::vector<double2> wf2 = fft_twiddles(false, 2 * FH), wi2 = fft_twiddles(true, 2 * FH);
+    auto sub = [](const std::vector<double2> &w, int g, int k) {
+      if (k == 0) return w[0];
+      int lv = 0;
+      while ((2 << lv) <= k) ++lv;
+      return w[k + (1 + g) * (1 << lv)];
+    };
+    for (int g = 0; g < 2 && e1 == cudaSuccess && e2 == cudaSuccess; ++g) {
+      const std::vector<double2> gf = thread_table_of<FH, FT, double2>([&](int k) { return sub(wf2, g, k); }, true);
+      const std::vector<double2> gi = thread_table_of<FH, FT, double2>([&](int k) { return sub(wi2, g, k); }, false);
+      e1 = cudaMalloc(&st.fft2_fwd[g], fb);
+      e2 = cudaMalloc(&st.fft2_inv[g], fb);
+      if (e1 == cudaSuccess) e1 = cudaMemcpy(st.fft2_fwd[g], gf.data(), fb, cudaMemcpyHostToDevice);
+      if (e2 == cudaSuccess) e2 = cudaMemcpy(st.fft2_inv[g], gi.data(), fb, cudaMemcpyHostToDevice);
+      for (int k = 0; k < 8; ++k) {
+        h_ftw[1 + g][0][k] = sub(wf2, g, k);
+        h_ftw[1 + g][1][k] = sub(wi2, g, k);
+      }
+    }
+    const double2 w0[2] = {wf2[1], wi2[1]};   // level-0 twiddle (forward tangent form, inverse conjugate)
+    if (e1 == cudaSuccess && e2 == cudaSuccess) e1 = cudaMemcpyToSymbol(c_fw0, w0, sizeof(w0));
     if (e1 == cudaSuccess && e2 == cudaSuccess) e1 = cudaMemcpyToSymbol(c_ftw, h_ftw, sizeof(h_ftw));
     if (e1 != cudaSuccess || e2 != cudaSuccess) return fail(HWB_ECUDA, "FFT twiddle upload failed");
   }
@@ -1065,6 +1089,290 @@ __global__ void __launch_bounds__(FT, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// FP64 FFT ladder at N = 2048 (FFT2): the folded polynomial has H = 1024 points
+// (z_i = a_i + i a_{i+1024}, a polynomial mod Y^1024 - i).  Its first
+// Cooley-Tukey stage (level 0: z_k +/- w0 z_{k+512}, w0 = e^{i pi/4}) is formed
+// while the digits are read, after which half g is an independent 512-point
+// merged-twist transform -- the N = 1024 machinery on 64 threads, with the
+// twiddles of the subtree under block (1, g) (tables fft2_*[g], c_ftw row 1 + g).
+// One ciphertext per CTA of 128 threads (group g = half g).  The inverse runs the
+// two 512-point inverses, then the level-0 Gentleman-Sande stage across the
+// halves through shared memory.  Thread (g, t) owns folded points g 512 + t + 64 j,
+// i.e. coefficients g 512 + t + 64 j and + 1024 of the product.
+// Digits: l <= 2 rows per component, base_log <= 15 (signed 16-bit), biased
+// halfwords [row][j][g][t]: word g holds positions k + 512 (2g) (low) and
+// k + 512 (2g + 1) (high), k = t + 64 j.
+
+constexpr int F2R = 4;   // digit rows 2l staged per product (l <= 2)
+
+struct FSmem2 {
+  uint32_t acc[2 * 4 * FH];        // working ciphertext (a, b), N = 2048
+  double2 scr[2][FH];              // per-half transpose scratch
+  uint32_t dig[F2R * FC * 2 * FT]; // the product's digits (biased halfwords)
+  double2 key[2 * 2 * 2 * FC * FT];   // the digit's key slice [c][h][g][j][t] (64 KB, TMA)
+  uint64_t key_full;
+};
+
+// (X, Y) -> X + w0 Y (g = 0) or X - w0 Y (g = 1), w0 in tangent form
+__device__ __forceinline__ double2 fft2_first(double2 X, double2 Y, int grp) {
+  const double2 w = c_fw0[0];
+  const double ux = fma(-w.y, Y.y, Y.x), uy = fma(w.y, Y.x, Y.y);
+  const double c = grp ? -w.x : w.x;
+  return make_double2(fma(c, ux, X.x), fma(c, uy, X.y));
+}
+
+template <typename Prep, typename Sink>
+__device__ __forceinline__ void fft2_ext_product(FSmem2 &sm, const double2 *__restrict__ G, const Gadget &g,
+                                                 int grp, int t, const FLay &lay, const double2 *__restrict__ twf,
+                                                 const double2 *__restrict__ twi, uint32_t &key_phase, Prep &&prep,
+                                                 Sink &&sink) {
+  constexpr uint32_t kSliceBytes = 2 * 2 * 2 * FC * FT * sizeof(double2);
+  const int lv = (int)g.levels;
+  const double dig_off = 4503599627370496.0 + (double)g.half;   // 2^52 + beta/2
+  // the decomposition once per product: thread (grp, t) forms the prep words of
+  // positions k + 512 q, q = 2 grp + {0, 1}
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    uint32_t pw[2 * FC];
+#pragma unroll
+    for (int j = 0; j < FC; ++j) {
+      const int k = t + FT * j;
+      pw[2 * j] = prep(c, k + FH * (2 * grp));
+      pw[2 * j + 1] = prep(c, k + FH * (2 * grp + 1));
+    }
+#pragma unroll 1
+    for (int tt = 0; tt < lv; ++tt) {
+      const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
+      const int r = (c == 1 ? 0 : lv) + tt;
+#pragma unroll
+      for (int j = 0; j < FC; ++j)
+        sm.dig[((r * FC + j) * 2 + grp) * FT + t] = ((pw[2 * j] >> sh) & g.mask) | (((pw[2 * j + 1] >> sh) & g.mask) << 16);
+    }
+  }
+  __syncthreads();
+  double2 Y[2][2][FC];
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int j = 0; j < FC; ++j) Y[c][h][j] = make_double2(0.0, 0.0);
+#pragma unroll 1
+  for (int r = 0; r < 2 * lv; ++r) {
+    const double2 *gr = G + (size_t)r * (2 * 2 * 2 * FC * FT);
+    double2 x[FC];
+#pragma unroll
+    for (int j = 0; j < FC; ++j) {
+      const uint32_t w0 = sm.dig[((r * FC + j) * 2) * FT + t], w1 = sm.dig[((r * FC + j) * 2 + 1) * FT + t];
+      const double2 zk = make_double2(u2d_minus(w0 & 0xFFFFu, dig_off), u2d_minus(w1 & 0xFFFFu, dig_off));
+      const double2 zh = make_double2(u2d_minus(w0 >> 16, dig_off), u2d_minus(w1 >> 16, dig_off));
+      x[j] = fft2_first(zk, zh, grp);
+    }
+    auto stage_key = [&] {
+      if (threadIdx.x == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&sm.key_full, kSliceBytes);
+        bulk_g2s(sm.key, gr, kSliceBytes, &sm.key_full);
+      }
+    };
+    // CTA-wide barriers: the hook runs once both halves are past the previous MAC
+    fwd_fft(x, sm.scr[grp], lay, t, twf, stage_key, 0, 1 + grp);
+    mbar_wait(&sm.key_full, key_phase);
+    key_phase ^= 1u;
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int j = 0; j < FC; ++j) {
+          const double2 k = sm.key[(((c * 2 + h) * 2 + grp) * FC + j) * FT + t];
+          double2 &y = Y[c][h][j];
+          y.x = fma(x[j].x, k.x, fma(-x[j].y, k.y, y.x));
+          y.y = fma(x[j].x, k.y, fma(x[j].y, k.x, y.y));
+        }
+  }
+  __syncthreads();   // every thread has finished reading the last key slice
+  inv_fft_k<4>(&Y[0][0], sm.key + grp * 4 * FH, lay, t, twi, 1 + grp);
+  // level-0 Gentleman-Sande stage across the halves: (X, Y) -> (X + Y, (X - Y) conj(w0))
+  double2 *xb = sm.key;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int j = 0; j < FC; ++j) xb[((grp * 4 + q) * FC + j) * FT + t] = (&Y[0][0])[q][j];
+  __syncthreads();
+  const double2 wi = c_fw0[1];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int j = 0; j < FC; ++j) {
+      const double2 o = xb[(((1 - grp) * 4 + q) * FC + j) * FT + t];
+      double2 &y = (&Y[0][0])[q][j];
+      if (grp == 0)
+        y = make_double2(y.x + o.x, y.y + o.y);
+      else
+        y = cmul(make_double2(o.x - y.x, o.y - y.y), wi);
+    }
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int j = 0; j < FC; ++j) {
+      const int f = grp * FH + t + FT * j;   // folded point: coefficients f and f + 1024
+      sink(c, f, round_u32(Y[c][0][j].x) + (round_u32(Y[c][1][j].x) << 16));
+      sink(c, f + 2 * FH, round_u32(Y[c][0][j].y) + (round_u32(Y[c][1][j].y) << 16));
+    }
+}
+
+// BSK/GGSW polynomials [count][2048] u32 -> FFT2 domain [count][2 halves][2 g][FC][FT]
+// double2 (scaled 1/1024): 128 threads per polynomial, both key halves in lockstep.
+__global__ void __launch_bounds__(2 * FT) bsk_to_fft2_kernel(const uint32_t *__restrict__ in, double2 *out,
+                                                              const double2 *__restrict__ twf0,
+                                                              const double2 *__restrict__ twf1) {
+  __shared__ double2 scr[2][2 * FH];
+  const int grp = threadIdx.x / FT, t = threadIdx.x % FT;
+  const int64_t poly = blockIdx.x;
+  const uint32_t *a = in + poly * (4 * FH);
+  const FLay lay = make_flay(t);
+  double2 x[2][FC];
+#pragma unroll
+  for (int j = 0; j < FC; ++j) {
+    const int k = t + FT * j;
+    double lo[4], hi[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {   // positions k, k + 512, k + 1024, k + 1536
+      const int64_t gword = (int32_t)a[k + q * FH];
+      const int64_t l16 = ((gword + 32768) & 0xFFFF) - 32768;
+      lo[q] = (double)l16;
+      hi[q] = (double)((gword - l16) >> 16);
+    }
+    x[0][j] = fft2_first(make_double2(lo[0], lo[2]), make_double2(lo[1], lo[3]), grp);
+    x[1][j] = fft2_first(make_double2(hi[0], hi[2]), make_double2(hi[1], hi[3]), grp);
+  }
+  fwd_fft_k<2>(x, scr[grp], lay, t, grp ? twf1 : twf0, 1 + grp);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    double2 *o = out + (poly * 2 + h) * (2 * FC * FT) + grp * (FC * FT);
+#pragma unroll
+    for (int j = 0; j < FC; ++j)
+      o[j * FT + t] = make_double2(x[h][j].x * (1.0 / (2 * FH)), x[h][j].y * (1.0 / (2 * FH)));
+  }
+}
+
+// The CMUX ladder on the FFT2 path: as blind_rotate_fft_kernel (PBS: mod switch to
+// 2N = 4096, TV X^-b~, steps [s0, s1) per launch, extraction at the end; !PBS: the
+// per-item rotation ladders of vertical packing), one ciphertext per 128-thread CTA.
+template <bool PBS>
+__global__ void __launch_bounds__(2 * FT, 1)
+    blind_rotate_fft2_kernel(const double2 *__restrict__ ggsw, const int32_t *__restrict__ gidx,
+                             const int32_t *__restrict__ exps, const uint32_t *__restrict__ lwe_in,
+                             const uint32_t *__restrict__ tv, int tv_per_item, uint32_t *lwe_out, int L, Gadget g,
+                             const double2 *__restrict__ twf0, const double2 *__restrict__ twf1,
+                             const double2 *__restrict__ twi0, const double2 *__restrict__ twi1, uint32_t *acc_io,
+                             int s0, int s1, int64_t B) {
+  constexpr int N = 4 * FH;
+  constexpr int LOG2M = 12;
+  constexpr int NT = 2 * FT;
+  extern __shared__ uint4 smem_raw[];
+  FSmem2 &sm = *reinterpret_cast<FSmem2 *>(smem_raw);
+  const int tid = threadIdx.x, grp = tid / FT, t = tid % FT;
+  const int64_t b = blockIdx.x;
+  uint32_t *acc = sm.acc;
+  const FLay lay = make_flay(t);
+  const double2 *twf = grp ? twf1 : twf0, *twi = grp ? twi1 : twi0;
+  const uint32_t *row = PBS ? lwe_in + b * (int64_t)(L + 1) : nullptr;
+  if (PBS && s0 == 0) {
+    const int bt = mod_switch(row[L], LOG2M);
+    const uint32_t *tp = tv + (tv_per_item ? b * 2 * N : 0);
+    const int e = (2 * N - bt) & (2 * N - 1);   // X^-b~
+    for (int k = tid; k < 2 * N; k += NT) {
+      const int c = k >= N, i = k & (N - 1);
+      acc[k] = rot_read<N>(tp + c * N, i, e);
+    }
+  } else {
+    for (int k = tid; k < 2 * N; k += NT) acc[k] = acc_io[b * 2 * N + k];
+  }
+  if (tid == 0) {
+    mbar_init(&sm.key_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t key_phase = 0;
+  const size_t ggsw_f = (size_t)2 * g.levels * 2 * 2 * 2 * FC * FT;   // double2 per GGSW
+#pragma unroll 1
+  for (int s = s0; s < s1; ++s) {
+    int e, gi = s;
+    if (PBS) {
+      e = mod_switch(row[s], LOG2M);   // X^{a~_s}
+    } else {
+      e = (int)((-(int64_t)exps[b * L + s]) % (2 * N));
+      if (e < 0) e += 2 * N;
+      if (gidx) gi = gidx[b * L + s];
+    }
+    if (e == 0 || gi < 0) continue;
+    fft2_ext_product(
+        sm, ggsw + (size_t)gi * ggsw_f, g, grp, t, lay, twf, twi, key_phase,
+        [&](int c, int i) {   // digits of (acc X^e - acc), straight from the accumulator
+          const uint32_t *ac = acc + c * N;
+          return decomp_prep(rot_read<N>(ac, i, e) - ac[i], g);
+        },
+        [&](int c, int i, uint32_t v) { acc[c * N + i] += v; });
+    __syncthreads();
+  }
+  if (!PBS || s1 < L) {
+    for (int k = tid; k < 2 * N; k += NT) acc_io[b * 2 * N + k] = acc[k];
+    return;
+  }
+  uint32_t *o = lwe_out + b * (int64_t)(N + 1);
+  for (int k = tid; k < N; k += NT) o[k] = k == 0 ? acc[0] : 0u - acc[N - k];
+  if (tid == 0) o[N] = acc[N];
+}
+
+// One vertical-packing tree level on the FFT2 path (level_fft_kernel at N = 2048).
+template <int MODE>
+__global__ void __launch_bounds__(2 * FT, 1)
+    level_fft2_kernel(const double2 *__restrict__ ggsw, const int32_t *__restrict__ gidx,
+                      const uint32_t *__restrict__ in, uint32_t *out, int m, Gadget g,
+                      const double2 *__restrict__ twf0, const double2 *__restrict__ twf1,
+                      const double2 *__restrict__ twi0, const double2 *__restrict__ twi1) {
+  constexpr int N = 4 * FH;
+  constexpr int NT = 2 * FT;
+  extern __shared__ uint4 smem_raw[];
+  FSmem2 &sm = *reinterpret_cast<FSmem2 *>(smem_raw);
+  const int64_t b = blockIdx.x, item = b / m, sub = b % m;
+  const int tid = threadIdx.x, grp = tid / FT, t = tid % FT;
+  const FLay lay = make_flay(t);
+  const double2 *twf = grp ? twf1 : twf0, *twi = grp ? twi1 : twi0;
+  const size_t ggsw_f = (size_t)2 * g.levels * 2 * 2 * 2 * FC * FT;
+  const double2 *G = ggsw + (size_t)gidx[item] * ggsw_f;
+  uint32_t key_phase = 0;
+  if (tid == 0) {
+    mbar_init(&sm.key_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (MODE == MODE_IVP_LEVEL) {
+    // CDEMUX (hw/lut.py:113-119, 294-313): hi = C (*) d, lo = d - hi
+    const uint32_t *d = in + (item * m + sub) * 2 * N;
+    uint32_t *o_lo = out + (item * 2 * m + sub) * 2 * N, *o_hi = out + (item * 2 * m + m + sub) * 2 * N;
+    for (int k = tid; k < 2 * N; k += NT) sm.acc[k] = d[k];
+    __syncthreads();
+    fft2_ext_product(
+        sm, G, g, grp, t, lay, twf, twi, key_phase, [&](int c, int i) { return decomp_prep(sm.acc[c * N + i], g); },
+        [&](int c, int i, uint32_t v) {
+          o_hi[c * N + i] = v;
+          o_lo[c * N + i] = sm.acc[c * N + i] - v;
+        });
+  } else {
+    // CMUX (hw/lut.py:130-136, 233-247): next = c0 + C (*) (c1 - c0)
+    const uint32_t *c0 = in + (item * 2 * m + sub) * 2 * N, *c1 = in + (item * 2 * m + m + sub) * 2 * N;
+    uint32_t *o = out + (item * m + sub) * 2 * N;
+    for (int k = tid; k < 2 * N; k += NT) sm.acc[k] = c1[k] - c0[k];
+    __syncthreads();
+    fft2_ext_product(
+        sm, G, g, grp, t, lay, twf, twi, key_phase, [&](int c, int i) { return decomp_prep(sm.acc[c * N + i], g); },
+        [&](int c, int i, uint32_t v) { o[c * N + i] = c0[c * N + i] + v; });
+  }
+}
+
 template <int N>
 __global__ void __launch_bounds__(Cfg<N>::THREADS) ggsw_to_ntt_kernel(const uint32_t *__restrict__ in,
                                                                       uint32_t *out, Tw tw) {
@@ -1869,7 +2177,7 @@ static size_t pbs_ext_bytes(const hwb_params *p, int64_t B) {
   return ((sizeof(uint32_t) * (size_t)B * (p->N + 1)) + 255) & ~(size_t)255;
 }
 
-static size_t fft_acc_bytes(int64_t B) { return ((size_t)B * 2 * 2 * FH * 4 + 255) & ~(size_t)255; }
+static size_t fft_acc_bytes(const hwb_params *p, int64_t B) { return ((size_t)B * 2 * p->N * 4 + 255) & ~(size_t)255; }
 // ladder steps per launch of the FFT ladder (L2 residency of the key slice)
 static int g_fft_segment = 64;
 // ciphertexts per CTA of the FFT PBS ladder (sharing each staged key slice)
@@ -1893,7 +2201,14 @@ static int launch_pbs_fft(const void *bsk_fft, const uint32_t *lwe_in, const uin
 static int check_fft(const hwb_params *p) {
   int rc = check_glwe(p);
   if (rc) return rc;
-  if (p->N != 2 * FH) return fail(HWB_EINVAL, "the FFT ladder supports N = 1024 only");
+  if (p->N == 4 * FH) {
+    // FFT2: int16 digits, 2l <= F2R rows; exactness as at N = 1024 (|sum| < 2^37,
+    // FFT error ~2^-12 for l 2^base_log <= 2^11)
+    if (2 * p->l > (uint32_t)F2R || p->base_log > 15 || p->l * (1u << p->base_log) > (1u << 11))
+      return fail(HWB_EINVAL, "the N = 2048 FFT ladder needs l <= 2 and l * 2^base_log <= 2^11");
+    return HWB_OK;
+  }
+  if (p->N != 2 * FH) return fail(HWB_EINVAL, "the FFT ladder supports N = 1024 and 2048");
   // rounding exactness: |sum| < 2l N beta/2 2^15 and FFT error << 1/2
   if (p->l * (1u << p->base_log) >= (1u << 19)) return fail(HWB_EINVAL, "gadget too wide for the FFT ladder");
 #if HWB_FFT_DIG
@@ -1905,7 +2220,17 @@ static int check_fft(const hwb_params *p) {
 
 size_t hwb_bsk_fft_bytes(const hwb_params *p) {
   if (!p || check_fft(p)) return 0;
-  return (size_t)p->n * 2 * p->l * 2 * 2 * FH * sizeof(double2);
+  return (size_t)p->n * 2 * p->l * 2 * 2 * (p->N / 2) * sizeof(double2);
+}
+
+static int launch_to_fft(const hwb_params *p, const uint32_t *in, void *out, int64_t polys, DevState *st,
+                         cudaStream_t s) {
+  if (p->N == 4 * FH) {
+    bsk_to_fft2_kernel<<<(unsigned)polys, 2 * FT, 0, s>>>(in, (double2 *)out, st->fft2_fwd[0], st->fft2_fwd[1]);
+    return post_launch("bsk_to_fft2_kernel");
+  }
+  bsk_to_fft_kernel<<<(unsigned)polys, FT, 0, s>>>(in, (double2 *)out, st->fft_fwd);
+  return post_launch("bsk_to_fft_kernel");
 }
 
 int hwb_bsk_to_fft(const hwb_params *p, const uint32_t *bsk, void *bsk_fft, void *stream) {
@@ -1917,8 +2242,7 @@ int hwb_bsk_to_fft(const hwb_params *p, const uint32_t *bsk, void *bsk_fft, void
   DevState *st;
   if ((rc = init_device(&st))) return rc;
   const int64_t polys = (int64_t)p->n * 2 * p->l * 2;
-  bsk_to_fft_kernel<<<(unsigned)polys, FT, 0, (cudaStream_t)stream>>>(bsk, (double2 *)bsk_fft, st->fft_fwd);
-  return post_launch("bsk_to_fft_kernel");
+  return launch_to_fft(p, bsk, bsk_fft, polys, st, (cudaStream_t)stream);
 }
 
 int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, const uint32_t *tv,
@@ -1940,12 +2264,19 @@ int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, co
   cudaStream_t s = (cudaStream_t)stream;
   uint8_t *ws = (uint8_t *)workspace;
   uint32_t *acc = (uint32_t *)ws;                               // [B][2][N] between segments
-  uint32_t *ext = ksk_tc ? (uint32_t *)(ws + fft_acc_bytes(B)) : lwe_out;
+  uint32_t *ext = ksk_tc ? (uint32_t *)(ws + fft_acc_bytes(p, B)) : lwe_out;
   const Gadget g = make_gadget(p->l, p->base_log);
   const int L = (int)p->n;
   for (int s0 = 0; s0 < L; s0 += g_fft_segment) {
     const int s1 = s0 + g_fft_segment < L ? s0 + g_fft_segment : L;
-    if (g_fft_cpb == 4)
+    if (p->N == 4 * FH) {
+      const size_t smem = sizeof(FSmem2);
+      if ((rc = set_smem(blind_rotate_fft2_kernel<true>, smem))) return rc;
+      blind_rotate_fft2_kernel<true><<<(unsigned)B, 2 * FT, smem, s>>>(
+          (const double2 *)bsk_fft, nullptr, nullptr, lwe_in, tv, tv_per_item, ext, L, g, st->fft2_fwd[0],
+          st->fft2_fwd[1], st->fft2_inv[0], st->fft2_inv[1], acc, s0, s1, B);
+      rc = post_launch("blind_rotate_fft2_kernel");
+    } else if (g_fft_cpb == 4)
       rc = launch_pbs_fft<4>(bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st, acc, s0, s1, B, s);
     else if (g_fft_cpb == 2)
       rc = launch_pbs_fft<2>(bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st, acc, s0, s1, B, s);
@@ -1955,12 +2286,12 @@ int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, co
   }
   if (!ksk_tc) return HWB_OK;
   return keyswitch_tc_launch(p, ksk_tc, ext, lwe_out, B,
-                             ws + fft_acc_bytes(B) + pbs_ext_bytes(p, B), s);
+                             ws + fft_acc_bytes(p, B) + pbs_ext_bytes(p, B), s);
 }
 
 size_t hwb_ggsw_fft_bytes(const hwb_params *p) {
   if (!p || check_fft(p)) return 0;
-  return (size_t)2 * p->l * 2 * 2 * FH * sizeof(double2);
+  return (size_t)2 * p->l * 2 * 2 * (p->N / 2) * sizeof(double2);
 }
 
 int hwb_ggsw_to_fft(const hwb_params *p, const uint32_t *ggsw, void *ggsw_fft, int64_t count, void *stream) {
@@ -1974,8 +2305,7 @@ int hwb_ggsw_to_fft(const hwb_params *p, const uint32_t *ggsw, void *ggsw_fft, i
   if (polys > 0x7FFFFFFF) return fail(HWB_EINVAL, "too many GGSWs");
   DevState *st;
   if ((rc = init_device(&st))) return rc;
-  bsk_to_fft_kernel<<<(unsigned)polys, FT, 0, (cudaStream_t)stream>>>(ggsw, (double2 *)ggsw_fft, st->fft_fwd);
-  return post_launch("bsk_to_fft_kernel");
+  return launch_to_fft(p, ggsw, ggsw_fft, polys, st, (cudaStream_t)stream);
 }
 
 int hwb_blind_rotate_fft(const hwb_params *p, const void *ggsw_fft, const int32_t *ggsw_idx, const int32_t *exps,
@@ -1988,6 +2318,14 @@ int hwb_blind_rotate_fft(const hwb_params *p, const void *ggsw_fft, const int32_
   if (!ggsw_fft || !exps || !acc) return fail(HWB_EINVAL, "null pointer");
   DevState *st;
   if ((rc = init_device(&st))) return rc;
+  if (p->N == 4 * FH) {
+    const size_t smem = sizeof(FSmem2);
+    if ((rc = set_smem(blind_rotate_fft2_kernel<false>, smem))) return rc;
+    blind_rotate_fft2_kernel<false><<<(unsigned)B, 2 * FT, smem, (cudaStream_t)stream>>>(
+        (const double2 *)ggsw_fft, ggsw_idx, exps, nullptr, nullptr, 0, nullptr, L, make_gadget(p->l, p->base_log),
+        st->fft2_fwd[0], st->fft2_fwd[1], st->fft2_inv[0], st->fft2_inv[1], acc, 0, L, B);
+    return post_launch("blind_rotate_fft2_kernel");
+  }
   const size_t smem = sizeof(FSmem);
   if ((rc = set_smem(blind_rotate_fft_kernel<false>, smem))) return rc;
   blind_rotate_fft_kernel<false><<<(unsigned)B, FT, smem, (cudaStream_t)stream>>>(
@@ -2008,6 +2346,14 @@ static int level_fft(const hwb_params *p, const void *ggsw_fft, const int32_t *g
   if (!ggsw_fft || !ggsw_idx || !cur || !next) return fail(HWB_EINVAL, "null pointer");
   DevState *st;
   if ((rc = init_device(&st))) return rc;
+  if (p->N == 4 * FH) {
+    const size_t smem = sizeof(FSmem2);
+    if ((rc = set_smem(level_fft2_kernel<MODE>, smem))) return rc;
+    level_fft2_kernel<MODE><<<(unsigned)(B * m), 2 * FT, smem, (cudaStream_t)stream>>>(
+        (const double2 *)ggsw_fft, ggsw_idx, cur, next, m, make_gadget(p->l, p->base_log), st->fft2_fwd[0],
+        st->fft2_fwd[1], st->fft2_inv[0], st->fft2_inv[1]);
+    return post_launch("level_fft2_kernel");
+  }
   const size_t smem = sizeof(FSmem);
   if ((rc = set_smem(level_fft_kernel<MODE>, smem))) return rc;
   level_fft_kernel<MODE><<<(unsigned)(B * m), FT, smem, (cudaStream_t)stream>>>(
@@ -2028,7 +2374,7 @@ int hwb_vp_level_fft(const hwb_params *p, const void *ggsw_fft, const int32_t *g
 
 size_t hwb_pbs_fft_workspace_bytes(const hwb_params *p, int64_t B, int with_keyswitch) {
   if (!p || B <= 0 || check_fft(p)) return 0;
-  size_t bytes = fft_acc_bytes(B);
+  size_t bytes = fft_acc_bytes(p, B);
   if (with_keyswitch) {
     if (check_ks_tc(p)) return 0;
     bytes += pbs_ext_bytes(p, B) + ks_tc_digit_bytes(p, B);

@@ -316,12 +316,12 @@ class _Staged:
 
 def _use_fft(params: HeParams, ladder: str) -> bool:
     """Vertical-packing ladders on the FP64 FFT path ("auto": wherever it applies,
-    N = 1024) or the two-prime NTT path; both are bit-identical."""
+    N = 1024 and 2048) or the two-prime NTT path; both are bit-identical."""
     if ladder not in ("auto", "fft", "ntt"):
         raise TfheError(f"unknown ladder {ladder!r}")
     ok = tfhe.ggsw_fft_bytes(params) > 0
     if ladder == "fft" and not ok:
-        raise TfheError("the FFT ladder needs N = 1024")
+        raise TfheError("the FFT ladder does not apply to these parameters (N = 1024 or 2048, narrow gadgets)")
     return ok and ladder != "ntt"
 
 

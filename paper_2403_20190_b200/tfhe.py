@@ -183,7 +183,7 @@ class GgswNtt:
 class GgswFft:
     """Device-resident FFT-domain GGSWs (hwb_ggsw_to_fft): `count` GGSWs of
     hwb_ggsw_fft_bytes each -- the spectra of the signed 16-bit halves of every key
-    polynomial, consumed by the FP64 FFT ladders (N = 1024)."""
+    polynomial, consumed by the FP64 FFT ladders (N = 1024 and 2048)."""
 
     params: HeParams
     data: torch.Tensor       # uint8, count * ggsw_bytes
@@ -203,7 +203,7 @@ def rgsw_to_fft(params: HeParams, ggsw) -> GgswFft:
         raise TfheError(f"GGSW batch must be (count, {2 * params.gadget.levels}, 2, {params.n})")
     nb = ggsw_fft_bytes(params)
     if nb == 0:
-        raise TfheError("FFT-domain GGSWs need N = 1024")
+        raise TfheError("no FFT-domain GGSWs for these parameters (N = 1024 or 2048, narrow gadgets)")
     out = torch.empty(t.shape[0] * nb, dtype=torch.uint8, device=t.device)
     cp = _lib.c_params(params)
     _lib.check(_lib.load().hwb_ggsw_to_fft(ctypes.byref(cp), _ptr(t), _ptr(out), t.shape[0], _stream()))
@@ -227,7 +227,7 @@ class RgswCiphertext:
 @dataclass
 class BootstrapKey:
     """RGSW_{S1}(s0_i) for i < n, resident on the device in the NTT domain and,
-    where the FP64 FFT ladder applies (N = 1024), as the FFT spectra of its signed
+    where the FP64 FFT ladder applies (N = 1024 and 2048), as the FFT spectra of its signed
     16-bit key halves (hwb_bsk_to_fft)."""
 
     params: HeParams
@@ -830,7 +830,7 @@ def _use_fft_ladder(bsk: BootstrapKey, B: int, ladder: str) -> bool:
         return False
     if bsk.fft is None:
         if ladder == "fft":
-            raise TfheError("no FFT bootstrapping key for these parameters (N = 1024 only)")
+            raise TfheError("no FFT bootstrapping key for these parameters (N = 1024 or 2048, narrow gadgets)")
         return False
     return ladder == "fft" or B > torch.cuda.get_device_properties(bsk.fft.device).multi_processor_count
 

@@ -242,7 +242,7 @@ def test_pbs_golden(name, variant, ladder):
     for engine in ("tc", "simt"):
         out = tfhe.pbs_batch(P, g["lwe_in"], g["tv"], bsk, ksk, engine=engine)
         assert_u32_equal(out, g["lwe_out"])
-    if bsk.fft is not None:                       # FP64 FFT ladder (N = 1024)
+    if bsk.fft is not None:                       # FP64 FFT ladder (N = 1024, 2048)
         assert_u32_equal(tfhe.pbs_batch(P, g["lwe_in"], g["tv"], bsk, None, ladder="fft"), g["extracted"])
         for engine in ("tc", "simt"):
             out = tfhe.pbs_batch(P, g["lwe_in"], g["tv"], bsk, ksk, engine=engine, ladder="fft")
@@ -267,7 +267,7 @@ def test_pbs_batch_vs_c_oracle_and_decrypt(coracle, ladder):
     assert_u32_equal(out2, coracle.pbs(lwe, tvs, K.bsk, K.ksk, P))
 
 
-@pytest.mark.parametrize("name", ["CFG1", "CFG2"])
+@pytest.mark.parametrize("name", ["CFG1", "CFG2", "CFG4", "INSECURE_2048"])
 def test_pbs_fft_ladder_vs_c_oracle(coracle, name):
     """FP64 FFT ladder: bit-exact with the C oracle (schoolbook) on random inputs,
     per-item test polynomials, several segment lengths and a ragged batch."""
@@ -290,11 +290,12 @@ def test_pbs_fft_ladder_vs_c_oracle(coracle, name):
         _lib.check(L.hwb_set_fft_group(1))
 
 
-def test_pbs_fft_ladder_extreme_key():
+@pytest.mark.parametrize("name", ["CFG2", "CFG4"])
+def test_pbs_fft_ladder_extreme_key(name):
     """Largest-magnitude key halves (word 0x7FFF8000: lo = -2^15, hi = +2^15) and
     all-ones / alternating inputs: the rounding margin's worst case, checked
     against the NTT ladder (itself pinned to the oracle)."""
-    P = dataclasses.replace(named_params("CFG2"), lwe_n=24)
+    P = dataclasses.replace(named_params(name), lwe_n=24)
     K = tfhe.pbs_keygen(P, 71)
     for word in (0x7FFF8000, 0x80000000, 0x7FFFFFFF):
         K.bsk[:] = word

@@ -99,23 +99,25 @@ def _random_codes(rng, B, k, R, clear_frac=0.25):
     return codes
 
 
+@pytest.mark.parametrize("name,p", [("CFG2", 256), ("CFG4", 4096)])
 @pytest.mark.parametrize("k", [4, 12, 13])
-def test_ivp_vp_codes_vs_oracle(k):
-    """Random selector matrices mixing encrypted and clear bits, tree (k > 10)
-    and rotation-only (k <= 10) shapes."""
-    P = named_params("CFG2", 256)
+def test_ivp_vp_codes_vs_oracle(k, name, p):
+    """Random selector matrices mixing encrypted and clear bits, tree (k > log2 N)
+    and rotation-only shapes, N = 1024 and 2048, on both ladders."""
+    P = named_params(name, p)
+    gl, gb = P.gadget.levels, P.gadget.base_log
     rng = np.random.default_rng(k)
     R = 6
-    table = rng.integers(0, 1 << 32, (R, 6, 2, P.n), dtype=np.uint64).astype(np.uint32)
+    table = rng.integers(0, 1 << 32, (R, 2 * gl, 2, P.n), dtype=np.uint64).astype(np.uint32)
     payload = rng.integers(0, 1 << 32, (2, P.n), dtype=np.uint64).astype(np.uint32)
     codes = _random_codes(rng, 5, k, R)
-    want = wnn32.ivp_batch(codes, table, payload, 3, 7, P.degree_log)
+    want = wnn32.ivp_batch(codes, table, payload, gl, gb, P.degree_log)
     z = lut.tree_depth(k, P)
     luts = rng.integers(0, 1 << 32, (3, max(1, 1 << z), 2, P.n), dtype=np.uint64).astype(np.uint32)
     lut_idx = rng.integers(0, 3, 5)
     vcodes = _random_codes(rng, 5, k, R)
     vcodes[:, 0] = lut.CLEAR1                       # exercise the clear-prefix slicing
-    vwant = wnn32.vp_batch(vcodes, table, luts[lut_idx], 3, 7, P.degree_log)
+    vwant = wnn32.vp_batch(vcodes, table, luts[lut_idx], gl, gb, P.degree_log)
     for tab in (tfhe.rgsw_to_ntt(P, table), tfhe.rgsw_to_fft(P, table)):     # both ladders
         assert_u32_equal(tfhe.to_host(lut.ivp_codes(P, codes, tab, payload)), want)
         got = tfhe.to_host(lut.vp_codes(P, vcodes, tab, tfhe.to_device(luts), lut_idx))

@@ -13,7 +13,7 @@ from paper_2403_20190_b200.params import named_params  # noqa: E402
 
 def main(B=4096):
     L = _lib.load()
-    for name in ("CFG2", "CFG1"):
+    for name in ("CFG2", "CFG1", "CFG4"):
         P = named_params(name)
         keys = tfhe.pbs_keygen(P, 1)
         bsk, _ = keys.device_keys()
