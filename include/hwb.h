@@ -247,6 +247,12 @@ int hwb_set_fft_segment(int steps);
 /* Ciphertexts per CTA of the FFT PBS ladder (1, 2 or 4): they share every staged key
  * slice (one shared-memory write, several reads). */
 int hwb_set_fft_group(int ciphertexts_per_cta);
+/* Batches of at most max_batch ciphertexts (-1: one per SM, the default) run the
+ * FFT latency ladder at N = 1024: one ciphertext per CTA of 2l groups of 64
+ * threads (one digit transform per group, the four accumulators on four groups),
+ * the whole ladder in one launch.  Bit-identical to the throughput ladder.
+ * Returns the previous setting (the reference has no counterpart). */
+int64_t hwb_set_fft_latency_batch(int64_t max_batch);
 /* hwb_pbs on the FFT ladder with the tensor-core key switch (ksk_tc from
  * hwb_ksk_to_tc); ksk_tc == NULL skips the key switch (lwe_out [B][N+1]). */
 int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, const uint32_t *tv,

@@ -1090,6 +1090,161 @@ __global__ void __launch_bounds__(FT, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Latency-mode FFT ladder (small batches, N = 1024): one ciphertext per CTA of 2l
+// groups of 64 threads.  Per CMUX step: (1) thread 0 stages the key rows
+// r in [l, 2l) (l x 32 KB, one TMA bulk copy) while groups 0..3 load their rows
+// r < l straight into registers; (2) group r extracts digit row r and runs its
+// forward transform (named barrier per group); (3) the 2l digit spectra meet in
+// shared memory; (4) group q = (c, h) < 4 forms accumulator Y[c][h] = sum_r D_r K[r][c][h]
+// and inverse-transforms it; (5) the h = 1 groups hand their rounded words to
+// the h = 0 groups, which update the accumulator.  Bit-identical to the
+// throughput ladder (same exact rounding).
+
+#ifndef HWB_FFT_LAT_PF
+#define HWB_FFT_LAT_PF 3   // steps of L2 prefetch ahead in the FFT latency ladder
+#endif
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+struct FSmemL {
+  uint32_t acc[2 * 2 * FH];
+  double2 D[FDR][FH];                 // digit spectra, layout-B position j * 64 + t
+  double2 scr[FDR][FH];               // per-group transpose scratch (scr[4] also hands over the hi words)
+  double2 key[FDR / 2][2][2][FC * FT];   // key rows [l, 2l) of the step (TMA)
+  uint64_t key_full;
+};
+
+__global__ void __launch_bounds__(FDR * FT, 1)
+    blind_rotate_fft_lat_kernel(const double2 *__restrict__ ggsw, const uint32_t *__restrict__ lwe_in,
+                                const uint32_t *__restrict__ tv, int tv_per_item, uint32_t *lwe_out, int L,
+                                Gadget g, const double2 *__restrict__ twf, const double2 *__restrict__ twi) {
+  constexpr int N = 2 * FH;
+  constexpr int LOG2M = 11;
+  extern __shared__ uint4 smem_raw[];
+  FSmemL &sm = *reinterpret_cast<FSmemL *>(smem_raw);
+  const int lv = (int)g.levels, ng = 2 * lv, nt = ng * FT;
+  const int tid = threadIdx.x, grp = tid / FT, t = tid % FT;
+  const int64_t b = blockIdx.x;
+  uint32_t *acc = sm.acc;
+  const FLay lay = make_flay(t);
+  const uint32_t *row = lwe_in + b * (int64_t)(L + 1);
+  {
+    const int bt = mod_switch(row[L], LOG2M);
+    const uint32_t *tp = tv + (tv_per_item ? b * 2 * N : 0);
+    const int e = (2 * N - bt) & (2 * N - 1);   // X^-b~
+    for (int k = tid; k < 2 * N; k += nt) {
+      const int c = k >= N, i = k & (N - 1);
+      acc[k] = rot_read<N>(tp + c * N, i, e);
+    }
+  }
+  if (tid == 0) {
+    mbar_init(&sm.key_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const size_t ggsw_f = (size_t)2 * lv * 2 * 2 * FC * FT;
+  const size_t row_f = (size_t)2 * 2 * FC * FT;   // double2 per key row r
+  const uint32_t smem_rows_bytes = (uint32_t)(lv * row_f * sizeof(double2));
+  const double dig_off = 4503599627370496.0 + (double)g.half;
+  const int mc = grp >> 1, mh = grp & 1;          // accumulator of a MAC group (grp < 4)
+  uint32_t key_phase = 0;
+  uint32_t *hi_words = reinterpret_cast<uint32_t *>(sm.scr[4]);   // [2 comps][N]
+#pragma unroll 1
+  for (int s = 0; s < L; ++s) {
+    const int e = mod_switch(row[s], LOG2M);   // X^{a~_s}
+    if (e == 0) continue;
+    const double2 *G = ggsw + (size_t)s * ggsw_f;
+    if (tid == 0) {
+      // a lone ciphertext streams the whole key from HBM: pull the GGSW of step
+      // s + HWB_FFT_LAT_PF into L2 now (one bulk prefetch), so its loads hit L2
+      if (s + HWB_FFT_LAT_PF < L)
+        bulk_prefetch_l2(ggsw + (size_t)(s + HWB_FFT_LAT_PF) * ggsw_f, (uint32_t)(ggsw_f * sizeof(double2)));
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&sm.key_full, smem_rows_bytes);
+      bulk_g2s(&sm.key[0][0][0][0], G + lv * row_f, smem_rows_bytes, &sm.key_full);
+    }
+    double2 kreg[FDR / 2][FC];
+    if (grp < 4) {
+#pragma unroll
+      for (int r = 0; r < FDR / 2; ++r)
+        if (r < lv) {
+          const double2 *src = G + r * row_f + (mc * 2 + mh) * (FC * FT) + t;
+#pragma unroll
+          for (int j = 0; j < FC; ++j) kreg[r][j] = __ldg(src + j * FT);
+        }
+    }
+    // digit row grp (hw/tfhe.py:290-298: rows 0..l-1 = digits of b, l..2l-1 of a)
+    {
+      const int comp = grp < lv ? 1 : 0;
+      const int tt = grp < lv ? grp : grp - lv;
+      const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
+      const uint32_t *ac = acc + comp * N;
+      double2 x[FC];
+#pragma unroll
+      for (int j = 0; j < FC; ++j) {
+        const int i = t + FT * j;
+        const uint32_t p0 = decomp_prep(rot_read<N>(ac, i, e) - ac[i], g);
+        const uint32_t p1 = decomp_prep(rot_read<N>(ac, i + FH, e) - ac[i + FH], g);
+        x[j] = make_double2(u2d_minus((p0 >> sh) & g.mask, dig_off), u2d_minus((p1 >> sh) & g.mask, dig_off));
+      }
+      fwd_fft(x, sm.scr[grp], lay, t, twf, NoHook(), 1 + grp);
+#pragma unroll
+      for (int j = 0; j < FC; ++j) sm.D[grp][j * FT + t] = x[j];
+    }
+    __syncthreads();
+    double2 Y[FC];
+    if (grp < 4) {
+#pragma unroll
+      for (int j = 0; j < FC; ++j) Y[j] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int r = 0; r < FDR / 2; ++r)
+        if (r < lv) {
+#pragma unroll
+          for (int j = 0; j < FC; ++j) {
+            const double2 x = sm.D[r][j * FT + t], k = kreg[r][j];
+            Y[j].x = fma(x.x, k.x, fma(-x.y, k.y, Y[j].x));
+            Y[j].y = fma(x.x, k.y, fma(x.y, k.x, Y[j].y));
+          }
+        }
+      mbar_wait(&sm.key_full, key_phase);
+#pragma unroll 1
+      for (int r = lv; r < 2 * lv; ++r) {
+#pragma unroll
+        for (int j = 0; j < FC; ++j) {
+          const double2 x = sm.D[r][j * FT + t], k = sm.key[r - lv][mc][mh][j * FT + t];
+          Y[j].x = fma(x.x, k.x, fma(-x.y, k.y, Y[j].x));
+          Y[j].y = fma(x.x, k.y, fma(x.y, k.x, Y[j].y));
+        }
+      }
+      inv_fft(Y, sm.scr[grp], lay, t, twi, 1 + grp);
+      if (mh == 1) {
+#pragma unroll
+        for (int j = 0; j < FC; ++j) {
+          const int i = t + FT * j;
+          hi_words[mc * N + i] = round_u32(Y[j].x) << 16;
+          hi_words[mc * N + i + FH] = round_u32(Y[j].y) << 16;
+        }
+      }
+    }
+    __syncthreads();
+    if (grp < 4 && mh == 0) {
+#pragma unroll
+      for (int j = 0; j < FC; ++j) {
+        const int i = t + FT * j;
+        acc[mc * N + i] += round_u32(Y[j].x) + hi_words[mc * N + i];
+        acc[mc * N + i + FH] += round_u32(Y[j].y) + hi_words[mc * N + i + FH];
+      }
+    }
+    key_phase ^= 1u;
+    __syncthreads();
+  }
+  uint32_t *o = lwe_out + b * (int64_t)(N + 1);
+  for (int k = tid; k < N; k += nt) o[k] = k == 0 ? acc[0] : 0u - acc[N - k];
+  if (tid == 0) o[N] = acc[N];
+}
+
+// ---------------------------------------------------------------------------
 // FP64 FFT ladder at N = 2048 (FFT2): the folded polynomial has H = 1024 points
 // (z_i = a_i + i a_{i+1024}, a polynomial mod Y^1024 - i).  Its first
 // Cooley-Tukey stage (level 0: z_k +/- w0 z_{k+512}, w0 = e^{i pi/4}) is formed
@@ -2182,6 +2337,14 @@ static size_t fft_acc_bytes(const hwb_params *p, int64_t B) { return ((size_t)B 
 static int g_fft_segment = 64;
 // ciphertexts per CTA of the FFT PBS ladder (sharing each staged key slice)
 static int g_fft_cpb = 1;
+// batches of at most this many ciphertexts run the FFT latency ladder (-1: one per SM)
+static int64_t g_fft_lat_max_batch = -1;
+
+int64_t hwb_set_fft_latency_batch(int64_t max_batch) {
+  const int64_t prev = g_fft_lat_max_batch;
+  if (max_batch >= -1) g_fft_lat_max_batch = max_batch;
+  return prev;
+}
 
 extern "C++" {
 template <int CPB>
@@ -2267,6 +2430,17 @@ int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, co
   uint32_t *ext = ksk_tc ? (uint32_t *)(ws + fft_acc_bytes(p, B)) : lwe_out;
   const Gadget g = make_gadget(p->l, p->base_log);
   const int L = (int)p->n;
+  const int64_t lat_max = g_fft_lat_max_batch >= 0 ? g_fft_lat_max_batch : (int64_t)st->sms;
+  if (p->N == 2 * FH && B <= lat_max) {
+    // latency mode: 2l groups of 64 threads per ciphertext, the whole ladder in one launch
+    const size_t smem = sizeof(FSmemL);
+    if ((rc = set_smem(blind_rotate_fft_lat_kernel, smem))) return rc;
+    blind_rotate_fft_lat_kernel<<<(unsigned)B, 2 * p->l * FT, smem, s>>>(
+        (const double2 *)bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st->fft_fwd, st->fft_inv);
+    if ((rc = post_launch("blind_rotate_fft_lat_kernel"))) return rc;
+    if (!ksk_tc) return HWB_OK;
+    return keyswitch_tc_launch(p, ksk_tc, ext, lwe_out, B, ws + fft_acc_bytes(p, B) + pbs_ext_bytes(p, B), s);
+  }
   for (int s0 = 0; s0 < L; s0 += g_fft_segment) {
     const int s1 = s0 + g_fft_segment < L ? s0 + g_fft_segment : L;
     if (p->N == 4 * FH) {

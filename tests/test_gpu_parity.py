@@ -280,14 +280,19 @@ def test_pbs_fft_ladder_vs_c_oracle(coracle, name):
     tvs = rand_u32(rng, (37, 2, P.n))
     want = coracle.pbs(lwe, tvs, K.bsk, K.ksk, P)
     L = _lib.load()
+    prev = L.hwb_set_fft_latency_batch(0)               # throughput ladder
     try:
         for seg, group in ((1, 1), (7, 2), (64, 4), (64, 1)):
             _lib.check(L.hwb_set_fft_segment(seg))
             _lib.check(L.hwb_set_fft_group(group))     # ragged: 37 items in CTAs of 1, 2 or 4
             assert_u32_equal(tfhe.pbs_batch(P, lwe, tvs, bsk, ksk, ladder="fft"), want)
+        L.hwb_set_fft_latency_batch(1 << 40)            # latency ladder (N = 1024)
+        assert_u32_equal(tfhe.pbs_batch(P, lwe, tvs, bsk, ksk, ladder="fft"), want)
+        assert_u32_equal(tfhe.pbs_batch(P, lwe[:1], tvs[:1], bsk, ksk, ladder="fft"), want[:1])
     finally:
         _lib.check(L.hwb_set_fft_segment(64))
         _lib.check(L.hwb_set_fft_group(1))
+        L.hwb_set_fft_latency_batch(prev)
 
 
 @pytest.mark.parametrize("name", ["CFG2", "CFG4"])
@@ -304,7 +309,7 @@ def test_pbs_fft_ladder_extreme_key(name):
         lwe[1::2, ::2] = 0x55555555
         lwe[2] = np.arange(P.lwe_n + 1, dtype=np.uint32) * 0x9E3779B9
         tv = np.full((2, P.n), 0x7FFFFFFF, np.uint32)
-        a = tfhe.pbs_batch(P, lwe, tv, bsk, None, ladder="fft")
+        a = tfhe.pbs_batch(P, lwe, tv, bsk, None, ladder="fft")   # 8 items: latency ladder at N = 1024
         b = tfhe.pbs_batch(P, lwe, tv, bsk, None, ladder="ntt")
         assert_u32_equal(a, b)
 
