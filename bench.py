@@ -470,6 +470,25 @@ def bench_hwb(args):
     pbs_roof = 1.0 / (w_main / peak + (w_ks_eff / p_ks if p_ks else 0.0))
 
     value = B * world * args.steps / (max_ms * 1e-3)
+    smem_roof = None
+    if use_fft:
+        # the FFT ladder's binding resource is on-chip: shared-memory bandwidth
+        # (128 B/clk/SM).  Algorithmic bytes per ciphertext-step:
+        # transposes (2 per transform, write + read), the key slices (TMA write +
+        # LDS read), digit extraction and byte digits, accumulator update.
+        Hf = N // 2
+        smem_step = ((2 * lv + 4) * 2 * 2 * Hf * 16 + 2 * (2 * lv * 2 * 2 * Hf * 16)
+                     + 2 * N * 4 * 2 + 2 * 2 * lv * N + 2 * N * 4 * 2)
+        sms = torch.cuda.get_device_properties(0).multi_processor_count
+        mhz = (clock_info or {}).get("sm_mhz") or 1965.0
+        sm_peak = 128.0 * sms * mhz * 1e6
+        sm_ach = smem_step * P.lwe_n * B / br_avg_s
+        smem_roof = {"bound": "smem", "achieved": round(sm_ach / 1e12, 2), "peak": round(sm_peak / 1e12, 2),
+                     "unit": "TB/s", "frac": round(sm_ach / sm_peak, 4),
+                     "bytes_per_step": smem_step,
+                     "peak_source": f"128 B/clk/SM x {sms} SMs x {mhz:.0f} MHz (median SM clock under load)",
+                     "ncu": "profiles/r01_ncu_fft_ladder_v2.txt: LSU wavefronts + TMA writes = 0.89 of the "
+                            "crossbar under ncu"}
     result = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 3),
@@ -498,7 +517,8 @@ def bench_hwb(args):
                                    "frac": round(w_ks_eff * B / ks_avg_s / p_ks, 4) if p_ks else None,
                                    "work_per_pbs": f"{w_ks_eff} MACs",
                                    "peak_source": "measured live: probe_i8mma_kernel (M128 N256 K32 from smem)"
-                                   if ks_tc else None}},
+                                   if ks_tc else None},
+                     "smem": smem_roof},
         "kernel_ms": {"blind_rotate": round(statistics.mean(br_ms), 3),
                       "keyswitch": round(statistics.mean(ks_ms), 3)},
         "gpu_launches": ((-(-P.lwe_n // 64) if use_fft else 1) + (2 if ks_tc else 1)) * args.steps,
