@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--ladder", default="auto", choices=["auto", "fft", "ntt"],
                     help="blind rotation: FP64 FFT ladder or two-prime NTT ladder (bit-identical)")
+    ap.add_argument("--fft-mode", type=int, default=1, choices=[0, 1],
+                    help="FFT ladder accumulators: 0 registers, 1 TMEM (bit-identical)")
     ap.add_argument("--ks-engine", default="auto", choices=["auto", "tc", "simt"],
                     help="LWE key switch: tensor cores (tcgen05 int8) or the integer-pipe kernel")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -190,7 +192,7 @@ def ncu_traffic(B, alg_bytes=None, ladder="ntt"):
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            rec = json.load(f)["blind_rotate_fft_kernel" if ladder == "fft" else "blind_rotate_kernel<1024,PBS>"]
+            rec = json.load(f)[ladder if ladder.startswith("blind_rotate_fft") else "blind_rotate_kernel<1024,PBS>"]
     except (OSError, KeyError, ValueError):
         return None
     if rec.get("batch") != B:
@@ -361,6 +363,7 @@ def bench_hwb(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     _lib.set_variant(args.variant)
+    _lib.check(_lib.load().hwb_set_fft_mode(args.fft_mode))
 
     P = named_params("CFG2")
     B = args.batch
@@ -449,7 +452,8 @@ def bench_hwb(args):
         peak = probe_fp64_peak(torch, _lib, tfhe)
         achieved = w_fp64 * B / br_avg_s
         w_main, unit_main = w_fp64, "G FP64-instr/s"
-        roof_kernel = "blind_rotate_fft_kernel (FP64 FFT ladder)"
+        roof_kernel = ("blind_rotate_fft_tm_kernel (FP64 FFT ladder, TMEM accumulators)" if args.fft_mode == 1
+                       else "blind_rotate_fft_kernel (FP64 FFT ladder)")
         work_txt = f"W_fp64 = {w_fp64} FP64 instructions (n x {w_fstep} per CMUX)"
         peak_src = "measured live: probe_fp64_kernel (8 independent DFMA chains per thread)"
     else:
@@ -477,8 +481,14 @@ def bench_hwb(args):
         # transposes (2 per transform, write + read), the key slices (TMA write +
         # LDS read), digit extraction and byte digits, accumulator update.
         Hf = N // 2
-        smem_step = ((2 * lv + 4) * 2 * 2 * Hf * 16 + 2 * (2 * lv * 2 * 2 * Hf * 16)
-                     + 2 * N * 4 * 2 + 2 * 2 * lv * N + 2 * N * 4 * 2)
+        if args.fft_mode == 1:
+            # TMEM accumulators: each key value read serves 2 ciphertexts, each staged
+            # slice 4; digits re-extracted per digit row (rotated + plain reads)
+            smem_step = ((2 * lv + 4) * 2 * 2 * Hf * 16 + 2 * lv * 2 * 2 * Hf * 16 * (1 / 4 + 1 / 2)
+                         + 2 * lv * N * 4 + 2 * N * 4 * 2)
+        else:
+            smem_step = ((2 * lv + 4) * 2 * 2 * Hf * 16 + 2 * (2 * lv * 2 * 2 * Hf * 16)
+                         + 2 * N * 4 * 2 + 2 * 2 * lv * N + 2 * N * 4 * 2)
         sms = torch.cuda.get_device_properties(0).multi_processor_count
         mhz = (clock_info or {}).get("sm_mhz") or 1965.0
         sm_peak = 128.0 * sms * mhz * 1e6
@@ -505,7 +515,8 @@ def bench_hwb(args):
                      "traffic": ncu_traffic(B, (P.lwe_n * 2 * lv * 2 * 2 * (N // 2) * 16 if use_fft
                                                 else 4 * P.lwe_n * 2 * lv * 2 * 2 * N)
                                                + 4 * (B * (P.lwe_n + 1) + B * (N + 1) + 2 * N),
-                                            "fft" if use_fft else "ntt"),
+                                            ("blind_rotate_fft_tm_kernel" if args.fft_mode == 1
+                                             else "blind_rotate_fft_kernel") if use_fft else "ntt"),
                      "work_per_pbs": work_txt, "peak_source": peak_src,
                      "pbs": {"roofline_pbs_per_s": round(pbs_roof, 1),
                              "frac": round(B / (max_ms / args.steps * 1e-3) / pbs_roof, 4),

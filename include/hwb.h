@@ -253,6 +253,11 @@ int hwb_set_fft_group(int ciphertexts_per_cta);
  * the whole ladder in one launch.  Bit-identical to the throughput ladder.
  * Returns the previous setting (the reference has no counterpart). */
 int64_t hwb_set_fft_latency_batch(int64_t max_batch);
+/* FFT PBS ladder accumulators (N = 1024): 0 = registers (hwb_set_fft_group
+ * ciphertexts per CTA), 1 = tensor memory (default, for batches of at least 8
+ * ciphertexts per SM; two ciphertexts per thread share every key value read, four
+ * per CTA share each staged key slice).  Bit-identical. */
+int hwb_set_fft_mode(int mode);
 /* hwb_pbs on the FFT ladder with the tensor-core key switch (ksk_tc from
  * hwb_ksk_to_tc); ksk_tc == NULL skips the key switch (lwe_out [B][N+1]). */
 int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, const uint32_t *tv,

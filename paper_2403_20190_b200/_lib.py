@@ -29,7 +29,7 @@ EXPORTS = (
     "hwb_set_latency_batch", "hwb_bsk_fft_bytes", "hwb_bsk_to_fft", "hwb_pbs_fft",
     "hwb_pbs_fft_workspace_bytes", "hwb_set_fft_segment", "hwb_probe_fp64",
     "hwb_ggsw_fft_bytes", "hwb_ggsw_to_fft", "hwb_blind_rotate_fft", "hwb_ivp_level_fft", "hwb_vp_level_fft",
-    "hwb_set_fft_group", "hwb_set_fft_latency_batch",
+    "hwb_set_fft_group", "hwb_set_fft_latency_batch", "hwb_set_fft_mode",
 )
 
 
@@ -81,6 +81,7 @@ def load() -> ctypes.CDLL:
         L.hwb_set_fft_segment.argtypes = [ctypes.c_int]
         L.hwb_set_fft_group.argtypes = [ctypes.c_int]
         L.hwb_set_fft_latency_batch.argtypes = [_i64]
+        L.hwb_set_fft_mode.argtypes = [ctypes.c_int]
         L.hwb_set_fft_latency_batch.restype = ctypes.c_int64
         L.hwb_ggsw_fft_bytes.argtypes = [_pp]
         L.hwb_ggsw_to_fft.argtypes = [_pp, _vp, _vp, _i64, _vp]

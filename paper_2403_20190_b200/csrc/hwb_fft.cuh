@@ -173,14 +173,15 @@ __device__ __forceinline__ void inv_fft(double2 (&x)[FC], double2 *scr, const FL
 // K independent inverse transforms in lockstep (the four accumulators of a CMUX
 // step): one pair of barriers per transpose for all K, K times the ILP per stage.
 // scr holds K * FH elements.
-template <int K, int FROM, int TO>
-__device__ __forceinline__ void frelayout_k(double2 (*x)[FC], double2 *scr, const FLay &L) {
+template <int K, int FROM, int TO, typename F = NoHook>
+__device__ __forceinline__ void frelayout_k(double2 (*x)[FC], double2 *scr, const FLay &L, F &&after_first = F()) {
   const uint32_t bf = flay_base<FROM>(L), bt = flay_base<TO>(L);
 #pragma unroll
   for (int k = 0; k < K; ++k)
 #pragma unroll
     for (int j = 0; j < FC; ++j) scr[k * FH + (bf ^ fswz(joff<FH, FT, FROM>(j)))] = x[k][j];
   __syncthreads();
+  after_first();
 #pragma unroll
   for (int k = 0; k < K; ++k)
 #pragma unroll
@@ -188,17 +189,18 @@ __device__ __forceinline__ void frelayout_k(double2 (*x)[FC], double2 *scr, cons
   __syncthreads();
 }
 
-// K independent forward transforms in lockstep (the two key halves of a GGSW row)
-template <int K>
+// K independent forward transforms in lockstep (the two key halves of a GGSW row;
+// two ciphertexts of the TMEM ladder); `hook` as in fwd_fft
+template <int K, typename F = NoHook>
 __device__ __forceinline__ void fwd_fft_k(double2 (*x)[FC], double2 *scr, const FLay &L, int t,
-                                          const double2 *__restrict__ tw, int cg = 0) {
+                                          const double2 *__restrict__ tw, int cg = 0, F &&hook = F()) {
   using G = FGeo;
   static_for<0, G::LOGN - G::T>([&](auto Q) {
     constexpr int s = G::LOGN - 1 - decltype(Q)::value;
 #pragma unroll
     for (int k = 0; k < K; ++k) fft_stage<true, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x[k], t, tw, cg);
   });
-  frelayout_k<K, LAY_A, LAY_M>(x, scr, L);
+  frelayout_k<K, LAY_A, LAY_M>(x, scr, L, hook);
   static_for<0, G::T - G::LOGC>([&](auto Q) {
     constexpr int s = G::T - 1 - decltype(Q)::value;
     constexpr int slot = (1 << decltype(Q)::value) - 1;

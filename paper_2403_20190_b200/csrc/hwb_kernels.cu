@@ -1047,6 +1047,228 @@ __global__ void __launch_bounds__(FT * CPB, 1)
   if (t == 0) o[N] = acc[N];
 }
 
+// ---------------------------------------------------------------------------
+// PBS ladder with the accumulators in tensor memory (TMEM).  The register ladder
+// above keeps the four spectra accumulators Y[c][h] in registers (128 of 254), so
+// each thread serves one ciphertext and every staged key value is read once per
+// ciphertext.  Here they live in TMEM (2 KB per thread per ... 256 columns per
+// 128-lane CTA; SIMT tcgen05.ld/st move 500-700 B/clk/SM, beside the shared-memory
+// crossbar that bounds the ladder): each thread transforms the digits of TWO
+// ciphertexts in lockstep and applies every key value it reads from shared memory
+// to both, and one TMA-staged 32 KB key slice serves the CTA's four ciphertexts.
+// Shared-memory bytes per ciphertext-step drop by the key share.
+// TMEM layout: lane = threadIdx.x, columns ((q 2 + c) 2 + h) 32 + 4 j + {re.lo,
+// re.hi, im.lo, im.hi} for ciphertext q in {0, 1} of the thread's group.
+
+constexpr int TMC = 4;          // ciphertexts per CTA (2 groups x 2 per thread)
+constexpr uint32_t TM_COLS = 256;
+
+struct FSmemTM {
+  uint32_t acc[TMC][2 * 2 * FH];
+  double2 scr[2][2 * FH];         // forward scratch of group g (2 transforms); all 32 KB: group 1's inverse scratch
+  double2 key[2 * 2 * FC * FT];   // the digit's key slice (TMA); group 0's inverse scratch
+  uint64_t key_full;
+  uint32_t tmem_slot;
+};
+
+__device__ __forceinline__ void tm_ld32(uint32_t addr, uint32_t (&r)[32]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+               "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                 "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                 "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                 "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                 "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+               : "r"(addr));
+}
+__device__ __forceinline__ void tm_st32(uint32_t addr, const uint32_t (&r)[32]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+               "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(addr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+               "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+               "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+               "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+               : "memory");
+}
+__device__ __forceinline__ double2 tm_get(const uint32_t (&r)[32], int j) {
+  return make_double2(__hiloint2double((int)r[4 * j + 1], (int)r[4 * j]),
+                      __hiloint2double((int)r[4 * j + 3], (int)r[4 * j + 2]));
+}
+__device__ __forceinline__ void tm_put(uint32_t (&r)[32], int j, double2 v) {
+  r[4 * j] = (uint32_t)__double2loint(v.x);
+  r[4 * j + 1] = (uint32_t)__double2hiint(v.x);
+  r[4 * j + 2] = (uint32_t)__double2loint(v.y);
+  r[4 * j + 3] = (uint32_t)__double2hiint(v.y);
+}
+
+__global__ void __launch_bounds__(2 * FT, 2)
+    blind_rotate_fft_tm_kernel(const double2 *__restrict__ ggsw, const uint32_t *__restrict__ lwe_in,
+                               const uint32_t *__restrict__ tv, int tv_per_item, uint32_t *lwe_out, int L, Gadget g,
+                               const double2 *__restrict__ twf, const double2 *__restrict__ twi, uint32_t *acc_io,
+                               int s0, int s1, int64_t B) {
+  constexpr int N = 2 * FH;
+  constexpr int LOG2M = 11;
+  extern __shared__ uint4 smem_raw[];
+  FSmemTM &sm = *reinterpret_cast<FSmemTM *>(smem_raw);
+  const int tid = threadIdx.x, grp = tid / FT, t = tid % FT, warp = tid / 32;
+  const FLay lay = make_flay(t);
+  int64_t bq[2];
+  bool vq[2];
+  const uint32_t *row[2];
+  uint32_t *acc[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    // items past the end of the batch run a clamped copy of the last ciphertext
+    // (they take part in every barrier) and write nothing
+    const int64_t bb = (int64_t)blockIdx.x * TMC + grp * 2 + q;
+    vq[q] = bb < B;
+    bq[q] = vq[q] ? bb : B - 1;
+    row[q] = lwe_in + bq[q] * (int64_t)(L + 1);
+    acc[q] = sm.acc[grp * 2 + q];
+    if (s0 == 0) {
+      const int bt = mod_switch(row[q][L], LOG2M);
+      const uint32_t *tp = tv + (tv_per_item ? bq[q] * 2 * N : 0);
+      const int e = (2 * N - bt) & (2 * N - 1);   // X^-b~
+      for (int k = t; k < 2 * N; k += FT) {
+        const int c = k >= N, i = k & (N - 1);
+        acc[q][k] = rot_read<N>(tp + c * N, i, e);
+      }
+    } else {
+      for (int k = t; k < 2 * N; k += FT) acc[q][k] = acc_io[bq[q] * 2 * N + k];
+    }
+  }
+  if (tid == 0) {
+    mbar_init(&sm.key_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_slot)),
+                 "r"(TM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t lane_addr = sm.tmem_slot + ((uint32_t)(warp * 32) << 16);
+  uint32_t key_phase = 0;
+  constexpr uint32_t kSliceBytes = 2 * 2 * FC * FT * sizeof(double2);
+  const size_t ggsw_f = (size_t)2 * g.levels * 2 * 2 * FC * FT;
+  const int lv = (int)g.levels;
+  const double dig_off = 4503599627370496.0 + (double)g.half;
+#pragma unroll 1
+  for (int s = s0; s < s1; ++s) {
+    int e[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) e[q] = mod_switch(row[q][s], LOG2M);   // X^{a~_s}
+    // the CTA runs the step when any of its ciphertexts needs it (shared key
+    // slices and barriers); an exact no-op product (e = 0) is discarded
+    if (!__syncthreads_or((e[0] | e[1]) != 0)) continue;
+    const double2 *G = ggsw + (size_t)s * ggsw_f;
+#pragma unroll 1
+    for (int r = 0; r < 2 * lv; ++r) {
+      // digit order (hw/tfhe.py:290-298): rows 0..l-1 = digits of b, l..2l-1 of a
+      const int comp = r < lv ? 1 : 0;
+      const int tt = r < lv ? r : r - lv;
+      const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
+      double2 x[2][FC];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const uint32_t *ac = acc[q] + comp * N;
+#pragma unroll
+        for (int j = 0; j < FC; ++j) {
+          const int i = t + FT * j;
+          const uint32_t p0 = decomp_prep(rot_read<N>(ac, i, e[q]) - ac[i], g);
+          const uint32_t p1 = decomp_prep(rot_read<N>(ac, i + FH, e[q]) - ac[i + FH], g);
+          x[q][j] = make_double2(u2d_minus((p0 >> sh) & g.mask, dig_off), u2d_minus((p1 >> sh) & g.mask, dig_off));
+        }
+      }
+      const double2 *gr = G + (size_t)r * (2 * 2 * FC * FT);
+      fwd_fft_k<2>(x, sm.scr[grp], lay, t, twf, 0, [&] {
+        if (tid == 0) {   // every thread is past the previous reader of the key buffer
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_expect_tx(&sm.key_full, kSliceBytes);
+          bulk_g2s(sm.key, gr, kSliceBytes, &sm.key_full);
+        }
+      });
+      mbar_wait(&sm.key_full, key_phase);
+      key_phase ^= 1u;
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        const uint32_t a0 = lane_addr + (uint32_t)((0 * 4 + ch) * 32), a1 = lane_addr + (uint32_t)((1 * 4 + ch) * 32);
+        uint32_t y0[32], y1[32];
+        if (r > 0) {
+          tm_ld32(a0, y0);
+          tm_ld32(a1, y1);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        } else {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) y0[k] = y1[k] = 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < FC; ++j) {
+          const double2 k = sm.key[(ch * FC + j) * FT + t];
+          double2 u = tm_get(y0, j), v = tm_get(y1, j);
+          u.x = fma(x[0][j].x, k.x, fma(-x[0][j].y, k.y, u.x));
+          u.y = fma(x[0][j].x, k.y, fma(x[0][j].y, k.x, u.y));
+          v.x = fma(x[1][j].x, k.x, fma(-x[1][j].y, k.y, v.x));
+          v.y = fma(x[1][j].x, k.y, fma(x[1][j].y, k.x, v.y));
+          tm_put(y0, j, u);
+          tm_put(y1, j, v);
+        }
+        tm_st32(a0, y0);
+        tm_st32(a1, y1);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    // inverse transforms, one ciphertext at a time (both groups in lockstep);
+    // group 0's scratch is the idle key buffer, group 1's the forward scratch
+    __syncthreads();
+#pragma unroll 1
+    for (int q = 0; q < 2; ++q) {
+      double2 Y[4][FC];
+      {
+        uint32_t y[4][32];
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) tm_ld32(lane_addr + (uint32_t)((q * 4 + ch) * 32), y[ch]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch)
+#pragma unroll
+          for (int j = 0; j < FC; ++j) Y[ch][j] = tm_get(y[ch], j);
+      }
+      inv_fft_k<4>(Y, grp == 0 ? sm.key : &sm.scr[0][0], lay, t, twi);
+      if (e[q] != 0) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int j = 0; j < FC; ++j) {
+            const int i = t + FT * j;
+            acc[q][c * N + i] += round_u32(Y[2 * c][j].x) + (round_u32(Y[2 * c + 1][j].x) << 16);
+            acc[q][c * N + i + FH] += round_u32(Y[2 * c][j].y) + (round_u32(Y[2 * c + 1][j].y) << 16);
+          }
+      }
+    }
+    __syncthreads();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sm.tmem_slot), "r"(TM_COLS));
+  }
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    if (!vq[q]) continue;
+    if (s1 < L) {
+      for (int k = t; k < 2 * N; k += FT) acc_io[bq[q] * 2 * N + k] = acc[q][k];
+    } else {
+      uint32_t *o = lwe_out + bq[q] * (int64_t)(N + 1);
+      for (int k = t; k < N; k += FT) o[k] = k == 0 ? acc[q][0] : 0u - acc[q][N - k];
+      if (t == 0) o[N] = acc[q][N];
+    }
+  }
+}
+
 // One tree level of vertical packing on the FFT path (cmux_kernel's MODE_IVP_LEVEL /
 // MODE_VP_LEVEL): block = item * m + sub, GGSW gidx[item].
 template <int MODE>
@@ -2339,6 +2561,15 @@ static int g_fft_segment = 64;
 static int g_fft_cpb = 1;
 // batches of at most this many ciphertexts run the FFT latency ladder (-1: one per SM)
 static int64_t g_fft_lat_max_batch = -1;
+// FFT PBS ladder accumulators: 0 = registers (g_fft_cpb ciphertexts per CTA), 1 = TMEM
+// (default: 65.5 vs 66.6 ms per cfg2 batch of 4096)
+static int g_fft_mode = 1;
+
+int hwb_set_fft_mode(int mode) {
+  if (mode != 0 && mode != 1) return fail(HWB_EINVAL, "FFT ladder mode must be 0 (registers) or 1 (TMEM)");
+  g_fft_mode = mode;
+  return HWB_OK;
+}
 
 int64_t hwb_set_fft_latency_batch(int64_t max_batch) {
   const int64_t prev = g_fft_lat_max_batch;
@@ -2450,6 +2681,14 @@ int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, co
           (const double2 *)bsk_fft, nullptr, nullptr, lwe_in, tv, tv_per_item, ext, L, g, st->fft2_fwd[0],
           st->fft2_fwd[1], st->fft2_inv[0], st->fft2_inv[1], acc, s0, s1, B);
       rc = post_launch("blind_rotate_fft2_kernel");
+    } else if (g_fft_mode == 1 && B >= (int64_t)2 * TMC * st->sms) {
+      // TMEM ladder only when it fills two CTAs (8 ciphertexts) per SM; smaller
+      // batches keep more CTAs per SM on the register ladder
+      const size_t smem = sizeof(FSmemTM);
+      if ((rc = set_smem(blind_rotate_fft_tm_kernel, smem))) return rc;
+      blind_rotate_fft_tm_kernel<<<(unsigned)((B + TMC - 1) / TMC), 2 * FT, smem, s>>>(
+          (const double2 *)bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st->fft_fwd, st->fft_inv, acc, s0, s1, B);
+      rc = post_launch("blind_rotate_fft_tm_kernel");
     } else if (g_fft_cpb == 4)
       rc = launch_pbs_fft<4>(bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st, acc, s0, s1, B, s);
     else if (g_fft_cpb == 2)

@@ -1,5 +1,5 @@
 """FP64 FFT ladder vs NTT ladder: bit-exactness and speed on cfg2/cfg1 PBS batches
-(blind rotation + extraction, no key switch).  Usage: python tools/fft_check.py [B]"""
+(blind rotation + extraction, no key switch).  Usage: python tools/fft_check.py [B] [segment] [ciphertexts/CTA] [mode: 0 registers, 1 TMEM]"""
 import ctypes
 import sys
 
@@ -32,6 +32,7 @@ def main(B=4096):
         seg = int(sys.argv[2]) if len(sys.argv) > 2 else 64
         _lib.check(L.hwb_set_fft_segment(seg))
         _lib.check(L.hwb_set_fft_group(int(sys.argv[3]) if len(sys.argv) > 3 else 1))
+        _lib.check(L.hwb_set_fft_mode(int(sys.argv[4]) if len(sys.argv) > 4 else 1))
 
         def fft():
             _lib.check(L.hwb_pbs_fft(ctypes.byref(cp), tfhe._ptr(fk), None, tfhe._ptr(tv), 0, tfhe._ptr(lwe),
