@@ -258,6 +258,15 @@ int64_t hwb_set_fft_latency_batch(int64_t max_batch);
  * ciphertexts per SM; two ciphertexts per thread share every key value read, four
  * per CTA share each staged key slice).  Bit-identical. */
 int hwb_set_fft_mode(int mode);
+/* Batches of at most max_batch ciphertexts (default -1: the cluster capacity) run the cluster latency
+ * ladder at N = 1024: one ciphertext per cluster of 2l CTAs on 2l SMs (digit row r
+ * on CTA r, partial products summed over distributed shared memory), so the key
+ * streams through 2l SMs.  Returns the previous setting (max_batch < -1: query only). */
+int64_t hwb_set_fft_cluster_batch(int64_t max_batch);
+/* Clusters of the cluster latency ladder that fit co-resident on the device for
+ * these parameters (cudaOccupancyMaxActiveClusters; 0 where the ladder does not
+ * apply): the default batch limit of that ladder. */
+int64_t hwb_fft_cluster_capacity(const hwb_params *p);
 /* hwb_pbs on the FFT ladder with the tensor-core key switch (ksk_tc from
  * hwb_ksk_to_tc); ksk_tc == NULL skips the key switch (lwe_out [B][N+1]). */
 int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, const uint32_t *tv,

@@ -14,6 +14,7 @@
 // groups exchange residues through shared memory and group g lifts component g
 // by CRT.  TPP = 32 (N = 1024) or 64 (N = 2048): 32 coefficients per thread.
 #include <cuda_runtime.h>
+#include <cooperative_groups.h>
 
 #include <cmath>
 #include <cstdio>
@@ -1467,6 +1468,246 @@ __global__ void __launch_bounds__(FDR * FT, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Cluster latency ladder (single ciphertexts, N = 1024): one ciphertext per
+// CLUSTER of 2l CTAs (64 threads each), so the 192 KB of key per CMUX step streams
+// through 2l SMs instead of one (a lone CTA gets ~27 GB/s).  CTA r
+// owns digit row r: it TMA-stages its key row K[r] (32 KB, one step ahead, double
+// buffered), transforms its digits and forms the four partial products
+// P_r[q] = D_r K[r][q] in its shared memory; CTA q < 4 (accumulator (c, h) = (q/2,
+// q%2)) sums P_0..P_{2l-1}[q] over distributed shared memory, inverse-transforms
+// it and rounds; CTA 2c + 1 hands its high words to CTA 2c, which owns the
+// master copy of component c and adds both; every CTA then copies the component
+// its digit row decomposes.  Three cluster barriers per step.  Bit-identical.
+
+namespace cg = cooperative_groups;
+
+struct FSmemC {
+  double2 Pin[FDR + 2][FC * FT];  // owner q: the partial products P_r[q] of every CTA r (<= 8)
+  double2 key[2][4][FC * FT];     // K[r] of the current / next step (TMA, double buffered)
+  double2 scr[FH];                // transpose scratch
+  uint32_t acc[2 * FH];           // this CTA's copy of component c(r), delivered by its master
+  uint32_t master[2 * FH];        // CTA 2c: the master copy of component c
+  uint32_t hi[2 * FH];            // CTA 2c: high words from CTA 2c + 1
+  uint64_t key_full[2];
+  uint64_t pin_full, hi_full, acc_full;   // arrival of pushed data (st.async complete_tx)
+};
+
+__device__ __forceinline__ uint32_t mapa_u32(const void *p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+// remote shared-memory store that completes `bytes` on the remote CTA's mbarrier
+__device__ __forceinline__ void st_async_f64x2(uint32_t raddr, double2 v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+               "d"(v.x), "d"(v.y), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_u32(uint32_t raddr, uint32_t v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(raddr), "r"(v),
+               "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) return;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 2000000000ull) __trap();   // 2 s
+  }
+}
+
+// Exchanges are pushes: st.async remote stores that complete bytes on the
+// receiver's mbarrier, so a CTA waits only for the data it consumes -- no cluster
+// barrier, no memory fence.  Buffer reuse is safe by causality: a producer's next
+// push depends (through the component it must first receive) on the receiver having
+// consumed the previous one.  (A two-hop variant -- one owner per component summing
+// and inverse-transforming both halves -- ran 2.85 vs 2.62 ms per cfg2 PBS: the
+// inverse transforms are better spread over four CTAs.)
+__global__ void __launch_bounds__(FT, 1)
+    blind_rotate_fft_cl_kernel(const double2 *__restrict__ ggsw, const uint32_t *__restrict__ lwe_in,
+                               const uint32_t *__restrict__ tv, int tv_per_item, uint32_t *lwe_out, int L, Gadget g,
+                               const double2 *__restrict__ twf, const double2 *__restrict__ twi) {
+  constexpr int N = 2 * FH;
+  constexpr int LOG2M = 11;
+  extern __shared__ uint4 smem_raw[];
+  FSmemC &sm = *reinterpret_cast<FSmemC *>(smem_raw);
+  cg::cluster_group cluster = cg::this_cluster();
+  const int lv = (int)g.levels, ng = 2 * lv;
+  const int r = (int)cluster.block_rank();
+  const int64_t b = blockIdx.x / ng;
+  const int t = threadIdx.x;
+  const FLay lay = make_flay(t);
+  const uint32_t *row = lwe_in + b * (int64_t)(L + 1);
+  const int comp = r < lv ? 1 : 0;                  // component this digit row decomposes
+  const int tt = r < lv ? r : r - lv;
+  const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
+  const double dig_off = 4503599627370496.0 + (double)g.half;
+  const bool owner = r < 4, master = owner && (r & 1) == 0;
+  const int mc = r >> 1;                            // accumulator component of an owner
+  const size_t ggsw_f = (size_t)2 * lv * 2 * 2 * FC * FT;
+  const size_t row_f = (size_t)2 * 2 * FC * FT;
+  constexpr uint32_t kRowBytes = 2 * 2 * FC * FT * sizeof(double2);
+  const uint32_t pin_bytes = (uint32_t)(ng * FC * FT * sizeof(double2)), comp_bytes = (uint32_t)(N * 4);
+  {
+    const int bt = mod_switch(row[L], LOG2M);
+    const uint32_t *tp = tv + (tv_per_item ? b * 2 * N : 0);
+    const int e = (2 * N - bt) & (2 * N - 1);       // X^-b~
+    for (int i = t; i < N; i += FT) {
+      sm.acc[i] = rot_read<N>(tp + comp * N, i, e);
+      if (master) sm.master[i] = rot_read<N>(tp + mc * N, i, e);
+    }
+  }
+  auto next_step = [&](int s) {   // zero-exponent steps are exact no-ops
+    while (s < L && mod_switch(row[s], LOG2M) == 0) ++s;
+    return s;
+  };
+  if (t == 0) {
+    mbar_init(&sm.key_full[0], 1);
+    mbar_init(&sm.key_full[1], 1);
+    mbar_init(&sm.pin_full, 1);
+    mbar_init(&sm.hi_full, 1);
+    mbar_init(&sm.acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (owner) mbar_expect_tx(&sm.pin_full, pin_bytes);
+    if (master) mbar_expect_tx(&sm.hi_full, comp_bytes);
+    mbar_expect_tx(&sm.acc_full, comp_bytes);
+  }
+  int s = next_step(0);
+  if (t == 0 && s < L) {
+    mbar_expect_tx(&sm.key_full[0], kRowBytes);
+    bulk_g2s(&sm.key[0][0][0], ggsw + (size_t)s * ggsw_f + r * row_f, kRowBytes, &sm.key_full[0]);
+  }
+  // remote addresses: my slot in owner q's Pin and its mbarrier; the master's hi
+  uint32_t pin_dst[4], pin_bar[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    pin_dst[q] = mapa_u32(&sm.Pin[r][0], (uint32_t)q);
+    pin_bar[q] = mapa_u32(&sm.pin_full, (uint32_t)q);
+  }
+  const uint32_t hi_dst = owner && !master ? mapa_u32(sm.hi, (uint32_t)(r - 1)) : 0u;
+  const uint32_t hi_bar = owner && !master ? mapa_u32(&sm.hi_full, (uint32_t)(r - 1)) : 0u;
+  uint32_t kphase[2] = {0u, 0u}, pphase = 0u, hphase = 0u, aphase = 0u;
+  int buf = 0;
+  cluster.sync();                                   // barriers initialised and armed cluster-wide
+  bool first = true;
+  while (s < L) {
+    const int e = mod_switch(row[s], LOG2M);        // X^{a~_s}
+    const int sn = next_step(s + 1);
+    if (!first) {
+      mbar_wait_cluster(&sm.acc_full, aphase);      // component c(r) of the previous step
+      aphase ^= 1u;
+      __syncthreads();                              // every thread past the wait before re-arming
+      if (t == 0) mbar_expect_tx(&sm.acc_full, comp_bytes);
+    }
+    first = false;
+    if (t == 0 && sn < L) {
+      // the other key buffer's last reader (step s - 1) is done (this CTA's threads
+      // passed the acc wait, which follows their reads)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&sm.key_full[buf ^ 1], kRowBytes);
+      bulk_g2s(&sm.key[buf ^ 1][0][0], ggsw + (size_t)sn * ggsw_f + r * row_f, kRowBytes, &sm.key_full[buf ^ 1]);
+    }
+    double2 x[FC];
+#pragma unroll
+    for (int j = 0; j < FC; ++j) {
+      const int i = t + FT * j;
+      const uint32_t p0 = decomp_prep(rot_read<N>(sm.acc, i, e) - sm.acc[i], g);
+      const uint32_t p1 = decomp_prep(rot_read<N>(sm.acc, i + FH, e) - sm.acc[i + FH], g);
+      x[j] = make_double2(u2d_minus((p0 >> sh) & g.mask, dig_off), u2d_minus((p1 >> sh) & g.mask, dig_off));
+    }
+    fwd_fft(x, sm.scr, lay, t, twf);
+    mbar_wait(&sm.key_full[buf], kphase[buf]);
+    kphase[buf] ^= 1u;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int j = 0; j < FC; ++j) {
+        const double2 k = sm.key[buf][q][j * FT + t];
+        st_async_f64x2(pin_dst[q] + (uint32_t)((j * FT + t) * sizeof(double2)),
+                       make_double2(fma(x[j].x, k.x, -x[j].y * k.y), fma(x[j].x, k.y, x[j].y * k.x)), pin_bar[q]);
+      }
+    if (owner) {
+      mbar_wait_cluster(&sm.pin_full, pphase);      // P_0..P_{2l-1}[q] have landed
+      pphase ^= 1u;
+      double2 Y[FC];
+#pragma unroll
+      for (int j = 0; j < FC; ++j) Y[j] = sm.Pin[0][j * FT + t];
+#pragma unroll
+      for (int rr = 1; rr < FDR + 2; ++rr)
+        if (rr < ng) {
+#pragma unroll
+          for (int j = 0; j < FC; ++j) {
+            const double2 v = sm.Pin[rr][j * FT + t];
+            Y[j].x += v.x;
+            Y[j].y += v.y;
+          }
+        }
+      __syncthreads();                              // Pin consumed by every thread
+      if (t == 0) mbar_expect_tx(&sm.pin_full, pin_bytes);
+      inv_fft(Y, sm.scr, lay, t, twi);
+      if (!master) {
+#pragma unroll
+        for (int j = 0; j < FC; ++j) {
+          const int i = t + FT * j;
+          st_async_u32(hi_dst + (uint32_t)(i * 4), round_u32(Y[j].x) << 16, hi_bar);
+          st_async_u32(hi_dst + (uint32_t)((i + FH) * 4), round_u32(Y[j].y) << 16, hi_bar);
+        }
+      } else {
+        mbar_wait_cluster(&sm.hi_full, hphase);
+        hphase ^= 1u;
+        uint32_t v0[FC], v1[FC];
+#pragma unroll
+        for (int j = 0; j < FC; ++j) {
+          const int i = t + FT * j;
+          v0[j] = sm.master[i] + round_u32(Y[j].x) + sm.hi[i];
+          v1[j] = sm.master[i + FH] + round_u32(Y[j].y) + sm.hi[i + FH];
+          sm.master[i] = v0[j];
+          sm.master[i + FH] = v1[j];
+        }
+        __syncthreads();                            // hi consumed by every thread
+        if (t == 0) mbar_expect_tx(&sm.hi_full, comp_bytes);
+        if (sn < L) {
+          // push the new component to every CTA whose digit rows decompose it
+          const int r0 = mc == 1 ? 0 : lv;
+#pragma unroll 1
+          for (int rr = r0; rr < r0 + lv; ++rr) {
+            const uint32_t dst = mapa_u32(sm.acc, (uint32_t)rr), bar = mapa_u32(&sm.acc_full, (uint32_t)rr);
+#pragma unroll
+            for (int j = 0; j < FC; ++j) {
+              const int i = t + FT * j;
+              st_async_u32(dst + (uint32_t)(i * 4), v0[j], bar);
+              st_async_u32(dst + (uint32_t)((i + FH) * 4), v1[j], bar);
+            }
+          }
+        }
+      }
+    }
+    buf ^= 1;
+    s = sn;
+  }
+  // extraction (coefficient 0): a' from component 0, b' = b[0] from component 1
+  cluster.sync();
+  if (r == 0) {
+    uint32_t *o = lwe_out + b * (int64_t)(N + 1);
+    for (int k = t; k < N; k += FT) o[k] = k == 0 ? sm.master[0] : 0u - sm.master[N - k];
+    if (t == 0) o[N] = cluster.map_shared_rank(sm.master, 2)[0];
+  }
+  cluster.sync();                                   // remote reads done before any CTA exits
+}
+
+// ---------------------------------------------------------------------------
 // FP64 FFT ladder at N = 2048 (FFT2): the folded polynomial has H = 1024 points
 // (z_i = a_i + i a_{i+1024}, a polynomial mod Y^1024 - i).  Its first
 // Cooley-Tukey stage (level 0: z_k +/- w0 z_{k+512}, w0 = e^{i pi/4}) is formed
@@ -2561,6 +2802,15 @@ static int g_fft_segment = 64;
 static int g_fft_cpb = 1;
 // batches of at most this many ciphertexts run the FFT latency ladder (-1: one per SM)
 static int64_t g_fft_lat_max_batch = -1;
+// batches of at most this many ciphertexts run the cluster latency ladder (2l SMs
+// each); -1: as many as fit co-resident (hwb_fft_cluster_capacity)
+static int64_t g_fft_cluster_max_batch = -1;
+
+int64_t hwb_set_fft_cluster_batch(int64_t max_batch) {
+  const int64_t prev = g_fft_cluster_max_batch;
+  if (max_batch >= -1) g_fft_cluster_max_batch = max_batch;
+  return prev;
+}
 // FFT PBS ladder accumulators: 0 = registers (g_fft_cpb ciphertexts per CTA), 1 = TMEM
 // (default: 65.5 vs 66.6 ms per cfg2 batch of 4096)
 static int g_fft_mode = 1;
@@ -2639,6 +2889,37 @@ int hwb_bsk_to_fft(const hwb_params *p, const uint32_t *bsk, void *bsk_fft, void
   return launch_to_fft(p, bsk, bsk_fft, polys, st, (cudaStream_t)stream);
 }
 
+int64_t hwb_fft_cluster_capacity(const hwb_params *p) {
+  static int64_t cache[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+  if (!p || check_fft(p) || p->N != 2 * FH || p->l < 2 || 2 * p->l > 8) return 0;
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (cache[p->l] >= 0) return cache[p->l];
+  const size_t smem = sizeof(FSmemC);
+  if (cudaFuncSetAttribute(blind_rotate_fft_cl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * p->l * 64));
+  cfg.blockDim = dim3(FT);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2 * p->l;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, blind_rotate_fft_cl_kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  cache[p->l] = n;
+  return n;
+}
+
 int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, const uint32_t *tv,
                 int tv_per_item, const uint32_t *lwe_in, uint32_t *lwe_out, int64_t B, void *workspace,
                 void *stream) {
@@ -2662,6 +2943,31 @@ int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, co
   const Gadget g = make_gadget(p->l, p->base_log);
   const int L = (int)p->n;
   const int64_t lat_max = g_fft_lat_max_batch >= 0 ? g_fft_lat_max_batch : (int64_t)st->sms;
+  const int64_t cl_max = g_fft_cluster_max_batch >= 0 ? g_fft_cluster_max_batch : hwb_fft_cluster_capacity(p);
+  if (p->N == 2 * FH && B <= cl_max && p->l >= 2 && 2 * p->l <= 8) {
+    // cluster latency ladder: 2l CTAs (SMs) per ciphertext
+    const size_t smem = sizeof(FSmemC);
+    if ((rc = set_smem(blind_rotate_fft_cl_kernel, smem))) return rc;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(B * 2 * p->l));
+    cfg.blockDim = dim3(FT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2 * p->l;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, blind_rotate_fft_cl_kernel, (const double2 *)bsk_fft, lwe_in, tv,
+                                             tv_per_item, ext, L, g, (const double2 *)st->fft_fwd,
+                                             (const double2 *)st->fft_inv);
+    if (e != cudaSuccess) return fail(HWB_ECUDA, std::string("cluster launch: ") + cudaGetErrorString(e));
+    if ((rc = post_launch("blind_rotate_fft_cl_kernel"))) return rc;
+    if (!ksk_tc) return HWB_OK;
+    return keyswitch_tc_launch(p, ksk_tc, ext, lwe_out, B, ws + fft_acc_bytes(p, B) + pbs_ext_bytes(p, B), s);
+  }
   if (p->N == 2 * FH && B <= lat_max) {
     // latency mode: 2l groups of 64 threads per ciphertext, the whole ladder in one launch
     const size_t smem = sizeof(FSmemL);

@@ -821,9 +821,10 @@ _default_ws = PbsWorkspace()
 
 
 def _use_fft_ladder(bsk: BootstrapKey, B: int, ladder: str) -> bool:
-    """"auto": the FP64 FFT ladder when its key exists and the batch fills more
-    than one CTA per SM (single ciphertexts run faster on the NTT latency ladder);
-    "fft" / "ntt" force one (all ladders are bit-identical)."""
+    """"auto": the FP64 FFT ladders when their key exists -- the cluster latency
+    ladder while the batch fits co-resident clusters (2l SMs per ciphertext), the
+    throughput ladders above one CTA per SM -- and the NTT latency ladder in
+    between; "fft" / "ntt" force one family (all ladders are bit-identical)."""
     if ladder not in ("auto", "fft", "ntt"):
         raise TfheError(f"unknown ladder {ladder!r}")
     if ladder == "ntt":
@@ -832,7 +833,14 @@ def _use_fft_ladder(bsk: BootstrapKey, B: int, ladder: str) -> bool:
         if ladder == "fft":
             raise TfheError("no FFT bootstrapping key for these parameters (N = 1024 or 2048, narrow gadgets)")
         return False
-    return ladder == "fft" or B > torch.cuda.get_device_properties(bsk.fft.device).multi_processor_count
+    if ladder == "fft" or B > torch.cuda.get_device_properties(bsk.fft.device).multi_processor_count:
+        return True
+    L = _lib.load()
+    cap = L.hwb_set_fft_cluster_batch(-2)          # query: values below -1 leave the setting
+    if cap < 0:
+        cp = _lib.c_params(bsk.params)
+        cap = int(L.hwb_fft_cluster_capacity(ctypes.byref(cp)))
+    return B <= cap
 
 
 def pbs_batch(params: HeParams, lwe, tv, bsk: BootstrapKey, ksk: LweKeySwitchKey | None,

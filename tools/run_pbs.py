@@ -1,5 +1,5 @@
 """One cfg2 PBS batch through tfhe.pbs_batch (for ncu captures of a single launch
-configuration).  Usage: python tools/run_pbs.py B [ladder] [fft_latency_batch] [reps] [fft_mode]"""
+configuration).  Usage: python tools/run_pbs.py B [ladder] [fft_latency_batch] [reps] [fft_mode] [cluster_batch]"""
 import sys
 
 import numpy as np
@@ -16,6 +16,8 @@ if len(sys.argv) > 3:
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
 if len(sys.argv) > 5:
     _lib.check(_lib.load().hwb_set_fft_mode(int(sys.argv[5])))
+if len(sys.argv) > 6:
+    _lib.load().hwb_set_fft_cluster_batch(int(sys.argv[6]))
 P = named_params("CFG2")
 keys = tfhe.pbs_keygen(P, 1)
 bsk, ksk = keys.device_keys()
