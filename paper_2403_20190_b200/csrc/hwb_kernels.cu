@@ -1485,11 +1485,9 @@ struct FSmemC {
   double2 Pin[FDR + 2][FC * FT];  // owner q: the partial products P_r[q] of every CTA r (<= 8)
   double2 key[2][4][FC * FT];     // K[r] of the current / next step (TMA, double buffered)
   double2 scr[FH];                // transpose scratch
-  uint32_t acc[2 * FH];           // this CTA's copy of component c(r), delivered by its master
-  uint32_t master[2 * FH];        // CTA 2c: the master copy of component c
-  uint32_t hi[2 * FH];            // CTA 2c: high words from CTA 2c + 1
+  uint32_t acc[2 * FH];           // this CTA's copy of component c(r); owners add their words into it
   uint64_t key_full[2];
-  uint64_t pin_full, hi_full, acc_full;   // arrival of pushed data (st.async complete_tx)
+  uint64_t pin_full, acc_full;    // arrival of pushed data (st.async / red.async complete_tx)
 };
 
 __device__ __forceinline__ uint32_t mapa_u32(const void *p, uint32_t rank) {
@@ -1508,6 +1506,16 @@ __device__ __forceinline__ void st_async_u32(uint32_t raddr, uint32_t v, uint32_
                "r"(rbar)
                : "memory");
 }
+// remote shared-memory add (mod 2^32) that completes 4 bytes on the remote mbarrier
+__device__ __forceinline__ void red_async_add_u32(uint32_t raddr, uint32_t v, uint32_t rbar) {
+  asm volatile("red.async.relaxed.cluster.shared::cluster.mbarrier::complete_tx::bytes.add.u32 [%0], %1, [%2];" ::"r"(
+                   raddr),
+               "r"(v), "r"(rbar)
+               : "memory");
+}
+// (CTA-scope acquire: the pushed data is async-proxy shared-memory traffic completed
+// through this CTA's own mbarrier; a cluster-scope acquire adds an L1 invalidate,
+// CCTL.IVALL, to every poll -- 13% of the cluster ladder's stall samples)
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   uint64_t t0;
@@ -1516,7 +1524,7 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity
     uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
         : "r"(a), "r"(parity)
@@ -1528,13 +1536,16 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity
   }
 }
 
-// Exchanges are pushes: st.async remote stores that complete bytes on the
-// receiver's mbarrier, so a CTA waits only for the data it consumes -- no cluster
-// barrier, no memory fence.  Buffer reuse is safe by causality: a producer's next
-// push depends (through the component it must first receive) on the receiver having
-// consumed the previous one.  (A two-hop variant -- one owner per component summing
-// and inverse-transforming both halves -- ran 2.85 vs 2.62 ms per cfg2 PBS: the
-// inverse transforms are better spread over four CTAs.)
+// Exchanges are pushes to the consumer: st.async / red.async remote operations that
+// complete bytes on the receiver's mbarrier, so a CTA waits only for the data it
+// consumes -- no cluster barrier, no memory fence.  Two hops per step: every CTA r
+// pushes P_r[q] to accumulator CTA q; CTA q = (c, h) sums, inverse-transforms,
+// rounds and ADDS its words (lo, or hi << 16) into every copy of component c
+// (red.async.add, mod 2^32 -- the two halves commute).  Buffer reuse is safe by
+// causality: a producer's next push depends on the receiver having consumed the
+// previous one.  (Measured variants: a master CTA per component combining the
+// halves, 3 hops, 2.60 ms per cfg2 PBS; one owner per component doing both
+// inverses, 2.85 ms.)
 __global__ void __launch_bounds__(FT, 1)
     blind_rotate_fft_cl_kernel(const double2 *__restrict__ ggsw, const uint32_t *__restrict__ lwe_in,
                                const uint32_t *__restrict__ tv, int tv_per_item, uint32_t *lwe_out, int L, Gadget g,
@@ -1554,20 +1565,17 @@ __global__ void __launch_bounds__(FT, 1)
   const int tt = r < lv ? r : r - lv;
   const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
   const double dig_off = 4503599627370496.0 + (double)g.half;
-  const bool owner = r < 4, master = owner && (r & 1) == 0;
-  const int mc = r >> 1;                            // accumulator component of an owner
+  const bool owner = r < 4;
+  const int mc = r >> 1, mh = r & 1;                // accumulator (c, h) of an owner
   const size_t ggsw_f = (size_t)2 * lv * 2 * 2 * FC * FT;
   const size_t row_f = (size_t)2 * 2 * FC * FT;
   constexpr uint32_t kRowBytes = 2 * 2 * FC * FT * sizeof(double2);
-  const uint32_t pin_bytes = (uint32_t)(ng * FC * FT * sizeof(double2)), comp_bytes = (uint32_t)(N * 4);
+  const uint32_t pin_bytes = (uint32_t)(ng * FC * FT * sizeof(double2)), delta_bytes = (uint32_t)(2 * N * 4);
   {
     const int bt = mod_switch(row[L], LOG2M);
     const uint32_t *tp = tv + (tv_per_item ? b * 2 * N : 0);
     const int e = (2 * N - bt) & (2 * N - 1);       // X^-b~
-    for (int i = t; i < N; i += FT) {
-      sm.acc[i] = rot_read<N>(tp + comp * N, i, e);
-      if (master) sm.master[i] = rot_read<N>(tp + mc * N, i, e);
-    }
+    for (int i = t; i < N; i += FT) sm.acc[i] = rot_read<N>(tp + comp * N, i, e);
   }
   auto next_step = [&](int s) {   // zero-exponent steps are exact no-ops
     while (s < L && mod_switch(row[s], LOG2M) == 0) ++s;
@@ -1577,28 +1585,23 @@ __global__ void __launch_bounds__(FT, 1)
     mbar_init(&sm.key_full[0], 1);
     mbar_init(&sm.key_full[1], 1);
     mbar_init(&sm.pin_full, 1);
-    mbar_init(&sm.hi_full, 1);
     mbar_init(&sm.acc_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (owner) mbar_expect_tx(&sm.pin_full, pin_bytes);
-    if (master) mbar_expect_tx(&sm.hi_full, comp_bytes);
-    mbar_expect_tx(&sm.acc_full, comp_bytes);
+    mbar_expect_tx(&sm.acc_full, delta_bytes);
   }
   int s = next_step(0);
   if (t == 0 && s < L) {
     mbar_expect_tx(&sm.key_full[0], kRowBytes);
     bulk_g2s(&sm.key[0][0][0], ggsw + (size_t)s * ggsw_f + r * row_f, kRowBytes, &sm.key_full[0]);
   }
-  // remote addresses: my slot in owner q's Pin and its mbarrier; the master's hi
-  uint32_t pin_dst[4], pin_bar[4];
+  uint32_t pin_dst[4], pin_bar[4];                  // my slot in owner q's Pin and its mbarrier
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     pin_dst[q] = mapa_u32(&sm.Pin[r][0], (uint32_t)q);
     pin_bar[q] = mapa_u32(&sm.pin_full, (uint32_t)q);
   }
-  const uint32_t hi_dst = owner && !master ? mapa_u32(sm.hi, (uint32_t)(r - 1)) : 0u;
-  const uint32_t hi_bar = owner && !master ? mapa_u32(&sm.hi_full, (uint32_t)(r - 1)) : 0u;
-  uint32_t kphase[2] = {0u, 0u}, pphase = 0u, hphase = 0u, aphase = 0u;
+  uint32_t kphase[2] = {0u, 0u}, pphase = 0u, aphase = 0u;
   int buf = 0;
   cluster.sync();                                   // barriers initialised and armed cluster-wide
   bool first = true;
@@ -1606,15 +1609,14 @@ __global__ void __launch_bounds__(FT, 1)
     const int e = mod_switch(row[s], LOG2M);        // X^{a~_s}
     const int sn = next_step(s + 1);
     if (!first) {
-      mbar_wait_cluster(&sm.acc_full, aphase);      // component c(r) of the previous step
+      mbar_wait_cluster(&sm.acc_full, aphase);      // both halves of the previous step's product added
       aphase ^= 1u;
       __syncthreads();                              // every thread past the wait before re-arming
-      if (t == 0) mbar_expect_tx(&sm.acc_full, comp_bytes);
+      if (t == 0) mbar_expect_tx(&sm.acc_full, delta_bytes);
     }
     first = false;
     if (t == 0 && sn < L) {
-      // the other key buffer's last reader (step s - 1) is done (this CTA's threads
-      // passed the acc wait, which follows their reads)
+      // the other key buffer's last reader (step s - 1) is done
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(&sm.key_full[buf ^ 1], kRowBytes);
       bulk_g2s(&sm.key[buf ^ 1][0][0], ggsw + (size_t)sn * ggsw_f + r * row_f, kRowBytes, &sm.key_full[buf ^ 1]);
@@ -1657,52 +1659,38 @@ __global__ void __launch_bounds__(FT, 1)
       __syncthreads();                              // Pin consumed by every thread
       if (t == 0) mbar_expect_tx(&sm.pin_full, pin_bytes);
       inv_fft(Y, sm.scr, lay, t, twi);
-      if (!master) {
+      const uint32_t shift = mh ? 16u : 0u;
+      uint32_t w0[FC], w1[FC];
 #pragma unroll
-        for (int j = 0; j < FC; ++j) {
-          const int i = t + FT * j;
-          st_async_u32(hi_dst + (uint32_t)(i * 4), round_u32(Y[j].x) << 16, hi_bar);
-          st_async_u32(hi_dst + (uint32_t)((i + FH) * 4), round_u32(Y[j].y) << 16, hi_bar);
-        }
-      } else {
-        mbar_wait_cluster(&sm.hi_full, hphase);
-        hphase ^= 1u;
-        uint32_t v0[FC], v1[FC];
-#pragma unroll
-        for (int j = 0; j < FC; ++j) {
-          const int i = t + FT * j;
-          v0[j] = sm.master[i] + round_u32(Y[j].x) + sm.hi[i];
-          v1[j] = sm.master[i + FH] + round_u32(Y[j].y) + sm.hi[i + FH];
-          sm.master[i] = v0[j];
-          sm.master[i + FH] = v1[j];
-        }
-        __syncthreads();                            // hi consumed by every thread
-        if (t == 0) mbar_expect_tx(&sm.hi_full, comp_bytes);
-        if (sn < L) {
-          // push the new component to every CTA whose digit rows decompose it
-          const int r0 = mc == 1 ? 0 : lv;
+      for (int j = 0; j < FC; ++j) {
+        w0[j] = round_u32(Y[j].x) << shift;
+        w1[j] = round_u32(Y[j].y) << shift;
+      }
+      // add this half of component mc into every copy of it (CTAs r0 .. r0 + l - 1)
+      const int r0 = mc == 1 ? 0 : lv;
 #pragma unroll 1
-          for (int rr = r0; rr < r0 + lv; ++rr) {
-            const uint32_t dst = mapa_u32(sm.acc, (uint32_t)rr), bar = mapa_u32(&sm.acc_full, (uint32_t)rr);
+      for (int rr = r0; rr < r0 + lv; ++rr) {
+        const uint32_t dst = mapa_u32(sm.acc, (uint32_t)rr), bar = mapa_u32(&sm.acc_full, (uint32_t)rr);
 #pragma unroll
-            for (int j = 0; j < FC; ++j) {
-              const int i = t + FT * j;
-              st_async_u32(dst + (uint32_t)(i * 4), v0[j], bar);
-              st_async_u32(dst + (uint32_t)((i + FH) * 4), v1[j], bar);
-            }
-          }
+        for (int j = 0; j < FC; ++j) {
+          const int i = t + FT * j;
+          red_async_add_u32(dst + (uint32_t)(i * 4), w0[j], bar);
+          red_async_add_u32(dst + (uint32_t)((i + FH) * 4), w1[j], bar);
         }
       }
     }
     buf ^= 1;
     s = sn;
   }
-  // extraction (coefficient 0): a' from component 0, b' = b[0] from component 1
+  if (!first) {
+    mbar_wait_cluster(&sm.acc_full, aphase);        // the last step's halves
+  }
+  // extraction (coefficient 0): a' from component 0 (CTA l), b' = b[0] from component 1 (CTA 0)
   cluster.sync();
-  if (r == 0) {
+  if (r == lv) {
     uint32_t *o = lwe_out + b * (int64_t)(N + 1);
-    for (int k = t; k < N; k += FT) o[k] = k == 0 ? sm.master[0] : 0u - sm.master[N - k];
-    if (t == 0) o[N] = cluster.map_shared_rank(sm.master, 2)[0];
+    for (int k = t; k < N; k += FT) o[k] = k == 0 ? sm.acc[0] : 0u - sm.acc[N - k];
+    if (t == 0) o[N] = cluster.map_shared_rank(sm.acc, 0)[0];
   }
   cluster.sync();                                   // remote reads done before any CTA exits
 }
