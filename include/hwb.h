@@ -267,6 +267,9 @@ int64_t hwb_set_fft_cluster_batch(int64_t max_batch);
  * these parameters (cudaOccupancyMaxActiveClusters; 0 where the ladder does not
  * apply): the default batch limit of that ladder. */
 int64_t hwb_fft_cluster_capacity(const hwb_params *p);
+/* Shape of the cluster latency ladder: 0 = 2l CTAs, one digit row each (default);
+ * 1 = 4 CTAs, one accumulator quarter each, every CTA transforming all digit rows. */
+int hwb_set_fft_cluster_mode(int mode);
 /* hwb_pbs on the FFT ladder with the tensor-core key switch (ksk_tc from
  * hwb_ksk_to_tc); ksk_tc == NULL skips the key switch (lwe_out [B][N+1]). */
 int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, const uint32_t *tv,

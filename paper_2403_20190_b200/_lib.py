@@ -30,7 +30,7 @@ EXPORTS = (
     "hwb_pbs_fft_workspace_bytes", "hwb_set_fft_segment", "hwb_probe_fp64",
     "hwb_ggsw_fft_bytes", "hwb_ggsw_to_fft", "hwb_blind_rotate_fft", "hwb_ivp_level_fft", "hwb_vp_level_fft",
     "hwb_set_fft_group", "hwb_set_fft_latency_batch", "hwb_set_fft_mode", "hwb_set_fft_cluster_batch",
-    "hwb_fft_cluster_capacity",
+    "hwb_fft_cluster_capacity", "hwb_set_fft_cluster_mode",
 )
 
 
@@ -87,6 +87,7 @@ def load() -> ctypes.CDLL:
         L.hwb_set_fft_cluster_batch.restype = ctypes.c_int64
         L.hwb_fft_cluster_capacity.argtypes = [ctypes.POINTER(HwbParams)]
         L.hwb_fft_cluster_capacity.restype = ctypes.c_int64
+        L.hwb_set_fft_cluster_mode.argtypes = [ctypes.c_int]
         L.hwb_set_fft_latency_batch.restype = ctypes.c_int64
         L.hwb_ggsw_fft_bytes.argtypes = [_pp]
         L.hwb_ggsw_to_fft.argtypes = [_pp, _vp, _vp, _i64, _vp]

@@ -1695,6 +1695,171 @@ __global__ void __launch_bounds__(FT, 1)
   cluster.sync();                                   // remote reads done before any CTA exits
 }
 
+// Four-CTA cluster variant: CTA q = (c, h) transforms ALL 2l digit rows itself (2l
+// groups of 64 threads), multiplies them by its key slices K[r][c][h] (48 KB per
+// step, TMA, double-buffered), sums the partials in shared memory, inverse-transforms
+// Y[c][h] and adds its rounded words into every CTA's copy of component c
+// (red.async).  The only cross-SM traffic per step is 4 KB per CTA pair (vs 48 KB of
+// partial products into each accumulator CTA above); a "free" mbarrier (one remote
+// arrival per peer after its digit extraction) keeps a fast CTA from adding step
+// s+1's words before a slow peer has read step s's component.
+struct FSmemC4 {
+  uint32_t acc[2][2 * FH];            // both components
+  double2 key[2][FDR][FC * FT];       // K[r][c][h] of the current / next step, r < 2l
+  double2 part[FDR][FC * FT];         // per-row partial products
+  double2 scr[FDR][FH];               // per-group transpose scratch
+  uint64_t key_full[2], acc_full, free_bar;
+};
+
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t rbar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rbar) : "memory");
+}
+
+__global__ void __launch_bounds__(FDR * FT, 1)
+    blind_rotate_fft_cl4_kernel(const double2 *__restrict__ ggsw, const uint32_t *__restrict__ lwe_in,
+                                const uint32_t *__restrict__ tv, int tv_per_item, uint32_t *lwe_out, int L, Gadget g,
+                                const double2 *__restrict__ twf, const double2 *__restrict__ twi) {
+  constexpr int N = 2 * FH;
+  constexpr int LOG2M = 11;
+  extern __shared__ uint4 smem_raw[];
+  FSmemC4 &sm = *reinterpret_cast<FSmemC4 *>(smem_raw);
+  cg::cluster_group cluster = cg::this_cluster();
+  const int lv = (int)g.levels, ng = 2 * lv;
+  const int q = (int)cluster.block_rank(), qc = q >> 1, qh = q & 1;
+  const int64_t b = blockIdx.x / 4;
+  const int tid = threadIdx.x, grp = tid / FT, t = tid % FT;
+  const FLay lay = make_flay(t);
+  const uint32_t *row = lwe_in + b * (int64_t)(L + 1);
+  const int comp = grp < lv ? 1 : 0;
+  const int tt = grp < lv ? grp : grp - lv;
+  const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
+  const double dig_off = 4503599627370496.0 + (double)g.half;
+  const size_t ggsw_f = (size_t)2 * lv * 2 * 2 * FC * FT;
+  const size_t row_f = (size_t)2 * 2 * FC * FT;
+  constexpr uint32_t kSliceBytes = FC * FT * sizeof(double2);   // one (r, c, h) key polynomial
+  const uint32_t key_bytes = (uint32_t)(ng * kSliceBytes), delta_bytes = (uint32_t)(4 * N * 4);
+  {
+    const int bt = mod_switch(row[L], LOG2M);
+    const uint32_t *tp = tv + (tv_per_item ? b * 2 * N : 0);
+    const int e = (2 * N - bt) & (2 * N - 1);       // X^-b~
+    for (int k = tid; k < 2 * N; k += ng * FT) sm.acc[k >> 10][k & (N - 1)] = rot_read<N>(tp + (k >> 10) * N, k & (N - 1), e);
+  }
+  auto next_step = [&](int s) {
+    while (s < L && mod_switch(row[s], LOG2M) == 0) ++s;
+    return s;
+  };
+  auto stage_key = [&](int s, int bf) {             // thread 0: the 2l slices (r, qc, qh) of GGSW s
+    mbar_expect_tx(&sm.key_full[bf], key_bytes);
+    const double2 *G = ggsw + (size_t)s * ggsw_f + (qc * 2 + qh) * (FC * FT);
+    for (int r = 0; r < ng; ++r) bulk_g2s(&sm.key[bf][r][0], G + r * row_f, kSliceBytes, &sm.key_full[bf]);
+  };
+  if (tid == 0) {
+    mbar_init(&sm.key_full[0], 1);
+    mbar_init(&sm.key_full[1], 1);
+    mbar_init(&sm.acc_full, 1);
+    mbar_init(&sm.free_bar, 3);                     // one arrival per peer per step
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&sm.acc_full, delta_bytes);
+  }
+  int s = next_step(0);
+  if (tid == 0 && s < L) stage_key(s, 0);
+  uint32_t acc_dst[4], acc_bar[4], free_rbar[4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    acc_dst[p] = mapa_u32(&sm.acc[qc][0], (uint32_t)p);
+    acc_bar[p] = mapa_u32(&sm.acc_full, (uint32_t)p);
+    free_rbar[p] = mapa_u32(&sm.free_bar, (uint32_t)p);
+  }
+  uint32_t kphase[2] = {0u, 0u}, aphase = 0u, fphase = 0u;
+  int buf = 0;
+  cluster.sync();
+  bool first = true;
+  while (s < L) {
+    const int e = mod_switch(row[s], LOG2M);
+    const int sn = next_step(s + 1);
+    if (!first) {
+      mbar_wait_cluster(&sm.acc_full, aphase);      // all four quarters of the previous product added
+      aphase ^= 1u;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      if (!first) mbar_expect_tx(&sm.acc_full, delta_bytes);
+      if (sn < L) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        stage_key(sn, buf ^ 1);
+      }
+    }
+    first = false;
+    // group grp: digit row grp of component comp
+    double2 x[FC];
+    {
+      const uint32_t *ac = sm.acc[comp];
+#pragma unroll
+      for (int j = 0; j < FC; ++j) {
+        const int i = t + FT * j;
+        const uint32_t p0 = decomp_prep(rot_read<N>(ac, i, e) - ac[i], g);
+        const uint32_t p1 = decomp_prep(rot_read<N>(ac, i + FH, e) - ac[i + FH], g);
+        x[j] = make_double2(u2d_minus((p0 >> sh) & g.mask, dig_off), u2d_minus((p1 >> sh) & g.mask, dig_off));
+      }
+    }
+    __syncthreads();                                // every group has read the component
+    if (tid == 0)
+      for (int p = 0; p < 4; ++p)
+        if (p != q) mbar_arrive_remote(free_rbar[p]);   // peers may add this step's words now
+    fwd_fft(x, sm.scr[grp], lay, t, twf, NoHook(), 1 + grp);
+    mbar_wait(&sm.key_full[buf], kphase[buf]);
+    kphase[buf] ^= 1u;
+#pragma unroll
+    for (int j = 0; j < FC; ++j) {
+      const double2 k = sm.key[buf][grp][j * FT + t];
+      sm.part[grp][j * FT + t] = make_double2(fma(x[j].x, k.x, -x[j].y * k.y), fma(x[j].x, k.y, x[j].y * k.x));
+    }
+    __syncthreads();
+    if (grp == 0) {
+      double2 Y[FC];
+#pragma unroll
+      for (int j = 0; j < FC; ++j) Y[j] = sm.part[0][j * FT + t];
+#pragma unroll
+      for (int r = 1; r < FDR; ++r)
+        if (r < ng) {
+#pragma unroll
+          for (int j = 0; j < FC; ++j) {
+            const double2 v = sm.part[r][j * FT + t];
+            Y[j].x += v.x;
+            Y[j].y += v.y;
+          }
+        }
+      inv_fft(Y, sm.scr[0], lay, t, twi, 1);
+      const uint32_t shift = qh ? 16u : 0u;
+      uint32_t w0[FC], w1[FC];
+#pragma unroll
+      for (int j = 0; j < FC; ++j) {
+        w0[j] = round_u32(Y[j].x) << shift;
+        w1[j] = round_u32(Y[j].y) << shift;
+      }
+      mbar_wait_cluster(&sm.free_bar, fphase);      // every peer has read this step's component
+#pragma unroll 1
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int j = 0; j < FC; ++j) {
+          const int i = t + FT * j;
+          red_async_add_u32(acc_dst[p] + (uint32_t)(i * 4), w0[j], acc_bar[p]);
+          red_async_add_u32(acc_dst[p] + (uint32_t)((i + FH) * 4), w1[j], acc_bar[p]);
+        }
+    }
+    fphase ^= 1u;
+    buf ^= 1;
+    s = sn;
+  }
+  if (!first) mbar_wait_cluster(&sm.acc_full, aphase);
+  if (q == 0) {
+    uint32_t *o = lwe_out + b * (int64_t)(N + 1);
+    for (int k = tid; k < N; k += ng * FT) o[k] = k == 0 ? sm.acc[0][0] : 0u - sm.acc[0][N - k];
+    if (tid == 0) o[N] = sm.acc[1][0];
+  }
+  cluster.sync();
+}
+
 // ---------------------------------------------------------------------------
 // FP64 FFT ladder at N = 2048 (FFT2): the folded polynomial has H = 1024 points
 // (z_i = a_i + i a_{i+1024}, a polynomial mod Y^1024 - i).  Its first
@@ -2790,6 +2955,14 @@ static int g_fft_segment = 64;
 static int g_fft_cpb = 1;
 // batches of at most this many ciphertexts run the FFT latency ladder (-1: one per SM)
 static int64_t g_fft_lat_max_batch = -1;
+// cluster latency ladder shape: 0 = 2l CTAs (one digit row each), 1 = 4 CTAs (one
+// accumulator quarter each, all digit rows per CTA)
+static int g_fft_cluster_mode = 0;
+int hwb_set_fft_cluster_mode(int mode) {
+  if (mode != 0 && mode != 1) return fail(HWB_EINVAL, "cluster mode must be 0 or 1");
+  g_fft_cluster_mode = mode;
+  return HWB_OK;
+}
 // batches of at most this many ciphertexts run the cluster latency ladder (2l SMs
 // each); -1: as many as fit co-resident (hwb_fft_cluster_capacity)
 static int64_t g_fft_cluster_max_batch = -1;
@@ -2933,24 +3106,27 @@ int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, co
   const int64_t lat_max = g_fft_lat_max_batch >= 0 ? g_fft_lat_max_batch : (int64_t)st->sms;
   const int64_t cl_max = g_fft_cluster_max_batch >= 0 ? g_fft_cluster_max_batch : hwb_fft_cluster_capacity(p);
   if (p->N == 2 * FH && B <= cl_max && p->l >= 2 && 2 * p->l <= 8) {
-    // cluster latency ladder: 2l CTAs (SMs) per ciphertext
-    const size_t smem = sizeof(FSmemC);
-    if ((rc = set_smem(blind_rotate_fft_cl_kernel, smem))) return rc;
+    // cluster latency ladder: 2l (or 4) CTAs (SMs) per ciphertext
+    const bool c4 = g_fft_cluster_mode == 1;
+    const size_t smem = c4 ? sizeof(FSmemC4) : sizeof(FSmemC);
+    if ((rc = c4 ? set_smem(blind_rotate_fft_cl4_kernel, smem) : set_smem(blind_rotate_fft_cl_kernel, smem)))
+      return rc;
+    const int csize = c4 ? 4 : 2 * (int)p->l;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(B * 2 * p->l));
-    cfg.blockDim = dim3(FT);
+    cfg.gridDim = dim3((unsigned)(B * csize));
+    cfg.blockDim = dim3(c4 ? 2 * p->l * FT : FT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2 * p->l;
+    attr[0].val.clusterDim.x = csize;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, blind_rotate_fft_cl_kernel, (const double2 *)bsk_fft, lwe_in, tv,
-                                             tv_per_item, ext, L, g, (const double2 *)st->fft_fwd,
-                                             (const double2 *)st->fft_inv);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, c4 ? blind_rotate_fft_cl4_kernel : blind_rotate_fft_cl_kernel,
+                                             (const double2 *)bsk_fft, lwe_in, tv, tv_per_item, ext, L, g,
+                                             (const double2 *)st->fft_fwd, (const double2 *)st->fft_inv);
     if (e != cudaSuccess) return fail(HWB_ECUDA, std::string("cluster launch: ") + cudaGetErrorString(e));
     if ((rc = post_launch("blind_rotate_fft_cl_kernel"))) return rc;
     if (!ksk_tc) return HWB_OK;

@@ -300,10 +300,13 @@ def test_pbs_fft_ladder_vs_c_oracle(coracle, name):
         assert_u32_equal(tfhe.pbs_batch(P, lwe[:1], tvs[:1], bsk, ksk, ladder="fft"), want[:1])
         prev_cl = L.hwb_set_fft_cluster_batch(1 << 40)  # cluster ladder: 2l CTAs per ciphertext
         try:
-            assert_u32_equal(tfhe.pbs_batch(P, lwe, tvs, bsk, ksk, ladder="fft"), want)
-            assert_u32_equal(tfhe.pbs_batch(P, lwe[:1], tvs[:1], bsk, ksk, ladder="fft"), want[:1])
+            for cmode in (0, 1):                        # 2l CTAs per ciphertext / 4 CTAs
+                _lib.check(L.hwb_set_fft_cluster_mode(cmode))
+                assert_u32_equal(tfhe.pbs_batch(P, lwe, tvs, bsk, ksk, ladder="fft"), want)
+                assert_u32_equal(tfhe.pbs_batch(P, lwe[:1], tvs[:1], bsk, ksk, ladder="fft"), want[:1])
         finally:
             L.hwb_set_fft_cluster_batch(prev_cl)
+            _lib.check(L.hwb_set_fft_cluster_mode(0))
     finally:
         _lib.check(L.hwb_set_fft_segment(64))
         _lib.check(L.hwb_set_fft_group(1))

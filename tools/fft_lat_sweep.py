@@ -38,14 +38,17 @@ def main():
             lw = tfhe.to_device(tfhe.enc_lwe_batch(ms * P.delta, keys.lwe_key, rng))
             row = {}
             outs = {}
-            for mode, thr, cl in (("fft_cluster", 0, 1 << 40), ("fft_lat", 1 << 40, 0), ("fft_thr", 0, 0)):
+            for mode, thr, cl, cm in (("fft_cluster", 0, 1 << 40, 0), ("fft_cluster4", 0, 1 << 40, 1),
+                                      ("fft_lat", 1 << 40, 0, 0), ("fft_thr", 0, 0, 0)):
                 L.hwb_set_fft_latency_batch(thr)
                 L.hwb_set_fft_cluster_batch(cl)
+                _lib.check(L.hwb_set_fft_cluster_mode(cm))
                 t, o = timed(lambda: tfhe.pbs_batch(P, lw, tv, bsk, ksk, ladder="fft"))
                 row[mode] = round(t, 3)
                 outs[mode] = o.clone()
             L.hwb_set_fft_latency_batch(-1)
             L.hwb_set_fft_cluster_batch(0)
+            _lib.check(L.hwb_set_fft_cluster_mode(0))
             t, o = timed(lambda: tfhe.pbs_batch(P, lw, tv, bsk, ksk, ladder="ntt"))
             row["ntt_auto"] = round(t, 3)
             row["bit_identical"] = all(bool(torch.equal(v, o)) for v in outs.values())
