@@ -1061,6 +1061,12 @@ __global__ void __launch_bounds__(FT * CPB, 1)
 // TMEM layout: lane = threadIdx.x, columns ((q 2 + c) 2 + h) 32 + 4 j + {re.lo,
 // re.hi, im.lo, im.hi} for ciphertext q in {0, 1} of the thread's group.
 
+#ifndef HWB_TM_ST2
+#define HWB_TM_ST2 1    // accumulator stores per double (tcgen05.st x2): no register moves into a 32-block
+#endif
+#ifndef HWB_TM_ZERO
+#define HWB_TM_ZERO 1   // accumulators re-zeroed in TMEM after the inverse reads them (no select on the first row)
+#endif
 constexpr int TMC = 4;          // ciphertexts per CTA (2 groups x 2 per thread)
 constexpr uint32_t TM_COLS = 256;
 
@@ -1089,6 +1095,16 @@ __device__ __forceinline__ void tm_st32(uint32_t addr, const uint32_t (&r)[32]) 
                "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
                "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
                "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+               : "memory");
+}
+__device__ __forceinline__ void tm_st_f64(uint32_t addr, double v) {   // one double: 2 columns
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(__double2loint(v)),
+               "r"(__double2hiint(v))
+               : "memory");
+}
+__device__ __forceinline__ void tm_zero32(uint32_t addr) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+               "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(addr), "r"(0u)
                : "memory");
 }
 __device__ __forceinline__ double2 tm_get(const uint32_t (&r)[32], int j) {
@@ -1151,6 +1167,11 @@ __global__ void __launch_bounds__(2 * FT, 2)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t lane_addr = sm.tmem_slot + ((uint32_t)(warp * 32) << 16);
+#if HWB_TM_ZERO
+#pragma unroll
+  for (int k = 0; k < 8; ++k) tm_zero32(lane_addr + (uint32_t)(k * 32));
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+#endif
   uint32_t key_phase = 0;
   constexpr uint32_t kSliceBytes = 2 * 2 * FC * FT * sizeof(double2);
   const size_t ggsw_f = (size_t)2 * g.levels * 2 * 2 * FC * FT;
@@ -1197,6 +1218,11 @@ __global__ void __launch_bounds__(2 * FT, 2)
       for (int ch = 0; ch < 4; ++ch) {
         const uint32_t a0 = lane_addr + (uint32_t)((0 * 4 + ch) * 32), a1 = lane_addr + (uint32_t)((1 * 4 + ch) * 32);
         uint32_t y0[32], y1[32];
+#if HWB_TM_ZERO
+        tm_ld32(a0, y0);   // zeroed at the end of the previous product
+        tm_ld32(a1, y1);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#else
         if (r > 0) {
           tm_ld32(a0, y0);
           tm_ld32(a1, y1);
@@ -1205,6 +1231,7 @@ __global__ void __launch_bounds__(2 * FT, 2)
 #pragma unroll
           for (int k = 0; k < 32; ++k) y0[k] = y1[k] = 0u;
         }
+#endif
 #pragma unroll
         for (int j = 0; j < FC; ++j) {
           const double2 k = sm.key[(ch * FC + j) * FT + t];
@@ -1213,11 +1240,21 @@ __global__ void __launch_bounds__(2 * FT, 2)
           u.y = fma(x[0][j].x, k.y, fma(x[0][j].y, k.x, u.y));
           v.x = fma(x[1][j].x, k.x, fma(-x[1][j].y, k.y, v.x));
           v.y = fma(x[1][j].x, k.y, fma(x[1][j].y, k.x, v.y));
+#if HWB_TM_ST2
+          // per-double stores: the results stay in whatever registers the DFMAs chose
+          tm_st_f64(a0 + 4 * j, u.x);
+          tm_st_f64(a0 + 4 * j + 2, u.y);
+          tm_st_f64(a1 + 4 * j, v.x);
+          tm_st_f64(a1 + 4 * j + 2, v.y);
+#else
           tm_put(y0, j, u);
           tm_put(y1, j, v);
+#endif
         }
+#if !HWB_TM_ST2
         tm_st32(a0, y0);
         tm_st32(a1, y1);
+#endif
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
@@ -1232,6 +1269,10 @@ __global__ void __launch_bounds__(2 * FT, 2)
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch) tm_ld32(lane_addr + (uint32_t)((q * 4 + ch) * 32), y[ch]);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#if HWB_TM_ZERO
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) tm_zero32(lane_addr + (uint32_t)((q * 4 + ch) * 32));   // next product
+#endif
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch)
 #pragma unroll
