@@ -1061,12 +1061,6 @@ __global__ void __launch_bounds__(FT * CPB, 1)
 // TMEM layout: lane = threadIdx.x, columns ((q 2 + c) 2 + h) 32 + 4 j + {re.lo,
 // re.hi, im.lo, im.hi} for ciphertext q in {0, 1} of the thread's group.
 
-#ifndef HWB_TM_ST2
-#define HWB_TM_ST2 1    // accumulator stores per double (tcgen05.st x2): no register moves into a 32-block
-#endif
-#ifndef HWB_TM_ZERO
-#define HWB_TM_ZERO 1   // accumulators re-zeroed in TMEM after the inverse reads them (no select on the first row)
-#endif
 constexpr int TMC = 4;          // ciphertexts per CTA (2 groups x 2 per thread)
 constexpr uint32_t TM_COLS = 256;
 
@@ -1118,6 +1112,125 @@ __device__ __forceinline__ void tm_put(uint32_t (&r)[32], int j, double2 v) {
   r[4 * j + 3] = (uint32_t)__double2hiint(v.y);
 }
 
+// One external product per ciphertext for the CTA's four ciphertexts (thread group
+// grp holds q = 0, 1), all against the same GGSW G: prep(q, c, i) gives the
+// decomposition-ready word of component c, coefficient i; sink(q, c, i, v) receives
+// the product's coefficients (i = t + 64 j and + 512).  The TMEM accumulators are
+// zero on entry and left zero on exit.
+template <typename Prep, typename Sink>
+__device__ __forceinline__ void tm_ext_product(FSmemTM &sm, const double2 *__restrict__ G, const Gadget &g, int grp,
+                                               int t, const FLay &lay, const double2 *__restrict__ twf,
+                                               const double2 *__restrict__ twi, uint32_t lane_addr,
+                                               uint32_t &key_phase, Prep &&prep, Sink &&sink) {
+  constexpr uint32_t kSliceBytes = 2 * 2 * FC * FT * sizeof(double2);
+  const int lv = (int)g.levels;
+  const double dig_off = 4503599627370496.0 + (double)g.half;
+#pragma unroll 1
+  for (int r = 0; r < 2 * lv; ++r) {
+    // digit order (hw/tfhe.py:290-298): rows 0..l-1 = digits of b, l..2l-1 of a
+    const int comp = r < lv ? 1 : 0;
+    const int tt = r < lv ? r : r - lv;
+    const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
+    double2 x[2][FC];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int j = 0; j < FC; ++j) {
+        const int i = t + FT * j;
+        const uint32_t p0 = prep(q, comp, i), p1 = prep(q, comp, i + FH);
+        x[q][j] = make_double2(u2d_minus((p0 >> sh) & g.mask, dig_off), u2d_minus((p1 >> sh) & g.mask, dig_off));
+      }
+    const double2 *gr = G + (size_t)r * (2 * 2 * FC * FT);
+    fwd_fft_k<2>(x, sm.scr[grp], lay, t, twf, 0, [&] {
+      if (threadIdx.x == 0) {   // every thread is past the previous reader of the key buffer
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&sm.key_full, kSliceBytes);
+        bulk_g2s(sm.key, gr, kSliceBytes, &sm.key_full);
+      }
+    });
+    mbar_wait(&sm.key_full, key_phase);
+    key_phase ^= 1u;
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch) {
+      const uint32_t a0 = lane_addr + (uint32_t)((0 * 4 + ch) * 32), a1 = lane_addr + (uint32_t)((1 * 4 + ch) * 32);
+      uint32_t y0[32], y1[32];
+      tm_ld32(a0, y0);
+      tm_ld32(a1, y1);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < FC; ++j) {
+        const double2 k = sm.key[(ch * FC + j) * FT + t];
+        double2 u = tm_get(y0, j), v = tm_get(y1, j);
+        u.x = fma(x[0][j].x, k.x, fma(-x[0][j].y, k.y, u.x));
+        u.y = fma(x[0][j].x, k.y, fma(x[0][j].y, k.x, u.y));
+        v.x = fma(x[1][j].x, k.x, fma(-x[1][j].y, k.y, v.x));
+        v.y = fma(x[1][j].x, k.y, fma(x[1][j].y, k.x, v.y));
+        // per-double stores: the results stay in whatever registers the DFMAs chose
+        // (32-register block stores made ptxas move them)
+        tm_st_f64(a0 + 4 * j, u.x);
+        tm_st_f64(a0 + 4 * j + 2, u.y);
+        tm_st_f64(a1 + 4 * j, v.x);
+        tm_st_f64(a1 + 4 * j + 2, v.y);
+      }
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  // inverse transforms, one ciphertext at a time (both groups in lockstep);
+  // group 0's scratch is the idle key buffer, group 1's the forward scratch
+  __syncthreads();
+#pragma unroll 1
+  for (int q = 0; q < 2; ++q) {
+    double2 Y[4][FC];
+    {
+      uint32_t y[4][32];
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) tm_ld32(lane_addr + (uint32_t)((q * 4 + ch) * 32), y[ch]);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) tm_zero32(lane_addr + (uint32_t)((q * 4 + ch) * 32));   // next product
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch)
+#pragma unroll
+        for (int j = 0; j < FC; ++j) Y[ch][j] = tm_get(y[ch], j);
+    }
+    inv_fft_k<4>(Y, grp == 0 ? sm.key : &sm.scr[0][0], lay, t, twi);
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int j = 0; j < FC; ++j) {
+        const int i = t + FT * j;
+        sink(q, c, i, round_u32(Y[2 * c][j].x) + (round_u32(Y[2 * c + 1][j].x) << 16));
+        sink(q, c, i + FH, round_u32(Y[2 * c][j].y) + (round_u32(Y[2 * c + 1][j].y) << 16));
+      }
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// TMEM allocation of a 128-thread CTA (warp 0 allocates, every thread sees the base)
+__device__ __forceinline__ uint32_t tm_alloc_cta(FSmemTM &sm) {
+  if (threadIdx.x / 32 == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_slot)),
+                 "r"(TM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t lane_addr = sm.tmem_slot + ((uint32_t)((threadIdx.x / 32) * 32) << 16);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) tm_zero32(lane_addr + (uint32_t)(k * 32));
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  return lane_addr;
+}
+__device__ __forceinline__ void tm_free_cta(FSmemTM &sm) {
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (threadIdx.x / 32 == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sm.tmem_slot), "r"(TM_COLS));
+  }
+}
+
 __global__ void __launch_bounds__(2 * FT, 2)
     blind_rotate_fft_tm_kernel(const double2 *__restrict__ ggsw, const uint32_t *__restrict__ lwe_in,
                                const uint32_t *__restrict__ tv, int tv_per_item, uint32_t *lwe_out, int L, Gadget g,
@@ -1167,11 +1280,9 @@ __global__ void __launch_bounds__(2 * FT, 2)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t lane_addr = sm.tmem_slot + ((uint32_t)(warp * 32) << 16);
-#if HWB_TM_ZERO
 #pragma unroll
   for (int k = 0; k < 8; ++k) tm_zero32(lane_addr + (uint32_t)(k * 32));
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-#endif
   uint32_t key_phase = 0;
   constexpr uint32_t kSliceBytes = 2 * 2 * FC * FT * sizeof(double2);
   const size_t ggsw_f = (size_t)2 * g.levels * 2 * 2 * FC * FT;
@@ -1218,20 +1329,9 @@ __global__ void __launch_bounds__(2 * FT, 2)
       for (int ch = 0; ch < 4; ++ch) {
         const uint32_t a0 = lane_addr + (uint32_t)((0 * 4 + ch) * 32), a1 = lane_addr + (uint32_t)((1 * 4 + ch) * 32);
         uint32_t y0[32], y1[32];
-#if HWB_TM_ZERO
         tm_ld32(a0, y0);   // zeroed at the end of the previous product
         tm_ld32(a1, y1);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#else
-        if (r > 0) {
-          tm_ld32(a0, y0);
-          tm_ld32(a1, y1);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        } else {
-#pragma unroll
-          for (int k = 0; k < 32; ++k) y0[k] = y1[k] = 0u;
-        }
-#endif
 #pragma unroll
         for (int j = 0; j < FC; ++j) {
           const double2 k = sm.key[(ch * FC + j) * FT + t];
@@ -1240,21 +1340,12 @@ __global__ void __launch_bounds__(2 * FT, 2)
           u.y = fma(x[0][j].x, k.y, fma(x[0][j].y, k.x, u.y));
           v.x = fma(x[1][j].x, k.x, fma(-x[1][j].y, k.y, v.x));
           v.y = fma(x[1][j].x, k.y, fma(x[1][j].y, k.x, v.y));
-#if HWB_TM_ST2
           // per-double stores: the results stay in whatever registers the DFMAs chose
           tm_st_f64(a0 + 4 * j, u.x);
           tm_st_f64(a0 + 4 * j + 2, u.y);
           tm_st_f64(a1 + 4 * j, v.x);
           tm_st_f64(a1 + 4 * j + 2, v.y);
-#else
-          tm_put(y0, j, u);
-          tm_put(y1, j, v);
-#endif
         }
-#if !HWB_TM_ST2
-        tm_st32(a0, y0);
-        tm_st32(a1, y1);
-#endif
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
@@ -1269,10 +1360,8 @@ __global__ void __launch_bounds__(2 * FT, 2)
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch) tm_ld32(lane_addr + (uint32_t)((q * 4 + ch) * 32), y[ch]);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#if HWB_TM_ZERO
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch) tm_zero32(lane_addr + (uint32_t)((q * 4 + ch) * 32));   // next product
-#endif
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch)
 #pragma unroll
@@ -1309,6 +1398,58 @@ __global__ void __launch_bounds__(2 * FT, 2)
       if (t == 0) o[N] = acc[q][N];
     }
   }
+}
+
+// One IVP (CDEMUX) / VP (CMUX) tree level on the TMEM path: the four
+// sub-ciphertexts 4k .. 4k+3 of an item share its GGSW (levels with m >= 4).
+template <int MODE>
+__global__ void __launch_bounds__(2 * FT, 2)
+    level_fft_tm_kernel(const double2 *__restrict__ ggsw, const int32_t *__restrict__ gidx,
+                        const uint32_t *__restrict__ in, uint32_t *out, int m, Gadget g,
+                        const double2 *__restrict__ twf, const double2 *__restrict__ twi) {
+  constexpr int N = 2 * FH;
+  extern __shared__ uint4 smem_raw[];
+  FSmemTM &sm = *reinterpret_cast<FSmemTM *>(smem_raw);
+  const int tid = threadIdx.x, grp = tid / FT, t = tid % FT;
+  const FLay lay = make_flay(t);
+  const int64_t cta = blockIdx.x, per_item = m / TMC, item = cta / per_item;
+  const int64_t sub0 = (cta % per_item) * TMC + grp * 2;   // this thread's subs sub0, sub0 + 1
+  const size_t ggsw_f = (size_t)2 * g.levels * 2 * 2 * FC * FT;
+  const double2 *G = ggsw + (size_t)gidx[item] * ggsw_f;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    uint32_t *a = sm.acc[grp * 2 + q];
+    const int64_t sub = sub0 + q;
+    if (MODE == MODE_IVP_LEVEL) {
+      const uint32_t *d = in + (item * m + sub) * 2 * N;
+      for (int k = t; k < 2 * N; k += FT) a[k] = d[k];
+    } else {
+      const uint32_t *c0 = in + (item * 2 * m + sub) * 2 * N, *c1 = in + (item * 2 * m + m + sub) * 2 * N;
+      for (int k = t; k < 2 * N; k += FT) a[k] = c1[k] - c0[k];
+    }
+  }
+  if (tid == 0) {
+    mbar_init(&sm.key_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const uint32_t lane_addr = tm_alloc_cta(sm);   // (its barrier also publishes the inputs)
+  uint32_t key_phase = 0;
+  tm_ext_product(
+      sm, G, g, grp, t, lay, twf, twi, lane_addr, key_phase,
+      [&](int q, int c, int i) { return decomp_prep(sm.acc[grp * 2 + q][c * N + i], g); },
+      [&](int q, int c, int i, uint32_t v) {
+        const int64_t sub = sub0 + q;
+        if (MODE == MODE_IVP_LEVEL) {
+          // CDEMUX (hw/lut.py:113-119, 294-313): hi = C (*) d, lo = d - hi
+          out[(item * 2 * m + m + sub) * 2 * N + c * N + i] = v;
+          out[(item * 2 * m + sub) * 2 * N + c * N + i] = sm.acc[grp * 2 + q][c * N + i] - v;
+        } else {
+          // CMUX (hw/lut.py:130-136, 233-247): next = c0 + C (*) (c1 - c0)
+          const uint32_t *c0 = in + (item * 2 * m + sub) * 2 * N;
+          out[(item * m + sub) * 2 * N + c * N + i] = c0[c * N + i] + v;
+        }
+      });
+  tm_free_cta(sm);
 }
 
 // One tree level of vertical packing on the FFT path (cmux_kernel's MODE_IVP_LEVEL /
@@ -3277,6 +3418,14 @@ static int level_fft(const hwb_params *p, const void *ggsw_fft, const int32_t *g
         (const double2 *)ggsw_fft, ggsw_idx, cur, next, m, make_gadget(p->l, p->base_log), st->fft2_fwd[0],
         st->fft2_fwd[1], st->fft2_inv[0], st->fft2_inv[1]);
     return post_launch("level_fft2_kernel");
+  }
+  if (g_fft_mode == 1 && m % TMC == 0 && B * m >= (int64_t)2 * TMC * st->sms) {
+    // sub-ciphertexts of an item share its GGSW: four per CTA on the TMEM path
+    const size_t smem_tm = sizeof(FSmemTM);
+    if ((rc = set_smem(level_fft_tm_kernel<MODE>, smem_tm))) return rc;
+    level_fft_tm_kernel<MODE><<<(unsigned)(B * m / TMC), 2 * FT, smem_tm, (cudaStream_t)stream>>>(
+        (const double2 *)ggsw_fft, ggsw_idx, cur, next, m, make_gadget(p->l, p->base_log), st->fft_fwd, st->fft_inv);
+    return post_launch("level_fft_tm_kernel");
   }
   const size_t smem = sizeof(FSmem);
   if ((rc = set_smem(level_fft_kernel<MODE>, smem))) return rc;
