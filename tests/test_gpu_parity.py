@@ -277,6 +277,8 @@ def test_pbs_fft_ladder_vs_c_oracle(coracle, name):
     assert bsk.fft is not None
     rng = np.random.default_rng(62)
     lwe = rand_u32(rng, (37, P.lwe_n + 1))
+    lwe[3, :-1] = 0                                    # every rotation skipped (exact no-op steps)
+    lwe[5, ::3] = 0                                    # some rotations skipped
     tvs = rand_u32(rng, (37, 2, P.n))
     want = coracle.pbs(lwe, tvs, K.bsk, K.ksk, P)
     L = _lib.load()
