@@ -241,6 +241,41 @@ def probe_i8mma_peak(torch, _lib, tfhe):
     return best
 
 
+def train_other(cfg, images, batch, rank, torch):
+    """Device-resident he_train throughput of another BASELINE training config
+    (images/s), with the decrypted-counter check where q = 2^32 can decrypt."""
+    from paper_2403_20190_b200 import data, hewnn, tfhe, wnn
+    from paper_2403_20190_b200.params import named_params
+    (s, l, a, r, p), pname = data.CONFIG_GEOMETRY[cfg]
+    P = named_params(pname, p)
+    geom = wnn.WisardGeometry(s, l, a, r, p)
+    ds = data.config_dataset(cfg, n=images, seed=rank)
+    key = tfhe.SecretKey(P, tfhe.make_rng(KEY_SEED).integers(0, 2, P.n).astype(np.uint32))
+    rng = tfhe.make_rng(ENC_SEED + 2000 + 1000 * rank)
+    samples = [hewnn.encrypt_sample(ds.bits[i], int(ds.labels[i]), key, rng, label_bits=geom.label_bits,
+                                    device=True) for i in range(images)]
+    hewnn.he_train(samples[:batch], geom, P, batch=batch)                    # warm-up
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    model = hewnn.he_train(samples, geom, P, batch=batch)
+    e1.record()
+    e1.synchronize()
+    out = {"images_per_s": round(images / (e0.elapsed_time(e1) * 1e-3), 2), "images": images, "batch": batch,
+           "params": f"{pname} N={P.n} Bg=2^{P.gadget.base_log} l={P.gadget.levels}",
+           "geometry": {"s": s, "l": l, "a": a, "k0": geom.k0},
+           "ladder": "fp64 FFT" if hewnn._use_fft(P, "auto") else "two-prime NTT"}
+    if P.p * 2 <= P.n or cfg != 4:
+        counters, cc = hewnn.decrypt_model(model, key)
+        ref, rc = wnn.train_integer(ds.bits, ds.labels, geom)
+        out["check"] = ("decrypted counters == train_integer"
+                        if np.array_equal(counters, ref) and np.array_equal(cc.counts, rc.counts)
+                        else "COUNTER MISMATCH")
+    else:
+        out["check"] = "not decryptable at q = 2^32 (p = 4096, DESIGN.md §6b); bit-exactness is tested"
+    return out
+
+
 def bench_train(args, world, rank, torch, dist):
     """Encrypted WiSARD training throughput (the metric's second half):
     hewnn.he_train over `--train-images` client-encrypted images of BASELINE
@@ -616,6 +651,10 @@ def bench_hwb(args):
         result["other_configs"] = other
     if args.train_images > 0:
         result["train"] = bench_train(args, world, rank, torch, dist)
+        if args.other_configs:
+            # the other BASELINE training workloads (cfg5 RGB 7 classes; cfg4 N = 2048)
+            result["train"]["other_configs"] = {f"cfg{c}": train_other(c, n, b, rank, torch)
+                                                for c, n, b in ((5, 32, 16), (4, 16, 8))}
     if world > 1:
         dist.destroy_process_group()
     if rank == 0:
