@@ -173,3 +173,25 @@ def test_pinned_sample_stream(tmp_path):
     got = list(F.read_samples(p, pin=True))
     assert all(g.rgsw.is_pinned() for g in got)
     assert all(np.array_equal(g.rgsw.numpy().view(np.uint32), w.rgsw) for g, w in zip(got, samples()))
+
+
+@pytest.mark.gpu
+def test_train_from_hwsd_stream(tmp_path):
+    """Storage -> pinned host -> HBM: samples written as an HWSD stream, read back into
+    pinned tensors and trained on -- the model equals the reference-pinned fixture."""
+    sys.path.insert(0, GOLDEN)
+    from cases import TRAIN_CASES, train_inputs
+    from conftest import golden
+    name = sorted(TRAIN_CASES)[0]
+    g = golden(f"{name}.npz")
+    P, s1, bits, labels, stacks = train_inputs(name)
+    s, l, a, r = TRAIN_CASES[name][2]
+    lb = max(1, (l - 1).bit_length())
+    smp = [hewnn.EncryptedSample(P, st, s, lb) for st in stacks]
+    path = tmp_path / "train.hwsd"
+    assert F.write_samples(path, smp, P, {"case": name}) == len(smp)
+    stream = F.read_samples(path, pin=True, expect_params=P)
+    model = hewnn.he_train(stream, wnn.WisardGeometry(s, l, a, r, P.p), P, batch=1)
+    import hashlib
+    h = hashlib.sha256(np.ascontiguousarray(tfhe.to_host(model.rams)).tobytes()).hexdigest()
+    assert h == str(g["sha_rams"])
