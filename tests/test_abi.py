@@ -107,3 +107,29 @@ def test_latency_threshold_roundtrip():
         assert _lib.set_latency_batch(-2) == -1
     finally:
         _lib.set_latency_batch(prev)
+
+
+def test_fft_ladder_knobs():
+    """FFT ladder settings: validation before any CUDA call, query-only values."""
+    L = _lib.load()
+    assert L.hwb_set_fft_mode(3) == _lib.HWB_EINVAL
+    assert "mode" in L.hwb_last_error().decode()
+    assert L.hwb_set_fft_cluster_mode(2) == _lib.HWB_EINVAL
+    assert L.hwb_set_fft_group(3) == _lib.HWB_EINVAL
+    for setter in (L.hwb_set_fft_cluster_batch, L.hwb_set_fft_latency_batch):
+        prev = setter(-2)                               # < -1 only queries
+        try:
+            assert setter(7) == prev
+            assert setter(-2) == 7
+        finally:
+            setter(prev)
+    cp = _lib.c_params(named_params("CFG4"))            # N = 2048: no cluster ladder
+    assert L.hwb_fft_cluster_capacity(ctypes.byref(cp)) == 0
+    # FFT key sizes: N = 1024 (double2 per folded point) and N = 2048 (two halves)
+    for name, n_pts in (("CFG2", 512), ("CFG4", 1024)):
+        P = named_params(name)
+        cp = _lib.c_params(P)
+        assert L.hwb_bsk_fft_bytes(ctypes.byref(cp)) == P.lwe_n * 2 * P.gadget.levels * 2 * 2 * n_pts * 16
+    cp = _lib.c_params(named_params("CFG2"))
+    cp.base_log, cp.l = 9, 2                            # FFT path needs byte digits at N = 1024
+    assert L.hwb_bsk_fft_bytes(ctypes.byref(cp)) == 0
