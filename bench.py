@@ -266,10 +266,10 @@ def train_other(cfg, images, batch, rank, torch):
            "geometry": {"s": s, "l": l, "a": a, "k0": geom.k0},
            "ladder": "fp64 FFT" if hewnn._use_fft(P, "auto") else "two-prime NTT"}
     if P.p * 2 <= P.n or cfg != 4:
-        counters, cc = hewnn.decrypt_model(model, key)
+        dm, cc = hewnn.decrypt_model(model, key)
         ref, rc = wnn.train_integer(ds.bits, ds.labels, geom)
         out["check"] = ("decrypted counters == train_integer"
-                        if np.array_equal(counters, ref) and np.array_equal(cc.counts, rc.counts)
+                        if np.array_equal(dm.counters, ref.counters) and np.array_equal(cc.counts, rc.counts)
                         else "COUNTER MISMATCH")
     else:
         out["check"] = "not decryptable at q = 2^32 (p = 4096, DESIGN.md §6b); bit-exactness is tested"
@@ -305,13 +305,13 @@ def bench_train(args, world, rank, torch, dist):
     e1.record()
     e1.synchronize()
     t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
-    counters, cc = hewnn.decrypt_model(model, key)
+    dm, cc = hewnn.decrypt_model(model, key)
     ref, rc = wnn.train_integer(ds.bits, ds.labels, geom)
-    ok = bool(np.array_equal(counters, ref) and np.array_equal(cc.counts, rc.counts))
+    ok = bool(np.array_equal(dm.counters, ref.counters) and np.array_equal(cc.counts, rc.counts))
     noise, margin = hewnn.model_noise(model, key)
-    frac_ok = float(np.mean(counters == ref))
+    frac_ok = float(np.mean(dm.counters == ref.counters))
     # end to end from pinned host ciphertexts, model read back
-    host = [hewnn.EncryptedSample(P, smp.rgsw.cpu().pin_memory(), smp.s, smp.label_bits) for smp in samples]
+    host = [hewnn.EncryptedSample.from_stack(P, smp.rgsw.cpu().pin_memory(), smp.s, smp.n_label_bits) for smp in samples]
     h2d = sum(int(h.rgsw.numel()) * 4 for h in host)
     rams_pin = torch.empty(model.rams.shape, dtype=torch.int32).pin_memory()
     del samples
@@ -362,7 +362,7 @@ def bench_train(args, world, rank, torch, dist):
         g1.synchronize()
         act = wnn.ActivationSpec("bin", 0)
         preds = [hewnn.client_finalize(pk, key, act).prediction for pk in packs]
-        plain = wnn.evaluate_dataset(ref, geom, tds.bits, act)
+        plain = wnn.evaluate_dataset(ref, tds.bits, act)
         vp_items = geom.l * geom.k0
         out["infer"] = {"metric": "encrypted inference images/sec", "unit": "images/s",
                         "value": round(args.infer_images / (g0.elapsed_time(g1) * 1e-3), 2),

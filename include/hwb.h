@@ -21,6 +21,12 @@
  *     HWB_ECUDA for launch/async CUDA errors (RuntimeError).  Nothing throws or
  *     exits across the ABI.  hwb_last_error() describes the last failure of the
  *     calling thread.
+ *   - Threading: calls are re-entrant and asynchronous on their
+ *     stream; there are no host threads in the library.  The tuning setters
+ *     (hwb_set_variant, hwb_set_*_batch, hwb_set_fft_*) are THREAD-LOCAL: they
+ *     change kernel selection for the calling thread only, so two threads
+ *     driving two streams never see each other's settings.  Kernel selection
+ *     never changes results (every ladder is bit-identical).
  *   - Supported envelope: N in {1024, 2048}; gadget levels <= 3 and
  *     2*levels * N * beta/2 * 2^31 < 2^55 (exact two-prime RNS NTT); see DESIGN.md.
  */
@@ -76,6 +82,13 @@ int64_t hwb_probe_modmul(uint32_t *sink, int32_t blocks, int32_t iters, void *st
  * chains each.  Returns the FP64 instructions enqueued; its rate is P_fp64, the
  * FFT ladder's roofline denominator. */
 int64_t hwb_probe_fp64(uint32_t *sink, int32_t blocks, int32_t iters, void *stream);
+
+/* FFT rounding margin (NEW, test instrumentation): in the build compiled with
+ * -DHWB_FFT_MARGIN=1 (libhwb200_margin.so) every FP64 ladder records the largest
+ * |y - rint(y)| over all rounded FFT outputs; *out receives it (synchronous) and
+ * reset != 0 clears it.  The exactness of the FFT ladders needs it below 1/2.
+ * The production build returns HWB_EINVAL. */
+int hwb_fft_margin(double *out, int reset);
 
 /* Tensor-core throughput probe (NEW): `blocks` CTAs (one per SM) each issue
  * iters x 4 tcgen05.mma kind::i8 M128 N256 K32 from shared memory into TMEM,

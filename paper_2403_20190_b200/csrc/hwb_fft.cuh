@@ -245,9 +245,24 @@ __device__ __forceinline__ void inv_fft_k(double2 (*x)[FC], double2 *scr, const 
 __device__ __forceinline__ double u2d_minus(uint32_t u, double two52_plus_off) {
   return __hiloint2double(0x43300000, (int)u) - two52_plus_off;
 }
+// Rounding-margin instrumentation (the build of libhwb200_margin.so, -DHWB_FFT_MARGIN=1):
+// every rounded FFT output records |y - rint(y)| into g_fft_margin (the bit pattern of
+// a non-negative double orders like an integer), read back by hwb_fft_margin().  The
+// exactness argument needs this to stay well below 1/2; tests assert < 2^-6.
+#ifndef HWB_FFT_MARGIN
+#define HWB_FFT_MARGIN 0
+#endif
+#if HWB_FFT_MARGIN
+__device__ unsigned long long g_fft_margin;
+#endif
 // round to nearest and reduce mod 2^32 (|y| < 2^51): low word of y + 1.5 * 2^52
 __device__ __forceinline__ uint32_t round_u32(double y) {
-  return (uint32_t)__double2loint(y + 6755399441055744.0);
+  const double r = y + 6755399441055744.0;
+#if HWB_FFT_MARGIN
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(fabs(y - (r - 6755399441055744.0)));
+  if (bits > *(volatile unsigned long long *)&g_fft_margin) atomicMax(&g_fft_margin, bits);
+#endif
+  return (uint32_t)__double2loint(r);
 }
 
 }  // namespace hwb

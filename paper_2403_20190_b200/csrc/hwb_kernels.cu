@@ -33,10 +33,10 @@ namespace hwb {
 static thread_local std::string g_err;
 // kernel variant: selects the register/occupancy build of the ladder kernels
 // (0 = default, 1 = alternative); both bit-identical, for A/B measurement.
-static int g_variant = 0;
+static thread_local int g_variant = 0;
 // batches up to this size run the latency-mode ladder (blind_rotate_lat_kernel);
 // -1 = automatic (3 x the SM count: up to three waves of 2 CTAs per SM).
-static int64_t g_lat_max_batch = -1;
+static thread_local int64_t g_lat_max_batch = -1;
 
 static int fail(int code, const std::string &msg) {
   g_err = msg;
@@ -1223,6 +1223,7 @@ __device__ __forceinline__ uint32_t tm_alloc_cta(FSmemTM &sm) {
   return lane_addr;
 }
 __device__ __forceinline__ void tm_free_cta(FSmemTM &sm) {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (threadIdx.x / 32 == 0) {
@@ -1381,6 +1382,8 @@ __global__ void __launch_bounds__(2 * FT, 2)
     }
     __syncthreads();
   }
+  // the last step's zeroing stores (tm_zero32) must land before the columns are freed
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0) {
@@ -1664,12 +1667,18 @@ __global__ void __launch_bounds__(FDR * FT, 1)
 namespace cg = cooperative_groups;
 
 struct FSmemC {
-  double2 Pin[FDR + 2][FC * FT];  // owner q: the partial products P_r[q] of every CTA r (<= 8)
+  // owner q: the partial products P_r[q] of every CTA r (<= 8), double-buffered by
+  // executed-step parity: a push for step s+2 is causally after every owner's read of
+  // step s (it needs this CTA's component of step s+1, whose owners needed every
+  // CTA's push of step s+1, each issued after that CTA's owner section of step s);
+  // a single buffer would let a push for s+1 overwrite a slow owner of the OTHER
+  // component still reading step s
+  double2 Pin[2][FDR + 2][FC * FT];
   double2 key[2][4][FC * FT];     // K[r] of the current / next step (TMA, double buffered)
   double2 scr[FH];                // transpose scratch
   uint32_t acc[2 * FH];           // this CTA's copy of component c(r); owners add their words into it
   uint64_t key_full[2];
-  uint64_t pin_full, acc_full;    // arrival of pushed data (st.async / red.async complete_tx)
+  uint64_t pin_full[2], acc_full; // arrival of pushed data (st.async / red.async complete_tx)
 };
 
 __device__ __forceinline__ uint32_t mapa_u32(const void *p, uint32_t rank) {
@@ -1766,10 +1775,14 @@ __global__ void __launch_bounds__(FT, 1)
   if (t == 0) {
     mbar_init(&sm.key_full[0], 1);
     mbar_init(&sm.key_full[1], 1);
-    mbar_init(&sm.pin_full, 1);
+    mbar_init(&sm.pin_full[0], 1);
+    mbar_init(&sm.pin_full[1], 1);
     mbar_init(&sm.acc_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (owner) mbar_expect_tx(&sm.pin_full, pin_bytes);
+    if (owner) {
+      mbar_expect_tx(&sm.pin_full[0], pin_bytes);
+      mbar_expect_tx(&sm.pin_full[1], pin_bytes);
+    }
     mbar_expect_tx(&sm.acc_full, delta_bytes);
   }
   int s = next_step(0);
@@ -1777,14 +1790,15 @@ __global__ void __launch_bounds__(FT, 1)
     mbar_expect_tx(&sm.key_full[0], kRowBytes);
     bulk_g2s(&sm.key[0][0][0], ggsw + (size_t)s * ggsw_f + r * row_f, kRowBytes, &sm.key_full[0]);
   }
-  uint32_t pin_dst[4], pin_bar[4];                  // my slot in owner q's Pin and its mbarrier
+  uint32_t pin_dst[4], pin_bar[4];                  // my slot in owner q's Pin[0] and its mbarrier
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    pin_dst[q] = mapa_u32(&sm.Pin[r][0], (uint32_t)q);
-    pin_bar[q] = mapa_u32(&sm.pin_full, (uint32_t)q);
+    pin_dst[q] = mapa_u32(&sm.Pin[0][r][0], (uint32_t)q);
+    pin_bar[q] = mapa_u32(&sm.pin_full[0], (uint32_t)q);
   }
-  uint32_t kphase[2] = {0u, 0u}, pphase = 0u, aphase = 0u;
-  int buf = 0;
+  constexpr uint32_t kPinBufBytes = (uint32_t)sizeof(sm.Pin[0]);
+  uint32_t kphase[2] = {0u, 0u}, pphase[2] = {0u, 0u}, aphase = 0u;
+  int buf = 0, pb = 0;                              // key buffer, Pin buffer (executed-step parity)
   cluster.sync();                                   // barriers initialised and armed cluster-wide
   bool first = true;
   while (s < L) {
@@ -1819,27 +1833,28 @@ __global__ void __launch_bounds__(FT, 1)
 #pragma unroll
       for (int j = 0; j < FC; ++j) {
         const double2 k = sm.key[buf][q][j * FT + t];
-        st_async_f64x2(pin_dst[q] + (uint32_t)((j * FT + t) * sizeof(double2)),
-                       make_double2(fma(x[j].x, k.x, -x[j].y * k.y), fma(x[j].x, k.y, x[j].y * k.x)), pin_bar[q]);
+        st_async_f64x2(pin_dst[q] + pb * kPinBufBytes + (uint32_t)((j * FT + t) * sizeof(double2)),
+                       make_double2(fma(x[j].x, k.x, -x[j].y * k.y), fma(x[j].x, k.y, x[j].y * k.x)),
+                       pin_bar[q] + pb * (uint32_t)sizeof(uint64_t));
       }
     if (owner) {
-      mbar_wait_cluster(&sm.pin_full, pphase);      // P_0..P_{2l-1}[q] have landed
-      pphase ^= 1u;
+      mbar_wait_cluster(&sm.pin_full[pb], pphase[pb]);   // P_0..P_{2l-1}[q] have landed
+      pphase[pb] ^= 1u;
       double2 Y[FC];
 #pragma unroll
-      for (int j = 0; j < FC; ++j) Y[j] = sm.Pin[0][j * FT + t];
+      for (int j = 0; j < FC; ++j) Y[j] = sm.Pin[pb][0][j * FT + t];
 #pragma unroll
       for (int rr = 1; rr < FDR + 2; ++rr)
         if (rr < ng) {
 #pragma unroll
           for (int j = 0; j < FC; ++j) {
-            const double2 v = sm.Pin[rr][j * FT + t];
+            const double2 v = sm.Pin[pb][rr][j * FT + t];
             Y[j].x += v.x;
             Y[j].y += v.y;
           }
         }
-      __syncthreads();                              // Pin consumed by every thread
-      if (t == 0) mbar_expect_tx(&sm.pin_full, pin_bytes);
+      __syncthreads();                              // Pin[pb] consumed by every thread
+      if (t == 0) mbar_expect_tx(&sm.pin_full[pb], pin_bytes);
       inv_fft(Y, sm.scr, lay, t, twi);
       const uint32_t shift = mh ? 16u : 0u;
       uint32_t w0[FC], w1[FC];
@@ -1862,6 +1877,7 @@ __global__ void __launch_bounds__(FT, 1)
       }
     }
     buf ^= 1;
+    pb ^= 1;
     s = sn;
   }
   if (!first) {
@@ -2824,6 +2840,27 @@ int64_t hwb_probe_modmul(uint32_t *sink, int32_t blocks, int32_t iters, void *st
   return (int64_t)blocks * 256 * 8 * iters;
 }
 
+int hwb_fft_margin(double *out, int reset) {
+#if HWB_FFT_MARGIN
+  unsigned long long bits = 0;
+  if (out) {
+    if (cudaMemcpyFromSymbol(&bits, g_fft_margin, sizeof(bits)) != cudaSuccess)
+      return fail(HWB_ECUDA, std::string("hwb_fft_margin: ") + cudaGetErrorString(cudaGetLastError()));
+    memcpy(out, &bits, sizeof(bits));
+  }
+  if (reset) {
+    bits = 0;
+    if (cudaMemcpyToSymbol(g_fft_margin, &bits, sizeof(bits)) != cudaSuccess)
+      return fail(HWB_ECUDA, std::string("hwb_fft_margin: ") + cudaGetErrorString(cudaGetLastError()));
+  }
+  return HWB_OK;
+#else
+  (void)out;
+  (void)reset;
+  return fail(HWB_EINVAL, "built without HWB_FFT_MARGIN (use libhwb200_margin.so)");
+#endif
+}
+
 int64_t hwb_probe_fp64(uint32_t *sink, int32_t blocks, int32_t iters, void *stream) {
   if (blocks < 1 || iters < 1) return -fail(HWB_EINVAL, "probe needs positive blocks and iters");
   probe_fp64_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(sink, iters);
@@ -3132,14 +3169,14 @@ static size_t pbs_ext_bytes(const hwb_params *p, int64_t B) {
 
 static size_t fft_acc_bytes(const hwb_params *p, int64_t B) { return ((size_t)B * 2 * p->N * 4 + 255) & ~(size_t)255; }
 // ladder steps per launch of the FFT ladder (L2 residency of the key slice)
-static int g_fft_segment = 64;
+static thread_local int g_fft_segment = 64;
 // ciphertexts per CTA of the FFT PBS ladder (sharing each staged key slice)
-static int g_fft_cpb = 1;
+static thread_local int g_fft_cpb = 1;
 // batches of at most this many ciphertexts run the FFT latency ladder (-1: one per SM)
-static int64_t g_fft_lat_max_batch = -1;
+static thread_local int64_t g_fft_lat_max_batch = -1;
 // cluster latency ladder shape: 0 = 2l CTAs (one digit row each), 1 = 4 CTAs (one
 // accumulator quarter each, all digit rows per CTA)
-static int g_fft_cluster_mode = 0;
+static thread_local int g_fft_cluster_mode = 0;
 int hwb_set_fft_cluster_mode(int mode) {
   if (mode != 0 && mode != 1) return fail(HWB_EINVAL, "cluster mode must be 0 or 1");
   g_fft_cluster_mode = mode;
@@ -3147,7 +3184,7 @@ int hwb_set_fft_cluster_mode(int mode) {
 }
 // batches of at most this many ciphertexts run the cluster latency ladder (2l SMs
 // each); -1: as many as fit co-resident (hwb_fft_cluster_capacity)
-static int64_t g_fft_cluster_max_batch = -1;
+static thread_local int64_t g_fft_cluster_max_batch = -1;
 
 int64_t hwb_set_fft_cluster_batch(int64_t max_batch) {
   const int64_t prev = g_fft_cluster_max_batch;
@@ -3156,7 +3193,7 @@ int64_t hwb_set_fft_cluster_batch(int64_t max_batch) {
 }
 // FFT PBS ladder accumulators: 0 = registers (g_fft_cpb ciphertexts per CTA), 1 = TMEM
 // (default: 65.5 vs 66.6 ms per cfg2 batch of 4096)
-static int g_fft_mode = 1;
+static thread_local int g_fft_mode = 1;
 
 int hwb_set_fft_mode(int mode) {
   if (mode != 0 && mode != 1) return fail(HWB_EINVAL, "FFT ladder mode must be 0 (registers) or 1 (TMEM)");

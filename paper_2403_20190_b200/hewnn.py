@@ -24,32 +24,75 @@ from . import lut, tfhe
 from ._lib import TfheError
 from .params import HeParams
 from .tfhe import RgswCiphertext, RlweCiphertext
-from .wnn import ClassCounts, WisardGeometry, permutation
+from .wnn import ClassCounts, IntegerWisardModel, WisardGeometry, permutation
 
 
-@dataclass
 class EncryptedSample:
     """One preprocessed sample encrypted bit by bit as RGSW (hw/hewnn.py:33-43).
 
-    `rgsw` holds all s data bits then the label bits (LSB-first) as one
-    (s + label_bits, 2l, 2, N) uint32 array (numpy or a device tensor)."""
+    Reference constructor: `EncryptedSample(params, data_bits, label_bits=None)`
+    with lists of RgswCiphertext (label bits LSB-first).  The batched GPU path
+    keeps all s data bits then the label bits as ONE stacked (s + nl, 2l, 2, N)
+    uint32 array -- numpy, a pinned host tensor or a device tensor -- built by
+    `from_stack` (or lazily from the lists); the list views are materialised on
+    demand from the stack."""
 
-    params: HeParams
-    rgsw: object
-    s: int
-    label_bits: int = 0
+    def __init__(self, params: HeParams, data_bits: Sequence[RgswCiphertext],
+                 label_bits: Sequence[RgswCiphertext] | None = None):
+        self.params = params
+        self._data = list(data_bits)
+        self._labels = None if label_bits is None else list(label_bits)
+        self._stack = None
+        self._s = len(self._data)
+        self._nl = 0 if self._labels is None else len(self._labels)
+
+    @classmethod
+    def from_stack(cls, params: HeParams, stack, s: int, n_label_bits: int = 0) -> "EncryptedSample":
+        obj = cls.__new__(cls)
+        obj.params, obj._stack, obj._s, obj._nl = params, stack, int(s), int(n_label_bits)
+        obj._data = obj._labels = None
+        return obj
+
+    @property
+    def s(self) -> int:
+        return self._s
+
+    @property
+    def n_label_bits(self) -> int:
+        return self._nl
+
+    @property
+    def rgsw(self):
+        """(s + nl, 2l, 2, N) stacked words (the batched path's input)."""
+        if self._stack is None:
+            g = self.params.gadget
+            rows = [np.asarray(c.data, dtype=np.uint32) for c in self._data + (self._labels or [])]
+            self._stack = (np.stack(rows) if rows else
+                           np.zeros((0, 2 * g.levels, 2, self.params.n), dtype=np.uint32))
+        return self._stack
+
+    def _host_rows(self, lo: int, hi: int) -> list[RgswCiphertext]:
+        st = self._stack
+        host = st[lo:hi] if isinstance(st, np.ndarray) else tfhe.to_host(st[lo:hi])
+        return [RgswCiphertext(self.params, np.asarray(host[i], dtype=np.uint32)) for i in range(hi - lo)]
 
     @property
     def data_bits(self) -> list[RgswCiphertext]:
-        host = self.rgsw if isinstance(self.rgsw, np.ndarray) else tfhe.to_host(self.rgsw)
-        return [RgswCiphertext(self.params, host[i]) for i in range(self.s)]
+        if self._data is None:
+            self._data = self._host_rows(0, self._s)
+        return self._data
 
     @property
-    def labels(self) -> list[RgswCiphertext] | None:
-        if not self.label_bits:
-            return None
-        host = self.rgsw if isinstance(self.rgsw, np.ndarray) else tfhe.to_host(self.rgsw)
-        return [RgswCiphertext(self.params, host[self.s + i]) for i in range(self.label_bits)]
+    def label_bits(self) -> list[RgswCiphertext] | None:
+        """The label's RGSW bits (LSB-first), None for an unlabelled sample."""
+        if self._labels is None and self._stack is not None and self._nl:
+            self._labels = self._host_rows(self._s, self._s + self._nl)
+        return self._labels
+
+    labels = label_bits       # round-1 name
+
+    def __repr__(self) -> str:
+        return f"EncryptedSample(s={self._s}, label_bits={self._nl}, params={self.params.name})"
 
 
 @dataclass
@@ -89,16 +132,30 @@ def _check_geometry(geometry: WisardGeometry, params: HeParams):
 
 
 class DeviceKey:
-    """A secret key's NTT image on the device, for GPU-side key products."""
+    """A secret key's NTT image on the device, for GPU-side key products.
+
+    Remembers what it was built from (parameters, device, a digest of the key
+    coefficients) so a cached image is never used for a different key."""
 
     def __init__(self, key: tfhe.SecretKey):
         params = key.params
         self.params = params
+        self.device = torch.cuda.current_device()
+        self.digest = _key_digest(key)
         s = tfhe.to_device(key.s)
         cp = _lib_params(params)
         self.ntt = torch.empty((2, params.n), dtype=torch.int32, device=s.device)
         tfhe._lib.check(tfhe._lib.load().hwb_poly_to_ntt(cp, tfhe._ptr(s), tfhe._ptr(self.ntt), 1,
                                                          tfhe._stream()))
+
+    def matches(self, key: tfhe.SecretKey) -> bool:
+        return (self.params == key.params and self.device == torch.cuda.current_device()
+                and self.digest == _key_digest(key))
+
+
+def _key_digest(key: tfhe.SecretKey) -> bytes:
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(key.s, dtype=np.uint32).tobytes()).digest()
 
 
 def _lib_params(params):
@@ -106,14 +163,13 @@ def _lib_params(params):
     return ctypes.byref(tfhe._lib.c_params(params))
 
 
-_device_keys: dict[int, DeviceKey] = {}
-
-
 def _device_key(key: tfhe.SecretKey) -> DeviceKey:
-    dk = _device_keys.get(id(key))
-    if dk is None or dk.params != key.params:
+    """The key's device image, cached on the key object itself (not by id(), which
+    CPython reuses) and rebuilt when the key, its parameters or the device change."""
+    dk = getattr(key, "_device_key", None)
+    if dk is None or not dk.matches(key):
         dk = DeviceKey(key)
-        _device_keys[id(key)] = dk
+        object.__setattr__(key, "_device_key", dk)
     return dk
 
 
@@ -164,7 +220,7 @@ def encrypt_sample(bits: Sequence[int], label: int | None, key: tfhe.SecretKey, 
         lab = enc(np.array([(label >> i) & 1 for i in range(label_bits)], dtype=np.int64), key, rng)
         data = torch.cat([data, lab]) if device else np.concatenate([data, lab])
         lb = label_bits
-    return EncryptedSample(key.params, data, len(bits), lb)
+    return EncryptedSample.from_stack(key.params, data, len(bits), lb)
 
 
 def _enc_rgsw_host(ms, key, rng) -> np.ndarray:
@@ -366,6 +422,18 @@ def _stack_table(params: HeParams, samples: list[EncryptedSample], staged: _Stag
     return tfhe.GgswFft(params, table, sum(rows)) if fft else tfhe.GgswNtt(params, table)
 
 
+def he_count_labels(label_bits: Sequence[RgswCiphertext], counts_ct, params: HeParams):
+    """hw/hewnn.py:180-186: add one to the encrypted per-class counter selected by
+    the label bits (an IVP of the payload (0, q/p) over the label bits alone).
+    Returns a new (2, N) ciphertext (numpy in -> numpy out, device -> device)."""
+    sel = [[lut.SelectorBit.enc(c) for c in label_bits]]
+    codes, table = lut._codes_of(sel, params)
+    row = lut.ivp_codes(params, codes, table, _payload(params))[0, 0]          # (2, N) on the device
+    if isinstance(counts_ct, torch.Tensor):
+        return lut.accumulate_(counts_ct.to(row.device).clone().contiguous(), row)
+    return (np.asarray(counts_ct, dtype=np.uint32) + tfhe.to_host(row)).astype(np.uint32)
+
+
 def he_count_labels_batch(params: HeParams, counts_ct: torch.Tensor, table, label_rows: np.ndarray,
                           dev_rows: torch.Tensor | None = None):
     """hw/hewnn.py:180-186 for several samples: counts += IVP(label bits, (0, q/p))."""
@@ -416,8 +484,10 @@ def he_train(samples: Iterable[EncryptedSample], geometry: WisardGeometry, param
     def check(sample):
         if sample.s != geometry.s:
             raise TfheError(f"sample has {sample.s} bits, geometry wants {geometry.s}")
-        if sample.label_bits != geometry.label_bits:
-            raise TfheError("training samples need encrypted label bits")
+        if sample.n_label_bits != geometry.label_bits:
+            raise TfheError("training samples need encrypted label bits"
+                            if not sample.n_label_bits else
+                            f"sample has {sample.n_label_bits} label bits, geometry wants {geometry.label_bits}")
 
     # one chunk in flight: chunk k+1's H2D is enqueued on the copy stream before
     # chunk k's ladders, so host->device traffic overlaps the GPU work
@@ -494,7 +564,7 @@ def he_train_multi(samples: Iterable[EncryptedSample], geometries: Sequence[Wisa
         chunk.clear()
 
     for sample in samples:
-        if sample.label_bits != base.label_bits:
+        if sample.n_label_bits != base.label_bits:
             raise TfheError("training samples need encrypted label bits")
         chunk.append(sample)
         if len(chunk) == batch:
@@ -506,7 +576,7 @@ def he_train_multi(samples: Iterable[EncryptedSample], geometries: Sequence[Wisa
 def decrypt_sample(sample: EncryptedSample, key: tfhe.SecretKey) -> tuple[list[int], int | None]:
     """hw/hewnn.py:122-130 (client side)."""
     bits = [tfhe.dec_rgsw(c, key) for c in sample.data_bits]
-    labs = sample.labels
+    labs = sample.label_bits
     if labs is None:
         return bits, None
     return bits, sum(tfhe.dec_rgsw(c, key) << i for i, c in enumerate(labs))
@@ -646,12 +716,13 @@ def model_noise(model: HomWisardModel, key: tfhe.SecretKey) -> tuple[int, int]:
 
 
 def decrypt_model(model: HomWisardModel, key: tfhe.SecretKey):
-    """Decrypt the RLWE matrix into integer counters (l, k0, 2^a) and class counts."""
+    """Decrypt the RLWE matrix back into a plaintext integer model (hw/hewnn.py:352-365):
+    (IntegerWisardModel with counters (l, k0, 2^a), ClassCounts)."""
     g, params = model.geometry, model.params
     rams = tfhe.to_host(model.rams)                               # (k0, k1, 2, N)
     phase = (rams[:, :, 1] - tfhe._key_mul_host(rams[:, :, 0], key.s)).astype(np.uint32)
     vals = tfhe.decode_phase(phase, params).reshape(g.k0, -1)[:, : 1 << g.selector_bits]
-    counters = np.zeros((g.l, g.k0, 1 << g.a), dtype=np.int64)
+    plain = IntegerWisardModel.zeros(g)
     for c in range(g.l):
-        counters[c] = vals[:, c << g.a: (c << g.a) + (1 << g.a)]
-    return counters, decrypt_counts(model.counts_ct, params, g.l, key)
+        plain.counters[c] = vals[:, c << g.a: (c << g.a) + (1 << g.a)]
+    return plain, decrypt_counts(model.counts_ct, params, g.l, key)

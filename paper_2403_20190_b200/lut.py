@@ -25,10 +25,13 @@ import torch
 
 from . import _lib, tfhe
 from ._lib import TfheError
-from .params import HeParams
+from .params import HeParams, named_params
 from .tfhe import GgswFft, GgswNtt, RgswCiphertext, RlweCiphertext
 
 CLEAR0, CLEAR1 = -1, -2
+# ring geometry only (the gather needs N): parameter sets of each supported degree
+_ANY_1024 = named_params("CFG2")
+_ANY_2048 = named_params("CFG4")
 
 
 @dataclass
@@ -51,6 +54,24 @@ class SelectorBit:
     @property
     def is_clear(self) -> bool:
         return self.ct is None
+
+
+@dataclass
+class EncryptedLut:
+    """2^k-entry table packed into max(1, 2^k / N) RLWE ciphertexts (hw/lut.py:47-63)."""
+
+    polys: list[RlweCiphertext]
+    k: int
+
+    def __post_init__(self):
+        n = self.polys[0].params.n
+        want = max(1, (1 << self.k) // n)
+        if len(self.polys) != want:
+            raise TfheError(f"a LUT with k = {self.k} holds {want} polynomials, not {len(self.polys)}")
+
+    @property
+    def params(self) -> HeParams:
+        return self.polys[0].params
 
 
 def tree_depth(k: int, params: HeParams) -> int:
@@ -87,15 +108,30 @@ def _i32(x, device) -> torch.Tensor:
     return t.to(device=device, dtype=torch.int32).contiguous()
 
 
-def monomial_gather(params: HeParams, x, es):
-    """Per-item x_i * X^(es_i) (hw/lut.py:317-325) on the GPU."""
+def monomial_gather(*args):
+    """Per-item x_i * X^(es_i) (hw/lut.py:317-325) on the GPU.  Reference form
+    `monomial_gather(x, es)` (ring degree from x), or `monomial_gather(params, x, es)`."""
+    if len(args) == 3:
+        params, x, es = args
+    elif len(args) == 2:
+        x, es = args
+        n = int(np.shape(x)[-1]) if not isinstance(x, torch.Tensor) else int(x.shape[-1])
+        params = {1024: _ANY_1024, 2048: _ANY_2048}.get(n)
+        if params is None:
+            raise TfheError(f"ring degree {n} is not supported (1024 or 2048)")
+    else:
+        raise TypeError("monomial_gather(x, es) or monomial_gather(params, x, es)")
     t = tfhe.to_device(x)
+    shape = t.shape
+    t = t.reshape(-1, 2, params.n) if t.dim() != 3 else t
     B = t.shape[0]
     e = _i32(np.asarray(es, dtype=np.int64) % (2 * params.n) if not isinstance(es, torch.Tensor) else es, t.device)
+    if e.numel() != B:
+        raise TfheError("one exponent per ciphertext")
     out = torch.empty_like(t)
     _lib.check(_lib.load().hwb_monomial_gather(_cp(params), tfhe._ptr(t), tfhe._ptr(out), tfhe._ptr(e), B,
                                                tfhe._stream()))
-    return tfhe._wrap(x, out)
+    return tfhe._wrap(x, out.reshape(shape))
 
 
 def accumulate_(dst: torch.Tensor, src: torch.Tensor, negate: bool = False) -> torch.Tensor:
@@ -321,45 +357,45 @@ def vp_batch(selectors: list[list[SelectorBit]], luts: list, params: HeParams):
     return out[:, :-1], out[:, -1].copy()
 
 
-def encode_lut(values, params: HeParams) -> list[RlweCiphertext]:
-    """Pack 2^k public values mod p into trivial ciphertexts (hw/lut.py:86-97)."""
+def encode_lut(values, params: HeParams) -> EncryptedLut:
+    """Pack 2^k public values mod p into trivial (noiseless) ciphertexts (hw/lut.py:86-97)."""
     values = np.asarray(values, dtype=np.int64)
     size = len(values)
     if size < 1 or size & (size - 1):
         raise TfheError("LUT size must be a power of two")
     n = params.n
-    if size >= n:
-        return [tfhe.trivial_rlwe(values[i: i + n], params) for i in range(0, size, n)]
-    return [tfhe.trivial_rlwe(values, params)]
+    chunks = [values[i: i + n] for i in range(0, size, n)] if size >= n else [values]
+    return EncryptedLut([tfhe.trivial_rlwe(c, params) for c in chunks], size.bit_length() - 1)
 
 
-def decode_lut(lut: list[RlweCiphertext], k: int, key: tfhe.SecretKey) -> np.ndarray:
+def decode_lut(lut: EncryptedLut, key: tfhe.SecretKey) -> np.ndarray:
     """Decrypt every entry (hw/lut.py:100-103, test helper)."""
-    vals = np.concatenate([tfhe.dec_rlwe(c, key) for c in lut])
-    return vals[: 1 << k]
+    vals = np.concatenate([tfhe.dec_rlwe(c, key) for c in lut.polys])
+    return vals[: 1 << lut.k]
 
 
-def lut_add(a: list[RlweCiphertext], b: list[RlweCiphertext]) -> list[RlweCiphertext]:
+def lut_add(a: EncryptedLut, b: EncryptedLut) -> EncryptedLut:
     """Entry-wise sum of equally shaped LUTs (hw/lut.py:106-110)."""
-    if len(a) != len(b):
+    if a.k != b.k or len(a.polys) != len(b.polys):
         raise TfheError("LUT geometries differ")
-    return [x + y for x, y in zip(a, b)]
+    return EncryptedLut([x + y for x, y in zip(a.polys, b.polys)], a.k)
 
 
-def vertical_packing(bits: list[SelectorBit], lut: list[RlweCiphertext]):
-    """hw/lut.py:122-149 for one selector vector: LWE (N+1,) of lut[m]."""
-    params = lut[0].params
-    k = len(bits)
-    if max(1, (1 << k) // params.n) != len(lut):
-        raise TfheError(f"selector arity {k} does not match a LUT of {len(lut)} polynomials")
-    a, b = vp_batch([bits], [np.stack([np.asarray(c.data) for c in lut])], params)
-    return np.concatenate([a[0], [b[0]]]).astype(np.uint32)
+def vertical_packing(bits: list[SelectorBit], lut: EncryptedLut) -> tfhe.LweCiphertext:
+    """hw/lut.py:122-149: LWE of lut[m], m the index the selector bits encode (one
+    item of vp_codes: CMUX tree, rotation ladder, extraction on the GPU)."""
+    params = lut.params
+    if len(bits) != lut.k:
+        raise TfheError(f"selector arity {len(bits)} != LUT k {lut.k}")
+    a, b = vp_batch([bits], [np.stack([np.asarray(c.data) for c in lut.polys])], params)
+    return tfhe.LweCiphertext(params, a[0].astype(np.uint32), np.uint32(b[0]))
 
 
-def inverse_vertical_packing(bits: list[SelectorBit], payload: RlweCiphertext) -> list[RlweCiphertext]:
-    """hw/lut.py:152-189: deposit the payload at the selected entry."""
+def inverse_vertical_packing(bits: list[SelectorBit], payload: RlweCiphertext) -> EncryptedLut:
+    """hw/lut.py:152-189: deposit the payload's constant term at the selected entry
+    (rotation ladder + CDEMUX tree on the GPU); every other entry encrypts zero."""
     rows = ivp_batch([bits], payload.data, payload.params)[0]
-    return [RlweCiphertext(payload.params, r) for r in rows]
+    return EncryptedLut([RlweCiphertext(payload.params, r) for r in rows], len(bits))
 
 
 def cdemux(C: RgswCiphertext, d: RlweCiphertext) -> tuple[RlweCiphertext, RlweCiphertext]:

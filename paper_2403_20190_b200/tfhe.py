@@ -16,6 +16,7 @@ back as numpy) or CUDA tensors (device-resident; the result stays on device).
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -39,7 +40,8 @@ __all__ = [
     "enc_rgsw_batch", "trivial_rgsw", "dec_rgsw", "enc_lwe_batch", "dec_lwe_batch",
     "phase_lwe_batch", "rgsw_rep", "rgsw_to_ntt", "ext_product_batch", "external_product",
     "cmux", "cmux_batch", "cdemux_batch", "blind_rotate", "blind_rotate_batch", "extract_lwe",
-    "sample_extract_batch", "mod_switch", "test_polynomial", "lwe_keyswitch", "pbs_batch",
+    "sample_extract_batch", "mod_switch", "LweCiphertext", "phase_lwe", "dec_lwe", "packing_key_switch",
+    "keygen", "pack_batch", "PackingKeySwitchKey", "measure_noise", "NoiseBudget", "test_polynomial", "lwe_keyswitch", "pbs_batch",
     "GgswFft", "rgsw_to_fft", "ggsw_fft_bytes",
 ]
 
@@ -65,7 +67,10 @@ def to_device(x) -> torch.Tensor:
     return torch.from_numpy(a.view(np.int32)).to(_device(), non_blocking=False)
 
 
-def to_host(t: torch.Tensor) -> np.ndarray:
+def to_host(t) -> np.ndarray:
+    """uint32 words on the host (a torch tensor is copied; numpy passes through)."""
+    if isinstance(t, np.ndarray):
+        return np.ascontiguousarray(t, dtype=np.uint32) if t.dtype != np.int32 else t.view(np.uint32)
     return t.detach().cpu().numpy().view(np.uint32)
 
 
@@ -162,6 +167,25 @@ class RlweCiphertext:
 
     def copy(self):
         return RlweCiphertext(self.params, self.data.copy())
+
+
+@dataclass
+class LweCiphertext:
+    """LWE ciphertext (a, b) (hw/tfhe.py:169-173): a uint32 (n,), b uint32.  The
+    batched entry points use packed (B, n+1) rows instead (b last); `row()` and
+    `from_row()` convert."""
+
+    params: HeParams
+    a: np.ndarray
+    b: np.uint32
+
+    def row(self) -> np.ndarray:
+        return np.concatenate([np.asarray(self.a, dtype=U32), np.asarray([self.b], dtype=U32)])
+
+    @classmethod
+    def from_row(cls, params: HeParams, row) -> "LweCiphertext":
+        r = np.asarray(row if isinstance(row, np.ndarray) else to_host(row), dtype=U32)
+        return cls(params, r[:-1].copy(), U32(r[-1]))
 
 
 @dataclass
@@ -400,12 +424,23 @@ def pack_batch(a_stacks, b_polys, ksk: PackingKeySwitchKey):
     return _wrap(a_stacks, out)
 
 
-def packing_key_switch(cs, ksk: PackingKeySwitchKey) -> RlweCiphertext:
-    """hw/tfhe.py:373-387: pack <= N extracted LWEs ((N+1,) rows, b last)."""
-    rows = np.stack([np.asarray(c, dtype=U32) for c in cs])
-    n = ksk.params.n
-    if len(rows) > n:
-        raise TfheError(f"cannot pack {len(rows)} > N = {n} ciphertexts")
+def packing_key_switch(cs: Sequence[LweCiphertext], ksk: PackingKeySwitchKey) -> RlweCiphertext:
+    """hw/tfhe.py:373-387: pack <= N extracted-LWE ciphertexts into one RLWE whose
+    coefficient i decrypts to message i (also accepts packed (N+1,) rows)."""
+    params = ksk.params
+    n = params.n
+    if len(cs) > n:
+        raise TfheError(f"cannot pack {len(cs)} > N = {n} ciphertexts")
+    if len(cs) == 0:
+        return RlweCiphertext(params, np.zeros((2, n), dtype=U32))
+    out_rows = []
+    for c in cs:
+        if isinstance(c, LweCiphertext):
+            _check_params(c.params, params)
+            out_rows.append(c.row())
+        else:
+            out_rows.append(np.asarray(c if isinstance(c, np.ndarray) else to_host(c), dtype=U32))
+    rows = np.stack(out_rows)
     b = np.zeros(n, dtype=U32)
     b[: len(rows)] = rows[:, n]
     out = pack_batch(rows[None, :, :n], b[None], ksk)[0]
@@ -554,6 +589,9 @@ def measure_noise(ct, key, params: HeParams | None = None) -> NoiseBudget:
     if isinstance(ct, RlweCiphertext):
         params = ct.params
         phase = phase_rlwe(ct, key).astype(np.int64)
+    elif isinstance(ct, LweCiphertext):
+        params = ct.params
+        phase = np.array([int(phase_lwe(ct, key))], dtype=np.int64)
     else:
         params = params or key.params
         phase = phase_lwe_batch(ct, key.s).astype(np.int64)
@@ -731,13 +769,30 @@ def sample_extract_batch(params: HeParams, rlwe, coeff: int = 0):
     return _wrap(rlwe, out)
 
 
-def extract_lwe(c: RlweCiphertext, i: int = 0):
-    """hw/tfhe.py:352-361: LWE (N+1,) of coefficient i under S1, b last."""
+def extract_lwe(c: RlweCiphertext, i: int = 0) -> LweCiphertext:
+    """hw/tfhe.py:352-361: LWE of coefficient i under the coefficients of S1
+    (a'[j] = a[i-j] for j <= i, -a[N+i-j] above; b' = b[i]) -- on the GPU."""
     n = c.params.n
     if not 0 <= i < n:
         raise TfheError(f"coefficient index {i} out of range [0, {n})")
     data = c.data[None] if isinstance(c.data, np.ndarray) else c.data.unsqueeze(0)
-    return sample_extract_batch(c.params, data, i)[0]
+    return LweCiphertext.from_row(c.params, sample_extract_batch(c.params, data, i)[0])
+
+
+def _key_coeffs(key) -> np.ndarray:
+    # SecretKey.extracted (S1's coefficients, hw/tfhe.py:64-66) or LweSecretKey.s
+    return np.asarray(key.extracted if hasattr(key, "extracted") else key.s, dtype=U64)
+
+
+def phase_lwe(ct: LweCiphertext, key) -> np.uint32:
+    """hw/tfhe.py:364-366: b - <a, s> mod 2^32 (key: SecretKey or LweSecretKey)."""
+    dot = (np.asarray(ct.a, dtype=U64) * _key_coeffs(key)).sum(dtype=U64)
+    return U32((int(ct.b) - int(dot)) & MASK32)
+
+
+def dec_lwe(ct: LweCiphertext, key) -> int:
+    """hw/tfhe.py:369-370."""
+    return int(decode_phase(np.array([phase_lwe(ct, key)], dtype=U32), ct.params)[0])
 
 
 # ---------------------------------------------------------------------------
@@ -787,7 +842,7 @@ def lwe_keyswitch(params: HeParams, lwe, ksk: LweKeySwitchKey, out=None, engine:
         raise TfheError(f"out must be a contiguous int32 (B, {params.lwe_n + 1}) tensor")
     cp = _lib.c_params(params)
     if _ks_engine(params, ksk, engine):
-        ws = (workspace or _default_ws).get(params, B, t.device, kind="ks_tc")
+        ws = _ws(workspace).get(params, B, t.device, kind="ks_tc")
         _lib.check(_lib.load().hwb_keyswitch_tc(ctypes.byref(cp), _ptr(ksk.tensor_core_tiles()), _ptr(t),
                                                 _ptr(out), B, _ptr(ws), _stream()))
     else:
@@ -817,7 +872,23 @@ class PbsWorkspace:
         return self.buf
 
 
-_default_ws = PbsWorkspace()
+_default_ws: dict = {}
+_default_ws_lock = threading.Lock()
+
+
+def _ws(workspace: "PbsWorkspace | None") -> PbsWorkspace:
+    """The caller's workspace, else a default one per (device, current stream): two
+    threads or streams running PBS concurrently never share scratch memory, and a
+    resize only frees a buffer last used on the same stream (the caching allocator
+    orders its reuse after that stream's queued kernels)."""
+    if workspace is not None:
+        return workspace
+    key = (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream)
+    with _default_ws_lock:
+        ws = _default_ws.get(key)
+        if ws is None:
+            ws = _default_ws[key] = PbsWorkspace()
+    return ws
 
 
 def _use_fft_ladder(bsk: BootstrapKey, B: int, ladder: str) -> bool:
@@ -875,16 +946,16 @@ def pbs_batch(params: HeParams, lwe, tv, bsk: BootstrapKey, ksk: LweKeySwitchKey
             # one runs as a separate pass
             ext = pbs_batch(params, t, tvt, bsk, None, workspace=workspace, ladder="fft")
             return _wrap(lwe, lwe_keyswitch(params, ext, ksk, out=out, engine=engine, workspace=workspace))
-        ws = (workspace or _default_ws).get(params, B, t.device, kind="pbs_fft_ks" if ks_tc else "pbs_fft")
+        ws = _ws(workspace).get(params, B, t.device, kind="pbs_fft_ks" if ks_tc else "pbs_fft")
         _lib.check(_lib.load().hwb_pbs_fft(ctypes.byref(cp), _ptr(bsk.fft),
                                            _ptr(ksk.tensor_core_tiles() if ks_tc else None), _ptr(tvt), per_item,
                                            _ptr(t), _ptr(out), B, _ptr(ws), _stream()))
     elif _ks_engine(params, ksk, engine):
-        ws = (workspace or _default_ws).get(params, B, t.device, kind="pbs_tc")
+        ws = _ws(workspace).get(params, B, t.device, kind="pbs_tc")
         _lib.check(_lib.load().hwb_pbs_tc(ctypes.byref(cp), _ptr(bsk.ntt.data), _ptr(ksk.tensor_core_tiles()),
                                           _ptr(tvt), per_item, _ptr(t), _ptr(out), B, _ptr(ws), _stream()))
     else:
-        ws = (workspace or _default_ws).get(params, B, t.device) if ksk is not None else None
+        ws = _ws(workspace).get(params, B, t.device) if ksk is not None else None
         _lib.check(_lib.load().hwb_pbs(ctypes.byref(cp), _ptr(bsk.ntt.data), _ptr(ksk.data if ksk else None),
                                        _ptr(tvt), per_item, _ptr(t), _ptr(out), B, _ptr(ws), _stream()))
     return _wrap(lwe, out)

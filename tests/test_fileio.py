@@ -42,7 +42,7 @@ def samples():
     out = []
     for d, lab in O["samples"]:
         stack = d if lab is None else np.concatenate([d, lab])
-        out.append(hewnn.EncryptedSample(P, stack, d.shape[0], 0 if lab is None else lab.shape[0]))
+        out.append(hewnn.EncryptedSample.from_stack(P, stack, d.shape[0], 0 if lab is None else lab.shape[0]))
     return out
 
 
@@ -86,7 +86,7 @@ def test_reader_loads_reference_files():
     got = list(F.read_samples(os.path.join(FIX, "samples.hwsd")))
     assert len(got) == 2
     for g, w in zip(got, samples()):
-        assert (g.s, g.label_bits) == (w.s, w.label_bits) and np.array_equal(g.rgsw, w.rgsw)
+        assert (g.s, g.n_label_bits) == (w.s, w.n_label_bits) and np.array_equal(g.rgsw, w.rgsw)
     assert F.samples_meta(os.path.join(FIX, "samples.hwsd"))["source"] == "fixture"
     m = F.load_he_model(os.path.join(FIX, "he_model.hwsd"), device=False)
     assert m.geometry == GEO
@@ -187,7 +187,7 @@ def test_train_from_hwsd_stream(tmp_path):
     P, s1, bits, labels, stacks = train_inputs(name)
     s, l, a, r = TRAIN_CASES[name][2]
     lb = max(1, (l - 1).bit_length())
-    smp = [hewnn.EncryptedSample(P, st, s, lb) for st in stacks]
+    smp = [hewnn.EncryptedSample.from_stack(P, st, s, lb) for st in stacks]
     path = tmp_path / "train.hwsd"
     assert F.write_samples(path, smp, P, {"case": name}) == len(smp)
     stream = F.read_samples(path, pin=True, expect_params=P)

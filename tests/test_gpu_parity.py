@@ -148,8 +148,10 @@ def test_sample_extract_all_positions(coeff):
     P = emb_params(10, 3, 7)
     c = rand_u32(rng, (2, 1024))
     a, b = o.extract_lwe(c, coeff)
-    out = tfhe.extract_lwe(tfhe.RlweCiphertext(P, c), coeff)
-    assert_u32_equal(out, np.concatenate([a, [b]]))
+    out = tfhe.extract_lwe(tfhe.RlweCiphertext(P, c), coeff)               # -> LweCiphertext
+    assert_u32_equal(out.a, a)
+    assert int(out.b) == int(b)
+    assert_u32_equal(out.row(), np.concatenate([a, [b]]))
 
 
 # ---------------------------------------------------------------- key switch and PBS

@@ -31,7 +31,7 @@ def samples_of(name, device=True):
     P, s1, bits, labels, stacks = train_inputs(name)
     s, l, a, r = TRAIN_CASES[name][2]
     lb = max(1, (l - 1).bit_length())
-    smp = [hewnn.EncryptedSample(P, tfhe.to_device(st) if device else st, s, lb) for st in stacks]
+    smp = [hewnn.EncryptedSample.from_stack(P, tfhe.to_device(st) if device else st, s, lb) for st in stacks]
     return P, s1, bits, labels, smp, wnn.WisardGeometry(s, l, a, r, P.p)
 
 
@@ -46,8 +46,8 @@ def test_he_train_matches_reference(name, batch, ladder):
     assert sha(rams) == str(g["sha_rams"])
     assert_u32_equal(rams[:, :2], g["rams_head"])
     assert_u32_equal(tfhe.to_host(model.counts_ct), g["counts_ct"])
-    counters, cc = hewnn.decrypt_model(model, tfhe.SecretKey(P, s1))
-    assert np.array_equal(counters, g["counters"])
+    plain, cc = hewnn.decrypt_model(model, tfhe.SecretKey(P, s1))
+    assert np.array_equal(plain.counters, g["counters"])
     assert np.array_equal(cc.counts, g["class_counts"])
 
 
@@ -59,7 +59,7 @@ def test_he_train_from_host_stacks_staged(host):
     g = golden(f"{name}.npz")
     P, s1, bits, labels, smp, geom = samples_of(name, device=False)
     if host == "pinned":
-        smp = [hewnn.EncryptedSample(P, torch.from_numpy(x.rgsw.view(np.int32)).pin_memory(), x.s, x.label_bits)
+        smp = [hewnn.EncryptedSample.from_stack(P, torch.from_numpy(x.rgsw.view(np.int32)).pin_memory(), x.s, x.n_label_bits)
                for x in smp]
     for batch in (1, 2):
         model = hewnn.he_train(smp, geom, P, batch=batch)
@@ -90,6 +90,25 @@ def test_device_rgsw_encryption_matches_host():
     key4 = tfhe.SecretKey(P4, tfhe.make_rng(3).integers(0, 2, P4.n).astype(np.uint32))
     host4 = np.stack([c.data for c in tfhe.enc_rgsw_batch(ms[:5], key4, tfhe.make_rng(6))])
     assert_u32_equal(tfhe.to_host(hewnn.enc_rgsw_batch_device(ms[:5], key4, tfhe.make_rng(6))), host4)
+
+
+def test_device_key_cache_never_stale():
+    """Advisor finding: the device image of a secret key must follow the key object
+    (a fresh key at a reused address, or a key changed in place, is re-uploaded)."""
+    P = named_params("CFG2", 256)
+    ms = tfhe.make_rng(4).integers(0, 2, 9)
+    for seed in (11, 12, 13):                        # keys created and dropped in sequence
+        key = tfhe.SecretKey(P, tfhe.make_rng(seed).integers(0, 2, P.n).astype(np.uint32))
+        host = np.stack([c.data for c in tfhe.enc_rgsw_batch(ms, key, tfhe.make_rng(5))])
+        assert_u32_equal(tfhe.to_host(hewnn.enc_rgsw_batch_device(ms, key, tfhe.make_rng(5))), host)
+        del key
+    key = tfhe.SecretKey(P, tfhe.make_rng(14).integers(0, 2, P.n).astype(np.uint32))
+    hewnn.enc_rgsw_batch_device(ms, key, tfhe.make_rng(5))
+    key.s[:] = 1 - key.s                             # mutated in place
+    host = np.stack([c.data for c in tfhe.enc_rgsw_batch(ms, key, tfhe.make_rng(5))])
+    assert_u32_equal(tfhe.to_host(hewnn.enc_rgsw_batch_device(ms, key, tfhe.make_rng(5))), host)
+    for c, m in zip(tfhe.enc_rgsw_batch(ms, key, tfhe.make_rng(6)), ms):
+        assert tfhe.dec_rgsw(c, key) == m
 
 
 def _random_codes(rng, B, k, R, clear_frac=0.25):
@@ -139,8 +158,8 @@ def test_lut_roundtrip_decrypts():
         expect = np.zeros(4 * P.n, dtype=np.int64)
         expect[m] = 5
         assert np.array_equal(dec, expect)
-        out = lut.vertical_packing(sel, [tfhe.RlweCiphertext(P, r) for r in rows])
-        assert tfhe.dec_lwe_batch(out[None], key)[0] == 5
+        out = lut.vertical_packing(sel, lut.EncryptedLut([tfhe.RlweCiphertext(P, r) for r in rows], k))
+        assert isinstance(out, tfhe.LweCiphertext) and tfhe.dec_lwe(out, key) == 5
 
 
 def test_monomial_gather_vs_oracle():
@@ -161,7 +180,7 @@ def test_pack_batch_and_he_infer_pd_match_reference():
     model = hewnn.he_train(smp, geom, P)
     test_rgsw = o.enc_rgsw_batch(g["test_bits"], s1, P.sigma, P.gadget.levels, P.gadget.base_log, o.make_rng(13))
     assert sha(test_rgsw) == str(g["sha_test_rgsw"])
-    tsample = hewnn.EncryptedSample(P, tfhe.to_device(test_rgsw), geom.s, 0)
+    tsample = hewnn.EncryptedSample.from_stack(P, tfhe.to_device(test_rgsw), geom.s, 0)
     pack = hewnn.he_infer_pd(model, tsample, pksk)                                         # hw/hewnn.py:278
     assert_u32_equal(pack.packed, g["infer_packed"])
     assert_u32_equal(hewnn.he_infer_pd_batch(model, [tsample], pksk, ladder="ntt")[0].packed, g["infer_packed"])
@@ -193,9 +212,9 @@ def test_full_geometry_training_vs_oracle(cfg):
     assert_u32_equal(tfhe.to_host(model.rams), rams)
     assert_u32_equal(tfhe.to_host(model.counts_ct), counts)
     if cfg != 4:
-        counters, cc = hewnn.decrypt_model(model, key)
+        plain, cc = hewnn.decrypt_model(model, key)
         ref, rc = wnn.train_integer(ds.bits, ds.labels, geom)
-        assert np.array_equal(counters, ref) and np.array_equal(cc.counts, rc.counts)
+        assert np.array_equal(plain.counters, ref.counters) and np.array_equal(cc.counts, rc.counts)
 
 
 def test_he_train_multi_equals_separate_runs():
@@ -219,8 +238,8 @@ def test_client_helpers():
     nb = tfhe.measure_noise(tfhe.RlweCiphertext(P, tfhe.to_host(model.rams[0, 0])), key)
     assert nb.ok and nb.max_abs == hewnn.model_noise(model, key)[0] or nb.max_abs <= hewnn.model_noise(model, key)[0]
     rows = lut.ivp_batch([[lut.SelectorBit.clear(1)] * 4], tfhe.trivial_rlwe(3, P).data, P)[0]
-    polys = [tfhe.RlweCiphertext(P, r) for r in rows]
-    vals = lut.decode_lut(lut.lut_add(polys, polys), 4, key)                  # hw/lut.py:100-110
+    polys = lut.EncryptedLut([tfhe.RlweCiphertext(P, r) for r in rows], 4)
+    vals = lut.decode_lut(lut.lut_add(polys, polys), key)                     # hw/lut.py:100-110
     expect = np.zeros(16, dtype=np.int64)
     expect[15] = 6
     assert np.array_equal(vals, expect)

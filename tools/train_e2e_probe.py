@@ -31,7 +31,7 @@ def main(images=128, batch=32):
     rng = tfhe.make_rng(2)
     dev = [hewnn.encrypt_sample(ds.bits[i], int(ds.labels[i]), key, rng, label_bits=geom.label_bits, device=True)
            for i in range(images)]
-    host = [hewnn.EncryptedSample(P, d.rgsw.cpu().pin_memory(), d.s, d.label_bits) for d in dev]
+    host = [hewnn.EncryptedSample.from_stack(P, d.rgsw.cpu().pin_memory(), d.s, d.n_label_bits) for d in dev]
     hewnn.he_train(dev[:batch], geom, P, batch=batch)
     hewnn.he_train(host[:batch], geom, P, batch=batch)
     nbytes = sum(h.rgsw.numel() * 4 for h in host)
@@ -64,7 +64,7 @@ def timeline(images=128, batch=32):
     key, _ = tfhe.keygen(P, 1)
     ds = data.config_dataset(3, n=images)
     rng = tfhe.make_rng(2)
-    host = [hewnn.EncryptedSample(P, hewnn.encrypt_sample(ds.bits[i], int(ds.labels[i]), key, rng,
+    host = [hewnn.EncryptedSample.from_stack(P, hewnn.encrypt_sample(ds.bits[i], int(ds.labels[i]), key, rng,
                                                           label_bits=geom.label_bits).rgsw.cpu().pin_memory(),
                                   s, geom.label_bits) for i in range(images)]
     hewnn.he_train(host[:batch], geom, P, batch=batch)
