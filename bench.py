@@ -545,7 +545,10 @@ def bench_hwb(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (seeded LWE encryptions, BASELINE cfg2 shapes)",
         "config": config(P, B, world, {"kernel_variant": args.variant, "ks_engine": ks_engine,
-                                       "ladder": "fp64 FFT" if use_fft else "two-prime NTT"}),
+                                       "ladder": "fp64 FFT" if use_fft else "two-prime NTT",
+                                       "launch": {"ranks": world, "backend": dist.get_backend() if world > 1
+                                                  else None, "nccl_nranks": world if world > 1 else None,
+                                                  "requested_gpus": args.gpus}}),
         "e2e": {"value": round(B * world * args.steps / (float(e2e_t.item()) * 1e-3), 2), "unit": UNIT,
                 "h2d_bytes_per_step": int(lwe.nbytes), "d2h_bytes_per_step": int(out_h.nbytes),
                 "api": "tfhe.pbs_batch from pinned host tensors", "matches_device_run": e2e_ok},
@@ -558,7 +561,12 @@ def bench_hwb(args):
                                             ("blind_rotate_fft_tm_kernel" if args.fft_mode == 1
                                              else "blind_rotate_fft_kernel") if use_fft else "ntt"),
                      "work_per_pbs": work_txt, "peak_source": peak_src,
-                     "pbs": {"roofline_pbs_per_s": round(pbs_roof, 1),
+                     "traffic_note": ("ncu --set full flushes L2 before each replayed launch, so the "
+                                      "64-step segment's accumulators (B x 8 KB) and key slices are read "
+                                      "from DRAM; bench runs keep them L2-resident (see "
+                                      "profiles/r02_dram_no_flush.txt)") if use_fft else None,
+                     "context": {}}}
+    ctx = {"pbs": {"roofline_pbs_per_s": round(pbs_roof, 1),
                              "frac": round(B / (max_ms / args.steps * 1e-3) / pbs_roof, 4),
                              "formula": ("1 / (W/P + 4 W_ks/P_i8)" if ks_tc else "W/P only")
                              + (" with W = W_fp64, P = P_fp64" if use_fft else " with W = W_mm, P = P_mm")},
@@ -575,13 +583,18 @@ def bench_hwb(args):
                                   "peak": round(p_mm / 1e9, 2), "unit": "G RNS-modmul/s",
                                   "work_per_pbs": f"W_mm = {w_mm} RNS modmuls (NTT formulation, SURVEY §8(d))",
                                   "formula": "1 / (W_mm/P_mm + 4 W_ks/P_i8)" if ks_tc else "W_mm/P_mm",
-                                  "peak_source": "measured live: probe_modmul_kernel (register-only Shoup, both primes)"}},
+                                  "peak_source": "measured live: probe_modmul_kernel (register-only Shoup, both primes)",
+                                  "note": ("context only: SURVEY §8(d)'s roofline of the NTT formulation on the "
+                                           "integer pipe; the FFT ladder computes the same exact products on the "
+                                           "FP64 pipe, whose own fraction (above) is the number of record")}}
+    result["roofline"]["context"] = ctx
+    result.update({
         "kernel_ms": {"blind_rotate": round(statistics.mean(br_ms), 3),
                       "keyswitch": round(statistics.mean(ks_ms), 3)},
         "gpu_launches": ((-(-P.lwe_n // 64) if use_fft else 1) + (2 if ks_tc else 1)) * args.steps,
         "clocks": clock_info,
         "check": "all outputs decrypt to the LUT" if ok else "DECRYPTION MISMATCH",
-    }
+    })
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = cpu_threads()
         sample = args.cpu_sample or max(16, min(256, 2 * threads))
@@ -697,8 +710,28 @@ def bench_reference(args):
     }), flush=True)
 
 
+def _self_launch(args) -> bool:
+    """`bench.py --gpus N` outside torchrun: re-exec this script under
+    torch.distributed.run with N ranks (one per GPU, NCCL, 127.0.0.1 rendezvous) so
+    a direct call really runs on N GPUs.  Returns True when the child ran."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
+        return False
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    rc = subprocess.call(cmd)
+    if rc:
+        sys.exit(rc)
+    return True
+
+
 def main():
     args = parse()
+    if _self_launch(args):
+        return
     if args.impl == "reference":
         bench_reference(args)
     else:

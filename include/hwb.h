@@ -158,6 +158,19 @@ int hwb_poly_to_ntt(const hwb_params *p, const uint32_t *in, uint32_t *out, int6
 int hwb_key_mul(const hwb_params *p, const uint32_t *key_ntt, const uint32_t *in, const uint32_t *add,
                 uint32_t *out, int64_t npolys, void *stream);
 
+/* LWE linear combination (NEW; the affine steps between the bootstraps of the
+ * PBS inference pipeline, paper_2403_20190_b200/infer_pbs.py): for b < B, k < width
+ *   out[b][k] = ((cx[b] x[b][k] + cy[b] y[b][k]) << shift) + (k == width-1 ? cb[b] : 0)
+ * mod 2^32.  cx NULL = 1; y NULL (or cy NULL) drops the y term; cb NULL = 0.
+ * out may alias x or y.  The word at width-1 is the LWE body b. */
+int hwb_lwe_lincomb(const uint32_t *x, const uint32_t *y, uint32_t *out, const int32_t *cx, const int32_t *cy,
+                    const uint32_t *cb, int64_t B, int32_t width, int32_t shift, void *stream);
+
+/* Row gather out[b] = table[idx[b]] (rows of row_words words, a multiple of 4,
+ * 16-byte aligned): per-item test polynomials drawn from a table of LUTs. */
+int hwb_gather_rows(const uint32_t *table, const int32_t *idx, uint32_t *out, int64_t B, int32_t row_words,
+                    void *stream);
+
 /* Add the RGSW gadget term m * q/beta^(t+1) (hw/tfhe.py:259-262) to B RGSW
  * ciphertexts [B][2l][2][N] for selector bits[B] in {0, 1}. */
 int hwb_rgsw_add_gadget(const hwb_params *p, uint32_t *rgsw, const int32_t *bits, int64_t B, void *stream);

@@ -31,7 +31,8 @@ EXPORTS = (
     "hwb_pbs_fft_workspace_bytes", "hwb_set_fft_segment", "hwb_probe_fp64",
     "hwb_ggsw_fft_bytes", "hwb_ggsw_to_fft", "hwb_blind_rotate_fft", "hwb_ivp_level_fft", "hwb_vp_level_fft",
     "hwb_set_fft_group", "hwb_set_fft_latency_batch", "hwb_set_fft_mode", "hwb_set_fft_cluster_batch",
-    "hwb_fft_cluster_capacity", "hwb_set_fft_cluster_mode", "hwb_fft_margin",
+    "hwb_fft_cluster_capacity", "hwb_set_fft_cluster_mode", "hwb_fft_margin", "hwb_lwe_lincomb",
+    "hwb_gather_rows",
 )
 
 
@@ -160,6 +161,8 @@ def _configure(L: ctypes.CDLL) -> ctypes.CDLL:
                         "hwb_fft_cluster_capacity", *sizes):
             getattr(L, name).restype = ctypes.c_int
     L.hwb_fft_margin.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int]
+    L.hwb_lwe_lincomb.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _i64, ctypes.c_int32, ctypes.c_int32, _vp]
+    L.hwb_gather_rows.argtypes = [_vp, _vp, _vp, _i64, ctypes.c_int32, _vp]
     return L
 
 

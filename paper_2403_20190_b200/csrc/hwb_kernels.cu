@@ -530,6 +530,37 @@ __global__ void accumulate_kernel(uint32_t *__restrict__ dst, const uint32_t *__
   dst[k] += negate ? 0u - v : v;
 }
 
+// LWE linear combination (the affine steps between bootstraps of the PBS inference
+// pipeline): out[b][k] = ((cx[b] x[b][k] + cy[b] y[b][k]) << shift) + [k == W-1] cb[b]
+// mod 2^32; a NULL multiplier is 1 (cx) or 0 (y NULL), a NULL constant 0.
+__global__ void lwe_lincomb_kernel(const uint32_t *__restrict__ x, const uint32_t *__restrict__ y,
+                                   uint32_t *__restrict__ out, const int32_t *__restrict__ cx,
+                                   const int32_t *__restrict__ cy, const uint32_t *__restrict__ cb, int64_t B,
+                                   int32_t W, int32_t shift) {
+  const int64_t b = blockIdx.y * (int64_t)gridDim.z + blockIdx.z;
+  if (b >= B) return;
+  const uint32_t mx = cx ? (uint32_t)cx[b] : 1u, my = cy ? (uint32_t)cy[b] : 0u;
+  const uint32_t c = cb ? cb[b] : 0u;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < W; k += gridDim.x * blockDim.x) {
+    uint32_t v = mx * x[b * W + k];
+    if (y) v += my * y[b * W + k];
+    v <<= shift;
+    if (k == W - 1) v += c;
+    out[b * W + k] = v;
+  }
+}
+
+// out[b] = table[idx[b]] (rows of `row_words` words): per-item test polynomials
+// drawn from a small table of LUTs.
+__global__ void gather_rows_kernel(const uint32_t *__restrict__ table, const int32_t *__restrict__ idx,
+                                   uint32_t *__restrict__ out, int64_t B, int32_t row_words) {
+  const int64_t b = blockIdx.y * (int64_t)gridDim.z + blockIdx.z;
+  if (b >= B) return;
+  const uint4 *src = reinterpret_cast<const uint4 *>(table + (int64_t)idx[b] * row_words);
+  uint4 *dst = reinterpret_cast<uint4 *>(out + b * row_words);
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < row_words / 4; k += gridDim.x * blockDim.x) dst[k] = src[k];
+}
+
 __device__ __forceinline__ int mod_switch(uint32_t x, int log2m) {
   return (int)((x + (1u << (31 - log2m))) >> (32 - log2m));
 }
@@ -3075,6 +3106,33 @@ int hwb_accumulate(uint32_t *dst, const uint32_t *src, int64_t words, int64_t sr
   accumulate_kernel<<<(unsigned)((words + 255) / 256), 256, 0, (cudaStream_t)stream>>>(dst, src, words, src_words,
                                                                                          negate);
   return post_launch("accumulate_kernel");
+}
+
+static dim3 rows_grid(int64_t B, int x_blocks) {
+  // B rows over (y, z) so batches beyond 65535 rows launch
+  const int64_t z = B < 65535 ? B : 65535;
+  return dim3((unsigned)x_blocks, (unsigned)((B + z - 1) / z), (unsigned)z);
+}
+
+int hwb_lwe_lincomb(const uint32_t *x, const uint32_t *y, uint32_t *out, const int32_t *cx, const int32_t *cy,
+                    const uint32_t *cb, int64_t B, int32_t width, int32_t shift, void *stream) {
+  if (B < 0 || width < 1 || shift < 0 || shift > 31) return fail(HWB_EINVAL, "lwe_lincomb: bad shape or shift");
+  if (B == 0) return HWB_OK;
+  if (!x || !out) return fail(HWB_EINVAL, "lwe_lincomb: null pointer");
+  lwe_lincomb_kernel<<<rows_grid(B, (width + 255) / 256), 256, 0, (cudaStream_t)stream>>>(x, y, out, cx, cy, cb, B,
+                                                                                          width, shift);
+  return post_launch("lwe_lincomb_kernel");
+}
+
+int hwb_gather_rows(const uint32_t *table, const int32_t *idx, uint32_t *out, int64_t B, int32_t row_words,
+                    void *stream) {
+  if (B < 0 || row_words < 4 || (row_words & 3)) return fail(HWB_EINVAL, "gather_rows: row_words must be a multiple of 4");
+  if (B == 0) return HWB_OK;
+  if (!table || !idx || !out) return fail(HWB_EINVAL, "gather_rows: null pointer");
+  if (((uintptr_t)table | (uintptr_t)out) & 15) return fail(HWB_EINVAL, "gather_rows: 16-byte alignment");
+  gather_rows_kernel<<<rows_grid(B, (row_words / 4 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(table, idx, out,
+                                                                                                  B, row_words);
+  return post_launch("gather_rows_kernel");
 }
 
 int hwb_ext_product(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_t *ggsw_idx,

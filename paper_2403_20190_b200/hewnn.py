@@ -636,26 +636,36 @@ class FinalizeResult:
         return self.noise_max < self.noise_margin
 
 
-def he_infer_pd_batch(model: HomWisardModel, samples: Sequence[EncryptedSample],
-                      ksk: tfhe.PackingKeySwitchKey, ladder: str = "auto") -> list[ScorePack]:
-    """he_infer_pd (hw/hewnn.py:278-320) for several samples in one pass: every
-    (sample, class, RAM) triple is one vertical-packing item (clear label bits,
-    encrypted address bits), then each sample's l*k0 extracted LWEs are packed."""
+def vp_lookups(model: HomWisardModel, samples: Sequence[EncryptedSample], ladder: str = "auto") -> torch.Tensor:
+    """Every (sample, class, RAM) counter lookup of PD-act inference (hw/hewnn.py:278-311):
+    vertical packing with clear label bits and the sample's encrypted address bits.
+    Returns the extracted LWEs under S1, (S * l * k0, N+1) on the device, ordered
+    (sample, class, RAM)."""
     geometry, params = model.geometry, model.params
     for smp in samples:
         if smp.s != geometry.s:
             raise TfheError(f"sample has {smp.s} bits, geometry wants {geometry.s}")
         if smp.params != params:
             raise TfheError("sample parameter set differs from the model's")
-    n = params.n
     l, k0 = geometry.l, geometry.k0
-    total = l * k0
     tmpl = np.concatenate([_selector_template(geometry, params, clear_label=i) for i in range(l)])
     strides = np.cumsum([0] + [int(np.asarray(smp.rgsw.shape[0])) for smp in samples])
     codes = np.concatenate([_shift(tmpl, int(strides[i])) for i in range(len(samples))])
     lut_idx = np.tile(np.tile(np.arange(k0), l), len(samples))
     table = _stack_table(params, list(samples), ladder=ladder)
-    lwe = lut.vp_codes(params, codes, table, model.rams, lut_idx)          # (S*l*k0, N+1)
+    return lut.vp_codes(params, codes, table, model.rams, lut_idx)
+
+
+def he_infer_pd_batch(model: HomWisardModel, samples: Sequence[EncryptedSample],
+                      ksk: tfhe.PackingKeySwitchKey, ladder: str = "auto") -> list[ScorePack]:
+    """he_infer_pd (hw/hewnn.py:278-320) for several samples in one pass: every
+    (sample, class, RAM) triple is one vertical-packing item (clear label bits,
+    encrypted address bits), then each sample's l*k0 extracted LWEs are packed."""
+    geometry, params = model.geometry, model.params
+    n = params.n
+    l, k0 = geometry.l, geometry.k0
+    total = l * k0
+    lwe = vp_lookups(model, samples, ladder)                               # (S*l*k0, N+1)
     n_ct = -(-total // n)
     S = len(samples)
     a_st = torch.zeros((S * n_ct, n, n), dtype=torch.int32, device=lwe.device)
