@@ -166,6 +166,25 @@ int hwb_key_mul(const hwb_params *p, const uint32_t *key_ntt, const uint32_t *in
 int hwb_lwe_lincomb(const uint32_t *x, const uint32_t *y, uint32_t *out, const int32_t *cx, const int32_t *cy,
                     const uint32_t *cb, int64_t B, int32_t width, int32_t shift, void *stream);
 
+/* numpy Philox4x64-10 generator state at the start of a uniform draw (NEW): the
+ * next words of Generator.bytes() are prefix[0 .. nprefix) (still buffered in the
+ * host generator), then the uint32 stream of blocks philox(ctr + 1 + g, key). */
+typedef struct hwb_philox {
+    uint64_t key[2];
+    uint64_t ctr[4];
+    uint32_t prefix[9];
+    int32_t nprefix;
+} hwb_philox;
+
+/* Rebuild RGSW rows from a seeded encryption (NEW): pair != 0: out [rows][2][N],
+ * out[r][0][j] = word r*N + j of the uniform stream (the a half drawn by
+ * enc_rgsw_batch, hw/tfhe.py:246-263, with the 4-byte rng.bytes idiom of
+ * hw/tfhe.py:38-40) and out[r][1][j] = b_rows[r][j] (b_rows NULL: untouched);
+ * pair == 0: out [rows][N] receives the a words only.  Bit-identical to the host
+ * draw. */
+int hwb_philox_rgsw(const hwb_philox *st, const uint32_t *b_rows, uint32_t *out, int64_t rows, int32_t N,
+                    int32_t pair, void *stream);
+
 /* Row gather out[b] = table[idx[b]] (rows of row_words words, a multiple of 4,
  * 16-byte aligned): per-item test polynomials drawn from a table of LUTs. */
 int hwb_gather_rows(const uint32_t *table, const int32_t *idx, uint32_t *out, int64_t B, int32_t row_words,

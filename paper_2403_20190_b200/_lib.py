@@ -32,7 +32,7 @@ EXPORTS = (
     "hwb_ggsw_fft_bytes", "hwb_ggsw_to_fft", "hwb_blind_rotate_fft", "hwb_ivp_level_fft", "hwb_vp_level_fft",
     "hwb_set_fft_group", "hwb_set_fft_latency_batch", "hwb_set_fft_mode", "hwb_set_fft_cluster_batch",
     "hwb_fft_cluster_capacity", "hwb_set_fft_cluster_mode", "hwb_fft_margin", "hwb_lwe_lincomb",
-    "hwb_gather_rows",
+    "hwb_gather_rows", "hwb_philox_rgsw",
 )
 
 
@@ -42,6 +42,11 @@ class TfheError(ValueError):
 
 class EncodingError(TfheError):
     """Message coefficient outside Z_p (reference hw/tfhe.py:29-30)."""
+
+
+class HwbPhilox(ctypes.Structure):
+    _fields_ = [("key", ctypes.c_uint64 * 2), ("ctr", ctypes.c_uint64 * 4), ("prefix", ctypes.c_uint32 * 9),
+                ("nprefix", ctypes.c_int32)]
 
 
 class HwbParams(ctypes.Structure):
@@ -163,6 +168,7 @@ def _configure(L: ctypes.CDLL) -> ctypes.CDLL:
     L.hwb_fft_margin.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int]
     L.hwb_lwe_lincomb.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _i64, ctypes.c_int32, ctypes.c_int32, _vp]
     L.hwb_gather_rows.argtypes = [_vp, _vp, _vp, _i64, ctypes.c_int32, _vp]
+    L.hwb_philox_rgsw.argtypes = [ctypes.POINTER(HwbPhilox), _vp, _vp, _i64, ctypes.c_int32, ctypes.c_int32, _vp]
     return L
 
 

@@ -561,6 +561,62 @@ __global__ void gather_rows_kernel(const uint32_t *__restrict__ table, const int
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < row_words / 4; k += gridDim.x * blockDim.x) dst[k] = src[k];
 }
 
+// numpy's Philox4x64-10 (Random123 rounds; numpy/random/src/philox): block g of a draw
+// is philox(ctr + 1 + g, key) -- numpy increments the counter before each block --
+// and its 4 uint64 outputs give the uint32 stream low half, high half (next_uint32).
+// Generator.bytes(4 n) is that uint32 stream (hw/tfhe.py:38-40 uniform_u64 at 4-byte
+// words).  `prefix` holds the words still buffered in the host generator.
+__device__ __forceinline__ void philox4x64_10(uint64_t (&c)[4], uint64_t k0, uint64_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += 0x9E3779B97F4A7C15ull;
+      k1 += 0xBB67AE8584CAA73Bull;
+    }
+    const uint64_t lo0 = 0xD2E7470EE14C6C93ull * c[0], hi0 = __umul64hi(0xD2E7470EE14C6C93ull, c[0]);
+    const uint64_t lo1 = 0xCA5A826395121157ull * c[2], hi1 = __umul64hi(0xCA5A826395121157ull, c[2]);
+    const uint64_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+  }
+}
+
+// out[r][0][j] = word r N + j of the stream (prefix words first), out[r][1][j] = b[r][j]:
+// the RGSW rows of enc_rgsw_batch (a drawn by rng.bytes, hw/tfhe.py:246-263) rebuilt
+// from the generator state and the shipped b half.
+__global__ void philox_rgsw_kernel(hwb_philox st, const uint32_t *__restrict__ b_rows, uint32_t *__restrict__ out,
+                                   int64_t rows, int32_t N, int32_t pair) {
+  const int64_t rs = pair ? 2 * (int64_t)N : N;     // row stride of out
+  const int64_t nwords = rows * N;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nblocks = (nwords - st.nprefix + 7) / 8;
+  if (g < nblocks) {
+    uint64_t c[4];
+    const uint64_t add = (uint64_t)g + 1;
+    c[0] = st.ctr[0] + add;
+    uint64_t carry = c[0] < add;
+#pragma unroll
+    for (int i = 1; i < 4; ++i) {
+      c[i] = st.ctr[i] + carry;
+      carry = carry && c[i] == 0;
+    }
+    philox4x64_10(c, st.key[0], st.key[1]);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t w = st.nprefix + 8 * g + q;
+      if (w < nwords) {
+        const uint64_t u = c[q >> 1];
+        out[(w / N) * rs + w % N] = (q & 1) ? (uint32_t)(u >> 32) : (uint32_t)u;
+      }
+    }
+  }
+  if (g < st.nprefix && g < nwords) out[(g / N) * rs + g % N] = st.prefix[g];
+  if (b_rows && pair)
+    for (int64_t w = g; w < nwords; w += (int64_t)gridDim.x * blockDim.x) out[(w / N) * 2 * N + N + w % N] = b_rows[w];
+}
+
 __device__ __forceinline__ int mod_switch(uint32_t x, int log2m) {
   return (int)((x + (1u << (31 - log2m))) >> (32 - log2m));
 }
@@ -3106,6 +3162,17 @@ int hwb_accumulate(uint32_t *dst, const uint32_t *src, int64_t words, int64_t sr
   accumulate_kernel<<<(unsigned)((words + 255) / 256), 256, 0, (cudaStream_t)stream>>>(dst, src, words, src_words,
                                                                                          negate);
   return post_launch("accumulate_kernel");
+}
+
+int hwb_philox_rgsw(const hwb_philox *st, const uint32_t *b_rows, uint32_t *out, int64_t rows, int32_t N,
+                    int32_t pair, void *stream) {
+  if (!st || !out || rows < 0 || N < 1 || st->nprefix < 0 || st->nprefix > 9)
+    return fail(HWB_EINVAL, "philox_rgsw: bad arguments");
+  if (rows == 0) return HWB_OK;
+  const int64_t nblocks = (rows * N + 7) / 8 + 1;
+  philox_rgsw_kernel<<<(unsigned)((nblocks + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*st, b_rows, out, rows, N,
+                                                                                          pair);
+  return post_launch("philox_rgsw_kernel");
 }
 
 static dim3 rows_grid(int64_t B, int x_blocks) {

@@ -92,6 +92,8 @@ def _i32(a, dev) -> torch.Tensor | None:
 def lincomb(x: torch.Tensor, y: torch.Tensor | None = None, cx=None, cy=None, cb=None, shift: int = 0) -> torch.Tensor:
     """((cx x + cy y) << shift) + cb on the LWE bodies, mod 2^32, per row (hwb_lwe_lincomb).
     cx, cy, cb: None, a scalar or one value per row."""
+    x = x.contiguous()                                  # the kernel reads dense (B, W) rows
+    y = None if y is None else y.contiguous()
     B, W = x.shape
     dev = x.device
 

@@ -109,6 +109,96 @@ def gaussian_u32(rng: np.random.Generator, sigma: float, shape) -> np.ndarray:
     return (e.astype(np.int64) & MASK32).astype(U32)
 
 
+# numpy Philox4x64-10 (Random123 constants; numpy/random/src/philox/philox.h): the
+# host side of seeded uniform draws whose words the GPU regenerates (hwb_philox_rgsw)
+_PH_M0, _PH_M1 = 0xD2E7470EE14C6C93, 0xCA5A826395121157
+_PH_W0, _PH_W1 = 0x9E3779B97F4A7C15, 0xBB67AE8584CAA73B
+_M64 = (1 << 64) - 1
+
+
+def philox4x64(ctr, key) -> list[int]:
+    """One Philox4x64-10 block (4 uint64) for a 256-bit counter and 128-bit key."""
+    c, k0, k1 = [int(x) for x in ctr], int(key[0]), int(key[1])
+    for r in range(10):
+        if r:
+            k0, k1 = (k0 + _PH_W0) & _M64, (k1 + _PH_W1) & _M64
+        p0, p1 = _PH_M0 * c[0], _PH_M1 * c[2]
+        c = [(p1 >> 64) ^ c[1] ^ k0, p1 & _M64, (p0 >> 64) ^ c[3] ^ k1, p0 & _M64]
+    return c
+
+
+def _ctr_add(ctr, n: int) -> list[int]:
+    v = sum(int(x) << (64 * i) for i, x in enumerate(ctr)) + n
+    v &= (1 << 256) - 1
+    return [(v >> (64 * i)) & _M64 for i in range(4)]
+
+
+def philox_take(rng: np.random.Generator, nwords: int):
+    """Claim the next `nwords` uint32 of rng's stream -- exactly what rng.bytes(4 nwords)
+    (hw/tfhe.py:38-40) would return -- WITHOUT generating them on the host: returns the
+    hwb_philox block the GPU regenerates them from and leaves rng in the state
+    rng.bytes would have left (bit-identical continuation)."""
+    bg = rng.bit_generator
+    st = bg.state
+    if st.get("bit_generator") != "Philox":
+        raise TfheError("seeded draws need a numpy Philox generator (make_rng)")
+    inner = st["state"]
+    ctr = [int(x) for x in inner["counter"]]
+    key = [int(x) for x in inner["key"]]
+    buf = [int(x) for x in st["buffer"]]
+    pos, has32, uint = int(st["buffer_pos"]), int(st["has_uint32"]), int(st["uinteger"])
+    prefix = [uint] if has32 else []
+    for u in buf[pos:]:
+        prefix += [u & 0xFFFFFFFF, u >> 32]
+    out = _lib.HwbPhilox()
+    out.key[:] = key
+    out.ctr[:] = ctr
+    if nwords <= len(prefix):
+        # served from the host buffer alone
+        take = prefix[:nwords]
+        out.prefix[: len(take)] = take
+        out.nprefix = len(take)
+        used = nwords - (1 if has32 else 0)              # words taken from buffer uint64s
+        if has32 and nwords >= 1:
+            has32 = 0
+        if used > 0:
+            pos += (used + 1) // 2
+            if used % 2:
+                has32, uint = 1, buf[pos - 1] >> 32
+        new = dict(st, buffer_pos=pos, has_uint32=has32, uinteger=uint)
+        bg.state = new
+        return out
+    out.prefix[: len(prefix)] = prefix
+    out.nprefix = len(prefix)
+    m = nwords - len(prefix)                             # words from fresh blocks ctr+1, ctr+2, ...
+    n64 = (m + 1) // 2
+    nblk = (n64 + 3) // 4
+    last_ctr = _ctr_add(ctr, nblk)
+    last = philox4x64(last_ctr, key)
+    new_pos = n64 - 4 * (nblk - 1)
+    if m % 2:
+        has32, uint = 1, last[new_pos - 1] >> 32
+    else:
+        has32, uint = 0, last[new_pos - 1] >> 32
+    bg.state = {"bit_generator": "Philox",
+                "state": {"counter": np.array(last_ctr, dtype=np.uint64), "key": np.array(key, dtype=np.uint64)},
+                "buffer": np.array(last, dtype=np.uint64), "buffer_pos": new_pos, "has_uint32": has32,
+                "uinteger": uint}
+    return out
+
+
+def philox_rgsw(st, rows: int, N: int, b_rows: torch.Tensor | None = None, out: torch.Tensor | None = None,
+                pair: bool = True) -> torch.Tensor:
+    """GPU regeneration of a seeded draw (hwb_philox_rgsw): (rows, 2, N) RGSW rows with
+    a from the stream and b from b_rows, or (rows, N) a words (pair=False)."""
+    dev = _device()
+    if out is None:
+        out = torch.empty((rows, 2, N) if pair else (rows, N), dtype=torch.int32, device=dev)
+    _lib.check(_lib.load().hwb_philox_rgsw(ctypes.byref(st), _ptr(b_rows), _ptr(out), rows, N, int(pair),
+                                           _stream()))
+    return out
+
+
 def _key_mul_host(x: np.ndarray, s: np.ndarray) -> np.ndarray:
     """x * s mod 2^32 for binary s, exactly: 16-bit limbs through a float64 FFT
     (the limb-exact product of hw/fft.py:88-119; limb sums < N 2^16 < 2^53)."""
