@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--train-images", type=int, default=128, help="0 disables the training measurement")
     ap.add_argument("--train-batch", type=int, default=32)
     ap.add_argument("--infer-images", type=int, default=32, help="0 disables the inference measurement")
+    ap.add_argument("--infer-pbs-images", type=int, default=4,
+                    help="images for the fully encrypted bleach/popcount/argmax inference (0 disables)")
+    ap.add_argument("--infer-pbs-thr", type=int, default=0, help="bleaching threshold of that inference")
     ap.add_argument("--no-other-configs", dest="other_configs", action="store_false",
                     help="skip the cfg1/cfg4 PBS measurements")
     ap.add_argument("--sweep", default="1,16,148,592,1184,4096,16384,65536",
@@ -290,11 +293,14 @@ def bench_train(args, world, rank, torch, dist):
     ds = data.config_dataset(cfg, n=images, seed=rank)
     key = tfhe.SecretKey(P, tfhe.make_rng(KEY_SEED).integers(0, 2, P.n).astype(np.uint32))
     rng = tfhe.make_rng(ENC_SEED + 1000 * rank)
+    # client: seeded encryption -- host draws the normals only, the GPU regenerates the
+    # uniform a-halves from the Philox stream and forms b; the wire form is b + seeds
     t0 = time.perf_counter()
-    samples = [hewnn.encrypt_sample(ds.bits[i], int(ds.labels[i]), key, rng, label_bits=geom.label_bits)
-               for i in range(images)]
+    seeded = [hewnn.encrypt_sample_seeded(ds.bits[i], int(ds.labels[i]), key, rng, label_bits=geom.label_bits)
+              for i in range(images)]
     torch.cuda.synchronize()
     enc_s = time.perf_counter() - t0
+    samples = [hewnn.EncryptedSample.from_stack(P, x.rgsw.expand(), x.s, x.n_label_bits) for x in seeded]
     hewnn.he_train(samples[:batch], geom, P, batch=batch)                    # warm-up
     torch.cuda.synchronize()
     if world > 1:
@@ -310,9 +316,9 @@ def bench_train(args, world, rank, torch, dist):
     ok = bool(np.array_equal(dm.counters, ref.counters) and np.array_equal(cc.counts, rc.counts))
     noise, margin = hewnn.model_noise(model, key)
     frac_ok = float(np.mean(dm.counters == ref.counters))
-    # end to end from pinned host ciphertexts, model read back
-    host = [hewnn.EncryptedSample.from_stack(P, smp.rgsw.cpu().pin_memory(), smp.s, smp.n_label_bits) for smp in samples]
-    h2d = sum(int(h.rgsw.numel()) * 4 for h in host)
+    # end to end from the pinned host wire form (b halves + Philox states), model read back
+    host = seeded
+    h2d = sum(int(h.rgsw.b.numel() + h.rgsw.a0.numel()) * 4 + 80 * len(h.rgsw.segments) for h in host)
     rams_pin = torch.empty(model.rams.shape, dtype=torch.int32).pin_memory()
     del samples
     # warm the pinned-host pipeline once (two chunks in flight: the staging and table
@@ -341,7 +347,8 @@ def bench_train(args, world, rank, torch, dist):
                       "data": "synthetic (data.config_dataset)"},
            "e2e": {"value": round(images * world / (float(te.item()) * 1e-3), 2), "unit": "images/s",
                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(model.rams.numel()) * 4,
-                   "api": "hewnn.he_train from pinned host RGSW stacks, model read back"},
+                   "api": "hewnn.he_train from pinned host seeded RGSW stacks (b halves + Philox states; "
+                          "the GPU regenerates a), model read back"},
            "client_encrypt_s_per_image": round(enc_s / images, 4),
            "noise": {"max_log2": round(float(np.log2(max(noise, 1))), 2),
                      "margin_log2": round(float(np.log2(margin)), 2), "counters_correct": round(frac_ok, 6)},
@@ -370,6 +377,9 @@ def bench_train(args, world, rank, torch, dist):
                         "packed_rlwe_per_image": -(-vp_items // P.n),
                         "check": "predictions == plaintext evaluate" if list(plain) == preds
                         else "PREDICTION MISMATCH"}
+        if args.infer_pbs_images > 0:
+            out["infer_pbs"] = bench_infer_pbs(args, model, key, ref, tsamples[: args.infer_pbs_images],
+                                               tds.bits[: args.infer_pbs_images], torch)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import coracle, wnn32
         coracle.build()
@@ -382,6 +392,37 @@ def bench_train(args, world, rank, torch, dist):
                                "kind": "port", "sample": f"{n_cpu} cfg{cfg} images, oracle/wnn32.he_train "
                                                          f"(C oracle exact ext products, OpenMP)"}
     return out
+
+
+def bench_infer_pbs(args, model, key, ref, tsamples, tbits, torch):
+    """OTF-act inference entirely on ciphertexts (paper_2403_20190_b200.infer_pbs):
+    VP lookups, bleaching threshold, popcount and argmax on the batched PBS engine,
+    self-bootstrapping (n = N) under the training key; the client only decrypts
+    the class index.  Checked against wnn.evaluate_dataset(bin thr)."""
+    from paper_2403_20190_b200 import infer_pbs, wnn
+    thr = args.infer_pbs_thr
+    k0 = time.perf_counter()
+    sbk = infer_pbs.self_bootstrap_keygen(key, KEY_SEED + 11)
+    keygen_s = time.perf_counter() - k0
+    infer_pbs.he_infer_bin_batch(model, tsamples[:1], sbk, thr)          # warm-up (LUT tables, workspaces)
+    torch.cuda.synchronize()
+    stats: dict = {}
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record()
+    preds = infer_pbs.he_infer_bin_batch(model, tsamples, sbk, thr, stats=stats)
+    g1.record()
+    g1.synchronize()
+    sec = g0.elapsed_time(g1) * 1e-3
+    got = [infer_pbs.decrypt_prediction(p, key) for p in preds]
+    want = list(wnn.evaluate_dataset(ref, tbits, wnn.ActivationSpec("bin", thr)))
+    n = len(tsamples)
+    return {"metric": "encrypted bleaching-threshold inference images/sec", "unit": "images/s",
+            "value": round(n / sec, 3), "images": n, "thr": thr,
+            "pbs_per_s": round(stats["pbs"] / sec, 1), "pbs_per_image": stats["pbs"] // n,
+            "pbs_rounds": stats["rounds"], "self_bsk": f"n = N = {model.params.n} (no key switch)",
+            "client_keygen_s": round(keygen_s, 2),
+            "note": "timed region includes the VP lookups; PBS/s counts bootstraps only",
+            "check": "encrypted argmax == evaluate_dataset(bin thr)" if got == want else "PREDICTION MISMATCH"}
 
 
 def bench_hwb(args):

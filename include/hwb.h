@@ -180,10 +180,12 @@ typedef struct hwb_philox {
  * out[r][0][j] = word r*N + j of the uniform stream (the a half drawn by
  * enc_rgsw_batch, hw/tfhe.py:246-263, with the 4-byte rng.bytes idiom of
  * hw/tfhe.py:38-40) and out[r][1][j] = b_rows[r][j] (b_rows NULL: untouched);
- * pair == 0: out [rows][N] receives the a words only.  Bit-identical to the host
- * draw. */
-int hwb_philox_rgsw(const hwb_philox *st, const uint32_t *b_rows, uint32_t *out, int64_t rows, int32_t N,
-                    int32_t pair, void *stream);
+ * pair == 0: out [rows][N] receives the a words only.  a0fix (NULL: none) holds,
+ * per RGSW (2*levels rows), the levels words a[l+t][0] that carry the gadget term
+ * m g_t (hw/tfhe.py:259-262); they replace the regenerated words.  Bit-identical
+ * to the host draw. */
+int hwb_philox_rgsw(const hwb_philox *st, const uint32_t *b_rows, const uint32_t *a0fix, int32_t levels,
+                    uint32_t *out, int64_t rows, int32_t N, int32_t pair, void *stream);
 
 /* Row gather out[b] = table[idx[b]] (rows of row_words words, a multiple of 4,
  * 16-byte aligned): per-item test polynomials drawn from a table of LUTs. */

@@ -168,7 +168,8 @@ def _configure(L: ctypes.CDLL) -> ctypes.CDLL:
     L.hwb_fft_margin.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int]
     L.hwb_lwe_lincomb.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _i64, ctypes.c_int32, ctypes.c_int32, _vp]
     L.hwb_gather_rows.argtypes = [_vp, _vp, _vp, _i64, ctypes.c_int32, _vp]
-    L.hwb_philox_rgsw.argtypes = [ctypes.POINTER(HwbPhilox), _vp, _vp, _i64, ctypes.c_int32, ctypes.c_int32, _vp]
+    L.hwb_philox_rgsw.argtypes = [ctypes.POINTER(HwbPhilox), _vp, _vp, ctypes.c_int32, _vp, _i64, ctypes.c_int32,
+                                  ctypes.c_int32, _vp]
     return L
 
 

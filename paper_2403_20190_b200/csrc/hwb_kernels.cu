@@ -586,7 +586,8 @@ __device__ __forceinline__ void philox4x64_10(uint64_t (&c)[4], uint64_t k0, uin
 // out[r][0][j] = word r N + j of the stream (prefix words first), out[r][1][j] = b[r][j]:
 // the RGSW rows of enc_rgsw_batch (a drawn by rng.bytes, hw/tfhe.py:246-263) rebuilt
 // from the generator state and the shipped b half.
-__global__ void philox_rgsw_kernel(hwb_philox st, const uint32_t *__restrict__ b_rows, uint32_t *__restrict__ out,
+__global__ void philox_rgsw_kernel(hwb_philox st, const uint32_t *__restrict__ b_rows,
+                                   const uint32_t *__restrict__ a0fix, int32_t levels, uint32_t *__restrict__ out,
                                    int64_t rows, int32_t N, int32_t pair) {
   const int64_t rs = pair ? 2 * (int64_t)N : N;     // row stride of out
   const int64_t nwords = rows * N;
@@ -613,6 +614,10 @@ __global__ void philox_rgsw_kernel(hwb_philox st, const uint32_t *__restrict__ b
     }
   }
   if (g < st.nprefix && g < nwords) out[(g / N) * rs + g % N] = st.prefix[g];
+  // rows l..2l-1 of each RGSW carry the gadget term m g_t on a[0] (hw/tfhe.py:259-262):
+  // those words ship explicitly (a0fix [rows / 2l][l]) and replace the regenerated ones
+  if (a0fix && g < rows && (g % (2 * levels)) >= levels)
+    out[g * rs] = a0fix[(g / (2 * levels)) * levels + (g % (2 * levels)) - levels];
   if (b_rows && pair)
     for (int64_t w = g; w < nwords; w += (int64_t)gridDim.x * blockDim.x) out[(w / N) * 2 * N + N + w % N] = b_rows[w];
 }
@@ -3164,14 +3169,15 @@ int hwb_accumulate(uint32_t *dst, const uint32_t *src, int64_t words, int64_t sr
   return post_launch("accumulate_kernel");
 }
 
-int hwb_philox_rgsw(const hwb_philox *st, const uint32_t *b_rows, uint32_t *out, int64_t rows, int32_t N,
-                    int32_t pair, void *stream) {
+int hwb_philox_rgsw(const hwb_philox *st, const uint32_t *b_rows, const uint32_t *a0fix, int32_t levels,
+                    uint32_t *out, int64_t rows, int32_t N, int32_t pair, void *stream) {
   if (!st || !out || rows < 0 || N < 1 || st->nprefix < 0 || st->nprefix > 9)
     return fail(HWB_EINVAL, "philox_rgsw: bad arguments");
+  if (a0fix && (levels < 1 || rows % (2 * levels))) return fail(HWB_EINVAL, "philox_rgsw: rows not whole RGSWs");
   if (rows == 0) return HWB_OK;
-  const int64_t nblocks = (rows * N + 7) / 8 + 1;
-  philox_rgsw_kernel<<<(unsigned)((nblocks + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*st, b_rows, out, rows, N,
-                                                                                          pair);
+  const int64_t nblocks = ((rows * N + 7) / 8 + 1) > rows ? (rows * N + 7) / 8 + 1 : rows;
+  philox_rgsw_kernel<<<(unsigned)((nblocks + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*st, b_rows, a0fix, levels,
+                                                                                          out, rows, N, pair);
   return post_launch("philox_rgsw_kernel");
 }
 

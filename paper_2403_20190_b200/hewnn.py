@@ -73,6 +73,8 @@ class EncryptedSample:
 
     def _host_rows(self, lo: int, hi: int) -> list[RgswCiphertext]:
         st = self._stack
+        if isinstance(st, SeededRgsw):
+            st = st.expand()
         host = st[lo:hi] if isinstance(st, np.ndarray) else tfhe.to_host(st[lo:hi])
         return [RgswCiphertext(self.params, np.asarray(host[i], dtype=np.uint32)) for i in range(hi - lo)]
 
@@ -173,25 +175,29 @@ def _device_key(key: tfhe.SecretKey) -> DeviceKey:
     return dk
 
 
-def enc_rgsw_batch_device(ms, key: tfhe.SecretKey, rng) -> torch.Tensor:
-    """enc_rgsw_batch (hw/tfhe.py:246-263) with the key product on the GPU.
-
-    Same RNG stream as the host version (a then e, drawn on the host); returns
-    the device tensor (B, 2l, 2, N), bit-identical to tfhe.enc_rgsw_batch."""
+def enc_rgsw_batch_device(ms, key: tfhe.SecretKey, rng, seeded: bool = False):
+    """enc_rgsw_batch (hw/tfhe.py:246-263) with the uniform half AND the key product on
+    the GPU: the host claims the a-words of rng's Philox stream without generating
+    them (tfhe.philox_take), draws only the normals e, and the GPU regenerates a
+    (hwb_philox_rgsw) and forms b = a s + e + m g.  Same stream as the host version;
+    returns the device tensor (B, 2l, 2, N), bit-identical to tfhe.enc_rgsw_batch.
+    seeded=True returns (b rows on the device (B 2l, N), hwb_philox) instead: the
+    compressed wire form the server expands with hwb_philox_rgsw."""
     ms = np.asarray(ms, dtype=np.int64)
     params = key.params
     g = params.gadget
     rows = 2 * g.levels
     B = len(ms)
+    N = params.n
     if np.any((ms != 0) & (ms != 1)):
         raise tfhe.EncodingError("RGSW messages are bits")
-    a = tfhe.uniform_u32(rng, (B, rows, params.n))
-    e = tfhe.gaussian_u32(rng, params.sigma, (B, rows, params.n))
+    st = tfhe.philox_take(rng, B * rows * N)                   # a: claimed, not drawn
+    e = tfhe.gaussian_u32(rng, params.sigma, (B, rows, N))
     dev = tfhe._device()
-    out = torch.empty((B, rows, 2, params.n), dtype=torch.int32, device=dev)
+    out = torch.empty((B, rows, 2, N), dtype=torch.int32, device=dev)
     if B == 0:
-        return out
-    a_d = tfhe.to_device(a)
+        return (out.view(0, N), st, out[:, :0, 0, 0]) if seeded else out
+    a_d = tfhe.philox_rgsw(st, B * rows, N, pair=False)        # (B rows, N) on the GPU
     e_d = tfhe.to_device(e)
     b_d = torch.empty_like(a_d)
     dk = _device_key(key)
@@ -199,11 +205,78 @@ def enc_rgsw_batch_device(ms, key: tfhe.SecretKey, rng) -> torch.Tensor:
     L = tfhe._lib.load()
     tfhe._lib.check(L.hwb_key_mul(cp, tfhe._ptr(dk.ntt), tfhe._ptr(a_d), tfhe._ptr(e_d), tfhe._ptr(b_d),
                                   B * rows, tfhe._stream()))
-    out[:, :, 0] = a_d
-    out[:, :, 1] = b_d
+    out[:, :, 0] = a_d.view(B, rows, N)
+    out[:, :, 1] = b_d.view(B, rows, N)
     bits = torch.as_tensor(ms, dtype=torch.int32).to(dev)
     tfhe._lib.check(L.hwb_rgsw_add_gadget(cp, tfhe._ptr(out), tfhe._ptr(bits), B, tfhe._stream()))
+    if seeded:
+        # wire form: the b rows, the Philox state of the a draw, and the l words per
+        # RGSW whose a[0] carries the gadget term (they cannot be regenerated)
+        return out[:, :, 1].reshape(B * rows, N).contiguous(), st, out[:, g.levels:, 0, 0].contiguous()
     return out
+
+
+class SeededRgsw:
+    """A sample's RGSW stack in compressed (seeded) form: only the b halves
+    (R = n_rgsw 2l rows of N words, pinned host or device) plus, per encryption
+    call, the Philox state its a-words were drawn from.  expand() rebuilds the
+    full (n_rgsw, 2l, 2, N) stack on the device, bit-identical (hwb_philox_rgsw):
+    half the bytes of a plain stack cross PCIe."""
+
+    def __init__(self, params: HeParams, b_rows: torch.Tensor, a0: torch.Tensor, segments: list):
+        self.params = params
+        self.b = b_rows                                  # (R, N) int32
+        self.a0 = a0                                     # (R / 2l, l): gadget-carrying a[l+t][0] words
+        self.segments = segments                         # [(hwb_philox, row0, rows)]
+        g = params.gadget
+        self.shape = (b_rows.shape[0] // (2 * g.levels), 2 * g.levels, 2, params.n)
+        self.is_cuda = False
+
+    def numel(self) -> int:
+        return int(np.prod(self.shape))
+
+    def expand(self, out: torch.Tensor | None = None, b_dev: torch.Tensor | None = None,
+               a0_dev: torch.Tensor | None = None) -> torch.Tensor:
+        """Full stack on the device; b_dev / a0_dev: the wire words already on the device."""
+        N = self.params.n
+        lv = self.params.gadget.levels
+        if out is None:
+            out = torch.empty(self.shape, dtype=torch.int32, device=tfhe._device())
+        bd = b_dev if b_dev is not None else tfhe.to_device(self.b)
+        ad = a0_dev if a0_dev is not None else tfhe.to_device(self.a0)
+        flat = out.view(-1, 2, N)
+        for st, r0, rows in self.segments:
+            g0 = r0 // (2 * lv)
+            tfhe.philox_rgsw(st, rows, N, b_rows=bd[r0: r0 + rows], out=flat[r0: r0 + rows],
+                             a0fix=ad[g0: g0 + rows // (2 * lv)], levels=lv)
+        return out
+
+
+def encrypt_sample_seeded(bits: Sequence[int], label: int | None, key: tfhe.SecretKey, rng, *,
+                          label_bits: int = 0, pin: bool = True) -> "EncryptedSample":
+    """encrypt_sample (hw/hewnn.py:109-119) in the compressed wire form: same RNG stream
+    (the data batch, then the label batch), but the sample carries only b halves and
+    Philox states (host pinned), expanded on the server's GPU."""
+    P = key.params
+    segs, parts, row = [], [], 0
+    rows_per = 2 * P.gadget.levels
+    batches = [np.asarray(bits, dtype=np.int64)]
+    if label is not None:
+        if label >= (1 << label_bits):
+            raise TfheError(f"label {label} does not fit in {label_bits} bits")
+        batches.append(np.array([(label >> i) & 1 for i in range(label_bits)], dtype=np.int64))
+    a0s = []
+    for ms in batches:
+        b_d, st, a0 = enc_rgsw_batch_device(ms, key, rng, seeded=True)
+        segs.append((st, row, len(ms) * rows_per))
+        parts.append(b_d)
+        a0s.append(a0)
+        row += len(ms) * rows_per
+    b, a0 = torch.cat(parts).cpu(), torch.cat(a0s).cpu()
+    if pin:
+        b, a0 = b.pin_memory(), a0.pin_memory()
+    lb = label_bits if label is not None else 0
+    return EncryptedSample.from_stack(P, SeededRgsw(P, b, a0, segs), len(bits), lb)
 
 
 def encrypt_sample(bits: Sequence[int], label: int | None, key: tfhe.SecretKey, rng, *,
@@ -293,9 +366,11 @@ class _StageRing:
     chunk k's host->device copy lands in slot k % 2 on the copy stream, and waits
     for the GPU to have consumed chunk k-2 from that slot (its table conversion)."""
 
-    def __init__(self, words: int):
+    def __init__(self, words: int, bwords: int = 0):
         dev = tfhe._device()
         self.slots = [torch.empty(words, dtype=torch.int32, device=dev) for _ in range(2)]
+        # seeded samples (SeededRgsw): their b halves land here, then expand into the slot
+        self.bslots = [torch.empty(bwords, dtype=torch.int32, device=dev) for _ in range(2)] if bwords else None
         self.free = [None, None]        # main-stream event: the slot's last reader is done
         self.k = 0
 
@@ -303,6 +378,10 @@ class _StageRing:
         slot = self.k % 2
         self.k += 1
         return slot
+
+
+def _stack_to_device(stack) -> torch.Tensor:
+    return stack.expand() if isinstance(stack, SeededRgsw) else tfhe.to_device(stack)
 
 
 class _Staged:
@@ -316,14 +395,16 @@ class _Staged:
         self.dev: list | None = None
         self.event = None
         self.ring, self.slot = ring, None
-        if not any(isinstance(s.rgsw, np.ndarray) or (isinstance(s.rgsw, torch.Tensor) and not s.rgsw.is_cuda)
-                   for s in samples):
+        if not any(isinstance(s.rgsw, (np.ndarray, SeededRgsw)) or
+                   (isinstance(s.rgsw, torch.Tensor) and not s.rgsw.is_cuda) for s in samples):
             return                                          # already device-resident
         if _Staged._copy_stream is None:
             _Staged._copy_stream = torch.cuda.Stream(device=tfhe._device())
         cs = _Staged._copy_stream
         need = sum(int(np.prod(s.rgsw.shape)) for s in samples)
-        if ring is not None and need <= ring.slots[0].numel():
+        bneed = sum(int(s.rgsw.b.numel() + s.rgsw.a0.numel()) for s in samples if isinstance(s.rgsw, SeededRgsw))
+        if ring is not None and need <= ring.slots[0].numel() and (
+                bneed == 0 or (ring.bslots is not None and bneed <= ring.bslots[0].numel())):
             self.slot = ring.take()
             if ring.free[self.slot] is not None:
                 cs.wait_event(ring.free[self.slot])         # chunk k-2 has left the slot
@@ -334,11 +415,26 @@ class _Staged:
             if _TRACE is not None:
                 _TRACE.append(("copy_start", _ev(cs)))
             if self.ring is None:
-                self.dev = [tfhe.to_device(s.rgsw) for s in samples]
+                self.dev = [_stack_to_device(s.rgsw) for s in samples]
             else:
                 buf, off, self.dev = ring.slots[self.slot], 0, []
+                boff = 0
                 for smp in samples:
                     src = smp.rgsw
+                    if isinstance(src, SeededRgsw):
+                        # half the bytes over PCIe: b rows, then the GPU regenerates a
+                        nb, na = src.b.numel(), src.a0.numel()
+                        bd = ring.bslots[self.slot][boff: boff + nb].view(src.b.shape)
+                        bd.copy_(src.b, non_blocking=True)
+                        ad = ring.bslots[self.slot][boff + nb: boff + nb + na].view(src.a0.shape)
+                        ad.copy_(src.a0, non_blocking=True)
+                        boff += nb + na
+                        n = src.numel()
+                        dst = buf[off: off + n].view(src.shape)
+                        src.expand(dst, bd, ad)
+                        self.dev.append(dst)
+                        off += n
+                        continue
                     if isinstance(src, np.ndarray):
                         src = torch.from_numpy(np.ascontiguousarray(src, dtype=np.uint32).view(np.int32))
                     src = src.view(torch.int32) if src.dtype == torch.uint32 else src
@@ -354,7 +450,7 @@ class _Staged:
 
     def tensors(self) -> list:
         if self.dev is None:
-            return [tfhe.to_device(s.rgsw) for s in self.samples]
+            return [_stack_to_device(s.rgsw) for s in self.samples]
         main = torch.cuda.current_stream()
         main.wait_event(self.event)
         if self.ring is None:
@@ -494,7 +590,9 @@ def he_train(samples: Iterable[EncryptedSample], geometry: WisardGeometry, param
     def stage(chunk):
         nonlocal ring
         if ring is None and any(not (isinstance(x.rgsw, torch.Tensor) and x.rgsw.is_cuda) for x in chunk):
-            ring = _StageRing(sum(int(np.prod(x.rgsw.shape)) for x in chunk))
+            ring = _StageRing(sum(int(np.prod(x.rgsw.shape)) for x in chunk),
+                              sum(int(x.rgsw.b.numel() + x.rgsw.a0.numel()) for x in chunk
+                                  if isinstance(x.rgsw, SeededRgsw)))
         return _Staged(chunk, ring)
 
     for chunk, staged in _chunks_staged(samples, batch, check, stage):

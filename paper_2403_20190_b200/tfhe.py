@@ -188,14 +188,15 @@ def philox_take(rng: np.random.Generator, nwords: int):
 
 
 def philox_rgsw(st, rows: int, N: int, b_rows: torch.Tensor | None = None, out: torch.Tensor | None = None,
-                pair: bool = True) -> torch.Tensor:
+                pair: bool = True, a0fix: torch.Tensor | None = None, levels: int = 0) -> torch.Tensor:
     """GPU regeneration of a seeded draw (hwb_philox_rgsw): (rows, 2, N) RGSW rows with
-    a from the stream and b from b_rows, or (rows, N) a words (pair=False)."""
+    a from the stream (gadget-carrying words from a0fix) and b from b_rows, or (rows, N)
+    a words (pair=False)."""
     dev = _device()
     if out is None:
         out = torch.empty((rows, 2, N) if pair else (rows, N), dtype=torch.int32, device=dev)
-    _lib.check(_lib.load().hwb_philox_rgsw(ctypes.byref(st), _ptr(b_rows), _ptr(out), rows, N, int(pair),
-                                           _stream()))
+    _lib.check(_lib.load().hwb_philox_rgsw(ctypes.byref(st), _ptr(b_rows), _ptr(a0fix), int(levels), _ptr(out),
+                                           rows, N, int(pair), _stream()))
     return out
 
 

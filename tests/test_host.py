@@ -98,3 +98,32 @@ def test_test_polynomial_validation():
     P = named_params("CFG2")
     with pytest.raises(tfhe.TfheError):
         tfhe.test_polynomial(np.arange(8), P)
+
+
+def test_philox_take_matches_numpy_stream():
+    """tfhe.philox_take claims the next words of rng.bytes() (hw/tfhe.py:38-40) without
+    drawing them: regenerating them from the returned state (host restatement of the
+    GPU kernel) gives rng.bytes's words, and the generator continues identically
+    (uint32 buffer, uint64 buffer and counter), also after normals."""
+    import numpy as np
+    from paper_2403_20190_b200 import tfhe
+    for pre in (0, 1, 3, 8, 9, 13):
+        for n in (1, 2, 5, 7, 8, 9, 16, 17, 1000, 1001):
+            r1, r2 = tfhe.make_rng(5), tfhe.make_rng(5)
+            if pre:
+                r1.bytes(4 * pre)
+                r2.bytes(4 * pre)
+            r1.normal(size=3)
+            r2.normal(size=3)
+            want = np.frombuffer(r1.bytes(4 * n), dtype="<u4")
+            st = tfhe.philox_take(r2, n)
+            words = list(st.prefix[: st.nprefix])
+            g = 0
+            while len(words) < n:
+                g += 1
+                for u in tfhe.philox4x64(tfhe._ctr_add(list(st.ctr), g), list(st.key)):
+                    words += [u & 0xFFFFFFFF, u >> 32]
+            assert list(want) == words[:n], (pre, n)
+            assert np.array_equal(r1.bytes(44), r2.bytes(44))
+            assert np.array_equal(r1.normal(size=5), r2.normal(size=5))
+            assert np.array_equal(r1.integers(0, 2, 7), r2.integers(0, 2, 7))
