@@ -384,7 +384,7 @@ def bench_train(args, world, rank, torch, dist):
         from oracle import coracle, wnn32
         coracle.build()
         n_cpu = min(2, images)
-        stacks = [np.asarray(tfhe.to_host(h.rgsw)) for h in host[:n_cpu]]
+        stacks = [np.asarray(tfhe.to_host(h.rgsw.expand())) for h in host[:n_cpu]]
         c0 = time.perf_counter()
         wnn32.he_train(stacks, s, l, a, r, P)
         dt = time.perf_counter() - c0

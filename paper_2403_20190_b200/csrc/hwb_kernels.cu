@@ -604,20 +604,29 @@ __global__ void philox_rgsw_kernel(hwb_philox st, const uint32_t *__restrict__ b
       carry = carry && c[i] == 0;
     }
     philox4x64_10(c, st.key[0], st.key[1]);
+    // rows l..2l-1 of each RGSW carry the gadget term m g_t on a[0] (hw/tfhe.py:259-262):
+    // those words ship explicitly (a0fix [rows / 2l][l]) and are written instead of the
+    // regenerated ones (by the thread that owns the word: no second writer)
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int64_t w = st.nprefix + 8 * g + q;
       if (w < nwords) {
         const uint64_t u = c[q >> 1];
-        out[(w / N) * rs + w % N] = (q & 1) ? (uint32_t)(u >> 32) : (uint32_t)u;
+        const int64_t r = w / N, col = w % N;
+        uint32_t v = (q & 1) ? (uint32_t)(u >> 32) : (uint32_t)u;
+        if (a0fix && col == 0 && (r % (2 * levels)) >= levels)
+          v = a0fix[(r / (2 * levels)) * levels + (r % (2 * levels)) - levels];
+        out[r * rs + col] = v;
       }
     }
   }
-  if (g < st.nprefix && g < nwords) out[(g / N) * rs + g % N] = st.prefix[g];
-  // rows l..2l-1 of each RGSW carry the gadget term m g_t on a[0] (hw/tfhe.py:259-262):
-  // those words ship explicitly (a0fix [rows / 2l][l]) and replace the regenerated ones
-  if (a0fix && g < rows && (g % (2 * levels)) >= levels)
-    out[g * rs] = a0fix[(g / (2 * levels)) * levels + (g % (2 * levels)) - levels];
+  if (g < st.nprefix && g < nwords) {
+    const int64_t r = g / N, col = g % N;
+    uint32_t v = st.prefix[g];
+    if (a0fix && col == 0 && (r % (2 * levels)) >= levels)
+      v = a0fix[(r / (2 * levels)) * levels + (r % (2 * levels)) - levels];
+    out[r * rs + col] = v;
+  }
   if (b_rows && pair)
     for (int64_t w = g; w < nwords; w += (int64_t)gridDim.x * blockDim.x) out[(w / N) * 2 * N + N + w % N] = b_rows[w];
 }
@@ -3175,7 +3184,7 @@ int hwb_philox_rgsw(const hwb_philox *st, const uint32_t *b_rows, const uint32_t
     return fail(HWB_EINVAL, "philox_rgsw: bad arguments");
   if (a0fix && (levels < 1 || rows % (2 * levels))) return fail(HWB_EINVAL, "philox_rgsw: rows not whole RGSWs");
   if (rows == 0) return HWB_OK;
-  const int64_t nblocks = ((rows * N + 7) / 8 + 1) > rows ? (rows * N + 7) / 8 + 1 : rows;
+  const int64_t nblocks = (rows * N + 7) / 8 + 1;
   philox_rgsw_kernel<<<(unsigned)((nblocks + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*st, b_rows, a0fix, levels,
                                                                                           out, rows, N, pair);
   return post_launch("philox_rgsw_kernel");

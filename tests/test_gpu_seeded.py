@@ -57,3 +57,15 @@ def test_seeded_samples_train_identically():
     m3 = hewnn.he_train(seeded, geom, P, batch=1)              # every staging slot reused
     assert torch.equal(m1.rams, m3.rams)
     assert hewnn.decrypt_sample(seeded[2], key) == (list(bits[2]), int(labels[2]))
+
+
+def test_seeded_full_size_sample_expands_exactly():
+    """A BASELINE cfg3-size sample (2352 data bits + 4 label bits, 14,136 rows): the
+    gadget-carrying a-words and the regenerated words never race."""
+    P = named_params("CFG3", 256)
+    key = tfhe.SecretKey(P, tfhe.make_rng(15).integers(0, 2, P.n).astype(np.uint32))
+    bits = np.random.default_rng(16).integers(0, 2, 2352)
+    plain = hewnn.encrypt_sample(bits, 9, key, tfhe.make_rng(17), label_bits=4)
+    seeded = hewnn.encrypt_sample_seeded(bits, 9, key, tfhe.make_rng(17), label_bits=4)
+    for _ in range(3):
+        assert_u32_equal(tfhe.to_host(seeded.rgsw.expand()), tfhe.to_host(plain.rgsw))
