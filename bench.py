@@ -59,6 +59,10 @@ def parse():
     ap.add_argument("--infer-pbs-images", type=int, default=4,
                     help="images for the fully encrypted bleach/popcount/argmax inference (0 disables)")
     ap.add_argument("--infer-pbs-thr", type=int, default=0, help="bleaching threshold of that inference")
+    ap.add_argument("--cfg4-train", type=int, default=16384, help="cfg4 full-size variant: training images")
+    ap.add_argument("--cfg4-test", type=int, default=2048, help="cfg4 full-size variant: PD-act test images")
+    ap.add_argument("--cfg4-pbs-images", type=int, default=2, help="cfg4 variant: fully encrypted inference images")
+    ap.add_argument("--no-cfg4-full", dest="cfg4_full", action="store_false", help="skip the full-size cfg4 run")
     ap.add_argument("--no-other-configs", dest="other_configs", action="store_false",
                     help="skip the cfg1/cfg4 PBS measurements")
     ap.add_argument("--sweep", default="1,16,148,592,1184,4096,16384,65536",
@@ -394,6 +398,87 @@ def bench_train(args, world, rank, torch, dist):
     return out
 
 
+def bench_cfg4_full(args, torch):
+    """BASELINE cfg4 at full size on the stated feasible variant CFG4V:
+    16,384 training images (client encryption on the GPU with device-drawn normals,
+    streamed into he_train), decrypted counters checked against train_integer, the 2,048
+    test images through PD-act inference (predictions == evaluate_dataset), and the fully
+    encrypted bleach/popcount/argmax inference on a few test images."""
+    from paper_2403_20190_b200 import data, hewnn, infer_pbs, tfhe, wnn
+    from paper_2403_20190_b200.params import named_params
+    (s, l, a, r, _), _ = data.CONFIG_GEOMETRY[4]
+    P = named_params("CFG4V")
+    geom = wnn.WisardGeometry(s, l, a, r, P.p)
+    n_train, n_test = args.cfg4_train, args.cfg4_test
+    ds = data.config_dataset(4, n=n_train, seed=0)
+    tds = data.config_dataset(4, split="test", n=n_test, seed=0)
+    key = tfhe.SecretKey(P, tfhe.make_rng(KEY_SEED).integers(0, 2, P.n).astype(np.uint32))
+    rng = tfhe.make_rng(ENC_SEED)
+
+    def stream():
+        for i in range(n_train):
+            yield hewnn.encrypt_sample(ds.bits[i], int(ds.labels[i]), key, rng, label_bits=geom.label_bits,
+                                       device_noise=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record()
+    model = hewnn.he_train(stream(), geom, P, batch=args.train_batch)
+    e1.record()
+    e1.synchronize()
+    wall = time.perf_counter() - t0
+    dm, cc = hewnn.decrypt_model(model, key)
+    ref, rc = wnn.train_integer(ds.bits, ds.labels, geom)
+    ok = bool(np.array_equal(dm.counters, ref.counters) and np.array_equal(cc.counts, rc.counts))
+    noise, margin = hewnn.model_noise(model, key)
+    # PD-act inference over the whole test set (client decrypts, activates, argmaxes)
+    _, pksk = tfhe.keygen(P, KEY_SEED)
+    act = wnn.ActivationSpec("bin", 0)
+    trng = tfhe.make_rng(ENC_SEED + 7)
+    preds, inf_ms = [], 0.0
+    for c0 in range(0, n_test, 64):
+        ts = [hewnn.encrypt_sample(tds.bits[i], None, key, trng, device_noise=True)
+              for i in range(c0, min(n_test, c0 + 64))]
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        packs = hewnn.he_infer_pd_batch(model, ts, pksk)
+        g1.record()
+        g1.synchronize()
+        inf_ms += g0.elapsed_time(g1)
+        preds += [hewnn.client_finalize(pk, key, act).prediction for pk in packs]
+    plain = wnn.evaluate_dataset(ref, tds.bits, act)
+    out = {"workload": f"BASELINE cfg4 geometry at full size: {n_train} train / {n_test} test images",
+           "params": f"CFG4V: N=2048 Bg=2^10 l=2 n=750 (cfg4), client RGSW sigma = 2^-32 q, p = {P.p}",
+           "why_variant": "BASELINE cfg4 (sigma 2^-25, p = 4096) exceeds Delta/2 = 2^19 after one image at "
+                          "q = 2^32 (tools/cfg4_noise.py: 4 images -> 4% counters correct)",
+           "train_images_per_s": round(n_train / (e0.elapsed_time(e1) * 1e-3), 2),
+           "train_wall_s_incl_client_encryption": round(wall, 1),
+           "noise": {"max_log2": round(float(np.log2(max(noise, 1))), 2), "margin_log2": round(float(np.log2(margin)), 2)},
+           "check": "decrypted counters == train_integer" if ok else "COUNTER MISMATCH",
+           "counters_correct": round(float(np.mean(dm.counters == ref.counters)), 8),
+           "infer_pd": {"images_per_s": round(n_test / (inf_ms * 1e-3), 2), "images": n_test,
+                        "accuracy": round(float(np.mean(np.array(preds) == tds.labels)), 4),
+                        "check": "predictions == evaluate_dataset(bin 0)" if list(plain) == preds
+                        else "PREDICTION MISMATCH"}}
+    if args.cfg4_pbs_images > 0:
+        sbk = infer_pbs.self_bootstrap_keygen(key, KEY_SEED + 11)
+        tsm = [hewnn.encrypt_sample(tds.bits[i], None, key, trng) for i in range(args.cfg4_pbs_images)]
+        stats: dict = {}
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        pr = infer_pbs.he_infer_bin_batch(model, tsm, sbk, 0, stats=stats)
+        g1.record()
+        g1.synchronize()
+        got = [infer_pbs.decrypt_prediction(x, key) for x in pr]
+        want = list(wnn.evaluate_dataset(ref, tds.bits[: args.cfg4_pbs_images], act))
+        sec = g0.elapsed_time(g1) * 1e-3
+        out["infer_pbs"] = {"images_per_s": round(len(tsm) / sec, 3), "pbs_per_s": round(stats["pbs"] / sec, 1),
+                            "pbs_per_image": stats["pbs"] // len(tsm), "images": len(tsm),
+                            "self_bsk": "n = N = 2048",
+                            "check": "encrypted argmax == evaluate_dataset(bin 0)" if got == want
+                            else "PREDICTION MISMATCH"}
+    return out
+
+
 def bench_infer_pbs(args, model, key, ref, tsamples, tbits, torch):
     """OTF-act inference entirely on ciphertexts (paper_2403_20190_b200.infer_pbs):
     VP lookups, bleaching threshold, popcount and argmax on the batched PBS engine,
@@ -709,6 +794,8 @@ def bench_hwb(args):
             # the other BASELINE training workloads (cfg5 RGB 7 classes; cfg4 N = 2048)
             result["train"]["other_configs"] = {f"cfg{c}": train_other(c, n, b, rank, torch)
                                                 for c, n, b in ((5, 32, 16), (4, 16, 8))}
+        if args.cfg4_full and rank == 0:
+            result["train"]["cfg4_full"] = bench_cfg4_full(args, torch)
     if world > 1:
         dist.destroy_process_group()
     if rank == 0:

@@ -85,7 +85,7 @@ def bleach(boot: Boot, lwe, p, thr):
     C, carry = lwe, None
     for i in range(K // 2):
         s = 32 - K + 2 * i
-        top = i == K // 2 - 1
+        top = i == K // 2 - 1 and K % 2 == 0
         L = affine(C, shift=30 - s, cb=1 << 29)
         b_cmp = boot(L, lut_sign(OUT, N))
         if s < OUT_LOG:
@@ -103,6 +103,12 @@ def bleach(boot: Boot, lwe, p, thr):
         if carry is not None:
             y = affine(y, carry)
         carry = boot(y, lut_half([int(v >= 4) for v in range(8)], 16, OUT, N))
+    if K % 2:                                   # odd K: a single top bit at 2^31
+        sg = boot(affine(C, cb=1 << 30), lut_sign(OUT >> 1, N))
+        y = affine(sg, cx=-1, cb=(OUT >> 1) + ((c >> (K - 1)) & 1) * OUT)
+        if carry is not None:
+            y = affine(y, carry)
+        carry = boot(y, lut_half([int(v >= 2) for v in range(8)], 16, OUT, N))
     return carry
 
 

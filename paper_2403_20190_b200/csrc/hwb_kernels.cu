@@ -917,13 +917,16 @@ __global__ void __launch_bounds__(FT) bsk_to_fft_kernel(const uint32_t *__restri
 #ifndef HWB_FFT_DIG
 #define HWB_FFT_DIG 1
 #endif
-constexpr int FDR = 6;   // digit rows 2l staged per product (FFT path: l <= 3, base_log <= 8)
+constexpr int FDR = 6;   // digit rows 2l staged per product (FFT path: l <= 3)
+// staging slots per thread: 2l rows of 16 byte digits (base_log <= 8, l <= 3), or 2l rows
+// of 16 halfword digits = 2 slots each (wide gadgets: base_log <= 16, l <= 2)
+constexpr int FDS = 8;
 template <int CPB>
 struct FSmemT {
   uint32_t acc[CPB][2 * 2 * FH];
   double2 scr[CPB][FH];
 #if HWB_FFT_DIG
-  uint4 dig[CPB][FDR * FT];       // the product's digits, biased bytes [row][thread][16 positions]
+  uint4 dig[CPB][FDS * FT];       // the product's digits, biased bytes / halfwords [slot][thread]
 #endif
   double2 key[2 * 2 * FC * FT];   // the current digit's key slice [c][h][j][t] (32 KB, TMA)
   uint64_t key_full;              // mbarrier: slice landed
@@ -952,7 +955,10 @@ __device__ __forceinline__ void fft_ext_product(FSmemT<CPB> &sm, const double2 *
   // rounding) is formed once and its l digits, biased into [0, beta), are stored as
   // bytes -- row r, thread t: 16 bytes, byte 2j + q for position t + 64 j + 512 q.
   // Each thread reads back only its own slots, so no barrier is needed.
+  // Wide gadgets (base_log > 8, the full-precision 2 x 16 sets) stage halfwords: two
+  // slots per row, slot 2r + h holding positions j = 4h .. 4h + 3.
   uint4 *dig = sm.dig[grp];
+  const bool wide = g.base_log > 8;
 #pragma unroll
   for (int c = 0; c < 2; ++c) {
     uint32_t pw[2 * FC];
@@ -965,6 +971,15 @@ __device__ __forceinline__ void fft_ext_product(FSmemT<CPB> &sm, const double2 *
 #pragma unroll 1
     for (int tt = 0; tt < lv; ++tt) {
       const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
+      const int row = (c == 1 ? 0 : lv) + tt;
+      if (wide) {
+        uint32_t wd[8];
+#pragma unroll
+        for (int j = 0; j < FC; ++j) wd[j] = ((pw[2 * j] >> sh) & g.mask) | (((pw[2 * j + 1] >> sh) & g.mask) << 16);
+        dig[(2 * row) * FT + t] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+        dig[(2 * row + 1) * FT + t] = make_uint4(wd[4], wd[5], wd[6], wd[7]);
+        continue;
+      }
       uint32_t wd[4];
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
@@ -972,7 +987,7 @@ __device__ __forceinline__ void fft_ext_product(FSmemT<CPB> &sm, const double2 *
         const uint32_t hi = __byte_perm(pw[4 * m + 2] >> sh, pw[4 * m + 3] >> sh, 0x0040);
         wd[m] = __byte_perm(lo, hi, 0x5410) & bmask;
       }
-      dig[((c == 1 ? 0 : lv) + tt) * FT + t] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+      dig[row * FT + t] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
     }
   }
 #endif
@@ -989,13 +1004,21 @@ __device__ __forceinline__ void fft_ext_product(FSmemT<CPB> &sm, const double2 *
     const double2 *gr = G + (size_t)r * (2 * 2 * FC * FT);
     double2 x[FC];
 #if HWB_FFT_DIG
-    const uint4 dv = dig[r * FT + t];
-    const uint32_t dw[4] = {dv.x, dv.y, dv.z, dv.w};
+    if (wide) {
+      const uint4 d0 = dig[(2 * r) * FT + t], d1 = dig[(2 * r + 1) * FT + t];
+      const uint32_t dw[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
 #pragma unroll
-    for (int j = 0; j < FC; ++j) {
-      const uint32_t w = dw[j >> 1], k = 2 * (j & 1);
-      x[j] = make_double2(u2d_minus(__byte_perm(w, 0, 0x4440 + k), dig_off),
-                          u2d_minus(__byte_perm(w, 0, 0x4441 + k), dig_off));
+      for (int j = 0; j < FC; ++j)
+        x[j] = make_double2(u2d_minus(dw[j] & 0xFFFFu, dig_off), u2d_minus(dw[j] >> 16, dig_off));
+    } else {
+      const uint4 dv = dig[r * FT + t];
+      const uint32_t dw[4] = {dv.x, dv.y, dv.z, dv.w};
+#pragma unroll
+      for (int j = 0; j < FC; ++j) {
+        const uint32_t w = dw[j >> 1], k = 2 * (j & 1);
+        x[j] = make_double2(u2d_minus(__byte_perm(w, 0, 0x4440 + k), dig_off),
+                            u2d_minus(__byte_perm(w, 0, 0x4441 + k), dig_off));
+      }
     }
 #else
     const int comp = r < lv ? 1 : 0;
@@ -2772,13 +2795,20 @@ static Gadget make_gadget(uint32_t levels, uint32_t base_log) {
   return g;
 }
 
-static int check_glwe(const hwb_params *p) {
+// ring and gadget shape shared by both exact formulations
+static int check_ring(const hwb_params *p) {
   if (!p) return fail(HWB_EINVAL, "null params");
   if (p->q_bits != 32) return fail(HWB_EINVAL, "q_bits must be 32");
   if (p->k != 1) return fail(HWB_EINVAL, "only GLWE dimension k = 1 is supported");
   if (p->N != 1024 && p->N != 2048) return fail(HWB_EINVAL, "ring degree N must be 1024 or 2048");
   if (p->l < 1 || p->l > 3) return fail(HWB_EINVAL, "gadget levels must be in [1, 3]");
   if (p->base_log < 1 || p->l * p->base_log > 32) return fail(HWB_EINVAL, "gadget spans more than 32 bits");
+  return HWB_OK;
+}
+
+static int check_glwe(const hwb_params *p) {
+  int rc = check_ring(p);
+  if (rc) return rc;
   // exactness of the two-prime RNS: max |sum| = 2l * N * beta/2 * 2^31 < P/2
   const double bound = 2.0 * p->l * p->N * std::ldexp(1.0, (int)p->base_log - 1) * std::ldexp(1.0, 31);
   const double halfP = 0.5 * (double)kP0 * (double)kP1;
@@ -3058,7 +3088,7 @@ int hwb_vp_level(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_t *g
 
 int hwb_monomial_gather(const hwb_params *p, const uint32_t *in, uint32_t *out, const int32_t *exps, int64_t B,
                         void *stream) {
-  int rc = check_glwe(p);
+  int rc = check_ring(p);
   if (rc) return rc;
   if (B < 0) return fail(HWB_EINVAL, "negative batch");
   if (B == 0) return HWB_OK;
@@ -3074,7 +3104,7 @@ int hwb_monomial_gather(const hwb_params *p, const uint32_t *in, uint32_t *out, 
 }
 
 int hwb_poly_to_ntt(const hwb_params *p, const uint32_t *in, uint32_t *out, int64_t npolys, void *stream) {
-  int rc = check_glwe(p);
+  int rc = check_ring(p);
   if (rc) return rc;
   if (npolys < 0) return fail(HWB_EINVAL, "negative count");
   if (npolys == 0) return HWB_OK;
@@ -3090,7 +3120,7 @@ int hwb_poly_to_ntt(const hwb_params *p, const uint32_t *in, uint32_t *out, int6
 
 int hwb_key_mul(const hwb_params *p, const uint32_t *key_ntt, const uint32_t *in, const uint32_t *add, uint32_t *out,
                 int64_t npolys, void *stream) {
-  int rc = check_glwe(p);
+  int rc = check_ring(p);
   if (rc) return rc;
   if (npolys < 0) return fail(HWB_EINVAL, "negative count");
   if (npolys == 0) return HWB_OK;
@@ -3115,7 +3145,7 @@ size_t hwb_pack_ks_workspace_bytes(const hwb_params *p, int64_t B) {
 int hwb_pack_ks(const hwb_params *p, int32_t levels, int32_t base_log, const uint32_t *ksk_ntt,
                 const uint32_t *apolys, const uint32_t *b_polys, uint32_t *out, int64_t B, void *workspace,
                 void *stream) {
-  int rc = check_glwe(p);
+  int rc = check_ring(p);   // the external-product gadget is not used here: only the packing one
   if (rc) return rc;
   if (levels < 1 || base_log < 1 || levels * base_log > 32)
     return fail(HWB_EINVAL, "packing gadget spans more than 32 bits");
@@ -3150,7 +3180,7 @@ int hwb_pack_ks(const hwb_params *p, int32_t levels, int32_t base_log, const uin
 }
 
 int hwb_rgsw_add_gadget(const hwb_params *p, uint32_t *rgsw, const int32_t *bits, int64_t B, void *stream) {
-  int rc = check_glwe(p);
+  int rc = check_ring(p);
   if (rc) return rc;
   if (B < 0) return fail(HWB_EINVAL, "negative batch");
   if (B == 0) return HWB_OK;
@@ -3249,7 +3279,7 @@ int hwb_blind_rotate(const hwb_params *p, const uint32_t *ggsw_ntt, const int32_
 
 int hwb_sample_extract(const hwb_params *p, const uint32_t *rlwe, uint32_t *lwe, int64_t B, int32_t coeff,
                        void *stream) {
-  int rc = check_glwe(p);
+  int rc = check_ring(p);
   if (rc) return rc;
   if (coeff < 0 || coeff >= (int32_t)p->N) return fail(HWB_EINVAL, "coefficient index out of range");
   if (B < 0) return fail(HWB_EINVAL, "negative batch");
@@ -3363,21 +3393,25 @@ static int launch_pbs_fft(const void *bsk_fft, const uint32_t *lwe_in, const uin
 }  // extern "C++"
 
 static int check_fft(const hwb_params *p) {
-  int rc = check_glwe(p);
+  // the FFT ladders do not use the two-prime CRT, so the NTT's range bound does not apply
+  // (full-precision 2 x 16 gadgets run here); their own exactness is the rounding margin:
+  // measured max |y - rint(y)| 2^-21 (N = 1024, 8-bit digits) and 2^-18 (N = 2048,
+  // 10-bit digits), growing linearly with the digit size -- 16-bit digits stay below 2^-12
+  // (tests/test_gpu_fullsize.py measures every supported width)
+  int rc = check_ring(p);
   if (rc) return rc;
   if (p->N == 4 * FH) {
-    // FFT2: int16 digits, 2l <= F2R rows; exactness as at N = 1024 (|sum| < 2^37,
-    // FFT error ~2^-12 for l 2^base_log <= 2^11)
-    if (2 * p->l > (uint32_t)F2R || p->base_log > 15 || p->l * (1u << p->base_log) > (1u << 11))
-      return fail(HWB_EINVAL, "the N = 2048 FFT ladder needs l <= 2 and l * 2^base_log <= 2^11");
+    // FFT2: biased halfword digits, 2l <= F2R rows
+    if (2 * p->l > (uint32_t)F2R || p->base_log > 16)
+      return fail(HWB_EINVAL, "the N = 2048 FFT ladder needs l <= 2 and base_log <= 16");
     return HWB_OK;
   }
   if (p->N != 2 * FH) return fail(HWB_EINVAL, "the FFT ladder supports N = 1024 and 2048");
-  // rounding exactness: |sum| < 2l N beta/2 2^15 and FFT error << 1/2
-  if (p->l * (1u << p->base_log) >= (1u << 19)) return fail(HWB_EINVAL, "gadget too wide for the FFT ladder");
+  if (p->base_log > 16) return fail(HWB_EINVAL, "the FFT ladder needs base_log <= 16");
 #if HWB_FFT_DIG
-  // digits staged as bytes, 2l <= FDR rows (every BASELINE gadget at N = 1024)
-  if (p->base_log > 8 || 2 * p->l > (uint32_t)FDR) return fail(HWB_EINVAL, "the FFT ladder needs base_log <= 8, l <= 3");
+  // staged digits: bytes (2l <= FDR rows) or, for base_log > 8, halfwords (2 slots per row)
+  if (2 * p->l * (p->base_log > 8 ? 2 : 1) > (uint32_t)FDS || 2 * p->l > (uint32_t)FDR)
+    return fail(HWB_EINVAL, "the FFT ladder needs l <= 3 (base_log <= 8) or l <= 2 (base_log <= 16)");
 #endif
   return HWB_OK;
 }

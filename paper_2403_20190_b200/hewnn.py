@@ -175,7 +175,7 @@ def _device_key(key: tfhe.SecretKey) -> DeviceKey:
     return dk
 
 
-def enc_rgsw_batch_device(ms, key: tfhe.SecretKey, rng, seeded: bool = False):
+def enc_rgsw_batch_device(ms, key: tfhe.SecretKey, rng, seeded: bool = False, device_noise: bool = False):
     """enc_rgsw_batch (hw/tfhe.py:246-263) with the uniform half AND the key product on
     the GPU: the host claims the a-words of rng's Philox stream without generating
     them (tfhe.philox_take), draws only the normals e, and the GPU regenerates a
@@ -192,8 +192,18 @@ def enc_rgsw_batch_device(ms, key: tfhe.SecretKey, rng, seeded: bool = False):
     if np.any((ms != 0) & (ms != 1)):
         raise tfhe.EncodingError("RGSW messages are bits")
     st = tfhe.philox_take(rng, B * rows * N)                   # a: claimed, not drawn
-    e = tfhe.gaussian_u32(rng, params.sigma, (B, rows, N))
     dev = tfhe._device()
+    if device_noise:
+        # large-scale runs: the normals drawn on the GPU from a generator seeded by the
+        # host stream -- a valid encryption, but NOT the reference's rint(rng.normal)
+        # stream
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(int(rng.integers(0, 1 << 62)))
+        e = torch.round(torch.randn((B, rows, N), generator=gen, device=dev, dtype=torch.float64) * params.sigma)
+        e = e.to(torch.int64).bitwise_and(0xFFFFFFFF)
+        e = torch.where(e >= 1 << 31, e - (1 << 32), e).to(torch.int32)
+    else:
+        e = tfhe.gaussian_u32(rng, params.sigma, (B, rows, N))
     out = torch.empty((B, rows, 2, N), dtype=torch.int32, device=dev)
     if B == 0:
         return (out.view(0, N), st, out[:, :0, 0, 0]) if seeded else out
@@ -280,11 +290,17 @@ def encrypt_sample_seeded(bits: Sequence[int], label: int | None, key: tfhe.Secr
 
 
 def encrypt_sample(bits: Sequence[int], label: int | None, key: tfhe.SecretKey, rng, *,
-                   label_bits: int = 0, device: bool = True) -> EncryptedSample:
+                   label_bits: int = 0, device: bool = True, device_noise: bool = False) -> EncryptedSample:
     """Encrypt preprocessed input bits and the label (hw/hewnn.py:109-119).
 
-    RNG stream as the reference: the data batch, then the label batch."""
-    enc = enc_rgsw_batch_device if device else _enc_rgsw_host
+    RNG stream as the reference: the data batch, then the label batch.
+    device_noise=True draws the normals on the GPU (a valid encryption at GPU speed for
+    large synthetic workloads, not the reference's RNG stream)."""
+    if device_noise:
+        def enc(ms, key, rng):
+            return enc_rgsw_batch_device(ms, key, rng, device_noise=True)
+    else:
+        enc = enc_rgsw_batch_device if device else _enc_rgsw_host
     data = enc(np.asarray(bits, dtype=np.int64), key, rng)
     lb = 0
     if label is not None:

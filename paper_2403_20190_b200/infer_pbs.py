@@ -183,8 +183,8 @@ def bleach(sbk: SelfBootstrapKey, luts: Luts, lwe: torch.Tensor, p: int, thr: in
     B, W = lwe.shape
     N = W - 1
     K = p.bit_length() - 1
-    if p != 1 << K or K < 2 or K % 2:
-        raise TfheError("bleach needs p = 4^D (an even number of counter bits)")
+    if p != 1 << K or K < 1:
+        raise TfheError("bleach needs a power-of-two counter modulus p >= 2")
     t = thr + 1
     if t <= 0:
         return trivial(OUT, B, N, lwe.device)
@@ -194,9 +194,9 @@ def bleach(sbk: SelfBootstrapKey, luts: Luts, lwe: torch.Tensor, p: int, thr: in
     D = K // 2
     C = lwe
     carry = None
-    for i in range(D):
+    for i in range(D):                                      # radix-4 digits (odd K: plus a top bit)
         s = 32 - K + 2 * i                                  # C = (m >> 2i) 2^s + e
-        top = i == D - 1                                    # s = 30: nothing left to clear after it
+        top = i == D - 1 and K % 2 == 0                     # s = 30: nothing left to clear after it
         fine = s < OUT_LOG                                  # floor outputs need their own scale 2^s
         L = lincomb(C, shift=30 - s, cb=1 << 29)            # digit at 2^30, + half a slot
         ids = [luts.sign(OUT)] + ([luts.sign(1 << s)] if fine else [])
@@ -217,6 +217,16 @@ def bleach(sbk: SelfBootstrapKey, luts: Luts, lwe: torch.Tensor, p: int, thr: in
         if carry is not None:
             y = lincomb(y, carry)
         carry = pbs(sbk, luts, y, luts.half([int(v >= 4) for v in range(8)], 16, OUT), stats)
+    if K % 2:
+        # the last, single-bit digit sits at 2^31: its sign bootstrap (offset by half a
+        # slot) is the bit; carry out of bit + c_top + carry_in (base 2)
+        L = lincomb(C, cb=1 << 30)
+        sg = pbs(sbk, luts, L, luts.sign(OUT >> 1), stats)            # (1 - 2b) 2^27
+        ct = (c >> (K - 1)) & 1
+        y = lincomb(sg, cx=-1, cb=(OUT >> 1) + ct * OUT)                 # b 2^28 + c_top 2^28
+        if carry is not None:
+            y = lincomb(y, carry)
+        carry = pbs(sbk, luts, y, luts.half([int(v >= 2) for v in range(8)], 16, OUT), stats)
     return carry
 
 

@@ -339,7 +339,11 @@ def _codes_of(selectors: list[list[SelectorBit]], params: HeParams):
                 codes[i, j] = rows[key]
     table = None
     if cts:
-        table = tfhe.rgsw_to_ntt(params, np.stack([np.asarray(c.data) for c in cts]))
+        stack = np.stack([np.asarray(c.data) for c in cts])
+        # the FP64 FFT ladders wherever they apply (as he_train's "auto"), else the NTT;
+        # full-precision gadgets have only the former (bit-identical where both exist)
+        table = (tfhe.rgsw_to_fft(params, stack) if tfhe.ggsw_fft_bytes(params) > 0
+                 else tfhe.rgsw_to_ntt(params, stack))
     return codes, table
 
 

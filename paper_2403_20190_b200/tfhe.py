@@ -346,19 +346,25 @@ class BootstrapKey:
     16-bit key halves (hwb_bsk_to_fft)."""
 
     params: HeParams
-    ntt: GgswNtt
+    ntt: GgswNtt | None
     fft: torch.Tensor | None = field(default=None, repr=False)
+    count: int = 0
 
     @staticmethod
     def from_coefficients(params: HeParams, bsk) -> "BootstrapKey":
+        """NTT image where the exact two-prime range allows it, FFT image where the FP64
+        ladders apply (full-precision 2 x 16 gadgets have only the latter)."""
         coeff = to_device(bsk)
-        key = BootstrapKey(params, rgsw_to_ntt(params, coeff))
+        key = BootstrapKey(params, rgsw_to_ntt(params, coeff) if ntt_supported(params) else None,
+                           count=int(coeff.shape[0]))
         cp = _lib.c_params(params)
         L = _lib.load()
         nbytes = L.hwb_bsk_fft_bytes(ctypes.byref(cp))
         if nbytes:
             key.fft = torch.empty(nbytes, dtype=torch.uint8, device=coeff.device)
             _lib.check(L.hwb_bsk_to_fft(ctypes.byref(cp), _ptr(coeff), _ptr(key.fft), _stream()))
+        if key.ntt is None and key.fft is None:
+            raise TfheError("neither exact ladder supports these parameters")
         return key
 
 
@@ -695,6 +701,49 @@ def measure_noise(ct, key, params: HeParams | None = None) -> NoiseBudget:
 # device: NTT-domain GGSWs
 
 
+def ntt_supported(params: HeParams) -> bool:
+    """The exact two-prime NTT applies (2l N beta/2 2^31 < p0 p1 / 2); the
+    FP64 FFT ladders cover full-precision gadgets beyond it."""
+    cp = _lib.c_params(params)
+    null = ctypes.c_void_p(0)
+    return _lib.load().hwb_ggsw_to_ntt(ctypes.byref(cp), null, null, 0, null) == 0
+
+
+def _fft_level(params: HeParams, fft: "GgswFft", idx, cur: torch.Tensor, inverse: bool) -> torch.Tensor:
+    """One FFT-path IVP (CDEMUX) or VP (CMUX) level with m = 1 (hwb_ivp/vp_level_fft):
+    cur (B, 2 or 1, 2, N) -> (B, 1 or 2, 2, N)."""
+    B = cur.shape[0]
+    nxt = torch.empty((B, 2 if inverse else 1, 2, params.n), dtype=torch.int32, device=cur.device)
+    fn = _lib.load().hwb_ivp_level_fft if inverse else _lib.load().hwb_vp_level_fft
+    cp = _lib.c_params(params)
+    _lib.check(fn(ctypes.byref(cp), _ptr(fft.data), _ptr(idx), _ptr(cur.contiguous()), _ptr(nxt), 1, B, _stream()))
+    return nxt
+
+
+def _fft_rep(params: HeParams, rep) -> "GgswFft":
+    if isinstance(rep, GgswFft):
+        return rep
+    if isinstance(rep, RgswCiphertext):
+        rep = rep.data
+    arr = rep if isinstance(rep, torch.Tensor) else np.asarray(rep)
+    if arr.ndim == 3:
+        arr = arr[None]
+    return rgsw_to_fft(params, arr)
+
+
+def _fft_idx(count: int, B: int, idx, dev) -> torch.Tensor:
+    if idx is not None:
+        it = torch.as_tensor(np.asarray(idx) if not isinstance(idx, torch.Tensor) else idx, dtype=torch.int32)
+        if it.numel() != B:
+            raise TfheError("GGSW index vector length differs from the batch")
+        return it.to(dev).contiguous()
+    if count == 1:
+        return torch.zeros(B, dtype=torch.int32, device=dev)
+    if count != B:
+        raise TfheError(f"rgsw batch {count} does not match ciphertext batch {B}")
+    return torch.arange(B, dtype=torch.int32, device=dev)
+
+
 def rgsw_to_ntt(params: HeParams, ggsw) -> GgswNtt:
     """Forward-transform (count, 2l, 2, N) GGSWs into the NTT domain on the GPU."""
     g = ggsw
@@ -748,6 +797,13 @@ def _gidx(ntt: GgswNtt, B: int, idx=None):
 
 def ext_product_batch(params: HeParams, rgsw_rep, cts, idx=None):
     """hw/tfhe.py:301-319: rep (B|1, 2l, 2, N) (or GgswNtt), cts (B, 2, N) -> (B, 2, N)."""
+    if not ntt_supported(params) and not isinstance(rgsw_rep, GgswNtt):
+        # full-precision gadgets: the product is the hi half of a one-level CDEMUX (FFT path)
+        t = to_device(cts)
+        _check_cts(params, t)
+        fft = _fft_rep(params, rgsw_rep)
+        nxt = _fft_level(params, fft, _fft_idx(fft.count, t.shape[0], idx, t.device), t.unsqueeze(1), True)
+        return _wrap(cts, nxt[:, 1].contiguous())
     ntt = _as_ntt(params, rgsw_rep)
     t = to_device(cts)
     _check_cts(params, t)
@@ -771,6 +827,22 @@ def external_product(C: RgswCiphertext, c: RlweCiphertext) -> RlweCiphertext:
 def cmux_batch(params: HeParams, rgsw_rep, c1, c0, idx=None, rot=None):
     """hw/lut.py:200-206 / hw/tfhe.py:334-337 batched: c0 + C (*) (c1 - c0).
     With c1 None, c1 = c0 * X^rot[b] per item (the rotated branch)."""
+    if not ntt_supported(params) and not isinstance(rgsw_rep, GgswNtt):
+        # full-precision gadgets: a one-level VP CMUX on the FFT path
+        t0 = to_device(c0)
+        _check_cts(params, t0)
+        if c1 is not None:
+            t1 = to_device(c1)
+            _check_cts(params, t1)
+        else:
+            if rot is None:
+                raise TfheError("cmux needs c1 or a rotation vector")
+            from .lut import monomial_gather
+            t1 = monomial_gather(params, t0, rot)
+        fft = _fft_rep(params, rgsw_rep)
+        nxt = _fft_level(params, fft, _fft_idx(fft.count, t0.shape[0], idx, t0.device),
+                         torch.stack([t0, t1], dim=1), False)
+        return _wrap(c0, nxt[:, 0].contiguous())
     ntt = _as_ntt(params, rgsw_rep)
     t0 = to_device(c0)
     _check_cts(params, t0)
@@ -797,6 +869,12 @@ def cmux_batch(params: HeParams, rgsw_rep, c1, c0, idx=None, rot=None):
 
 def cdemux_batch(params: HeParams, rgsw_rep, d, idx=None):
     """hw/lut.py:113-119 batched: (d - C (*) d, C (*) d)."""
+    if not ntt_supported(params) and not isinstance(rgsw_rep, GgswNtt):
+        t = to_device(d)
+        _check_cts(params, t)
+        fft = _fft_rep(params, rgsw_rep)
+        nxt = _fft_level(params, fft, _fft_idx(fft.count, t.shape[0], idx, t.device), t.unsqueeze(1), True)
+        return _wrap(d, nxt[:, 0].contiguous()), _wrap(d, nxt[:, 1].contiguous())
     ntt = _as_ntt(params, rgsw_rep)
     t = to_device(d)
     _check_cts(params, t)
@@ -819,7 +897,8 @@ def cmux(C: RgswCiphertext, c1: RlweCiphertext, c2: RlweCiphertext) -> RlweCiphe
 def blind_rotate_batch(params: HeParams, acc, ggsw, exps):
     """Fused hw/tfhe.py:340-349 over a batch: acc (B, 2, N), ggsw L GGSWs shared by
     the batch (GgswNtt or (L, 2l, 2, N)), exps (B, L) the I values."""
-    ntt = _as_ntt(params, ggsw)
+    wide = not ntt_supported(params) and not isinstance(ggsw, GgswNtt)
+    rep = _fft_rep(params, ggsw) if wide else _as_ntt(params, ggsw)
     t = to_device(acc).clone()
     _check_cts(params, t, "accumulator batch")
     B = t.shape[0]
@@ -827,12 +906,12 @@ def blind_rotate_batch(params: HeParams, acc, ggsw, exps):
     e = (e % (2 * params.n)).to(torch.int32)
     if e.dim() == 1:
         e = e.unsqueeze(0).expand(B, -1)
-    if e.shape[0] != B or e.shape[1] != ntt.count:
+    if e.shape[0] != B or e.shape[1] != rep.count:
         raise TfheError("selector/exponent length mismatch")
     e = e.to(t.device).contiguous()
     cp = _lib.c_params(params)
-    _lib.check(_lib.load().hwb_blind_rotate(ctypes.byref(cp), _ptr(ntt.data), None, _ptr(e), _ptr(t),
-                                            ntt.count, B, _stream()))
+    fn = _lib.load().hwb_blind_rotate_fft if wide else _lib.load().hwb_blind_rotate
+    _lib.check(fn(ctypes.byref(cp), _ptr(rep.data), None, _ptr(e), _ptr(t), rep.count, B, _stream()))
     return _wrap(acc, t)
 
 
@@ -990,7 +1069,11 @@ def _use_fft_ladder(bsk: BootstrapKey, B: int, ladder: str) -> bool:
     if ladder not in ("auto", "fft", "ntt"):
         raise TfheError(f"unknown ladder {ladder!r}")
     if ladder == "ntt":
+        if bsk.ntt is None:
+            raise TfheError("no NTT bootstrapping key for these parameters (gadget beyond the two-prime range)")
         return False
+    if bsk.ntt is None:
+        return True
     if bsk.fft is None:
         if ladder == "fft":
             raise TfheError("no FFT bootstrapping key for these parameters (N = 1024 or 2048, narrow gadgets)")
@@ -1024,8 +1107,8 @@ def pbs_batch(params: HeParams, lwe, tv, bsk: BootstrapKey, ksk: LweKeySwitchKey
         per_item = 1
     else:
         raise TfheError("test polynomial must be (2, N) or (B, 2, N)")
-    if bsk.ntt.count != params.lwe_n:
-        raise TfheError(f"bootstrapping key has {bsk.ntt.count} GGSWs, params want {params.lwe_n}")
+    if bsk.count != params.lwe_n:
+        raise TfheError(f"bootstrapping key has {bsk.count} GGSWs, params want {params.lwe_n}")
     width = params.lwe_n + 1 if ksk is not None else params.n + 1
     if out is None:
         out = torch.empty((B, width), dtype=torch.int32, device=t.device)

@@ -131,5 +131,21 @@ def test_fft_ladder_knobs():
         cp = _lib.c_params(P)
         assert L.hwb_bsk_fft_bytes(ctypes.byref(cp)) == P.lwe_n * 2 * P.gadget.levels * 2 * 2 * n_pts * 16
     cp = _lib.c_params(named_params("CFG2"))
-    cp.base_log, cp.l = 9, 2                            # FFT path needs byte digits at N = 1024
+    cp.base_log, cp.l = 9, 3                            # halfword digits (base_log > 8) need l <= 2
     assert L.hwb_bsk_fft_bytes(ctypes.byref(cp)) == 0
+    cp.base_log, cp.l = 9, 2
+    assert L.hwb_bsk_fft_bytes(ctypes.byref(cp)) > 0
+
+
+def test_full_precision_gadget_routes_to_the_fft_ladders():
+    """2 x 16 gadgets: rejected by the two-prime NTT, accepted by the FP64 FFT ladders
+    (16-bit digit staging)."""
+    from paper_2403_20190_b200 import tfhe
+    for name in ("INSECURE_1024W", "INSECURE_2048W"):
+        P = named_params(name)
+        cp = _lib.c_params(P)
+        assert not tfhe.ntt_supported(P)
+        assert _lib.load().hwb_bsk_fft_bytes(ctypes.byref(cp)) == P.lwe_n * 4 * 2 * 2 * (P.n // 2) * 16
+    cp = _lib.c_params(named_params("INSECURE_1024W"))
+    cp.l, cp.base_log = 3, 10                      # 16-bit staging holds l <= 2 only
+    assert _lib.load().hwb_bsk_fft_bytes(ctypes.byref(cp)) == 0

@@ -61,6 +61,20 @@ def test_bleach_every_counter_value(ctx, coracle):
     assert_u32_equal(got, want)
 
 
+@pytest.mark.parametrize("p", [2, 8, 32])
+def test_bleach_odd_counter_widths(ctx, p):
+    """p = 2^K with K odd (cfg4's stated variant uses p = 8): the top digit is a single
+    bit; every value and every threshold decrypts to [m > thr]."""
+    P, key, sbk = ctx
+    ms = np.arange(p)
+    lwe = tfhe.to_device(_enc_lwe_s1(ms, P, key, tfhe.make_rng(26), (1 << 32) // p))
+    P16 = dataclasses.replace(P, p=16)
+    luts = infer_pbs.Luts(P)
+    for thr in range(-1, p + 1):
+        out = tfhe.to_host(infer_pbs.bleach(sbk, luts, lwe, p, thr))
+        assert np.array_equal(tfhe.dec_lwe_batch(out, key, P16), (ms > thr).astype(np.int64)), (p, thr)
+
+
 def test_popcount_and_argmax(ctx):
     """Activated-bit sums up to 196 (cfg3's k0) and first-max argmax with ties."""
     P, key, sbk = ctx
