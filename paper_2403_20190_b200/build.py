@@ -21,7 +21,8 @@ NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC", "-shared",
-    "-split-compile=0",          # parallel optimisation passes (same kernels, ~3x faster build)
+    # (not -split-compile: measured to cost registers / add stack frames in the ladder
+    # kernels -- blind_rotate_fft_tm_kernel 234 -> 255 registers + 160 B stack)
 ]
 
 

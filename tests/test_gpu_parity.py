@@ -50,11 +50,17 @@ def test_ext_product_golden(tag, N_log, lv, w, variant):
     assert_u32_equal(tfhe.ext_product_batch(P, G[:1], cts), g[f"{tag}_out_bcast"])
 
 
-def test_ext_product_outside_envelope_raises():
+def test_ext_product_full_precision_gadget_matches_reference():
+    """The reference's exact-mode gadget (2 x 16 = 32 bits, hw/params.py:94-101) is
+    beyond the two-prime NTT (the C ABI's hwb_ext_product rejects it) and runs on the FP64
+    FFT path with 16-bit digits: bit-exact with the reference-generated fixture."""
     g = golden("ext_product.npz")
     P = emb_params(10, 2, 16)
+    assert not tfhe.ntt_supported(P)
+    assert_u32_equal(tfhe.ext_product_batch(P, g["ins_G"], g["ins_cts"]), g["ins_out"])
+    assert_u32_equal(tfhe.ext_product_batch(P, g["ins_G"][:1], g["ins_cts"]), g["ins_out_bcast"])
     with pytest.raises(tfhe.TfheError):
-        tfhe.ext_product_batch(P, g["ins_G"], g["ins_cts"])
+        tfhe.ext_product_batch(P, tfhe.rgsw_to_ntt(emb_params(10, 3, 7), g["cfg2_G"]), g["ins_cts"])
 
 
 def test_ext_product_random_batch_and_index(coracle):
