@@ -1220,6 +1220,23 @@ __device__ __forceinline__ void tm_st_f64(uint32_t addr, double v) {   // one do
                "r"(__double2hiint(v))
                : "memory");
 }
+__device__ __forceinline__ void tm_st_c64(uint32_t addr, double2 v) {   // one complex: 4 columns
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr),
+               "r"(__double2loint(v.x)), "r"(__double2hiint(v.x)), "r"(__double2loint(v.y)), "r"(__double2hiint(v.y))
+               : "memory");
+}
+#ifndef HWB_TM_ST4
+#define HWB_TM_ST4 0
+#endif
+// store one complex accumulator value: x4 (one STTM) or two x2 halves
+__device__ __forceinline__ void tm_st_acc(uint32_t addr, double2 v) {
+#if HWB_TM_ST4
+  tm_st_c64(addr, v);
+#else
+  tm_st_f64(addr, v.x);
+  tm_st_f64(addr + 2, v.y);
+#endif
+}
 __device__ __forceinline__ void tm_zero32(uint32_t addr) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
                "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(addr), "r"(0u)
@@ -1291,10 +1308,8 @@ __device__ __forceinline__ void tm_ext_product(FSmemTM &sm, const double2 *__res
         v.y = fma(x[1][j].x, k.y, fma(x[1][j].y, k.x, v.y));
         // per-double stores: the results stay in whatever registers the DFMAs chose
         // (32-register block stores made ptxas move them)
-        tm_st_f64(a0 + 4 * j, u.x);
-        tm_st_f64(a0 + 4 * j + 2, u.y);
-        tm_st_f64(a1 + 4 * j, v.x);
-        tm_st_f64(a1 + 4 * j + 2, v.y);
+        tm_st_acc(a0 + 4 * j, u);
+        tm_st_acc(a1 + 4 * j, v);
       }
     }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -1466,10 +1481,8 @@ __global__ void __launch_bounds__(2 * FT, 2)
           v.x = fma(x[1][j].x, k.x, fma(-x[1][j].y, k.y, v.x));
           v.y = fma(x[1][j].x, k.y, fma(x[1][j].y, k.x, v.y));
           // per-double stores: the results stay in whatever registers the DFMAs chose
-          tm_st_f64(a0 + 4 * j, u.x);
-          tm_st_f64(a0 + 4 * j + 2, u.y);
-          tm_st_f64(a1 + 4 * j, v.x);
-          tm_st_f64(a1 + 4 * j + 2, v.y);
+          tm_st_acc(a0 + 4 * j, u);
+          tm_st_acc(a1 + 4 * j, v);
         }
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
