@@ -2212,10 +2212,15 @@ __global__ void __launch_bounds__(FDR * FT, 1)
 
 constexpr int F2R = 4;   // digit rows 2l staged per product (l <= 2)
 
+#ifndef HWB_FFT2_ONFLY
+#define HWB_FFT2_ONFLY 0
+#endif
 struct FSmem2 {
   uint32_t acc[2 * 4 * FH];        // working ciphertext (a, b), N = 2048
   double2 scr[2][FH];              // per-half transpose scratch
+#if !HWB_FFT2_ONFLY
   uint32_t dig[F2R * FC * 2 * FT]; // the product's digits (biased halfwords)
+#endif
   double2 key[2 * 2 * 2 * FC * FT];   // the digit's key slice [c][h][g][j][t] (64 KB, TMA)
   uint64_t key_full;
 };
@@ -2236,6 +2241,7 @@ __device__ __forceinline__ void fft2_ext_product(FSmem2 &sm, const double2 *__re
   constexpr uint32_t kSliceBytes = 2 * 2 * 2 * FC * FT * sizeof(double2);
   const int lv = (int)g.levels;
   const double dig_off = 4503599627370496.0 + (double)g.half;   // 2^52 + beta/2
+#if !HWB_FFT2_ONFLY
   // the decomposition once per product: thread (grp, t) forms the prep words of
   // positions k + 512 q, q = 2 grp + {0, 1}
 #pragma unroll
@@ -2257,6 +2263,7 @@ __device__ __forceinline__ void fft2_ext_product(FSmem2 &sm, const double2 *__re
     }
   }
   __syncthreads();
+#endif
   double2 Y[2][2][FC];
 #pragma unroll
   for (int c = 0; c < 2; ++c)
@@ -2268,6 +2275,24 @@ __device__ __forceinline__ void fft2_ext_product(FSmem2 &sm, const double2 *__re
   for (int r = 0; r < 2 * lv; ++r) {
     const double2 *gr = G + (size_t)r * (2 * 2 * 2 * FC * FT);
     double2 x[FC];
+#if HWB_FFT2_ONFLY
+    {
+      // digits straight from the accumulator (no staging buffer: 16 KB more L1 for the
+      // per-thread twiddle tables)
+      const int comp = r < lv ? 1 : 0;
+      const int tt = r < lv ? r : r - lv;
+      const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
+#pragma unroll
+      for (int j = 0; j < FC; ++j) {
+        const int k = t + FT * j;
+        const uint32_t d0 = (prep(comp, k) >> sh) & g.mask, d1 = (prep(comp, k + FH) >> sh) & g.mask;
+        const uint32_t d2 = (prep(comp, k + 2 * FH) >> sh) & g.mask, d3 = (prep(comp, k + 3 * FH) >> sh) & g.mask;
+        const double2 zk = make_double2(u2d_minus(d0, dig_off), u2d_minus(d2, dig_off));
+        const double2 zh = make_double2(u2d_minus(d1, dig_off), u2d_minus(d3, dig_off));
+        x[j] = fft2_first(zk, zh, grp);
+      }
+    }
+#else
 #pragma unroll
     for (int j = 0; j < FC; ++j) {
       const uint32_t w0 = sm.dig[((r * FC + j) * 2) * FT + t], w1 = sm.dig[((r * FC + j) * 2 + 1) * FT + t];
@@ -2275,6 +2300,7 @@ __device__ __forceinline__ void fft2_ext_product(FSmem2 &sm, const double2 *__re
       const double2 zh = make_double2(u2d_minus(w0 >> 16, dig_off), u2d_minus(w1 >> 16, dig_off));
       x[j] = fft2_first(zk, zh, grp);
     }
+#endif
     auto stage_key = [&] {
       if (threadIdx.x == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

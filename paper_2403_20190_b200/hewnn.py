@@ -411,6 +411,7 @@ class _Staged:
         self.dev: list | None = None
         self.event = None
         self.ring, self.slot = ring, None
+        self.pending: list = []          # seeded samples: expanded on the main stream in tensors()
         if not any(isinstance(s.rgsw, (np.ndarray, SeededRgsw)) or
                    (isinstance(s.rgsw, torch.Tensor) and not s.rgsw.is_cuda) for s in samples):
             return                                          # already device-resident
@@ -447,7 +448,9 @@ class _Staged:
                         boff += nb + na
                         n = src.numel()
                         dst = buf[off: off + n].view(src.shape)
-                        src.expand(dst, bd, ad)
+                        # the a-regeneration runs on the MAIN stream (tensors()), so the copy
+                        # stream only moves bytes and the next chunk's H2D is not delayed
+                        self.pending.append((src, dst, bd, ad))
                         self.dev.append(dst)
                         off += n
                         continue
@@ -469,6 +472,9 @@ class _Staged:
             return [_stack_to_device(s.rgsw) for s in self.samples]
         main = torch.cuda.current_stream()
         main.wait_event(self.event)
+        for src, dst, bd, ad in self.pending:
+            src.expand(dst, bd, ad)
+        self.pending = []
         if self.ring is None:
             for t in self.dev:
                 t.record_stream(main)                       # allocator: used on the main stream
