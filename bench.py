@@ -700,8 +700,8 @@ def bench_hwb(args):
                      "work_per_pbs": work_txt, "peak_source": peak_src,
                      "traffic_note": ("ncu --set full flushes L2 before each replayed launch, so the "
                                       "64-step segment's accumulators (B x 8 KB) and key slices are read "
-                                      "from DRAM; bench runs keep them L2-resident (see "
-                                      "profiles/r02_dram_no_flush.txt)") if use_fft else None,
+                                      "from DRAM (471 MB per batch); without the flush a batch reads "
+                                      "~178 MB (profiles/r02_dram_no_flush.txt) against 148 MB algorithmic") if use_fft else None,
                      "context": {}}}
     ctx = {"pbs": {"roofline_pbs_per_s": round(pbs_roof, 1),
                              "frac": round(B / (max_ms / args.steps * 1e-3) / pbs_roof, 4),
