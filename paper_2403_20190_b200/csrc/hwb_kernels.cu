@@ -917,10 +917,11 @@ __global__ void __launch_bounds__(FT) bsk_to_fft_kernel(const uint32_t *__restri
 #ifndef HWB_FFT_DIG
 #define HWB_FFT_DIG 1
 #endif
-constexpr int FDR = 6;   // digit rows 2l staged per product (FFT path: l <= 3)
-// staging slots per thread: 2l rows of 16 byte digits (base_log <= 8, l <= 3), or 2l rows
-// of 16 halfword digits = 2 slots each (wide gadgets: base_log <= 16, l <= 2)
-constexpr int FDS = 8;
+constexpr int FDR = 6;   // digit rows 2l staged per product (FFT path: l <= 3, byte digits)
+// staging slots per thread: 2l rows of 16 byte digits (base_log <= 8).  Wide gadgets
+// (base_log > 8) extract their digits on the fly instead: 8 slots would grow the CTA past
+// the 4 CTAs/SM that the register ladder needs (measured: B = 592 at 13.9 vs 10.0 ms).
+constexpr int FDS = FDR;
 template <int CPB>
 struct FSmemT {
   uint32_t acc[CPB][2 * 2 * FH];
@@ -955,12 +956,13 @@ __device__ __forceinline__ void fft_ext_product(FSmemT<CPB> &sm, const double2 *
   // rounding) is formed once and its l digits, biased into [0, beta), are stored as
   // bytes -- row r, thread t: 16 bytes, byte 2j + q for position t + 64 j + 512 q.
   // Each thread reads back only its own slots, so no barrier is needed.
-  // Wide gadgets (base_log > 8, the full-precision 2 x 16 sets) stage halfwords: two
-  // slots per row, slot 2r + h holding positions j = 4h .. 4h + 3.
+  // Wide gadgets (base_log > 8, the full-precision 2 x 16 sets) skip the staging and
+  // extract each row's digits from prep on the fly (below).
   uint4 *dig = sm.dig[grp];
   const bool wide = g.base_log > 8;
 #pragma unroll
   for (int c = 0; c < 2; ++c) {
+    if (wide) break;
     uint32_t pw[2 * FC];
 #pragma unroll
     for (int j = 0; j < FC; ++j) {
@@ -972,14 +974,6 @@ __device__ __forceinline__ void fft_ext_product(FSmemT<CPB> &sm, const double2 *
     for (int tt = 0; tt < lv; ++tt) {
       const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
       const int row = (c == 1 ? 0 : lv) + tt;
-      if (wide) {
-        uint32_t wd[8];
-#pragma unroll
-        for (int j = 0; j < FC; ++j) wd[j] = ((pw[2 * j] >> sh) & g.mask) | (((pw[2 * j + 1] >> sh) & g.mask) << 16);
-        dig[(2 * row) * FT + t] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
-        dig[(2 * row + 1) * FT + t] = make_uint4(wd[4], wd[5], wd[6], wd[7]);
-        continue;
-      }
       uint32_t wd[4];
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
@@ -1005,11 +999,15 @@ __device__ __forceinline__ void fft_ext_product(FSmemT<CPB> &sm, const double2 *
     double2 x[FC];
 #if HWB_FFT_DIG
     if (wide) {
-      const uint4 d0 = dig[(2 * r) * FT + t], d1 = dig[(2 * r + 1) * FT + t];
-      const uint32_t dw[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+      const int comp = r < lv ? 1 : 0;
+      const int tt = r < lv ? r : r - lv;
+      const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
 #pragma unroll
-      for (int j = 0; j < FC; ++j)
-        x[j] = make_double2(u2d_minus(dw[j] & 0xFFFFu, dig_off), u2d_minus(dw[j] >> 16, dig_off));
+      for (int j = 0; j < FC; ++j) {
+        const int i = t + FT * j;
+        x[j] = make_double2(u2d_minus((prep(comp, i) >> sh) & g.mask, dig_off),
+                            u2d_minus((prep(comp, i + FH) >> sh) & g.mask, dig_off));
+      }
     } else {
       const uint4 dv = dig[r * FT + t];
       const uint32_t dw[4] = {dv.x, dv.y, dv.z, dv.w};
@@ -3448,9 +3446,8 @@ static int check_fft(const hwb_params *p) {
   if (p->N != 2 * FH) return fail(HWB_EINVAL, "the FFT ladder supports N = 1024 and 2048");
   if (p->base_log > 16) return fail(HWB_EINVAL, "the FFT ladder needs base_log <= 16");
 #if HWB_FFT_DIG
-  // staged digits: bytes (2l <= FDR rows) or, for base_log > 8, halfwords (2 slots per row)
-  if (2 * p->l * (p->base_log > 8 ? 2 : 1) > (uint32_t)FDS || 2 * p->l > (uint32_t)FDR)
-    return fail(HWB_EINVAL, "the FFT ladder needs l <= 3 (base_log <= 8) or l <= 2 (base_log <= 16)");
+  // staged byte digits (base_log <= 8) or on-the-fly extraction (base_log <= 16), 2l <= FDR
+  if (2 * p->l > (uint32_t)FDR) return fail(HWB_EINVAL, "the FFT ladder needs l <= 3");
 #endif
   return HWB_OK;
 }

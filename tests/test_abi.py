@@ -131,9 +131,9 @@ def test_fft_ladder_knobs():
         cp = _lib.c_params(P)
         assert L.hwb_bsk_fft_bytes(ctypes.byref(cp)) == P.lwe_n * 2 * P.gadget.levels * 2 * 2 * n_pts * 16
     cp = _lib.c_params(named_params("CFG2"))
-    cp.base_log, cp.l = 9, 3                            # halfword digits (base_log > 8) need l <= 2
+    cp.base_log, cp.l = 17, 1                           # digits wider than 16 bits
     assert L.hwb_bsk_fft_bytes(ctypes.byref(cp)) == 0
-    cp.base_log, cp.l = 9, 2
+    cp.base_log, cp.l = 9, 3
     assert L.hwb_bsk_fft_bytes(ctypes.byref(cp)) > 0
 
 
@@ -147,5 +147,5 @@ def test_full_precision_gadget_routes_to_the_fft_ladders():
         assert not tfhe.ntt_supported(P)
         assert _lib.load().hwb_bsk_fft_bytes(ctypes.byref(cp)) == P.lwe_n * 4 * 2 * 2 * (P.n // 2) * 16
     cp = _lib.c_params(named_params("INSECURE_1024W"))
-    cp.l, cp.base_log = 3, 10                      # 16-bit staging holds l <= 2 only
+    cp.l, cp.base_log = 3, 11                      # 3 x 11 = 33 bits: no gadget
     assert _lib.load().hwb_bsk_fft_bytes(ctypes.byref(cp)) == 0
