@@ -21,6 +21,19 @@
 
 #include <cstdint>
 
+// Timing-only sensitivity switches (wrong results; tools/ab_variants.sh builds only):
+// HWB_X_NOTRANS skips the transposes' shared-memory traffic, HWB_X_NOTW the per-thread
+// twiddle loads, HWB_X_NOKEY the key-slice reads of the TMEM ladders' MAC.
+#ifndef HWB_X_NOTRANS
+#define HWB_X_NOTRANS 0
+#endif
+#ifndef HWB_X_NOTW
+#define HWB_X_NOTW 0
+#endif
+#ifndef HWB_X_NOKEY
+#define HWB_X_NOKEY 0
+#endif
+
 namespace hwb {
 
 constexpr int FH = 512;       // complex points per folded polynomial (N = 1024)
@@ -61,21 +74,61 @@ __device__ __forceinline__ void fft_gs(double2 &X, double2 &Y, double2 w) {
   X = make_double2(X.x + Y.x, X.y + Y.y);
   Y = cmul(d, w);
 }
+// Sibling twiddles: blocks 2m and 2m + 1 of a level have roots r and -r, so their
+// butterfly twiddles (square roots) differ by exactly i: w(2m+1) = i w(2m) (checked on
+// the host table, fft_twiddles).  The odd block's butterfly is formed from the even
+// block's twiddle at the same cost -- half the per-thread twiddle loads.
+// forward, twiddle i w (w in tangent form): (X + i w Y, X - i w Y)
+__device__ __forceinline__ void fft_ct_i(double2 &X, double2 &Y, double2 w) {
+#if HWB_FFT_TAN
+  const double ux = fma(-w.y, Y.y, Y.x), uy = fma(w.y, Y.x, Y.y);   // w Y = cos (ux, uy); i w Y = cos (-uy, ux)
+  Y = make_double2(fma(w.x, uy, X.x), fma(-w.x, ux, X.y));
+  X = make_double2(fma(-w.x, uy, X.x), fma(w.x, ux, X.y));
+#else
+  const double2 t = cmul(Y, w);
+  Y = make_double2(X.x + t.y, X.y - t.x);
+  X = make_double2(X.x - t.y, X.y + t.x);
+#endif
+}
+// inverse, conj(i w) = -i conj(w): (X + Y, -i (X - Y) conj(w)), w passed conjugated
+__device__ __forceinline__ void fft_gs_i(double2 &X, double2 &Y, double2 w) {
+  const double2 d = make_double2(X.x - Y.x, X.y - Y.y);
+  X = make_double2(X.x + Y.x, X.y + Y.y);
+  Y = make_double2(fma(d.x, w.y, d.y * w.x), fma(-d.x, w.x, d.y * w.y));   // -i (d w) = (Im, -Re)
+}
+#ifndef HWB_FFT_SIB
+#define HWB_FFT_SIB 1
+#endif
 
 template <bool FWD, int JB, bool UNIFORM, int MBASE, int SLOT>
 __device__ __forceinline__ void fft_stage(double2 (&x)[FC], int t, const double2 *__restrict__ tw, int cg = 0) {
   constexpr int NBT = FC >> (JB + 1);
   constexpr int HALF = 1 << JB;
+  double2 w;
 #pragma unroll
   for (int u = 0; u < NBT; ++u) {
-    const double2 w = UNIFORM ? c_ftw[cg][FWD ? 0 : 1][MBASE + u] : __ldg(&tw[(SLOT + u) * FT + t]);
+    // per-thread twiddles: consecutive u are consecutive blocks of one level, the
+    // odd one reuses the even one's twiddle (fft_ct_i / fft_gs_i)
+    const bool sib = !UNIFORM && HWB_FFT_SIB && (u & 1);
+#if HWB_X_NOTW   // timing-only sensitivity build: per-thread twiddles replaced by constants
+    w = c_ftw[cg][FWD ? 0 : 1][(MBASE + u + SLOT) & 7];
+#else
+    if (!sib) w = UNIFORM ? c_ftw[cg][FWD ? 0 : 1][MBASE + u] : __ldg(&tw[(SLOT + u) * FT + t]);
+#endif
 #pragma unroll
     for (int lo = 0; lo < HALF; ++lo) {
       const int j = (u << (JB + 1)) | lo;
-      if (FWD)
-        fft_ct(x[j], x[j + HALF], w);
-      else
-        fft_gs(x[j], x[j + HALF], w);
+      if (FWD) {
+        if (sib)
+          fft_ct_i(x[j], x[j + HALF], w);
+        else
+          fft_ct(x[j], x[j + HALF], w);
+      } else {
+        if (sib)
+          fft_gs_i(x[j], x[j + HALF], w);
+        else
+          fft_gs(x[j], x[j + HALF], w);
+      }
     }
   }
 }
@@ -176,6 +229,12 @@ __device__ __forceinline__ void inv_fft(double2 (&x)[FC], double2 *scr, const FL
 template <int K, int FROM, int TO, typename F = NoHook>
 __device__ __forceinline__ void frelayout_k(double2 (*x)[FC], double2 *scr, const FLay &L, F &&after_first = F()) {
   const uint32_t bf = flay_base<FROM>(L), bt = flay_base<TO>(L);
+#if HWB_X_NOTRANS   // timing-only sensitivity build: barriers kept, no shared-memory round trip
+  __syncthreads();
+  after_first();
+  __syncthreads();
+  return;
+#endif
 #pragma unroll
   for (int k = 0; k < K; ++k)
 #pragma unroll

@@ -1472,7 +1472,11 @@ __global__ void __launch_bounds__(2 * FT, 2)
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
         for (int j = 0; j < FC; ++j) {
+#if HWB_X_NOKEY
+          const double2 k = make_double2(1.0 + j + ch, 0.5 * r);
+#else
           const double2 k = sm.key[(ch * FC + j) * FT + t];
+#endif
           double2 u = tm_get(y0, j), v = tm_get(y1, j);
           u.x = fma(x[0][j].x, k.x, fma(-x[0][j].y, k.y, u.x));
           u.y = fma(x[0][j].x, k.y, fma(x[0][j].y, k.x, u.y));
@@ -1535,6 +1539,210 @@ __global__ void __launch_bounds__(2 * FT, 2)
       for (int k = t; k < N; k += FT) o[k] = k == 0 ? acc[q][0] : 0u - acc[q][N - k];
       if (t == 0) o[N] = acc[q][N];
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// TMEM ladder, one ciphertext per thread (`blind_rotate_fft_tx_kernel`, FFT mode 2).
+//
+// The TMEM ladder above runs 8 warps per SM: TMEM (256 KB) holds the spectral
+// accumulators of exactly 8 ciphertexts, and each thread carries two of them.  Here
+// each 64-thread group owns ONE ciphertext (8 complex values per thread), so the same
+// 8 ciphertexts per SM run on 16 warps at <= 128 registers: twice the warps to hide
+// the FFT's dependency and shared-memory latencies, at the price of reading each
+// key value once per ciphertext instead of once per two.  CTA = 4 groups (256
+// threads, 4 ciphertexts, one TMA-staged key slice per digit row shared by all four);
+// 2 CTAs per SM.  The decomposition-ready words of a component are computed once per
+// step (rotation and difference), and its l digit rows are extracted from registers.
+// TMEM: group q's warps 2q, 2q+1 sit in sub-partitions (2q) % 4 and (2q+1) % 4, so
+// groups q and q + 2 share lanes and split the CTA's 256 columns: column
+// (q >> 1) 128 + ((c 2 + h) 32) + 4 j + {re.lo, re.hi, im.lo, im.hi}.
+// Inverse: the two halves (lo, hi) of one component at a time (two transforms in
+// lockstep), scratch = the forward scratch (groups 0, 1) or the idle key buffer
+// (groups 2, 3).  Bit-identical to the other FFT ladders.
+
+constexpr int TXC = 4;   // ciphertexts (64-thread groups) per CTA
+
+struct FSmemTX {
+  uint32_t acc[TXC][2 * 2 * FH];
+  double2 scr[2][2 * FH];          // forward scratch of groups 0..3 (8 KB each); inverse: groups 0, 1
+  double2 key[2 * 2 * FC * FT];    // the digit's key slice (TMA); inverse scratch of groups 2, 3
+  uint64_t key_full;
+  uint32_t tmem_slot;
+};
+
+#ifndef HWB_TX_HOIST
+#define HWB_TX_HOIST 1
+#endif
+
+__global__ void __launch_bounds__(TXC * FT, 2)
+    blind_rotate_fft_tx_kernel(const double2 *__restrict__ ggsw, const uint32_t *__restrict__ lwe_in,
+                               const uint32_t *__restrict__ tv, int tv_per_item, uint32_t *lwe_out, int L, Gadget g,
+                               const double2 *__restrict__ twf, const double2 *__restrict__ twi, uint32_t *acc_io,
+                               int s0, int s1, int64_t B) {
+  constexpr int N = 2 * FH;
+  constexpr int LOG2M = 11;
+  extern __shared__ uint4 smem_raw[];
+  FSmemTX &sm = *reinterpret_cast<FSmemTX *>(smem_raw);
+  const int tid = threadIdx.x, grp = tid / FT, t = tid % FT, warp = tid / 32;
+  const FLay lay = make_flay(t);
+  // items past the end of the batch run a clamped copy of the last ciphertext
+  // (they take part in every barrier) and write nothing
+  const int64_t bb = (int64_t)blockIdx.x * TXC + grp;
+  const bool valid = bb < B;
+  const int64_t bq = valid ? bb : B - 1;
+  const uint32_t *row = lwe_in + bq * (int64_t)(L + 1);
+  uint32_t *acc = sm.acc[grp];
+  if (s0 == 0) {
+    const int bt = mod_switch(row[L], LOG2M);
+    const uint32_t *tp = tv + (tv_per_item ? bq * 2 * N : 0);
+    const int e = (2 * N - bt) & (2 * N - 1);   // X^-b~
+    for (int k = t; k < 2 * N; k += FT) {
+      const int c = k >= N, i = k & (N - 1);
+      acc[k] = rot_read<N>(tp + c * N, i, e);
+    }
+  } else {
+    for (int k = t; k < 2 * N; k += FT) acc[k] = acc_io[bq * 2 * N + k];
+  }
+  if (tid == 0) {
+    mbar_init(&sm.key_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_slot)),
+                 "r"(TM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t lane_addr = sm.tmem_slot + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((grp >> 1) * 128);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) tm_zero32(lane_addr + (uint32_t)(k * 32));
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  uint32_t key_phase = 0;
+  constexpr uint32_t kSliceBytes = 2 * 2 * FC * FT * sizeof(double2);
+  const size_t ggsw_f = (size_t)2 * g.levels * 2 * 2 * FC * FT;
+  const int lv = (int)g.levels;
+  const double dig_off = 4503599627370496.0 + (double)g.half;
+  double2 *fscr = &sm.scr[0][0] + grp * FH;                               // forward: 8 KB per group
+  double2 *iscr = grp < 2 ? &sm.scr[0][0] + grp * 2 * FH : sm.key + (grp - 2) * 2 * FH;   // inverse: 16 KB
+#pragma unroll 1
+  for (int s = s0; s < s1; ++s) {
+    const int e = mod_switch(row[s], LOG2M);   // X^{a~_s}
+    // the CTA runs the step when any of its ciphertexts needs it (shared key
+    // slices and barriers); an exact no-op product (e = 0) is discarded
+    if (!__syncthreads_or(e != 0)) continue;
+    const double2 *G = ggsw + (size_t)s * ggsw_f;
+#if HWB_TX_HOIST
+    uint32_t pw[2][FC];   // decomposition-ready words of the current component
+#endif
+#pragma unroll 1
+    for (int r = 0; r < 2 * lv; ++r) {
+      // digit order (hw/tfhe.py:290-298): rows 0..l-1 = digits of b, l..2l-1 of a
+      const int comp = r < lv ? 1 : 0;
+      const int tt = r < lv ? r : r - lv;
+      const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
+      const uint32_t *ac = acc + comp * N;
+      double2 x[1][FC];
+#if HWB_TX_HOIST
+      if (tt == 0) {
+#pragma unroll
+        for (int j = 0; j < FC; ++j) {
+          const int i = t + FT * j;
+          pw[0][j] = decomp_prep(rot_read<N>(ac, i, e) - ac[i], g);
+          pw[1][j] = decomp_prep(rot_read<N>(ac, i + FH, e) - ac[i + FH], g);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < FC; ++j)
+        x[0][j] = make_double2(u2d_minus((pw[0][j] >> sh) & g.mask, dig_off),
+                               u2d_minus((pw[1][j] >> sh) & g.mask, dig_off));
+#else
+#pragma unroll
+      for (int j = 0; j < FC; ++j) {
+        const int i = t + FT * j;
+        const uint32_t p0 = decomp_prep(rot_read<N>(ac, i, e) - ac[i], g);
+        const uint32_t p1 = decomp_prep(rot_read<N>(ac, i + FH, e) - ac[i + FH], g);
+        x[0][j] = make_double2(u2d_minus((p0 >> sh) & g.mask, dig_off), u2d_minus((p1 >> sh) & g.mask, dig_off));
+      }
+#endif
+      const double2 *gr = G + (size_t)r * (2 * 2 * FC * FT);
+      fwd_fft_k<1>(x, fscr, lay, t, twf, 0, [&] {
+        if (tid == 0) {   // every thread is past the previous reader of the key buffer
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_expect_tx(&sm.key_full, kSliceBytes);
+          bulk_g2s(sm.key, gr, kSliceBytes, &sm.key_full);
+        }
+      });
+      mbar_wait(&sm.key_full, key_phase);
+      key_phase ^= 1u;
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        const uint32_t a = lane_addr + (uint32_t)(ch * 32);
+        uint32_t y[32];
+        tm_ld32(a, y);   // zeroed at the end of the previous product
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < FC; ++j) {
+#if HWB_X_NOKEY
+          const double2 k = make_double2(1.0 + j + ch, 0.5 * r);
+#else
+          const double2 k = sm.key[(ch * FC + j) * FT + t];
+#endif
+          double2 u = tm_get(y, j);
+          u.x = fma(x[0][j].x, k.x, fma(-x[0][j].y, k.y, u.x));
+          u.y = fma(x[0][j].x, k.y, fma(x[0][j].y, k.x, u.y));
+          tm_st_acc(a + 4 * j, u);
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    // inverse transforms: the two halves of one component at a time; groups 2, 3
+    // use the idle key buffer as scratch, so every thread must be past its MAC
+    __syncthreads();
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      double2 Y[2][FC];
+      {
+        uint32_t y[2][32];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) tm_ld32(lane_addr + (uint32_t)((c * 2 + h) * 32), y[h]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int h = 0; h < 2; ++h) tm_zero32(lane_addr + (uint32_t)((c * 2 + h) * 32));   // next product
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int j = 0; j < FC; ++j) Y[h][j] = tm_get(y[h], j);
+      }
+      inv_fft_k<2>(Y, iscr, lay, t, twi);
+      if (e != 0) {
+#pragma unroll
+        for (int j = 0; j < FC; ++j) {
+          const int i = t + FT * j;
+          acc[c * N + i] += round_u32(Y[0][j].x) + (round_u32(Y[1][j].x) << 16);
+          acc[c * N + i + FH] += round_u32(Y[0][j].y) + (round_u32(Y[1][j].y) << 16);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // the last step's zeroing stores (tm_zero32) must land before the columns are freed
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sm.tmem_slot), "r"(TM_COLS));
+  }
+  if (!valid) return;
+  if (s1 < L) {
+    for (int k = t; k < 2 * N; k += FT) acc_io[bq * 2 * N + k] = acc[k];
+  } else {
+    uint32_t *o = lwe_out + bq * (int64_t)(N + 1);
+    for (int k = t; k < N; k += FT) o[k] = k == 0 ? acc[0] : 0u - acc[N - k];
+    if (t == 0) o[N] = acc[N];
   }
 }
 
@@ -3403,7 +3611,8 @@ int64_t hwb_set_fft_cluster_batch(int64_t max_batch) {
 static thread_local int g_fft_mode = 1;
 
 int hwb_set_fft_mode(int mode) {
-  if (mode != 0 && mode != 1) return fail(HWB_EINVAL, "FFT ladder mode must be 0 (registers) or 1 (TMEM)");
+  if (mode < 0 || mode > 2)
+    return fail(HWB_EINVAL, "FFT ladder mode must be 0 (registers), 1 (TMEM) or 2 (TMEM, one ciphertext per thread)");
   g_fft_mode = mode;
   return HWB_OK;
 }
@@ -3580,6 +3789,12 @@ int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, co
           (const double2 *)bsk_fft, nullptr, nullptr, lwe_in, tv, tv_per_item, ext, L, g, st->fft2_fwd[0],
           st->fft2_fwd[1], st->fft2_inv[0], st->fft2_inv[1], acc, s0, s1, B);
       rc = post_launch("blind_rotate_fft2_kernel");
+    } else if (g_fft_mode == 2 && B >= (int64_t)2 * TXC * st->sms) {
+      const size_t smem = sizeof(FSmemTX);
+      if ((rc = set_smem(blind_rotate_fft_tx_kernel, smem))) return rc;
+      blind_rotate_fft_tx_kernel<<<(unsigned)((B + TXC - 1) / TXC), TXC * FT, smem, s>>>(
+          (const double2 *)bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st->fft_fwd, st->fft_inv, acc, s0, s1, B);
+      rc = post_launch("blind_rotate_fft_tx_kernel");
     } else if (g_fft_mode == 1 && B >= (int64_t)2 * TMC * st->sms) {
       // TMEM ladder only when it fills two CTAs (8 ciphertexts) per SM; smaller
       // batches keep more CTAs per SM on the register ladder
