@@ -100,7 +100,21 @@ __device__ __forceinline__ void fft_gs_i(double2 &X, double2 &Y, double2 w) {
 #define HWB_FFT_SIB 1
 #endif
 
-template <bool FWD, int JB, bool UNIFORM, int MBASE, int SLOT>
+// Compact per-thread twiddle table (CT = true, e.g. staged in shared memory): only the
+// slots fft_stage loads -- the even u of every stage, siblings dropped -- in the order
+// of the full table: forward slots {0, 1, 3, 5, 7, 8, 10, 12}, inverse {0, 2, 4, 6, 7,
+// 9, 11, 13} of Geo<512, 64>'s 14 (hwb_kernels.cu: thread_table_of).
+constexpr int kTwc = 8;
+template <bool FWD>
+__host__ __device__ constexpr int twc_slot(int s) {
+  return FWD ? (s < 7 ? (s + 1) / 2 : 4 + (s - 6) / 2) : (s < 7 ? s / 2 : 4 + (s - 7) / 2);
+}
+template <bool FWD>
+__host__ __device__ constexpr int twc_full(int c) {   // inverse map: compact slot -> full slot
+  return FWD ? (c < 5 ? (c == 0 ? 0 : 2 * c - 1) : 6 + 2 * (c - 4)) : (c < 4 ? 2 * c : 7 + 2 * (c - 4));
+}
+
+template <bool FWD, int JB, bool UNIFORM, int MBASE, int SLOT, bool CT = false>
 __device__ __forceinline__ void fft_stage(double2 (&x)[FC], int t, const double2 *__restrict__ tw, int cg = 0) {
   constexpr int NBT = FC >> (JB + 1);
   constexpr int HALF = 1 << JB;
@@ -113,7 +127,9 @@ __device__ __forceinline__ void fft_stage(double2 (&x)[FC], int t, const double2
 #if HWB_X_NOTW   // timing-only sensitivity build: per-thread twiddles replaced by constants
     w = c_ftw[cg][FWD ? 0 : 1][(MBASE + u + SLOT) & 7];
 #else
-    if (!sib) w = UNIFORM ? c_ftw[cg][FWD ? 0 : 1][MBASE + u] : __ldg(&tw[(SLOT + u) * FT + t]);
+    if (!sib)
+      w = UNIFORM ? c_ftw[cg][FWD ? 0 : 1][MBASE + u]
+                  : (CT ? tw[twc_slot<FWD>(SLOT + u) * FT + t] : __ldg(&tw[(SLOT + u) * FT + t]));
 #endif
 #pragma unroll
     for (int lo = 0; lo < HALF; ++lo) {
@@ -250,7 +266,7 @@ __device__ __forceinline__ void frelayout_k(double2 (*x)[FC], double2 *scr, cons
 
 // K independent forward transforms in lockstep (the two key halves of a GGSW row;
 // two ciphertexts of the TMEM ladder); `hook` as in fwd_fft
-template <int K, typename F = NoHook>
+template <int K, bool CT = false, typename F = NoHook>
 __device__ __forceinline__ void fwd_fft_k(double2 (*x)[FC], double2 *scr, const FLay &L, int t,
                                           const double2 *__restrict__ tw, int cg = 0, F &&hook = F()) {
   using G = FGeo;
@@ -264,18 +280,18 @@ __device__ __forceinline__ void fwd_fft_k(double2 (*x)[FC], double2 *scr, const 
     constexpr int s = G::T - 1 - decltype(Q)::value;
     constexpr int slot = (1 << decltype(Q)::value) - 1;
 #pragma unroll
-    for (int k = 0; k < K; ++k) fft_stage<true, s - G::LO, false, 0, slot>(x[k], t, tw, cg);
+    for (int k = 0; k < K; ++k) fft_stage<true, s - G::LO, false, 0, slot, CT>(x[k], t, tw, cg);
   });
   frelayout_k<K, LAY_M, LAY_B>(x, scr, L);
   static_for<0, G::B_TOP>([&](auto Q) {
     constexpr int s = G::B_TOP - 1 - decltype(Q)::value;
     constexpr int slot = G::M_SLOTS + (G::C >> G::B_TOP) * ((1 << decltype(Q)::value) - 1);
 #pragma unroll
-    for (int k = 0; k < K; ++k) fft_stage<true, s, false, 0, slot>(x[k], t, tw, cg);
+    for (int k = 0; k < K; ++k) fft_stage<true, s, false, 0, slot, CT>(x[k], t, tw, cg);
   });
 }
 
-template <int K>
+template <int K, bool CT = false>
 __device__ __forceinline__ void inv_fft_k(double2 (*x)[FC], double2 *scr, const FLay &L, int t,
                                           const double2 *__restrict__ tw, int cg = 0) {
   using G = FGeo;
@@ -283,14 +299,14 @@ __device__ __forceinline__ void inv_fft_k(double2 (*x)[FC], double2 *scr, const 
     constexpr int s = decltype(Q)::value;
     constexpr int slot = G::C - 2 * (G::C >> (s + 1));
 #pragma unroll
-    for (int k = 0; k < K; ++k) fft_stage<false, s, false, 0, slot>(x[k], t, tw, cg);
+    for (int k = 0; k < K; ++k) fft_stage<false, s, false, 0, slot, CT>(x[k], t, tw, cg);
   });
   frelayout_k<K, LAY_B, LAY_M>(x, scr, L);
   static_for<0, G::T - G::LOGC>([&](auto Q) {
     constexpr int s = G::LOGC + decltype(Q)::value;
     constexpr int slot = G::B_SLOTS + (1 << (G::T - G::LOGC)) - (1 << (G::T - s));
 #pragma unroll
-    for (int k = 0; k < K; ++k) fft_stage<false, s - G::LO, false, 0, slot>(x[k], t, tw, cg);
+    for (int k = 0; k < K; ++k) fft_stage<false, s - G::LO, false, 0, slot, CT>(x[k], t, tw, cg);
   });
   frelayout_k<K, LAY_M, LAY_A>(x, scr, L);
   static_for<0, G::LOGN - G::T>([&](auto Q) {
@@ -322,6 +338,158 @@ __device__ __forceinline__ uint32_t round_u32(double y) {
   if (bits > *(volatile unsigned long long *)&g_fft_margin) atomicMax(&g_fft_margin, bits);
 #endif
   return (uint32_t)__double2loint(r);
+}
+
+}  // namespace hwb
+
+namespace hwb {
+
+// ---- ping-pong transforms (group-local named barriers, one barrier per transpose) ----
+// The two transposes of a transform use two different scratch buffers (s0: the first,
+// s1: the second), so a transpose needs no trailing barrier: the next write into a
+// buffer always follows the barrier of the other buffer's transpose, which every
+// reader of the first passed only after its loads.  `bar` is a named barrier over the
+// NT threads of the transform group; per-thread twiddles come from the compact table
+// (CT) or the full global table.
+template <int NT>
+__device__ __forceinline__ void gsync(int bar) {
+  asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(NT) : "memory");
+}
+
+template <int K, int FROM, int TO, int NT, typename F = NoHook>
+__device__ __forceinline__ void frelayout_pp(double2 (*x)[FC], double2 *scr, const FLay &L, int bar,
+                                             F &&after_first = F()) {
+  const uint32_t bf = flay_base<FROM>(L), bt = flay_base<TO>(L);
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int j = 0; j < FC; ++j) scr[k * FH + (bf ^ fswz(joff<FH, FT, FROM>(j)))] = x[k][j];
+  gsync<NT>(bar);
+  after_first();
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int j = 0; j < FC; ++j) x[k][j] = scr[k * FH + (bt ^ fswz(joff<FH, FT, TO>(j)))];
+}
+
+template <int K, int NT, bool CT = false, typename F = NoHook>
+__device__ __forceinline__ void fwd_fft_pp(double2 (*x)[FC], double2 *s0, double2 *s1, const FLay &L, int t,
+                                           const double2 *__restrict__ tw, int bar, F &&hook = F()) {
+  using G = FGeo;
+  static_for<0, G::LOGN - G::T>([&](auto Q) {
+    constexpr int s = G::LOGN - 1 - decltype(Q)::value;
+#pragma unroll
+    for (int k = 0; k < K; ++k) fft_stage<true, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x[k], t, tw);
+  });
+  frelayout_pp<K, LAY_A, LAY_M, NT>(x, s0, L, bar, hook);
+  static_for<0, G::T - G::LOGC>([&](auto Q) {
+    constexpr int s = G::T - 1 - decltype(Q)::value;
+    constexpr int slot = (1 << decltype(Q)::value) - 1;
+#pragma unroll
+    for (int k = 0; k < K; ++k) fft_stage<true, s - G::LO, false, 0, slot, CT>(x[k], t, tw);
+  });
+  frelayout_pp<K, LAY_M, LAY_B, NT>(x, s1, L, bar);
+  static_for<0, G::B_TOP>([&](auto Q) {
+    constexpr int s = G::B_TOP - 1 - decltype(Q)::value;
+    constexpr int slot = G::M_SLOTS + (G::C >> G::B_TOP) * ((1 << decltype(Q)::value) - 1);
+#pragma unroll
+    for (int k = 0; k < K; ++k) fft_stage<true, s, false, 0, slot, CT>(x[k], t, tw);
+  });
+}
+
+template <int K, int NT, bool CT = false>
+__device__ __forceinline__ void inv_fft_pp(double2 (*x)[FC], double2 *s0, double2 *s1, const FLay &L, int t,
+                                           const double2 *__restrict__ tw, int bar) {
+  using G = FGeo;
+  static_for<0, G::B_TOP>([&](auto Q) {
+    constexpr int s = decltype(Q)::value;
+    constexpr int slot = G::C - 2 * (G::C >> (s + 1));
+#pragma unroll
+    for (int k = 0; k < K; ++k) fft_stage<false, s, false, 0, slot, CT>(x[k], t, tw);
+  });
+  frelayout_pp<K, LAY_B, LAY_M, NT>(x, s0, L, bar);
+  static_for<0, G::T - G::LOGC>([&](auto Q) {
+    constexpr int s = G::LOGC + decltype(Q)::value;
+    constexpr int slot = G::B_SLOTS + (1 << (G::T - G::LOGC)) - (1 << (G::T - s));
+#pragma unroll
+    for (int k = 0; k < K; ++k) fft_stage<false, s - G::LO, false, 0, slot, CT>(x[k], t, tw);
+  });
+  frelayout_pp<K, LAY_M, LAY_A, NT>(x, s1, L, bar);
+  static_for<0, G::LOGN - G::T>([&](auto Q) {
+    constexpr int s = G::T + decltype(Q)::value;
+#pragma unroll
+    for (int k = 0; k < K; ++k) fft_stage<false, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x[k], t, tw);
+  });
+}
+
+}  // namespace hwb
+
+namespace hwb {
+
+// frelayout_k with a named barrier over NT threads (both barriers kept: one scratch)
+template <int K, int FROM, int TO, int NT>
+__device__ __forceinline__ void frelayout_hk(double2 (*x)[FC], double2 *scr, const FLay &L, int bar) {
+  const uint32_t bf = flay_base<FROM>(L), bt = flay_base<TO>(L);
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int j = 0; j < FC; ++j) scr[k * FH + (bf ^ fswz(joff<FH, FT, FROM>(j)))] = x[k][j];
+  gsync<NT>(bar);
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int j = 0; j < FC; ++j) x[k][j] = scr[k * FH + (bt ^ fswz(joff<FH, FT, TO>(j)))];
+  gsync<NT>(bar);
+}
+
+template <int K, int NT, bool CT = false>
+__device__ __forceinline__ void fwd_fft_hk(double2 (*x)[FC], double2 *scr, const FLay &L, int t,
+                                           const double2 *__restrict__ tw, int bar) {
+  using G = FGeo;
+  static_for<0, G::LOGN - G::T>([&](auto Q) {
+    constexpr int s = G::LOGN - 1 - decltype(Q)::value;
+#pragma unroll
+    for (int k = 0; k < K; ++k) fft_stage<true, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x[k], t, tw);
+  });
+  frelayout_hk<K, LAY_A, LAY_M, NT>(x, scr, L, bar);
+  static_for<0, G::T - G::LOGC>([&](auto Q) {
+    constexpr int s = G::T - 1 - decltype(Q)::value;
+    constexpr int slot = (1 << decltype(Q)::value) - 1;
+#pragma unroll
+    for (int k = 0; k < K; ++k) fft_stage<true, s - G::LO, false, 0, slot, CT>(x[k], t, tw);
+  });
+  frelayout_hk<K, LAY_M, LAY_B, NT>(x, scr, L, bar);
+  static_for<0, G::B_TOP>([&](auto Q) {
+    constexpr int s = G::B_TOP - 1 - decltype(Q)::value;
+    constexpr int slot = G::M_SLOTS + (G::C >> G::B_TOP) * ((1 << decltype(Q)::value) - 1);
+#pragma unroll
+    for (int k = 0; k < K; ++k) fft_stage<true, s, false, 0, slot, CT>(x[k], t, tw);
+  });
+}
+
+template <int K, int NT, bool CT = false>
+__device__ __forceinline__ void inv_fft_hk(double2 (*x)[FC], double2 *scr, const FLay &L, int t,
+                                           const double2 *__restrict__ tw, int bar) {
+  using G = FGeo;
+  static_for<0, G::B_TOP>([&](auto Q) {
+    constexpr int s = decltype(Q)::value;
+    constexpr int slot = G::C - 2 * (G::C >> (s + 1));
+#pragma unroll
+    for (int k = 0; k < K; ++k) fft_stage<false, s, false, 0, slot, CT>(x[k], t, tw);
+  });
+  frelayout_hk<K, LAY_B, LAY_M, NT>(x, scr, L, bar);
+  static_for<0, G::T - G::LOGC>([&](auto Q) {
+    constexpr int s = G::LOGC + decltype(Q)::value;
+    constexpr int slot = G::B_SLOTS + (1 << (G::T - G::LOGC)) - (1 << (G::T - s));
+#pragma unroll
+    for (int k = 0; k < K; ++k) fft_stage<false, s - G::LO, false, 0, slot, CT>(x[k], t, tw);
+  });
+  frelayout_hk<K, LAY_M, LAY_A, NT>(x, scr, L, bar);
+  static_for<0, G::LOGN - G::T>([&](auto Q) {
+    constexpr int s = G::T + decltype(Q)::value;
+#pragma unroll
+    for (int k = 0; k < K; ++k) fft_stage<false, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x[k], t, tw);
+  });
 }
 
 }  // namespace hwb

@@ -1131,11 +1131,13 @@ __global__ void __launch_bounds__(FT * CPB, 1)
   __syncthreads();
   uint32_t key_phase = 0;
   const size_t ggsw_f = (size_t)2 * g.levels * 2 * 2 * FC * FT;   // double2 per GGSW
+  uint32_t a_nx = PBS ? row[s0] : 0u;   // the next step's mask word, loaded a step ahead
 #pragma unroll 1
   for (int s = s0; s < s1; ++s) {
     int e, gi = s;
     if (PBS) {
-      e = mod_switch(row[s], LOG2M);   // X^{a~_s}
+      e = mod_switch(a_nx, LOG2M);   // X^{a~_s}
+      a_nx = row[s + 1];
     } else {
       e = (int)((-(int64_t)exps[b * L + s]) % (2 * N));
       if (e < 0) e += 2 * N;
@@ -1426,11 +1428,15 @@ __global__ void __launch_bounds__(2 * FT, 2)
   const size_t ggsw_f = (size_t)2 * g.levels * 2 * 2 * FC * FT;
   const int lv = (int)g.levels;
   const double dig_off = 4503599627370496.0 + (double)g.half;
+  uint32_t a_nx[2] = {row[0][s0], row[1][s0]};   // the next step's mask words, loaded a step ahead
 #pragma unroll 1
   for (int s = s0; s < s1; ++s) {
     int e[2];
 #pragma unroll
-    for (int q = 0; q < 2; ++q) e[q] = mod_switch(row[q][s], LOG2M);   // X^{a~_s}
+    for (int q = 0; q < 2; ++q) {
+      e[q] = mod_switch(a_nx[q], LOG2M);   // X^{a~_s}
+      a_nx[q] = row[q][s + 1];
+    }
     // the CTA runs the step when any of its ciphertexts needs it (shared key
     // slices and barriers); an exact no-op product (e = 0) is discarded
     if (!__syncthreads_or((e[0] | e[1]) != 0)) continue;
@@ -1627,9 +1633,11 @@ __global__ void __launch_bounds__(TXC * FT, 2)
   const double dig_off = 4503599627370496.0 + (double)g.half;
   double2 *fscr = &sm.scr[0][0] + grp * FH;                               // forward: 8 KB per group
   double2 *iscr = grp < 2 ? &sm.scr[0][0] + grp * 2 * FH : sm.key + (grp - 2) * 2 * FH;   // inverse: 16 KB
+  uint32_t a_nx = row[s0];   // the next step's mask word, loaded a step ahead (s + 1 <= L)
 #pragma unroll 1
   for (int s = s0; s < s1; ++s) {
-    const int e = mod_switch(row[s], LOG2M);   // X^{a~_s}
+    const int e = mod_switch(a_nx, LOG2M);   // X^{a~_s}
+    a_nx = row[s + 1];
     // the CTA runs the step when any of its ciphertexts needs it (shared key
     // slices and barriers); an exact no-op product (e = 0) is discarded
     if (!__syncthreads_or(e != 0)) continue;
@@ -1735,6 +1743,590 @@ __global__ void __launch_bounds__(TXC * FT, 2)
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sm.tmem_slot), "r"(TM_COLS));
+  }
+  if (!valid) return;
+  if (s1 < L) {
+    for (int k = t; k < 2 * N; k += FT) acc_io[bq * 2 * N + k] = acc[k];
+  } else {
+    uint32_t *o = lwe_out + bq * (int64_t)(N + 1);
+    for (int k = t; k < N; k += FT) o[k] = k == 0 ? acc[0] : 0u - acc[N - k];
+    if (t == 0) o[N] = acc[N];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// TMEM ladder, lane-paired (`blind_rotate_fft_tp_kernel`, FFT mode 3).
+//
+// Mode 2's layout (one ciphertext per thread, 16 warps per SM) with the two
+// ciphertexts of a lane pair (2m, 2m + 1) at the SAME spectral position: the key
+// value and the twiddles a pair needs sit at one shared-memory address, and a
+// quarter-warp LDS.128 that serves 4 addresses to 8 lanes costs 2.4 instead of 4
+// crossbar cycles (tools/lds_bcast_bench.cu).  Thread (warp w, lane L): ciphertext
+// q = 2 (w & 1) + (L & 1), transform position t = 16 (w >> 1) + (L >> 1) -- each
+// transform spans half the lanes of 4 warps.  Bank offsets keep the pairs
+// conflict-free: odd ciphertexts' transpose scratch is displaced by 64 B (4 of the 8
+// 16-byte bank groups), their accumulators by 16 words.  The per-thread twiddles
+// (compact: sibling slots dropped, hwb_fft.cuh) are staged in shared memory.
+
+constexpr int TPC = 4;                   // ciphertexts per CTA
+constexpr int TP_ACC = 2 * 2 * FH + 16;  // words per accumulator (+16: pair bank offset)
+
+struct FSmemTP {
+  uint32_t acc[TPC][TP_ACC];
+  double2 scr[4 * (FH + 4)];            // forward scratch (8 KB per ciphertext); inverse: ciphertexts 0, 1
+  double2 key[2 * 2 * FC * FT + 4];     // the digit's key slice (TMA); inverse scratch of ciphertexts 2, 3
+  double2 twf[kTwc * FT], twi[kTwc * FT];
+  uint64_t key_full;
+  uint32_t key_cnt;   // mode 5: halves done with the key buffer
+  uint32_t tmem_slot;
+};
+
+__global__ void __launch_bounds__(TPC * FT, 2)
+    blind_rotate_fft_tp_kernel(const double2 *__restrict__ ggsw, const uint32_t *__restrict__ lwe_in,
+                               const uint32_t *__restrict__ tv, int tv_per_item, uint32_t *lwe_out, int L, Gadget g,
+                               const double2 *__restrict__ twf, const double2 *__restrict__ twi, uint32_t *acc_io,
+                               int s0, int s1, int64_t B) {
+  constexpr int N = 2 * FH;
+  constexpr int LOG2M = 11;
+  extern __shared__ uint4 smem_raw[];
+  FSmemTP &sm = *reinterpret_cast<FSmemTP *>(smem_raw);
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int q = 2 * (warp & 1) + (lane & 1), t = 16 * (warp >> 1) + (lane >> 1);
+  const FLay lay = make_flay(t);
+  const int64_t bb = (int64_t)blockIdx.x * TPC + q;
+  const bool valid = bb < B;
+  const int64_t bq = valid ? bb : B - 1;
+  const uint32_t *row = lwe_in + bq * (int64_t)(L + 1);
+  uint32_t *acc = sm.acc[q];
+  if (s0 == 0) {
+    const int bt = mod_switch(row[L], LOG2M);
+    const uint32_t *tp = tv + (tv_per_item ? bq * 2 * N : 0);
+    const int e = (2 * N - bt) & (2 * N - 1);   // X^-b~
+    for (int k = t; k < 2 * N; k += FT) {
+      const int c = k >= N, i = k & (N - 1);
+      acc[k] = rot_read<N>(tp + c * N, i, e);
+    }
+  } else {
+    for (int k = t; k < 2 * N; k += FT) acc[k] = acc_io[bq * 2 * N + k];
+  }
+  for (int k = tid; k < kTwc * FT; k += TPC * FT) {
+    sm.twf[k] = twf[twc_full<true>(k / FT) * FT + k % FT];
+    sm.twi[k] = twi[twc_full<false>(k / FT) * FT + k % FT];
+  }
+  if (tid == 0) {
+    mbar_init(&sm.key_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_slot)),
+                 "r"(TM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t lane_addr = sm.tmem_slot + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 128);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) tm_zero32(lane_addr + (uint32_t)(k * 32));
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  uint32_t key_phase = 0;
+  constexpr uint32_t kSliceBytes = 2 * 2 * FC * FT * sizeof(double2);
+  const size_t ggsw_f = (size_t)2 * g.levels * 2 * 2 * FC * FT;
+  const int lv = (int)g.levels;
+  const double dig_off = 4503599627370496.0 + (double)g.half;
+  double2 *fscr = sm.scr + q * (FH + 4);                                                      // 8 KB
+  double2 *iscr = (q < 2 ? sm.scr : sm.key) + (q & 1) * (2 * FH + 4);                        // 16 KB
+  uint32_t a_nx = row[s0];   // the next step's mask word, loaded a step ahead (s + 1 <= L)
+#pragma unroll 1
+  for (int s = s0; s < s1; ++s) {
+    const int e = mod_switch(a_nx, LOG2M);   // X^{a~_s}
+    a_nx = row[s + 1];
+    if (!__syncthreads_or(e != 0)) continue;
+    const double2 *G = ggsw + (size_t)s * ggsw_f;
+    uint32_t pw[2][FC];   // decomposition-ready words of the current component
+#pragma unroll 1
+    for (int r = 0; r < 2 * lv; ++r) {
+      // digit order (hw/tfhe.py:290-298): rows 0..l-1 = digits of b, l..2l-1 of a
+      const int comp = r < lv ? 1 : 0;
+      const int tt = r < lv ? r : r - lv;
+      const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
+      const uint32_t *ac = acc + comp * N;
+      double2 x[1][FC];
+      if (tt == 0) {
+#pragma unroll
+        for (int j = 0; j < FC; ++j) {
+          const int i = t + FT * j;
+          pw[0][j] = decomp_prep(rot_read<N>(ac, i, e) - ac[i], g);
+          pw[1][j] = decomp_prep(rot_read<N>(ac, i + FH, e) - ac[i + FH], g);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < FC; ++j)
+        x[0][j] = make_double2(u2d_minus((pw[0][j] >> sh) & g.mask, dig_off),
+                               u2d_minus((pw[1][j] >> sh) & g.mask, dig_off));
+      const double2 *gr = G + (size_t)r * (2 * 2 * FC * FT);
+      fwd_fft_k<1, true>(x, fscr, lay, t, sm.twf, 0, [&] {
+        if (tid == 0) {   // every thread is past the previous reader of the key buffer
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_expect_tx(&sm.key_full, kSliceBytes);
+          bulk_g2s(sm.key, gr, kSliceBytes, &sm.key_full);
+        }
+      });
+      mbar_wait(&sm.key_full, key_phase);
+      key_phase ^= 1u;
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        const uint32_t a = lane_addr + (uint32_t)(ch * 32);
+        uint32_t y[32];
+        tm_ld32(a, y);   // zeroed at the end of the previous product
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < FC; ++j) {
+#if HWB_X_NOKEY
+          const double2 k = make_double2(1.0 + j + ch, 0.5 * r);
+#else
+          const double2 k = sm.key[(ch * FC + j) * FT + t];
+#endif
+          double2 u = tm_get(y, j);
+          u.x = fma(x[0][j].x, k.x, fma(-x[0][j].y, k.y, u.x));
+          u.y = fma(x[0][j].x, k.y, fma(x[0][j].y, k.x, u.y));
+          tm_st_acc(a + 4 * j, u);
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    // inverse transforms: the two halves of one component at a time; ciphertexts 2, 3
+    // use the idle key buffer as scratch, so every thread must be past its MAC
+    __syncthreads();
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      double2 Y[2][FC];
+      {
+        uint32_t y[2][32];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) tm_ld32(lane_addr + (uint32_t)((c * 2 + h) * 32), y[h]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int h = 0; h < 2; ++h) tm_zero32(lane_addr + (uint32_t)((c * 2 + h) * 32));   // next product
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int j = 0; j < FC; ++j) Y[h][j] = tm_get(y[h], j);
+      }
+      inv_fft_k<2, true>(Y, iscr, lay, t, sm.twi);
+      if (e != 0) {
+#pragma unroll
+        for (int j = 0; j < FC; ++j) {
+          const int i = t + FT * j;
+          acc[c * N + i] += round_u32(Y[0][j].x) + (round_u32(Y[1][j].x) << 16);
+          acc[c * N + i + FH] += round_u32(Y[0][j].y) + (round_u32(Y[1][j].y) << 16);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // the last step's zeroing stores (tm_zero32) must land before the columns are freed
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sm.tmem_slot), "r"(TM_COLS));
+  }
+  if (!valid) return;
+  if (s1 < L) {
+    for (int k = t; k < 2 * N; k += FT) acc_io[bq * 2 * N + k] = acc[k];
+  } else {
+    uint32_t *o = lwe_out + bq * (int64_t)(N + 1);
+    for (int k = t; k < N; k += FT) o[k] = k == 0 ? acc[0] : 0u - acc[N - k];
+    if (t == 0) o[N] = acc[N];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// TMEM ladder, lane-paired, decoupled halves (`blind_rotate_fft_td_kernel`, FFT mode 5).
+//
+// Mode 3 with its two halves (warps w & 1 = 0: ciphertexts 0, 1; w & 1 = 1: 2, 3)
+// synchronising only among their own 128 threads (named barriers).  They share the
+// TMA-staged key slice: each half releases it after its MAC and the second release
+// issues the next row's copy (it lands while the halves run their next digit
+// transforms).  The inverse runs one accumulator at a time in the ciphertext's own
+// 8 KB scratch, so the halves share nothing else.
+
+__global__ void __launch_bounds__(TPC * FT, 2)
+    blind_rotate_fft_td_kernel(const double2 *__restrict__ ggsw, const uint32_t *__restrict__ lwe_in,
+                               const uint32_t *__restrict__ tv, int tv_per_item, uint32_t *lwe_out, int L, Gadget g,
+                               const double2 *__restrict__ twf, const double2 *__restrict__ twi, uint32_t *acc_io,
+                               int s0, int s1, int64_t B) {
+  constexpr int N = 2 * FH;
+  constexpr int LOG2M = 11;
+  constexpr int GT = 128;   // threads per half (named barriers)
+  extern __shared__ uint4 smem_raw[];
+  FSmemTP &sm = *reinterpret_cast<FSmemTP *>(smem_raw);
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int q = 2 * (warp & 1) + (lane & 1), t = 16 * (warp >> 1) + (lane >> 1);
+  const FLay lay = make_flay(t);
+  const int64_t bb = (int64_t)blockIdx.x * TPC + q;
+  const bool valid = bb < B;
+  const int64_t bq = valid ? bb : B - 1;
+  const uint32_t *row = lwe_in + bq * (int64_t)(L + 1);
+  uint32_t *acc = sm.acc[q];
+  if (s0 == 0) {
+    const int bt = mod_switch(row[L], LOG2M);
+    const uint32_t *tp = tv + (tv_per_item ? bq * 2 * N : 0);
+    const int e = (2 * N - bt) & (2 * N - 1);   // X^-b~
+    for (int k = t; k < 2 * N; k += FT) {
+      const int c = k >= N, i = k & (N - 1);
+      acc[k] = rot_read<N>(tp + c * N, i, e);
+    }
+  } else {
+    for (int k = t; k < 2 * N; k += FT) acc[k] = acc_io[bq * 2 * N + k];
+  }
+  for (int k = tid; k < kTwc * FT; k += TPC * FT) {
+    sm.twf[k] = twf[twc_full<true>(k / FT) * FT + k % FT];
+    sm.twi[k] = twi[twc_full<false>(k / FT) * FT + k % FT];
+  }
+  constexpr uint32_t kSliceBytes = 2 * 2 * FC * FT * sizeof(double2);
+  const size_t ggsw_f = (size_t)2 * g.levels * 2 * 2 * FC * FT;
+  if (tid == 0) {
+    mbar_init(&sm.key_full, 1);
+    sm.key_cnt = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&sm.key_full, kSliceBytes);   // the first row's slice
+    bulk_g2s(sm.key, ggsw + (size_t)s0 * ggsw_f, kSliceBytes, &sm.key_full);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_slot)),
+                 "r"(TM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t lane_addr = sm.tmem_slot + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 128);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) tm_zero32(lane_addr + (uint32_t)(k * 32));
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  uint32_t key_phase = 0;
+  const int lv = (int)g.levels;
+  const int half = warp & 1, hbar = 1 + half;
+  const bool leader = lane == 0 && warp < 2;
+  // a half is done with the key buffer (slice or, for half 1, inverse scratch):
+  // the second half to finish issues the next row's slice
+  auto release = [&](int s_, int r_) {
+    if (!leader) return;
+    __threadfence_block();
+    if (atomicAdd(&sm.key_cnt, 1u) == 1u) {
+      sm.key_cnt = 0;
+      const int nr = r_ + 1 < 2 * lv ? r_ + 1 : 0, ns = r_ + 1 < 2 * lv ? s_ : s_ + 1;
+      if (ns < s1) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&sm.key_full, kSliceBytes);
+        bulk_g2s(sm.key, ggsw + (size_t)ns * ggsw_f + (size_t)nr * (2 * 2 * FC * FT), kSliceBytes, &sm.key_full);
+      }
+    }
+  };
+  const double dig_off = 4503599627370496.0 + (double)g.half;
+  double2 *fscr = sm.scr + q * (FH + 4);                                                      // 8 KB
+  uint32_t a_nx = row[s0];   // the next step's mask word, loaded a step ahead (s + 1 <= L)
+#pragma unroll 1
+  for (int s = s0; s < s1; ++s) {
+    const int e = mod_switch(a_nx, LOG2M);   // X^{a~_s}
+    a_nx = row[s + 1];
+      uint32_t pw[2][FC];   // decomposition-ready words of the current component
+#pragma unroll 1
+    for (int r = 0; r < 2 * lv; ++r) {
+      // digit order (hw/tfhe.py:290-298): rows 0..l-1 = digits of b, l..2l-1 of a
+      const int comp = r < lv ? 1 : 0;
+      const int tt = r < lv ? r : r - lv;
+      const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
+      const uint32_t *ac = acc + comp * N;
+      double2 x[1][FC];
+      if (tt == 0) {
+#pragma unroll
+        for (int j = 0; j < FC; ++j) {
+          const int i = t + FT * j;
+          pw[0][j] = decomp_prep(rot_read<N>(ac, i, e) - ac[i], g);
+          pw[1][j] = decomp_prep(rot_read<N>(ac, i + FH, e) - ac[i + FH], g);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < FC; ++j)
+        x[0][j] = make_double2(u2d_minus((pw[0][j] >> sh) & g.mask, dig_off),
+                               u2d_minus((pw[1][j] >> sh) & g.mask, dig_off));
+      fwd_fft_hk<1, GT, true>(x, fscr, lay, t, sm.twf, hbar);
+      mbar_wait(&sm.key_full, key_phase);
+      key_phase ^= 1u;
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        const uint32_t a = lane_addr + (uint32_t)(ch * 32);
+        uint32_t y[32];
+        tm_ld32(a, y);   // zeroed at the end of the previous product
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < FC; ++j) {
+#if HWB_X_NOKEY
+          const double2 k = make_double2(1.0 + j + ch, 0.5 * r);
+#else
+          const double2 k = sm.key[(ch * FC + j) * FT + t];
+#endif
+          double2 u = tm_get(y, j);
+          u.x = fma(x[0][j].x, k.x, fma(-x[0][j].y, k.y, u.x));
+          u.y = fma(x[0][j].x, k.y, fma(x[0][j].y, k.x, u.y));
+          tm_st_acc(a + 4 * j, u);
+        }
+      }
+      gsync<GT>(hbar);   // the half is past the slice
+      release(s, r);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    // inverse transforms, one accumulator at a time (lo then hi of each component), in
+    // the ciphertext's own forward scratch: the key buffer only ever holds slices
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      uint32_t lo[2][FC];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double2 Y[1][FC];
+        {
+          uint32_t y[32];
+          tm_ld32(lane_addr + (uint32_t)((c * 2 + h) * 32), y);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          tm_zero32(lane_addr + (uint32_t)((c * 2 + h) * 32));   // next product
+#pragma unroll
+          for (int j = 0; j < FC; ++j) Y[0][j] = tm_get(y, j);
+        }
+        inv_fft_hk<1, GT, true>(Y, fscr, lay, t, sm.twi, hbar);
+        if (h == 0) {
+#pragma unroll
+          for (int j = 0; j < FC; ++j) {
+            lo[0][j] = round_u32(Y[0][j].x);
+            lo[1][j] = round_u32(Y[0][j].y);
+          }
+        } else if (e != 0) {
+#pragma unroll
+          for (int j = 0; j < FC; ++j) {
+            const int i = t + FT * j;
+            acc[c * N + i] += lo[0][j] + (round_u32(Y[0][j].x) << 16);
+            acc[c * N + i + FH] += lo[1][j] + (round_u32(Y[0][j].y) << 16);
+          }
+        }
+      }
+    }
+    gsync<GT>(hbar);   // the half's accumulator updates before the next step's digits
+  }
+  // the last step's zeroing stores (tm_zero32) must land before the columns are freed
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sm.tmem_slot), "r"(TM_COLS));
+  }
+  if (!valid) return;
+  if (s1 < L) {
+    for (int k = t; k < 2 * N; k += FT) acc_io[bq * 2 * N + k] = acc[k];
+  } else {
+    uint32_t *o = lwe_out + bq * (int64_t)(N + 1);
+    for (int k = t; k < N; k += FT) o[k] = k == 0 ? acc[0] : 0u - acc[N - k];
+    if (t == 0) o[N] = acc[N];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// TMEM ladder, decoupled lane-paired groups (`blind_rotate_fft_tq_kernel`, FFT mode 4).
+//
+// One CTA of 16 warps per SM holds 8 ciphertexts (the TMEM capacity) as 4 independent
+// groups of 4 warps; a group carries two lane-paired ciphertexts (mode 3's mapping:
+// lanes 2m, 2m + 1 share a spectral position, so they read one key address).  Groups
+// synchronise only among their own 128 threads (named barriers), and each transpose
+// has one barrier instead of two: the two transposes of a transform use two scratch
+// buffers (fwd_fft_pp / inv_fft_pp).  All 8 ciphertexts share one TMA-staged key
+// slice: the last group to finish a row's MAC (shared counter) issues the next row's
+// copy, which lands while the groups run their digit transforms.  The inverse runs
+// one accumulator at a time.  Odd ciphertexts' transpose addresses are XOR-ed with 4
+// (the 16-byte bank group's top bit) so a pair never conflicts.
+
+constexpr int TQC = 8;   // ciphertexts per CTA
+constexpr int TQG = 4;   // groups (4 warps, 2 ciphertexts each)
+
+struct FSmemTQ {
+  uint32_t acc[TQC][2 * 2 * FH];
+  double2 buf[2][TQC][FH];          // ping-pong transpose scratch, 8 KB per ciphertext each
+  double2 key[2 * 2 * FC * FT];     // the row's key slice (TMA), shared by all groups
+  uint64_t key_full;
+  uint32_t key_cnt;                 // groups done with the current slice
+  uint32_t tmem_slot;
+};
+
+__global__ void __launch_bounds__(TQG * 4 * 32, 1)
+    blind_rotate_fft_tq_kernel(const double2 *__restrict__ ggsw, const uint32_t *__restrict__ lwe_in,
+                               const uint32_t *__restrict__ tv, int tv_per_item, uint32_t *lwe_out, int L, Gadget g,
+                               const double2 *__restrict__ twf, const double2 *__restrict__ twi, uint32_t *acc_io,
+                               int s0, int s1, int64_t B) {
+  constexpr int N = 2 * FH;
+  constexpr int LOG2M = 11;
+  constexpr int GT = 128;   // threads per group
+  extern __shared__ uint4 smem_raw[];
+  FSmemTQ &sm = *reinterpret_cast<FSmemTQ *>(smem_raw);
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int grp = warp >> 2, bar = 1 + grp;
+  const int q = 2 * grp + (lane & 1), t = 16 * (warp & 3) + (lane >> 1);
+  FLay lay = make_flay(t);
+  if (q & 1) {   // pair partner: the other half of the 8 bank groups
+    lay.a ^= 4u;
+    lay.m ^= 4u;
+    lay.b ^= 4u;
+  }
+  const int64_t bb = (int64_t)blockIdx.x * TQC + q;
+  const bool valid = bb < B;
+  const int64_t bq = valid ? bb : B - 1;
+  const uint32_t *row = lwe_in + bq * (int64_t)(L + 1);
+  uint32_t *acc = sm.acc[q];
+  if (s0 == 0) {
+    const int bt = mod_switch(row[L], LOG2M);
+    const uint32_t *tp = tv + (tv_per_item ? bq * 2 * N : 0);
+    const int e = (2 * N - bt) & (2 * N - 1);   // X^-b~
+    for (int k = t; k < 2 * N; k += FT) {
+      const int c = k >= N, i = k & (N - 1);
+      acc[k] = rot_read<N>(tp + c * N, i, e);
+    }
+  } else {
+    for (int k = t; k < 2 * N; k += FT) acc[k] = acc_io[bq * 2 * N + k];
+  }
+  constexpr uint32_t kSliceBytes = 2 * 2 * FC * FT * sizeof(double2);
+  const size_t ggsw_f = (size_t)2 * g.levels * 2 * 2 * FC * FT;
+  const int lv = (int)g.levels;
+  if (tid == 0) {
+    mbar_init(&sm.key_full, 1);
+    sm.key_cnt = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&sm.key_full, kSliceBytes);   // the first row's slice
+    bulk_g2s(sm.key, ggsw + (size_t)s0 * ggsw_f, kSliceBytes, &sm.key_full);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_slot)),
+                 "r"(512u));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t lane_addr = sm.tmem_slot + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 128);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) tm_zero32(lane_addr + (uint32_t)(k * 32));
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  uint32_t key_phase = 0;
+  const double dig_off = 4503599627370496.0 + (double)g.half;
+  double2 *b0 = sm.buf[0][q], *b1 = sm.buf[1][q];
+  const bool leader = (tid % GT) == 0;
+  uint32_t a_nx = row[s0];   // the next step's mask word, loaded a step ahead (s + 1 <= L)
+#pragma unroll 1
+  for (int s = s0; s < s1; ++s) {
+    const int e = mod_switch(a_nx, LOG2M);   // X^{a~_s}
+    a_nx = row[s + 1];
+    uint32_t pw[2][FC];   // decomposition-ready words of the current component
+#pragma unroll 1
+    for (int r = 0; r < 2 * lv; ++r) {
+      // digit order (hw/tfhe.py:290-298): rows 0..l-1 = digits of b, l..2l-1 of a
+      const int comp = r < lv ? 1 : 0;
+      const int tt = r < lv ? r : r - lv;
+      const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
+      const uint32_t *ac = acc + comp * N;
+      double2 x[1][FC];
+      if (tt == 0) {
+#pragma unroll
+        for (int j = 0; j < FC; ++j) {
+          const int i = t + FT * j;
+          pw[0][j] = decomp_prep(rot_read<N>(ac, i, e) - ac[i], g);
+          pw[1][j] = decomp_prep(rot_read<N>(ac, i + FH, e) - ac[i + FH], g);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < FC; ++j)
+        x[0][j] = make_double2(u2d_minus((pw[0][j] >> sh) & g.mask, dig_off),
+                               u2d_minus((pw[1][j] >> sh) & g.mask, dig_off));
+      fwd_fft_pp<1, GT>(x, b0, b1, lay, t, twf, bar);
+      mbar_wait(&sm.key_full, key_phase);
+      key_phase ^= 1u;
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        const uint32_t a = lane_addr + (uint32_t)(ch * 32);
+        uint32_t y[32];
+        tm_ld32(a, y);   // zeroed at the end of the previous product
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < FC; ++j) {
+#if HWB_X_NOKEY
+          const double2 k = make_double2(1.0 + j + ch, 0.5 * r);
+#else
+          const double2 k = sm.key[(ch * FC + j) * FT + t];
+#endif
+          double2 u = tm_get(y, j);
+          u.x = fma(x[0][j].x, k.x, fma(-x[0][j].y, k.y, u.x));
+          u.y = fma(x[0][j].x, k.y, fma(x[0][j].y, k.x, u.y));
+          tm_st_acc(a + 4 * j, u);
+        }
+      }
+      // the group is done with the slice; the last group fetches the next row's
+      gsync<GT>(bar);
+      if (leader) {
+        __threadfence_block();
+        const uint32_t done = atomicAdd(&sm.key_cnt, 1u);
+        if (done == TQG - 1) {
+          sm.key_cnt = 0;
+          const int nr = r + 1 < 2 * lv ? r + 1 : 0, ns = r + 1 < 2 * lv ? s : s + 1;
+          if (ns < s1) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&sm.key_full, kSliceBytes);
+            bulk_g2s(sm.key, ggsw + (size_t)ns * ggsw_f + (size_t)nr * (2 * 2 * FC * FT), kSliceBytes,
+                     &sm.key_full);
+          }
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    // inverse transforms, one accumulator at a time (lo then hi of each component)
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      uint32_t lo[2][FC];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double2 Y[1][FC];
+        {
+          uint32_t y[32];
+          tm_ld32(lane_addr + (uint32_t)((c * 2 + h) * 32), y);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          tm_zero32(lane_addr + (uint32_t)((c * 2 + h) * 32));   // next product
+#pragma unroll
+          for (int j = 0; j < FC; ++j) Y[0][j] = tm_get(y, j);
+        }
+        inv_fft_pp<1, GT>(Y, b0, b1, lay, t, twi, bar);
+        if (h == 0) {
+#pragma unroll
+          for (int j = 0; j < FC; ++j) {
+            lo[0][j] = round_u32(Y[0][j].x);
+            lo[1][j] = round_u32(Y[0][j].y);
+          }
+        } else if (e != 0) {
+#pragma unroll
+          for (int j = 0; j < FC; ++j) {
+            const int i = t + FT * j;
+            acc[c * N + i] += lo[0][j] + (round_u32(Y[0][j].x) << 16);
+            acc[c * N + i + FH] += lo[1][j] + (round_u32(Y[0][j].y) << 16);
+          }
+        }
+      }
+    }
+    gsync<GT>(bar);   // the group's accumulator updates before the next step's digits
+  }
+  // the last step's zeroing stores (tm_zero32) must land before the columns are freed
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sm.tmem_slot), "r"(512u));
   }
   if (!valid) return;
   if (s1 < L) {
@@ -2636,11 +3228,13 @@ __global__ void __launch_bounds__(2 * FT, 1)
   __syncthreads();
   uint32_t key_phase = 0;
   const size_t ggsw_f = (size_t)2 * g.levels * 2 * 2 * 2 * FC * FT;   // double2 per GGSW
+  uint32_t a_nx = PBS ? row[s0] : 0u;   // the next step's mask word, loaded a step ahead
 #pragma unroll 1
   for (int s = s0; s < s1; ++s) {
     int e, gi = s;
     if (PBS) {
-      e = mod_switch(row[s], LOG2M);   // X^{a~_s}
+      e = mod_switch(a_nx, LOG2M);   // X^{a~_s}
+      a_nx = row[s + 1];
     } else {
       e = (int)((-(int64_t)exps[b * L + s]) % (2 * N));
       if (e < 0) e += 2 * N;
@@ -3611,8 +4205,9 @@ int64_t hwb_set_fft_cluster_batch(int64_t max_batch) {
 static thread_local int g_fft_mode = 1;
 
 int hwb_set_fft_mode(int mode) {
-  if (mode < 0 || mode > 2)
-    return fail(HWB_EINVAL, "FFT ladder mode must be 0 (registers), 1 (TMEM) or 2 (TMEM, one ciphertext per thread)");
+  if (mode < 0 || mode > 5)
+    return fail(HWB_EINVAL, "FFT ladder mode must be 0 (registers), 1 (TMEM), 2 (TMEM, one ciphertext per thread) "
+                            "3 (TMEM, lane-paired), 4 (TMEM, decoupled groups) or 5 (TMEM, lane-paired, decoupled halves)");
   g_fft_mode = mode;
   return HWB_OK;
 }
@@ -3789,6 +4384,24 @@ int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, co
           (const double2 *)bsk_fft, nullptr, nullptr, lwe_in, tv, tv_per_item, ext, L, g, st->fft2_fwd[0],
           st->fft2_fwd[1], st->fft2_inv[0], st->fft2_inv[1], acc, s0, s1, B);
       rc = post_launch("blind_rotate_fft2_kernel");
+    } else if (g_fft_mode == 5 && B >= (int64_t)2 * TPC * st->sms) {
+      const size_t smem = sizeof(FSmemTP);
+      if ((rc = set_smem(blind_rotate_fft_td_kernel, smem))) return rc;
+      blind_rotate_fft_td_kernel<<<(unsigned)((B + TPC - 1) / TPC), TPC * FT, smem, s>>>(
+          (const double2 *)bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st->fft_fwd, st->fft_inv, acc, s0, s1, B);
+      rc = post_launch("blind_rotate_fft_td_kernel");
+    } else if (g_fft_mode == 4 && B >= (int64_t)TQC * st->sms) {
+      const size_t smem = sizeof(FSmemTQ);
+      if ((rc = set_smem(blind_rotate_fft_tq_kernel, smem))) return rc;
+      blind_rotate_fft_tq_kernel<<<(unsigned)((B + TQC - 1) / TQC), TQG * 4 * 32, smem, s>>>(
+          (const double2 *)bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st->fft_fwd, st->fft_inv, acc, s0, s1, B);
+      rc = post_launch("blind_rotate_fft_tq_kernel");
+    } else if (g_fft_mode == 3 && B >= (int64_t)2 * TPC * st->sms) {
+      const size_t smem = sizeof(FSmemTP);
+      if ((rc = set_smem(blind_rotate_fft_tp_kernel, smem))) return rc;
+      blind_rotate_fft_tp_kernel<<<(unsigned)((B + TPC - 1) / TPC), TPC * FT, smem, s>>>(
+          (const double2 *)bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st->fft_fwd, st->fft_inv, acc, s0, s1, B);
+      rc = post_launch("blind_rotate_fft_tp_kernel");
     } else if (g_fft_mode == 2 && B >= (int64_t)2 * TXC * st->sms) {
       const size_t smem = sizeof(FSmemTX);
       if ((rc = set_smem(blind_rotate_fft_tx_kernel, smem))) return rc;
