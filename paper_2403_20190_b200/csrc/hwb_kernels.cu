@@ -1964,7 +1964,14 @@ __global__ void __launch_bounds__(TPC * FT, 2)
   extern __shared__ uint4 smem_raw[];
   FSmemTP &sm = *reinterpret_cast<FSmemTP *>(smem_raw);
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
-  const int q = 2 * (warp & 1) + (lane & 1), t = 16 * (warp >> 1) + (lane >> 1);
+#ifndef HWB_TD_SPLIT
+#define HWB_TD_SPLIT 1
+#endif
+  // HWB_TD_SPLIT: half = warp >> 2, so every scheduler (warp % 4) runs one warp of each
+  // half (independent instruction streams); 0: half = warp & 1 (a scheduler's warps in
+  // lockstep)
+  const int hsel = HWB_TD_SPLIT ? (warp >> 2) : (warp & 1), hpos = HWB_TD_SPLIT ? (warp & 3) : (warp >> 1);
+  const int q = 2 * hsel + (lane & 1), t = 16 * hpos + (lane >> 1);
   const FLay lay = make_flay(t);
   const int64_t bb = (int64_t)blockIdx.x * TPC + q;
   const bool valid = bb < B;
@@ -2009,8 +2016,8 @@ __global__ void __launch_bounds__(TPC * FT, 2)
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   uint32_t key_phase = 0;
   const int lv = (int)g.levels;
-  const int half = warp & 1, hbar = 1 + half;
-  const bool leader = lane == 0 && warp < 2;
+  const int half = hsel, hbar = 1 + half;
+  const bool leader = lane == 0 && hpos == 0;
   // a half is done with the key buffer (slice or, for half 1, inverse scratch):
   // the second half to finish issues the next row's slice
   auto release = [&](int s_, int r_) {
