@@ -30,6 +30,9 @@ sys.path.insert(0, REPO)
 
 import numpy as np  # noqa: E402
 
+# FFT ladder mode (hwb_set_fft_mode) -> the kernel that runs a cfg2 batch of 4096
+FFT_KERNELS = {0: "blind_rotate_fft_kernel", 1: "blind_rotate_fft_tm_kernel", 2: "blind_rotate_fft_tx_kernel",
+               3: "blind_rotate_fft_tp_kernel", 4: "blind_rotate_fft_tq_kernel", 5: "blind_rotate_fft_td_kernel"}
 METRIC = "bootstrappings/sec"
 UNIT = "PBS/s"
 KEY_SEED, ENC_SEED = 1, 2
@@ -46,8 +49,10 @@ def parse():
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--ladder", default="auto", choices=["auto", "fft", "ntt"],
                     help="blind rotation: FP64 FFT ladder or two-prime NTT ladder (bit-identical)")
-    ap.add_argument("--fft-mode", type=int, default=1, choices=[0, 1],
-                    help="FFT ladder accumulators: 0 registers, 1 TMEM (bit-identical)")
+    ap.add_argument("--fft-mode", type=int, default=5, choices=list(range(6)),
+                    help="FFT ladder (bit-identical): 0 register accumulators; TMEM accumulators with "
+                         "1 two ciphertexts per thread, 2 one per thread, 3 lane-paired, 4 one 16-warp CTA, "
+                         "5 lane-paired decoupled halves (default)")
     ap.add_argument("--ks-engine", default="auto", choices=["auto", "tc", "simt"],
                     help="LWE key switch: tensor cores (tcgen05 int8) or the integer-pipe kernel")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -624,8 +629,7 @@ def bench_hwb(args):
         peak = probe_fp64_peak(torch, _lib, tfhe)
         achieved = w_fp64 * B / br_avg_s
         w_main, unit_main = w_fp64, "G FP64-instr/s"
-        roof_kernel = ("blind_rotate_fft_tm_kernel (FP64 FFT ladder, TMEM accumulators)" if args.fft_mode == 1
-                       else "blind_rotate_fft_kernel (FP64 FFT ladder)")
+        roof_kernel = f"{FFT_KERNELS[args.fft_mode]} (FP64 FFT ladder, FFT mode {args.fft_mode})"
         work_txt = f"W_fp64 = {w_fp64} FP64 instructions (n x {w_fstep} per CMUX)"
         peak_src = "measured live: probe_fp64_kernel (8 independent DFMA chains per thread)"
     else:
@@ -658,7 +662,14 @@ def bench_hwb(args):
         # transposes (2 per transform, write + read), the key slices (TMA write +
         # LDS read), digit extraction and byte digits, accumulator update.
         Hf = N // 2
-        if args.fft_mode == 1:
+        if args.fft_mode == 5:
+            # lane-paired TMEM ladder: a key / twiddle LDS.128 serves a lane pair (2 of 4
+            # wavefronts per warp instruction, tools/lds_bcast_bench.cu), each staged
+            # slice 4 ciphertexts (TMA write); decomposition words once per component;
+            # compact per-thread twiddles (8 per transform) from shared memory
+            smem_step = ((2 * lv + 4) * 2 * 2 * Hf * 16 + 2 * lv * 2 * 2 * Hf * 16 * (1 / 4 + 1 / 2)
+                         + (2 * lv + 4) * 8 * 64 * 16 / 2 + 2 * N * 4 * 2 + 2 * N * 4 * 2)
+        elif args.fft_mode == 1:
             # TMEM accumulators: each key value read serves 2 ciphertexts, each staged
             # slice 4; digits re-extracted per digit row (rotated + plain reads)
             smem_step = ((2 * lv + 4) * 2 * 2 * Hf * 16 + 2 * lv * 2 * 2 * Hf * 16 * (1 / 4 + 1 / 2)
@@ -695,8 +706,7 @@ def bench_hwb(args):
                      "traffic": ncu_traffic(B, (P.lwe_n * 2 * lv * 2 * 2 * (N // 2) * 16 if use_fft
                                                 else 4 * P.lwe_n * 2 * lv * 2 * 2 * N)
                                                + 4 * (B * (P.lwe_n + 1) + B * (N + 1) + 2 * N),
-                                            ("blind_rotate_fft_tm_kernel" if args.fft_mode == 1
-                                             else "blind_rotate_fft_kernel") if use_fft else "ntt"),
+                                            FFT_KERNELS[args.fft_mode] if use_fft else "ntt"),
                      "work_per_pbs": work_txt, "peak_source": peak_src,
                      "traffic_note": ("ncu --set full flushes L2 before each replayed launch, so the "
                                       "64-step segment's accumulators (B x 8 KB) and key slices are read "

@@ -427,7 +427,7 @@ __device__ __forceinline__ void inv_fft_pp(double2 (*x)[FC], double2 *s0, double
 namespace hwb {
 
 // frelayout_k with a named barrier over NT threads (both barriers kept: one scratch)
-template <int K, int FROM, int TO, int NT>
+template <int K, int FROM, int TO, int NT, bool TRAIL = true>
 __device__ __forceinline__ void frelayout_hk(double2 (*x)[FC], double2 *scr, const FLay &L, int bar) {
   const uint32_t bf = flay_base<FROM>(L), bt = flay_base<TO>(L);
 #pragma unroll
@@ -439,10 +439,12 @@ __device__ __forceinline__ void frelayout_hk(double2 (*x)[FC], double2 *scr, con
   for (int k = 0; k < K; ++k)
 #pragma unroll
     for (int j = 0; j < FC; ++j) x[k][j] = scr[k * FH + (bt ^ fswz(joff<FH, FT, TO>(j)))];
-  gsync<NT>(bar);
+  if (TRAIL) gsync<NT>(bar);
 }
 
-template <int K, int NT, bool CT = false>
+// TRAIL2 = false drops the trailing barrier of the second transpose: the caller
+// guarantees a group barrier before the next write into scr.
+template <int K, int NT, bool CT = false, bool TRAIL2 = true>
 __device__ __forceinline__ void fwd_fft_hk(double2 (*x)[FC], double2 *scr, const FLay &L, int t,
                                            const double2 *__restrict__ tw, int bar) {
   using G = FGeo;
@@ -458,7 +460,7 @@ __device__ __forceinline__ void fwd_fft_hk(double2 (*x)[FC], double2 *scr, const
 #pragma unroll
     for (int k = 0; k < K; ++k) fft_stage<true, s - G::LO, false, 0, slot, CT>(x[k], t, tw);
   });
-  frelayout_hk<K, LAY_M, LAY_B, NT>(x, scr, L, bar);
+  frelayout_hk<K, LAY_M, LAY_B, NT, TRAIL2>(x, scr, L, bar);
   static_for<0, G::B_TOP>([&](auto Q) {
     constexpr int s = G::B_TOP - 1 - decltype(Q)::value;
     constexpr int slot = G::M_SLOTS + (G::C >> G::B_TOP) * ((1 << decltype(Q)::value) - 1);
@@ -467,7 +469,7 @@ __device__ __forceinline__ void fwd_fft_hk(double2 (*x)[FC], double2 *scr, const
   });
 }
 
-template <int K, int NT, bool CT = false>
+template <int K, int NT, bool CT = false, bool TRAIL2 = true>
 __device__ __forceinline__ void inv_fft_hk(double2 (*x)[FC], double2 *scr, const FLay &L, int t,
                                            const double2 *__restrict__ tw, int bar) {
   using G = FGeo;
@@ -484,7 +486,7 @@ __device__ __forceinline__ void inv_fft_hk(double2 (*x)[FC], double2 *scr, const
 #pragma unroll
     for (int k = 0; k < K; ++k) fft_stage<false, s - G::LO, false, 0, slot, CT>(x[k], t, tw);
   });
-  frelayout_hk<K, LAY_M, LAY_A, NT>(x, scr, L, bar);
+  frelayout_hk<K, LAY_M, LAY_A, NT, TRAIL2>(x, scr, L, bar);
   static_for<0, G::LOGN - G::T>([&](auto Q) {
     constexpr int s = G::T + decltype(Q)::value;
 #pragma unroll

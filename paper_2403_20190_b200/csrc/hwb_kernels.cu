@@ -2061,7 +2061,9 @@ __global__ void __launch_bounds__(TPC * FT, 2)
       for (int j = 0; j < FC; ++j)
         x[0][j] = make_double2(u2d_minus((pw[0][j] >> sh) & g.mask, dig_off),
                                u2d_minus((pw[1][j] >> sh) & g.mask, dig_off));
-      fwd_fft_hk<1, GT, true>(x, fscr, lay, t, sm.twf, hbar);
+      // (no trailing barrier on the second transpose: the release barrier after the MAC
+      // precedes the next write into fscr)
+      fwd_fft_hk<1, GT, true, false>(x, fscr, lay, t, sm.twf, hbar);
       mbar_wait(&sm.key_full, key_phase);
       key_phase ^= 1u;
 #pragma unroll
@@ -2103,7 +2105,10 @@ __global__ void __launch_bounds__(TPC * FT, 2)
 #pragma unroll
           for (int j = 0; j < FC; ++j) Y[0][j] = tm_get(y, j);
         }
-        inv_fft_hk<1, GT, true>(Y, fscr, lay, t, sm.twi, hbar);
+        if (c == 1 && h == 1)   // the end-of-step barrier precedes the next write into fscr
+          inv_fft_hk<1, GT, true, false>(Y, fscr, lay, t, sm.twi, hbar);
+        else
+          inv_fft_hk<1, GT, true>(Y, fscr, lay, t, sm.twi, hbar);
         if (h == 0) {
 #pragma unroll
           for (int j = 0; j < FC; ++j) {
@@ -4207,9 +4212,13 @@ int64_t hwb_set_fft_cluster_batch(int64_t max_batch) {
   if (max_batch >= -1) g_fft_cluster_max_batch = max_batch;
   return prev;
 }
-// FFT PBS ladder accumulators: 0 = registers (g_fft_cpb ciphertexts per CTA), 1 = TMEM
-// (default: 65.5 vs 66.6 ms per cfg2 batch of 4096)
-static thread_local int g_fft_mode = 1;
+// FFT PBS ladder (batches of >= 8 ciphertexts per SM; smaller ones use the register
+// ladder): 0 = registers (g_fft_cpb ciphertexts per CTA), 1 = TMEM accumulators, two
+// ciphertexts per thread; 2 = TMEM, one per thread (16 warps/SM); 3 = 2 with lane-paired
+// ciphertexts; 4 = 3 as one 16-warp CTA of decoupled groups; 5 = 3 with decoupled halves
+// (default: cfg2 B = 4096 in 54.5 ms vs 61.6 / 60.1 / 59.6 / 63.2 ms for modes 1-4,
+// DESIGN.md §3b).  All bit-identical.
+static thread_local int g_fft_mode = 5;
 
 int hwb_set_fft_mode(int mode) {
   if (mode < 0 || mode > 5)
@@ -4501,7 +4510,7 @@ static int level_fft(const hwb_params *p, const void *ggsw_fft, const int32_t *g
         st->fft2_fwd[1], st->fft2_inv[0], st->fft2_inv[1]);
     return post_launch("level_fft2_kernel");
   }
-  if (g_fft_mode == 1 && m % TMC == 0 && B * m >= (int64_t)2 * TMC * st->sms) {
+  if (g_fft_mode >= 1 && m % TMC == 0 && B * m >= (int64_t)2 * TMC * st->sms) {
     // sub-ciphertexts of an item share its GGSW: four per CTA on the TMEM path
     const size_t smem_tm = sizeof(FSmemTM);
     if ((rc = set_smem(level_fft_tm_kernel<MODE>, smem_tm))) return rc;

@@ -112,7 +112,8 @@ def test_latency_threshold_roundtrip():
 def test_fft_ladder_knobs():
     """FFT ladder settings: validation before any CUDA call, query-only values."""
     L = _lib.load()
-    assert L.hwb_set_fft_mode(3) == _lib.HWB_EINVAL
+    assert L.hwb_set_fft_mode(len(_lib.FFT_MODES)) == _lib.HWB_EINVAL
+    assert L.hwb_set_fft_mode(-1) == _lib.HWB_EINVAL
     assert "mode" in L.hwb_last_error().decode()
     assert L.hwb_set_fft_cluster_mode(2) == _lib.HWB_EINVAL
     assert L.hwb_set_fft_group(3) == _lib.HWB_EINVAL

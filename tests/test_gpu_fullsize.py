@@ -1,7 +1,7 @@
 """GPU parity at the BASELINE sizes, through the default (`ladder="auto"`) path.
 
-The headline number comes from the TMEM FFT ladder (`blind_rotate_fft_tm_kernel`,
-batches >= 8 ciphertexts per SM) fused with the tcgen05 key switch; cfg4 runs the
+The headline number comes from the TMEM FFT ladder (`blind_rotate_fft_td_kernel`,
+FFT mode 5, batches >= 8 ciphertexts per SM) fused with the tcgen05 key switch; cfg4 runs the
 N = 2048 FFT ladder.  Each test runs a full-size batch (n = 630 / 500 / 750 steps,
 including cfg2's partial last 64-step segment, 630 = 9 x 64 + 54), then
 

@@ -297,14 +297,15 @@ def test_pbs_fft_ladder_vs_c_oracle(coracle, name):
             _lib.check(L.hwb_set_fft_segment(seg))
             _lib.check(L.hwb_set_fft_group(group))     # ragged: 37 items in CTAs of 1, 2 or 4
             assert_u32_equal(tfhe.pbs_batch(P, lwe, tvs, bsk, ksk, ladder="fft"), want)
-        _lib.check(L.hwb_set_fft_mode(1))               # TMEM accumulators, 4 items per CTA
         sms = torch.cuda.get_device_properties(0).multi_processor_count
-        big = 8 * sms + 5                               # the TMEM ladder needs >= 8 items per SM; ragged
+        big = 8 * sms + 5                               # the TMEM ladders need >= 8 items per SM; ragged
         rep = np.resize(np.arange(37), big)
         want_big = want[rep]
-        for seg in (1, 64):
-            _lib.check(L.hwb_set_fft_segment(seg))
-            assert_u32_equal(tfhe.pbs_batch(P, lwe[rep], tvs[rep], bsk, ksk, ladder="fft"), want_big)
+        for mode in _lib.FFT_MODES[1:]:                  # TMEM accumulators: every CTA shape
+            _lib.check(L.hwb_set_fft_mode(mode))
+            for seg in (1, 64):
+                _lib.check(L.hwb_set_fft_segment(seg))
+                assert_u32_equal(tfhe.pbs_batch(P, lwe[rep], tvs[rep], bsk, ksk, ladder="fft"), want_big)
         L.hwb_set_fft_latency_batch(1 << 40)            # latency ladder (N = 1024)
         assert_u32_equal(tfhe.pbs_batch(P, lwe, tvs, bsk, ksk, ladder="fft"), want)
         assert_u32_equal(tfhe.pbs_batch(P, lwe[:1], tvs[:1], bsk, ksk, ladder="fft"), want[:1])
@@ -320,7 +321,7 @@ def test_pbs_fft_ladder_vs_c_oracle(coracle, name):
     finally:
         _lib.check(L.hwb_set_fft_segment(64))
         _lib.check(L.hwb_set_fft_group(1))
-        _lib.check(L.hwb_set_fft_mode(1))
+        _lib.check(L.hwb_set_fft_mode(_lib.FFT_MODE_DEFAULT))
         L.hwb_set_fft_latency_batch(prev)
 
 
