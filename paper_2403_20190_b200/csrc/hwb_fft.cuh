@@ -178,7 +178,12 @@ __device__ __forceinline__ void fsync(int bar) {
 // The CTA is exactly the 64 threads of the transform: CTA barriers.  `after_first`
 // runs once all threads have passed the first barrier (everyone finished the
 // previous consumer of any shared buffer -- the key-slice prefetch hook).
-template <int FROM, int TO, typename F>
+// TRAIL = false drops the trailing barrier.  Legal for the FIRST transpose of a
+// transform (A -> M forward, B -> M inverse): the second transpose then stores each
+// thread's values to exactly the addresses that thread loaded in the first (its
+// middle-layout slots), so no thread can overwrite a location another thread has yet
+// to read; the second transpose's own barrier orders everything after it.
+template <int FROM, int TO, typename F, bool TRAIL = true>
 __device__ __forceinline__ void frelayout(double2 (&x)[FC], double2 *scr, const FLay &L, F &&after_first,
                                           int bar = 0) {
   const uint32_t bf = flay_base<FROM>(L), bt = flay_base<TO>(L);
@@ -188,7 +193,7 @@ __device__ __forceinline__ void frelayout(double2 (&x)[FC], double2 *scr, const 
   after_first();
 #pragma unroll
   for (int j = 0; j < FC; ++j) x[j] = scr[bt ^ fswz(joff<FH, FT, TO>(j))];
-  fsync(bar);
+  if (TRAIL) fsync(bar);
 }
 struct NoHook {
   __device__ __forceinline__ void operator()() const {}
@@ -203,7 +208,7 @@ __device__ __forceinline__ void fwd_fft(double2 (&x)[FC], double2 *scr, const FL
     constexpr int s = G::LOGN - 1 - decltype(K)::value;
     fft_stage<true, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x, t, tw, cg);
   });
-  frelayout<LAY_A, LAY_M>(x, scr, L, hook, bar);
+  frelayout<LAY_A, LAY_M, F &, false>(x, scr, L, hook, bar);
   static_for<0, G::T - G::LOGC>([&](auto K) {
     constexpr int s = G::T - 1 - decltype(K)::value;
     constexpr int slot = (1 << decltype(K)::value) - 1;
@@ -226,7 +231,7 @@ __device__ __forceinline__ void inv_fft(double2 (&x)[FC], double2 *scr, const FL
     constexpr int slot = G::C - 2 * (G::C >> (s + 1));
     fft_stage<false, s, false, 0, slot>(x, t, tw, cg);
   });
-  frelayout<LAY_B, LAY_M>(x, scr, L, NoHook(), bar);
+  frelayout<LAY_B, LAY_M, NoHook, false>(x, scr, L, NoHook(), bar);
   static_for<0, G::T - G::LOGC>([&](auto K) {
     constexpr int s = G::LOGC + decltype(K)::value;
     constexpr int slot = G::B_SLOTS + (1 << (G::T - G::LOGC)) - (1 << (G::T - s));
@@ -242,7 +247,7 @@ __device__ __forceinline__ void inv_fft(double2 (&x)[FC], double2 *scr, const FL
 // K independent inverse transforms in lockstep (the four accumulators of a CMUX
 // step): one pair of barriers per transpose for all K, K times the ILP per stage.
 // scr holds K * FH elements.
-template <int K, int FROM, int TO, typename F = NoHook>
+template <int K, int FROM, int TO, typename F = NoHook, bool TRAIL = true>
 __device__ __forceinline__ void frelayout_k(double2 (*x)[FC], double2 *scr, const FLay &L, F &&after_first = F()) {
   const uint32_t bf = flay_base<FROM>(L), bt = flay_base<TO>(L);
 #if HWB_X_NOTRANS   // timing-only sensitivity build: barriers kept, no shared-memory round trip
@@ -261,7 +266,7 @@ __device__ __forceinline__ void frelayout_k(double2 (*x)[FC], double2 *scr, cons
   for (int k = 0; k < K; ++k)
 #pragma unroll
     for (int j = 0; j < FC; ++j) x[k][j] = scr[k * FH + (bt ^ fswz(joff<FH, FT, TO>(j)))];
-  __syncthreads();
+  if (TRAIL) __syncthreads();
 }
 
 // K independent forward transforms in lockstep (the two key halves of a GGSW row;
@@ -275,7 +280,7 @@ __device__ __forceinline__ void fwd_fft_k(double2 (*x)[FC], double2 *scr, const 
 #pragma unroll
     for (int k = 0; k < K; ++k) fft_stage<true, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x[k], t, tw, cg);
   });
-  frelayout_k<K, LAY_A, LAY_M>(x, scr, L, hook);
+  frelayout_k<K, LAY_A, LAY_M, F &, false>(x, scr, L, hook);
   static_for<0, G::T - G::LOGC>([&](auto Q) {
     constexpr int s = G::T - 1 - decltype(Q)::value;
     constexpr int slot = (1 << decltype(Q)::value) - 1;
@@ -301,7 +306,7 @@ __device__ __forceinline__ void inv_fft_k(double2 (*x)[FC], double2 *scr, const 
 #pragma unroll
     for (int k = 0; k < K; ++k) fft_stage<false, s, false, 0, slot, CT>(x[k], t, tw, cg);
   });
-  frelayout_k<K, LAY_B, LAY_M>(x, scr, L);
+  frelayout_k<K, LAY_B, LAY_M, NoHook, false>(x, scr, L);
   static_for<0, G::T - G::LOGC>([&](auto Q) {
     constexpr int s = G::LOGC + decltype(Q)::value;
     constexpr int slot = G::B_SLOTS + (1 << (G::T - G::LOGC)) - (1 << (G::T - s));
@@ -453,7 +458,7 @@ __device__ __forceinline__ void fwd_fft_hk(double2 (*x)[FC], double2 *scr, const
 #pragma unroll
     for (int k = 0; k < K; ++k) fft_stage<true, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x[k], t, tw);
   });
-  frelayout_hk<K, LAY_A, LAY_M, NT>(x, scr, L, bar);
+  frelayout_hk<K, LAY_A, LAY_M, NT, false>(x, scr, L, bar);
   static_for<0, G::T - G::LOGC>([&](auto Q) {
     constexpr int s = G::T - 1 - decltype(Q)::value;
     constexpr int slot = (1 << decltype(Q)::value) - 1;
@@ -479,7 +484,7 @@ __device__ __forceinline__ void inv_fft_hk(double2 (*x)[FC], double2 *scr, const
 #pragma unroll
     for (int k = 0; k < K; ++k) fft_stage<false, s, false, 0, slot, CT>(x[k], t, tw);
   });
-  frelayout_hk<K, LAY_B, LAY_M, NT>(x, scr, L, bar);
+  frelayout_hk<K, LAY_B, LAY_M, NT, false>(x, scr, L, bar);
   static_for<0, G::T - G::LOGC>([&](auto Q) {
     constexpr int s = G::LOGC + decltype(Q)::value;
     constexpr int slot = G::B_SLOTS + (1 << (G::T - G::LOGC)) - (1 << (G::T - s));
