@@ -451,51 +451,51 @@ __device__ __forceinline__ void frelayout_hk(double2 (*x)[FC], double2 *scr, con
 // guarantees a group barrier before the next write into scr.
 template <int K, int NT, bool CT = false, bool TRAIL2 = true>
 __device__ __forceinline__ void fwd_fft_hk(double2 (*x)[FC], double2 *scr, const FLay &L, int t,
-                                           const double2 *__restrict__ tw, int bar) {
+                                           const double2 *__restrict__ tw, int bar, int cg = 0) {
   using G = FGeo;
   static_for<0, G::LOGN - G::T>([&](auto Q) {
     constexpr int s = G::LOGN - 1 - decltype(Q)::value;
 #pragma unroll
-    for (int k = 0; k < K; ++k) fft_stage<true, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x[k], t, tw);
+    for (int k = 0; k < K; ++k) fft_stage<true, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x[k], t, tw, cg);
   });
   frelayout_hk<K, LAY_A, LAY_M, NT, false>(x, scr, L, bar);
   static_for<0, G::T - G::LOGC>([&](auto Q) {
     constexpr int s = G::T - 1 - decltype(Q)::value;
     constexpr int slot = (1 << decltype(Q)::value) - 1;
 #pragma unroll
-    for (int k = 0; k < K; ++k) fft_stage<true, s - G::LO, false, 0, slot, CT>(x[k], t, tw);
+    for (int k = 0; k < K; ++k) fft_stage<true, s - G::LO, false, 0, slot, CT>(x[k], t, tw, cg);
   });
   frelayout_hk<K, LAY_M, LAY_B, NT, TRAIL2>(x, scr, L, bar);
   static_for<0, G::B_TOP>([&](auto Q) {
     constexpr int s = G::B_TOP - 1 - decltype(Q)::value;
     constexpr int slot = G::M_SLOTS + (G::C >> G::B_TOP) * ((1 << decltype(Q)::value) - 1);
 #pragma unroll
-    for (int k = 0; k < K; ++k) fft_stage<true, s, false, 0, slot, CT>(x[k], t, tw);
+    for (int k = 0; k < K; ++k) fft_stage<true, s, false, 0, slot, CT>(x[k], t, tw, cg);
   });
 }
 
 template <int K, int NT, bool CT = false, bool TRAIL2 = true>
 __device__ __forceinline__ void inv_fft_hk(double2 (*x)[FC], double2 *scr, const FLay &L, int t,
-                                           const double2 *__restrict__ tw, int bar) {
+                                           const double2 *__restrict__ tw, int bar, int cg = 0) {
   using G = FGeo;
   static_for<0, G::B_TOP>([&](auto Q) {
     constexpr int s = decltype(Q)::value;
     constexpr int slot = G::C - 2 * (G::C >> (s + 1));
 #pragma unroll
-    for (int k = 0; k < K; ++k) fft_stage<false, s, false, 0, slot, CT>(x[k], t, tw);
+    for (int k = 0; k < K; ++k) fft_stage<false, s, false, 0, slot, CT>(x[k], t, tw, cg);
   });
   frelayout_hk<K, LAY_B, LAY_M, NT, false>(x, scr, L, bar);
   static_for<0, G::T - G::LOGC>([&](auto Q) {
     constexpr int s = G::LOGC + decltype(Q)::value;
     constexpr int slot = G::B_SLOTS + (1 << (G::T - G::LOGC)) - (1 << (G::T - s));
 #pragma unroll
-    for (int k = 0; k < K; ++k) fft_stage<false, s - G::LO, false, 0, slot, CT>(x[k], t, tw);
+    for (int k = 0; k < K; ++k) fft_stage<false, s - G::LO, false, 0, slot, CT>(x[k], t, tw, cg);
   });
   frelayout_hk<K, LAY_M, LAY_A, NT, TRAIL2>(x, scr, L, bar);
   static_for<0, G::LOGN - G::T>([&](auto Q) {
     constexpr int s = G::T + decltype(Q)::value;
 #pragma unroll
-    for (int k = 0; k < K; ++k) fft_stage<false, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x[k], t, tw);
+    for (int k = 0; k < K; ++k) fft_stage<false, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x[k], t, tw, cg);
   });
 }
 

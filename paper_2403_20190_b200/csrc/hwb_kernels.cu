@@ -3271,6 +3271,254 @@ __global__ void __launch_bounds__(2 * FT, 1)
   if (tid == 0) o[N] = acc[N];
 }
 
+// ---------------------------------------------------------------------------
+// N = 2048 TMEM ladder (`blind_rotate_fft2_td_kernel`, FFT mode >= 1 at N = 2048).
+//
+// The register FFT2 ladder above holds one ciphertext's 4 spectral accumulators in
+// registers (2 ciphertexts per SM) and stages a 64 KB key slice per ciphertext.  Here
+// the accumulators live in TMEM (64 KB per ciphertext: 4 per SM) and one CTA of 16
+// warps runs 4 ciphertexts as two decoupled lane-paired pairs (mode 5's layout at
+// N = 2048): warp w carries pair P = w >> 3, half g = (w >> 2) & 1 of the folded
+// 1024-point transform, positions t = 16 (w & 3) + (lane >> 1), ciphertext
+// q = 2 P + (lane & 1).  All 4 ciphertexts share each TMA-staged 64 KB key slice
+// (released per pair; the second release issues the next row's copy), a lane pair
+// reads each key value and twiddle at one address, and every scheduler (w % 4) runs
+// one warp of each (pair, half).  The level-0 stage joins the halves: forward, each
+// thread forms it from the four quarter positions of its digits; inverse, the halves
+// exchange their values through the transpose scratch.
+
+constexpr int T2C = 4;   // ciphertexts per CTA
+
+struct FSmem2TD {
+  // working ciphertexts (a, b), N = 2048, padded (t2_pad): coefficient i of component
+  // c at c (N + 16) + i + 8 (i >> 10), odd ciphertexts 16 words further -- a lane
+  // quad's 4 (ciphertext, half) digit reads land on 4 different bank octets
+  uint32_t acc[T2C][2 * (4 * FH + 16) + 16];
+  double2 scr[T2C][2][FH];         // transpose / level-0 scratch per (ciphertext, half)
+  // the row's key slice [c][h][g][j][t] (64 KB, 8 TMA chunks of 8 KB at a stride of
+  // 8 KB + 64 B, so a lane quad's two halves hit different bank groups)
+  double2 key[8 * (FC * FT + 4)];
+  double2 twf[2][kTwc * FT + 4], twi[2][kTwc * FT + 4];   // compact per-thread twiddles of half g (+64 B)
+  uint64_t key_full;
+  uint32_t key_cnt;
+  uint32_t tmem_slot;
+};
+
+__device__ __forceinline__ int t2_pad(int c, int i) { return c * (4 * FH + 16) + i + 8 * (i >> 10); }
+// rot_read on a t2_pad-ded component
+__device__ __forceinline__ uint32_t rot_read_t2(const uint32_t *poly, int i, int e) {
+  constexpr int N = 4 * FH;
+  const int src = (i - e) & (2 * N - 1), idx = src & (N - 1);
+  const uint32_t val = poly[idx + 8 * (idx >> 10)];
+  return src >= N ? 0u - val : val;
+}
+
+__global__ void __launch_bounds__(16 * 32, 1)
+    blind_rotate_fft2_td_kernel(const double2 *__restrict__ ggsw, const uint32_t *__restrict__ lwe_in,
+                                const uint32_t *__restrict__ tv, int tv_per_item, uint32_t *lwe_out, int L, Gadget g,
+                                const double2 *__restrict__ twf0, const double2 *__restrict__ twf1,
+                                const double2 *__restrict__ twi0, const double2 *__restrict__ twi1, uint32_t *acc_io,
+                                int s0, int s1, int64_t B) {
+  constexpr int N = 4 * FH;
+  constexpr int LOG2M = 12;
+  constexpr int GT = 256;   // threads per pair (named barrier)
+  extern __shared__ uint4 smem_raw[];
+  FSmem2TD &sm = *reinterpret_cast<FSmem2TD *>(smem_raw);
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  // lane quad (4m .. 4m + 3) = position t for both ciphertexts of the pair (lane bit 0)
+  // and both halves (lane bit 1): key and twiddle addresses shared by lane bit 0, the
+  // halves' exchanges (level-0 digits forward, level-0 stage inverse) by shuffles
+  const int pr = warp >> 3, hf = (lane >> 1) & 1, bar = 1 + pr;
+  const int q = 2 * pr + (lane & 1), t = 8 * (warp & 7) + (lane >> 2), tq = hf * FT + t;
+  FLay lay = make_flay(t);
+  {   // the quad's four (ciphertext, half) buffers on distinct 16-byte bank groups
+    const uint32_t xo = (uint32_t)((q & 1) * 4 + hf * 2);
+    lay.a ^= xo;
+    lay.m ^= xo;
+    lay.b ^= xo;
+  }
+  const int64_t bb = (int64_t)blockIdx.x * T2C + q;
+  const bool valid = bb < B;
+  const int64_t bq = valid ? bb : B - 1;
+  const uint32_t *row = lwe_in + bq * (int64_t)(L + 1);
+  uint32_t *acc = sm.acc[q] + (q & 1) * 16;
+  if (s0 == 0) {
+    const int bt = mod_switch(row[L], LOG2M);
+    const uint32_t *tp = tv + (tv_per_item ? bq * 2 * N : 0);
+    const int e = (2 * N - bt) & (2 * N - 1);   // X^-b~
+    for (int k = tq; k < 2 * N; k += 2 * FT) {
+      const int c = k >= N, i = k & (N - 1);
+      acc[t2_pad(c, i)] = rot_read<N>(tp + c * N, i, e);
+    }
+  } else {
+    for (int k = tq; k < 2 * N; k += 2 * FT) acc[t2_pad(k >= N, k & (N - 1))] = acc_io[bq * 2 * N + k];
+  }
+  for (int k = tid; k < kTwc * FT; k += 16 * 32) {
+    const int fs = twc_full<true>(k / FT) * FT + k % FT, is = twc_full<false>(k / FT) * FT + k % FT;
+    sm.twf[0][k] = twf0[fs];
+    sm.twf[1][k] = twf1[fs];
+    sm.twi[0][k] = twi0[is];
+    sm.twi[1][k] = twi1[is];
+  }
+  constexpr uint32_t kSliceBytes = 2 * 2 * 2 * FC * FT * sizeof(double2);
+  const size_t ggsw_f = (size_t)2 * g.levels * 2 * 2 * 2 * FC * FT;
+  const int lv = (int)g.levels;
+  auto key_chunks = [&](const double2 *src) {   // 8 chunks [c][h][g] of 8 KB
+#pragma unroll 1
+    for (int c8 = 0; c8 < 8; ++c8)
+      bulk_g2s(sm.key + c8 * (FC * FT + 4), src + c8 * FC * FT, FC * FT * sizeof(double2), &sm.key_full);
+  };
+  if (tid == 0) {
+    mbar_init(&sm.key_full, 1);
+    sm.key_cnt = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&sm.key_full, kSliceBytes);   // the first row's slice
+    key_chunks(ggsw + (size_t)s0 * ggsw_f);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_slot)),
+                 "r"(512u));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t lane_addr = sm.tmem_slot + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 128);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) tm_zero32(lane_addr + (uint32_t)(k * 32));
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  uint32_t key_phase = 0;
+  const double dig_off = 4503599627370496.0 + (double)g.half;
+  double2 *fscr = sm.scr[q][hf];
+  const bool leader = lane == 0 && (warp & 7) == 0;   // warps 0 and 8
+  auto release = [&](int s_, int r_) {   // the second pair to finish the slice fetches the next
+    if (!leader) return;
+    __threadfence_block();
+    if (atomicAdd(&sm.key_cnt, 1u) == 1u) {
+      sm.key_cnt = 0;
+      const int nr = r_ + 1 < 2 * lv ? r_ + 1 : 0, ns = r_ + 1 < 2 * lv ? s_ : s_ + 1;
+      if (ns < s1) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&sm.key_full, kSliceBytes);
+        key_chunks(ggsw + (size_t)ns * ggsw_f + (size_t)nr * (2 * 2 * 2 * FC * FT));
+      }
+    }
+  };
+  const double2 wi0 = c_fw0[1];
+  uint32_t a_nx = row[s0];   // the next step's mask word, loaded a step ahead
+#pragma unroll 1
+  for (int s = s0; s < s1; ++s) {
+    const int e = mod_switch(a_nx, LOG2M);   // X^{a~_s}
+    a_nx = row[s + 1];
+#pragma unroll 1
+    for (int r = 0; r < 2 * lv; ++r) {
+      // digit order (hw/tfhe.py:290-298): rows 0..l-1 = digits of b, l..2l-1 of a
+      const int comp = r < lv ? 1 : 0;
+      const int tt = r < lv ? r : r - lv;
+      const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
+      const uint32_t *ac = acc + t2_pad(comp, 0);
+      double2 x[1][FC];
+#pragma unroll
+      for (int j = 0; j < FC; ++j) {
+        const int k = t + FT * j;
+        // this half's two quarter positions k + 512 (2 hf + {0, 1}); the partner half
+        // (lane ^ 2) forms the other two
+        uint32_t own = 0;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int i = k + FH * (2 * hf + u);
+          own |= ((decomp_prep(rot_read_t2(ac, i, e) - ac[i + 8 * (i >> 10)], g) >> sh) & g.mask) << (16 * u);
+        }
+        const uint32_t par = __shfl_xor_sync(0xffffffffu, own, 2);
+        const uint32_t q01 = hf ? par : own, q23 = hf ? own : par;
+        const double2 zk = make_double2(u2d_minus(q01 & 0xFFFFu, dig_off), u2d_minus(q23 & 0xFFFFu, dig_off));
+        const double2 zh = make_double2(u2d_minus(q01 >> 16, dig_off), u2d_minus(q23 >> 16, dig_off));
+        x[0][j] = fft2_first(zk, zh, hf);
+      }
+      // (no trailing barrier on the second transpose: the release barrier after the MAC
+      // precedes the next write into fscr)
+      fwd_fft_hk<1, GT, true, false>(x, fscr, lay, t, sm.twf[hf], bar, 1 + hf);
+      mbar_wait(&sm.key_full, key_phase);
+      key_phase ^= 1u;
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        const uint32_t a = lane_addr + (uint32_t)(ch * 32);
+        uint32_t y[32];
+        tm_ld32(a, y);   // zeroed at the end of the previous product
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < FC; ++j) {
+          const double2 k = sm.key[(ch * 2 + hf) * (FC * FT + 4) + j * FT + t];
+          double2 u = tm_get(y, j);
+          u.x = fma(x[0][j].x, k.x, fma(-x[0][j].y, k.y, u.x));
+          u.y = fma(x[0][j].x, k.y, fma(x[0][j].y, k.x, u.y));
+          tm_st_acc(a + 4 * j, u);
+        }
+      }
+      gsync<GT>(bar);   // the pair is past the slice
+      release(s, r);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    // inverse transforms, one accumulator at a time: the half's 512-point inverse, then
+    // the level-0 Gentleman-Sande stage across the halves, (X, Y) -> (X + Y, (X - Y) conj(w0))
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      uint32_t lo[2][FC];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double2 Y[1][FC];
+        {
+          uint32_t y[32];
+          tm_ld32(lane_addr + (uint32_t)((c * 2 + h) * 32), y);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          tm_zero32(lane_addr + (uint32_t)((c * 2 + h) * 32));   // next product
+#pragma unroll
+          for (int j = 0; j < FC; ++j) Y[0][j] = tm_get(y, j);
+        }
+        inv_fft_hk<1, GT, true>(Y, fscr, lay, t, sm.twi[hf], bar, 1 + hf);
+#pragma unroll
+        for (int j = 0; j < FC; ++j) {   // the partner half's value at the same position (lane ^ 2)
+          double2 o;
+          o.x = __shfl_xor_sync(0xffffffffu, Y[0][j].x, 2);
+          o.y = __shfl_xor_sync(0xffffffffu, Y[0][j].y, 2);
+          Y[0][j] = hf == 0 ? make_double2(Y[0][j].x + o.x, Y[0][j].y + o.y)
+                            : cmul(make_double2(o.x - Y[0][j].x, o.y - Y[0][j].y), wi0);
+        }
+        if (h == 0) {
+#pragma unroll
+          for (int j = 0; j < FC; ++j) {
+            lo[0][j] = round_u32(Y[0][j].x);
+            lo[1][j] = round_u32(Y[0][j].y);
+          }
+        } else if (e != 0) {
+#pragma unroll
+          for (int j = 0; j < FC; ++j) {
+            const int f = hf * FH + t + FT * j;   // folded point: coefficients f and f + 1024
+            acc[t2_pad(c, f)] += lo[0][j] + (round_u32(Y[0][j].x) << 16);
+            acc[t2_pad(c, f + 2 * FH)] += lo[1][j] + (round_u32(Y[0][j].y) << 16);
+          }
+        }
+      }
+    }
+    gsync<GT>(bar);   // the pair's accumulator updates before the next step's digits
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sm.tmem_slot), "r"(512u));
+  }
+  if (!valid) return;
+  if (s1 < L) {
+    for (int k = tq; k < 2 * N; k += 2 * FT) acc_io[bq * 2 * N + k] = acc[t2_pad(k >= N, k & (N - 1))];
+  } else {
+    uint32_t *o = lwe_out + bq * (int64_t)(N + 1);
+    for (int k = tq; k < N; k += 2 * FT) o[k] = k == 0 ? acc[0] : 0u - acc[t2_pad(0, N - k)];
+    if (tq == 0) o[N] = acc[t2_pad(1, 0)];
+  }
+}
+
 // One vertical-packing tree level on the FFT2 path (level_fft_kernel at N = 2048).
 template <int MODE>
 __global__ void __launch_bounds__(2 * FT, 1)
@@ -4393,7 +4641,15 @@ int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, co
   }
   for (int s0 = 0; s0 < L; s0 += g_fft_segment) {
     const int s1 = s0 + g_fft_segment < L ? s0 + g_fft_segment : L;
-    if (p->N == 4 * FH) {
+    if (p->N == 4 * FH && g_fft_mode >= 1 && B >= (int64_t)T2C * st->sms) {
+      // TMEM ladder: 4 ciphertexts per SM (one 16-warp CTA) sharing each key slice
+      const size_t smem = sizeof(FSmem2TD);
+      if ((rc = set_smem(blind_rotate_fft2_td_kernel, smem))) return rc;
+      blind_rotate_fft2_td_kernel<<<(unsigned)((B + T2C - 1) / T2C), 16 * 32, smem, s>>>(
+          (const double2 *)bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st->fft2_fwd[0], st->fft2_fwd[1],
+          st->fft2_inv[0], st->fft2_inv[1], acc, s0, s1, B);
+      rc = post_launch("blind_rotate_fft2_td_kernel");
+    } else if (p->N == 4 * FH) {
       const size_t smem = sizeof(FSmem2);
       if ((rc = set_smem(blind_rotate_fft2_kernel<true>, smem))) return rc;
       blind_rotate_fft2_kernel<true><<<(unsigned)B, 2 * FT, smem, s>>>(

@@ -91,9 +91,17 @@ def test_cfg1_full_batch(coracle, keys):
 
 
 def test_cfg4_fft2_ladder(coracle, keys):
-    """cfg4 (N = 2048, n = 750): the N = 2048 FFT ladder at B = 320."""
+    """cfg4 (N = 2048, n = 750): the register N = 2048 FFT ladder at B = 320."""
     P, K, bsk, ksk = keys("CFG4")
     _run_and_check(coracle, P, K, bsk, ksk, 320, 5, 64)
+
+
+def test_cfg4_fft2_tmem_ladder(coracle, keys):
+    """cfg4 (N = 2048, n = 750), B = 4 x #SMs + 3: the N = 2048 TMEM ladder
+    (blind_rotate_fft2_td_kernel, >= 4 ciphertexts per SM), ragged last CTA."""
+    P, K, bsk, ksk = keys("CFG4")
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    _run_and_check(coracle, P, K, bsk, ksk, 4 * sms + 3, 6, 64)
 
 
 def test_cfg2_encrypted_full_batch_decrypts_and_matches(coracle, keys):
@@ -112,6 +120,7 @@ def test_cfg2_encrypted_full_batch_decrypts_and_matches(coracle, keys):
 
 
 @pytest.mark.parametrize("name,B", [("CFG2", 1189), ("CFG2", 600), ("CFG2", 5), ("CFG1", 1189), ("CFG4", 300),
+                                    ("CFG4", 595),
                                     ("INSECURE_1024", 64), ("INSECURE_2048", 64), ("INSECURE_1024W", 64),
                                     ("INSECURE_2048W", 64)])
 def test_fft_rounding_margin(name, B, coracle):
