@@ -685,8 +685,8 @@ def bench_hwb(args):
                      "unit": "TB/s", "frac": round(sm_ach / sm_peak, 4),
                      "bytes_per_step": smem_step,
                      "peak_source": f"128 B/clk/SM x {sms} SMs x {mhz:.0f} MHz (median SM clock under load)",
-                     "ncu": "profiles/r01_ncu_fft_ladder_v2.txt: LSU wavefronts + TMA writes = 0.89 of the "
-                            "crossbar under ncu"}
+                     "ncu": "profiles/r02b_ncu_td.txt: l1tex throughput (LSU wavefronts + TMA writes) "
+                            "0.72 of peak; the register ladder reached 0.89 (profiles/r01_ncu_fft_ladder_v2.txt)"}
     result = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 3),
@@ -708,10 +708,11 @@ def bench_hwb(args):
                                                + 4 * (B * (P.lwe_n + 1) + B * (N + 1) + 2 * N),
                                             FFT_KERNELS[args.fft_mode] if use_fft else "ntt"),
                      "work_per_pbs": work_txt, "peak_source": peak_src,
-                     "traffic_note": ("ncu --set full flushes L2 before each replayed launch, so the "
-                                      "64-step segment's accumulators (B x 8 KB) and key slices are read "
-                                      "from DRAM (471 MB per batch); without the flush a batch reads "
-                                      "~178 MB (profiles/r02_dram_no_flush.txt) against 148 MB algorithmic") if use_fft else None,
+                     "traffic_note": ("DRAM bytes per batch measured without ncu's cache flush "
+                                      "(--cache-control none, profiles/r02b_dram_no_flush_td.txt): the key "
+                                      "streams once per batch; ncu --set full's per-launch flush would force "
+                                      "the segment accumulators (B x 8 KB) through DRAM as well (~470 MB)")
+                     if use_fft else None,
                      "context": {}}}
     ctx = {"pbs": {"roofline_pbs_per_s": round(pbs_roof, 1),
                              "frac": round(B / (max_ms / args.steps * 1e-3) / pbs_roof, 4),

@@ -4467,6 +4467,10 @@ int64_t hwb_set_fft_cluster_batch(int64_t max_batch) {
 // (default: cfg2 B = 4096 in 54.5 ms vs 61.6 / 60.1 / 59.6 / 63.2 ms for modes 1-4,
 // DESIGN.md §3b).  All bit-identical.
 static thread_local int g_fft_mode = 5;
+// smallest batch (ciphertexts per SM) for the mode-5 TMEM ladder: from 4 per SM (one
+// CTA) it beats the register ladder (cfg2 B = 592: 9.27 vs 9.97 ms; 1036: 16.2 vs 19.4;
+// 444: 9.29 vs 8.84)
+constexpr int64_t g_fft_tmem_min = 4;
 
 int hwb_set_fft_mode(int mode) {
   if (mode < 0 || mode > 5)
@@ -4656,7 +4660,7 @@ int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, co
           (const double2 *)bsk_fft, nullptr, nullptr, lwe_in, tv, tv_per_item, ext, L, g, st->fft2_fwd[0],
           st->fft2_fwd[1], st->fft2_inv[0], st->fft2_inv[1], acc, s0, s1, B);
       rc = post_launch("blind_rotate_fft2_kernel");
-    } else if (g_fft_mode == 5 && B >= (int64_t)2 * TPC * st->sms) {
+    } else if (g_fft_mode == 5 && B >= g_fft_tmem_min * (int64_t)st->sms) {
       const size_t smem = sizeof(FSmemTP);
       if ((rc = set_smem(blind_rotate_fft_td_kernel, smem))) return rc;
       blind_rotate_fft_td_kernel<<<(unsigned)((B + TPC - 1) / TPC), TPC * FT, smem, s>>>(

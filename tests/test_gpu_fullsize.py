@@ -78,11 +78,18 @@ def test_cfg2_ragged_tmem_ladder(coracle, keys):
 
 
 def test_cfg2_register_ladder_range(coracle, keys):
-    """cfg2 batches between one ciphertext per SM and the TMEM threshold run the
-    register FFT ladder (4 CTAs per SM)."""
+    """cfg2 batches between one ciphertext per SM and the TMEM threshold (4 per SM)
+    run the register FFT ladder (4 CTAs per SM)."""
     P, K, bsk, ksk = keys("CFG2")
     sms = torch.cuda.get_device_properties(0).multi_processor_count
-    _run_and_check(coracle, P, K, bsk, ksk, 4 * sms + 3, 3, 96)
+    _run_and_check(coracle, P, K, bsk, ksk, 3 * sms + 3, 3, 96)
+
+
+def test_cfg2_tmem_ladder_one_cta_per_sm(coracle, keys):
+    """cfg2, B = 4 x #SMs + 3: the TMEM ladder from its threshold (one CTA per SM)."""
+    P, K, bsk, ksk = keys("CFG2")
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    _run_and_check(coracle, P, K, bsk, ksk, 4 * sms + 3, 7, 96)
 
 
 def test_cfg1_full_batch(coracle, keys):
@@ -119,7 +126,8 @@ def test_cfg2_encrypted_full_batch_decrypts_and_matches(coracle, keys):
     assert_u32_equal(out[idx], coracle.pbs(lwe[idx], tv, K.bsk, K.ksk, P))
 
 
-@pytest.mark.parametrize("name,B", [("CFG2", 1189), ("CFG2", 600), ("CFG2", 5), ("CFG1", 1189), ("CFG4", 300),
+@pytest.mark.parametrize("name,B", [("CFG2", 1189), ("CFG2", 600), ("CFG2", 447), ("CFG2", 5), ("CFG1", 1189),
+                                    ("CFG4", 300),
                                     ("CFG4", 595),
                                     ("INSECURE_1024", 64), ("INSECURE_2048", 64), ("INSECURE_1024W", 64),
                                     ("INSECURE_2048W", 64)])
