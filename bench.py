@@ -32,7 +32,8 @@ import numpy as np  # noqa: E402
 
 # FFT ladder mode (hwb_set_fft_mode) -> the kernel that runs a cfg2 batch of 4096
 FFT_KERNELS = {0: "blind_rotate_fft_kernel", 1: "blind_rotate_fft_tm_kernel", 2: "blind_rotate_fft_tx_kernel",
-               3: "blind_rotate_fft_tp_kernel", 4: "blind_rotate_fft_tq_kernel", 5: "blind_rotate_fft_td_kernel"}
+               3: "blind_rotate_fft_tp_kernel", 4: "blind_rotate_fft_tq_kernel", 5: "blind_rotate_fft_td_kernel",
+               6: "blind_rotate_fft_td_kernel<4,2>"}
 METRIC = "bootstrappings/sec"
 UNIT = "PBS/s"
 KEY_SEED, ENC_SEED = 1, 2
@@ -49,10 +50,10 @@ def parse():
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--ladder", default="auto", choices=["auto", "fft", "ntt"],
                     help="blind rotation: FP64 FFT ladder or two-prime NTT ladder (bit-identical)")
-    ap.add_argument("--fft-mode", type=int, default=5, choices=list(range(6)),
+    ap.add_argument("--fft-mode", type=int, default=5, choices=list(range(7)),
                     help="FFT ladder (bit-identical): 0 register accumulators; TMEM accumulators with "
                          "1 two ciphertexts per thread, 2 one per thread, 3 lane-paired, 4 one 16-warp CTA, "
-                         "5 lane-paired decoupled halves (default)")
+                         "5 lane-paired decoupled halves (default), 6 = 5 as one 16-warp CTA with a 2-slot key ring")
     ap.add_argument("--ks-engine", default="auto", choices=["auto", "tc", "simt"],
                     help="LWE key switch: tensor cores (tcgen05 int8) or the integer-pipe kernel")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -1953,7 +1953,21 @@ __global__ void __launch_bounds__(TPC * FT, 2)
 // transforms).  The inverse runs one accumulator at a time in the ciphertext's own
 // 8 KB scratch, so the halves share nothing else.
 
-__global__ void __launch_bounds__(TPC * FT, 2)
+template <int NG, int KS>
+struct FSmemTDT {
+  uint32_t acc[2 * NG][TP_ACC];     // working ciphertexts; odd ones 16 words further (TP_ACC)
+  double2 scr[2 * NG][FH];          // transpose scratch per ciphertext (odd: addresses XOR 4)
+  double2 key[KS][2 * 2 * FC * FT];   // key-slice ring (TMA)
+  double2 twf[kTwc * FT], twi[kTwc * FT];
+  uint64_t key_full[KS];
+  uint32_t key_cnt[KS];             // groups done with the slot's slice
+  uint32_t tmem_slot;
+};
+
+// NG groups of 4 warps (2 lane-paired ciphertexts each), KS key slots: <2, 1> = mode 5
+// (2 CTAs per SM), <4, 2> = mode 6 (one 16-warp CTA per SM, the slice shared by 8).
+template <int NG, int KS>
+__global__ void __launch_bounds__(NG * 128, NG == 2 ? 2 : 1)
     blind_rotate_fft_td_kernel(const double2 *__restrict__ ggsw, const uint32_t *__restrict__ lwe_in,
                                const uint32_t *__restrict__ tv, int tv_per_item, uint32_t *lwe_out, int L, Gadget g,
                                const double2 *__restrict__ twf, const double2 *__restrict__ twi, uint32_t *acc_io,
@@ -1962,7 +1976,7 @@ __global__ void __launch_bounds__(TPC * FT, 2)
   constexpr int LOG2M = 11;
   constexpr int GT = 128;   // threads per half (named barriers)
   extern __shared__ uint4 smem_raw[];
-  FSmemTP &sm = *reinterpret_cast<FSmemTP *>(smem_raw);
+  FSmemTDT<NG, KS> &sm = *reinterpret_cast<FSmemTDT<NG, KS> *>(smem_raw);
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
 #ifndef HWB_TD_SPLIT
 #define HWB_TD_SPLIT 1
@@ -1970,14 +1984,20 @@ __global__ void __launch_bounds__(TPC * FT, 2)
   // HWB_TD_SPLIT: half = warp >> 2, so every scheduler (warp % 4) runs one warp of each
   // half (independent instruction streams); 0: half = warp & 1 (a scheduler's warps in
   // lockstep)
-  const int hsel = HWB_TD_SPLIT ? (warp >> 2) : (warp & 1), hpos = HWB_TD_SPLIT ? (warp & 3) : (warp >> 1);
+  const int hsel = HWB_TD_SPLIT || NG != 2 ? (warp >> 2) : (warp & 1),
+            hpos = HWB_TD_SPLIT || NG != 2 ? (warp & 3) : (warp >> 1);
   const int q = 2 * hsel + (lane & 1), t = 16 * hpos + (lane >> 1);
-  const FLay lay = make_flay(t);
-  const int64_t bb = (int64_t)blockIdx.x * TPC + q;
+  FLay lay = make_flay(t);
+  if (q & 1) {   // pair partner: the other half of the 8 bank groups
+    lay.a ^= 4u;
+    lay.m ^= 4u;
+    lay.b ^= 4u;
+  }
+  const int64_t bb = (int64_t)blockIdx.x * (2 * NG) + q;
   const bool valid = bb < B;
   const int64_t bq = valid ? bb : B - 1;
   const uint32_t *row = lwe_in + bq * (int64_t)(L + 1);
-  uint32_t *acc = sm.acc[q];
+  uint32_t *acc = sm.acc[q];   // TP_ACC stride: odd ciphertexts 16 banks over
   if (s0 == 0) {
     const int bt = mod_switch(row[L], LOG2M);
     const uint32_t *tp = tv + (tv_per_item ? bq * 2 * N : 0);
@@ -1989,22 +2009,34 @@ __global__ void __launch_bounds__(TPC * FT, 2)
   } else {
     for (int k = t; k < 2 * N; k += FT) acc[k] = acc_io[bq * 2 * N + k];
   }
-  for (int k = tid; k < kTwc * FT; k += TPC * FT) {
+  for (int k = tid; k < kTwc * FT; k += NG * 128) {
     sm.twf[k] = twf[twc_full<true>(k / FT) * FT + k % FT];
     sm.twi[k] = twi[twc_full<false>(k / FT) * FT + k % FT];
   }
   constexpr uint32_t kSliceBytes = 2 * 2 * FC * FT * sizeof(double2);
   const size_t ggsw_f = (size_t)2 * g.levels * 2 * 2 * FC * FT;
+  const int lv = (int)g.levels;
+  const int rows = (s1 - s0) * 2 * lv;   // key-slice rows of this launch, u = (s - s0) 2l + r
+  auto slice = [&](int u) {
+    return ggsw + (size_t)(s0 + u / (2 * lv)) * ggsw_f + (size_t)(u % (2 * lv)) * (2 * 2 * FC * FT);
+  };
   if (tid == 0) {
-    mbar_init(&sm.key_full, 1);
-    sm.key_cnt = 0;
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+      mbar_init(&sm.key_full[k], 1);
+      sm.key_cnt[k] = 0;
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(&sm.key_full, kSliceBytes);   // the first row's slice
-    bulk_g2s(sm.key, ggsw + (size_t)s0 * ggsw_f, kSliceBytes, &sm.key_full);
+#pragma unroll
+    for (int k = 0; k < KS; ++k)   // the first KS rows' slices
+      if (k < rows) {
+        mbar_expect_tx(&sm.key_full[k], kSliceBytes);
+        bulk_g2s(sm.key[k], slice(k), kSliceBytes, &sm.key_full[k]);
+      }
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_slot)),
-                 "r"(TM_COLS));
+                 "r"((uint32_t)(NG * 128)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -2014,27 +2046,25 @@ __global__ void __launch_bounds__(TPC * FT, 2)
 #pragma unroll
   for (int k = 0; k < 4; ++k) tm_zero32(lane_addr + (uint32_t)(k * 32));
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-  uint32_t key_phase = 0;
-  const int lv = (int)g.levels;
   const int half = hsel, hbar = 1 + half;
   const bool leader = lane == 0 && hpos == 0;
   // a half is done with the key buffer (slice or, for half 1, inverse scratch):
   // the second half to finish issues the next row's slice
-  auto release = [&](int s_, int r_) {
+  auto release = [&](int u) {   // the last group done with slot u % KS fetches row u + KS
     if (!leader) return;
     __threadfence_block();
-    if (atomicAdd(&sm.key_cnt, 1u) == 1u) {
-      sm.key_cnt = 0;
-      const int nr = r_ + 1 < 2 * lv ? r_ + 1 : 0, ns = r_ + 1 < 2 * lv ? s_ : s_ + 1;
-      if (ns < s1) {
+    if (atomicAdd(&sm.key_cnt[u % KS], 1u) == (uint32_t)(NG - 1)) {
+      sm.key_cnt[u % KS] = 0;
+      if (u + KS < rows) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&sm.key_full, kSliceBytes);
-        bulk_g2s(sm.key, ggsw + (size_t)ns * ggsw_f + (size_t)nr * (2 * 2 * FC * FT), kSliceBytes, &sm.key_full);
+        mbar_expect_tx(&sm.key_full[u % KS], kSliceBytes);
+        bulk_g2s(sm.key[u % KS], slice(u + KS), kSliceBytes, &sm.key_full[u % KS]);
       }
     }
   };
+
   const double dig_off = 4503599627370496.0 + (double)g.half;
-  double2 *fscr = sm.scr + q * (FH + 4);                                                      // 8 KB
+  double2 *fscr = sm.scr[q];   // 8 KB
   uint32_t a_nx = row[s0];   // the next step's mask word, loaded a step ahead (s + 1 <= L)
 #pragma unroll 1
   for (int s = s0; s < s1; ++s) {
@@ -2064,8 +2094,9 @@ __global__ void __launch_bounds__(TPC * FT, 2)
       // (no trailing barrier on the second transpose: the release barrier after the MAC
       // precedes the next write into fscr)
       fwd_fft_hk<1, GT, true, false>(x, fscr, lay, t, sm.twf, hbar);
-      mbar_wait(&sm.key_full, key_phase);
-      key_phase ^= 1u;
+      const int u = (s - s0) * 2 * lv + r;   // this row's slot u % KS, use u / KS
+      mbar_wait(&sm.key_full[u % KS], (uint32_t)(u / KS) & 1u);
+      const double2 *key = sm.key[u % KS];
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
         const uint32_t a = lane_addr + (uint32_t)(ch * 32);
@@ -2077,7 +2108,7 @@ __global__ void __launch_bounds__(TPC * FT, 2)
 #if HWB_X_NOKEY
           const double2 k = make_double2(1.0 + j + ch, 0.5 * r);
 #else
-          const double2 k = sm.key[(ch * FC + j) * FT + t];
+          const double2 k = key[(ch * FC + j) * FT + t];
 #endif
           double2 u = tm_get(y, j);
           u.x = fma(x[0][j].x, k.x, fma(-x[0][j].y, k.y, u.x));
@@ -2086,7 +2117,7 @@ __global__ void __launch_bounds__(TPC * FT, 2)
         }
       }
       gsync<GT>(hbar);   // the half is past the slice
-      release(s, r);
+      release(u);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
     // inverse transforms, one accumulator at a time (lo then hi of each component), in
@@ -2133,7 +2164,8 @@ __global__ void __launch_bounds__(TPC * FT, 2)
   __syncthreads();
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sm.tmem_slot), "r"(TM_COLS));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sm.tmem_slot),
+                 "r"((uint32_t)(NG * 128)));
   }
   if (!valid) return;
   if (s1 < L) {
@@ -4464,8 +4496,9 @@ int64_t hwb_set_fft_cluster_batch(int64_t max_batch) {
 // ladder): 0 = registers (g_fft_cpb ciphertexts per CTA), 1 = TMEM accumulators, two
 // ciphertexts per thread; 2 = TMEM, one per thread (16 warps/SM); 3 = 2 with lane-paired
 // ciphertexts; 4 = 3 as one 16-warp CTA of decoupled groups; 5 = 3 with decoupled halves
-// (default: cfg2 B = 4096 in 54.5 ms vs 61.6 / 60.1 / 59.6 / 63.2 ms for modes 1-4,
-// DESIGN.md §3b).  All bit-identical.
+// (default: cfg2 B = 4096 in 54.2 ms vs 61.0 / 60.1 / 59.6 / 63.2 ms for modes 1-4);
+// 6 = 5 as one 16-warp CTA with a two-slot key ring (62.1 ms; 62.5 vs 61.8 ms at full
+// waves, B = 4736), DESIGN.md §3b.  All bit-identical.
 static thread_local int g_fft_mode = 5;
 // smallest batch (ciphertexts per SM) for the mode-5 TMEM ladder: from 4 per SM (one
 // CTA) it beats the register ladder (cfg2 B = 592: 9.27 vs 9.97 ms; 1036: 16.2 vs 19.4;
@@ -4473,9 +4506,10 @@ static thread_local int g_fft_mode = 5;
 constexpr int64_t g_fft_tmem_min = 4;
 
 int hwb_set_fft_mode(int mode) {
-  if (mode < 0 || mode > 5)
+  if (mode < 0 || mode > 6)
     return fail(HWB_EINVAL, "FFT ladder mode must be 0 (registers), 1 (TMEM), 2 (TMEM, one ciphertext per thread) "
-                            "3 (TMEM, lane-paired), 4 (TMEM, decoupled groups) or 5 (TMEM, lane-paired, decoupled halves)");
+                            "3 (TMEM, lane-paired), 4 (TMEM, decoupled groups), 5 (TMEM, lane-paired, decoupled halves) or 6 (5 as one "
+                            "16-warp CTA with a two-slot key ring)");
   g_fft_mode = mode;
   return HWB_OK;
 }
@@ -4660,10 +4694,16 @@ int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, co
           (const double2 *)bsk_fft, nullptr, nullptr, lwe_in, tv, tv_per_item, ext, L, g, st->fft2_fwd[0],
           st->fft2_fwd[1], st->fft2_inv[0], st->fft2_inv[1], acc, s0, s1, B);
       rc = post_launch("blind_rotate_fft2_kernel");
-    } else if (g_fft_mode == 5 && B >= g_fft_tmem_min * (int64_t)st->sms) {
-      const size_t smem = sizeof(FSmemTP);
-      if ((rc = set_smem(blind_rotate_fft_td_kernel, smem))) return rc;
-      blind_rotate_fft_td_kernel<<<(unsigned)((B + TPC - 1) / TPC), TPC * FT, smem, s>>>(
+    } else if (g_fft_mode == 6 && B >= 8 * (int64_t)st->sms) {
+      const size_t smem = sizeof(FSmemTDT<4, 2>);
+      if ((rc = set_smem(blind_rotate_fft_td_kernel<4, 2>, smem))) return rc;
+      blind_rotate_fft_td_kernel<4, 2><<<(unsigned)((B + 7) / 8), 512, smem, s>>>(
+          (const double2 *)bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st->fft_fwd, st->fft_inv, acc, s0, s1, B);
+      rc = post_launch("blind_rotate_fft_td_kernel<4,2>");
+    } else if (g_fft_mode >= 5 && B >= g_fft_tmem_min * (int64_t)st->sms) {
+      const size_t smem = sizeof(FSmemTDT<2, 1>);
+      if ((rc = set_smem(blind_rotate_fft_td_kernel<2, 1>, smem))) return rc;
+      blind_rotate_fft_td_kernel<2, 1><<<(unsigned)((B + 3) / 4), 256, smem, s>>>(
           (const double2 *)bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st->fft_fwd, st->fft_inv, acc, s0, s1, B);
       rc = post_launch("blind_rotate_fft_td_kernel");
     } else if (g_fft_mode == 4 && B >= (int64_t)TQC * st->sms) {
