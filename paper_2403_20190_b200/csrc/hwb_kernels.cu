@@ -1193,6 +1193,7 @@ struct FSmemTM {
   double2 scr[2][2 * FH];         // forward scratch of group g (2 transforms); all 32 KB: group 1's inverse scratch
   double2 key[2 * 2 * FC * FT];   // the digit's key slice (TMA); group 0's inverse scratch
   uint64_t key_full;
+  uint64_t in_full;               // level kernels: the inputs' bulk copies landed
   uint32_t tmem_slot;
 };
 
@@ -2398,23 +2399,40 @@ __global__ void __launch_bounds__(2 * FT, 2)
   const int64_t sub0 = (cta % per_item) * TMC + grp * 2;   // this thread's subs sub0, sub0 + 1
   const size_t ggsw_f = (size_t)2 * g.levels * 2 * 2 * FC * FT;
   const double2 *G = ggsw + (size_t)gidx[item] * ggsw_f;
+  // inputs: IVP -- the CTA's 4 consecutive sub-ciphertexts are one contiguous 32 KB
+  // run, fetched by one bulk copy; VP -- c1 - c0 with every 16-byte load in flight at once
+  // (the element-wise copy loop it replaces exposed one global latency per word: 26% of
+  // the kernel's stall samples, profiles/r02b_ncu_lvl.txt)
+  if (MODE != MODE_IVP_LEVEL) {
 #pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    uint32_t *a = sm.acc[grp * 2 + q];
-    const int64_t sub = sub0 + q;
-    if (MODE == MODE_IVP_LEVEL) {
-      const uint32_t *d = in + (item * m + sub) * 2 * N;
-      for (int k = t; k < 2 * N; k += FT) a[k] = d[k];
-    } else {
-      const uint32_t *c0 = in + (item * 2 * m + sub) * 2 * N, *c1 = in + (item * 2 * m + m + sub) * 2 * N;
-      for (int k = t; k < 2 * N; k += FT) a[k] = c1[k] - c0[k];
+    for (int q = 0; q < 2; ++q) {
+      uint4 *a = reinterpret_cast<uint4 *>(sm.acc[grp * 2 + q]);
+      const int64_t sub = sub0 + q;
+      const uint4 *c0 = reinterpret_cast<const uint4 *>(in + (item * 2 * m + sub) * 2 * N);
+      const uint4 *c1 = reinterpret_cast<const uint4 *>(in + (item * 2 * m + m + sub) * 2 * N);
+      uint4 v0[2 * N / 4 / FT], v1[2 * N / 4 / FT];
+#pragma unroll
+      for (int k = 0; k < 2 * N / 4 / FT; ++k) {
+        v0[k] = c0[t + FT * k];
+        v1[k] = c1[t + FT * k];
+      }
+#pragma unroll
+      for (int k = 0; k < 2 * N / 4 / FT; ++k)
+        a[t + FT * k] = make_uint4(v1[k].x - v0[k].x, v1[k].y - v0[k].y, v1[k].z - v0[k].z, v1[k].w - v0[k].w);
     }
   }
   if (tid == 0) {
     mbar_init(&sm.key_full, 1);
+    mbar_init(&sm.in_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (MODE == MODE_IVP_LEVEL) {
+      const uint32_t *d = in + (item * m + (cta % per_item) * TMC) * 2 * N;
+      mbar_expect_tx(&sm.in_full, (uint32_t)sizeof(sm.acc));
+      bulk_g2s(&sm.acc[0][0], d, (uint32_t)sizeof(sm.acc), &sm.in_full);
+    }
   }
   const uint32_t lane_addr = tm_alloc_cta(sm);   // (its barrier also publishes the inputs)
+  if (MODE == MODE_IVP_LEVEL) mbar_wait(&sm.in_full, 0);
   uint32_t key_phase = 0;
   tm_ext_product(
       sm, G, g, grp, t, lay, twf, twi, lane_addr, key_phase,
@@ -2432,6 +2450,36 @@ __global__ void __launch_bounds__(2 * FT, 2)
         }
       });
   tm_free_cta(sm);
+}
+
+// Global -> shared copies of a ciphertext with every 16-byte load in flight at once
+// (element-wise copy loops exposed one global latency per word in the level kernels).
+template <int WORDS, int NT>
+__device__ __forceinline__ void ld_vec(uint32_t *dst, const uint32_t *src, int tid) {
+  constexpr int V = WORDS / 4 / NT;
+  static_assert(V * 4 * NT == WORDS, "ld_vec shape");
+  const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+  uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+  uint4 r[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) r[k] = s4[tid + NT * k];
+#pragma unroll
+  for (int k = 0; k < V; ++k) d4[tid + NT * k] = r[k];
+}
+template <int WORDS, int NT>   // dst = c1 - c0
+__device__ __forceinline__ void ld_vec_diff(uint32_t *dst, const uint32_t *c1, const uint32_t *c0, int tid) {
+  constexpr int V = WORDS / 4 / NT;
+  static_assert(V * 4 * NT == WORDS, "ld_vec shape");
+  const uint4 *a4 = reinterpret_cast<const uint4 *>(c1), *b4 = reinterpret_cast<const uint4 *>(c0);
+  uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+  uint4 x[V], y[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    x[k] = a4[tid + NT * k];
+    y[k] = b4[tid + NT * k];
+  }
+#pragma unroll
+  for (int k = 0; k < V; ++k) d4[tid + NT * k] = make_uint4(x[k].x - y[k].x, x[k].y - y[k].y, x[k].z - y[k].z, x[k].w - y[k].w);
 }
 
 // One tree level of vertical packing on the FFT path (cmux_kernel's MODE_IVP_LEVEL /
@@ -2454,7 +2502,7 @@ __global__ void __launch_bounds__(FT, 1)
     // CDEMUX (hw/lut.py:113-119, 294-313): hi = C (*) d, lo = d - hi
     const uint32_t *d = in + (item * m + sub) * 2 * N;
     uint32_t *o_lo = out + (item * 2 * m + sub) * 2 * N, *o_hi = out + (item * 2 * m + m + sub) * 2 * N;
-    for (int k = t; k < 2 * N; k += FT) sm.acc[0][k] = d[k];
+    ld_vec<2 * N, FT>(sm.acc[0], d, t);
     fft_smem_init(sm, t);
     __syncthreads();
     fft_ext_product(
@@ -2467,7 +2515,7 @@ __global__ void __launch_bounds__(FT, 1)
     // CMUX (hw/lut.py:130-136, 233-247): next = c0 + C (*) (c1 - c0)
     const uint32_t *c0 = in + (item * 2 * m + sub) * 2 * N, *c1 = in + (item * 2 * m + m + sub) * 2 * N;
     uint32_t *o = out + (item * m + sub) * 2 * N;
-    for (int k = t; k < 2 * N; k += FT) sm.acc[0][k] = c1[k] - c0[k];
+    ld_vec_diff<2 * N, FT>(sm.acc[0], c1, c0, t);
     fft_smem_init(sm, t);
     __syncthreads();
     fft_ext_product(
@@ -3577,7 +3625,7 @@ __global__ void __launch_bounds__(2 * FT, 1)
     // CDEMUX (hw/lut.py:113-119, 294-313): hi = C (*) d, lo = d - hi
     const uint32_t *d = in + (item * m + sub) * 2 * N;
     uint32_t *o_lo = out + (item * 2 * m + sub) * 2 * N, *o_hi = out + (item * 2 * m + m + sub) * 2 * N;
-    for (int k = tid; k < 2 * N; k += NT) sm.acc[k] = d[k];
+    ld_vec<2 * N, NT>(sm.acc, d, tid);
     __syncthreads();
     fft2_ext_product(
         sm, G, g, grp, t, lay, twf, twi, key_phase, [&](int c, int i) { return decomp_prep(sm.acc[c * N + i], g); },
@@ -3589,7 +3637,7 @@ __global__ void __launch_bounds__(2 * FT, 1)
     // CMUX (hw/lut.py:130-136, 233-247): next = c0 + C (*) (c1 - c0)
     const uint32_t *c0 = in + (item * 2 * m + sub) * 2 * N, *c1 = in + (item * 2 * m + m + sub) * 2 * N;
     uint32_t *o = out + (item * m + sub) * 2 * N;
-    for (int k = tid; k < 2 * N; k += NT) sm.acc[k] = c1[k] - c0[k];
+    ld_vec_diff<2 * N, NT>(sm.acc, c1, c0, tid);
     __syncthreads();
     fft2_ext_product(
         sm, G, g, grp, t, lay, twf, twi, key_phase, [&](int c, int i) { return decomp_prep(sm.acc[c * N + i], g); },
