@@ -210,7 +210,7 @@ def ncu_traffic(B, alg_bytes=None, ladder="ntt"):
         return None
     if rec.get("batch") != B:
         return None
-    return {"bytes": int(rec["dram_bytes_read"] + rec["dram_bytes_write"]), "unit": "B/launch",
+    return {"bytes": int(rec["dram_bytes_read"] + rec["dram_bytes_write"]), "unit": "B per PBS batch",
             "algorithmic_bytes": alg_bytes, "source": rec.get("source")}
 
 
