@@ -300,10 +300,14 @@ int hwb_set_fft_group(int ciphertexts_per_cta);
  * the whole ladder in one launch.  Bit-identical to the throughput ladder.
  * Returns the previous setting (the reference has no counterpart). */
 int64_t hwb_set_fft_latency_batch(int64_t max_batch);
-/* FFT PBS ladder accumulators (N = 1024): 0 = registers (hwb_set_fft_group
- * ciphertexts per CTA), 1 = tensor memory (default, for batches of at least 8
- * ciphertexts per SM; two ciphertexts per thread share every key value read, four
- * per CTA share each staged key slice).  Bit-identical. */
+/* FFT PBS ladder shape (per calling thread): 0 = register accumulators
+ * (hwb_set_fft_group ciphertexts per CTA); tensor-memory accumulators with
+ * 1 = two ciphertexts per thread (8 warps/SM), 2 = one per thread (16 warps/SM),
+ * 3 = lane-paired ciphertexts (a lane pair reads each key value / twiddle at one
+ * address), 4 = 3 as one 16-warp CTA of decoupled groups, 5 = 3 with decoupled halves
+ * (default; from 4 ciphertexts per SM), 6 = 5 as one 16-warp CTA with a two-slot key
+ * ring.  At N = 2048 any mode >= 1 selects the N = 2048 TMEM ladder (from 4 per SM).
+ * All bit-identical; EINVAL outside 0..6 (the reference has no counterpart). */
 int hwb_set_fft_mode(int mode);
 /* Batches of at most max_batch ciphertexts (default -1: the cluster capacity) run the cluster latency
  * ladder at N = 1024: one ciphertext per cluster of 2l CTAs on 2l SMs (digit row r
