@@ -3490,6 +3490,7 @@ __global__ void __launch_bounds__(16 * 32, 1)
   for (int s = s0; s < s1; ++s) {
     const int e = mod_switch(a_nx, LOG2M);   // X^{a~_s}
     a_nx = row[s + 1];
+    uint32_t nxt[FC];   // packed digits of the component's next row (two-row gadgets)
 #pragma unroll 1
     for (int r = 0; r < 2 * lv; ++r) {
       // digit order (hw/tfhe.py:290-298): rows 0..l-1 = digits of b, l..2l-1 of a
@@ -3498,16 +3499,27 @@ __global__ void __launch_bounds__(16 * 32, 1)
       const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
       const uint32_t *ac = acc + t2_pad(comp, 0);
       double2 x[1][FC];
+      // two-row gadgets (cfg4): the second row's digits are extracted with the first's
+      // and kept packed (one word per position) -- the decomposition once per component
+      const bool reuse = lv == 2 && tt == 1;
 #pragma unroll
       for (int j = 0; j < FC; ++j) {
         const int k = t + FT * j;
         // this half's two quarter positions k + 512 (2 hf + {0, 1}); the partner half
         // (lane ^ 2) forms the other two
         uint32_t own = 0;
+        if (reuse) {
+          own = nxt[j];
+        } else {
+          uint32_t o1 = 0;
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int i = k + FH * (2 * hf + u);
-          own |= ((decomp_prep(rot_read_t2(ac, i, e) - ac[i + 8 * (i >> 10)], g) >> sh) & g.mask) << (16 * u);
+          for (int u = 0; u < 2; ++u) {
+            const int i = k + FH * (2 * hf + u);
+            const uint32_t pw = decomp_prep(rot_read_t2(ac, i, e) - ac[i + 8 * (i >> 10)], g);
+            own |= ((pw >> sh) & g.mask) << (16 * u);
+            o1 |= ((pw >> (sh - g.base_log)) & g.mask) << (16 * u);   // row tt + 1 (used iff lv == 2)
+          }
+          nxt[j] = o1;
         }
         const uint32_t par = __shfl_xor_sync(0xffffffffu, own, 2);
         const uint32_t q01 = hf ? par : own, q23 = hf ? own : par;
