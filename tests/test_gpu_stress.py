@@ -73,3 +73,31 @@ def test_tensor_core_keyswitch_under_contention():
     torch.cuda.synchronize()
     for o in outs:
         assert_u32_equal(tfhe.to_host(o), want)
+
+
+@pytest.mark.parametrize("name,per_sm", [("CFG2", 4), ("CFG4", 4)])
+def test_decoupled_tmem_ladders_under_contention(name, per_sm):
+    """The decoupled-group TMEM ladders (mode 5 at N = 1024, the N = 2048 TMEM ladder:
+    per-group key-slice release counters, mbarrier-tracked TMA slots, shuffle exchanges)
+    re-run under a second stream's load, ragged batches from one CTA per SM."""
+    P = dataclasses.replace(named_params(name), lwe_n=48)
+    K = tfhe.pbs_keygen(P, 7)
+    bsk, ksk = K.device_keys()
+    rng = np.random.default_rng(8)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    cases = {B: (tfhe.to_device(_rand(rng, (B, P.lwe_n + 1))), tfhe.to_device(_rand(rng, (B, 2, P.n))))
+             for B in (per_sm * sms + 3, 2 * per_sm * sms + 1)}
+    want = {B: tfhe.to_host(tfhe.pbs_batch(P, l, t, bsk, ksk, ladder="ntt", engine="simt"))
+            for B, (l, t) in cases.items()}
+    bg = torch.cuda.Stream()
+    big_l = tfhe.to_device(_rand(rng, (3 * per_sm * sms, P.lwe_n + 1)))
+    big_t = tfhe.to_device(_rand(rng, (2, P.n)))
+    outs = []
+    for it in range(12):
+        with torch.cuda.stream(bg):
+            tfhe.pbs_batch(P, big_l, big_t, bsk, None, ladder="fft")
+        for B, (l, t) in cases.items():
+            outs.append((B, tfhe.pbs_batch(P, l, t, bsk, ksk, ladder="fft")))
+    torch.cuda.synchronize()
+    for B, o in outs:
+        assert_u32_equal(tfhe.to_host(o), want[B])
