@@ -435,6 +435,11 @@ namespace hwb {
 template <int K, int FROM, int TO, int NT, bool TRAIL = true>
 __device__ __forceinline__ void frelayout_hk(double2 (*x)[FC], double2 *scr, const FLay &L, int bar) {
   const uint32_t bf = flay_base<FROM>(L), bt = flay_base<TO>(L);
+#if HWB_X_NOTRANS   // timing-only sensitivity build: barriers kept, no shared-memory round trip
+  gsync<NT>(bar);
+  if (TRAIL) gsync<NT>(bar);
+  return;
+#endif
 #pragma unroll
   for (int k = 0; k < K; ++k)
 #pragma unroll

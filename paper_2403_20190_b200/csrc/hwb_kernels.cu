@@ -2109,7 +2109,11 @@ __global__ void __launch_bounds__(NG * 128, NG == 2 ? 2 : 1)
 #if HWB_X_NOKEY
           const double2 k = make_double2(1.0 + j + ch, 0.5 * r);
 #else
+#if HWB_X_NOKEY
+          const double2 k = make_double2(1.0 + j + ch, 0.5 * r);
+#else
           const double2 k = key[(ch * FC + j) * FT + t];
+#endif
 #endif
           double2 u = tm_get(y, j);
           u.x = fma(x[0][j].x, k.x, fma(-x[0][j].y, k.y, u.x));
@@ -3540,7 +3544,11 @@ __global__ void __launch_bounds__(16 * 32, 1)
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
         for (int j = 0; j < FC; ++j) {
+#if HWB_X_NOKEY
+          const double2 k = make_double2(1.0 + j + ch, 0.5 * r);
+#else
           const double2 k = sm.key[(ch * 2 + hf) * (FC * FT + 4) + j * FT + t];
+#endif
           double2 u = tm_get(y, j);
           u.x = fma(x[0][j].x, k.x, fma(-x[0][j].y, k.y, u.x));
           u.y = fma(x[0][j].x, k.y, fma(x[0][j].y, k.x, u.y));
