@@ -1961,6 +1961,7 @@ struct FSmemTDT {
   double2 key[KS][2 * 2 * FC * FT];   // key-slice ring (TMA)
   double2 twf[kTwc * FT], twi[kTwc * FT];
   uint64_t key_full[KS];
+  uint64_t in_full;                 // level kernel: the inputs' bulk copies landed
   uint32_t key_cnt[KS];             // groups done with the slot's slice
   uint32_t tmem_slot;
 };
@@ -2484,6 +2485,171 @@ __device__ __forceinline__ void ld_vec_diff(uint32_t *dst, const uint32_t *c1, c
   }
 #pragma unroll
   for (int k = 0; k < V; ++k) d4[tid + NT * k] = make_uint4(x[k].x - y[k].x, x[k].y - y[k].y, x[k].z - y[k].z, x[k].w - y[k].w);
+}
+
+// One IVP / VP tree level on mode 5's layout (`level_fft_td_kernel`, FFT mode >= 5): the
+// CTA's 4 sub-ciphertexts 4k .. 4k + 3 of an item share its GGSW; two decoupled halves
+// of two lane-paired ciphertexts each (blind_rotate_fft_td_kernel's mapping), one
+// product per CTA.  The inputs (IVP: one bulk copy) and the first key slice are
+// fetched at once; per-thread twiddles from the global table.
+template <int MODE>
+__global__ void __launch_bounds__(256, 2)
+    level_fft_td_kernel(const double2 *__restrict__ ggsw, const int32_t *__restrict__ gidx,
+                        const uint32_t *__restrict__ in, uint32_t *out, int m, Gadget g,
+                        const double2 *__restrict__ twf, const double2 *__restrict__ twi) {
+  constexpr int N = 2 * FH;
+  constexpr int GT = 128;
+  extern __shared__ uint4 smem_raw[];
+  FSmemTDT<2, 1> &sm = *reinterpret_cast<FSmemTDT<2, 1> *>(smem_raw);
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int half = warp >> 2, hbar = 1 + half;
+  const int q = 2 * half + (lane & 1), t = 16 * (warp & 3) + (lane >> 1);
+  FLay lay = make_flay(t);
+  if (q & 1) {
+    lay.a ^= 4u;
+    lay.m ^= 4u;
+    lay.b ^= 4u;
+  }
+  const int64_t cta = blockIdx.x, per_item = m / 4, item = cta / per_item;
+  const int64_t sub0 = (cta % per_item) * 4, sub = sub0 + q;
+  const int lv = (int)g.levels;
+  const size_t ggsw_f = (size_t)2 * lv * 2 * 2 * FC * FT;
+  const double2 *G = ggsw + (size_t)gidx[item] * ggsw_f;
+  constexpr uint32_t kSliceBytes = 2 * 2 * FC * FT * sizeof(double2);
+  uint32_t *acc = sm.acc[q];   // TP_ACC stride
+  if (MODE != MODE_IVP_LEVEL) {
+    const uint32_t *c0 = in + (item * 2 * m + sub) * 2 * N, *c1 = in + (item * 2 * m + m + sub) * 2 * N;
+    ld_vec_diff<2 * N, FT>(acc, c1, c0, t);
+  }
+  if (tid == 0) {
+    mbar_init(&sm.key_full[0], 1);
+    mbar_init(&sm.in_full, 1);
+    sm.key_cnt[0] = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&sm.key_full[0], kSliceBytes);
+    bulk_g2s(sm.key[0], G, kSliceBytes, &sm.key_full[0]);
+    if (MODE == MODE_IVP_LEVEL) {   // 4 contiguous sub-ciphertexts into the padded slots
+      mbar_expect_tx(&sm.in_full, 4 * 2 * N * 4);
+#pragma unroll 1
+      for (int k = 0; k < 4; ++k)
+        bulk_g2s(sm.acc[k], in + (item * m + sub0 + k) * 2 * N, 2 * N * 4, &sm.in_full);
+    }
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_slot)),
+                 "r"(256u));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t lane_addr = sm.tmem_slot + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 128);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) tm_zero32(lane_addr + (uint32_t)(k * 32));
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  if (MODE == MODE_IVP_LEVEL) mbar_wait(&sm.in_full, 0);
+  const double dig_off = 4503599627370496.0 + (double)g.half;
+  double2 *fscr = sm.scr[q];
+  const bool leader = lane == 0 && (warp & 3) == 0;
+  uint32_t pw[2][FC];
+#pragma unroll 1
+  for (int r = 0; r < 2 * lv; ++r) {
+    // digit order (hw/tfhe.py:290-298): rows 0..l-1 = digits of b, l..2l-1 of a
+    const int comp = r < lv ? 1 : 0;
+    const int tt = r < lv ? r : r - lv;
+    const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
+    double2 x[1][FC];
+    if (tt == 0) {
+#pragma unroll
+      for (int j = 0; j < FC; ++j) {
+        const int i = t + FT * j;
+        pw[0][j] = decomp_prep(acc[comp * N + i], g);
+        pw[1][j] = decomp_prep(acc[comp * N + i + FH], g);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < FC; ++j)
+      x[0][j] = make_double2(u2d_minus((pw[0][j] >> sh) & g.mask, dig_off),
+                             u2d_minus((pw[1][j] >> sh) & g.mask, dig_off));
+    fwd_fft_hk<1, GT, false, false>(x, fscr, lay, t, twf, hbar);
+    mbar_wait(&sm.key_full[0], (uint32_t)r & 1u);
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch) {
+      const uint32_t a = lane_addr + (uint32_t)(ch * 32);
+      uint32_t y[32];
+      tm_ld32(a, y);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < FC; ++j) {
+        const double2 k = sm.key[0][(ch * FC + j) * FT + t];
+        double2 u = tm_get(y, j);
+        u.x = fma(x[0][j].x, k.x, fma(-x[0][j].y, k.y, u.x));
+        u.y = fma(x[0][j].x, k.y, fma(x[0][j].y, k.x, u.y));
+        tm_st_acc(a + 4 * j, u);
+      }
+    }
+    gsync<GT>(hbar);   // the half is past the slice; the second half fetches the next row's
+    if (leader) {
+      __threadfence_block();
+      if (atomicAdd(&sm.key_cnt[0], 1u) == 1u) {
+        sm.key_cnt[0] = 0;
+        if (r + 1 < 2 * lv) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_expect_tx(&sm.key_full[0], kSliceBytes);
+          bulk_g2s(sm.key[0], G + (size_t)(r + 1) * (2 * 2 * FC * FT), kSliceBytes, &sm.key_full[0]);
+        }
+      }
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+#pragma unroll 1
+  for (int c = 0; c < 2; ++c) {
+    uint32_t lo[2][FC];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double2 Y[1][FC];
+      {
+        uint32_t y[32];
+        tm_ld32(lane_addr + (uint32_t)((c * 2 + h) * 32), y);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < FC; ++j) Y[0][j] = tm_get(y, j);
+      }
+      inv_fft_hk<1, GT, false>(Y, fscr, lay, t, twi, hbar);
+      if (h == 0) {
+#pragma unroll
+        for (int j = 0; j < FC; ++j) {
+          lo[0][j] = round_u32(Y[0][j].x);
+          lo[1][j] = round_u32(Y[0][j].y);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < FC; ++j) {
+#pragma unroll
+          for (int u2 = 0; u2 < 2; ++u2) {
+            const int i = t + FT * j + FH * u2;
+            const uint32_t v = lo[u2][j] + (round_u32(u2 ? Y[0][j].y : Y[0][j].x) << 16);
+            if (MODE == MODE_IVP_LEVEL) {
+              // CDEMUX (hw/lut.py:113-119, 294-313): hi = C (*) d, lo = d - hi
+              out[(item * 2 * m + m + sub) * 2 * N + c * N + i] = v;
+              out[(item * 2 * m + sub) * 2 * N + c * N + i] = acc[c * N + i] - v;
+            } else {
+              // CMUX (hw/lut.py:130-136, 233-247): next = c0 + C (*) (c1 - c0)
+              const uint32_t *c0 = in + (item * 2 * m + sub) * 2 * N;
+              out[(item * m + sub) * 2 * N + c * N + i] = c0[c * N + i] + v;
+            }
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sm.tmem_slot), "r"(256u));
+  }
 }
 
 // One tree level of vertical packing on the FFT path (cmux_kernel's MODE_IVP_LEVEL /
@@ -4877,6 +5043,17 @@ static int level_fft(const hwb_params *p, const void *ggsw_fft, const int32_t *g
         (const double2 *)ggsw_fft, ggsw_idx, cur, next, m, make_gadget(p->l, p->base_log), st->fft2_fwd[0],
         st->fft2_fwd[1], st->fft2_inv[0], st->fft2_inv[1]);
     return post_launch("level_fft2_kernel");
+  }
+#ifndef HWB_LEVEL_TD
+#define HWB_LEVEL_TD 1   // bit 0: IVP levels, bit 1: VP levels on level_fft_td_kernel
+#endif
+  if ((HWB_LEVEL_TD >> (MODE == MODE_IVP_LEVEL ? 0 : 1)) & 1 && g_fft_mode >= 5 && m % 4 == 0 &&
+      B * m >= (int64_t)8 * st->sms) {
+    const size_t smem_td = sizeof(FSmemTDT<2, 1>);
+    if ((rc = set_smem(level_fft_td_kernel<MODE>, smem_td))) return rc;
+    level_fft_td_kernel<MODE><<<(unsigned)(B * m / 4), 256, smem_td, (cudaStream_t)stream>>>(
+        (const double2 *)ggsw_fft, ggsw_idx, cur, next, m, make_gadget(p->l, p->base_log), st->fft_fwd, st->fft_inv);
+    return post_launch("level_fft_td_kernel");
   }
   if (g_fft_mode >= 1 && m % TMC == 0 && B * m >= (int64_t)2 * TMC * st->sms) {
     // sub-ciphertexts of an item share its GGSW: four per CTA on the TMEM path
