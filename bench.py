@@ -33,7 +33,7 @@ import numpy as np  # noqa: E402
 # FFT ladder mode (hwb_set_fft_mode) -> the kernel that runs a cfg2 batch of 4096
 FFT_KERNELS = {0: "blind_rotate_fft_kernel", 1: "blind_rotate_fft_tm_kernel", 2: "blind_rotate_fft_tx_kernel",
                3: "blind_rotate_fft_tp_kernel", 4: "blind_rotate_fft_tq_kernel", 5: "blind_rotate_fft_td_kernel",
-               6: "blind_rotate_fft_td_kernel<4,2>"}
+               6: "blind_rotate_fft_td_kernel<4,2>", 7: "blind_rotate_fft_w_kernel"}
 METRIC = "bootstrappings/sec"
 UNIT = "PBS/s"
 KEY_SEED, ENC_SEED = 1, 2

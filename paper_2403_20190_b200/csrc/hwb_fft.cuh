@@ -166,6 +166,19 @@ __device__ __forceinline__ uint32_t flay_base(const FLay &L) {
   return LAY == LAY_A ? L.a : (LAY == LAY_M ? L.m : L.b);
 }
 
+// The M <-> B transposes are warp-local.  Layout M is i = (t & 7) | (j << 3) | ((t >> 3) << 6)
+// and layout B is i = 8 t + j: both keep index bits 6..8 in t >> 3 (and the swizzle only
+// touches bits 0..2), so a value only ever moves between the 8 threads that share t >> 3.
+// Every FFT kernel maps those 8 threads (of one ciphertext) into one warp (t = tid % 64,
+// 16 hpos + (lane >> 1) or 8 w + (lane >> 2)), so the stores are ordered before the loads
+// by __syncwarp() alone -- no CTA or named barrier over the transform's 2 to 8 warps.
+// HWB_MB_LOCAL=0 restores the barrier.
+#ifndef HWB_MB_LOCAL
+#define HWB_MB_LOCAL 1
+#endif
+template <int FROM, int TO>
+constexpr bool kMbLocal = HWB_MB_LOCAL && ((FROM == LAY_M && TO == LAY_B) || (FROM == LAY_B && TO == LAY_M));
+
 // Barrier of the 64 threads of one transform: the whole CTA (bar == 0) or a named
 // barrier when a CTA holds several transform groups.
 __device__ __forceinline__ void fsync(int bar) {
@@ -189,7 +202,10 @@ __device__ __forceinline__ void frelayout(double2 (&x)[FC], double2 *scr, const 
   const uint32_t bf = flay_base<FROM>(L), bt = flay_base<TO>(L);
 #pragma unroll
   for (int j = 0; j < FC; ++j) scr[bf ^ fswz(joff<FH, FT, FROM>(j))] = x[j];
-  fsync(bar);
+  if (kMbLocal<FROM, TO>)
+    __syncwarp();
+  else
+    fsync(bar);
   after_first();
 #pragma unroll
   for (int j = 0; j < FC; ++j) x[j] = scr[bt ^ fswz(joff<FH, FT, TO>(j))];
@@ -260,7 +276,10 @@ __device__ __forceinline__ void frelayout_k(double2 (*x)[FC], double2 *scr, cons
   for (int k = 0; k < K; ++k)
 #pragma unroll
     for (int j = 0; j < FC; ++j) scr[k * FH + (bf ^ fswz(joff<FH, FT, FROM>(j)))] = x[k][j];
-  __syncthreads();
+  if (kMbLocal<FROM, TO>)
+    __syncwarp();
+  else
+    __syncthreads();
   after_first();
 #pragma unroll
   for (int k = 0; k < K; ++k)
@@ -444,7 +463,10 @@ __device__ __forceinline__ void frelayout_hk(double2 (*x)[FC], double2 *scr, con
   for (int k = 0; k < K; ++k)
 #pragma unroll
     for (int j = 0; j < FC; ++j) scr[k * FH + (bf ^ fswz(joff<FH, FT, FROM>(j)))] = x[k][j];
-  gsync<NT>(bar);
+  if (kMbLocal<FROM, TO>)
+    __syncwarp();
+  else
+    gsync<NT>(bar);
 #pragma unroll
   for (int k = 0; k < K; ++k)
 #pragma unroll
@@ -454,15 +476,18 @@ __device__ __forceinline__ void frelayout_hk(double2 (*x)[FC], double2 *scr, con
 
 // TRAIL2 = false drops the trailing barrier of the second transpose: the caller
 // guarantees a group barrier before the next write into scr.
-template <int K, int NT, bool CT = false, bool TRAIL2 = true>
+// `pre` runs right before the first store into scr (the split scratch-free wait of the
+// mode-5 ladder's HWB_TD_SPLITBAR build).
+template <int K, int NT, bool CT = false, bool TRAIL2 = true, typename F = NoHook>
 __device__ __forceinline__ void fwd_fft_hk(double2 (*x)[FC], double2 *scr, const FLay &L, int t,
-                                           const double2 *__restrict__ tw, int bar, int cg = 0) {
+                                           const double2 *__restrict__ tw, int bar, int cg = 0, F &&pre = F()) {
   using G = FGeo;
   static_for<0, G::LOGN - G::T>([&](auto Q) {
     constexpr int s = G::LOGN - 1 - decltype(Q)::value;
 #pragma unroll
     for (int k = 0; k < K; ++k) fft_stage<true, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x[k], t, tw, cg);
   });
+  pre();
   frelayout_hk<K, LAY_A, LAY_M, NT, false>(x, scr, L, bar);
   static_for<0, G::T - G::LOGC>([&](auto Q) {
     constexpr int s = G::T - 1 - decltype(Q)::value;
@@ -479,9 +504,9 @@ __device__ __forceinline__ void fwd_fft_hk(double2 (*x)[FC], double2 *scr, const
   });
 }
 
-template <int K, int NT, bool CT = false, bool TRAIL2 = true>
+template <int K, int NT, bool CT = false, bool TRAIL2 = true, typename F = NoHook>
 __device__ __forceinline__ void inv_fft_hk(double2 (*x)[FC], double2 *scr, const FLay &L, int t,
-                                           const double2 *__restrict__ tw, int bar, int cg = 0) {
+                                           const double2 *__restrict__ tw, int bar, int cg = 0, F &&pre = F()) {
   using G = FGeo;
   static_for<0, G::B_TOP>([&](auto Q) {
     constexpr int s = decltype(Q)::value;
@@ -489,6 +514,7 @@ __device__ __forceinline__ void inv_fft_hk(double2 (*x)[FC], double2 *scr, const
 #pragma unroll
     for (int k = 0; k < K; ++k) fft_stage<false, s, false, 0, slot, CT>(x[k], t, tw, cg);
   });
+  pre();
   frelayout_hk<K, LAY_B, LAY_M, NT, false>(x, scr, L, bar);
   static_for<0, G::T - G::LOGC>([&](auto Q) {
     constexpr int s = G::LOGC + decltype(Q)::value;
@@ -503,5 +529,147 @@ __device__ __forceinline__ void inv_fft_hk(double2 (*x)[FC], double2 *scr, const
     for (int k = 0; k < K; ++k) fft_stage<false, s - G::T, true, (1 << (G::LOGN - 1 - s)), 0>(x[k], t, tw, cg);
   });
 }
+
+// ---------------------------------------------------------------------------
+// Wide-thread transform: the same 512-point merged-twist network on 32 threads with 16
+// complex values each (FFT mode 7, blind_rotate_fft_w_kernel).  Nine levels = 4 (layout
+// A16) + 4 (layout M16) + 1 (partner exchange): ONE shared-memory transpose per
+// transform instead of two, and the last level's pairs (i, i + 1) meet through warp
+// shuffles.  Index bits i8..i0 of the in-place array:
+//   A16: thread t = i4..i0, slot j = i8..i5          (levels 0-3, uniform twiddles)
+//   M16: thread u = (i8..i5) << 1 | i0, slot jj = i4..i1   (levels 4-7)
+//   X16: thread u, b = u & 1: slots s < 8 hold i0 = 0, s + 8 hold i0 = 1 of the pairs
+//        with i4 = b, (i3 i2 i1) = s & 7, i.e. i = (u >> 1) << 5 | b << 4 | (s & 7) << 1 | s >> 3
+// Level L, block m uses the twiddle k = 2^L + m of fft_twiddles (as every other ladder),
+// and the network is in place, so array position i of the spectrum holds what it holds in
+// the 64-thread transforms: the FFT key is read in its usual [c][h][j][t] layout at
+// (j, t) = (i & 7, i >> 3).
+constexpr int WT = 32;   // threads per transform
+constexpr int WC = 16;   // complex values per thread
+
+__constant__ double2 c_w16[2][16];   // twiddles k = 1..15 (levels 0-3): [0] forward (cos, tan), [1] inverse (conjugate)
+
+// 16-byte-element swizzle of the one transpose: a quarter-warp (4 threads x the two
+// lane-paired ciphertexts, the odd one XOR 4) must hit 8 distinct slots mod 8.  In A16 the
+// 4 threads differ in (i0, i1), in M16 in (i0, i5): folding i5 into bit 1 serves both.
+__host__ __device__ constexpr uint32_t wswz(uint32_t i) { return i ^ (((i >> 5) & 1u) << 1); }
+// array index of slot s of thread u in the final (X16) layout
+__host__ __device__ constexpr int w16_index(int u, int s) {
+  return ((u >> 1) << 5) | ((u & 1) << 4) | ((s & 7) << 1) | (s >> 3);
+}
+// Per-thread twiddle tables of one direction, [kW16Tab] double2: twm[slot][u >> 1] (slots:
+// level 4 -> 0, level 5 -> 1, level 6 -> 2, 3, level 7 -> 4..7; even blocks only, the odd
+// sibling reuses them) then tw8[slot][u] (level 8, blocks 8 u + {0, 2, 4, 6}).
+constexpr int kW16Twm = 8 * 16, kW16Tab = kW16Twm + 4 * WT;
+
+// one level on the thread's 16 values: pairs (v, v + 2^P); block b = v >> (P + 1) uses
+// tw(b); SIB: odd blocks reuse the even block's twiddle (fft_ct_i / fft_gs_i)
+template <bool FWD, int P, bool SIB, typename TW>
+__device__ __forceinline__ void stage16(double2 (&x)[WC], TW &&tw) {
+  constexpr int NB = WC >> (P + 1), HALF = 1 << P;
+  double2 w = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const bool sib = SIB && (b & 1);
+    if (!sib) w = tw(b);
+#pragma unroll
+    for (int lo = 0; lo < HALF; ++lo) {
+      const int v = (b << (P + 1)) | lo;
+      if (FWD) {
+        if (sib)
+          fft_ct_i(x[v], x[v + HALF], w);
+        else
+          fft_ct(x[v], x[v + HALF], w);
+      } else {
+        if (sib)
+          fft_gs_i(x[v], x[v + HALF], w);
+        else
+          fft_gs(x[v], x[v + HALF], w);
+      }
+    }
+  }
+}
+
+// the partner exchange between M16 and X16 (its own inverse): the thread with i0 = b
+// keeps slots s < 8 (b = 0) or s >= 8 (b = 1) and swaps the others with lane ^ 2
+__device__ __forceinline__ void w16_exchange(double2 (&x)[WC], bool b) {
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const double2 snd = b ? x[s] : x[s + 8];
+    double2 r;
+    r.x = __shfl_xor_sync(0xffffffffu, snd.x, 2);
+    r.y = __shfl_xor_sync(0xffffffffu, snd.y, 2);
+    if (b)
+      x[s] = r;
+    else
+      x[s + 8] = r;
+  }
+}
+
+// natural order (A16) -> spectrum (X16).  ea / em: the thread's swizzled element bases in
+// the two layouts (make_w16_bases), tab: the forward table (shared memory), `bar`: named
+// barrier of the transform's 64 threads (2 warps x 2 lane-paired ciphertexts).
+__device__ __forceinline__ void fwd_fft16(double2 (&x)[WC], double2 *scr, uint32_t ea, uint32_t em, int u,
+                                          const double2 *__restrict__ tab, int bar) {
+  static_for<0, 4>([&](auto Q) {
+    constexpr int L = decltype(Q)::value;
+    stage16<true, 3 - L, false>(x, [&](int b) { return c_w16[0][(1 << L) + b]; });
+  });
+#pragma unroll
+  for (int j = 0; j < WC; ++j) scr[ea ^ wswz((uint32_t)(WT * j))] = x[j];
+  gsync<64>(bar);
+#pragma unroll
+  for (int jj = 0; jj < WC; ++jj) x[jj] = scr[em ^ (uint32_t)(jj << 1)];
+  const double2 *tm = tab + (u >> 1), *tw8 = tab + kW16Twm + u;
+  stage16<true, 3, true>(x, [&](int) { return tm[0 * 16]; });
+  stage16<true, 2, true>(x, [&](int) { return tm[1 * 16]; });
+  stage16<true, 1, true>(x, [&](int b) { return tm[(2 + (b >> 1)) * 16]; });
+  stage16<true, 0, true>(x, [&](int b) { return tm[(4 + (b >> 1)) * 16]; });
+  w16_exchange(x, u & 1);
+  double2 w = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {   // level 8: one butterfly per block, siblings in pairs
+    if (s & 1) {
+      fft_ct_i(x[s], x[s + 8], w);
+    } else {
+      w = tw8[(s >> 1) * WT];
+      fft_ct(x[s], x[s + 8], w);
+    }
+  }
+}
+
+// spectrum (X16) -> natural order (A16), unscaled (1/H is in the key); TRAIL: trailing
+// barrier (the next writer of scr may be the other warp)
+template <bool TRAIL>
+__device__ __forceinline__ void inv_fft16(double2 (&x)[WC], double2 *scr, uint32_t ea, uint32_t em, int u,
+                                          const double2 *__restrict__ tab, int bar) {
+  const double2 *tm = tab + (u >> 1), *tw8 = tab + kW16Twm + u;
+  double2 w = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    if (s & 1) {
+      fft_gs_i(x[s], x[s + 8], w);
+    } else {
+      w = tw8[(s >> 1) * WT];
+      fft_gs(x[s], x[s + 8], w);
+    }
+  }
+  w16_exchange(x, u & 1);
+  stage16<false, 0, true>(x, [&](int b) { return tm[(4 + (b >> 1)) * 16]; });
+  stage16<false, 1, true>(x, [&](int b) { return tm[(2 + (b >> 1)) * 16]; });
+  stage16<false, 2, true>(x, [&](int) { return tm[1 * 16]; });
+  stage16<false, 3, true>(x, [&](int) { return tm[0 * 16]; });
+#pragma unroll
+  for (int jj = 0; jj < WC; ++jj) scr[em ^ (uint32_t)(jj << 1)] = x[jj];
+  gsync<64>(bar);
+#pragma unroll
+  for (int j = 0; j < WC; ++j) x[j] = scr[ea ^ wswz((uint32_t)(WT * j))];
+  if (TRAIL) gsync<64>(bar);
+  static_for<0, 4>([&](auto Q) {
+    constexpr int L = 3 - decltype(Q)::value;
+    stage16<false, 3 - L, false>(x, [&](int b) { return c_w16[1][(1 << L) + b]; });
+  });
+}
+
 
 }  // namespace hwb

@@ -92,6 +92,7 @@ struct DevState {
   uint2 *lane_inv[2][2] = {};
   uint2 *lane_inv64[2] = {};    // N = 1024 inverse transform on 64 threads (latency ladder)
   double2 *fft_fwd = nullptr, *fft_inv = nullptr;   // FP64 FFT per-thread twiddles
+  double2 *fft_w16 = nullptr;   // wide-thread transform (mode 7): [forward, inverse][kW16Tab]
   double2 *fft2_fwd[2] = {}, *fft2_inv[2] = {};     // N = 2048: the sub-transform of half g
 };
 
@@ -244,6 +245,27 @@ static int init_device(DevState **out) {
     for (int k = 0; k < 8; ++k) {
       h_ftw[0][0][k] = wf[k];
       h_ftw[0][1][k] = wi[k];
+    }
+    {   // wide-thread transform (hwb_fft.cuh: fwd_fft16 / inv_fft16)
+      std::vector<double2> w16(2 * kW16Tab);
+      double2 h_w16[2][16];
+      for (int d = 0; d < 2; ++d) {
+        const std::vector<double2> &w = d == 0 ? wf : wi;
+        double2 *tab = w16.data() + d * kW16Tab;
+        for (int v = 0; v < 16; ++v) {
+          tab[0 * 16 + v] = w[16 + v];                                              // level 4, block v
+          tab[1 * 16 + v] = w[32 + 2 * v];                                          // level 5, block 2 v
+          for (int b = 0; b < 2; ++b) tab[(2 + b) * 16 + v] = w[64 + 4 * v + 2 * b];    // level 6
+          for (int b = 0; b < 4; ++b) tab[(4 + b) * 16 + v] = w[128 + 8 * v + 2 * b];   // level 7
+        }
+        for (int b = 0; b < 4; ++b)
+          for (int uu = 0; uu < WT; ++uu) tab[kW16Twm + b * WT + uu] = w[256 + 8 * uu + 2 * b];   // level 8
+        for (int k = 0; k < 16; ++k) h_w16[d][k] = w[k];
+      }
+      if (e1 == cudaSuccess) e1 = cudaMalloc(&st.fft_w16, sizeof(double2) * w16.size());
+      if (e1 == cudaSuccess)
+        e1 = cudaMemcpy(st.fft_w16, w16.data(), sizeof(double2) * w16.size(), cudaMemcpyHostToDevice);
+      if (e1 == cudaSuccess) e1 = cudaMemcpyToSymbol(c_w16, h_w16, sizeof(h_w16));
     }
     // N = 2048 (FFT2): the 1024-point folded transform's first stage (level 0,
     // twiddle k = 1) is done by hand; half g is a 512-point transform whose local
@@ -1962,7 +1984,8 @@ struct FSmemTDT {
   double2 twf[kTwc * FT], twi[kTwc * FT];
   uint64_t key_full[KS];
   uint64_t in_full;                 // level kernel: the inputs' bulk copies landed
-  uint32_t key_cnt[KS];             // groups done with the slot's slice
+  uint64_t scr_free[NG];            // mode 5/6: a group's 4 warps are past their reads of scr (split barrier)
+  uint32_t key_cnt[KS];             // warps (HWB_TD_SPLITBAR) or groups done with the slot's slice
   uint32_t tmem_slot;
 };
 
@@ -2028,6 +2051,8 @@ __global__ void __launch_bounds__(NG * 128, NG == 2 ? 2 : 1)
       mbar_init(&sm.key_full[k], 1);
       sm.key_cnt[k] = 0;
     }
+#pragma unroll
+    for (int k = 0; k < NG; ++k) mbar_init(&sm.scr_free[k], 4);   // one arrival per warp of the group
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 #pragma unroll
     for (int k = 0; k < KS; ++k)   // the first KS rows' slices
@@ -2052,10 +2077,31 @@ __global__ void __launch_bounds__(NG * 128, NG == 2 ? 2 : 1)
   const bool leader = lane == 0 && hpos == 0;
   // a half is done with the key buffer (slice or, for half 1, inverse scratch):
   // the second half to finish issues the next row's slice
-  auto release = [&](int u) {   // the last group done with slot u % KS fetches row u + KS
+#ifndef HWB_TD_SPLITBAR
+#define HWB_TD_SPLITBAR 0
+#endif
+#ifndef HWB_TD_LATEWAIT
+#define HWB_TD_LATEWAIT 0
+#endif
+  // HWB_TD_SPLITBAR: the barriers that only guard buffer REUSE become split barriers.
+  // (a) Key slot: every warp counts itself out after its MAC (its key loads have returned:
+  // the tcgen05.st of their products have issued) and the last of the CTA's warps issues
+  // the next slice's copy -- nobody waits.  (b) Transpose scratch: a warp arrives on the
+  // group's scr_free mbarrier once its last loads from scr are consumed (the stages after
+  // the transform's second transpose) and waits on it only right before the next
+  // transform's first store, a whole stage group later.  The barriers between a
+  // transpose's stores and loads (a data dependency) stay.
+  auto release = [&](int u) {   // the last warp / group done with slot u % KS fetches row u + KS
+#if HWB_TD_SPLITBAR
+    __syncwarp();
+    if (lane != 0) return;
+    constexpr uint32_t kLast = NG * 4 - 1;
+#else
     if (!leader) return;
+    constexpr uint32_t kLast = NG - 1;
+#endif
     __threadfence_block();
-    if (atomicAdd(&sm.key_cnt[u % KS], 1u) == (uint32_t)(NG - 1)) {
+    if (atomicAdd(&sm.key_cnt[u % KS], 1u) == kLast) {
       sm.key_cnt[u % KS] = 0;
       if (u + KS < rows) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -2064,6 +2110,17 @@ __global__ void __launch_bounds__(NG * 128, NG == 2 ? 2 : 1)
       }
     }
   };
+#if HWB_TD_SPLITBAR
+  uint32_t sf_phase = 0;   // completed scr_free phases this thread has waited for
+  auto scr_arrive = [&] {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.scr_free[half]);
+  };
+  auto scr_wait = [&] {
+    mbar_wait(&sm.scr_free[half], sf_phase & 1u);
+    ++sf_phase;
+  };
+#endif
 
   const double dig_off = 4503599627370496.0 + (double)g.half;
   double2 *fscr = sm.scr[q];   // 8 KB
@@ -2095,10 +2152,20 @@ __global__ void __launch_bounds__(NG * 128, NG == 2 ? 2 : 1)
                                u2d_minus((pw[1][j] >> sh) & g.mask, dig_off));
       // (no trailing barrier on the second transpose: the release barrier after the MAC
       // precedes the next write into fscr)
+#if HWB_TD_SPLITBAR
+      fwd_fft_hk<1, GT, true, false>(x, fscr, lay, t, sm.twf, hbar, 0, [&] {
+        if (r != 0) scr_wait();   // (row 0 follows the end-of-step barrier)
+      });
+      scr_arrive();   // the last stages consumed every value loaded from fscr
+#else
       fwd_fft_hk<1, GT, true, false>(x, fscr, lay, t, sm.twf, hbar);
+#endif
       const int u = (s - s0) * 2 * lv + r;   // this row's slot u % KS, use u / KS
       mbar_wait(&sm.key_full[u % KS], (uint32_t)(u / KS) & 1u);
       const double2 *key = sm.key[u % KS];
+#if HWB_TD_LATEWAIT   // the previous row's (or the inverse's zeroing) stores: drained during the transform
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+#endif
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
         const uint32_t a = lane_addr + (uint32_t)(ch * 32);
@@ -2110,11 +2177,7 @@ __global__ void __launch_bounds__(NG * 128, NG == 2 ? 2 : 1)
 #if HWB_X_NOKEY
           const double2 k = make_double2(1.0 + j + ch, 0.5 * r);
 #else
-#if HWB_X_NOKEY
-          const double2 k = make_double2(1.0 + j + ch, 0.5 * r);
-#else
           const double2 k = key[(ch * FC + j) * FT + t];
-#endif
 #endif
           double2 u = tm_get(y, j);
           u.x = fma(x[0][j].x, k.x, fma(-x[0][j].y, k.y, u.x));
@@ -2122,10 +2185,17 @@ __global__ void __launch_bounds__(NG * 128, NG == 2 ? 2 : 1)
           tm_st_acc(a + 4 * j, u);
         }
       }
+#if !HWB_TD_SPLITBAR
       gsync<GT>(hbar);   // the half is past the slice
+#endif
       release(u);
+#if !HWB_TD_LATEWAIT
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+#endif
     }
+#if HWB_TD_LATEWAIT
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");   // the last row's products
+#endif
     // inverse transforms, one accumulator at a time (lo then hi of each component), in
     // the ciphertext's own forward scratch: the key buffer only ever holds slices
 #pragma unroll 1
@@ -2142,10 +2212,15 @@ __global__ void __launch_bounds__(NG * 128, NG == 2 ? 2 : 1)
 #pragma unroll
           for (int j = 0; j < FC; ++j) Y[0][j] = tm_get(y, j);
         }
+#if HWB_TD_SPLITBAR
+        inv_fft_hk<1, GT, true, false>(Y, fscr, lay, t, sm.twi, hbar, 0, [&] { scr_wait(); });
+        if (!(c == 1 && h == 1)) scr_arrive();   // (the end-of-step barrier follows the last one)
+#else
         if (c == 1 && h == 1)   // the end-of-step barrier precedes the next write into fscr
           inv_fft_hk<1, GT, true, false>(Y, fscr, lay, t, sm.twi, hbar);
         else
           inv_fft_hk<1, GT, true>(Y, fscr, lay, t, sm.twi, hbar);
+#endif
         if (h == 0) {
 #pragma unroll
           for (int j = 0; j < FC; ++j) {
@@ -2180,6 +2255,230 @@ __global__ void __launch_bounds__(NG * 128, NG == 2 ? 2 : 1)
     uint32_t *o = lwe_out + bq * (int64_t)(N + 1);
     for (int k = t; k < N; k += FT) o[k] = k == 0 ? acc[0] : 0u - acc[N - k];
     if (t == 0) o[N] = acc[N];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// TMEM ladder on wide threads (`blind_rotate_fft_w_kernel`, FFT mode 7).
+//
+// Mode 5's structure (lane-paired ciphertexts, decoupled groups, the TMA-staged key slice
+// shared by the CTA's 4 ciphertexts, spectra accumulators in tensor memory) on the
+// 32-thread transform of hwb_fft.cuh (fwd_fft16 / inv_fft16): 16 complex values per
+// thread, so a transform has ONE shared-memory transpose (16 KB of traffic instead of
+// 32 KB) plus 16 register exchanges with the neighbouring position through shuffles.  A
+// CTA is 4 warps = 2 groups of 2 warps; a group carries two lane-paired ciphertexts
+// (lanes 2m, 2m + 1: the same position u = 16 (warp & 1) + m of ciphertexts 2 g, 2 g + 1)
+// and synchronises on its own 64-thread named barrier.  Each thread owns 256 TMEM
+// columns (4 accumulators x 16 complex), a CTA the 4 lane quadrants x 256 columns; two
+// CTAs per SM fill the tensor memory with 8 ciphertexts, as in mode 5.  The key is read
+// in its usual layout at (j, t) = (i & 7, i >> 3), i = w16_index(u, s): 4 positions of a
+// quarter-warp read 4 distinct 16-byte bank groups, each serving a lane pair.
+
+struct FSmemW {
+  uint32_t acc[4][TP_ACC];          // working ciphertexts; odd ones 16 words further (TP_ACC)
+  double2 scr[4][FH];               // transpose scratch per ciphertext (odd: addresses XOR 4)
+  double2 key[2 * 2 * FC * FT];     // the row's key slice (TMA), shared by both groups
+  double2 twf[kW16Tab], twi[kW16Tab];
+  uint64_t key_full;
+  uint32_t key_cnt;                 // groups done with the slice
+  uint32_t tmem_slot;
+};
+
+__global__ void __launch_bounds__(128, 2)
+    blind_rotate_fft_w_kernel(const double2 *__restrict__ ggsw, const uint32_t *__restrict__ lwe_in,
+                              const uint32_t *__restrict__ tv, int tv_per_item, uint32_t *lwe_out, int L, Gadget g,
+                              const double2 *__restrict__ w16tab, uint32_t *acc_io, int s0, int s1, int64_t B) {
+  constexpr int N = 2 * FH;
+  constexpr int LOG2M = 11;
+  extern __shared__ uint4 smem_raw[];
+  FSmemW &sm = *reinterpret_cast<FSmemW *>(smem_raw);
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int grp = warp >> 1, bar = 1 + grp;
+  const int q = 2 * grp + (lane & 1), u = 16 * (warp & 1) + (lane >> 1);
+  // swizzled element bases of the thread in layouts A16 (i = u + 32 j) and M16
+  // (i = (u >> 1) << 5 | jj << 1 | (u & 1)); the pair partner takes the other half of the
+  // 8 bank groups
+  const uint32_t px = (q & 1) ? 4u : 0u;
+  const uint32_t ea = wswz((uint32_t)u) ^ px, em = wswz((uint32_t)(((u >> 1) << 5) | (u & 1))) ^ px;
+  const int64_t bb = (int64_t)blockIdx.x * 4 + q;
+  const bool valid = bb < B;
+  const int64_t bq = valid ? bb : B - 1;
+  const uint32_t *row = lwe_in + bq * (int64_t)(L + 1);
+  uint32_t *acc = sm.acc[q];
+  if (s0 == 0) {
+    const int bt = mod_switch(row[L], LOG2M);
+    const uint32_t *tp = tv + (tv_per_item ? bq * 2 * N : 0);
+    const int e = (2 * N - bt) & (2 * N - 1);   // X^-b~
+    for (int k = u; k < 2 * N; k += WT) {
+      const int c = k >= N, i = k & (N - 1);
+      acc[k] = rot_read<N>(tp + c * N, i, e);
+    }
+  } else {
+    for (int k = u; k < 2 * N; k += WT) acc[k] = acc_io[bq * 2 * N + k];
+  }
+  for (int k = tid; k < kW16Tab; k += 128) {
+    sm.twf[k] = w16tab[k];
+    sm.twi[k] = w16tab[kW16Tab + k];
+  }
+  constexpr uint32_t kSliceBytes = 2 * 2 * FC * FT * sizeof(double2);
+  const size_t ggsw_f = (size_t)2 * g.levels * 2 * 2 * FC * FT;
+  const int lv = (int)g.levels;
+  const int rows = (s1 - s0) * 2 * lv;   // key-slice rows of this launch, r_abs = (s - s0) 2l + r
+  auto slice = [&](int ra) {
+    return ggsw + (size_t)(s0 + ra / (2 * lv)) * ggsw_f + (size_t)(ra % (2 * lv)) * (2 * 2 * FC * FT);
+  };
+  if (tid == 0) {
+    mbar_init(&sm.key_full, 1);
+    sm.key_cnt = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&sm.key_full, kSliceBytes);
+    bulk_g2s(sm.key, slice(0), kSliceBytes, &sm.key_full);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_slot)),
+                 "r"(256u));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  // lane quadrant = warp (4 warps); columns (ch 16 + s) 4 + {re.lo, re.hi, im.lo, im.hi}
+  const uint32_t lane_addr = sm.tmem_slot + ((uint32_t)(warp * 32) << 16);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) tm_zero32(lane_addr + (uint32_t)(k * 32));
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  const bool leader = lane == 0 && (warp & 1) == 0;
+  // a group is done with the slice: the second one issues the next row's copy
+  auto release = [&](int ra) {
+    if (!leader) return;
+    __threadfence_block();
+    if (atomicAdd(&sm.key_cnt, 1u) == 1u) {
+      sm.key_cnt = 0;
+      if (ra + 1 < rows) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&sm.key_full, kSliceBytes);
+        bulk_g2s(sm.key, slice(ra + 1), kSliceBytes, &sm.key_full);
+      }
+    }
+  };
+
+  const double dig_off = 4503599627370496.0 + (double)g.half;
+  double2 *fscr = sm.scr[q];   // 8 KB
+  // key address of slot s: (j, t) = (i & 7, i >> 3), i = w16_index(u, s): t = 2 u + ((s >> 2) & 1)
+  const double2 *keyu = sm.key + 2 * u;
+  uint32_t a_nx = row[s0];   // the next step's mask word, loaded a step ahead (s + 1 <= L)
+#pragma unroll 1
+  for (int s = s0; s < s1; ++s) {
+    const int e = mod_switch(a_nx, LOG2M);   // X^{a~_s}
+    a_nx = row[s + 1];
+    uint32_t pw[2][WC];   // decomposition-ready words of the current component
+#pragma unroll 1
+    for (int r = 0; r < 2 * lv; ++r) {
+      // digit order (hw/tfhe.py:290-298): rows 0..l-1 = digits of b, l..2l-1 of a
+      const int comp = r < lv ? 1 : 0;
+      const int tt = r < lv ? r : r - lv;
+      const uint32_t sh = g.base_log * (uint32_t)(lv - 1 - tt);
+      const uint32_t *ac = acc + comp * N;
+      double2 x[WC];
+      if (tt == 0) {
+#pragma unroll
+        for (int j = 0; j < WC; ++j) {
+          const int i = u + WT * j;
+          pw[0][j] = decomp_prep(rot_read<N>(ac, i, e) - ac[i], g);
+          pw[1][j] = decomp_prep(rot_read<N>(ac, i + FH, e) - ac[i + FH], g);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < WC; ++j)
+        x[j] = make_double2(u2d_minus((pw[0][j] >> sh) & g.mask, dig_off),
+                            u2d_minus((pw[1][j] >> sh) & g.mask, dig_off));
+      // (no trailing barrier: the release barrier after the MAC precedes the next write
+      // into fscr)
+      fwd_fft16(x, fscr, ea, em, u, sm.twf, bar);
+      const int ra = (s - s0) * 2 * lv + r;
+      mbar_wait(&sm.key_full, (uint32_t)ra & 1u);
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          const uint32_t a = lane_addr + (uint32_t)(ch * 64 + hf * 32);
+          uint32_t y[32];
+          tm_ld32(a, y);   // zeroed at the end of the previous product
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int s8 = 0; s8 < 8; ++s8) {
+            const int sl = hf * 8 + s8;
+            const int kj = ((sl & 3) << 1) | (sl >> 3), kt = (sl >> 2) & 1;
+#if HWB_X_NOKEY
+            const double2 k = make_double2(1.0 + sl + ch, 0.5 * r);
+#else
+            const double2 k = keyu[(ch * FC + kj) * FT + kt];
+#endif
+            double2 v = tm_get(y, s8);
+            v.x = fma(x[sl].x, k.x, fma(-x[sl].y, k.y, v.x));
+            v.y = fma(x[sl].x, k.y, fma(x[sl].y, k.x, v.y));
+            tm_st_acc(a + 4 * s8, v);
+          }
+        }
+      }
+      gsync<64>(bar);   // the group is past the slice (and its reads of fscr)
+      release(ra);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    // inverse transforms, one accumulator at a time (lo then hi of each component)
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      uint32_t lo[2][WC];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double2 Y[WC];
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          const uint32_t a = lane_addr + (uint32_t)((c * 2 + h) * 64 + hf * 32);
+          uint32_t y[32];
+          tm_ld32(a, y);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          tm_zero32(a);   // next product
+#pragma unroll
+          for (int s8 = 0; s8 < 8; ++s8) Y[hf * 8 + s8] = tm_get(y, s8);
+        }
+        if (c == 1 && h == 1)   // the end-of-step barrier precedes the next write into fscr
+          inv_fft16<false>(Y, fscr, ea, em, u, sm.twi, bar);
+        else
+          inv_fft16<true>(Y, fscr, ea, em, u, sm.twi, bar);
+        if (h == 0) {
+#pragma unroll
+          for (int j = 0; j < WC; ++j) {
+            lo[0][j] = round_u32(Y[j].x);
+            lo[1][j] = round_u32(Y[j].y);
+          }
+        } else if (e != 0) {
+#pragma unroll
+          for (int j = 0; j < WC; ++j) {
+            const int i = u + WT * j;
+            acc[c * N + i] += lo[0][j] + (round_u32(Y[j].x) << 16);
+            acc[c * N + i + FH] += lo[1][j] + (round_u32(Y[j].y) << 16);
+          }
+        }
+      }
+    }
+    gsync<64>(bar);   // the group's accumulator updates before the next step's digits
+  }
+  // the last step's zeroing stores (tm_zero32) must land before the columns are freed
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sm.tmem_slot), "r"(256u));
+  }
+  if (!valid) return;
+  if (s1 < L) {
+    for (int k = u; k < 2 * N; k += WT) acc_io[bq * 2 * N + k] = acc[k];
+  } else {
+    uint32_t *o = lwe_out + bq * (int64_t)(N + 1);
+    for (int k = u; k < N; k += WT) o[k] = k == 0 ? acc[0] : 0u - acc[N - k];
+    if (u == 0) o[N] = acc[N];
   }
 }
 
@@ -4740,10 +5039,10 @@ static thread_local int g_fft_mode = 5;
 constexpr int64_t g_fft_tmem_min = 4;
 
 int hwb_set_fft_mode(int mode) {
-  if (mode < 0 || mode > 6)
+  if (mode < 0 || mode > 7)
     return fail(HWB_EINVAL, "FFT ladder mode must be 0 (registers), 1 (TMEM), 2 (TMEM, one ciphertext per thread) "
                             "3 (TMEM, lane-paired), 4 (TMEM, decoupled groups), 5 (TMEM, lane-paired, decoupled halves) or 6 (5 as one "
-                            "16-warp CTA with a two-slot key ring)");
+                            "16-warp CTA with a two-slot key ring) or 7 (5 on 32-thread transforms: one transpose per transform)");
   g_fft_mode = mode;
   return HWB_OK;
 }
@@ -4928,6 +5227,12 @@ int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, co
           (const double2 *)bsk_fft, nullptr, nullptr, lwe_in, tv, tv_per_item, ext, L, g, st->fft2_fwd[0],
           st->fft2_fwd[1], st->fft2_inv[0], st->fft2_inv[1], acc, s0, s1, B);
       rc = post_launch("blind_rotate_fft2_kernel");
+    } else if (g_fft_mode == 7 && B >= g_fft_tmem_min * (int64_t)st->sms) {
+      const size_t smem = sizeof(FSmemW);
+      if ((rc = set_smem(blind_rotate_fft_w_kernel, smem))) return rc;
+      blind_rotate_fft_w_kernel<<<(unsigned)((B + 3) / 4), 128, smem, s>>>(
+          (const double2 *)bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st->fft_w16, acc, s0, s1, B);
+      rc = post_launch("blind_rotate_fft_w_kernel");
     } else if (g_fft_mode == 6 && B >= 8 * (int64_t)st->sms) {
       const size_t smem = sizeof(FSmemTDT<4, 2>);
       if ((rc = set_smem(blind_rotate_fft_td_kernel<4, 2>, smem))) return rc;
