@@ -638,11 +638,10 @@ __device__ __forceinline__ void fwd_fft16(double2 (&x)[WC], double2 *scr, uint32
   }
 }
 
-// spectrum (X16) -> natural order (A16), unscaled (1/H is in the key); TRAIL: trailing
+// spectrum (X16) -> natural order (A16), unscaled (1/H is in the key); trail: trailing
 // barrier (the next writer of scr may be the other warp)
-template <bool TRAIL>
 __device__ __forceinline__ void inv_fft16(double2 (&x)[WC], double2 *scr, uint32_t ea, uint32_t em, int u,
-                                          const double2 *__restrict__ tab, int bar) {
+                                          const double2 *__restrict__ tab, int bar, bool trail) {
   const double2 *tm = tab + (u >> 1), *tw8 = tab + kW16Twm + u;
   double2 w = make_double2(0.0, 0.0);
 #pragma unroll
@@ -664,7 +663,7 @@ __device__ __forceinline__ void inv_fft16(double2 (&x)[WC], double2 *scr, uint32
   gsync<64>(bar);
 #pragma unroll
   for (int j = 0; j < WC; ++j) x[j] = scr[ea ^ wswz((uint32_t)(WT * j))];
-  if (TRAIL) gsync<64>(bar);
+  if (trail) gsync<64>(bar);
   static_for<0, 4>([&](auto Q) {
     constexpr int L = 3 - decltype(Q)::value;
     stage16<false, 3 - L, false>(x, [&](int b) { return c_w16[1][(1 << L) + b]; });
