@@ -3843,12 +3843,16 @@ __global__ void __launch_bounds__(2 * FT, 1)
 // exchange their values through the transpose scratch.
 
 constexpr int T2C = 4;   // ciphertexts per CTA
+constexpr int T2_COMP = 4 * FH + 48;   // words per padded component (t2_off)
 
 struct FSmem2TD {
-  // working ciphertexts (a, b), N = 2048, padded (t2_pad): coefficient i of component
-  // c at c (N + 16) + i + 8 (i >> 10), odd ciphertexts 16 words further -- a lane
-  // quad's 4 (ciphertext, half) digit reads land on 4 different bank octets
-  uint32_t acc[T2C][2 * (4 * FH + 16) + 16];
+  // working ciphertexts (a, b), N = 2048, padded (t2_off): each 512-coefficient block
+  // starts 8 banks after the previous one (offsets 0, 8, 40, 48 words), odd ciphertexts 16
+  // banks further (the row stride).  A lane quad's 4 (ciphertext, half) accesses then land on
+  // 4 different bank octets both in the digit reads (halves 1024 apart) and in the
+  // accumulator update after the inverse (halves 512 apart; 4-way conflicts before:
+  // profiles/r02c_smem_lines_f2td.txt)
+  uint32_t acc[T2C][2 * T2_COMP + 16];
   double2 scr[T2C][2][FH];         // transpose / level-0 scratch per (ciphertext, half)
   // the row's key slice [c][h][g][j][t] (64 KB, 8 TMA chunks of 8 KB at a stride of
   // 8 KB + 64 B, so a lane quad's two halves hit different bank groups)
@@ -3859,12 +3863,14 @@ struct FSmem2TD {
   uint32_t tmem_slot;
 };
 
-__device__ __forceinline__ int t2_pad(int c, int i) { return c * (4 * FH + 16) + i + 8 * (i >> 10); }
+static_assert(sizeof(FSmem2TD) <= 232448, "FSmem2TD exceeds the 227 KB of shared memory a CTA can opt into");
+__device__ __forceinline__ int t2_off(int i) { return i + 8 * ((i >> 9) & 1) + 40 * (i >> 10); }
+__device__ __forceinline__ int t2_pad(int c, int i) { return c * T2_COMP + t2_off(i); }
 // rot_read on a t2_pad-ded component
 __device__ __forceinline__ uint32_t rot_read_t2(const uint32_t *poly, int i, int e) {
   constexpr int N = 4 * FH;
   const int src = (i - e) & (2 * N - 1), idx = src & (N - 1);
-  const uint32_t val = poly[idx + 8 * (idx >> 10)];
+  const uint32_t val = poly[t2_off(idx)];
   return src >= N ? 0u - val : val;
 }
 
@@ -3896,7 +3902,7 @@ __global__ void __launch_bounds__(16 * 32, 1)
   const bool valid = bb < B;
   const int64_t bq = valid ? bb : B - 1;
   const uint32_t *row = lwe_in + bq * (int64_t)(L + 1);
-  uint32_t *acc = sm.acc[q] + (q & 1) * 16;
+  uint32_t *acc = sm.acc[q];   // row stride = 16 mod 32 words: odd ciphertexts 16 banks over
   if (s0 == 0) {
     const int bt = mod_switch(row[L], LOG2M);
     const uint32_t *tp = tv + (tv_per_item ? bq * 2 * N : 0);
@@ -3990,7 +3996,7 @@ __global__ void __launch_bounds__(16 * 32, 1)
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             const int i = k + FH * (2 * hf + u);
-            const uint32_t pw = decomp_prep(rot_read_t2(ac, i, e) - ac[i + 8 * (i >> 10)], g);
+            const uint32_t pw = decomp_prep(rot_read_t2(ac, i, e) - ac[i + 8 * u + 40 * hf], g);   // = t2_off(i)
             own |= ((pw >> sh) & g.mask) << (16 * u);
             o1 |= ((pw >> (sh - g.base_log)) & g.mask) << (16 * u);   // row tt + 1 (used iff lv == 2)
           }
@@ -4065,8 +4071,9 @@ __global__ void __launch_bounds__(16 * 32, 1)
 #pragma unroll
           for (int j = 0; j < FC; ++j) {
             const int f = hf * FH + t + FT * j;   // folded point: coefficients f and f + 1024
-            acc[t2_pad(c, f)] += lo[0][j] + (round_u32(Y[0][j].x) << 16);
-            acc[t2_pad(c, f + 2 * FH)] += lo[1][j] + (round_u32(Y[0][j].y) << 16);
+            uint32_t *af = acc + c * T2_COMP + f + 8 * hf;   // t2_pad(c, f), f < 1024 in block hf
+            af[0] += lo[0][j] + (round_u32(Y[0][j].x) << 16);
+            af[2 * FH + 40] += lo[1][j] + (round_u32(Y[0][j].y) << 16);   // t2_pad(c, f + 1024)
           }
         }
       }
