@@ -21,7 +21,7 @@ python tools/run_pbs.py 4096 fft -1 1 7 > gpurun_out/r02c_plain_w.log 2>&1 && \
 # gpurun brings back at most 64 MiB: summarise on the box, keep the per-line source page
 for k in td f2td w; do
   python profiles/ncu_summary.py gpurun_out/r02c_ncu_$k.ncu-rep > gpurun_out/r02c_ncu_$k.txt 2>&1
-  ncu -i gpurun_out/r02c_ncu_$k.ncu-rep --page source --csv --print-source cuda > gpurun_out/r02c_src_$k.csv 2>/dev/null
+  ncu -i gpurun_out/r02c_ncu_$k.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/r02c_src_$k.csv 2>/dev/null
   rm -f gpurun_out/r02c_ncu_$k.ncu-rep
 done
 echo done
