@@ -663,11 +663,11 @@ __device__ __forceinline__ void inv_fft16(double2 (&x)[WC], double2 *scr, uint32
   gsync<64>(bar);
 #pragma unroll
   for (int j = 0; j < WC; ++j) x[j] = scr[ea ^ wswz((uint32_t)(WT * j))];
-  if (trail) gsync<64>(bar);
   static_for<0, 4>([&](auto Q) {
     constexpr int L = 3 - decltype(Q)::value;
     stage16<false, 3 - L, false>(x, [&](int b) { return c_w16[1][(1 << L) + b]; });
   });
+  if (trail) gsync<64>(bar);   // (after the last levels, as in mode 5: 54.3 -> 52.4 ms there)
 }
 
 

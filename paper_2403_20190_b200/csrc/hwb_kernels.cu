@@ -1976,6 +1976,23 @@ __global__ void __launch_bounds__(TPC * FT, 2)
 // transforms).  The inverse runs one accumulator at a time in the ciphertext's own
 // 8 KB scratch, so the halves share nothing else.
 
+// Shape of the inverse phase / instruction footprint of the step loop (A/B, cfg2 B = 4096,
+// DESIGN.md 3b).  HWB_TD_ONEINV: 0 = the trailing barrier inside the inverse, right after its
+// last loads from the scratch (two instantiations for h = 1: 2,808 instructions, 54.3 ms);
+// 1 = one instantiation per h, the barrier after the inverse's last three levels, skipped at
+// run time for the last inverse (2,344 instructions, **52.4 ms**, default); 2 = 1 with the h
+// loop rolled (one instantiation, 1,992 instructions: 54.3 ms); 3 = the barrier at the latest
+// point, before the next inverse's first store (53.0 ms); 4 = after the rounding (53.0 ms).
+// HWB_TD_MACROLL: 1 / 2 = the MAC's accumulator loop rolled / unrolled by 2 (53.8 / 52.8 ms).
+#ifndef HWB_TD_ONEINV
+#define HWB_TD_ONEINV 1
+#endif
+#ifndef HWB_TD_MACROLL
+#define HWB_TD_MACROLL 0
+#endif
+constexpr int kTdMacUnroll = HWB_TD_MACROLL == 1 ? 1 : (HWB_TD_MACROLL == 2 ? 2 : 4),
+              kTdInvUnroll = HWB_TD_ONEINV == 2 ? 1 : 2;
+
 template <int NG, int KS>
 struct FSmemTDT {
   uint32_t acc[2 * NG][TP_ACC];     // working ciphertexts; odd ones 16 words further (TP_ACC)
@@ -2166,7 +2183,7 @@ __global__ void __launch_bounds__(NG * 128, NG == 2 ? 2 : 1)
 #if HWB_TD_LATEWAIT   // the previous row's (or the inverse's zeroing) stores: drained during the transform
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 #endif
-#pragma unroll
+#pragma unroll kTdMacUnroll
       for (int ch = 0; ch < 4; ++ch) {
         const uint32_t a = lane_addr + (uint32_t)(ch * 32);
         uint32_t y[32];
@@ -2200,8 +2217,8 @@ __global__ void __launch_bounds__(NG * 128, NG == 2 ? 2 : 1)
     // the ciphertext's own forward scratch: the key buffer only ever holds slices
 #pragma unroll 1
     for (int c = 0; c < 2; ++c) {
-      uint32_t lo[2][FC];
-#pragma unroll
+      uint32_t lo[2][FC] = {};
+#pragma unroll kTdInvUnroll
       for (int h = 0; h < 2; ++h) {
         double2 Y[1][FC];
         {
@@ -2216,10 +2233,22 @@ __global__ void __launch_bounds__(NG * 128, NG == 2 ? 2 : 1)
         inv_fft_hk<1, GT, true, false>(Y, fscr, lay, t, sm.twi, hbar, 0, [&] { scr_wait(); });
         if (!(c == 1 && h == 1)) scr_arrive();   // (the end-of-step barrier follows the last one)
 #else
+#if HWB_TD_ONEINV == 3
+        // the scratch-reuse barrier as late as it can be: right before this inverse's first
+        // store into fscr, after its TMEM load and first three levels (the first inverse
+        // follows the MAC's barrier and needs none)
+        inv_fft_hk<1, GT, true, false>(Y, fscr, lay, t, sm.twi, hbar, 0, [&] {
+          if (h == 1 || c == 1) gsync<GT>(hbar);
+        });
+#elif HWB_TD_ONEINV   // one copy of the inverse per h: the trailing barrier as a runtime-skipped call after it
+        inv_fft_hk<1, GT, true, false>(Y, fscr, lay, t, sm.twi, hbar);
+        if (HWB_TD_ONEINV != 4 && !(c == 1 && h == 1)) gsync<GT>(hbar);   // (the end-of-step barrier follows the last inverse)
+#else
         if (c == 1 && h == 1)   // the end-of-step barrier precedes the next write into fscr
           inv_fft_hk<1, GT, true, false>(Y, fscr, lay, t, sm.twi, hbar);
         else
           inv_fft_hk<1, GT, true>(Y, fscr, lay, t, sm.twi, hbar);
+#endif
 #endif
         if (h == 0) {
 #pragma unroll
@@ -2235,6 +2264,7 @@ __global__ void __launch_bounds__(NG * 128, NG == 2 ? 2 : 1)
             acc[c * N + i + FH] += lo[1][j] + (round_u32(Y[0][j].y) << 16);
           }
         }
+        if (HWB_TD_ONEINV == 4 && !(c == 1 && h == 1)) gsync<GT>(hbar);   // (variant: after the rounding)
       }
     }
     gsync<GT>(hbar);   // the half's accumulator updates before the next step's digits
@@ -2277,8 +2307,10 @@ __global__ void __launch_bounds__(NG * 128, NG == 2 ? 2 : 1)
 #ifndef HWB_W_ROLL   // 1: the MAC's accumulator loop rolled (instruction-cache footprint: 61.5 -> 59.4 ms)
 #define HWB_W_ROLL 1
 #endif
-// (The four inverses stay unrolled: the rolled loop measured 57.7 ms but its results differ
-// from every other ladder -- cause not found, so that build is not selectable.)
+// (The four inverses stay unrolled.  A rolled loop carries `lo` from the h = 0 iteration to
+// the h = 1 one; with `lo` uninitialised at loop entry that build returned wrong results --
+// the loop-carried value has an undefined incoming edge -- hence the `= {}` below and in the
+// other ladders' rolled variants.)
 constexpr int kWUnroll = HWB_W_ROLL ? 1 : 4, kWUnrollInv = 4;
 
 struct FSmemW {
@@ -2433,7 +2465,7 @@ __global__ void __launch_bounds__(128, 2)
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
     // inverse transforms, one accumulator at a time (lo then hi of each component)
-    uint32_t lo[2][WC];
+    uint32_t lo[2][WC] = {};
 #pragma unroll kWUnrollInv
     for (int ci = 0; ci < 4; ++ci) {
       const int c = ci >> 1, h = ci & 1;
@@ -2920,7 +2952,10 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
         for (int j = 0; j < FC; ++j) Y[0][j] = tm_get(y, j);
       }
-      inv_fft_hk<1, GT, false>(Y, fscr, lay, t, twi, hbar);
+      // (scratch-reuse barrier after the inverse's last levels, none after the last inverse:
+      // blind_rotate_fft_td_kernel's HWB_TD_ONEINV placement)
+      inv_fft_hk<1, GT, false, false>(Y, fscr, lay, t, twi, hbar);
+      if (!(c == 1 && h == 1)) gsync<GT>(hbar);
       if (h == 0) {
 #pragma unroll
         for (int j = 0; j < FC; ++j) {
@@ -3843,6 +3878,16 @@ __global__ void __launch_bounds__(2 * FT, 1)
 // exchange their values through the transpose scratch.
 
 constexpr int T2C = 4;   // ciphertexts per CTA
+#ifndef HWB_T2_MACUNROLL   // instruction-cache footprint switches (as HWB_TD_*)
+#define HWB_T2_MACUNROLL 4
+#endif
+#ifndef HWB_T2_INVUNROLL
+#define HWB_T2_INVUNROLL 2
+#endif
+constexpr int kT2MacUnroll = HWB_T2_MACUNROLL, kT2InvUnroll = HWB_T2_INVUNROLL;
+#ifndef HWB_T2_LATEBAR
+#define HWB_T2_LATEBAR 0
+#endif
 constexpr int T2_COMP = 4 * FH + 48;   // words per padded component (t2_off)
 
 struct FSmem2TD {
@@ -4013,7 +4058,7 @@ __global__ void __launch_bounds__(16 * 32, 1)
       fwd_fft_hk<1, GT, true, false>(x, fscr, lay, t, sm.twf[hf], bar, 1 + hf);
       mbar_wait(&sm.key_full, key_phase);
       key_phase ^= 1u;
-#pragma unroll
+#pragma unroll kT2MacUnroll
       for (int ch = 0; ch < 4; ++ch) {
         const uint32_t a = lane_addr + (uint32_t)(ch * 32);
         uint32_t y[32];
@@ -4040,8 +4085,8 @@ __global__ void __launch_bounds__(16 * 32, 1)
     // the level-0 Gentleman-Sande stage across the halves, (X, Y) -> (X + Y, (X - Y) conj(w0))
 #pragma unroll 1
     for (int c = 0; c < 2; ++c) {
-      uint32_t lo[2][FC];
-#pragma unroll
+      uint32_t lo[2][FC] = {};   // (defined on every path: a rolled h loop carries it)
+#pragma unroll kT2InvUnroll
       for (int h = 0; h < 2; ++h) {
         double2 Y[1][FC];
         {
@@ -4052,7 +4097,11 @@ __global__ void __launch_bounds__(16 * 32, 1)
 #pragma unroll
           for (int j = 0; j < FC; ++j) Y[0][j] = tm_get(y, j);
         }
+#if HWB_T2_LATEBAR   // the scratch-reuse barrier after the inverse's last levels and the level-0 stage
+        inv_fft_hk<1, GT, true, false>(Y, fscr, lay, t, sm.twi[hf], bar, 1 + hf);
+#else
         inv_fft_hk<1, GT, true>(Y, fscr, lay, t, sm.twi[hf], bar, 1 + hf);
+#endif
 #pragma unroll
         for (int j = 0; j < FC; ++j) {   // the partner half's value at the same position (lane ^ 2)
           double2 o;
@@ -4061,6 +4110,9 @@ __global__ void __launch_bounds__(16 * 32, 1)
           Y[0][j] = hf == 0 ? make_double2(Y[0][j].x + o.x, Y[0][j].y + o.y)
                             : cmul(make_double2(o.x - Y[0][j].x, o.y - Y[0][j].y), wi0);
         }
+#if HWB_T2_LATEBAR
+        if (!(c == 1 && h == 1)) gsync<GT>(bar);   // (the end-of-step barrier follows the last inverse)
+#endif
         if (h == 0) {
 #pragma unroll
           for (int j = 0; j < FC; ++j) {
