@@ -33,7 +33,7 @@ import numpy as np  # noqa: E402
 # FFT ladder mode (hwb_set_fft_mode) -> the kernel that runs a cfg2 batch of 4096
 FFT_KERNELS = {0: "blind_rotate_fft_kernel", 1: "blind_rotate_fft_tm_kernel", 2: "blind_rotate_fft_tx_kernel",
                3: "blind_rotate_fft_tp_kernel", 4: "blind_rotate_fft_tq_kernel", 5: "blind_rotate_fft_td_kernel",
-               6: "blind_rotate_fft_td_kernel<4,2>", 7: "blind_rotate_fft_w_kernel"}
+               6: "blind_rotate_fft_td_kernel<4,2>", 7: "blind_rotate_fft_w_kernel", 8: "blind_rotate_fft_td_kernel"}
 METRIC = "bootstrappings/sec"
 UNIT = "PBS/s"
 KEY_SEED, ENC_SEED = 1, 2
@@ -709,10 +709,9 @@ def bench_hwb(args):
                                                + 4 * (B * (P.lwe_n + 1) + B * (N + 1) + 2 * N),
                                             FFT_KERNELS[args.fft_mode] if use_fft else "ntt"),
                      "work_per_pbs": work_txt, "peak_source": peak_src,
-                     "traffic_note": ("DRAM bytes per batch measured without ncu's cache flush "
-                                      "(--cache-control none, profiles/r02b_dram_no_flush_td.txt): the key "
-                                      "streams once per batch; ncu --set full's per-launch flush would force "
-                                      "the segment accumulators (B x 8 KB) through DRAM as well (~470 MB)")
+                     "traffic_note": ("DRAM bytes of the ladder's single launch (one batch), ncu --set full "
+                                      "--clock-control none, profiles/r02c_ncu_td.txt: the key streams once per "
+                                      "batch, the segment accumulators (B x 8 KB) stay in L2 between segments")
                      if use_fft else None,
                      "context": {}}}
     ctx = {"pbs": {"roofline_pbs_per_s": round(pbs_roof, 1),
@@ -740,7 +739,11 @@ def bench_hwb(args):
     result.update({
         "kernel_ms": {"blind_rotate": round(statistics.mean(br_ms), 3),
                       "keyswitch": round(statistics.mean(ks_ms), 3)},
-        "gpu_launches": ((-(-P.lwe_n // 64) if use_fft else 1) + (2 if ks_tc else 1)) * args.steps,
+        # the ladder: one launch per batch in FFT mode 5 (>= 4 ciphertexts per SM), else one per
+        # 64-step segment; + key-switch digits and GEMM.  (The progress words' memset is a
+        # driver memset node, not one of this repo's kernels.)
+        "gpu_launches": (((1 if args.fft_mode == 5 and B >= 4 * 148 else -(-P.lwe_n // 64)) if use_fft else 1)
+                         + (2 if ks_tc else 1)) * args.steps,
         "clocks": clock_info,
         "check": "all outputs decrypt to the LUT" if ok else "DECRYPTION MISMATCH",
     })

@@ -307,8 +307,9 @@ int64_t hwb_set_fft_latency_batch(int64_t max_batch);
  * address), 4 = 3 as one 16-warp CTA of decoupled groups, 5 = 3 with decoupled halves
  * (default; from 4 ciphertexts per SM), 6 = 5 as one 16-warp CTA with a two-slot key
  * ring, 7 = 5 on 32-thread transforms with 16 values per thread (one shared-memory
- * transpose per transform).  At N = 2048 any mode >= 1 selects the N = 2048 TMEM ladder
- * (from 4 per SM).  All bit-identical; EINVAL outside 0..7 (the reference has no counterpart). */
+ * transpose per transform), 8 = 5 with one launch per segment (5 runs the whole ladder
+ * as one launch whose CTAs are (segment, ciphertext group) pairs in segment-major order).  At N = 2048 any mode >= 1 selects the N = 2048 TMEM ladder
+ * (from 4 per SM).  All bit-identical; EINVAL outside 0..8 (the reference has no counterpart). */
 int hwb_set_fft_mode(int mode);
 /* Batches of at most max_batch ciphertexts (default -1: the cluster capacity) run the cluster latency
  * ladder at N = 1024: one ciphertext per cluster of 2l CTAs on 2l SMs (digit row r

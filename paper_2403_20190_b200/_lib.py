@@ -17,8 +17,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HWB_LIB_PATH") or os.path.join(HERE, "libhwb200.so")
 
 HWB_OK, HWB_EINVAL, HWB_ECUDA = 0, 1, 2
-FFT_MODE_DEFAULT = 5   # hwb_set_fft_mode's default (libhwb200: g_fft_mode), FFT_MODES = 0..7
-FFT_MODES = tuple(range(8))
+FFT_MODE_DEFAULT = 5   # hwb_set_fft_mode's default (libhwb200: g_fft_mode), FFT_MODES = 0..8
+FFT_MODES = tuple(range(9))
 
 # every symbol include/hwb.h declares (checked by tests/test_abi.py)
 EXPORTS = (

@@ -2013,8 +2013,22 @@ __global__ void __launch_bounds__(NG * 128, NG == 2 ? 2 : 1)
     blind_rotate_fft_td_kernel(const double2 *__restrict__ ggsw, const uint32_t *__restrict__ lwe_in,
                                const uint32_t *__restrict__ tv, int tv_per_item, uint32_t *lwe_out, int L, Gadget g,
                                const double2 *__restrict__ twf, const double2 *__restrict__ twi, uint32_t *acc_io,
-                               int s0, int s1, int64_t B) {
+                               int s0_arg, int s1_arg, int64_t B, uint32_t *progress) {
   constexpr int N = 2 * FH;
+  // One launch per segment (progress == nullptr: steps [s0_arg, s1_arg), group blockIdx.x) or
+  // ONE launch for the whole ladder (progress != nullptr, s1_arg - s0_arg = segment length):
+  // CTA b runs segment b / groups of group b % groups, so a segment's partial last wave is
+  // filled with the next segment's first groups.  A group's segment s waits until
+  // progress[group] == s (its accumulator rests in acc_io; normally done `groups` CTAs ago)
+  // and publishes s + 1.  CTAs start in blockIdx order, so a CTA only ever waits for one
+  // that is running or done; the wait is bounded and traps instead of hanging.  All of it
+  // derives from blockIdx: uniform values, no registers across the steps.
+  constexpr int kPerCta = 2 * NG;
+  const uint32_t groups = progress ? (uint32_t)((B + 2 * NG - 1) / (2 * NG)) : gridDim.x;
+  const uint32_t seg = blockIdx.x / groups, grp = blockIdx.x % groups;
+  const int s0 = progress ? (int)seg * (s1_arg - s0_arg) : s0_arg;
+  const int s1 = progress ? (s0 + (s1_arg - s0_arg) < L ? s0 + (s1_arg - s0_arg) : L) : s1_arg;
+  // (a compile-time SINGLE flag instead of the run-time test measured slower: 52.2 vs 51.9 ms)
   constexpr int LOG2M = 11;
   constexpr int GT = 128;   // threads per half (named barriers)
   extern __shared__ uint4 smem_raw[];
@@ -2035,11 +2049,23 @@ __global__ void __launch_bounds__(NG * 128, NG == 2 ? 2 : 1)
     lay.m ^= 4u;
     lay.b ^= 4u;
   }
-  const int64_t bb = (int64_t)blockIdx.x * (2 * NG) + q;
+  const int64_t bb = (int64_t)grp * (2 * NG) + q;
   const bool valid = bb < B;
   const int64_t bq = valid ? bb : B - 1;
   const uint32_t *row = lwe_in + bq * (int64_t)(L + 1);
   uint32_t *acc = sm.acc[q];   // TP_ACC stride: odd ciphertexts 16 banks over
+  if (progress && seg > 0) {   // the group's previous segment
+    if (tid == 0) {
+      uint32_t done, spins = 0;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(done) : "l"(progress + grp) : "memory");
+        if (done >= seg) break;
+        __nanosleep(256);
+        if (++spins > (1u << 24)) __trap();   // (seconds: a lost predecessor surfaces as an error)
+      }
+    }
+    __syncthreads();
+  }
   if (s0 == 0) {
     const int bt = mod_switch(row[L], LOG2M);
     const uint32_t *tp = tv + (tv_per_item ? bq * 2 * N : 0);
@@ -2049,7 +2075,7 @@ __global__ void __launch_bounds__(NG * 128, NG == 2 ? 2 : 1)
       acc[k] = rot_read<N>(tp + c * N, i, e);
     }
   } else {
-    for (int k = t; k < 2 * N; k += FT) acc[k] = acc_io[bq * 2 * N + k];
+    for (int k = t; k < 2 * N; k += FT) acc[k] = __ldcg(&acc_io[bq * 2 * N + k]);   // (another SM wrote it)
   }
   for (int k = tid; k < kTwc * FT; k += NG * 128) {
     sm.twf[k] = twf[twc_full<true>(k / FT) * FT + k % FT];
@@ -2278,13 +2304,25 @@ __global__ void __launch_bounds__(NG * 128, NG == 2 ? 2 : 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sm.tmem_slot),
                  "r"((uint32_t)(NG * 128)));
   }
-  if (!valid) return;
-  if (s1 < L) {
-    for (int k = t; k < 2 * N; k += FT) acc_io[bq * 2 * N + k] = acc[k];
-  } else {
-    uint32_t *o = lwe_out + bq * (int64_t)(N + 1);
-    for (int k = t; k < N; k += FT) o[k] = k == 0 ? acc[0] : 0u - acc[N - k];
-    if (t == 0) o[N] = acc[N];
+  if (valid) {
+    if (s1 < L) {
+      for (int k = t; k < 2 * N; k += FT) acc_io[bq * 2 * N + k] = acc[k];
+    } else {
+      uint32_t *o = lwe_out + bq * (int64_t)(N + 1);
+      for (int k = t; k < N; k += FT) o[k] = k == 0 ? acc[0] : 0u - acc[N - k];
+      if (t == 0) o[N] = acc[N];
+    }
+  }
+  if (progress) {   // publish after every thread's accumulator stores
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      // (recomputed from blockIdx: nothing of the protocol stays live across the steps)
+      const uint32_t groups2 = (uint32_t)((B + kPerCta - 1) / kPerCta);
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(progress + blockIdx.x % groups2),
+                   "r"(blockIdx.x / groups2 + 1)
+                   : "memory");
+    }
   }
 }
 
@@ -3919,15 +3957,23 @@ __device__ __forceinline__ uint32_t rot_read_t2(const uint32_t *poly, int i, int
   return src >= N ? 0u - val : val;
 }
 
+template <bool SINGLE>
 __global__ void __launch_bounds__(16 * 32, 1)
     blind_rotate_fft2_td_kernel(const double2 *__restrict__ ggsw, const uint32_t *__restrict__ lwe_in,
                                 const uint32_t *__restrict__ tv, int tv_per_item, uint32_t *lwe_out, int L, Gadget g,
                                 const double2 *__restrict__ twf0, const double2 *__restrict__ twf1,
                                 const double2 *__restrict__ twi0, const double2 *__restrict__ twi1, uint32_t *acc_io,
-                                int s0, int s1, int64_t B) {
+                                int s0_arg, int s1_arg, int64_t B, uint32_t *progress) {
   constexpr int N = 4 * FH;
   constexpr int LOG2M = 12;
   constexpr int GT = 256;   // threads per pair (named barrier)
+  // SINGLE: one launch for the whole ladder, CTA = (segment, group) in segment-major order,
+  // s1_arg = the segment length (blind_rotate_fft_td_kernel has the protocol)
+  constexpr int kPerCta = T2C;
+  const uint32_t groups = SINGLE ? (uint32_t)((B + T2C - 1) / T2C) : gridDim.x;
+  const uint32_t seg = blockIdx.x / groups, grp = blockIdx.x % groups;
+  const int s0 = SINGLE ? (int)seg * s1_arg : s0_arg;
+  const int s1 = SINGLE ? (s0 + s1_arg < L ? s0 + s1_arg : L) : s1_arg;
   extern __shared__ uint4 smem_raw[];
   FSmem2TD &sm = *reinterpret_cast<FSmem2TD *>(smem_raw);
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
@@ -3943,11 +3989,23 @@ __global__ void __launch_bounds__(16 * 32, 1)
     lay.m ^= xo;
     lay.b ^= xo;
   }
-  const int64_t bb = (int64_t)blockIdx.x * T2C + q;
+  const int64_t bb = (int64_t)grp * T2C + q;
   const bool valid = bb < B;
   const int64_t bq = valid ? bb : B - 1;
   const uint32_t *row = lwe_in + bq * (int64_t)(L + 1);
   uint32_t *acc = sm.acc[q];   // row stride = 16 mod 32 words: odd ciphertexts 16 banks over
+  if (SINGLE && seg > 0) {   // the group's previous segment
+    if (tid == 0) {
+      uint32_t done, spins = 0;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(done) : "l"(progress + grp) : "memory");
+        if (done >= seg) break;
+        __nanosleep(256);
+        if (++spins > (1u << 24)) __trap();
+      }
+    }
+    __syncthreads();
+  }
   if (s0 == 0) {
     const int bt = mod_switch(row[L], LOG2M);
     const uint32_t *tp = tv + (tv_per_item ? bq * 2 * N : 0);
@@ -3957,7 +4015,7 @@ __global__ void __launch_bounds__(16 * 32, 1)
       acc[t2_pad(c, i)] = rot_read<N>(tp + c * N, i, e);
     }
   } else {
-    for (int k = tq; k < 2 * N; k += 2 * FT) acc[t2_pad(k >= N, k & (N - 1))] = acc_io[bq * 2 * N + k];
+    for (int k = tq; k < 2 * N; k += 2 * FT) acc[t2_pad(k >= N, k & (N - 1))] = __ldcg(&acc_io[bq * 2 * N + k]);
   }
   for (int k = tid; k < kTwc * FT; k += 16 * 32) {
     const int fs = twc_full<true>(k / FT) * FT + k % FT, is = twc_full<false>(k / FT) * FT + k % FT;
@@ -4139,13 +4197,25 @@ __global__ void __launch_bounds__(16 * 32, 1)
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sm.tmem_slot), "r"(512u));
   }
-  if (!valid) return;
-  if (s1 < L) {
-    for (int k = tq; k < 2 * N; k += 2 * FT) acc_io[bq * 2 * N + k] = acc[t2_pad(k >= N, k & (N - 1))];
-  } else {
-    uint32_t *o = lwe_out + bq * (int64_t)(N + 1);
-    for (int k = tq; k < N; k += 2 * FT) o[k] = k == 0 ? acc[0] : 0u - acc[t2_pad(0, N - k)];
-    if (tq == 0) o[N] = acc[t2_pad(1, 0)];
+  if (valid) {
+    if (s1 < L) {
+      for (int k = tq; k < 2 * N; k += 2 * FT) acc_io[bq * 2 * N + k] = acc[t2_pad(k >= N, k & (N - 1))];
+    } else {
+      uint32_t *o = lwe_out + bq * (int64_t)(N + 1);
+      for (int k = tq; k < N; k += 2 * FT) o[k] = k == 0 ? acc[0] : 0u - acc[t2_pad(0, N - k)];
+      if (tq == 0) o[N] = acc[t2_pad(1, 0)];
+    }
+  }
+  if (SINGLE) {   // publish after every thread's accumulator stores
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      // (recomputed from blockIdx: nothing of the protocol stays live across the steps)
+      const uint32_t groups2 = (uint32_t)((B + kPerCta - 1) / kPerCta);
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(progress + blockIdx.x % groups2),
+                   "r"(blockIdx.x / groups2 + 1)
+                   : "memory");
+    }
   }
 }
 
@@ -5066,7 +5136,11 @@ static size_t pbs_ext_bytes(const hwb_params *p, int64_t B) {
   return ((sizeof(uint32_t) * (size_t)B * (p->N + 1)) + 255) & ~(size_t)255;
 }
 
-static size_t fft_acc_bytes(const hwb_params *p, int64_t B) { return ((size_t)B * 2 * p->N * 4 + 255) & ~(size_t)255; }
+// accumulators between segments [B][2][N], then the single-launch ladder's progress words
+// (segments done per CTA-group of 4 ciphertexts)
+static size_t fft_accs_only_bytes(const hwb_params *p, int64_t B) { return ((size_t)B * 2 * p->N * 4 + 255) & ~(size_t)255; }
+static size_t fft_queue_bytes(int64_t B) { return (((size_t)(B + 3) / 4) * 4 + 255) & ~(size_t)255; }
+static size_t fft_acc_bytes(const hwb_params *p, int64_t B) { return fft_accs_only_bytes(p, B) + fft_queue_bytes(B); }
 // ladder steps per launch of the FFT ladder (L2 residency of the key slice)
 static thread_local int g_fft_segment = 64;
 // ciphertexts per CTA of the FFT PBS ladder (sharing each staged key slice)
@@ -5104,10 +5178,11 @@ static thread_local int g_fft_mode = 5;
 constexpr int64_t g_fft_tmem_min = 4;
 
 int hwb_set_fft_mode(int mode) {
-  if (mode < 0 || mode > 7)
+  if (mode < 0 || mode > 8)
     return fail(HWB_EINVAL, "FFT ladder mode must be 0 (registers), 1 (TMEM), 2 (TMEM, one ciphertext per thread) "
                             "3 (TMEM, lane-paired), 4 (TMEM, decoupled groups), 5 (TMEM, lane-paired, decoupled halves) or 6 (5 as one "
-                            "16-warp CTA with a two-slot key ring) or 7 (5 on 32-thread transforms: one transpose per transform)");
+                            "16-warp CTA with a two-slot key ring) 7 (5 on 32-thread transforms: one transpose per transform) or 8 (5 with one launch per segment "
+                            "instead of one launch for the whole ladder)");
   g_fft_mode = mode;
   return HWB_OK;
 }
@@ -5275,15 +5350,46 @@ int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, co
     if (!ksk_tc) return HWB_OK;
     return keyswitch_tc_launch(p, ksk_tc, ext, lwe_out, B, ws + fft_acc_bytes(p, B) + pbs_ext_bytes(p, B), s);
   }
-  for (int s0 = 0; s0 < L; s0 += g_fft_segment) {
+  // mode 5: ONE launch for the whole ladder, CTA = (segment, group) in segment-major order,
+  // so a segment's partial last wave overlaps the next segment (mode 8: one launch per
+  // segment, each with its own tail)
+  const bool single = p->N == 2 * FH && g_fft_mode == 5 && B >= g_fft_tmem_min * (int64_t)st->sms;
+  if (single) {
+    uint32_t *progress = (uint32_t *)(ws + fft_accs_only_bytes(p, B));
+    const cudaError_t e = cudaMemsetAsync(progress, 0, fft_queue_bytes(B), s);
+    if (e != cudaSuccess) return fail(HWB_ECUDA, std::string("progress memset: ") + cudaGetErrorString(e));
+    const int64_t ctas = ((B + 3) / 4) * (int64_t)((L + g_fft_segment - 1) / g_fft_segment);
+    if (ctas > 0x7FFFFFFF) return fail(HWB_EINVAL, "batch too large");
+    const size_t smem = sizeof(FSmemTDT<2, 1>);
+    if ((rc = set_smem(blind_rotate_fft_td_kernel<2, 1>, smem))) return rc;
+    blind_rotate_fft_td_kernel<2, 1><<<(unsigned)ctas, 256, smem, s>>>(
+        (const double2 *)bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st->fft_fwd, st->fft_inv, acc, 0, g_fft_segment,
+        B, progress);
+    if ((rc = post_launch("blind_rotate_fft_td_kernel (single launch)"))) return rc;
+  }
+  const bool single2 = p->N == 4 * FH && g_fft_mode == 5 && B >= (int64_t)T2C * st->sms;
+  if (single2) {   // the N = 2048 TMEM ladder, same single-launch protocol
+    uint32_t *progress = (uint32_t *)(ws + fft_accs_only_bytes(p, B));
+    const cudaError_t e = cudaMemsetAsync(progress, 0, fft_queue_bytes(B), s);
+    if (e != cudaSuccess) return fail(HWB_ECUDA, std::string("progress memset: ") + cudaGetErrorString(e));
+    const int64_t ctas = ((B + T2C - 1) / T2C) * (int64_t)((L + g_fft_segment - 1) / g_fft_segment);
+    if (ctas > 0x7FFFFFFF) return fail(HWB_EINVAL, "batch too large");
+    const size_t smem = sizeof(FSmem2TD);
+    if ((rc = set_smem(blind_rotate_fft2_td_kernel<true>, smem))) return rc;
+    blind_rotate_fft2_td_kernel<true><<<(unsigned)ctas, 16 * 32, smem, s>>>(
+        (const double2 *)bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st->fft2_fwd[0], st->fft2_fwd[1],
+        st->fft2_inv[0], st->fft2_inv[1], acc, 0, g_fft_segment, B, progress);
+    if ((rc = post_launch("blind_rotate_fft2_td_kernel (single launch)"))) return rc;
+  }
+  for (int s0 = 0; s0 < L && !single && !single2; s0 += g_fft_segment) {
     const int s1 = s0 + g_fft_segment < L ? s0 + g_fft_segment : L;
     if (p->N == 4 * FH && g_fft_mode >= 1 && B >= (int64_t)T2C * st->sms) {
       // TMEM ladder: 4 ciphertexts per SM (one 16-warp CTA) sharing each key slice
       const size_t smem = sizeof(FSmem2TD);
-      if ((rc = set_smem(blind_rotate_fft2_td_kernel, smem))) return rc;
-      blind_rotate_fft2_td_kernel<<<(unsigned)((B + T2C - 1) / T2C), 16 * 32, smem, s>>>(
+      if ((rc = set_smem(blind_rotate_fft2_td_kernel<false>, smem))) return rc;
+      blind_rotate_fft2_td_kernel<false><<<(unsigned)((B + T2C - 1) / T2C), 16 * 32, smem, s>>>(
           (const double2 *)bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st->fft2_fwd[0], st->fft2_fwd[1],
-          st->fft2_inv[0], st->fft2_inv[1], acc, s0, s1, B);
+          st->fft2_inv[0], st->fft2_inv[1], acc, s0, s1, B, nullptr);
       rc = post_launch("blind_rotate_fft2_td_kernel");
     } else if (p->N == 4 * FH) {
       const size_t smem = sizeof(FSmem2);
@@ -5302,13 +5408,15 @@ int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, co
       const size_t smem = sizeof(FSmemTDT<4, 2>);
       if ((rc = set_smem(blind_rotate_fft_td_kernel<4, 2>, smem))) return rc;
       blind_rotate_fft_td_kernel<4, 2><<<(unsigned)((B + 7) / 8), 512, smem, s>>>(
-          (const double2 *)bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st->fft_fwd, st->fft_inv, acc, s0, s1, B);
+          (const double2 *)bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st->fft_fwd, st->fft_inv, acc, s0, s1, B,
+          nullptr);
       rc = post_launch("blind_rotate_fft_td_kernel<4,2>");
     } else if (g_fft_mode >= 5 && B >= g_fft_tmem_min * (int64_t)st->sms) {
       const size_t smem = sizeof(FSmemTDT<2, 1>);
       if ((rc = set_smem(blind_rotate_fft_td_kernel<2, 1>, smem))) return rc;
       blind_rotate_fft_td_kernel<2, 1><<<(unsigned)((B + 3) / 4), 256, smem, s>>>(
-          (const double2 *)bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st->fft_fwd, st->fft_inv, acc, s0, s1, B);
+          (const double2 *)bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st->fft_fwd, st->fft_inv, acc, s0, s1, B,
+          nullptr);
       rc = post_launch("blind_rotate_fft_td_kernel");
     } else if (g_fft_mode == 4 && B >= (int64_t)TQC * st->sms) {
       const size_t smem = sizeof(FSmemTQ);

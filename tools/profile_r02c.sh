@@ -9,12 +9,12 @@ B="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --sweep '' --no-other-
 eval "$B" > gpurun_out/r02c_plain.log 2>&1 && \
   eval "ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02c_launches.csv $B" \
   > gpurun_out/r02c_ncu_launch.log 2>&1
-python tools/run_pbs.py 4096 fft -1 1 > gpurun_out/r02c_plain_td.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:blind_rotate_fft_td -s 2 -c 1 \
-  -o gpurun_out/r02c_ncu_td python tools/run_pbs.py 4096 fft -1 1 > gpurun_out/r02c_ncu_td.log 2>&1
-python tools/run_pbs_cfg.py CFG4 4096 fft 1 > gpurun_out/r02c_plain_f2.log 2>&1 && \
+python tools/run_pbs.py 4096 fft -1 2 > gpurun_out/r02c_plain_td.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:blind_rotate_fft_td -s 1 -c 1 \
+  -o gpurun_out/r02c_ncu_td python tools/run_pbs.py 4096 fft -1 2 > gpurun_out/r02c_ncu_td.log 2>&1
+python tools/run_pbs_cfg.py CFG4 4096 fft 2 > gpurun_out/r02c_plain_f2.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:blind_rotate_fft2_td -s 1 -c 1 \
-  -o gpurun_out/r02c_ncu_f2td python tools/run_pbs_cfg.py CFG4 4096 fft 1 > gpurun_out/r02c_ncu_f2td.log 2>&1
+  -o gpurun_out/r02c_ncu_f2td python tools/run_pbs_cfg.py CFG4 4096 fft 2 > gpurun_out/r02c_ncu_f2td.log 2>&1
 python tools/run_pbs.py 4096 fft -1 1 7 > gpurun_out/r02c_plain_w.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:blind_rotate_fft_w -s 2 -c 1 \
   -o gpurun_out/r02c_ncu_w python tools/run_pbs.py 4096 fft -1 1 7 > gpurun_out/r02c_ncu_w.log 2>&1
