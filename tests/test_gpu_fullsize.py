@@ -77,6 +77,33 @@ def test_cfg2_ragged_tmem_ladder(coracle, keys):
     _run_and_check(coracle, P, K, bsk, ksk, 8 * sms + 5, 2, 128)
 
 
+@pytest.mark.parametrize("name,B", [("CFG2", 8 * 148 + 5), ("CFG4", 4 * 148 + 5)])
+def test_single_launch_ladder_matches_per_segment_launches(keys, name, B):
+    """FFT mode 5 runs the whole ladder as ONE launch whose CTAs are (segment, group) pairs
+    waiting on per-group progress words; mode 8 launches once per segment.  Short segments
+    (7 steps: 90 / 108 dependent CTAs per group, thousands of waits) on a ragged batch, against
+    the per-segment launches, the NTT ladder and a second run on the recycled workspace (the
+    progress words are cleared per call)."""
+    P, K, bsk, ksk = keys(name)
+    rng = np.random.default_rng(77)
+    d_lwe = tfhe.to_device(_rand(rng, (B, P.lwe_n + 1)))
+    d_tv = tfhe.to_device(_rand(rng, (B, 2, P.n)))
+    L = _lib.load()
+    try:
+        _lib.check(L.hwb_set_fft_segment(7))
+        _lib.check(L.hwb_set_fft_mode(8))
+        per_segment = tfhe.to_host(tfhe.pbs_batch(P, d_lwe, d_tv, bsk, ksk, ladder="fft"))
+        _lib.check(L.hwb_set_fft_mode(5))
+        single = tfhe.to_host(tfhe.pbs_batch(P, d_lwe, d_tv, bsk, ksk, ladder="fft"))
+        again = tfhe.to_host(tfhe.pbs_batch(P, d_lwe, d_tv, bsk, ksk, ladder="fft"))
+    finally:
+        _lib.check(L.hwb_set_fft_segment(64))
+        _lib.check(L.hwb_set_fft_mode(_lib.FFT_MODE_DEFAULT))
+    assert_u32_equal(single, per_segment)
+    assert_u32_equal(again, single)
+    assert_u32_equal(single, tfhe.to_host(tfhe.pbs_batch(P, d_lwe, d_tv, bsk, ksk, ladder="ntt")))
+
+
 def test_cfg2_register_ladder_range(coracle, keys):
     """cfg2 batches between one ciphertext per SM and the TMEM threshold (4 per SM)
     run the register FFT ladder (4 CTAs per SM)."""
