@@ -289,7 +289,9 @@ int hwb_vp_level_fft(const hwb_params *p, const void *ggsw_fft, const int32_t *g
 /* Workspace of hwb_pbs_fft: the accumulators between ladder segments, plus the
  * key switch's buffers when with_keyswitch. */
 size_t hwb_pbs_fft_workspace_bytes(const hwb_params *p, int64_t B, int with_keyswitch);
-/* Ladder steps per launch (default 64): each launch's key slice stays L2-resident. */
+/* Ladder steps per segment (per calling thread): a segment's key slices stay L2-resident.
+ * Default 64 for the modes that launch once per segment and 48 for the single-launch
+ * ladders (FFT mode 5) until this is called; afterwards `steps` for both. */
 int hwb_set_fft_segment(int steps);
 /* Ciphertexts per CTA of the FFT PBS ladder (1, 2 or 4): they share every staged key
  * slice (one shared-memory write, several reads). */

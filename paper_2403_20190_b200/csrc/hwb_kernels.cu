@@ -5143,6 +5143,11 @@ static size_t fft_queue_bytes(int64_t B) { return (((size_t)(B + 3) / 4) * 4 + 2
 static size_t fft_acc_bytes(const hwb_params *p, int64_t B) { return fft_accs_only_bytes(p, B) + fft_queue_bytes(B); }
 // ladder steps per launch of the FFT ladder (L2 residency of the key slice)
 static thread_local int g_fft_segment = 64;
+// the single-launch ladders' segment while hwb_set_fft_segment has not been called: shorter
+// segments fill the launch's only tail more finely (cfg2 B = 4096: 51.5 ms at 48 steps, 52.0 at
+// 64, 51.7 at 32; cfg1 31.7 / 31.8; tools/seg_sweep.py), the per-segment modes keep 64
+static thread_local bool g_fft_segment_set = false;
+constexpr int kSingleLaunchSegment = 48;
 // ciphertexts per CTA of the FFT PBS ladder (sharing each staged key slice)
 static thread_local int g_fft_cpb = 1;
 // batches of at most this many ciphertexts run the FFT latency ladder (-1: one per SM)
@@ -5168,9 +5173,11 @@ int64_t hwb_set_fft_cluster_batch(int64_t max_batch) {
 // ladder): 0 = registers (g_fft_cpb ciphertexts per CTA), 1 = TMEM accumulators, two
 // ciphertexts per thread; 2 = TMEM, one per thread (16 warps/SM); 3 = 2 with lane-paired
 // ciphertexts; 4 = 3 as one 16-warp CTA of decoupled groups; 5 = 3 with decoupled halves
-// (default: cfg2 B = 4096 in 54.2 ms vs 61.0 / 60.1 / 59.6 / 63.2 ms for modes 1-4);
-// 6 = 5 as one 16-warp CTA with a two-slot key ring (62.1 ms; 62.5 vs 61.8 ms at full
-// waves, B = 4736), DESIGN.md §3b.  All bit-identical.
+// and the whole ladder in ONE launch (default: cfg2 B = 4096 in 51.5 ms vs 61.0 / 60.1 /
+// 59.6 / 63.2 ms for modes 1-4); 6 = 5 as one 16-warp CTA with a two-slot key ring
+// (62.1 ms; 62.5 vs 61.8 ms at full waves, B = 4736); 7 = 5 on 32-thread transforms, one
+// transpose per transform (59.4 ms); 8 = 5 with one launch per segment (53.2 ms),
+// DESIGN.md §3b.  All bit-identical.
 static thread_local int g_fft_mode = 5;
 // smallest batch (ciphertexts per SM) for the mode-5 TMEM ladder: from 4 per SM (one
 // CTA) it beats the register ladder (cfg2 B = 592: 9.27 vs 9.97 ms; 1036: 16.2 vs 19.4;
@@ -5358,13 +5365,14 @@ int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, co
     uint32_t *progress = (uint32_t *)(ws + fft_accs_only_bytes(p, B));
     const cudaError_t e = cudaMemsetAsync(progress, 0, fft_queue_bytes(B), s);
     if (e != cudaSuccess) return fail(HWB_ECUDA, std::string("progress memset: ") + cudaGetErrorString(e));
-    const int64_t ctas = ((B + 3) / 4) * (int64_t)((L + g_fft_segment - 1) / g_fft_segment);
+    const int seg_len = g_fft_segment_set ? g_fft_segment : kSingleLaunchSegment;
+    const int64_t ctas = ((B + 3) / 4) * (int64_t)((L + seg_len - 1) / seg_len);
     if (ctas > 0x7FFFFFFF) return fail(HWB_EINVAL, "batch too large");
     const size_t smem = sizeof(FSmemTDT<2, 1>);
     if ((rc = set_smem(blind_rotate_fft_td_kernel<2, 1>, smem))) return rc;
     blind_rotate_fft_td_kernel<2, 1><<<(unsigned)ctas, 256, smem, s>>>(
-        (const double2 *)bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st->fft_fwd, st->fft_inv, acc, 0, g_fft_segment,
-        B, progress);
+        (const double2 *)bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st->fft_fwd, st->fft_inv, acc, 0, seg_len, B,
+        progress);
     if ((rc = post_launch("blind_rotate_fft_td_kernel (single launch)"))) return rc;
   }
   const bool single2 = p->N == 4 * FH && g_fft_mode == 5 && B >= (int64_t)T2C * st->sms;
@@ -5372,13 +5380,14 @@ int hwb_pbs_fft(const hwb_params *p, const void *bsk_fft, const void *ksk_tc, co
     uint32_t *progress = (uint32_t *)(ws + fft_accs_only_bytes(p, B));
     const cudaError_t e = cudaMemsetAsync(progress, 0, fft_queue_bytes(B), s);
     if (e != cudaSuccess) return fail(HWB_ECUDA, std::string("progress memset: ") + cudaGetErrorString(e));
-    const int64_t ctas = ((B + T2C - 1) / T2C) * (int64_t)((L + g_fft_segment - 1) / g_fft_segment);
+    const int seg_len = g_fft_segment_set ? g_fft_segment : kSingleLaunchSegment;
+    const int64_t ctas = ((B + T2C - 1) / T2C) * (int64_t)((L + seg_len - 1) / seg_len);
     if (ctas > 0x7FFFFFFF) return fail(HWB_EINVAL, "batch too large");
     const size_t smem = sizeof(FSmem2TD);
     if ((rc = set_smem(blind_rotate_fft2_td_kernel<true>, smem))) return rc;
     blind_rotate_fft2_td_kernel<true><<<(unsigned)ctas, 16 * 32, smem, s>>>(
         (const double2 *)bsk_fft, lwe_in, tv, tv_per_item, ext, L, g, st->fft2_fwd[0], st->fft2_fwd[1],
-        st->fft2_inv[0], st->fft2_inv[1], acc, 0, g_fft_segment, B, progress);
+        st->fft2_inv[0], st->fft2_inv[1], acc, 0, seg_len, B, progress);
     if ((rc = post_launch("blind_rotate_fft2_td_kernel (single launch)"))) return rc;
   }
   for (int s0 = 0; s0 < L && !single && !single2; s0 += g_fft_segment) {
@@ -5579,6 +5588,7 @@ int hwb_set_fft_group(int ciphertexts_per_cta) {
 int hwb_set_fft_segment(int steps) {
   if (steps < 1) return fail(HWB_EINVAL, "segment must be >= 1 step");
   g_fft_segment = steps;
+  g_fft_segment_set = true;
   return HWB_OK;
 }
 

@@ -4,13 +4,13 @@ import torch, numpy as np
 from paper_2403_20190_b200 import _lib, tfhe
 from paper_2403_20190_b200.params import named_params
 L = _lib.load()
-P = named_params("CFG2"); B = 4096
+P = named_params(sys.argv[2] if len(sys.argv) > 2 else "CFG2"); B = int(sys.argv[3]) if len(sys.argv) > 3 else 4096
 K = tfhe.pbs_keygen(P, 1); bsk, ksk = K.device_keys()
 rng = tfhe.make_rng(9)
-lwe = tfhe.to_device(tfhe.enc_lwe_batch(rng.integers(0, 8, B) * P.delta, K.lwe_key, rng))
-tv = tfhe.to_device(tfhe.test_polynomial(np.arange(4), P))
+lwe = tfhe.to_device(tfhe.enc_lwe_batch(rng.integers(0, P.p, B) * P.delta, K.lwe_key, rng))
+tv = tfhe.to_device(tfhe.test_polynomial(np.arange(P.p // 2), P))
 ref = None
-for seg in (64, 128, 256, 630):
+for seg in (tuple(int(a) for a in sys.argv[1].split(",")) if len(sys.argv) > 1 else (64, 128, 256, 630)):
     _lib.check(L.hwb_set_fft_segment(seg))
     out = tfhe.pbs_batch(P, lwe, tv, bsk, None, ladder="fft"); torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
