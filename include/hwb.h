@@ -286,8 +286,10 @@ int hwb_ivp_level_fft(const hwb_params *p, const void *ggsw_fft, const int32_t *
                       uint32_t *next, int32_t m, int64_t B, void *stream);
 int hwb_vp_level_fft(const hwb_params *p, const void *ggsw_fft, const int32_t *ggsw_idx, const uint32_t *cur,
                      uint32_t *next, int32_t m, int64_t B, void *stream);
-/* Workspace of hwb_pbs_fft: the accumulators between ladder segments, plus the
- * key switch's buffers when with_keyswitch. */
+/* Workspace of hwb_pbs_fft: the accumulators between ladder segments and the
+ * single-launch ladders' progress words (one per group of 4 ciphertexts, cleared by
+ * hwb_pbs_fft on the caller's stream), plus the key switch's buffers when
+ * with_keyswitch.  One workspace serves one call at a time (one per stream). */
 size_t hwb_pbs_fft_workspace_bytes(const hwb_params *p, int64_t B, int with_keyswitch);
 /* Ladder steps per segment (per calling thread): a segment's key slices stay L2-resident.
  * Default 64 for the modes that launch once per segment and 48 for the single-launch
