@@ -686,8 +686,8 @@ def bench_hwb(args):
                      "unit": "TB/s", "frac": round(sm_ach / sm_peak, 4),
                      "bytes_per_step": smem_step,
                      "peak_source": f"128 B/clk/SM x {sms} SMs x {mhz:.0f} MHz (median SM clock under load)",
-                     "ncu": "profiles/r02b_ncu_td.txt: l1tex throughput (LSU wavefronts + TMA writes) "
-                            "0.72 of peak; the register ladder reached 0.89 (profiles/r01_ncu_fft_ladder_v2.txt)"}
+                     "ncu": "profiles/r02c_ncu_td.txt: l1tex throughput (LSU wavefronts + TMA writes) "
+                            "0.74 of peak; the register ladder reached 0.89 (profiles/r01_ncu_fft_ladder_v2.txt)"}
     result = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 3),
